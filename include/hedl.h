@@ -1,0 +1,220 @@
+/*
+ * hedl.h -- C ABI of the B200-native HT-HEDL hot path (arxiv 2412.00802).
+ *
+ * The library evaluates ALCQI(D) concept hypotheses against an ABox under the
+ * paper's closed-world / unique-name instance semantics (§III,
+ * PAPER.md:53 §III-A) and counts covered positive/negative examples
+ * (§IV Alg. 15).  Problem statement: "evaluate hypotheses up
+ * to the ALCQI(D) DL language"; evaluation plan PAPER.md:532.
+ *
+ * Conventions
+ *  - Every function returns hedl_status (HEDL_OK == 0).  On error no handle is
+ *    created, outputs are unspecified, and hedl_last_error() returns a
+ *    thread-local message naming the offending node / hypothesis index.  No C++
+ *    exception crosses this boundary.
+ *  - A bitset ("row") over the N individuals is W = ceil(N/32) uint32 words,
+ *    LSB-first: individual i is bit (i & 31) of word (i >> 5).  Tail bits of the
+ *    last word are 0 in every input, stored, returned or compared row
+ *    (SURVEY Q6).  This replaces the paper's one byte per membership
+ *    ("16 (8-bit) concept memberships").
+ *  - "device" pointers are CUDA device addresses on the KB's device; "host"
+ *    pointers are ordinary CPU memory.  Input arrays are borrowed for the call
+ *    and copied; output buffers are owned by the caller.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Handles are opaque.  A hedl_kb is immutable after load and may be shared by
+ *    concurrent evaluations.  A hedl_program owns a workspace; concurrent eval
+ *    calls on ONE program serialise on an internal mutex (use one program per
+ *    stream for concurrency).  A CUDA error poisons the KB handle: every later
+ *    call on it returns HEDL_ERR_CUDA.
+ */
+#ifndef HEDL_H
+#define HEDL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t hedl_status;
+#define HEDL_OK 0
+#define HEDL_ERR_INVALID_ARG 1     /* null/ill-sized argument, non-zero tail bits, E >= 2^32 */
+#define HEDL_ERR_OUT_OF_RANGE 2    /* an id >= its count (individual, concept, role, data, root) */
+#define HEDL_ERR_EXAMPLE_CONFLICT 3 /* an individual is both positive and negative */
+#define HEDL_ERR_BAD_EXPR 4        /* arity, cycle, NaN bound, n > 2^32-2, inverse data property */
+#define HEDL_ERR_PARSE 5           /* reserved (text front end lives in the Python binding) */
+#define HEDL_ERR_CUDA 6            /* CUDA runtime error; the KB handle is poisoned */
+#define HEDL_ERR_OOM 7             /* host or device allocation failed */
+#define HEDL_ERR_UNSUPPORTED 8     /* e.g. no sm_100 device */
+
+typedef struct hedl_kb hedl_kb;
+typedef struct hedl_program hedl_program;
+
+/* ---------------------------------------------------------------------------
+ * Knowledge base (§III-A, Fig. 3).  Fields:
+ *   n_individuals  N; every individual id is < N.  N == 0 is legal (W == 0).
+ *   n_concepts, concept_bits   host u32[C][W], row c = extension of concept c
+ *                  (the transposed concepts matrix of PAPER.md:63, bit-packed).
+ *   n_roles, role_edge_off     host u64[R+1]; role r's assertions are
+ *                  (edge_subj[k], edge_obj[k]) for k in [off[r], off[r+1]).  Any
+ *                  order; duplicates are removed (role extensions are sets,
+ *                  SURVEY Q4).  Stored as CSR plus transposed CSR (r^-,
+ *                  PAPER.md:299).  Each role must have < 2^32 distinct pairs.
+ *   n_data, data_off, data_subj, data_val   numeric concrete roles
+ *                  (§III-B3): assertions (data_subj[k], data_val[k])
+ *                  for k in [data_off[d], data_off[d+1]); several values per
+ *                  subject allowed; NaN values never match
+ *                   and are dropped at load.
+ *   pos_ids / neg_ids   host u32 lists of positive / negative examples
+ *                  (ExMat); duplicates allowed; must be disjoint.
+ * ------------------------------------------------------------------------- */
+typedef struct hedl_kb_desc {
+    uint32_t n_individuals;
+    uint32_t n_concepts;
+    const uint32_t *concept_bits;
+    uint32_t n_roles;
+    const uint64_t *role_edge_off;
+    const uint32_t *edge_subj;
+    const uint32_t *edge_obj;
+    uint32_t n_data;
+    const uint64_t *data_off;
+    const uint32_t *data_subj;
+    const float *data_val;
+    uint32_t n_pos;
+    const uint32_t *pos_ids;
+    uint32_t n_neg;
+    const uint32_t *neg_ids;
+} hedl_kb_desc;
+
+typedef struct hedl_kb_info {
+    uint32_t n_individuals, words, words_padded, n_concepts, n_roles, n_data;
+    uint64_t n_pos, n_neg;
+    uint64_t device_bytes;          /* bytes of device memory the KB holds */
+    uint64_t edges[64];             /* distinct pairs per direction 2r (r) / 2r+1 (r^-), r < 32 */
+    uint64_t heavy[64];             /* individuals above the heavy-degree threshold per direction */
+} hedl_kb_info;
+
+/* Build the device layout on `device` (copying through `stream`; returns after
+ * the upload completed).  Errors: INVALID_ARG (null arrays with non-zero
+ * counts, tail bits set), OUT_OF_RANGE (id >= N), EXAMPLE_CONFLICT, OOM, CUDA,
+ * UNSUPPORTED (device is not sm_100). */
+hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *stream, hedl_kb **out);
+hedl_status hedl_kb_free(hedl_kb *kb);
+hedl_status hedl_kb_get_info(const hedl_kb *kb, hedl_kb_info *out);
+
+/* ---------------------------------------------------------------------------
+ * Hypotheses (§IV: "a series of (potentially) nested DL
+ * operations", stored contiguously; an "evaluation plan ... determines the
+ * computational order").  A hypothesis batch is a node array; node i's
+ * children are child_idx[child_begin .. child_begin+child_count).  Children
+ * may be shared (a DAG is accepted); cycles are rejected.
+ * ------------------------------------------------------------------------- */
+#define HEDL_OP_TOP 0
+#define HEDL_OP_BOTTOM 1
+#define HEDL_OP_ATOM 2     /* arg = concept id */
+#define HEDL_OP_NOT 3      /* 1 child; complement over Delta = {0..N-1} */
+#define HEDL_OP_AND 4      /* k >= 0 children; empty AND = TOP (Alg. 1/2 "r=1")  */
+#define HEDL_OP_OR 5       /* k >= 0 children; empty OR = BOTTOM ("=0 for disj.") */
+#define HEDL_OP_EXISTS 6   /* arg = role; 1 child (Alg. 4)     */
+#define HEDL_OP_FORALL 7   /* arg = role; 1 child (Alg. 6)     */
+#define HEDL_OP_MIN 8      /* arg = role, n; >=n (Alg. 8 MIN)       */
+#define HEDL_OP_MAX 9      /* arg = role, n; <=n, 0 included          */
+#define HEDL_OP_EXACT 10   /* arg = role, n; ==n (Alg. 7 EXACTLY)   */
+#define HEDL_OP_DRANGE 11  /* arg = data property; exists v in [lo,hi] (Alg. 10) */
+
+#define HEDL_FLAG_INV 1u   /* node.flags: the role is the inverse r^-  */
+
+typedef struct hedl_node {
+    uint8_t op;
+    uint8_t flags;
+    uint16_t reserved;      /* must be 0 */
+    uint32_t arg;
+    uint32_t n;             /* cardinality bound for MIN/MAX/EXACT; n <= 2^32-2 */
+    float lo, hi;           /* DRANGE closed float32 bounds; +-inf allowed, NaN rejected */
+    uint32_t child_begin, child_count;
+} hedl_node;
+
+/* compile flags */
+#define HEDL_COMPILE_NO_CSE 1u            /* do not merge identical subexpressions */
+#define HEDL_COMPILE_NO_REWRITE 2u        /* no flatten / sort / dedupe of AND-OR operands */
+#define HEDL_COMPILE_COMPAT_PAPER_MAX 4u  /* MAX as the paper's cVal>0 && cVal<=rVal */
+
+/* Compile `roots` (indices into nodes) into a program: canonical DAG with
+ * common-subexpression reuse across all roots, topological levels, per-node
+ * algorithmic byte cost.  Host-only; `kb` supplies the id
+ * bounds and sizes.  Errors: INVALID_ARG, OUT_OF_RANGE (child/root/arg id),
+ * BAD_EXPR (arity, cycle, NaN bound, inverse data property, n > 2^32-2). */
+hedl_status hedl_compile(const hedl_kb *kb, const hedl_node *nodes, uint32_t n_nodes,
+                         const uint32_t *child_idx, uint64_t n_child_idx,
+                         const uint32_t *roots, uint32_t n_roots, uint32_t flags,
+                         hedl_program **out);
+hedl_status hedl_program_free(hedl_program *prog);
+
+typedef struct hedl_program_info {
+    uint32_t n_roots;
+    uint32_t n_nodes;             /* computed canonical nodes after CSE */
+    uint32_t n_levels;
+    uint32_t n_bool, n_restrict, n_drange;
+    double alg_bytes_total;       /* sum over roots of B(h) (per-hypothesis CSE only) */
+    double alg_bytes_shared;      /* sum over canonical nodes (batch-wide CSE) */
+} hedl_program_info;
+hedl_status hedl_program_get_info(const hedl_program *prog, hedl_program_info *out);
+/* per-root algorithmic bytes B(h), host double[n] for roots [first, first+n) */
+hedl_status hedl_program_root_bytes(const hedl_program *prog, uint32_t first, uint32_t n, double *out);
+
+/* ---------------------------------------------------------------------------
+ * Evaluation.  Counts per hypothesis: tp = |H & P|, fp = |H & N|,
+ * fn = |P| - tp, tn = |N| - fp (Alg. 15).
+ * ------------------------------------------------------------------------- */
+typedef struct hedl_counts {
+    uint64_t tp, fp, fn, tn;
+} hedl_counts;
+
+/* Latency path: evaluate one root.  out_bits: device u32[W] (nullable) receives
+ * the instance bitset; out: HOST pointer, filled before return (the call
+ * synchronises `stream`).  Errors: OUT_OF_RANGE (root), CUDA, OOM. */
+hedl_status hedl_eval_one(const hedl_kb *kb, hedl_program *prog, uint32_t root,
+                          uint32_t *out_bits, hedl_counts *out, void *stream);
+
+/* eval_batch flags */
+#define HEDL_EVAL_COUNTS_DEVICE 1u   /* `counts` is a device pointer; return after enqueue */
+#define HEDL_EVAL_PER_NODE 2u        /* force the per-node kernels (disable lane-packed restrictions) */
+
+/* Throughput path: evaluate roots [first_root, first_root + n_roots) of prog.
+ * Output position i <-> root first_root + i (input order).
+ * out_bits: device u32[n_roots][W] (nullable).  counts: host (default; the call
+ * synchronises) or device (HEDL_EVAL_COUNTS_DEVICE; asynchronous) hedl_counts[n].
+ * Results do not depend on chunking, CSE or flags. */
+hedl_status hedl_eval_batch(const hedl_kb *kb, hedl_program *prog, uint32_t first_root,
+                            uint32_t n_roots, uint32_t *out_bits, hedl_counts *counts,
+                            void *stream, uint32_t flags);
+
+/* Device-memory cap for one program's evaluation workspace (default 8 GiB). */
+hedl_status hedl_program_set_workspace_limit(hedl_program *prog, uint64_t bytes);
+
+/* ---------------------------------------------------------------------------
+ * Diagnostics
+ * ------------------------------------------------------------------------- */
+const char *hedl_last_error(void);
+const char *hedl_version(void);
+
+/* Kernel-level timing: when enabled, every kernel launch of the library is
+ * bracketed by CUDA events on its launch stream; hedl_prof_read synchronises
+ * and returns per kernel class {name, launches, total_ms, alg_bytes}. */
+typedef struct hedl_prof_entry {
+    char name[32];
+    uint64_t launches;
+    double total_ms;
+    double alg_bytes;
+} hedl_prof_entry;
+hedl_status hedl_prof_enable(int on);
+hedl_status hedl_prof_reset(void);
+int hedl_prof_read(hedl_prof_entry *out, int max_entries);
+/* number of library kernel launches since process start (always counted) */
+uint64_t hedl_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEDL_H */

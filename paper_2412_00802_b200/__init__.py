@@ -1,0 +1,297 @@
+"""B200-native HT-HEDL hot path (arxiv 2412.00802): Python binding of libhedl.so.
+
+Argument marshalling only -- every step of the evaluation runs in the CUDA
+library (paper_2412_00802_b200/csrc, C ABI in include/hedl.h).  PyTorch is
+used for device memory (output buffers) and streams.  There is no CPU
+fallback: if libhedl.so is missing or fails to load, every entry point raises.
+
+Names follow the ABI: hedl_kb_load, hedl_compile, hedl_eval_one, hedl_eval_batch.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhedl.so")
+
+HEDL_COMPILE_NO_CSE = 1
+HEDL_COMPILE_NO_REWRITE = 2
+HEDL_COMPILE_COMPAT_PAPER_MAX = 4
+HEDL_EVAL_COUNTS_DEVICE = 1
+HEDL_EVAL_PER_NODE = 2
+
+STATUS = {0: "OK", 1: "INVALID_ARG", 2: "OUT_OF_RANGE", 3: "EXAMPLE_CONFLICT", 4: "BAD_EXPR",
+          5: "PARSE", 6: "CUDA", 7: "OOM", 8: "UNSUPPORTED"}
+
+# every symbol include/hedl.h declares (checked by tests/test_abi.py)
+ABI_SYMBOLS = ["hedl_kb_load", "hedl_kb_free", "hedl_kb_get_info", "hedl_compile", "hedl_program_free",
+               "hedl_program_get_info", "hedl_program_root_bytes", "hedl_eval_one", "hedl_eval_batch",
+               "hedl_program_set_workspace_limit", "hedl_last_error", "hedl_version", "hedl_prof_enable",
+               "hedl_prof_reset", "hedl_prof_read", "hedl_launch_count"]
+
+
+class HedlError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"hedl {STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class _KbDesc(C.Structure):
+    _fields_ = [("n_individuals", C.c_uint32), ("n_concepts", C.c_uint32), ("concept_bits", C.c_void_p),
+                ("n_roles", C.c_uint32), ("role_edge_off", C.c_void_p), ("edge_subj", C.c_void_p),
+                ("edge_obj", C.c_void_p), ("n_data", C.c_uint32), ("data_off", C.c_void_p),
+                ("data_subj", C.c_void_p), ("data_val", C.c_void_p), ("n_pos", C.c_uint32),
+                ("pos_ids", C.c_void_p), ("n_neg", C.c_uint32), ("neg_ids", C.c_void_p)]
+
+
+class _KbInfo(C.Structure):
+    _fields_ = [("n_individuals", C.c_uint32), ("words", C.c_uint32), ("words_padded", C.c_uint32),
+                ("n_concepts", C.c_uint32), ("n_roles", C.c_uint32), ("n_data", C.c_uint32),
+                ("n_pos", C.c_uint64), ("n_neg", C.c_uint64), ("device_bytes", C.c_uint64),
+                ("edges", C.c_uint64 * 64), ("heavy", C.c_uint64 * 64)]
+
+
+class _ProgInfo(C.Structure):
+    _fields_ = [("n_roots", C.c_uint32), ("n_nodes", C.c_uint32), ("n_levels", C.c_uint32),
+                ("n_bool", C.c_uint32), ("n_restrict", C.c_uint32), ("n_drange", C.c_uint32),
+                ("alg_bytes_total", C.c_double), ("alg_bytes_shared", C.c_double)]
+
+
+class _ProfEntry(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_uint64), ("total_ms", C.c_double),
+                ("alg_bytes", C.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libhedl.so (raises if it is missing: there is no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build() (no CPU fallback exists)")
+    L = C.CDLL(LIB_PATH)
+    P, U32, U64, I32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int32
+    sig = {
+        "hedl_kb_load": ([C.POINTER(_KbDesc), C.c_int, P, C.POINTER(P)], I32),
+        "hedl_kb_free": ([P], I32),
+        "hedl_kb_get_info": ([P, C.POINTER(_KbInfo)], I32),
+        "hedl_compile": ([P, P, U32, P, U64, P, U32, U32, C.POINTER(P)], I32),
+        "hedl_program_free": ([P], I32),
+        "hedl_program_get_info": ([P, C.POINTER(_ProgInfo)], I32),
+        "hedl_program_root_bytes": ([P, U32, U32, P], I32),
+        "hedl_eval_one": ([P, P, U32, P, P, P], I32),
+        "hedl_eval_batch": ([P, P, U32, U32, P, P, P, U32], I32),
+        "hedl_program_set_workspace_limit": ([P, U64], I32),
+        "hedl_last_error": ([], C.c_char_p),
+        "hedl_version": ([], C.c_char_p),
+        "hedl_prof_enable": ([C.c_int], I32),
+        "hedl_prof_reset": ([], I32),
+        "hedl_prof_read": ([C.POINTER(_ProfEntry), C.c_int], C.c_int),
+        "hedl_launch_count": ([], U64),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _check(code: int):
+    if code:
+        raise HedlError(code, lib().hedl_last_error().decode(errors="replace"))
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return C.c_void_p(a.ctypes.data) if a is not None and a.size else None
+
+
+def _stream(stream):
+    import torch
+    if stream is None and not torch.cuda.is_available():
+        return None               # the library itself reports HEDL_ERR_UNSUPPORTED
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+class KB:
+    """A loaded knowledge base (hedl_kb*) on one CUDA device."""
+
+    def __init__(self, handle, device: int, n: int):
+        self._h = handle
+        self.device = device
+        self.N = n
+        self.W = (n + 31) // 32
+
+    def info(self) -> dict:
+        inf = _KbInfo()
+        _check(lib().hedl_kb_get_info(self._h, C.byref(inf)))
+        R = inf.n_roles
+        return {"N": inf.n_individuals, "W": inf.words, "W4": inf.words_padded, "C": inf.n_concepts,
+                "R": R, "D": inf.n_data, "n_pos": inf.n_pos, "n_neg": inf.n_neg,
+                "device_bytes": inf.device_bytes, "edges": list(inf.edges[:2 * R]),
+                "heavy": list(inf.heavy[:2 * R])}
+
+    def free(self):
+        if self._h:
+            lib().hedl_kb_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Program:
+    """A compiled hypothesis batch (hedl_program*)."""
+
+    def __init__(self, handle, kb: KB, n_roots: int):
+        self._h = handle
+        self.kb = kb
+        self.n_roots = n_roots
+
+    def info(self) -> dict:
+        inf = _ProgInfo()
+        _check(lib().hedl_program_get_info(self._h, C.byref(inf)))
+        return {k: getattr(inf, k) for k, _ in _ProgInfo._fields_}
+
+    def root_bytes(self, first: int = 0, n: Optional[int] = None) -> np.ndarray:
+        n = self.n_roots - first if n is None else n
+        out = np.zeros(n, dtype=np.float64)
+        _check(lib().hedl_program_root_bytes(self._h, first, n, _ptr(out)))
+        return out
+
+    def set_workspace_limit(self, nbytes: int):
+        _check(lib().hedl_program_set_workspace_limit(self._h, int(nbytes)))
+
+    def free(self):
+        if self._h:
+            lib().hedl_program_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def hedl_kb_load(kb: dict, device: int = 0, stream=None) -> KB:
+    """hedl_kb_load over a KB dict with the hedl_kb_desc arrays (see synth/format.py)."""
+    import torch
+    L = lib()
+    arrs = {
+        "concept_bits": np.ascontiguousarray(kb["concept_bits"], dtype=np.uint32),
+        "role_edge_off": np.ascontiguousarray(kb["role_edge_off"], dtype=np.uint64),
+        "edge_subj": np.ascontiguousarray(kb["edge_subj"], dtype=np.uint32),
+        "edge_obj": np.ascontiguousarray(kb["edge_obj"], dtype=np.uint32),
+        "data_off": np.ascontiguousarray(kb["data_off"], dtype=np.uint64),
+        "data_subj": np.ascontiguousarray(kb["data_subj"], dtype=np.uint32),
+        "data_val": np.ascontiguousarray(kb["data_val"], dtype=np.float32),
+        "pos_ids": np.ascontiguousarray(kb["pos_ids"], dtype=np.uint32),
+        "neg_ids": np.ascontiguousarray(kb["neg_ids"], dtype=np.uint32),
+    }
+    cb = arrs["concept_bits"]
+    d = _KbDesc()
+    d.n_individuals = int(kb["N"])
+    d.n_concepts = cb.shape[0] if cb.ndim == 2 else 0
+    d.concept_bits = _ptr(cb)
+    d.n_roles = len(arrs["role_edge_off"]) - 1
+    d.role_edge_off = _ptr(arrs["role_edge_off"])
+    d.edge_subj, d.edge_obj = _ptr(arrs["edge_subj"]), _ptr(arrs["edge_obj"])
+    d.n_data = len(arrs["data_off"]) - 1
+    d.data_off = _ptr(arrs["data_off"])
+    d.data_subj, d.data_val = _ptr(arrs["data_subj"]), _ptr(arrs["data_val"])
+    d.n_pos, d.pos_ids = len(arrs["pos_ids"]), _ptr(arrs["pos_ids"])
+    d.n_neg, d.neg_ids = len(arrs["neg_ids"]), _ptr(arrs["neg_ids"])
+    h = C.c_void_p()
+    if not torch.cuda.is_available():
+        _check(L.hedl_kb_load(C.byref(d), device, None, C.byref(h)))
+    with torch.cuda.device(device):
+        _check(L.hedl_kb_load(C.byref(d), device, _stream(stream), C.byref(h)))
+    return KB(h, device, int(kb["N"]))
+
+
+def hedl_compile(kb: KB, nodes: np.ndarray, child_idx: np.ndarray, roots: np.ndarray,
+                 flags: int = 0) -> Program:
+    nodes = np.ascontiguousarray(nodes)
+    assert nodes.dtype.itemsize == 28, "nodes must use synth.format.NODE_DTYPE (hedl_node)"
+    kids = np.ascontiguousarray(child_idx, dtype=np.uint32)
+    roots = np.ascontiguousarray(roots, dtype=np.uint32)
+    h = C.c_void_p()
+    _check(lib().hedl_compile(kb._h, _ptr(nodes), len(nodes), _ptr(kids), len(kids), _ptr(roots),
+                              len(roots), flags, C.byref(h)))
+    return Program(h, kb, len(roots))
+
+
+def hedl_eval_one(kb: KB, prog: Program, root: int, want_bits: bool = False, stream=None):
+    """-> (bits int32 tensor [W] on the KB's device or None, (tp, fp, fn, tn))."""
+    import torch
+    out = np.zeros(4, dtype=np.uint64)
+    bits = None
+    with torch.cuda.device(kb.device):
+        if want_bits:
+            bits = torch.empty(max(kb.W, 1), dtype=torch.int32, device=f"cuda:{kb.device}")
+        _check(lib().hedl_eval_one(kb._h, prog._h, root, C.c_void_p(bits.data_ptr()) if want_bits else None,
+                                   _ptr(out), _stream(stream)))
+    return (bits[:kb.W] if want_bits else None), tuple(int(v) for v in out)
+
+
+def hedl_eval_batch(kb: KB, prog: Program, first: int = 0, n: Optional[int] = None, want_bits: bool = False,
+                    counts_device: bool = False, stream=None, flags: int = 0, out_bits=None, out_counts=None):
+    """-> (bits int32 tensor [n][W] or None, counts [n][4] (numpy u64 on host, or int64 tensor on device))."""
+    import torch
+    n = prog.n_roots - first if n is None else n
+    dev = f"cuda:{kb.device}"
+    with torch.cuda.device(kb.device):
+        bits = out_bits
+        if want_bits and bits is None:
+            bits = torch.empty((n, max(kb.W, 1)), dtype=torch.int32, device=dev)
+        if counts_device:
+            counts = out_counts if out_counts is not None else torch.empty((n, 4), dtype=torch.int64, device=dev)
+            cptr = C.c_void_p(counts.data_ptr())
+            flags |= HEDL_EVAL_COUNTS_DEVICE
+        else:
+            counts = np.zeros((n, 4), dtype=np.uint64)
+            cptr = _ptr(counts)
+        _check(lib().hedl_eval_batch(kb._h, prog._h, first, n,
+                                     C.c_void_p(bits.data_ptr()) if bits is not None else None,
+                                     cptr, _stream(stream), flags))
+    if bits is not None and kb.W == 0:
+        bits = bits[:, :0]
+    return bits, counts
+
+
+def prof_enable(on: bool = True):
+    _check(lib().hedl_prof_enable(1 if on else 0))
+
+
+def prof_reset():
+    _check(lib().hedl_prof_reset())
+
+
+def prof_read() -> list:
+    L = lib()
+    n = L.hedl_prof_read(None, 0)
+    arr = (_ProfEntry * max(n, 1))()
+    n = L.hedl_prof_read(arr, n)
+    return [{"name": arr[i].name.decode(), "launches": arr[i].launches, "total_ms": arr[i].total_ms,
+             "alg_bytes": arr[i].alg_bytes} for i in range(n)]
+
+
+def launch_count() -> int:
+    return int(lib().hedl_launch_count())
+
+
+def version() -> str:
+    return lib().hedl_version().decode()

@@ -1,0 +1,117 @@
+// Diagnostics of the C ABI: thread-local last error, version, launch counter,
+// CUDA-event kernel timing (used by bench.py for the roofline "achieved").
+#include <cstdio>
+
+#include "internal.h"
+
+namespace hedl {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+hedl_status fail(hedl_status st, const std::string &msg) {
+    g_last_error = msg;
+    return st;
+}
+
+hedl_status cuda_fail(const hedl_kb *kb, cudaError_t e, const char *where) {
+    if (kb) const_cast<hedl_kb *>(kb)->poisoned = true;
+    g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+    cudaGetLastError();
+    return HEDL_ERR_CUDA;
+}
+
+const char *kKClassName[KC_N] = {"bool", "restrict", "restrict_heavy", "drange", "cover_init", "gather",
+                                 "slice_pack", "slice", "slice_heavy", "kb"};
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+uint64_t launches_total() { return g_launches.load(); }
+
+struct ProfRec {
+    cudaEvent_t a, b;
+    int kc;
+    double bytes;
+};
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_ev_pool;
+static thread_local cudaEvent_t g_pending = nullptr;
+
+static cudaEvent_t get_event() {
+    if (!g_ev_pool.empty()) {
+        cudaEvent_t e = g_ev_pool.back();
+        g_ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void prof_begin(cudaStream_t s, int) {
+    if (!g_prof_on) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_pending = get_event();
+    cudaEventRecord(g_pending, s);
+}
+
+void prof_end(cudaStream_t s, int kc, double bytes) {
+    if (!g_prof_on || !g_pending) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEvent_t b = get_event();
+    cudaEventRecord(b, s);
+    g_prof.push_back({g_pending, b, kc, bytes});
+    g_pending = nullptr;
+}
+
+}  // namespace hedl
+
+using namespace hedl;
+
+extern "C" const char *hedl_last_error(void) { return g_last_error.c_str(); }
+extern "C" const char *hedl_version(void) { return "hedl-b200 0.1 (sm_100a)"; }
+extern "C" uint64_t hedl_launch_count(void) { return launches_total(); }
+
+extern "C" hedl_status hedl_prof_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_on = on != 0;
+    return HEDL_OK;
+}
+
+extern "C" hedl_status hedl_prof_reset(void) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto &r : g_prof) {
+        cudaEventSynchronize(r.b);
+        g_ev_pool.push_back(r.a);
+        g_ev_pool.push_back(r.b);
+    }
+    g_prof.clear();
+    return HEDL_OK;
+}
+
+extern "C" int hedl_prof_read(hedl_prof_entry *out, int max_entries) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    hedl_prof_entry acc[KC_N];
+    std::memset(acc, 0, sizeof(acc));
+    for (auto &r : g_prof) {
+        cudaEventSynchronize(r.b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        acc[r.kc].launches++;
+        acc[r.kc].total_ms += ms;
+        acc[r.kc].alg_bytes += r.bytes;
+    }
+    int n = 0;
+    for (int k = 0; k < KC_N; ++k) {
+        if (!acc[k].launches) continue;
+        if (out && n < max_entries) {
+            out[n] = acc[k];
+            std::snprintf(out[n].name, sizeof(out[n].name), "%s", kKClassName[k]);
+        }
+        ++n;
+    }
+    return n;
+}

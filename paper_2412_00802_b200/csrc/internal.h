@@ -1,0 +1,192 @@
+// Internal definitions of the hedl library (not part of the ABI).
+// Device layout of the knowledge base: SURVEY 8(a) row a0 / DESIGN.md "Data layout".
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/hedl.h"
+
+namespace hedl {
+
+// ---- degree bins ------------------------------------------
+// light  : deg <= kLightDeg      lane = individual, ballot builds the word
+// medium : deg <= kHeavyDeg      warp-cooperative, 32 neighbours per step
+// heavy  : deg >  kHeavyDeg      CTA chunks of kHeavyChunk edges, atomics + last-CTA finalise
+constexpr uint32_t kLightDeg = 32;
+constexpr uint32_t kHeavyDeg = 512;
+constexpr uint32_t kHeavyChunk = 4096;
+
+// ---- restriction predicates ---------------------------------------------------
+// Every role restriction counts the neighbours y of x whose (possibly
+// complemented) child bit is 1, saturating at `sat`, then applies `pred`:
+//   EXISTS  : count C,      GE n=1   (Alg. 4: a matching assertion sets x)
+//   FORALL  : count not-C,  LE n=0   (Alg. 6: a non-matching assertion clears x)
+//   MIN/MAX/EXACT: count C, GE / LE / EQ n  (Alg. 7-8), LEP = paper MAX
+enum Pred : uint8_t { P_GE = 0, P_LE = 1, P_EQ = 2, P_LEP = 3 };
+
+// ---- canonical program ---------------------------------------------------------
+// Operand reference: bit0 = complement, bits1-2 = type, bits 3.. = id.
+enum RefType : uint32_t { RT_NODE = 0, RT_ATOM = 1, RT_TOP = 2 };
+inline uint32_t mkref(RefType t, uint32_t id, uint32_t comp) { return (id << 3) | (uint32_t(t) << 1) | comp; }
+inline uint32_t ref_comp(uint32_t r) { return r & 1u; }
+inline RefType ref_type(uint32_t r) { return RefType((r >> 1) & 3u); }
+inline uint32_t ref_id(uint32_t r) { return r >> 3; }
+
+enum NodeKind : uint8_t { NK_AND = 0, NK_OR = 1, NK_RESTRICT = 2, NK_DRANGE = 3 };
+
+struct CNode {
+    uint8_t kind;        // NodeKind
+    uint8_t pred;        // restrict: Pred
+    uint16_t dir;        // restrict: 2*role + inverse ; drange: data property
+    uint32_t n;          // restrict: threshold
+    uint32_t sat;        // restrict: saturation point of the count
+    float lo, hi;        // drange
+    uint32_t op_begin;   // operands in Program::ops
+    uint32_t op_count;   // AND/OR: k ; RESTRICT: 1 (child, complement already folded) ; DRANGE: 0
+    uint32_t level;      // 1 + max level of node operands (0 if none)
+    double bytes;        // algorithmic bytes of this node
+};
+
+}  // namespace hedl
+
+// ---- handles -------------------------------------------------------------------
+struct hedl_dir {                  // one role direction
+    uint32_t *row_ptr = nullptr;   // device [N+1]
+    uint32_t *col = nullptr;       // device [E], sorted per row
+    uint64_t E = 0;
+    uint32_t n_heavy = 0, n_chunks = 0;
+    uint32_t *heavy_x = nullptr;       // device [n_heavy]
+    uint32_t *heavy_nchunks = nullptr; // device [n_heavy]
+    uint4 *chunks = nullptr;           // device [n_chunks] {heavy idx, e0, e1, 0}
+    std::vector<uint32_t> h_row_ptr;   // host copy (planning of lane-packed kernels)
+    uint32_t max_deg = 0;
+    uint64_t E_heavy = 0;              // edges of heavy rows
+};
+
+struct hedl_data {
+    uint32_t *row_ptr = nullptr;   // device [N+1]
+    float *val = nullptr;          // device [V], ascending within each individual
+    uint64_t V = 0;
+};
+
+struct hedl_kb {
+    int device = 0;
+    int sm_count = 148;
+    uint32_t N = 0, W = 0, W4 = 0, C = 0, R = 0, D = 0;
+    uint32_t *concepts = nullptr;  // device [C][W4]
+    uint32_t *ones = nullptr;      // device [W4], tail-masked TOP row
+    uint32_t *zeros = nullptr;     // device [W4]
+    uint32_t *pos = nullptr, *neg = nullptr;  // device [W4]
+    uint64_t npos = 0, nneg = 0;
+    std::vector<hedl_dir> dirs;    // 2R
+    std::vector<hedl_data> data;   // D
+    std::vector<void *> allocs;
+    uint64_t device_bytes = 0;
+    std::atomic<bool> poisoned{false};
+    std::vector<double> dir_bytes;  // 4(N+1) + 4E per direction
+    std::vector<double> data_bytes; // 4(N+1) + 4V per property
+};
+
+struct hedl_program {
+    const hedl_kb *kb = nullptr;
+    uint32_t flags = 0;
+    std::vector<hedl::CNode> nodes;
+    std::vector<uint32_t> ops;
+    std::vector<uint32_t> root_node;   // per root: computed canonical node id
+    std::vector<double> root_bytes;    // B(h)
+    uint32_t n_levels = 0;
+    // evaluation workspace (device), grown on demand
+    std::mutex mu;
+    void *ws = nullptr;
+    size_t ws_bytes = 0;
+    void *pinned = nullptr;
+    size_t pinned_bytes = 0;
+    uint64_t ws_limit = 8ull << 30;
+    // planning scratch (host)
+    std::vector<uint32_t> stamp;
+    uint32_t stamp_gen = 0;
+};
+
+namespace hedl {
+
+// ---- errors --------------------------------------------------------------------
+void set_error(const std::string &msg);
+hedl_status fail(hedl_status st, const std::string &msg);
+hedl_status cuda_fail(const hedl_kb *kb, cudaError_t e, const char *where);
+
+#define HEDL_CUDA(kb, call)                                  \
+    do {                                                     \
+        cudaError_t _e = (call);                             \
+        if (_e != cudaSuccess) return hedl::cuda_fail(kb, _e, #call); \
+    } while (0)
+
+// ---- profiling -----------------------------------------------------------------
+enum KClass { KC_BOOL, KC_RESTRICT, KC_HEAVY, KC_DRANGE, KC_COVER_INIT, KC_GATHER,
+              KC_SLICE_IN, KC_SLICE, KC_SLICE_HEAVY, KC_KB, KC_N };
+extern const char *kKClassName[KC_N];
+void prof_begin(cudaStream_t s, int kc);
+void prof_end(cudaStream_t s, int kc, double alg_bytes);
+
+// ---- kernels launchers (kernels.cu) -----------------------------------------
+struct BoolDesc {
+    uint32_t *out;
+    uint32_t op_first, op_count;   // into the operand table
+    uint32_t is_or;
+    int32_t cover;                 // counts slot or -1
+};
+struct Operand {
+    const uint32_t *ptr;
+    uint32_t mask;                 // 0 or ~0 (complement)
+    uint32_t pad;
+};
+struct RestrictDesc {
+    const uint32_t *child;
+    uint32_t *out;
+    uint32_t cmask;                // 0 or ~0
+    uint32_t pred, n, sat;
+    int32_t cover;                 // counts slot or -1
+    uint32_t heavy_slot;           // scratch base index for heavy counters of this node
+};
+struct DrangeDesc {
+    uint32_t *out;
+    float lo, hi;
+    int32_t cover;
+    uint32_t prop;
+};
+struct DirDev {                   // passed by value
+    const uint32_t *row_ptr;
+    const uint32_t *col;
+    const uint32_t *heavy_x;
+    const uint32_t *heavy_nchunks;
+    const uint4 *chunks;
+    uint32_t n_heavy, n_chunks;
+};
+struct KbDev {
+    uint32_t N, W, W4;
+    const uint32_t *pos, *neg;
+};
+
+void launch_cover_init(cudaStream_t s, hedl_counts *counts, uint32_t n, uint64_t npos, uint64_t nneg);
+void launch_bool(cudaStream_t s, const KbDev &kb, const BoolDesc *d_desc, uint32_t n_desc,
+                 const Operand *d_ops, hedl_counts *counts, double alg_bytes);
+void launch_restrict(cudaStream_t s, const KbDev &kb, const DirDev &dir, const RestrictDesc *d_desc,
+                     uint32_t n_desc, hedl_counts *counts, uint32_t *heavy_scratch, double alg_light,
+                     double alg_heavy);
+void launch_drange(cudaStream_t s, const KbDev &kb, const uint32_t *row_ptr, const float *val,
+                   const DrangeDesc *d_desc, uint32_t n_desc, hedl_counts *counts, double alg_bytes);
+void launch_gather_counts(cudaStream_t s, const hedl_counts *slots, const uint32_t *slot_of,
+                          hedl_counts *out, uint32_t n);
+void launch_gather_bits(cudaStream_t s, const uint32_t *const *rows, uint32_t *out, uint32_t W,
+                        uint32_t n);
+void launch_kb_build(cudaStream_t s);
+uint64_t launches_total();
+void count_launch();
+
+}  // namespace hedl

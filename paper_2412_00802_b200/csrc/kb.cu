@@ -1,0 +1,285 @@
+// hedl_kb_load: host build of the device KB layout, then upload.
+//
+// Paper: concepts matrix transposed (rows = concepts), roles as
+// 2-column (subj, obj) matrices with an offset table, numeric
+// concrete roles as (subj, value), examples matrix
+// (PAPER.md:541).  Here: bit-packed rows padded to 16 B, per role a deduped
+// CSR + transposed CSR (inverse roles), heavy-row chunk lists,
+// per data property a CSR of ascending non-NaN values, example bitsets.
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <thread>
+
+#include "internal.h"
+
+using namespace hedl;
+
+namespace {
+
+template <class F>
+void parallel_ranges(uint64_t n, F f) {
+    unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    if (n < (1u << 16) || nt == 1) { f(0, n); return; }
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) {
+        uint64_t a = n * t / nt, b = n * (t + 1) / nt;
+        th.emplace_back([=] { f(a, b); });
+    }
+    for (auto &x : th) x.join();
+}
+
+struct HostCSR {
+    std::vector<uint32_t> row_ptr, col;
+};
+
+// counting sort of (s, o) pairs by s, then sort + dedupe each row (sets)
+hedl_status build_forward(uint32_t N, const uint32_t *s, const uint32_t *o, uint64_t m, HostCSR &out) {
+    std::vector<uint64_t> cnt(N + 1, 0);
+    for (uint64_t k = 0; k < m; ++k) {
+        if (s[k] >= N || o[k] >= N) return fail(HEDL_ERR_OUT_OF_RANGE, "role assertion id >= N at index " + std::to_string(k));
+        cnt[s[k] + 1]++;
+    }
+    for (uint32_t i = 0; i < N; ++i) cnt[i + 1] += cnt[i];
+    std::vector<uint32_t> tmp(m);
+    {
+        std::vector<uint64_t> pos(cnt.begin(), cnt.end() - 1);
+        for (uint64_t k = 0; k < m; ++k) tmp[pos[s[k]]++] = o[k];
+    }
+    std::vector<uint32_t> ucnt(N, 0);
+    parallel_ranges(N, [&](uint64_t a, uint64_t b) {
+        for (uint64_t i = a; i < b; ++i) {
+            auto first = tmp.begin() + cnt[i], last = tmp.begin() + cnt[i + 1];
+            std::sort(first, last);
+            ucnt[i] = (uint32_t)(std::unique(first, last) - first);
+        }
+    });
+    out.row_ptr.assign(N + 1, 0);
+    uint64_t acc = 0;
+    for (uint32_t i = 0; i < N; ++i) {
+        out.row_ptr[i] = (uint32_t)acc;
+        acc += ucnt[i];
+        if (acc > 0xffffffffull) return fail(HEDL_ERR_INVALID_ARG, "a role has >= 2^32 distinct assertions");
+    }
+    out.row_ptr[N] = (uint32_t)acc;
+    out.col.resize(acc);
+    parallel_ranges(N, [&](uint64_t a, uint64_t b) {
+        for (uint64_t i = a; i < b; ++i)
+            std::copy(tmp.begin() + cnt[i], tmp.begin() + cnt[i] + ucnt[i], out.col.begin() + out.row_ptr[i]);
+    });
+    return HEDL_OK;
+}
+
+// transposed CSR of a deduped CSR: rows = objects, sorted subjects (PAPER.md:299 swap)
+void build_transpose(uint32_t N, const HostCSR &f, HostCSR &t) {
+    t.row_ptr.assign(N + 1, 0);
+    for (uint32_t y : f.col) t.row_ptr[y + 1]++;
+    for (uint32_t i = 0; i < N; ++i) t.row_ptr[i + 1] += t.row_ptr[i];
+    t.col.resize(f.col.size());
+    std::vector<uint32_t> pos(t.row_ptr.begin(), t.row_ptr.end() - 1);
+    for (uint32_t x = 0; x < N; ++x)
+        for (uint32_t e = f.row_ptr[x]; e < f.row_ptr[x + 1]; ++e) t.col[pos[f.col[e]]++] = x;
+}
+
+template <class T>
+hedl_status upload(hedl_kb *kb, cudaStream_t st, T **dst, const T *src, size_t n) {
+    size_t bytes = std::max<size_t>(n * sizeof(T), 16);
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? fail(HEDL_ERR_OOM, "device allocation failed")
+                                                                : cuda_fail(kb, e, "cudaMalloc");
+    kb->allocs.push_back(p);
+    kb->device_bytes += bytes;
+    if (n) HEDL_CUDA(kb, cudaMemcpyAsync(p, src, n * sizeof(T), cudaMemcpyHostToDevice, st));
+    *dst = (T *)p;
+    return HEDL_OK;
+}
+
+void free_kb(hedl_kb *kb) {
+    if (!kb) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(kb->device);
+    for (void *p : kb->allocs) cudaFree(p);
+    cudaSetDevice(prev);
+    delete kb;
+}
+
+}  // namespace
+
+extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *stream, hedl_kb **out) {
+    if (!desc || !out) return fail(HEDL_ERR_INVALID_ARG, "null desc/out");
+    *out = nullptr;
+    const uint32_t N = desc->n_individuals, W = (N + 31) / 32, W4 = (W + 3) & ~3u;
+    const uint32_t C = desc->n_concepts, R = desc->n_roles, D = desc->n_data;
+    if (R > 32) return fail(HEDL_ERR_INVALID_ARG, "at most 32 roles supported");
+    if (C && W && !desc->concept_bits) return fail(HEDL_ERR_INVALID_ARG, "concept_bits is null");
+    if (R && !desc->role_edge_off) return fail(HEDL_ERR_INVALID_ARG, "role_edge_off is null");
+    if (D && !desc->data_off) return fail(HEDL_ERR_INVALID_ARG, "data_off is null");
+    if (desc->n_pos && !desc->pos_ids) return fail(HEDL_ERR_INVALID_ARG, "pos_ids is null");
+    if (desc->n_neg && !desc->neg_ids) return fail(HEDL_ERR_INVALID_ARG, "neg_ids is null");
+    // tail bits of every concept row must be 0
+    if (C && W && (N & 31)) {
+        const uint32_t tail = ~((1u << (N & 31)) - 1u);
+        for (uint32_t c = 0; c < C; ++c)
+            if (desc->concept_bits[(uint64_t)c * W + W - 1] & tail)
+                return fail(HEDL_ERR_INVALID_ARG, "concept " + std::to_string(c) + " has non-zero tail bits");
+    }
+    if (R) {
+        if (desc->role_edge_off[0] != 0) return fail(HEDL_ERR_INVALID_ARG, "role_edge_off[0] != 0");
+        for (uint32_t r = 0; r < R; ++r)
+            if (desc->role_edge_off[r + 1] < desc->role_edge_off[r]) return fail(HEDL_ERR_INVALID_ARG, "role_edge_off not monotone");
+        if (desc->role_edge_off[R] && (!desc->edge_subj || !desc->edge_obj)) return fail(HEDL_ERR_INVALID_ARG, "edge arrays null");
+    }
+    if (D) {
+        if (desc->data_off[0] != 0) return fail(HEDL_ERR_INVALID_ARG, "data_off[0] != 0");
+        for (uint32_t d = 0; d < D; ++d)
+            if (desc->data_off[d + 1] < desc->data_off[d]) return fail(HEDL_ERR_INVALID_ARG, "data_off not monotone");
+        if (desc->data_off[D] && (!desc->data_subj || !desc->data_val)) return fail(HEDL_ERR_INVALID_ARG, "data arrays null");
+    }
+    // examples (P and N disjoint)
+    std::vector<uint32_t> pos(W4, 0), neg(W4, 0);
+    for (uint32_t i = 0; i < desc->n_pos; ++i) {
+        uint32_t x = desc->pos_ids[i];
+        if (x >= N) return fail(HEDL_ERR_OUT_OF_RANGE, "pos id >= N");
+        pos[x >> 5] |= 1u << (x & 31);
+    }
+    for (uint32_t i = 0; i < desc->n_neg; ++i) {
+        uint32_t x = desc->neg_ids[i];
+        if (x >= N) return fail(HEDL_ERR_OUT_OF_RANGE, "neg id >= N");
+        if (pos[x >> 5] & (1u << (x & 31))) return fail(HEDL_ERR_EXAMPLE_CONFLICT, "individual " + std::to_string(x) + " is both + and -");
+        neg[x >> 5] |= 1u << (x & 31);
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+        return fail(HEDL_ERR_UNSUPPORTED, "no such CUDA device");
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return fail(HEDL_ERR_UNSUPPORTED, "device query failed");
+    if (prop.major != 10) return fail(HEDL_ERR_UNSUPPORTED, "library is built for sm_100a (B200) only");
+
+    // ---- host build ------------------------------------------------------------
+    std::vector<HostCSR> fw(R), tr(R);
+    for (uint32_t r = 0; r < R; ++r) {
+        const uint64_t a = desc->role_edge_off[r], b = desc->role_edge_off[r + 1];
+        hedl_status st = build_forward(N, desc->edge_subj + a, desc->edge_obj + a, b - a, fw[r]);
+        if (st) return st;
+        build_transpose(N, fw[r], tr[r]);
+    }
+    struct HostData { std::vector<uint32_t> row_ptr; std::vector<float> val; };
+    std::vector<HostData> hd(D);
+    for (uint32_t d = 0; d < D; ++d) {
+        const uint64_t a = desc->data_off[d], b = desc->data_off[d + 1];
+        std::vector<uint64_t> cnt(N + 1, 0);
+        for (uint64_t k = a; k < b; ++k) {
+            if (desc->data_subj[k] >= N) return fail(HEDL_ERR_OUT_OF_RANGE, "data subject id >= N");
+            if (!std::isnan(desc->data_val[k])) cnt[desc->data_subj[k] + 1]++;   // NaN never matches (Q10)
+        }
+        for (uint32_t i = 0; i < N; ++i) cnt[i + 1] += cnt[i];
+        if (cnt[N] > 0xffffffffull) return fail(HEDL_ERR_INVALID_ARG, "data property has >= 2^32 values");
+        hd[d].row_ptr.resize(N + 1);
+        for (uint32_t i = 0; i <= N; ++i) hd[d].row_ptr[i] = (uint32_t)cnt[i];
+        hd[d].val.resize(cnt[N]);
+        std::vector<uint64_t> p(cnt.begin(), cnt.end() - 1);
+        for (uint64_t k = a; k < b; ++k)
+            if (!std::isnan(desc->data_val[k])) hd[d].val[p[desc->data_subj[k]]++] = desc->data_val[k];
+        auto &v = hd[d].val;
+        auto &rp = hd[d].row_ptr;
+        parallel_ranges(N, [&](uint64_t x0, uint64_t x1) {
+            for (uint64_t i = x0; i < x1; ++i) std::sort(v.begin() + rp[i], v.begin() + rp[i + 1]);
+        });
+    }
+
+    // ---- upload -------------------------------------------------------------------
+    int prev_dev = 0;
+    cudaGetDevice(&prev_dev);
+    if (cudaSetDevice(device) != cudaSuccess) return fail(HEDL_ERR_CUDA, "cudaSetDevice failed");
+    cudaStream_t st = (cudaStream_t)stream;
+    hedl_kb *kb = new hedl_kb();
+    kb->device = device;
+    kb->sm_count = prop.multiProcessorCount;
+    kb->N = N; kb->W = W; kb->W4 = W4; kb->C = C; kb->R = R; kb->D = D;
+    auto bail = [&](hedl_status s) { free_kb(kb); cudaSetDevice(prev_dev); return s; };
+    hedl_status s;
+    {
+        std::vector<uint32_t> cpad((uint64_t)C * W4, 0);
+        for (uint32_t c = 0; c < C; ++c)
+            if (W) std::memcpy(&cpad[(uint64_t)c * W4], desc->concept_bits + (uint64_t)c * W, W * 4ull);
+        std::vector<uint32_t> ones(W4, 0), zeros(W4, 0);
+        for (uint32_t w = 0; w < W; ++w) ones[w] = 0xffffffffu;
+        if (W && (N & 31)) ones[W - 1] = (1u << (N & 31)) - 1u;
+        if ((s = upload(kb, st, &kb->concepts, cpad.data(), cpad.size()))) return bail(s);
+        if ((s = upload(kb, st, &kb->ones, ones.data(), ones.size()))) return bail(s);
+        if ((s = upload(kb, st, &kb->zeros, zeros.data(), zeros.size()))) return bail(s);
+        if ((s = upload(kb, st, &kb->pos, pos.data(), pos.size()))) return bail(s);
+        if ((s = upload(kb, st, &kb->neg, neg.data(), neg.size()))) return bail(s);
+        for (uint32_t w = 0; w < W4; ++w) { kb->npos += __builtin_popcount(pos[w]); kb->nneg += __builtin_popcount(neg[w]); }
+        if (cudaStreamSynchronize(st) != cudaSuccess) return bail(fail(HEDL_ERR_CUDA, "upload failed"));
+    }
+    kb->dirs.resize(2 * R);
+    kb->dir_bytes.resize(2 * R);
+    for (uint32_t r = 0; r < R; ++r) {
+        for (int inv = 0; inv < 2; ++inv) {
+            HostCSR &h = inv ? tr[r] : fw[r];
+            hedl_dir &dr = kb->dirs[2 * r + inv];
+            dr.E = h.col.size();
+            if ((s = upload(kb, st, &dr.row_ptr, h.row_ptr.data(), h.row_ptr.size()))) return bail(s);
+            if ((s = upload(kb, st, &dr.col, h.col.data(), h.col.size()))) return bail(s);
+            std::vector<uint32_t> hx, hn;
+            std::vector<uint4> chunks;
+            for (uint32_t x = 0; x < N; ++x) {
+                const uint32_t a = h.row_ptr[x], b = h.row_ptr[x + 1], deg = b - a;
+                dr.max_deg = std::max(dr.max_deg, deg);
+                if (deg > kHeavyDeg) {
+                    const uint32_t hi = (uint32_t)hx.size();
+                    hx.push_back(x);
+                    uint32_t nc = 0;
+                    for (uint32_t e = a; e < b; e += kHeavyChunk, ++nc)
+                        chunks.push_back(make_uint4(hi, e, std::min(b, e + kHeavyChunk), 0));
+                    hn.push_back(nc);
+                    dr.E_heavy += deg;
+                }
+            }
+            dr.n_heavy = (uint32_t)hx.size();
+            dr.n_chunks = (uint32_t)chunks.size();
+            if ((s = upload(kb, st, &dr.heavy_x, hx.data(), hx.size()))) return bail(s);
+            if ((s = upload(kb, st, &dr.heavy_nchunks, hn.data(), hn.size()))) return bail(s);
+            if ((s = upload(kb, st, &dr.chunks, chunks.data(), chunks.size()))) return bail(s);
+            kb->dir_bytes[2 * r + inv] = 4.0 * (N + 1) + 4.0 * dr.E;
+            // the uploads read host vectors that die at scope end: wait before reuse
+            if (cudaStreamSynchronize(st) != cudaSuccess) return bail(fail(HEDL_ERR_CUDA, "upload failed"));
+            dr.h_row_ptr = std::move(h.row_ptr);
+            std::vector<uint32_t>().swap(h.col);
+        }
+    }
+    kb->data.resize(D);
+    kb->data_bytes.resize(D);
+    for (uint32_t d = 0; d < D; ++d) {
+        kb->data[d].V = hd[d].val.size();
+        if ((s = upload(kb, st, &kb->data[d].row_ptr, hd[d].row_ptr.data(), hd[d].row_ptr.size()))) return bail(s);
+        if ((s = upload(kb, st, &kb->data[d].val, hd[d].val.data(), hd[d].val.size()))) return bail(s);
+        kb->data_bytes[d] = 4.0 * (N + 1) + 4.0 * kb->data[d].V;
+        if (cudaStreamSynchronize(st) != cudaSuccess) return bail(fail(HEDL_ERR_CUDA, "upload failed"));
+    }
+    cudaSetDevice(prev_dev);
+    *out = kb;
+    return HEDL_OK;
+}
+
+extern "C" hedl_status hedl_kb_free(hedl_kb *kb) {
+    free_kb(kb);
+    return HEDL_OK;
+}
+
+extern "C" hedl_status hedl_kb_get_info(const hedl_kb *kb, hedl_kb_info *out) {
+    if (!kb || !out) return fail(HEDL_ERR_INVALID_ARG, "null kb/out");
+    std::memset(out, 0, sizeof(*out));
+    out->n_individuals = kb->N; out->words = kb->W; out->words_padded = kb->W4;
+    out->n_concepts = kb->C; out->n_roles = kb->R; out->n_data = kb->D;
+    out->n_pos = kb->npos; out->n_neg = kb->nneg;
+    out->device_bytes = kb->device_bytes;
+    for (size_t i = 0; i < kb->dirs.size() && i < 64; ++i) {
+        out->edges[i] = kb->dirs[i].E;
+        out->heavy[i] = kb->dirs[i].n_heavy;
+    }
+    return HEDL_OK;
+}

@@ -1,0 +1,353 @@
+// Per-node sm_100a kernels of the hot path.
+//
+//  k_bool           n-ary AND/OR with per-operand complement (Alg. 2),
+//                   128-bit words, tail mask, fused coverage (Alg. 15).
+//  k_restrict       exists / forall / >=n / <=n / =n over a role direction's CSR
+//                   (Algs. 4, 6, 8; inverse = transposed CSR):
+//                   light + medium degree bins, ballot-assembled output words,
+//                   saturating counts with early exit, fused coverage.
+//  k_restrict_heavy heavy rows (deg > kHeavyDeg) split over CTAs; the last CTA
+//                   of a row finalises its bit with atomicOr (no other atomics on rows).
+//  k_drange         exists d.[lo,hi] over sorted per-individual values (Alg. 10, Q9).
+//
+// Every output word is written exactly once by one warp (plus commutative
+// atomicOr of heavy bits), so results are deterministic (no paper-style
+// check-then-write race).
+#include "internal.h"
+
+namespace hedl {
+
+namespace {
+constexpr uint32_t FULL = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t probe(const uint32_t *__restrict__ child, uint32_t y, uint32_t cmask) {
+    return ((__ldg(child + (y >> 5)) ^ cmask) >> (y & 31)) & 1u;
+}
+
+__device__ __forceinline__ bool pred_eval(uint32_t pred, uint32_t cnt, uint32_t n) {
+    switch (pred) {
+    case P_GE: return cnt >= n;
+    case P_LE: return cnt <= n;
+    case P_EQ: return cnt == n;
+    default: return cnt > 0 && cnt <= n;   // P_LEP: paper MAX
+    }
+}
+
+__device__ __forceinline__ uint32_t tail_word(uint32_t v, uint32_t w, uint32_t W, uint32_t N) {
+    if (w >= W) return 0u;
+    if (w == W - 1 && (N & 31u)) v &= (1u << (N & 31u)) - 1u;
+    return v;
+}
+
+// block-wide reduction of (tp, fp) and one u64 atomic per CTA.  All threads call.
+__device__ __forceinline__ void block_cover(hedl_counts *counts, int slot, uint32_t tp, uint32_t fp) {
+    __shared__ uint32_t s_tp[32], s_fp[32];
+    tp = __reduce_add_sync(FULL, tp);
+    fp = __reduce_add_sync(FULL, fp);
+    const uint32_t wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) { s_tp[wid] = tp; s_fp[wid] = fp; }
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t nw = blockDim.x >> 5;
+        uint32_t a = lane < nw ? s_tp[lane] : 0u, b = lane < nw ? s_fp[lane] : 0u;
+        a = __reduce_add_sync(FULL, a);
+        b = __reduce_add_sync(FULL, b);
+        if (lane == 0) {
+            hedl_counts *c = counts + slot;
+            if (a) {
+                atomicAdd((unsigned long long *)&c->tp, (unsigned long long)a);
+                atomicAdd((unsigned long long *)&c->fn, (unsigned long long)(0ull - a));
+            }
+            if (b) {
+                atomicAdd((unsigned long long *)&c->fp, (unsigned long long)b);
+                atomicAdd((unsigned long long *)&c->tn, (unsigned long long)(0ull - b));
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------
+__global__ void k_cover_init(hedl_counts *c, uint32_t n, uint64_t npos, uint64_t nneg) {
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) c[i] = hedl_counts{0, 0, npos, nneg};
+}
+
+// ------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_bool(KbDev kb, const BoolDesc *__restrict__ descs,
+                                              const Operand *__restrict__ ops, hedl_counts *counts) {
+    const BoolDesc d = descs[blockIdx.y];
+    const uint32_t n4 = kb.W4 >> 2;
+    uint32_t tp = 0, fp = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+        uint4 acc = d.is_or ? make_uint4(0, 0, 0, 0) : make_uint4(FULL, FULL, FULL, FULL);
+        for (uint32_t j = 0; j < d.op_count; ++j) {
+            const Operand o = ops[d.op_first + j];
+            uint4 v = __ldg(reinterpret_cast<const uint4 *>(o.ptr) + i);
+            v.x ^= o.mask; v.y ^= o.mask; v.z ^= o.mask; v.w ^= o.mask;
+            if (d.is_or) { acc.x |= v.x; acc.y |= v.y; acc.z |= v.z; acc.w |= v.w; }
+            else { acc.x &= v.x; acc.y &= v.y; acc.z &= v.z; acc.w &= v.w; }
+        }
+        const uint32_t w0 = i << 2;
+        acc.x = tail_word(acc.x, w0, kb.W, kb.N);
+        acc.y = tail_word(acc.y, w0 + 1, kb.W, kb.N);
+        acc.z = tail_word(acc.z, w0 + 2, kb.W, kb.N);
+        acc.w = tail_word(acc.w, w0 + 3, kb.W, kb.N);
+        reinterpret_cast<uint4 *>(d.out)[i] = acc;
+        if (d.cover >= 0) {
+            const uint4 p = __ldg(reinterpret_cast<const uint4 *>(kb.pos) + i);
+            const uint4 q = __ldg(reinterpret_cast<const uint4 *>(kb.neg) + i);
+            tp += __popc(acc.x & p.x) + __popc(acc.y & p.y) + __popc(acc.z & p.z) + __popc(acc.w & p.w);
+            fp += __popc(acc.x & q.x) + __popc(acc.y & q.y) + __popc(acc.z & q.z) + __popc(acc.w & q.w);
+        }
+    }
+    if (d.cover >= 0) block_cover(counts, d.cover, tp, fp);
+}
+
+// ------------------------------------------------------------------------------
+// warp per output word (32 individuals); 8 warps per CTA; blockIdx.y = node.
+__global__ void __launch_bounds__(256) k_restrict(KbDev kb, DirDev dir, const RestrictDesc *__restrict__ descs,
+                                                  hedl_counts *counts) {
+    const RestrictDesc d = descs[blockIdx.y];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t w = blockIdx.x * 8 + (threadIdx.x >> 5);
+    uint32_t tp = 0, fp = 0;
+    if (w < kb.W4) {
+        uint32_t word = 0;
+        if (w < kb.W) {
+            const uint32_t x = (w << 5) + lane;
+            const bool valid = x < kb.N;
+            uint32_t a = 0, b = 0;
+            if (valid) { a = __ldg(dir.row_ptr + x); b = __ldg(dir.row_ptr + x + 1); }
+            const uint32_t deg = b - a;
+            const uint32_t sat = d.sat;
+            uint32_t cnt = 0;
+            if (deg <= kLightDeg) {
+                // light: the lane scans its own neighbours, 4 probes in flight, early exit
+                for (uint32_t e = a; e < b && cnt < sat; e += 4) {
+                    uint32_t y0 = __ldg(dir.col + e);
+                    uint32_t y1 = e + 1 < b ? __ldg(dir.col + e + 1) : 0xffffffffu;
+                    uint32_t y2 = e + 2 < b ? __ldg(dir.col + e + 2) : 0xffffffffu;
+                    uint32_t y3 = e + 3 < b ? __ldg(dir.col + e + 3) : 0xffffffffu;
+                    uint32_t c = probe(d.child, y0, d.cmask);
+                    if (y1 != 0xffffffffu) c += probe(d.child, y1, d.cmask);
+                    if (y2 != 0xffffffffu) c += probe(d.child, y2, d.cmask);
+                    if (y3 != 0xffffffffu) c += probe(d.child, y3, d.cmask);
+                    cnt += c;
+                }
+            }
+            // medium: the whole warp scans one individual's neighbours, 128 per step
+            unsigned med = __ballot_sync(FULL, valid && deg > kLightDeg && deg <= kHeavyDeg);
+            while (med) {
+                const int l = __ffs(med) - 1;
+                med &= med - 1;
+                const uint32_t ma = __shfl_sync(FULL, a, l), mb = __shfl_sync(FULL, b, l);
+                uint32_t c = 0;
+                for (uint32_t e = ma; e < mb && c < sat; e += 128) {
+                    uint32_t bit[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint32_t k = e + u * 32 + lane;
+                        bit[u] = k < mb ? probe(d.child, __ldg(dir.col + k), d.cmask) : 0u;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) c += __popc(__ballot_sync(FULL, bit[u]));
+                }
+                if (lane == (uint32_t)l) cnt = c;
+            }
+            const bool res = valid && deg <= kHeavyDeg && pred_eval(d.pred, min(cnt, sat), d.n);
+            word = __ballot_sync(FULL, res);
+        }
+        if (lane == 0) {
+            d.out[w] = word;
+            if (d.cover >= 0) {
+                tp = __popc(word & __ldg(kb.pos + w));
+                fp = __popc(word & __ldg(kb.neg + w));
+            }
+        }
+    }
+    if (d.cover >= 0) block_cover(counts, d.cover, tp, fp);
+}
+
+// ------------------------------------------------------------------------------
+// heavy rows: blockIdx.x = chunk of <= kHeavyChunk edges, blockIdx.y = node.
+__global__ void __launch_bounds__(256) k_restrict_heavy(KbDev kb, DirDev dir, const RestrictDesc *__restrict__ descs,
+                                                        hedl_counts *counts, uint32_t *scratch) {
+    const RestrictDesc d = descs[blockIdx.y];
+    const uint4 ch = dir.chunks[blockIdx.x];
+    uint32_t *cp = scratch + 2ull * (d.heavy_slot + ch.x);   // {count, ticket}
+    __shared__ uint32_t s_skip, s_last, s_red[8];
+    if (threadIdx.x == 0) s_skip = (*(volatile uint32_t *)cp) >= d.sat;
+    __syncthreads();
+    uint32_t c = 0;
+    if (!s_skip) {
+        for (uint32_t k = ch.y + threadIdx.x; k < ch.z; k += 1024) {
+            uint32_t y[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) y[u] = k + u * 256 < ch.z ? __ldg(dir.col + k + u * 256) : 0xffffffffu;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) if (y[u] != 0xffffffffu) c += probe(d.child, y[u], d.cmask);
+        }
+    }
+    c = __reduce_add_sync(FULL, c);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t tot = 0;
+        for (int i = 0; i < 8; ++i) tot += s_red[i];
+        if (tot) atomicAdd(cp, tot);
+        __threadfence();
+        const uint32_t t = atomicAdd(cp + 1, 1u);
+        s_last = (t == __ldg(dir.heavy_nchunks + ch.x) - 1);
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t tot = atomicAdd(cp, 0u);
+        const uint32_t x = __ldg(dir.heavy_x + ch.x);
+        if (pred_eval(d.pred, min(tot, d.sat), d.n)) {
+            const uint32_t bit = 1u << (x & 31);
+            atomicOr(d.out + (x >> 5), bit);
+            if (d.cover >= 0) {
+                hedl_counts *cc = counts + d.cover;
+                if (__ldg(kb.pos + (x >> 5)) & bit) {
+                    atomicAdd((unsigned long long *)&cc->tp, 1ull);
+                    atomicAdd((unsigned long long *)&cc->fn, ~0ull);
+                }
+                if (__ldg(kb.neg + (x >> 5)) & bit) {
+                    atomicAdd((unsigned long long *)&cc->fp, 1ull);
+                    atomicAdd((unsigned long long *)&cc->tn, ~0ull);
+                }
+            }
+        }
+        cp[0] = 0;   // self-clean: the scratch is zero again for the next launch
+        cp[1] = 0;
+    }
+}
+
+// ------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_drange(KbDev kb, const uint32_t *__restrict__ row_ptr,
+                                                const float *__restrict__ val, const DrangeDesc *__restrict__ descs,
+                                                hedl_counts *counts) {
+    const DrangeDesc d = descs[blockIdx.y];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t w = blockIdx.x * 8 + (threadIdx.x >> 5);
+    uint32_t tp = 0, fp = 0;
+    if (w < kb.W4) {
+        uint32_t word = 0;
+        if (w < kb.W) {
+            const uint32_t x = (w << 5) + lane;
+            bool res = false;
+            if (x < kb.N) {
+                uint32_t lo = __ldg(row_ptr + x), hi = __ldg(row_ptr + x + 1);
+                // first value >= d.lo in the ascending segment, then test <= d.hi
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (__ldg(val + mid) < d.lo) lo = mid + 1; else hi = mid;
+                }
+                res = lo < __ldg(row_ptr + x + 1) && __ldg(val + lo) <= d.hi;
+            }
+            word = __ballot_sync(FULL, res);
+        }
+        if (lane == 0) {
+            d.out[w] = word;
+            if (d.cover >= 0) {
+                tp = __popc(word & __ldg(kb.pos + w));
+                fp = __popc(word & __ldg(kb.neg + w));
+            }
+        }
+    }
+    if (d.cover >= 0) block_cover(counts, d.cover, tp, fp);
+}
+
+__global__ void k_gather_counts(const hedl_counts *__restrict__ slots, const uint32_t *__restrict__ slot_of,
+                                hedl_counts *out, uint32_t n) {
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = slots[slot_of[i]];
+}
+
+__global__ void k_gather_bits(const uint32_t *const *__restrict__ rows, uint32_t *out, uint32_t W) {
+    const uint32_t *src = rows[blockIdx.y];
+    uint32_t *dst = out + (uint64_t)blockIdx.y * W;
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gridDim.x * blockDim.x) dst[w] = src[w];
+}
+}  // namespace
+
+// ---- launchers -------------------------------------------------------------------
+static inline uint32_t cdiv(uint64_t a, uint64_t b) { return (uint32_t)((a + b - 1) / b); }
+
+void launch_cover_init(cudaStream_t s, hedl_counts *counts, uint32_t n, uint64_t npos, uint64_t nneg) {
+    if (!n) return;
+    prof_begin(s, KC_COVER_INIT);
+    k_cover_init<<<cdiv(n, 256), 256, 0, s>>>(counts, n, npos, nneg);
+    count_launch();
+    prof_end(s, KC_COVER_INIT, 32.0 * n);
+}
+
+void launch_bool(cudaStream_t s, const KbDev &kb, const BoolDesc *d_desc, uint32_t n_desc,
+                 const Operand *d_ops, hedl_counts *counts, double alg_bytes) {
+    for (uint32_t off = 0; off < n_desc; off += 65535) {
+        const uint32_t nd = n_desc - off < 65535 ? n_desc - off : 65535;
+        const uint32_t gx = kb.W4 ? cdiv(kb.W4 / 4, 256) : 0;
+        if (!gx) return;
+        dim3 grid(gx < 64 ? gx : 64, nd);
+        prof_begin(s, KC_BOOL);
+        k_bool<<<grid, 256, 0, s>>>(kb, d_desc + off, d_ops, counts);
+        count_launch();
+        prof_end(s, KC_BOOL, alg_bytes * nd / n_desc);
+    }
+}
+
+void launch_restrict(cudaStream_t s, const KbDev &kb, const DirDev &dir, const RestrictDesc *d_desc,
+                     uint32_t n_desc, hedl_counts *counts, uint32_t *heavy_scratch, double alg_light,
+                     double alg_heavy) {
+    const uint32_t gx = cdiv(kb.W4, 8);
+    if (!gx) return;
+    for (uint32_t off = 0; off < n_desc; off += 65535) {
+        const uint32_t nd = n_desc - off < 65535 ? n_desc - off : 65535;
+        prof_begin(s, KC_RESTRICT);
+        k_restrict<<<dim3(gx, nd), 256, 0, s>>>(kb, dir, d_desc + off, counts);
+        count_launch();
+        prof_end(s, KC_RESTRICT, alg_light * nd / n_desc);
+        if (dir.n_chunks) {
+            prof_begin(s, KC_HEAVY);
+            k_restrict_heavy<<<dim3(dir.n_chunks, nd), 256, 0, s>>>(kb, dir, d_desc + off, counts, heavy_scratch);
+            count_launch();
+            prof_end(s, KC_HEAVY, alg_heavy * nd / n_desc);
+        }
+    }
+}
+
+void launch_drange(cudaStream_t s, const KbDev &kb, const uint32_t *row_ptr, const float *val,
+                   const DrangeDesc *d_desc, uint32_t n_desc, hedl_counts *counts, double alg_bytes) {
+    const uint32_t gx = cdiv(kb.W4, 8);
+    if (!gx) return;
+    for (uint32_t off = 0; off < n_desc; off += 65535) {
+        const uint32_t nd = n_desc - off < 65535 ? n_desc - off : 65535;
+        prof_begin(s, KC_DRANGE);
+        k_drange<<<dim3(gx, nd), 256, 0, s>>>(kb, row_ptr, val, d_desc + off, counts);
+        count_launch();
+        prof_end(s, KC_DRANGE, alg_bytes * nd / n_desc);
+    }
+}
+
+void launch_gather_counts(cudaStream_t s, const hedl_counts *slots, const uint32_t *slot_of,
+                          hedl_counts *out, uint32_t n) {
+    if (!n) return;
+    prof_begin(s, KC_GATHER);
+    k_gather_counts<<<cdiv(n, 256), 256, 0, s>>>(slots, slot_of, out, n);
+    count_launch();
+    prof_end(s, KC_GATHER, 68.0 * n);
+}
+
+void launch_gather_bits(cudaStream_t s, const uint32_t *const *rows, uint32_t *out, uint32_t W, uint32_t n) {
+    if (!n || !W) return;
+    for (uint32_t off = 0; off < n; off += 65535) {
+        const uint32_t nd = n - off < 65535 ? n - off : 65535;
+        prof_begin(s, KC_GATHER);
+        k_gather_bits<<<dim3(cdiv(W, 256) < 32 ? cdiv(W, 256) : 32, nd), 256, 0, s>>>(rows + off, out + (uint64_t)off * W, W);
+        count_launch();
+        prof_end(s, KC_GATHER, 8.0 * W * nd);
+    }
+}
+
+}  // namespace hedl

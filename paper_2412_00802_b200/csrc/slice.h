@@ -1,0 +1,15 @@
+// Lane-packed ("bit-sliced") batch restriction path (SURVEY 8(d) "Optional
+// bit-sliced batch variant"): many restriction nodes on one role direction
+// share one CSR pass.  Declarations; implementation in slice.cu.
+#pragma once
+#include "internal.h"
+
+namespace hedl {
+bool slice_enabled(const hedl_kb *kb);
+bool slice_worthwhile(const hedl_kb *kb, uint32_t n_nodes);
+// h_desc: host copies of the group's restriction descriptors (pinned, valid
+// until the stream reaches this point); d_desc: the same on the device.
+hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream_t s, const KbDev &kd,
+                      uint32_t dir, const RestrictDesc *h_desc, const RestrictDesc *d_desc, uint32_t n,
+                      hedl_counts *counts);
+}  // namespace hedl
