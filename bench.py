@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""Benchmark of the HT-HEDL hot path on B200 (BASELINE.json metric: hypotheses evaluated/s).
+
+Workload (config C4 of SURVEY 8(d), BASELINE.json configs[3]): a 10^6-individual
+power-law ABox (50 concepts, 2 roles + inverses, 1 numeric property, 1%/1%
+examples) and a batch of 10^6 refinement-style hypotheses, KB replicated per
+GPU, batch sharded across ranks (weak scaling: per-GPU share fixed... the
+batch is the config's 10^6 at N=1 and 10^6 x N at N GPUs).
+
+One step = one pass of the whole hot path over the batch: every hypothesis
+evaluated to its instance set and TP/FP/FN/TN counts.
+  value : hyps/s with the KB and the compiled program resident on the device,
+          counts left on the device (+ the NCCL all_gather of counts at N>1).
+  e2e   : the same through the public API from host node arrays every step:
+          hedl_compile (plan + descriptor upload) + hedl_eval_batch with host counts.
+`python bench.py --impl reference` times the oracle (the plain C set evaluator)
+on the same workload, on bounded samples (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="hedl", choices=["hedl", "reference"])
+    ap.add_argument("--n-hyps", type=int, default=1_000_000, help="hypotheses per GPU")
+    ap.add_argument("--n-individuals", type=int, default=1_000_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--per-node", action="store_true", help="disable the lane-packed restriction path")
+    ap.add_argument("--cache", default=os.environ.get("HEDL_CACHE", "/tmp/hedl_cache"))
+    ap.add_argument("--seed", type=int, default=4)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------ inputs
+def _cached(cache, name, fn):
+    """Optional disk cache of generated inputs (a speed-up only; regenerated when absent)."""
+    path = os.path.join(cache, name + ".npz") if cache else None
+    if path and os.path.exists(path):
+        try:
+            z = np.load(path, allow_pickle=False)
+            return {k: z[k] for k in z.files}
+        except Exception:
+            pass
+    d = fn()
+    if path:
+        try:
+            os.makedirs(cache, exist_ok=True)
+            np.savez(path + ".tmp.npz", **d)
+            os.replace(path + ".tmp.npz", path)
+        except Exception:
+            pass
+    return d
+
+
+def c4_inputs(args, world):
+    from synth import abox, hyps
+    n_ind = args.n_individuals
+    kb = _cached(args.cache, f"c4kb_{n_ind}_{args.seed}",
+                 lambda: {k: np.asarray(v) for k, v in
+                          abox.powerlaw_kb(n_ind, 50, 2, 8.0, 10_000, 0.7, 1.0, 0.01, args.seed).items()})
+    kb["N"] = int(kb["N"])
+    total = args.n_hyps * world
+
+    def gen():
+        nodes, kids, roots = hyps.batch_arrays("c4", kb, total, args.seed)
+        return {"nodes": nodes, "kids": kids, "roots": roots}
+
+    h = _cached(args.cache, f"c4hyps_{n_ind}_{total}_{args.seed}", gen)
+    return kb, h["nodes"], h["kids"], h["roots"]
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(10)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and "Active" in r[4 + i]
+                          and "Not" not in r[4 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of each kernel class from the committed `ncu --set full` summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(path))
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------------------ oracle timing
+def oracle_rate(kb, nodes, kids, roots, budget_s, seed=0, threads=None):
+    """Time the oracle (as it stands) on a seeded sample of roots; -> (hyps/s, sample size, cores)."""
+    from oracle import setsem
+    threads = threads or os.cpu_count() or 1
+    okb = setsem.OracleKB(kb)
+    rng = np.random.default_rng(seed)
+    n = max(threads, 8)
+    t = 0.0
+    while True:
+        sample = np.sort(rng.choice(len(roots), size=min(n, len(roots)), replace=False))
+        t0 = time.perf_counter()
+        okb.evaluate(nodes, kids, roots[sample], want_bits=False, threads=threads)
+        t = time.perf_counter() - t0
+        if t >= budget_s * 0.3 or n >= len(roots):
+            break
+        n = int(min(len(roots), n * max(2.0, budget_s / max(t, 1e-3) * 0.8)))
+    return n / t, n, threads, t
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    kb, nodes, kids, roots = c4_inputs(args, world)
+    from oracle import setsem
+    threads = os.cpu_count() or 1
+    okb = setsem.OracleKB(kb)
+    rng = np.random.default_rng(123)
+    # size one step so the whole --steps K --warmup W run stays within a few minutes
+    probe = np.sort(rng.choice(len(roots), size=threads * 2, replace=False))
+    t0 = time.perf_counter()
+    okb.evaluate(nodes, kids, roots[probe], want_bits=False, threads=threads)
+    per = (time.perf_counter() - t0) / len(probe)
+    step_budget = max(2.0, 150.0 / max(1, args.steps + args.warmup))
+    S = int(max(threads, min(len(roots), step_budget / max(per, 1e-6))))
+    times = []
+    for i in range(args.warmup + args.steps):
+        sample = np.sort(rng.choice(len(roots), size=S, replace=False))
+        t0 = time.perf_counter()
+        okb.evaluate(nodes, kids, roots[sample], want_bits=False, threads=threads)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    ms = 1000.0 * float(np.mean(times))
+    val = S / (ms / 1000.0)
+    line = {
+        "impl": "reference", "metric": "hypotheses evaluated/sec", "value": val, "unit": "hyps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": "C4: 1M-individual power-law ABox x 1M refinement hypotheses",
+                   "n_individuals": int(kb["N"]), "global_batch": int(len(roots)),
+                   "parallelism": "oracle, hypothesis-parallel host threads"},
+        "cpu_baseline": {"value": val, "unit": "hyps/s", "cores": threads, "kind": "oracle",
+                         "sample": f"{S} seeded-uniform hypotheses of the C4 batch per step"},
+        "e2e": {"value": val, "unit": "hyps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------ main arm
+def c2_latency(hedl, device):
+    """1-hypothesis latency (host wall time, eval_one entry -> counts on host), C2 config."""
+    from synth import abox, hyps
+    from synth.format import flatten
+    kb = abox.c2_kb()
+    trees = hyps.c2_hypotheses(kb)
+    nodes, kids, roots = flatten(trees)
+    k = hedl.hedl_kb_load(kb, device)
+    prog = hedl.hedl_compile(k, nodes, kids, roots)
+    for i in range(100):
+        hedl.hedl_eval_one(k, prog, i % len(roots))
+    lat = []
+    for rep in range(4):
+        for i in range(len(roots)):
+            t0 = time.perf_counter()
+            hedl.hedl_eval_one(k, prog, i)
+            lat.append(time.perf_counter() - t0)
+    lat_c = []
+    for i in range(len(roots)):
+        t0 = time.perf_counter()
+        p1 = hedl.hedl_compile(k, nodes, kids, roots[i:i + 1])
+        hedl.hedl_eval_one(k, p1, 0)
+        lat_c.append(time.perf_counter() - t0)
+        p1.free()
+    us = np.array(lat) * 1e6
+    uc = np.array(lat_c) * 1e6
+    return {"config": "C2 carcinogenesis-shaped, N=22372, 256 depth-4 refinements",
+            "p50_us": float(np.percentile(us, 50)), "p99_us": float(np.percentile(us, 99)),
+            "p50_us_incl_compile": float(np.percentile(uc, 50)), "reps": len(us)}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2412_00802_b200 as hedl
+    from paper_2412_00802_b200 import dist as hdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+
+    kb_np, nodes, kids, roots = c4_inputs(args, world)
+    costs = hdist.root_costs(nodes, kids, roots)
+    ranges = hdist.shard_ranges(costs, world)
+    lo, hi = ranges[rank]
+    my_roots = np.ascontiguousarray(roots[lo:hi])
+    kb = hedl.hedl_kb_load(kb_np, local)
+    t0 = time.perf_counter()
+    prog = hedl.hedl_compile(kb, nodes, kids, my_roots)
+    compile_s = time.perf_counter() - t0
+    pinfo = prog.info()
+    eflags = hedl.HEDL_EVAL_PER_NODE if args.per_node else 0
+    n_loc = hi - lo
+    counts_dev = torch.empty((max(n_loc, 1), 4), dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step(c_out):
+        if n_loc:
+            hedl.hedl_eval_batch(kb, prog, 0, n_loc, counts_device=True, out_counts=c_out[:n_loc], flags=eflags)
+        if world > 1:
+            hdist.gather_counts(c_out[:n_loc], len(roots), ranges, device=dev)
+
+    for _ in range(args.warmup):
+        step(counts_dev)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    hedl.prof_reset()
+    hedl.prof_enable(True)
+    l0 = hedl.launch_count()
+    times = []
+    for _ in range(args.steps):
+        flush.zero_()                                   # L2 flushed between timed steps
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        step(counts_dev)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    launches = hedl.launch_count() - l0
+    hedl.prof_enable(False)
+    prof = hedl.prof_read()
+    clk = clocks.stop()
+    t_loc = float(np.sum(times))
+    t_max = t_loc
+    if world > 1:
+        tt = torch.tensor([t_loc], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    ms_per_step = t_max / args.steps
+    value = len(roots) / (ms_per_step / 1000.0)
+
+    # ---- e2e through the public API from host arrays every step ----
+    e2e = None
+    if not args.no_e2e:
+        nodes_pin = torch.from_numpy(nodes.view(np.uint8)).pin_memory().numpy().view(nodes.dtype)
+        kids_pin = torch.from_numpy(kids).pin_memory().numpy()
+        roots_pin = torch.from_numpy(my_roots).pin_memory().numpy()
+        h2d0, d2h0 = hedl.io_counters()
+        et = []
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            p2 = hedl.hedl_compile(kb, nodes_pin, kids_pin, roots_pin)
+            _, c_host = hedl.hedl_eval_batch(kb, p2, 0, n_loc, flags=eflags)
+            if world > 1:
+                hdist.gather_counts(torch.from_numpy(c_host.view(np.int64)).to(dev), len(roots), ranges, device=dev)
+                torch.cuda.synchronize()
+            et.append(time.perf_counter() - t0)
+            p2.free()
+        h2d1, d2h1 = hedl.io_counters()
+        e_loc = float(np.sum(et))
+        if world > 1:
+            tt = torch.tensor([e_loc], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e_loc = float(tt.item())
+        e2e = {"value": len(roots) / (e_loc / args.steps), "unit": "hyps/s",
+               "h2d_bytes_per_step": int((h2d1 - h2d0) / args.steps),
+               "d2h_bytes_per_step": int((d2h1 - d2h0) / args.steps),
+               "ms_per_step": 1000.0 * e_loc / args.steps,
+               "compile_ms": 1000.0 * compile_s}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel class ----
+    peaks = measured_peaks()
+    peak = peaks.get("hbm_gbs")
+    peak_src = "measured" if peak else "fallback"
+    peak = peak or 6650.0
+    top = max(prof, key=lambda e: e["total_ms"]) if prof else None
+    traffic = ncu_traffic()
+    roofline = None
+    if top:
+        ach = top["alg_bytes"] / (top["total_ms"] / 1000.0) / 1e9
+        tr = traffic.get(top["name"], {}).get("dram_bytes_per_launch") if traffic else None
+        roofline = {"bound": "hbm", "kernel": top["name"], "achieved": ach, "peak": peak, "unit": "GB/s",
+                    "frac": ach / peak, "traffic": tr, "peak_source": peak_src,
+                    "alg_bytes_per_launch": top["alg_bytes"] / top["launches"],
+                    "avg_launch_ms": top["total_ms"] / top["launches"],
+                    "share_of_step": top["total_ms"] / t_loc}
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        rate, S, cores, secs = oracle_rate(kb_np, nodes, kids, roots, budget_s=12.0)
+        cpu = {"value": rate, "unit": "hyps/s", "cores": cores, "kind": "oracle",
+               "sample": f"{S} seeded-uniform hypotheses of the C4 batch ({secs:.1f} s)"}
+    lat = None
+    if not args.no_latency and world == 1:
+        try:
+            lat = c2_latency(hedl, local)
+        except Exception as e:  # latency is an extra; never hide the main number
+            lat = {"error": str(e)}
+    line = {
+        "metric": "hypotheses evaluated/sec", "value": value, "unit": "hyps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": "C4: 1M-individual power-law ABox x 1M refinement hypotheses per GPU",
+                   "n_individuals": int(kb_np["N"]), "global_batch": int(len(roots)),
+                   "hyps_per_gpu": int(n_loc), "parallelism": f"dp{world} (KB replicated, batch sharded)",
+                   "l2": "flushed (256 MB write) between timed steps; KB 150 MB > L2",
+                   "path": "per-node" if args.per_node else "default",
+                   "canonical_nodes": pinfo["n_nodes"], "restrict_nodes": pinfo["n_restrict"],
+                   "levels": pinfo["n_levels"], "alg_bytes_per_hyp": pinfo["alg_bytes_total"] / max(1, n_loc)},
+        "roofline": roofline,
+        "roofline_hyps": {"unshared_alg_bytes_per_hyp": pinfo["alg_bytes_total"] / max(1, n_loc),
+                          "roofline_hyps_per_s": world * peak * 1e9 / max(1.0, pinfo["alg_bytes_total"] / max(1, n_loc)),
+                          "frac": value / (world * peak * 1e9 / max(1.0, pinfo["alg_bytes_total"] / max(1, n_loc)))},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "kernels": prof,
+        "latency": lat,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -213,6 +213,8 @@ hedl_status hedl_prof_reset(void);
 int hedl_prof_read(hedl_prof_entry *out, int max_entries);
 /* number of library kernel launches since process start (always counted) */
 uint64_t hedl_launch_count(void);
+/* bytes the library copied host->device / device->host since process start */
+hedl_status hedl_io_counters(uint64_t *h2d_bytes, uint64_t *d2h_bytes);
 
 #ifdef __cplusplus
 }

@@ -31,7 +31,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "OUT_OF_RANGE", 3: "EXAMPLE_CONFLICT", 4
 ABI_SYMBOLS = ["hedl_kb_load", "hedl_kb_free", "hedl_kb_get_info", "hedl_compile", "hedl_program_free",
                "hedl_program_get_info", "hedl_program_root_bytes", "hedl_eval_one", "hedl_eval_batch",
                "hedl_program_set_workspace_limit", "hedl_last_error", "hedl_version", "hedl_prof_enable",
-               "hedl_prof_reset", "hedl_prof_read", "hedl_launch_count"]
+               "hedl_prof_reset", "hedl_prof_read", "hedl_launch_count", "hedl_io_counters"]
 
 
 class HedlError(RuntimeError):
@@ -95,6 +95,7 @@ def lib():
         "hedl_prof_reset": ([], I32),
         "hedl_prof_read": ([C.POINTER(_ProfEntry), C.c_int], C.c_int),
         "hedl_launch_count": ([], U64),
+        "hedl_io_counters": ([C.POINTER(U64), C.POINTER(U64)], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -291,6 +292,12 @@ def prof_read() -> list:
 
 def launch_count() -> int:
     return int(lib().hedl_launch_count())
+
+
+def io_counters() -> tuple:
+    a, b = C.c_uint64(), C.c_uint64()
+    _check(lib().hedl_io_counters(C.byref(a), C.byref(b)))
+    return int(a.value), int(b.value)
 
 
 def version() -> str:

@@ -28,6 +28,11 @@ const char *kKClassName[KC_N] = {"bool", "restrict", "restrict_heavy", "drange",
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 uint64_t launches_total() { return g_launches.load(); }
+static std::atomic<uint64_t> g_h2d{0}, g_d2h{0};
+void count_io(uint64_t h2d, uint64_t d2h) {
+    g_h2d.fetch_add(h2d, std::memory_order_relaxed);
+    g_d2h.fetch_add(d2h, std::memory_order_relaxed);
+}
 
 struct ProfRec {
     cudaEvent_t a, b;
@@ -74,6 +79,12 @@ using namespace hedl;
 extern "C" const char *hedl_last_error(void) { return g_last_error.c_str(); }
 extern "C" const char *hedl_version(void) { return "hedl-b200 0.1 (sm_100a)"; }
 extern "C" uint64_t hedl_launch_count(void) { return launches_total(); }
+
+extern "C" hedl_status hedl_io_counters(uint64_t *h2d, uint64_t *d2h) {
+    if (h2d) *h2d = g_h2d.load();
+    if (d2h) *d2h = g_d2h.load();
+    return HEDL_OK;
+}
 
 extern "C" hedl_status hedl_prof_enable(int on) {
     std::lock_guard<std::mutex> lk(g_prof_mu);

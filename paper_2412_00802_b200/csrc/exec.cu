@@ -279,6 +279,7 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
             for (uint32_t k = 0; k < nroots; ++k) hrows[k] = rows + (size_t)local[p->root_node[ri + k]] * kb->W4;
         }
         HEDL_CUDA(kb, cudaMemcpyAsync(d, h, desc_bytes, cudaMemcpyHostToDevice, s));
+        count_io(desc_bytes, 0);
         if (!w->pinned_ev[w->pin_idx]) HEDL_CUDA(kb, cudaEventCreateWithFlags(&w->pinned_ev[w->pin_idx], cudaEventDisableTiming));
         HEDL_CUDA(kb, cudaEventRecord(w->pinned_ev[w->pin_idx], s));
         w->pin_idx ^= 1;
@@ -352,6 +353,7 @@ extern "C" hedl_status hedl_eval_batch(const hedl_kb *kb, hedl_program *p, uint3
     if (!(flags & HEDL_EVAL_COUNTS_DEVICE)) {
         if (st == HEDL_OK) {
             cudaError_t e = cudaMemcpyAsync(counts, dcounts, (size_t)n * sizeof(hedl_counts), cudaMemcpyDeviceToHost, s);
+            count_io(0, (uint64_t)n * sizeof(hedl_counts));
             if (e != cudaSuccess) st = cuda_fail(kb, e, "count D2H");
         }
         cudaFreeAsync(out_stage.p, s);

@@ -188,5 +188,6 @@ void launch_gather_bits(cudaStream_t s, const uint32_t *const *rows, uint32_t *o
 void launch_kb_build(cudaStream_t s);
 uint64_t launches_total();
 void count_launch();
+void count_io(uint64_t h2d, uint64_t d2h);
 
 }  // namespace hedl

@@ -1,0 +1,86 @@
+"""Multi-process (world_size 2 and 3, gloo on CPU) coverage of the sharded dispatcher's host logic.
+
+The per-rank evaluator is injected (the oracle stands in for the CUDA path,
+which needs a GPU); sharding, padding, all_gather and un-padding are the
+product code in paper_2412_00802_b200/dist.py.  Results must be independent
+of the number of ranks and in input order.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from paper_2412_00802_b200 import dist as hdist
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    from oracle import setsem
+    from synth import abox, hyps
+    from synth.format import flatten
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    kb = abox.random_tiny_kb(3, n=40, n_roles=2, n_data=1)
+    rng = np.random.default_rng(5)
+    trees = [hyps.random_tree(rng, abox.kb_shape(kb), depth=4) for _ in range(37)]
+    nodes, kids, roots = flatten(trees)
+    okb = setsem.OracleKB(kb)
+
+    def evaluator(n, k, r):
+        _, c = okb.evaluate(n, k, r, want_bits=False)
+        return torch.from_numpy(c.astype(np.int64))
+
+    counts, info = hdist.eval_batch_sharded(None, nodes, kids, roots, evaluator=evaluator)
+    if rank == 0:
+        _, ref = okb.evaluate(nodes, kids, roots, want_bits=False)
+        q.put((counts.numpy().tolist(), ref.astype(np.int64).tolist(), info["ranges"]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_counts_match_single_process(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got, ref, ranges = q.get()
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    assert got == ref
+    assert ranges[0][0] == 0 and ranges[-1][1] == 37
+    assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+
+
+def test_shard_ranges_balanced():
+    rng = np.random.default_rng(0)
+    costs = rng.integers(1, 100, 10_000)
+    for world in (1, 2, 4, 8):
+        rs = hdist.shard_ranges(costs, world)
+        assert rs[0][0] == 0 and rs[-1][1] == len(costs) and len(rs) == world
+        loads = [costs[a:b].sum() for a, b in rs]
+        assert max(loads) <= costs.sum() / world + costs.max()
+    assert hdist.shard_ranges(np.ones(3), 8)[-1] == (3, 3)
+
+
+def test_root_costs_counts_restrictions():
+    from synth.format import flatten
+    trees = [("ATOM", 0), ("EXISTS", 0, False, ("AND", [("ATOM", 1), ("FORALL", 1, True, ("TOP",))])),
+             ("DRANGE", 0, 0.0, 1.0)]
+    nodes, kids, roots = flatten(trees)
+    assert hdist.root_costs(nodes, kids, roots).tolist() == [1, 33, 17]
