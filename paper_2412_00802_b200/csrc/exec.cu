@@ -141,6 +141,10 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
             if (x.level != y.level) return x.level < y.level;
             if (x.kind != y.kind) return x.kind < y.kind;
             if (x.dir != y.dir) return x.dir < y.dir;
+            if (x.kind == NK_RESTRICT) {
+                const uint32_t cx = slice_class(x.pred, x.n, x.sat), cy = slice_class(y.pred, y.n, y.sat);
+                if (cx != cy) return cx < cy;
+            }
             return a < b;
         });
         const uint32_t nn = (uint32_t)list.size();
@@ -168,7 +172,25 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
                 ++e;
             }
             Group g{kind, key, k, e - k};
-            g.slice = use_slice && kind == NK_RESTRICT && slice_worthwhile(kb, g.count);
+            if (use_slice && kind == NK_RESTRICT) {
+                uint32_t ns = 0;   // leading lane-packable nodes (class 0/1 sort first)
+                while (ns < g.count) {
+                    const CNode &c = p->nodes[list[k + ns]];
+                    if (slice_class(c.pred, c.n, c.sat) == 2) break;
+                    ++ns;
+                }
+                if (ns && slice_worthwhile(kb, ns, eflags & HEDL_EVAL_FORCE_SLICE)) {
+                    if (ns < g.count) {            // split: packable prefix + per-node rest
+                        Group g1{kind, key, k, ns};
+                        g1.slice = true;
+                        groups.push_back(g1);
+                        g.first = k + ns;
+                        g.count -= ns;
+                    } else {
+                        g.slice = true;
+                    }
+                }
+            }
             groups.push_back(g);
             k = e;
         }
@@ -296,8 +318,8 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
                 DirDev dd{dr.row_ptr, dr.col, dr.heavy_x, dr.heavy_nchunks, dr.chunks, dr.n_heavy, dr.n_chunks};
                 const RestrictDesc *dd_desc = (const RestrictDesc *)(d + off_res) + lr.first_desc;
                 if (g.slice) {
-                    stt = slice_run(kb, &w->slice.p, &w->slice.bytes, s, kd, g.key,
-                                    hr + lr.first_desc, dd_desc, g.count, cov);
+                    stt = slice_run(kb, &w->slice.p, &w->slice.bytes, s, kd, g.key, hr + lr.first_desc, dd_desc,
+                                    g.count, cov);
                     if (stt) return stt;
                 } else {
                     launch_restrict(s, kd, dd, dd_desc, g.count, cov, (uint32_t *)w->heavy.p, lr.bytes, lr.bytes2);

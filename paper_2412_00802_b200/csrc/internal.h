@@ -68,6 +68,10 @@ struct hedl_dir {                  // one role direction
     std::vector<uint32_t> h_row_ptr;   // host copy (planning of lane-packed kernels)
     uint32_t max_deg = 0;
     uint64_t E_heavy = 0;              // edges of heavy rows
+    // lane-packed path: per 1024-individual tile {order begin, n_medium, n_light, heavy begin}
+    uint32_t n_tiles = 0;
+    uint4 *tiles = nullptr;            // device [n_tiles + 1]
+    uint32_t *order = nullptr;         // device [N - n_heavy]: per tile medium rows then light rows, degree-descending
 };
 
 struct hedl_data {

@@ -239,6 +239,41 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
                     dr.E_heavy += deg;
                 }
             }
+            // lane-packed path: per tile of 1024 rows, medium rows then light rows, degree-descending
+            dr.n_tiles = (N + 1023) / 1024;
+            std::vector<uint4> tiles(dr.n_tiles + 1);
+            std::vector<uint32_t> order;
+            order.reserve(N - hx.size());
+            {
+                uint32_t hpos = 0;
+                std::vector<uint32_t> med, light;
+                for (uint32_t t = 0; t < dr.n_tiles; ++t) {
+                    med.clear();
+                    light.clear();
+                    const uint32_t xa = t * 1024, xb = std::min(N, xa + 1024);
+                    while (hpos < hx.size() && hx[hpos] < xa) ++hpos;
+                    tiles[t].w = hpos;
+                    for (uint32_t x = xa; x < xb; ++x) {
+                        const uint32_t deg = h.row_ptr[x + 1] - h.row_ptr[x];
+                        if (deg > kHeavyDeg) continue;
+                        (deg > kLightDeg ? med : light).push_back(x);
+                    }
+                    auto by_deg = [&](uint32_t a, uint32_t b) {
+                        const uint32_t da = h.row_ptr[a + 1] - h.row_ptr[a], db = h.row_ptr[b + 1] - h.row_ptr[b];
+                        return da != db ? da > db : a < b;
+                    };
+                    std::sort(med.begin(), med.end(), by_deg);
+                    std::sort(light.begin(), light.end(), by_deg);
+                    tiles[t].x = (uint32_t)order.size();
+                    tiles[t].y = (uint32_t)med.size();
+                    tiles[t].z = (uint32_t)light.size();
+                    order.insert(order.end(), med.begin(), med.end());
+                    order.insert(order.end(), light.begin(), light.end());
+                }
+                tiles[dr.n_tiles] = make_uint4((uint32_t)order.size(), 0, 0, (uint32_t)hx.size());
+            }
+            if ((s = upload(kb, st, &dr.tiles, tiles.data(), tiles.size()))) return bail(s);
+            if ((s = upload(kb, st, &dr.order, order.data(), order.size()))) return bail(s);
             dr.n_heavy = (uint32_t)hx.size();
             dr.n_chunks = (uint32_t)chunks.size();
             if ((s = upload(kb, st, &dr.heavy_x, hx.data(), hx.size()))) return bail(s);

@@ -1,11 +1,476 @@
-// Lane-packed batch restriction kernels (placeholder until implemented).
+// Lane-packed ("bit-sliced") batch restriction kernels (SURVEY 8(d) "Optional
+// bit-sliced batch variant").
+//
+// Up to 256 restriction nodes on one role direction form a pack: lane j of the
+// pack is node j.  One CSR pass then evaluates all 256 nodes:
+//   k_slice_pack   T[y] = 256-bit word of child_j(y) ^ cmask_j   (32x32 warp bit transposes)
+//   k_slice_heavy  heavy rows (deg > kHeavyDeg) in CTA chunks, combined with atomics
+//   k_slice_tile   per 1024-individual tile: for every x, acc = OR / saturating count of
+//                  T[y] over y in N(x) (thread per light row, warp per medium row), the
+//                  per-lane predicate, then transpose back to the nodes' bitset rows with
+//                  fused Alg. 15 coverage.
+// OR packs hold nodes whose count saturates at 1 (exists, forall, >=1, <=0, ...);
+// COUNT packs keep 5-plane bit-sliced saturating counters (counts 0..31, n <= 30).
+// Semantics are exactly the per-node kernels' (kernels.cu): same predicates,
+// same saturation rule (pred(min(cnt, sat)) == pred(cnt)).
 #include "slice.h"
 
+#include <algorithm>
+
 namespace hedl {
-bool slice_enabled(const hedl_kb *) { return false; }
-bool slice_worthwhile(const hedl_kb *, uint32_t) { return false; }
-hedl_status slice_run(const hedl_kb *, void **, size_t *, cudaStream_t, const KbDev &, uint32_t,
-                      const RestrictDesc *, const RestrictDesc *, uint32_t, hedl_counts *) {
-    return fail(HEDL_ERR_UNSUPPORTED, "lane-packed path not built");
+
+namespace {
+constexpr uint32_t FULL = 0xffffffffu;
+constexpr int LW = 8;             // u32 words per individual in T: 256 lanes
+constexpr int NPL = 5;            // counter bit planes (0..31)
+constexpr int TROW = LW + 1;      // smem row stride (bank-conflict-free transposes)
+
+struct SliceDir {
+    const uint32_t *row_ptr, *col;
+    const uint4 *tiles;           // [n_tiles + 1] {order begin, n_med, n_light, heavy begin}
+    const uint32_t *order;
+    const uint32_t *heavy_x, *heavy_nchunks;
+    const uint4 *chunks;
+    uint32_t n_heavy, n_chunks, n_tiles;
+};
+
+struct SliceScratch {
+    uint4 *T;                     // [W4*32][2] : 32 B per individual
+    uint32_t *hacc;               // [n_heavy][8]     OR accumulators
+    uint32_t *hcnt;               // [n_heavy][256]   per-lane counts
+    uint32_t *ticket;             // [n_heavy]
+    uint32_t *hout;               // [n_heavy][8]     finished heavy rows
+};
+
+// per-pack lane constants, built in shared memory from the node descriptors
+struct PackConst {
+    uint32_t fl[LW], am[LW], om[LW];              // OR class: out = ((acc ^ fl) & am) | om
+    uint32_t nb[NPL][LW];                         // COUNT class: bit planes of n
+    uint32_t mge[LW], mle[LW], meq[LW], mlep[LW];
+};
+
+__device__ __forceinline__ uint32_t transpose_step(uint32_t x, uint32_t lane, int j, uint32_t m) {
+    const uint32_t y = __shfl_xor_sync(FULL, x, j);
+    return (lane & j) ? ((x & ~m) | ((y >> j) & m)) : ((x & m) | ((y & m) << j));
 }
+// 32x32 bit transpose across a warp: in lane r bit c = M[r][c]; out lane c bit r = M[r][c]
+__device__ __forceinline__ uint32_t warp_transpose(uint32_t x, uint32_t lane) {
+    x = transpose_step(x, lane, 16, 0x0000FFFFu);
+    x = transpose_step(x, lane, 8, 0x00FF00FFu);
+    x = transpose_step(x, lane, 4, 0x0F0F0F0Fu);
+    x = transpose_step(x, lane, 2, 0x33333333u);
+    x = transpose_step(x, lane, 1, 0x55555555u);
+    return x;
+}
+
+// every thread of the CTA calls; lanes >= count get "always 0" (am = om = 0, masks 0)
+__device__ void build_consts(PackConst &pc, const RestrictDesc *__restrict__ d, uint32_t count) {
+    uint32_t *w = reinterpret_cast<uint32_t *>(&pc);
+    for (uint32_t i = threadIdx.x; i < sizeof(PackConst) / 4; i += blockDim.x) w[i] = 0;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < count; j += blockDim.x) {
+        const RestrictDesc r = d[j];
+        const uint32_t k = j >> 5, bit = 1u << (j & 31);
+        // OR class (sat <= 1): result is a function of b = (cnt >= 1)
+        //   GE 0 -> 1 ; GE 1 -> b ; LE 0 / EQ 0 -> !b ; LEP 0 -> 0
+        bool am = false, fl = false, om = false;
+        if (r.pred == P_GE) { if (r.n == 0) om = true; else am = true; }
+        else if (r.pred == P_LE || r.pred == P_EQ) { am = true; fl = true; }
+        if (am) atomicOr(&pc.am[k], bit);
+        if (fl) atomicOr(&pc.fl[k], bit);
+        if (om) atomicOr(&pc.om[k], bit);
+        for (int q = 0; q < NPL; ++q)
+            if ((r.n >> q) & 1u) atomicOr(&pc.nb[q][k], bit);
+        if (r.pred == P_GE) atomicOr(&pc.mge[k], bit);
+        else if (r.pred == P_LE) atomicOr(&pc.mle[k], bit);
+        else if (r.pred == P_EQ) atomicOr(&pc.meq[k], bit);
+        else atomicOr(&pc.mlep[k], bit);
+    }
+    __syncthreads();
+}
+
+template <bool COUNT>
+struct Acc {
+    uint32_t c[COUNT ? NPL : 1][LW];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int q = 0; q < (COUNT ? NPL : 1); ++q)
+#pragma unroll
+            for (int k = 0; k < LW; ++k) c[q][k] = 0;
+    }
+    __device__ __forceinline__ void add(const uint32_t (&v)[LW]) {
+#pragma unroll
+        for (int k = 0; k < LW; ++k) {
+            if (!COUNT) {
+                c[0][k] |= v[k];
+            } else {
+                uint32_t s = FULL;
+#pragma unroll
+                for (int q = 0; q < NPL; ++q) s &= c[q][k];
+                uint32_t carry = v[k] & ~s;     // saturated lanes stay at 31
+#pragma unroll
+                for (int q = 0; q < NPL; ++q) {
+                    const uint32_t t = c[q][k] & carry;
+                    c[q][k] ^= carry;
+                    carry = t;
+                }
+            }
+        }
+    }
+    // saturating add of another accumulator (bit-sliced ripple-carry adder)
+    __device__ __forceinline__ void merge(const Acc &o) {
+#pragma unroll
+        for (int k = 0; k < LW; ++k) {
+            if (!COUNT) {
+                c[0][k] |= o.c[0][k];
+            } else {
+                uint32_t carry = 0;
+#pragma unroll
+                for (int q = 0; q < NPL; ++q) {
+                    const uint32_t a = c[q][k], b = o.c[q][k];
+                    c[q][k] = a ^ b ^ carry;
+                    carry = (a & b) | (carry & (a ^ b));
+                }
+#pragma unroll
+                for (int q = 0; q < NPL; ++q) c[q][k] |= carry;
+            }
+        }
+    }
+    __device__ __forceinline__ void warp_reduce() {
+        if (!COUNT) {
+#pragma unroll
+            for (int k = 0; k < LW; ++k) c[0][k] = __reduce_or_sync(FULL, c[0][k]);
+        } else {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                Acc o;
+#pragma unroll
+                for (int q = 0; q < NPL; ++q)
+#pragma unroll
+                    for (int k = 0; k < LW; ++k) o.c[q][k] = __shfl_xor_sync(FULL, c[q][k], off);
+                merge(o);
+            }
+        }
+    }
+    __device__ __forceinline__ uint32_t result(const PackConst &pc, int k) const {
+        if (!COUNT) return ((c[0][k] ^ pc.fl[k]) & pc.am[k]) | pc.om[k];
+        uint32_t gt = 0, eq = FULL, nz = 0;
+#pragma unroll
+        for (int q = NPL - 1; q >= 0; --q) {
+            const uint32_t cq = c[q][k], nq = pc.nb[q][k];
+            gt |= eq & cq & ~nq;
+            eq &= ~(cq ^ nq);
+            nz |= cq;
+        }
+        const uint32_t ge = gt | eq, le = ~gt;
+        return (ge & pc.mge[k]) | (le & pc.mle[k]) | (eq & pc.meq[k]) | (le & nz & pc.mlep[k]);
+    }
+};
+
+__device__ __forceinline__ void gather(const uint4 *__restrict__ T, uint32_t y, uint32_t (&v)[LW]) {
+    const uint4 a = __ldg(T + 2ull * y), b = __ldg(T + 2ull * y + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+// ------------------------------------------------------------------------------
+// T[y] for the pack: warp per 8 consecutive words (256 individuals).
+__global__ void __launch_bounds__(256) k_slice_pack(KbDev kb, const RestrictDesc *__restrict__ d, uint32_t count,
+                                                    uint4 *__restrict__ T) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t w0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 8;
+    if (w0 >= kb.W4) return;
+    uint32_t v[LW][8];
+#pragma unroll
+    for (int g = 0; g < LW; ++g) {
+        const uint32_t j = g * 32 + lane;
+        uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
+        if (j < count) {
+            const RestrictDesc r = d[j];
+            const uint4 *row = reinterpret_cast<const uint4 *>(r.child + w0);
+            a = __ldg(row);
+            if (w0 + 4 < kb.W4) b = __ldg(row + 1);
+            a.x ^= r.cmask; a.y ^= r.cmask; a.z ^= r.cmask; a.w ^= r.cmask;
+            b.x ^= r.cmask; b.y ^= r.cmask; b.z ^= r.cmask; b.w ^= r.cmask;
+        }
+        v[g][0] = a.x; v[g][1] = a.y; v[g][2] = a.z; v[g][3] = a.w;
+        v[g][4] = b.x; v[g][5] = b.y; v[g][6] = b.z; v[g][7] = b.w;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        if (w0 + k >= kb.W4) break;
+        uint32_t o[LW];
+#pragma unroll
+        for (int g = 0; g < LW; ++g) o[g] = warp_transpose(v[g][k], lane);
+        const uint64_t y = (uint64_t)(w0 + k) * 32 + lane;
+        T[2 * y] = make_uint4(o[0], o[1], o[2], o[3]);
+        T[2 * y + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+    }
+}
+
+// ------------------------------------------------------------------------------
+// heavy rows: CTA (128 threads) per chunk of <= kHeavyChunk edges.
+template <bool COUNT>
+__global__ void __launch_bounds__(128) k_slice_heavy(SliceDir dir, SliceScratch sc, const RestrictDesc *__restrict__ d,
+                                                     uint32_t count) {
+    __shared__ PackConst pc;
+    __shared__ uint32_t red[4][COUNT ? NPL : 1][LW];
+    __shared__ uint32_t fin[COUNT ? NPL : 1][LW];
+    __shared__ uint32_t s_last;
+    const uint4 ch = dir.chunks[blockIdx.x];
+    const uint32_t h = ch.x;
+    Acc<COUNT> acc;
+    acc.zero();
+    uint32_t v[LW];
+    for (uint32_t e = ch.y + threadIdx.x; e < ch.z; e += 128) {
+        gather(sc.T, __ldg(dir.col + e), v);
+        acc.add(v);
+    }
+    acc.warp_reduce();
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0)
+        for (int q = 0; q < (COUNT ? NPL : 1); ++q)
+            for (int k = 0; k < LW; ++k) red[wid][q][k] = acc.c[q][k];
+    __syncthreads();
+    if (!COUNT) {
+        if (threadIdx.x < LW) {
+            const uint32_t x = red[0][0][threadIdx.x] | red[1][0][threadIdx.x] | red[2][0][threadIdx.x] | red[3][0][threadIdx.x];
+            if (x) atomicOr(sc.hacc + (size_t)h * LW + threadIdx.x, x);
+        }
+    } else {
+        if (threadIdx.x == 0) {
+            Acc<true> a, b;
+            for (int q = 0; q < NPL; ++q) for (int k = 0; k < LW; ++k) a.c[q][k] = red[0][q][k];
+            for (int w = 1; w < 4; ++w) {
+                for (int q = 0; q < NPL; ++q) for (int k = 0; k < LW; ++k) b.c[q][k] = red[w][q][k];
+                a.merge(b);
+            }
+            for (int q = 0; q < NPL; ++q) for (int k = 0; k < LW; ++k) fin[q][k] = a.c[q][k];
+        }
+        __syncthreads();
+        for (uint32_t L = threadIdx.x; L < 256; L += 128) {
+            const uint32_t k = L >> 5, bit = L & 31;
+            uint32_t val = 0;
+            for (int q = 0; q < NPL; ++q) val |= ((fin[q][k] >> bit) & 1u) << q;
+            if (val) atomicAdd(sc.hcnt + (size_t)h * 256 + L, val);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t t = atomicAdd(sc.ticket + h, 1u);
+        s_last = (t == __ldg(dir.heavy_nchunks + h) - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    build_consts(pc, d, count);
+    if (!COUNT) {
+        if (threadIdx.x < LW) {
+            const uint32_t k = threadIdx.x;
+            const uint32_t a = atomicExch(sc.hacc + (size_t)h * LW + k, 0u);   // read + self-clean
+            sc.hout[(size_t)h * LW + k] = ((a ^ pc.fl[k]) & pc.am[k]) | pc.om[k];
+        }
+    } else {
+        __shared__ uint32_t outw[LW];
+        if (threadIdx.x < LW) outw[threadIdx.x] = 0;
+        __syncthreads();
+        for (uint32_t L = threadIdx.x; L < 256; L += 128) {
+            uint32_t c = atomicExch(sc.hcnt + (size_t)h * 256 + L, 0u);
+            c = c > 31u ? 31u : c;
+            const uint32_t k = L >> 5, bit = 1u << (L & 31);
+            uint32_t n = 0;
+            for (int q = 0; q < NPL; ++q) n |= ((pc.nb[q][k] & bit) ? 1u : 0u) << q;
+            bool r;
+            if (pc.mge[k] & bit) r = c >= n;
+            else if (pc.mle[k] & bit) r = c <= n;
+            else if (pc.meq[k] & bit) r = c == n;
+            else if (pc.mlep[k] & bit) r = c > 0 && c <= n;
+            else r = false;
+            if (r) atomicOr(&outw[k], bit);
+        }
+        __syncthreads();
+        if (threadIdx.x < LW) sc.hout[(size_t)h * LW + threadIdx.x] = outw[threadIdx.x];
+    }
+    if (threadIdx.x == 0) sc.ticket[h] = 0;
+}
+
+// ------------------------------------------------------------------------------
+// tile of 1024 consecutive individuals per CTA (256 threads).
+template <bool COUNT>
+__global__ void __launch_bounds__(256) k_slice_tile(KbDev kb, SliceDir dir, SliceScratch sc,
+                                                    const RestrictDesc *__restrict__ d, uint32_t count,
+                                                    hedl_counts *counts) {
+    extern __shared__ uint32_t smem[];
+    PackConst &pc = *reinterpret_cast<PackConst *>(smem);
+    uint32_t *ot = smem + sizeof(PackConst) / 4;          // [1024][TROW]
+    const uint32_t t = blockIdx.x;
+    const uint32_t x0 = t * 1024;
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (uint32_t i = threadIdx.x; i < 1024 * TROW; i += 256) ot[i] = 0;
+    build_consts(pc, d, count);                           // (contains __syncthreads)
+    const uint4 ti = dir.tiles[t];
+    const uint32_t hbeg = ti.w, hend = dir.tiles[t + 1].w;
+    for (uint32_t h = hbeg + threadIdx.x; h < hend; h += 256) {
+        const uint32_t xl = __ldg(dir.heavy_x + h) - x0;
+#pragma unroll
+        for (int k = 0; k < LW; ++k) ot[xl * TROW + k] = sc.hout[(size_t)h * LW + k];
+    }
+    uint32_t v[LW];
+    // medium rows: warp per row
+    for (uint32_t m = wid; m < ti.y; m += 8) {
+        const uint32_t x = __ldg(dir.order + ti.x + m);
+        const uint32_t a = __ldg(dir.row_ptr + x), b = __ldg(dir.row_ptr + x + 1);
+        Acc<COUNT> acc;
+        acc.zero();
+        for (uint32_t e = a + lane; e < b; e += 32) {
+            gather(sc.T, __ldg(dir.col + e), v);
+            acc.add(v);
+        }
+        acc.warp_reduce();
+        if (lane < LW) {
+            uint32_t r = 0;
+#pragma unroll
+            for (int k = 0; k < LW; ++k) if (k == (int)lane) r = acc.result(pc, k);
+            ot[(x - x0) * TROW + lane] = r;
+        }
+    }
+    // light rows: thread per row (rows sorted by degree, so a warp's trip counts agree)
+    for (uint32_t l = threadIdx.x; l < ti.z; l += 256) {
+        const uint32_t x = __ldg(dir.order + ti.x + ti.y + l);
+        const uint32_t a = __ldg(dir.row_ptr + x), b = __ldg(dir.row_ptr + x + 1);
+        Acc<COUNT> acc;
+        acc.zero();
+        uint32_t e = a;
+        for (; e + 1 < b; e += 2) {
+            uint32_t v2[LW];
+            const uint32_t y0 = __ldg(dir.col + e), y1 = __ldg(dir.col + e + 1);
+            gather(sc.T, y0, v);
+            gather(sc.T, y1, v2);
+            acc.add(v);
+            acc.add(v2);
+        }
+        if (e < b) {
+            gather(sc.T, __ldg(dir.col + e), v);
+            acc.add(v);
+        }
+#pragma unroll
+        for (int k = 0; k < LW; ++k) ot[(x - x0) * TROW + k] = acc.result(pc, k);
+    }
+    __syncthreads();
+    // transpose back: warp g writes lanes 32g..32g+31 (node rows), 4 words per store
+    const uint32_t g = wid;
+    const uint32_t j = g * 32 + lane;
+    const bool live = j < count;
+    RestrictDesc r{};
+    if (live) r = d[j];
+    uint32_t tp = 0, fp = 0;
+    for (uint32_t wl = 0; wl < 32; wl += 4) {
+        const uint32_t w = t * 32 + wl;
+        if (w >= kb.W4) break;
+        uint32_t o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) o[q] = warp_transpose(ot[((wl + q) * 32 + lane) * TROW + g], lane);
+        if (live) {
+            *reinterpret_cast<uint4 *>(r.out + w) = make_uint4(o[0], o[1], o[2], o[3]);
+            if (r.cover >= 0) {
+                const uint4 p = __ldg(reinterpret_cast<const uint4 *>(kb.pos + w));
+                const uint4 n = __ldg(reinterpret_cast<const uint4 *>(kb.neg + w));
+                tp += __popc(o[0] & p.x) + __popc(o[1] & p.y) + __popc(o[2] & p.z) + __popc(o[3] & p.w);
+                fp += __popc(o[0] & n.x) + __popc(o[1] & n.y) + __popc(o[2] & n.z) + __popc(o[3] & n.w);
+            }
+        }
+    }
+    if (live && r.cover >= 0 && (tp | fp)) {
+        hedl_counts *c = counts + r.cover;
+        if (tp) {
+            atomicAdd((unsigned long long *)&c->tp, (unsigned long long)tp);
+            atomicAdd((unsigned long long *)&c->fn, 0ull - tp);
+        }
+        if (fp) {
+            atomicAdd((unsigned long long *)&c->fp, (unsigned long long)fp);
+            atomicAdd((unsigned long long *)&c->tn, 0ull - fp);
+        }
+    }
+}
+
+inline uint32_t cdiv(uint64_t a, uint64_t b) { return (uint32_t)((a + b - 1) / b); }
+}  // namespace
+
+bool slice_enabled(const hedl_kb *kb) { return kb->N > 0; }
+
+bool slice_worthwhile(const hedl_kb *, uint32_t n_nodes, bool force) { return n_nodes >= (force ? 1u : kSliceMinNodes); }
+
+uint32_t slice_class(uint32_t pred, uint32_t n, uint32_t sat) {
+    if (sat <= 1) return 0;                  // OR pack
+    if (n <= 30 && sat <= 31) return 1;      // COUNT pack
+    (void)pred;
+    return 2;                                // per-node kernel
+}
+
+hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream_t s, const KbDev &kd, uint32_t dirid,
+                      const RestrictDesc *h_desc, const RestrictDesc *d_desc, uint32_t n, hedl_counts *counts) {
+    const hedl_dir &dr = kb->dirs[dirid];
+    const size_t t_bytes = (size_t)kb->W4 * 32 * 32;
+    // one fixed layout for every direction (sized by the largest heavy list), so the
+    // self-cleaning accumulators of one direction never alias another's results
+    size_t nh = 0;
+    for (const hedl_dir &x : kb->dirs) nh = std::max<size_t>(nh, x.n_heavy);
+    const size_t need = t_bytes + nh * (LW * 4 + 256 * 4 + 4 + LW * 4) + 256;
+    if (*ws_bytes < need) {
+        HEDL_CUDA(kb, cudaStreamSynchronize(s));
+        if (*ws) cudaFree(*ws);
+        *ws = nullptr;
+        *ws_bytes = 0;
+        if (cudaMalloc(ws, need) != cudaSuccess) { cudaGetLastError(); *ws = nullptr; return fail(HEDL_ERR_OOM, "slice workspace"); }
+        HEDL_CUDA(kb, cudaMemsetAsync(*ws, 0, need, s));
+        *ws_bytes = need;
+    }
+    char *base = (char *)*ws;
+    SliceScratch sc;
+    sc.T = (uint4 *)base;
+    sc.hacc = (uint32_t *)(base + t_bytes);
+    sc.hcnt = sc.hacc + nh * LW;
+    sc.ticket = sc.hcnt + nh * 256;
+    sc.hout = sc.ticket + nh;
+    SliceDir sd{dr.row_ptr, dr.col, dr.tiles, dr.order, dr.heavy_x, dr.heavy_nchunks, dr.chunks,
+                dr.n_heavy, dr.n_chunks, dr.n_tiles};
+    const size_t smem = sizeof(PackConst) + 1024 * TROW * 4;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_slice_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_slice_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
+    const double csr = 4.0 * (kb->N + 1) + 4.0 * dr.E;
+    for (uint32_t off = 0; off < n;) {
+        const uint32_t cls = slice_class(h_desc[off].pred, h_desc[off].n, h_desc[off].sat);
+        uint32_t cnt = 1;
+        while (off + cnt < n && cnt < 256 &&
+               slice_class(h_desc[off + cnt].pred, h_desc[off + cnt].n, h_desc[off + cnt].sat) == cls)
+            ++cnt;
+        const RestrictDesc *dd = d_desc + off;
+        prof_begin(s, KC_SLICE_IN);
+        k_slice_pack<<<cdiv(kb->W4, 64), 256, 0, s>>>(kd, dd, cnt, sc.T);
+        count_launch();
+        prof_end(s, KC_SLICE_IN, 4.0 * kb->W * cnt + 32.0 * 32 * kb->W4);
+        if (dr.n_chunks) {
+            prof_begin(s, KC_SLICE_HEAVY);
+            if (cls == 0) k_slice_heavy<false><<<dr.n_chunks, 128, 0, s>>>(sd, sc, dd, cnt);
+            else k_slice_heavy<true><<<dr.n_chunks, 128, 0, s>>>(sd, sc, dd, cnt);
+            count_launch();
+            prof_end(s, KC_SLICE_HEAVY, 4.0 * dr.E_heavy + 32.0 * dr.E_heavy);
+        }
+        prof_begin(s, KC_SLICE);
+        if (cls == 0) k_slice_tile<false><<<dr.n_tiles, 256, smem, s>>>(kd, sd, sc, dd, cnt, counts);
+        else k_slice_tile<true><<<dr.n_tiles, 256, smem, s>>>(kd, sd, sc, dd, cnt, counts);
+        count_launch();
+        // minimal DRAM bytes of one lane-packed pass: CSR once + T once (32 B per individual)
+        // + the cnt output rows; the 32 B-per-edge T gathers are L2 traffic (DESIGN.md K-SLICE)
+        prof_end(s, KC_SLICE, csr + 32.0 * 32 * kb->W4 + 4.0 * kb->W * cnt);
+        off += cnt;
+    }
+    return HEDL_OK;
+}
+
 }  // namespace hedl

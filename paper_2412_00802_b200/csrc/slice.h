@@ -5,8 +5,11 @@
 #include "internal.h"
 
 namespace hedl {
+constexpr uint32_t kSliceMinNodes = 8;   // smaller groups use the per-node kernels
 bool slice_enabled(const hedl_kb *kb);
-bool slice_worthwhile(const hedl_kb *kb, uint32_t n_nodes);
+bool slice_worthwhile(const hedl_kb *kb, uint32_t n_nodes, bool force);
+// 0 = OR pack (count saturates at 1), 1 = COUNT pack (n <= 30), 2 = per-node kernel
+uint32_t slice_class(uint32_t pred, uint32_t n, uint32_t sat);
 // h_desc: host copies of the group's restriction descriptors (pinned, valid
 // until the stream reaches this point); d_desc: the same on the device.
 hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream_t s, const KbDev &kd,

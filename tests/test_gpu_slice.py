@@ -1,0 +1,97 @@
+"""GPU parity of the lane-packed batch restriction path (K-SLICE) vs the oracle.
+
+HEDL_EVAL_FORCE_SLICE packs every eligible restriction group, however small,
+so the tiny and random cases exercise the OR packs, COUNT packs (bit-sliced
+saturating counters), heavy-row chunks and the per-node fallback (n > 30).
+"""
+import numpy as np
+import pytest
+
+from synth import abox, hyps
+from synth.format import COMPILE_COMPAT_PAPER_MAX, COMPILE_NO_CSE, flatten
+from test_gpu_parity import assert_parity, gpu_eval
+
+pytestmark = pytest.mark.gpu
+FORCE = 4       # HEDL_EVAL_FORCE_SLICE
+PER_NODE = 2    # HEDL_EVAL_PER_NODE
+
+
+def test_slice_random_tiny():
+    for seed in range(60):
+        kb = abox.random_tiny_kb(seed)
+        rng = np.random.default_rng(20_000 + seed)
+        trees = [hyps.random_tree(rng, abox.kb_shape(kb), depth=4, n_max=6) for _ in range(40)]
+        assert_parity(kb, trees, eflags=FORCE, tag=f"slice seed {seed}")
+        if seed % 10 == 0:
+            assert_parity(kb, trees, flags=COMPILE_COMPAT_PAPER_MAX, eflags=FORCE, tag=f"slice compat {seed}")
+
+
+def test_slice_counts_boundaries():
+    """n around the COUNT-pack limits: 0..33 (n <= 30 packed, larger n per-node), all predicates."""
+    kb = abox.regime_kb("single", 40, seed=3, n_concepts=3, density=0.9)
+    kb2 = abox.powerlaw_kb(5000, 3, 2, 12.0, 600, 0.5, 1.0, 0.05, 5)
+    for k in (kb, kb2):
+        trees = []
+        for n in range(0, 34):
+            for op in ("MIN", "MAX", "EXACT"):
+                for inv in (False, True):
+                    trees.append((op, n, 0, inv, ("ATOM", n % 3)))
+                    trees.append((op, n, 0, inv, ("NOT", ("ATOM", (n + 1) % 3))))
+        trees += [("EXISTS", 0, False, ("ATOM", 1)), ("FORALL", 0, True, ("ATOM", 2))]
+        assert_parity(k, trees, eflags=FORCE, tag="boundaries")
+        assert_parity(k, trees, flags=COMPILE_COMPAT_PAPER_MAX, eflags=FORCE, tag="boundaries compat")
+
+
+@pytest.mark.parametrize("E", [513, 4097, 100_000])
+def test_slice_heavy_single_subject(E):
+    kb = abox.regime_kb("single", E, seed=E, n_concepts=4)
+    T = ("TOP",)
+    trees = []
+    for c in range(4):
+        trees += [("EXISTS", 0, False, ("ATOM", c)), ("FORALL", 0, False, ("ATOM", c)),
+                  ("MIN", 17, 0, False, ("ATOM", c)), ("MAX", 30, 0, False, ("ATOM", c)),
+                  ("EXACT", 0, 0, False, ("NOT", ("ATOM", c))), ("MIN", 2, 0, True, ("ATOM", c)),
+                  ("MIN", E // 2, 0, False, ("ATOM", c))]
+    trees += [("MIN", E, 0, False, T), ("MAX", E - 1, 0, False, T)]
+    assert_parity(kb, trees, eflags=FORCE, tag=f"slice heavy {E}")
+
+
+def test_slice_powerlaw_many_packs():
+    """More than 256 restriction nodes per (level, direction): several packs per group."""
+    kb = abox.powerlaw_kb(50_000, 40, 2, 8.0, 3_000, 0.7, 1.0, 0.01, 21)
+    rng = np.random.default_rng(21)
+    trees = []
+    for _ in range(1500):
+        r, inv = int(rng.integers(2)), bool(rng.integers(2))
+        c = ("ATOM", int(rng.integers(40)))
+        if rng.random() < 0.3:
+            c = ("NOT", c)
+        k = rng.integers(5)
+        if k == 0:
+            trees.append(("EXISTS", r, inv, c))
+        elif k == 1:
+            trees.append(("FORALL", r, inv, c))
+        else:
+            trees.append((["MIN", "MAX", "EXACT"][k - 2], int(rng.integers(0, 17)), r, inv, c))
+    trees += [hyps.random_tree(rng, abox.kb_shape(kb), depth=4) for _ in range(300)]
+    gb, gc = assert_parity(kb, trees, tag="slice powerlaw")          # default path (packs >= 8)
+    nodes, kids, roots = flatten(trees)
+    b2, c2, _ = gpu_eval(kb, nodes, kids, roots, eflags=PER_NODE)
+    assert np.array_equal(b2, gb) and np.array_equal(c2, gc)
+    b3, c3, _ = gpu_eval(kb, nodes, kids, roots, COMPILE_NO_CSE, eflags=FORCE)
+    assert np.array_equal(b3, gb) and np.array_equal(c3, gc)
+
+
+def test_slice_c4_shape():
+    kb = abox.powerlaw_kb(300_000, 50, 2, 8.0, 10_000, 0.7, 1.0, 0.01, 4)
+    arrays = hyps.batch_arrays("c4", kb, 20_000, 4, chunk=5000, workers=4)
+    assert_parity(kb, arrays=arrays, tag="slice c4-shape")
+
+
+def test_slice_tail_sizes():
+    for n in (1, 31, 32, 33, 1023, 1024, 1025, 2049, 4000):
+        kb = abox.random_tiny_kb(n, n=n, n_concepts=3, n_roles=2, n_data=0) if n <= 40 else \
+            abox.powerlaw_kb(n, 3, 2, 4.0, min(n, 700), 0.0, 1.0, 0.05, n)
+        rng = np.random.default_rng(n)
+        trees = [hyps.random_tree(rng, abox.kb_shape(kb), depth=3, n_max=5) for _ in range(64)]
+        assert_parity(kb, trees, eflags=FORCE, tag=f"slice N={n}")
