@@ -191,7 +191,9 @@ hedl_status hedl_eval_batch(const hedl_kb *kb, hedl_program *prog, uint32_t firs
                             uint32_t n_roots, uint32_t *out_bits, hedl_counts *counts,
                             void *stream, uint32_t flags);
 
-/* Device-memory cap for one program's evaluation workspace (default 8 GiB). */
+/* Device-memory cap for one program's evaluation workspace (default: half the
+ * device memory free at first use, at most 48 GiB).  Larger caps give larger
+ * chunks, i.e. fuller lane packs. */
 hedl_status hedl_program_set_workspace_limit(hedl_program *prog, uint64_t bytes);
 
 /* ---------------------------------------------------------------------------

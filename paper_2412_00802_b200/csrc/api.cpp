@@ -1,12 +1,25 @@
 // Diagnostics of the C ABI: thread-local last error, version, launch counter,
 // CUDA-event kernel timing (used by bench.py for the roofline "achieved").
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 
 namespace hedl {
 
 static thread_local std::string g_last_error;
+
+bool timing_enabled() {
+    static const bool on = [] { const char *e = std::getenv("HEDL_TIMING"); return e && *e && *e != '0'; }();
+    return on;
+}
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+void timing_note(const char *what, double ms) {
+    if (timing_enabled()) std::fprintf(stderr, "[hedl timing] %-28s %9.3f ms\n", what, ms);
+}
 
 void set_error(const std::string &msg) { g_last_error = msg; }
 

@@ -6,12 +6,22 @@
 // (common-subexpression reuse), with topological levels for level-synchronous
 // batched launches and the per-node algorithmic byte model of SURVEY 8(d).
 //
+// Plans are generated in parallel on host threads, as in the paper (PAPER.md:578
+// "Using CPU multithreading, HT-HEDL first generates evaluation plans ... in
+// parallel"): the roots are cut into contiguous shards canonicalised
+// independently, then merged level by level into one DAG through a lock-free
+// hash-consing table, so CSE stays global across the whole batch.
+//
 // Canonicalisation (default): complement folded into operand
 // references (the paper's per-operand isNegated XOR flag, Alg. 1-2),
 // so NOT NOT C == C; n-ary AND/OR flattened, operands sorted and deduplicated
 // (an n-ary operation is one step).  No algebraic rewrites.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <cstdlib>
+#include <memory>
+#include <thread>
 
 #include "internal.h"
 
@@ -19,80 +29,346 @@ using namespace hedl;
 
 namespace {
 
+constexpr uint8_t NK_DEAD = 0xff;     // a node id reserved by a thread that lost an insert race
+
 inline uint64_t mix(uint64_t h, uint64_t v) {
     h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
     return h * 0xff51afd7ed558ccdull;
 }
 
-struct Builder {
-    hedl_program *p;
-    const hedl_kb *kb;
-    bool cse;
+uint64_t hash_node(const CNode &n, const uint32_t *ops) {
+    uint64_t h = mix(n.kind, n.pred);
+    h = mix(h, n.dir);
+    h = mix(h, n.n);
+    uint32_t lo, hi;
+    std::memcpy(&lo, &n.lo, 4);
+    std::memcpy(&hi, &n.hi, 4);
+    h = mix(h, ((uint64_t)lo << 32) | hi);
+    for (uint32_t i = 0; i < n.op_count; ++i) h = mix(h, ops[i]);
+    return h;
+}
+
+bool same_node(const CNode &a, const uint32_t *aops, const CNode &b, const uint32_t *bops) {
+    if (a.kind != b.kind || a.pred != b.pred || a.dir != b.dir || a.n != b.n || a.op_count != b.op_count) return false;
+    if (std::memcmp(&a.lo, &b.lo, 4) || std::memcmp(&a.hi, &b.hi, 4)) return false;
+    return std::equal(aops, aops + a.op_count, bops);
+}
+
+double node_bytes(const hedl_kb *kb, const CNode &n) {
+    const double W4b = 4.0 * kb->W;
+    if (n.kind == NK_AND || n.kind == NK_OR) return (n.op_count + 1) * W4b;
+    if (n.kind == NK_RESTRICT) return kb->dir_bytes[n.dir] + 2 * W4b;
+    return kb->data_bytes[n.dir] + W4b;
+}
+
+// ---- single-threaded DAG of one shard ---------------------------------------------
+struct LocalDag {
+    std::vector<CNode> nodes;
+    std::vector<uint32_t> ops;
     std::vector<uint32_t> table;   // open addressing: node id + 1, 0 = empty
     uint64_t mask = 0;
-    uint32_t count = 0;
+    bool cse = true;
 
-    uint64_t hash_node(const CNode &n, const uint32_t *ops) const {
-        uint64_t h = mix(n.kind, n.pred);
-        h = mix(h, n.dir);
-        h = mix(h, n.n);
-        uint32_t lo, hi;
-        std::memcpy(&lo, &n.lo, 4);
-        std::memcpy(&hi, &n.hi, 4);
-        h = mix(h, ((uint64_t)lo << 32) | hi);
-        for (uint32_t i = 0; i < n.op_count; ++i) h = mix(h, ops[i]);
-        return h;
-    }
-    bool same(const CNode &a, const CNode &b, const uint32_t *bops) const {
-        if (a.kind != b.kind || a.pred != b.pred || a.dir != b.dir || a.n != b.n || a.op_count != b.op_count) return false;
-        if (std::memcmp(&a.lo, &b.lo, 4) || std::memcmp(&a.hi, &b.hi, 4)) return false;
-        return std::equal(bops, bops + b.op_count, p->ops.begin() + a.op_begin);
-    }
     void grow() {
-        uint64_t cap = table.empty() ? 1024 : table.size() * 2;
+        const uint64_t cap = table.empty() ? 1024 : table.size() * 2;
         std::vector<uint32_t> t(cap, 0);
-        uint64_t m = cap - 1;
-        for (uint32_t id = 0; id < p->nodes.size(); ++id) {
-            const CNode &n = p->nodes[id];
-            uint64_t h = hash_node(n, p->ops.data() + n.op_begin) & m;
+        const uint64_t m = cap - 1;
+        for (uint32_t id = 0; id < nodes.size(); ++id) {
+            uint64_t h = hash_node(nodes[id], ops.data() + nodes[id].op_begin) & m;
             while (t[h]) h = (h + 1) & m;
             t[h] = id + 1;
         }
         table.swap(t);
         mask = m;
     }
-    // intern node `n` with operands `ops`; returns node id
-    uint32_t intern(CNode n, const uint32_t *ops) {
+    uint32_t intern(CNode n, const uint32_t *o) {
         uint64_t h = 0;
         if (cse) {
-            if ((uint64_t)(p->nodes.size() + 1) * 2 > table.size()) grow();
-            h = hash_node(n, ops) & mask;
+            if ((uint64_t)(nodes.size() + 1) * 2 > table.size()) grow();
+            h = hash_node(n, o) & mask;
             while (table[h]) {
                 const uint32_t id = table[h] - 1;
-                if (same(p->nodes[id], n, ops)) return id;
+                if (same_node(nodes[id], ops.data() + nodes[id].op_begin, n, o)) return id;
                 h = (h + 1) & mask;
             }
         }
-        n.op_begin = (uint32_t)p->ops.size();
-        p->ops.insert(p->ops.end(), ops, ops + n.op_count);
+        n.op_begin = (uint32_t)ops.size();
+        ops.insert(ops.end(), o, o + n.op_count);
         uint32_t lvl = 0;
         bool has_node = false;
         for (uint32_t i = 0; i < n.op_count; ++i)
-            if (ref_type(ops[i]) == RT_NODE) {
+            if (ref_type(o[i]) == RT_NODE) {
                 has_node = true;
-                lvl = std::max(lvl, p->nodes[ref_id(ops[i])].level);
+                lvl = std::max(lvl, nodes[ref_id(o[i])].level);
             }
         n.level = has_node ? lvl + 1 : 0;
-        const double W4b = 4.0 * kb->W;
-        if (n.kind == NK_AND || n.kind == NK_OR) n.bytes = (n.op_count + 1) * W4b;
-        else if (n.kind == NK_RESTRICT) n.bytes = kb->dir_bytes[n.dir] + 2 * W4b;
-        else n.bytes = kb->data_bytes[n.dir] + W4b;
-        const uint32_t id = (uint32_t)p->nodes.size();
-        p->nodes.push_back(n);
+        const uint32_t id = (uint32_t)nodes.size();
+        nodes.push_back(n);
         if (cse) table[h] = id + 1;
         return id;
     }
 };
+
+// memo over hypothesis-node ids: id -> (canonical ref, DFS state)
+struct Memo {
+    std::vector<uint32_t> keys, vals;
+    std::vector<uint8_t> st;
+    uint64_t mask = 0, used = 0;
+    explicit Memo(uint64_t expect) {
+        uint64_t cap = 1024;
+        while (cap < expect * 2) cap <<= 1;
+        keys.assign(cap, 0xffffffffu);
+        vals.assign(cap, 0);
+        st.assign(cap, 0);
+        mask = cap - 1;
+    }
+    static uint64_t h(uint32_t k) { return (uint64_t)k * 0x9E3779B97F4A7C15ull >> 20; }
+    uint64_t slot(uint32_t k) {
+        uint64_t i = h(k) & mask;
+        while (keys[i] != 0xffffffffu && keys[i] != k) i = (i + 1) & mask;
+        return i;
+    }
+    uint8_t state(uint32_t k) {
+        const uint64_t i = slot(k);
+        return keys[i] == k ? st[i] : 0;
+    }
+    void set(uint32_t k, uint8_t s, uint32_t v) {
+        if ((used + 1) * 2 > keys.size()) rehash();
+        const uint64_t i = slot(k);
+        if (keys[i] != k) { keys[i] = k; ++used; }
+        st[i] = s;
+        vals[i] = v;
+    }
+    uint32_t val(uint32_t k) { return vals[slot(k)]; }
+    void rehash() {
+        std::vector<uint32_t> ok, ov;
+        std::vector<uint8_t> os;
+        ok.swap(keys); ov.swap(vals); os.swap(st);
+        keys.assign(ok.size() * 2, 0xffffffffu);
+        vals.assign(ok.size() * 2, 0);
+        st.assign(ok.size() * 2, 0);
+        mask = keys.size() - 1;
+        for (size_t i = 0; i < ok.size(); ++i)
+            if (ok[i] != 0xffffffffu) {
+                uint64_t j = h(ok[i]) & mask;
+                while (keys[j] != 0xffffffffu) j = (j + 1) & mask;
+                keys[j] = ok[i]; vals[j] = ov[i]; st[j] = os[i];
+            }
+    }
+};
+
+struct Shard {
+    LocalDag dag;
+    std::vector<uint32_t> root_ref;   // canonical (local) reference of each root of the shard
+    hedl_status err = HEDL_OK;
+    std::string msg;
+};
+
+struct Input {
+    const hedl_kb *kb;
+    const hedl_node *nodes;
+    uint32_t n_nodes;
+    const uint32_t *child_idx;
+    uint64_t n_child_idx;
+    const uint32_t *roots;
+    uint32_t n_roots;
+    uint32_t flags;
+};
+
+// canonicalise roots [r0, r1) into sh.dag (iterative post-order DFS, cycle check)
+void canon_shard(const Input &in, uint32_t r0, uint32_t r1, Shard &sh) {
+    const hedl_kb *kb = in.kb;
+    const bool rewrite = !(in.flags & HEDL_COMPILE_NO_REWRITE);
+    const bool compat = in.flags & HEDL_COMPILE_COMPAT_PAPER_MAX;
+    LocalDag &D = sh.dag;
+    D.cse = !(in.flags & HEDL_COMPILE_NO_CSE);
+    const uint64_t expect = (uint64_t)in.n_nodes * (r1 - r0) / std::max<uint32_t>(1, in.n_roots) + 64;
+    D.nodes.reserve(expect / 3 + 16);
+    D.ops.reserve(expect / 2 + 16);
+    Memo memo(expect);
+    std::vector<std::pair<uint32_t, uint32_t>> stack;
+    std::vector<uint32_t> tmp;
+    sh.root_ref.resize(r1 - r0);
+    auto bad = [&](hedl_status st, uint32_t i, const std::string &m) {
+        sh.err = st;
+        sh.msg = "node " + std::to_string(i) + ": " + m;
+    };
+    for (uint32_t ri = r0; ri < r1; ++ri) {
+        const uint32_t root = in.roots[ri];
+        if (root >= in.n_nodes) { sh.err = HEDL_ERR_OUT_OF_RANGE; sh.msg = "root " + std::to_string(ri) + " out of range"; return; }
+        if (memo.state(root) != 2) {
+            stack.clear();
+            stack.push_back({root, 0});
+            memo.set(root, 1, 0);
+            while (!stack.empty()) {
+                const uint32_t i = stack.back().first;
+                const hedl_node &nd = in.nodes[i];
+                if ((uint64_t)nd.child_begin + nd.child_count > in.n_child_idx)
+                    return bad(HEDL_ERR_OUT_OF_RANGE, i, "child range out of bounds");
+                uint32_t &k = stack.back().second;
+                if (k < nd.child_count) {
+                    const uint32_t c = in.child_idx[nd.child_begin + k++];
+                    if (c >= in.n_nodes) return bad(HEDL_ERR_OUT_OF_RANGE, i, "child id out of range");
+                    const uint8_t cs = memo.state(c);
+                    if (cs == 1) return bad(HEDL_ERR_BAD_EXPR, i, "cycle");
+                    if (cs == 0) { memo.set(c, 1, 0); stack.push_back({c, 0}); }
+                    continue;
+                }
+                // all children are done: build the canonical reference of node i
+                const uint32_t *ch = in.child_idx + nd.child_begin;
+                const uint32_t cc = nd.child_count;
+                const bool is_role = nd.op >= HEDL_OP_EXISTS && nd.op <= HEDL_OP_EXACT;
+                if (nd.flags & ~HEDL_FLAG_INV) return bad(HEDL_ERR_BAD_EXPR, i, "unknown flag bits");
+                if ((nd.flags & HEDL_FLAG_INV) && !is_role) return bad(HEDL_ERR_BAD_EXPR, i, "inverse flag on a non-role node");
+                uint32_t r = 0;
+                switch (nd.op) {
+                case HEDL_OP_TOP:
+                case HEDL_OP_BOTTOM:
+                    if (cc) return bad(HEDL_ERR_BAD_EXPR, i, "TOP/BOTTOM take no children");
+                    r = mkref(RT_TOP, 0, nd.op == HEDL_OP_BOTTOM);
+                    break;
+                case HEDL_OP_ATOM:
+                    if (cc) return bad(HEDL_ERR_BAD_EXPR, i, "ATOM takes no children");
+                    if (nd.arg >= kb->C) return bad(HEDL_ERR_OUT_OF_RANGE, i, "concept id out of range");
+                    r = mkref(RT_ATOM, nd.arg, 0);
+                    break;
+                case HEDL_OP_NOT:
+                    if (cc != 1) return bad(HEDL_ERR_BAD_EXPR, i, "NOT takes one child");
+                    r = memo.val(ch[0]) ^ 1u;   // complement over Delta (Q1); NOT NOT C == C
+                    break;
+                case HEDL_OP_AND:
+                case HEDL_OP_OR: {
+                    const uint8_t kind = nd.op == HEDL_OP_AND ? NK_AND : NK_OR;
+                    tmp.clear();
+                    for (uint32_t j = 0; j < cc; ++j) {
+                        const uint32_t cr = memo.val(ch[j]);
+                        if (rewrite && ref_type(cr) == RT_NODE && !ref_comp(cr) && D.nodes[ref_id(cr)].kind == kind) {
+                            const CNode &sub = D.nodes[ref_id(cr)];
+                            for (uint32_t q = 0; q < sub.op_count; ++q) tmp.push_back(D.ops[sub.op_begin + q]);
+                        } else {
+                            tmp.push_back(cr);
+                        }
+                    }
+                    if (rewrite) {
+                        std::sort(tmp.begin(), tmp.end());
+                        tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+                    }
+                    if (tmp.empty()) {                         // empty AND = TOP, empty OR = BOTTOM
+                        r = mkref(RT_TOP, 0, kind == NK_OR);
+                    } else if (tmp.size() == 1 && rewrite) {
+                        r = tmp[0];
+                    } else {
+                        CNode n{};
+                        n.kind = kind;
+                        n.op_count = (uint32_t)tmp.size();
+                        r = mkref(RT_NODE, D.intern(n, tmp.data()), 0);
+                    }
+                    break;
+                }
+                case HEDL_OP_EXISTS: case HEDL_OP_FORALL: case HEDL_OP_MIN: case HEDL_OP_MAX: case HEDL_OP_EXACT: {
+                    if (cc != 1) return bad(HEDL_ERR_BAD_EXPR, i, "role restriction takes one child");
+                    if (nd.arg >= kb->R) return bad(HEDL_ERR_OUT_OF_RANGE, i, "role id out of range");
+                    if (nd.n > 0xfffffffeu) return bad(HEDL_ERR_BAD_EXPR, i, "n > 2^32-2");
+                    CNode n{};
+                    n.kind = NK_RESTRICT;
+                    n.dir = (uint16_t)(2 * nd.arg + (nd.flags & HEDL_FLAG_INV ? 1 : 0));
+                    n.op_count = 1;
+                    uint32_t child = memo.val(ch[0]);
+                    switch (nd.op) {
+                    case HEDL_OP_EXISTS: n.pred = P_GE; n.n = 1; n.sat = 1; break;           // Alg. 4
+                    case HEDL_OP_FORALL: n.pred = P_LE; n.n = 0; n.sat = 1; child ^= 1u; break; // Alg. 6
+                    case HEDL_OP_MIN: n.pred = P_GE; n.n = nd.n; n.sat = nd.n; break;        // Alg. 7 MIN
+                    case HEDL_OP_MAX: n.pred = compat ? P_LEP : P_LE; n.n = nd.n; n.sat = nd.n + 1; break;
+                    default: n.pred = P_EQ; n.n = nd.n; n.sat = nd.n + 1; break;             // EXACTLY
+                    }
+                    r = mkref(RT_NODE, D.intern(n, &child), 0);
+                    break;
+                }
+                case HEDL_OP_DRANGE: {
+                    if (cc) return bad(HEDL_ERR_BAD_EXPR, i, "DRANGE takes no children");
+                    if (std::isnan(nd.lo) || std::isnan(nd.hi)) return bad(HEDL_ERR_BAD_EXPR, i, "NaN bound");
+                    if (nd.arg >= kb->D) return bad(HEDL_ERR_OUT_OF_RANGE, i, "data property id out of range");
+                    CNode n{};
+                    n.kind = NK_DRANGE;
+                    n.dir = (uint16_t)nd.arg;
+                    n.lo = nd.lo;
+                    n.hi = nd.hi;
+                    r = mkref(RT_NODE, D.intern(n, nullptr), 0);
+                    break;
+                }
+                default:
+                    return bad(HEDL_ERR_BAD_EXPR, i, "unknown opcode");
+                }
+                memo.set(i, 2, r);
+                stack.pop_back();
+            }
+        }
+        sh.root_ref[ri - r0] = memo.val(root);
+    }
+}
+
+// ---- lock-free global DAG (level-synchronous merge of the shards) -------------------
+struct Global {
+    hedl_program *p;
+    const hedl_kb *kb;
+    bool cse;
+    std::unique_ptr<std::atomic<uint32_t>[]> table;
+    uint64_t mask = 0;
+    std::atomic<uint32_t> n_count{0};
+    std::atomic<uint64_t> ops_count{0};
+
+    uint32_t intern(CNode n, const uint32_t *o) {
+        uint32_t mine = 0xffffffffu;
+        auto materialise = [&]() {
+            mine = n_count.fetch_add(1, std::memory_order_relaxed);
+            const uint64_t ob = ops_count.fetch_add(n.op_count, std::memory_order_relaxed);
+            std::copy(o, o + n.op_count, p->ops.begin() + ob);
+            n.op_begin = (uint32_t)ob;
+            uint32_t lvl = 0;
+            bool has_node = false;
+            for (uint32_t i = 0; i < n.op_count; ++i)
+                if (ref_type(o[i]) == RT_NODE) {
+                    has_node = true;
+                    lvl = std::max(lvl, p->nodes[ref_id(o[i])].level);
+                }
+            n.level = has_node ? lvl + 1 : 0;
+            n.bytes = node_bytes(kb, n);
+            p->nodes[mine] = n;
+        };
+        if (!cse) {
+            materialise();
+            return mine;
+        }
+        uint64_t h = hash_node(n, o) & mask;
+        for (;;) {
+            uint32_t v = table[h].load(std::memory_order_acquire);
+            if (v == 0) {
+                if (mine == 0xffffffffu) materialise();
+                uint32_t expected = 0;
+                if (table[h].compare_exchange_strong(expected, mine + 1, std::memory_order_acq_rel,
+                                                     std::memory_order_acquire))
+                    return mine;
+                v = expected;
+            }
+            const uint32_t id = v - 1;
+            const CNode &c = p->nodes[id];
+            if (same_node(c, p->ops.data() + c.op_begin, n, o)) {
+                if (mine != 0xffffffffu) p->nodes[mine].kind = NK_DEAD;   // lost the race: a hole
+                return id;
+            }
+            h = (h + 1) & mask;
+        }
+    }
+};
+
+template <class F>
+void run_threads(unsigned n, F f) {
+    if (n <= 1) { f(0u); return; }
+    std::vector<std::thread> th;
+    th.reserve(n);
+    for (unsigned t = 0; t < n; ++t) th.emplace_back(f, t);
+    for (auto &x : th) x.join();
+}
 
 }  // namespace
 
@@ -105,155 +381,137 @@ extern "C" hedl_status hedl_compile(const hedl_kb *kb, const hedl_node *nodes, u
     if ((n_nodes && !nodes) || (n_child_idx && !child_idx) || (n_roots && !roots))
         return fail(HEDL_ERR_INVALID_ARG, "null node/child/root array");
     if (n_nodes >= (1u << 28)) return fail(HEDL_ERR_INVALID_ARG, "too many nodes in one program (max 2^28)");
-    const bool rewrite = !(flags & HEDL_COMPILE_NO_REWRITE);
-    const bool compat = flags & HEDL_COMPILE_COMPAT_PAPER_MAX;
+    const double t0 = now_ms();
+    const Input in{kb, nodes, n_nodes, child_idx, n_child_idx, roots, n_roots, flags};
+    unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    if (const char *e = std::getenv("HEDL_COMPILE_THREADS")) hw = std::max(1, std::atoi(e));   // tests / tuning
+    const unsigned T = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>({(uint64_t)hw, 32ull, (uint64_t)n_roots / 4096}));
+    std::vector<Shard> sh(T);
+    run_threads(T, [&](unsigned t) {
+        const uint32_t a = (uint32_t)((uint64_t)n_roots * t / T), b = (uint32_t)((uint64_t)n_roots * (t + 1) / T);
+        canon_shard(in, a, b, sh[t]);
+    });
+    for (unsigned t = 0; t < T; ++t)
+        if (sh[t].err) return fail(sh[t].err, sh[t].msg);
+    const double t1 = now_ms();
 
     hedl_program *p = new hedl_program();
     p->kb = kb;
     p->flags = flags;
-    p->nodes.reserve(n_nodes);
-    p->ops.reserve(n_child_idx + n_roots);
-    Builder B{p, kb, !(flags & HEDL_COMPILE_NO_CSE)};
-
-    const uint32_t UNSET = 0xffffffffu;
-    std::vector<uint32_t> ref(n_nodes, UNSET);
-    std::vector<uint8_t> state(n_nodes, 0);     // 0 new, 1 on stack, 2 done
-    std::vector<std::pair<uint32_t, uint32_t>> stack;
-    std::vector<uint32_t> tmp;
-    auto bad = [&](hedl_status st, uint32_t i, const std::string &m) {
-        delete p;
-        return fail(st, "node " + std::to_string(i) + ": " + m);
-    };
-
-    for (uint32_t ri = 0; ri < n_roots; ++ri) {
-        if (roots[ri] >= n_nodes) { delete p; return fail(HEDL_ERR_OUT_OF_RANGE, "root " + std::to_string(ri) + " out of range"); }
-        if (state[roots[ri]] == 2) continue;
-        stack.clear();
-        stack.push_back({roots[ri], 0});
-        state[roots[ri]] = 1;
-        while (!stack.empty()) {
-            const uint32_t i = stack.back().first;
-            const hedl_node &nd = nodes[i];
-            if ((uint64_t)nd.child_begin + nd.child_count > n_child_idx)
-                return bad(HEDL_ERR_OUT_OF_RANGE, i, "child range out of bounds");
-            uint32_t &k = stack.back().second;
-            if (k < nd.child_count) {
-                const uint32_t c = child_idx[nd.child_begin + k++];
-                if (c >= n_nodes) return bad(HEDL_ERR_OUT_OF_RANGE, i, "child id out of range");
-                if (state[c] == 1) return bad(HEDL_ERR_BAD_EXPR, i, "cycle");
-                if (state[c] == 0) { state[c] = 1; stack.push_back({c, 0}); }
-                continue;
+    p->root_node.resize(n_roots);
+    if (T == 1) {
+        // one shard: its DAG is the program
+        Shard &s0 = sh[0];
+        p->nodes.swap(s0.dag.nodes);
+        p->ops.swap(s0.dag.ops);
+        for (CNode &n : p->nodes) n.bytes = node_bytes(kb, n);
+        LocalDag &D = s0.dag;
+        D.nodes.swap(p->nodes);      // intern below needs the DAG: swap back temporarily
+        D.ops.swap(p->ops);
+        for (uint32_t ri = 0; ri < n_roots; ++ri) {
+            const uint32_t r = s0.root_ref[ri];
+            if (ref_type(r) == RT_NODE && !ref_comp(r)) {
+                p->root_node[ri] = ref_id(r);
+            } else {                 // a 1-operand AND materialises atoms, constants, complements
+                CNode n{};
+                n.kind = NK_AND;
+                n.op_count = 1;
+                const uint32_t id = D.intern(n, &r);
+                D.nodes[id].bytes = node_bytes(kb, D.nodes[id]);
+                p->root_node[ri] = id;
             }
-            // all children are done: build the canonical reference of node i
-            const uint32_t *ch = child_idx + nd.child_begin;
-            const uint32_t cc = nd.child_count;
-            const bool is_role = nd.op >= HEDL_OP_EXISTS && nd.op <= HEDL_OP_EXACT;
-            if (nd.flags & ~HEDL_FLAG_INV) return bad(HEDL_ERR_BAD_EXPR, i, "unknown flag bits");
-            if ((nd.flags & HEDL_FLAG_INV) && !is_role) return bad(HEDL_ERR_BAD_EXPR, i, "inverse flag on a non-role node");
-            uint32_t r = 0;
-            switch (nd.op) {
-            case HEDL_OP_TOP:
-            case HEDL_OP_BOTTOM:
-                if (cc) return bad(HEDL_ERR_BAD_EXPR, i, "TOP/BOTTOM take no children");
-                r = mkref(RT_TOP, 0, nd.op == HEDL_OP_BOTTOM);
-                break;
-            case HEDL_OP_ATOM:
-                if (cc) return bad(HEDL_ERR_BAD_EXPR, i, "ATOM takes no children");
-                if (nd.arg >= kb->C) return bad(HEDL_ERR_OUT_OF_RANGE, i, "concept id out of range");
-                r = mkref(RT_ATOM, nd.arg, 0);
-                break;
-            case HEDL_OP_NOT:
-                if (cc != 1) return bad(HEDL_ERR_BAD_EXPR, i, "NOT takes one child");
-                r = ref[ch[0]] ^ 1u;   // complement over Delta (Q1); NOT NOT C == C
-                break;
-            case HEDL_OP_AND:
-            case HEDL_OP_OR: {
-                const uint8_t kind = nd.op == HEDL_OP_AND ? NK_AND : NK_OR;
-                tmp.clear();
-                for (uint32_t j = 0; j < cc; ++j) {
-                    const uint32_t cr = ref[ch[j]];
-                    if (rewrite && ref_type(cr) == RT_NODE && !ref_comp(cr) && p->nodes[ref_id(cr)].kind == kind) {
-                        const CNode &sub = p->nodes[ref_id(cr)];
-                        for (uint32_t q = 0; q < sub.op_count; ++q) tmp.push_back(p->ops[sub.op_begin + q]);
-                    } else {
-                        tmp.push_back(cr);
-                    }
+        }
+        p->nodes.swap(D.nodes);
+        p->ops.swap(D.ops);
+    } else {
+        // level-synchronous merge into one lock-free hash-consed DAG
+        uint64_t tot_nodes = n_roots, tot_ops = n_roots;
+        uint32_t maxl = 0;
+        for (auto &s : sh) {
+            tot_nodes += s.dag.nodes.size();
+            tot_ops += s.dag.ops.size();
+            for (const CNode &n : s.dag.nodes) maxl = std::max(maxl, n.level);
+        }
+        p->nodes.resize(tot_nodes);
+        p->ops.resize(tot_ops);
+        Global G{p, kb, !(flags & HEDL_COMPILE_NO_CSE)};
+        if (G.cse) {
+            uint64_t cap = 1024;
+            while (cap < tot_nodes * 2) cap <<= 1;
+            G.table.reset(new std::atomic<uint32_t>[cap]);
+            for (uint64_t i = 0; i < cap; ++i) G.table[i].store(0, std::memory_order_relaxed);
+            G.mask = cap - 1;
+        }
+        std::vector<std::vector<uint32_t>> gmap(T);
+        std::vector<std::vector<uint32_t>> by_level(T);   // local ids ordered by level
+        std::vector<std::vector<uint32_t>> lvl_off(T);
+        run_threads(T, [&](unsigned t) {
+            const auto &L = sh[t].dag.nodes;
+            gmap[t].assign(L.size(), 0);
+            std::vector<uint32_t> cnt(maxl + 2, 0);
+            for (const CNode &n : L) cnt[n.level + 1]++;
+            for (uint32_t l = 0; l <= maxl; ++l) cnt[l + 1] += cnt[l];
+            lvl_off[t] = cnt;
+            by_level[t].resize(L.size());
+            std::vector<uint32_t> pos(cnt.begin(), cnt.end() - 1);
+            for (uint32_t i = 0; i < L.size(); ++i) by_level[t][pos[L[i].level]++] = i;
+        });
+        const bool rewrite = !(flags & HEDL_COMPILE_NO_REWRITE);
+        auto remap = [&](unsigned t, uint32_t r) {
+            return ref_type(r) == RT_NODE ? mkref(RT_NODE, gmap[t][ref_id(r)], ref_comp(r)) : r;
+        };
+        for (uint32_t l = 0; l <= maxl; ++l) {
+            run_threads(T, [&](unsigned t) {
+                const LocalDag &D = sh[t].dag;
+                std::vector<uint32_t> tmp;
+                for (uint32_t k = lvl_off[t][l]; k < lvl_off[t][l + 1]; ++k) {
+                    const uint32_t li = by_level[t][k];
+                    CNode n = D.nodes[li];
+                    tmp.resize(n.op_count);
+                    for (uint32_t q = 0; q < n.op_count; ++q) tmp[q] = remap(t, D.ops[n.op_begin + q]);
+                    if (rewrite && (n.kind == NK_AND || n.kind == NK_OR)) std::sort(tmp.begin(), tmp.end());
+                    gmap[t][li] = G.intern(n, tmp.data());
                 }
-                if (rewrite) {
-                    std::sort(tmp.begin(), tmp.end());
-                    tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
-                }
-                if (tmp.empty()) {                         // empty AND = TOP, empty OR = BOTTOM
-                    r = mkref(RT_TOP, 0, kind == NK_OR);
-                } else if (tmp.size() == 1 && rewrite) {
-                    r = tmp[0];
+            });
+        }
+        run_threads(T, [&](unsigned t) {
+            const uint32_t a = (uint32_t)((uint64_t)n_roots * t / T);
+            for (uint32_t k = 0; k < sh[t].root_ref.size(); ++k) {
+                const uint32_t r = remap(t, sh[t].root_ref[k]);
+                if (ref_type(r) == RT_NODE && !ref_comp(r)) {
+                    p->root_node[a + k] = ref_id(r);
                 } else {
                     CNode n{};
-                    n.kind = kind;
-                    n.op_count = (uint32_t)tmp.size();
-                    r = mkref(RT_NODE, B.intern(n, tmp.data()), 0);
+                    n.kind = NK_AND;
+                    n.op_count = 1;
+                    p->root_node[a + k] = G.intern(n, &r);
                 }
-                break;
             }
-            case HEDL_OP_EXISTS: case HEDL_OP_FORALL: case HEDL_OP_MIN: case HEDL_OP_MAX: case HEDL_OP_EXACT: {
-                if (cc != 1) return bad(HEDL_ERR_BAD_EXPR, i, "role restriction takes one child");
-                if (nd.arg >= kb->R) return bad(HEDL_ERR_OUT_OF_RANGE, i, "role id out of range");
-                if (nd.n > 0xfffffffeu) return bad(HEDL_ERR_BAD_EXPR, i, "n > 2^32-2");
-                CNode n{};
-                n.kind = NK_RESTRICT;
-                n.dir = (uint16_t)(2 * nd.arg + (nd.flags & HEDL_FLAG_INV ? 1 : 0));
-                n.op_count = 1;
-                uint32_t child = ref[ch[0]];
-                switch (nd.op) {
-                case HEDL_OP_EXISTS: n.pred = P_GE; n.n = 1; n.sat = 1; break;           // Alg. 4
-                case HEDL_OP_FORALL: n.pred = P_LE; n.n = 0; n.sat = 1; child ^= 1u; break; // Alg. 6
-                case HEDL_OP_MIN: n.pred = P_GE; n.n = nd.n; n.sat = nd.n; break;        // Alg. 7 MIN
-                case HEDL_OP_MAX: n.pred = compat ? P_LEP : P_LE; n.n = nd.n; n.sat = nd.n + 1; break;
-                default: n.pred = P_EQ; n.n = nd.n; n.sat = nd.n + 1; break;             // EXACTLY
-                }
-                r = mkref(RT_NODE, B.intern(n, &child), 0);
-                break;
-            }
-            case HEDL_OP_DRANGE: {
-                if (cc) return bad(HEDL_ERR_BAD_EXPR, i, "DRANGE takes no children");
-                if (std::isnan(nd.lo) || std::isnan(nd.hi)) return bad(HEDL_ERR_BAD_EXPR, i, "NaN bound");
-                if (nd.arg >= kb->D) return bad(HEDL_ERR_OUT_OF_RANGE, i, "data property id out of range");
-                CNode n{};
-                n.kind = NK_DRANGE;
-                n.dir = (uint16_t)nd.arg;
-                n.lo = nd.lo;
-                n.hi = nd.hi;
-                r = mkref(RT_NODE, B.intern(n, nullptr), 0);
-                break;
-            }
-            default:
-                return bad(HEDL_ERR_BAD_EXPR, i, "unknown opcode");
-            }
-            ref[i] = r;
-            state[i] = 2;
-            stack.pop_back();
-        }
-    }
-    // every root becomes a computed, uncomplemented node (a 1-operand AND
-    // materialises atoms, constants and complemented references)
-    p->root_node.resize(n_roots);
-    for (uint32_t ri = 0; ri < n_roots; ++ri) {
-        const uint32_t r = ref[roots[ri]];
-        if (ref_type(r) == RT_NODE && !ref_comp(r)) {
-            p->root_node[ri] = ref_id(r);
-        } else {
-            CNode n{};
-            n.kind = NK_AND;
-            n.op_count = 1;
-            p->root_node[ri] = B.intern(n, &r);
-        }
+        });
+        p->nodes.resize(G.n_count.load());
+        p->ops.resize(G.ops_count.load());
     }
     uint32_t maxl = 0;
-    for (const CNode &n : p->nodes) maxl = std::max(maxl, n.level);
-    p->n_levels = p->nodes.empty() ? 0 : maxl + 1;
-    // B(h): bytes of the root's sub-DAG (each node once) + fused coverage (8W + 32)
-    p->root_bytes.resize(n_roots);
+    bool any = false;
+    for (const CNode &n : p->nodes)
+        if (n.kind != NK_DEAD) { maxl = std::max(maxl, n.level); any = true; }
+    p->n_levels = any ? maxl + 1 : 0;
     p->stamp.assign(p->nodes.size(), 0);
+    timing_note("compile: shards", t1 - t0);
+    timing_note("compile: total", now_ms() - t0);
+    *out = p;
+    return HEDL_OK;
+}
+
+// B(h): bytes of the root's sub-DAG (each node once) + fused coverage (8W + 32).
+// Computed lazily (only the info/bytes queries need it), so compile stays lean.
+static void ensure_root_bytes(hedl_program *p) {
+    std::lock_guard<std::mutex> lk(p->mu);
+    if (p->root_bytes.size() == p->root_node.size()) return;
+    const hedl_kb *kb = p->kb;
+    const uint32_t n_roots = (uint32_t)p->root_node.size();
+    p->root_bytes.resize(n_roots);
+    if (p->stamp.size() < p->nodes.size()) p->stamp.assign(p->nodes.size(), 0);
     std::vector<uint32_t> st;
     for (uint32_t ri = 0; ri < n_roots; ++ri) {
         const uint32_t gen = ++p->stamp_gen;
@@ -275,17 +533,18 @@ extern "C" hedl_status hedl_compile(const hedl_kb *kb, const hedl_node *nodes, u
         }
         p->root_bytes[ri] = b;
     }
-    *out = p;
-    return HEDL_OK;
 }
 
 extern "C" hedl_status hedl_program_get_info(const hedl_program *p, hedl_program_info *out) {
     if (!p || !out) return fail(HEDL_ERR_INVALID_ARG, "null program/out");
+    ensure_root_bytes(const_cast<hedl_program *>(p));
     std::memset(out, 0, sizeof(*out));
     out->n_roots = (uint32_t)p->root_node.size();
-    out->n_nodes = (uint32_t)p->nodes.size();
+    out->n_nodes = 0;
     out->n_levels = p->n_levels;
     for (const CNode &n : p->nodes) {
+        if (n.kind == NK_DEAD) continue;
+        out->n_nodes++;
         if (n.kind == NK_AND || n.kind == NK_OR) out->n_bool++;
         else if (n.kind == NK_RESTRICT) out->n_restrict++;
         else out->n_drange++;
@@ -297,6 +556,7 @@ extern "C" hedl_status hedl_program_get_info(const hedl_program *p, hedl_program
 
 extern "C" hedl_status hedl_program_root_bytes(const hedl_program *p, uint32_t first, uint32_t n, double *out) {
     if (!p || (n && !out)) return fail(HEDL_ERR_INVALID_ARG, "null program/out");
+    ensure_root_bytes(const_cast<hedl_program *>(p));
     if ((uint64_t)first + n > p->root_bytes.size()) return fail(HEDL_ERR_OUT_OF_RANGE, "root range");
     std::copy(p->root_bytes.begin() + first, p->root_bytes.begin() + first + n, out);
     return HEDL_OK;

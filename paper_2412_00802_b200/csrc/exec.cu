@@ -4,9 +4,12 @@
 // canonical nodes are collected, grouped by topological level and then by
 // (kind, role direction / data property), and each group runs as ONE launch
 // whose blockIdx.y walks the group's nodes (consecutive nodes of one direction
-// re-hit the same CSR in L2).  Root nodes fuse the Alg. 15 coverage
-// (PAPER.md:548-553).  One H2D copy of descriptors per chunk; counts come back
-// with one D2H per call (the paper's single cudaMemcpyAsync).
+// re-hit the same CSR in L2); restriction groups of >= kSliceMinNodes nodes run
+// as lane-packed passes (slice.cu).  Root nodes fuse the Alg. 15 coverage
+// (PAPER.md:548-553).  The plan (descriptors of every launch) is the paper's
+// "evaluation plan": built on the first call for a root range,
+// kept device-resident in the program, and replayed by later calls.  Counts come
+// back with one D2H per call (the paper's single cudaMemcpyAsync).
 #include <algorithm>
 
 #include "internal.h"
@@ -21,13 +24,36 @@ struct DevBuf {
     size_t bytes = 0;
 };
 
-// per-program device/pinned buffers (kept in hedl_program via an opaque side table)
+struct LaunchRec {
+    uint8_t kind;          // NK_AND (AND+OR), NK_RESTRICT, NK_DRANGE
+    uint16_t key;          // dir / prop
+    bool slice;
+    uint32_t count, first_desc;
+    double bytes, bytes2;
+};
+
+struct ChunkPlan {
+    uint32_t ri, rc;       // roots [ri, rc) relative to the program
+    uint32_t nn, ncov, nrows;
+    size_t blob_off, blob_bytes;          // into PlanCache host/device blobs
+    size_t off_bool, off_ops, off_res, off_dr, off_cov, off_rows;
+    std::vector<LaunchRec> recs;
+};
+
+struct PlanCache {
+    bool valid = false;
+    uint32_t r0 = 0, r1 = 0, eflags = 0;
+    bool bits = false;
+    void *rows_base = nullptr, *heavy_base = nullptr;
+    std::vector<ChunkPlan> chunks;
+    void *host = nullptr;                 // pinned descriptor blob
+    void *dev = nullptr;                  // device descriptor blob
+    size_t cap = 0;                       // capacity of both blobs
+};
+
 struct Workspace {
-    DevBuf rows, heavy, desc, counts, slice;
-    void *pinned[2] = {nullptr, nullptr};
-    size_t pinned_bytes[2] = {0, 0};
-    cudaEvent_t pinned_ev[2] = {nullptr, nullptr};
-    int pin_idx = 0;
+    DevBuf rows, heavy, counts, slice;
+    PlanCache plan;
     cudaEvent_t done = nullptr;
     cudaStream_t last_stream = nullptr;
     bool used = false;
@@ -41,7 +67,7 @@ Workspace *ws_of(hedl_program *p) {
 hedl_status grow(const hedl_kb *kb, cudaStream_t s, DevBuf &b, size_t need, bool zero) {
     if (b.bytes >= need) return HEDL_OK;
     HEDL_CUDA(kb, cudaStreamSynchronize(s));
-    size_t sz = std::max(need, b.bytes * 3 / 2);
+    size_t sz = std::max(need, b.bytes * 5 / 4);
     if (b.p) cudaFree(b.p);
     b.p = nullptr;
     b.bytes = 0;
@@ -50,7 +76,7 @@ hedl_status grow(const hedl_kb *kb, cudaStream_t s, DevBuf &b, size_t need, bool
     if (e != cudaSuccess) {
         cudaGetLastError();
         e = cudaMalloc(&b.p, need);
-        if (e != cudaSuccess) { cudaGetLastError(); return fail(HEDL_ERR_OOM, "workspace allocation failed"); }
+        if (e != cudaSuccess) { cudaGetLastError(); b.p = nullptr; return fail(HEDL_ERR_OOM, "workspace allocation failed"); }
         sz = need;
     }
     b.bytes = sz;
@@ -58,63 +84,92 @@ hedl_status grow(const hedl_kb *kb, cudaStream_t s, DevBuf &b, size_t need, bool
     return HEDL_OK;
 }
 
-hedl_status get_pinned(Workspace *w, size_t need, void **out) {
-    const int i = w->pin_idx;
-    if (w->pinned_ev[i]) cudaEventSynchronize(w->pinned_ev[i]);
-    if (w->pinned_bytes[i] < need) {
-        if (w->pinned[i]) cudaFreeHost(w->pinned[i]);
-        size_t sz = std::max(need, w->pinned_bytes[i] * 3 / 2);
-        if (cudaMallocHost(&w->pinned[i], sz) != cudaSuccess) {
-            w->pinned[i] = nullptr;
-            w->pinned_bytes[i] = 0;
-            cudaGetLastError();
-            return fail(HEDL_ERR_OOM, "pinned allocation failed");
-        }
-        w->pinned_bytes[i] = sz;
+void invalidate_plan(PlanCache &pc) {
+    pc.valid = false;
+    pc.chunks.clear();
+}
+
+void release_plan(PlanCache &pc) {
+    if (pc.host) cudaFreeHost(pc.host);
+    if (pc.dev) cudaFree(pc.dev);
+    pc = PlanCache();
+}
+
+hedl_status reserve_plan(PlanCache &pc, size_t bytes) {
+    if (pc.cap >= bytes) return HEDL_OK;
+    if (pc.host) cudaFreeHost(pc.host);
+    if (pc.dev) cudaFree(pc.dev);
+    pc.host = pc.dev = nullptr;
+    pc.cap = 0;
+    const size_t cap = std::max(bytes, (size_t)4096) * 5 / 4;
+    if (cudaMallocHost(&pc.host, cap) != cudaSuccess) { cudaGetLastError(); pc.host = nullptr; return fail(HEDL_ERR_OOM, "pinned plan"); }
+    if (cudaMalloc(&pc.dev, cap) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFreeHost(pc.host);
+        pc.host = pc.dev = nullptr;
+        return fail(HEDL_ERR_OOM, "device plan");
     }
-    *out = w->pinned[i];
+    pc.cap = cap;
     return HEDL_OK;
 }
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-struct Group {          // one launch
-    uint8_t kind;       // NK_*
-    uint16_t key;       // dir or prop
-    uint32_t first, count;   // into the chunk node list
+struct Group {
+    uint8_t kind;
+    uint16_t key;
+    uint32_t first, count;
     bool slice = false;
 };
 
-// Evaluate roots [r0, r1) of the program as consecutive chunks.
-// counts_dev: device hedl_counts[r1-r0] output; out_bits: device [r1-r0][W] or null.
-hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, uint32_t *out_bits,
-                hedl_counts *counts_dev, cudaStream_t s, uint32_t eflags) {
-    Workspace *w = ws_of(p);
-    if (w->used && w->last_stream != s && w->done) HEDL_CUDA(kb, cudaStreamWaitEvent(s, w->done, 0));
-    const size_t row_bytes = (size_t)kb->W4 * 4;
-    const KbDev kd{kb->N, kb->W, kb->W4, kb->pos, kb->neg};
-    const uint64_t max_nodes = std::max<uint64_t>(1, row_bytes ? p->ws_limit / row_bytes : (1ull << 20));
-    const uint64_t node_cap = std::min<uint64_t>(max_nodes, 1u << 20);
-    const bool use_slice = !(eflags & HEDL_EVAL_PER_NODE) && slice_enabled(kb);
+// ---- planning -------------------------------------------------------------------
+// order key: level, kind, direction / property, lane-pack class, node id
+inline uint64_t order_key(const CNode &n, uint32_t id) {
+    const uint64_t cls = n.kind == NK_RESTRICT ? slice_class(n.pred, n.n, n.sat) : 0;
+    return ((uint64_t)std::min<uint32_t>(n.level, 4095) << 52) | ((uint64_t)(n.kind & 3) << 50) |
+           ((uint64_t)n.dir << 34) | (cls << 32) | id;
+}
 
+void sort_by_key(const hedl_program *p, std::vector<uint32_t> &list) {
+    std::vector<uint64_t> keys(list.size());
+    for (size_t k = 0; k < list.size(); ++k) keys[k] = order_key(p->nodes[list[k]], list[k]);
+    std::sort(keys.begin(), keys.end());
+    for (size_t k = 0; k < list.size(); ++k) list[k] = (uint32_t)keys[k];
+}
+
+// Phase A: the node list of every chunk (host only).  Rows are materialised only
+// for nodes some other node reads, so the row budget counts operand nodes.
+void collect_chunks(hedl_program *p, uint32_t r0, uint32_t r1, uint64_t row_cap,
+                    std::vector<std::vector<uint32_t>> &lists, std::vector<std::pair<uint32_t, uint32_t>> &ranges) {
     if (p->stamp.size() < p->nodes.size()) p->stamp.assign(p->nodes.size(), 0);
-    std::vector<uint32_t> list, st, slot_of_node_tmp;
-    std::vector<uint32_t> cover_of_root;   // per root in chunk: cover slot
-    std::vector<uint32_t> local;           // node id -> index in list (valid when stamped)
-    if (local.size() < p->nodes.size()) local.resize(p->nodes.size());
-    std::vector<int32_t> cover_of_node;
-
+    if (r0 == 0 && r1 == p->root_node.size()) {
+        // the whole program: every live node is reachable from a root
+        uint64_t live = 0;
+        for (const CNode &n : p->nodes) live += n.kind <= NK_DRANGE;
+        if (live - std::min<uint64_t>(live, r1) <= row_cap) {
+            std::vector<uint32_t> list;
+            list.reserve(live);
+            for (uint32_t i = 0; i < p->nodes.size(); ++i)
+                if (p->nodes[i].kind <= NK_DRANGE) list.push_back(i);
+            sort_by_key(p, list);
+            lists.push_back(std::move(list));
+            ranges.push_back({r0, r1});
+            return;
+        }
+    }
+    std::vector<uint32_t> st;
     uint32_t ri = r0;
     while (ri < r1) {
-        // ---- collect the chunk's nodes (DFS from roots, stamp-deduplicated) ----
         const uint32_t gen = ++p->stamp_gen;
-        list.clear();
+        std::vector<uint32_t> list;
+        uint64_t operands = 0;
         uint32_t rc = ri;
         for (; rc < r1; ++rc) {
             const size_t before = list.size();
-            st.assign(1, p->root_node[rc]);
+            const uint64_t ob = operands;
             if (p->stamp[p->root_node[rc]] == gen) continue;
             p->stamp[p->root_node[rc]] = gen;
+            st.assign(1, p->root_node[rc]);
             while (!st.empty()) {
                 const uint32_t id = st.back();
                 st.pop_back();
@@ -125,216 +180,313 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
                     if (ref_type(o) == RT_NODE && p->stamp[ref_id(o)] != gen) {
                         p->stamp[ref_id(o)] = gen;
                         st.push_back(ref_id(o));
+                        ++operands;
                     }
                 }
             }
-            if (list.size() > node_cap && rc > ri) {    // this root overflows: defer it
+            if (operands > row_cap && rc > ri) {    // this root overflows the chunk: defer it
                 for (size_t k = before; k < list.size(); ++k) p->stamp[list[k]] = 0;
                 list.resize(before);
+                operands = ob;
                 break;
             }
         }
-        const uint32_t nroots = rc - ri;
-        // ---- order: level, kind, direction ----
-        std::sort(list.begin(), list.end(), [&](uint32_t a, uint32_t b) {
-            const CNode &x = p->nodes[a], &y = p->nodes[b];
-            if (x.level != y.level) return x.level < y.level;
-            if (x.kind != y.kind) return x.kind < y.kind;
-            if (x.dir != y.dir) return x.dir < y.dir;
-            if (x.kind == NK_RESTRICT) {
-                const uint32_t cx = slice_class(x.pred, x.n, x.sat), cy = slice_class(y.pred, y.n, y.sat);
-                if (cx != cy) return cx < cy;
-            }
-            return a < b;
-        });
-        const uint32_t nn = (uint32_t)list.size();
-        for (uint32_t k = 0; k < nn; ++k) local[list[k]] = k;
-        // cover slots: one per distinct root node of the chunk
-        cover_of_node.assign(nn, -1);
-        cover_of_root.resize(nroots);
-        uint32_t ncov = 0;
-        for (uint32_t k = 0; k < nroots; ++k) {
-            const uint32_t li = local[p->root_node[ri + k]];
-            if (cover_of_node[li] < 0) cover_of_node[li] = (int32_t)ncov++;
-            cover_of_root[k] = (uint32_t)cover_of_node[li];
-        }
-        // groups
-        std::vector<Group> groups;
-        for (uint32_t k = 0; k < nn;) {
-            const CNode &a = p->nodes[list[k]];
-            const uint8_t kind = (a.kind == NK_OR) ? NK_AND : a.kind;   // AND and OR share a launch
-            const uint16_t key = (kind == NK_AND) ? 0 : a.dir;
-            uint32_t e = k + 1;
-            while (e < nn) {
-                const CNode &b = p->nodes[list[e]];
-                const uint8_t kb2 = (b.kind == NK_OR) ? NK_AND : b.kind;
-                if (b.level != a.level || kb2 != kind || (kind != NK_AND && b.dir != key)) break;
-                ++e;
-            }
-            Group g{kind, key, k, e - k};
-            if (use_slice && kind == NK_RESTRICT) {
-                uint32_t ns = 0;   // leading lane-packable nodes (class 0/1 sort first)
-                while (ns < g.count) {
-                    const CNode &c = p->nodes[list[k + ns]];
-                    if (slice_class(c.pred, c.n, c.sat) == 2) break;
-                    ++ns;
-                }
-                if (ns && slice_worthwhile(kb, ns, eflags & HEDL_EVAL_FORCE_SLICE)) {
-                    if (ns < g.count) {            // split: packable prefix + per-node rest
-                        Group g1{kind, key, k, ns};
-                        g1.slice = true;
-                        groups.push_back(g1);
-                        g.first = k + ns;
-                        g.count -= ns;
-                    } else {
-                        g.slice = true;
-                    }
-                }
-            }
-            groups.push_back(g);
-            k = e;
-        }
-        // ---- sizes ----
-        size_t n_ops = 0, n_bool = 0, n_res = 0, n_dr = 0, heavy_need = 0;
-        for (const Group &g : groups) {
-            if (g.kind == NK_AND) {
-                n_bool += g.count;
-                for (uint32_t k = g.first; k < g.first + g.count; ++k) n_ops += p->nodes[list[k]].op_count;
-            } else if (g.kind == NK_RESTRICT) {
-                n_res += g.count;
-                heavy_need = std::max(heavy_need, (size_t)g.count * kb->dirs[g.key].n_heavy * 8);
-            } else {
-                n_dr += g.count;
-            }
-        }
-        const size_t off_bool = 0;
-        const size_t off_ops = align_up(off_bool + n_bool * sizeof(BoolDesc), 16);
-        const size_t off_res = align_up(off_ops + n_ops * sizeof(Operand), 16);
-        const size_t off_dr = align_up(off_res + n_res * sizeof(RestrictDesc), 16);
-        const size_t off_cov = align_up(off_dr + n_dr * sizeof(DrangeDesc), 16);
-        const size_t off_rows = align_up(off_cov + nroots * sizeof(uint32_t), 16);
-        const size_t desc_bytes = align_up(off_rows + (out_bits ? nroots * sizeof(void *) : 0), 16);
-
-        hedl_status stt;
-        if ((stt = grow(kb, s, w->rows, std::max<size_t>(16, nn * row_bytes), false))) return stt;
-        if ((stt = grow(kb, s, w->heavy, std::max<size_t>(16, heavy_need), true))) return stt;
-        if ((stt = grow(kb, s, w->desc, desc_bytes, false))) return stt;
-        if ((stt = grow(kb, s, w->counts, std::max<size_t>(32, ncov * sizeof(hedl_counts)), false))) return stt;
-        void *hp = nullptr;
-        if ((stt = get_pinned(w, desc_bytes, &hp))) return stt;
-        char *h = (char *)hp;
-        char *d = (char *)w->desc.p;
-        uint32_t *rows = (uint32_t *)w->rows.p;
-        hedl_counts *cov = (hedl_counts *)w->counts.p;
-        auto ptr_of = [&](uint32_t r) -> const uint32_t * {
-            switch (ref_type(r)) {
-            case RT_NODE: return rows + (size_t)local[ref_id(r)] * kb->W4;
-            case RT_ATOM: return kb->concepts + (size_t)ref_id(r) * kb->W4;
-            default: return kb->ones;
-            }
-        };
-        // ---- fill descriptors (host, pinned) ----
-        BoolDesc *hb = (BoolDesc *)(h + off_bool);
-        Operand *ho = (Operand *)(h + off_ops);
-        RestrictDesc *hr = (RestrictDesc *)(h + off_res);
-        DrangeDesc *hd = (DrangeDesc *)(h + off_dr);
-        uint32_t ib = 0, io = 0, ir = 0, idr = 0;
-        struct LaunchRec { const Group *g; uint32_t first_desc; double bytes, bytes2; };
-        std::vector<LaunchRec> recs;
-        for (const Group &g : groups) {
-            LaunchRec lr{&g, 0, 0, 0};
-            if (g.kind == NK_AND) {
-                lr.first_desc = ib;
-                for (uint32_t k = g.first; k < g.first + g.count; ++k) {
-                    const CNode &n = p->nodes[list[k]];
-                    BoolDesc bd;
-                    bd.out = rows + (size_t)k * kb->W4;
-                    bd.op_first = io;
-                    bd.op_count = n.op_count;
-                    bd.is_or = n.kind == NK_OR;
-                    bd.cover = cover_of_node[k];
-                    for (uint32_t q = 0; q < n.op_count; ++q) {
-                        const uint32_t o = p->ops[n.op_begin + q];
-                        ho[io++] = Operand{ptr_of(o), ref_comp(o) ? 0xffffffffu : 0u, 0};
-                    }
-                    hb[ib++] = bd;
-                    lr.bytes += n.bytes + (bd.cover >= 0 ? 8.0 * kb->W : 0);
-                }
-            } else if (g.kind == NK_RESTRICT) {
-                lr.first_desc = ir;
-                const hedl_dir &dr = kb->dirs[g.key];
-                for (uint32_t k = g.first; k < g.first + g.count; ++k) {
-                    const CNode &n = p->nodes[list[k]];
-                    const uint32_t c = p->ops[n.op_begin];
-                    RestrictDesc rd;
-                    rd.child = ptr_of(c);
-                    rd.out = rows + (size_t)k * kb->W4;
-                    rd.cmask = ref_comp(c) ? 0xffffffffu : 0u;
-                    rd.pred = n.pred;
-                    rd.n = n.n;
-                    rd.sat = n.sat;
-                    rd.cover = cover_of_node[k];
-                    rd.heavy_slot = (k - g.first) * dr.n_heavy;
-                    hr[ir++] = rd;
-                    lr.bytes += 4.0 * (kb->N + 1) + 4.0 * (dr.E - dr.E_heavy) + 8.0 * kb->W + (rd.cover >= 0 ? 8.0 * kb->W : 0);
-                    lr.bytes2 += 4.0 * dr.E_heavy;
-                }
-            } else {
-                lr.first_desc = idr;
-                for (uint32_t k = g.first; k < g.first + g.count; ++k) {
-                    const CNode &n = p->nodes[list[k]];
-                    DrangeDesc dd;
-                    dd.out = rows + (size_t)k * kb->W4;
-                    dd.lo = n.lo;
-                    dd.hi = n.hi;
-                    dd.cover = cover_of_node[k];
-                    dd.prop = n.dir;
-                    hd[idr++] = dd;
-                    lr.bytes += n.bytes + (dd.cover >= 0 ? 8.0 * kb->W : 0);
-                }
-            }
-            recs.push_back(lr);
-        }
-        std::memcpy(h + off_cov, cover_of_root.data(), nroots * sizeof(uint32_t));
-        if (out_bits) {
-            const uint32_t **hrows = (const uint32_t **)(h + off_rows);
-            for (uint32_t k = 0; k < nroots; ++k) hrows[k] = rows + (size_t)local[p->root_node[ri + k]] * kb->W4;
-        }
-        HEDL_CUDA(kb, cudaMemcpyAsync(d, h, desc_bytes, cudaMemcpyHostToDevice, s));
-        count_io(desc_bytes, 0);
-        if (!w->pinned_ev[w->pin_idx]) HEDL_CUDA(kb, cudaEventCreateWithFlags(&w->pinned_ev[w->pin_idx], cudaEventDisableTiming));
-        HEDL_CUDA(kb, cudaEventRecord(w->pinned_ev[w->pin_idx], s));
-        w->pin_idx ^= 1;
-
-        // ---- launches ----
-        launch_cover_init(s, cov, ncov, kb->npos, kb->nneg);
-        for (const LaunchRec &lr : recs) {
-            const Group &g = *lr.g;
-            if (g.kind == NK_AND) {
-                launch_bool(s, kd, (const BoolDesc *)(d + off_bool) + lr.first_desc, g.count,
-                            (const Operand *)(d + off_ops), cov, lr.bytes);
-            } else if (g.kind == NK_RESTRICT) {
-                const hedl_dir &dr = kb->dirs[g.key];
-                DirDev dd{dr.row_ptr, dr.col, dr.heavy_x, dr.heavy_nchunks, dr.chunks, dr.n_heavy, dr.n_chunks};
-                const RestrictDesc *dd_desc = (const RestrictDesc *)(d + off_res) + lr.first_desc;
-                if (g.slice) {
-                    stt = slice_run(kb, &w->slice.p, &w->slice.bytes, s, kd, g.key, hr + lr.first_desc, dd_desc,
-                                    g.count, cov);
-                    if (stt) return stt;
-                } else {
-                    launch_restrict(s, kd, dd, dd_desc, g.count, cov, (uint32_t *)w->heavy.p, lr.bytes, lr.bytes2);
-                }
-            } else {
-                const hedl_data &dp = kb->data[g.key];
-                launch_drange(s, kd, dp.row_ptr, dp.val, (const DrangeDesc *)(d + off_dr) + lr.first_desc, g.count,
-                              cov, lr.bytes);
-            }
-        }
-        launch_gather_counts(s, cov, (const uint32_t *)(d + off_cov), counts_dev + (ri - r0), nroots);
-        if (out_bits)
-            launch_gather_bits(s, (const uint32_t *const *)(d + off_rows), out_bits + (size_t)(ri - r0) * kb->W, kb->W, nroots);
-        HEDL_CUDA(kb, cudaGetLastError());
+        sort_by_key(p, list);
+        lists.push_back(std::move(list));
+        ranges.push_back({ri, rc});
         ri = rc;
+    }
+}
+
+struct ChunkTmp {            // per-chunk planning state kept between the sizing and filling passes
+    std::vector<uint32_t> slot, cover_of_root;
+    std::vector<int32_t> cover_of_node;
+    std::vector<uint8_t> need_row;
+    std::vector<Group> groups;
+};
+
+// Phase C: descriptors of one chunk into `h` (host blob) with device addresses.
+// Called twice: sizes_only (fills tmp and the blob layout), then with the final buffers.
+void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> &list, ChunkPlan &cp,
+                bool out_bits, bool use_slice, bool force_slice, uint32_t *rows, std::vector<uint32_t> &local,
+                char *h_blob, size_t *blob_cursor, size_t *heavy_need, bool sizes_only, ChunkTmp &tmp) {
+    const uint32_t nn = (uint32_t)list.size();
+    cp.nn = nn;
+    for (uint32_t k = 0; k < nn; ++k) local[list[k]] = k;
+    const uint32_t nroots = cp.rc - cp.ri;
+    std::vector<uint8_t> &need_row = tmp.need_row;
+    std::vector<uint32_t> &slot = tmp.slot;
+    std::vector<int32_t> &cover_of_node = tmp.cover_of_node;
+    std::vector<uint32_t> &cover_of_root = tmp.cover_of_root;
+    std::vector<Group> &groups = tmp.groups;
+    if (sizes_only) {
+    need_row.assign(nn, 0);
+    for (uint32_t k = 0; k < nn; ++k) {
+        const CNode &n = p->nodes[list[k]];
+        for (uint32_t q = 0; q < n.op_count; ++q) {
+            const uint32_t o = p->ops[n.op_begin + q];
+            if (ref_type(o) == RT_NODE) need_row[local[ref_id(o)]] = 1;
+        }
+    }
+    if (out_bits)
+        for (uint32_t k = 0; k < nroots; ++k) need_row[local[p->root_node[cp.ri + k]]] = 1;
+    slot.assign(nn, 0);
+    uint32_t nrows = 0;
+    for (uint32_t k = 0; k < nn; ++k)
+        if (need_row[k]) slot[k] = nrows++;
+    cp.nrows = nrows;
+    cover_of_node.assign(nn, -1);
+    cover_of_root.resize(nroots);
+    uint32_t ncov = 0;
+    for (uint32_t k = 0; k < nroots; ++k) {
+        const uint32_t li = local[p->root_node[cp.ri + k]];
+        if (cover_of_node[li] < 0) cover_of_node[li] = (int32_t)ncov++;
+        cover_of_root[k] = (uint32_t)cover_of_node[li];
+    }
+    cp.ncov = ncov;
+    groups.clear();
+    for (uint32_t k = 0; k < nn;) {
+        const CNode &a = p->nodes[list[k]];
+        const uint8_t kind = (a.kind == NK_OR) ? NK_AND : a.kind;   // AND and OR share a launch
+        const uint16_t key = (kind == NK_AND) ? 0 : a.dir;
+        uint32_t e = k + 1;
+        while (e < nn) {
+            const CNode &b = p->nodes[list[e]];
+            const uint8_t kb2 = (b.kind == NK_OR) ? NK_AND : b.kind;
+            if (b.level != a.level || kb2 != kind || (kind != NK_AND && b.dir != key)) break;
+            ++e;
+        }
+        Group g{kind, key, k, e - k};
+        if (use_slice && kind == NK_RESTRICT) {
+            uint32_t ns = 0;   // leading lane-packable nodes (class 0/1 sort first)
+            while (ns < g.count) {
+                const CNode &c = p->nodes[list[k + ns]];
+                if (slice_class(c.pred, c.n, c.sat) == 2) break;
+                ++ns;
+            }
+            if (ns && slice_worthwhile(kb, ns, force_slice)) {
+                if (ns < g.count) {
+                    Group g1{kind, key, k, ns};
+                    g1.slice = true;
+                    groups.push_back(g1);
+                    g.first = k + ns;
+                    g.count -= ns;
+                } else {
+                    g.slice = true;
+                }
+            }
+        }
+        groups.push_back(g);
+        k = e;
+    }
+    size_t n_ops = 0, n_bool = 0, n_res = 0, n_dr = 0;
+    for (const Group &g : groups) {
+        if (g.kind == NK_AND) {
+            n_bool += g.count;
+            for (uint32_t k = g.first; k < g.first + g.count; ++k) n_ops += p->nodes[list[k]].op_count;
+        } else if (g.kind == NK_RESTRICT) {
+            n_res += g.count;
+            if (!g.slice) *heavy_need = std::max(*heavy_need, (size_t)g.count * kb->dirs[g.key].n_heavy * 8);
+        } else {
+            n_dr += g.count;
+        }
+    }
+    cp.off_bool = 0;
+    cp.off_ops = align_up(cp.off_bool + n_bool * sizeof(BoolDesc), 16);
+    cp.off_res = align_up(cp.off_ops + n_ops * sizeof(Operand), 16);
+    cp.off_dr = align_up(cp.off_res + n_res * sizeof(RestrictDesc), 16);
+    cp.off_cov = align_up(cp.off_dr + n_dr * sizeof(DrangeDesc), 16);
+    cp.off_rows = align_up(cp.off_cov + nroots * sizeof(uint32_t), 16);
+    cp.blob_bytes = align_up(cp.off_rows + (out_bits ? nroots * sizeof(void *) : 0), 256);
+    cp.blob_off = *blob_cursor;
+    *blob_cursor += cp.blob_bytes;
+    return;
+    }
+
+    char *h = h_blob + cp.blob_off;
+    auto ptr_of = [&](uint32_t r) -> const uint32_t * {
+        switch (ref_type(r)) {
+        case RT_NODE: return rows + (size_t)slot[local[ref_id(r)]] * kb->W4;
+        case RT_ATOM: return kb->concepts + (size_t)ref_id(r) * kb->W4;
+        default: return kb->ones;
+        }
+    };
+    BoolDesc *hb = (BoolDesc *)(h + cp.off_bool);
+    Operand *ho = (Operand *)(h + cp.off_ops);
+    RestrictDesc *hr = (RestrictDesc *)(h + cp.off_res);
+    DrangeDesc *hd = (DrangeDesc *)(h + cp.off_dr);
+    uint32_t ib = 0, io = 0, ir = 0, idr = 0;
+    cp.recs.clear();
+    for (const Group &g : groups) {
+        LaunchRec lr{g.kind, g.key, g.slice, g.count, 0, 0, 0};
+        if (g.kind == NK_AND) {
+            lr.first_desc = ib;
+            for (uint32_t k = g.first; k < g.first + g.count; ++k) {
+                const CNode &n = p->nodes[list[k]];
+                BoolDesc bd;
+                bd.out = need_row[k] ? rows + (size_t)slot[k] * kb->W4 : nullptr;
+                bd.op_first = io;
+                bd.op_count = n.op_count;
+                bd.is_or = n.kind == NK_OR;
+                bd.cover = cover_of_node[k];
+                for (uint32_t q = 0; q < n.op_count; ++q) {
+                    const uint32_t o = p->ops[n.op_begin + q];
+                    ho[io++] = Operand{ptr_of(o), ref_comp(o) ? 0xffffffffu : 0u, 0};
+                }
+                hb[ib++] = bd;
+                lr.bytes += n.bytes + (bd.cover >= 0 ? 8.0 * kb->W : 0);
+            }
+        } else if (g.kind == NK_RESTRICT) {
+            lr.first_desc = ir;
+            const hedl_dir &dr = kb->dirs[g.key];
+            for (uint32_t k = g.first; k < g.first + g.count; ++k) {
+                const CNode &n = p->nodes[list[k]];
+                const uint32_t c = p->ops[n.op_begin];
+                RestrictDesc rd;
+                rd.child = ptr_of(c);
+                rd.out = need_row[k] ? rows + (size_t)slot[k] * kb->W4 : nullptr;
+                rd.cmask = ref_comp(c) ? 0xffffffffu : 0u;
+                rd.pred = n.pred;
+                rd.n = n.n;
+                rd.sat = n.sat;
+                rd.cover = cover_of_node[k];
+                rd.heavy_slot = (k - g.first) * dr.n_heavy;
+                hr[ir++] = rd;
+                lr.bytes += 4.0 * (kb->N + 1) + 4.0 * (dr.E - dr.E_heavy) + 8.0 * kb->W + (rd.cover >= 0 ? 8.0 * kb->W : 0);
+                lr.bytes2 += 4.0 * dr.E_heavy;
+            }
+        } else {
+            lr.first_desc = idr;
+            for (uint32_t k = g.first; k < g.first + g.count; ++k) {
+                const CNode &n = p->nodes[list[k]];
+                DrangeDesc dd;
+                dd.out = need_row[k] ? rows + (size_t)slot[k] * kb->W4 : nullptr;
+                dd.lo = n.lo;
+                dd.hi = n.hi;
+                dd.cover = cover_of_node[k];
+                dd.prop = n.dir;
+                hd[idr++] = dd;
+                lr.bytes += n.bytes + (dd.cover >= 0 ? 8.0 * kb->W : 0);
+            }
+        }
+        cp.recs.push_back(lr);
+    }
+    std::memcpy(h + cp.off_cov, cover_of_root.data(), nroots * sizeof(uint32_t));
+    if (out_bits) {
+        const uint32_t **hrows = (const uint32_t **)(h + cp.off_rows);
+        for (uint32_t k = 0; k < nroots; ++k) hrows[k] = rows + (size_t)slot[local[p->root_node[cp.ri + k]]] * kb->W4;
+    }
+}
+
+// Phase D: the launches of one chunk.
+hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, uint32_t r0, uint32_t *out_bits,
+                         hedl_counts *counts_dev, cudaStream_t s) {
+    const KbDev kd{kb->N, kb->W, kb->W4, kb->pos, kb->neg};
+    const char *d = (const char *)w->plan.dev + cp.blob_off;
+    const char *h = (const char *)w->plan.host + cp.blob_off;
+    hedl_counts *cov = (hedl_counts *)w->counts.p;
+    const uint32_t nroots = cp.rc - cp.ri;
+    launch_cover_init(s, cov, cp.ncov, kb->npos, kb->nneg);
+    for (const LaunchRec &lr : cp.recs) {
+        if (lr.kind == NK_AND) {
+            launch_bool(s, kd, (const BoolDesc *)(d + cp.off_bool) + lr.first_desc, lr.count,
+                        (const Operand *)(d + cp.off_ops), cov, lr.bytes);
+        } else if (lr.kind == NK_RESTRICT) {
+            const hedl_dir &dr = kb->dirs[lr.key];
+            const RestrictDesc *dd_desc = (const RestrictDesc *)(d + cp.off_res) + lr.first_desc;
+            if (lr.slice) {
+                hedl_status st = slice_run(kb, &w->slice.p, &w->slice.bytes, s, kd, lr.key,
+                                           (const RestrictDesc *)(h + cp.off_res) + lr.first_desc, dd_desc, lr.count, cov);
+                if (st) return st;
+            } else {
+                DirDev dd{dr.row_ptr, dr.col, dr.heavy_x, dr.heavy_nchunks, dr.chunks, dr.n_heavy, dr.n_chunks};
+                launch_restrict(s, kd, dd, dd_desc, lr.count, cov, (uint32_t *)w->heavy.p, lr.bytes, lr.bytes2);
+            }
+        } else {
+            const hedl_data &dp = kb->data[lr.key];
+            launch_drange(s, kd, dp.row_ptr, dp.val, (const DrangeDesc *)(d + cp.off_dr) + lr.first_desc, lr.count, cov,
+                          lr.bytes);
+        }
+    }
+    launch_gather_counts(s, cov, (const uint32_t *)(d + cp.off_cov), counts_dev + (cp.ri - r0), nroots);
+    if (out_bits)
+        launch_gather_bits(s, (const uint32_t *const *)(d + cp.off_rows), out_bits + (size_t)(cp.ri - r0) * kb->W, kb->W,
+                           nroots);
+    HEDL_CUDA(kb, cudaGetLastError());
+    return HEDL_OK;
+}
+
+// Evaluate roots [r0, r1) of the program.  counts_dev: device hedl_counts[r1-r0];
+// out_bits: device [r1-r0][W] or null.
+hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, uint32_t *out_bits,
+                hedl_counts *counts_dev, cudaStream_t s, uint32_t eflags) {
+    Workspace *w = ws_of(p);
+    if (w->used && w->last_stream != s && w->done) HEDL_CUDA(kb, cudaStreamWaitEvent(s, w->done, 0));
+    PlanCache &pc = w->plan;
+    const bool bits = out_bits != nullptr;
+    const bool hit = pc.valid && pc.r0 == r0 && pc.r1 == r1 && pc.bits == bits && pc.eflags == eflags &&
+                     pc.rows_base == w->rows.p && pc.heavy_base == w->heavy.p;
+    hedl_status st;
+    if (!hit) {
+        // the previous plan's blobs may still be read by queued work: wait, then reuse them
+        if (w->used && w->done) HEDL_CUDA(kb, cudaEventSynchronize(w->done));
+        invalidate_plan(pc);
+        const size_t row_bytes = (size_t)kb->W4 * 4;
+        if (!p->ws_limit) {            // default: half the free device memory, at most 48 GiB
+            size_t fr = 0, tot = 0;
+            cudaMemGetInfo(&fr, &tot);
+            p->ws_limit = std::max<uint64_t>(1ull << 28, std::min<uint64_t>(fr / 2, 48ull << 30));
+        }
+        const uint64_t row_cap = std::max<uint64_t>(1, row_bytes ? p->ws_limit / row_bytes : (1ull << 22));
+        const bool use_slice = !(eflags & HEDL_EVAL_PER_NODE) && slice_enabled(kb);
+        const bool force = eflags & HEDL_EVAL_FORCE_SLICE;
+        std::vector<std::vector<uint32_t>> lists;
+        std::vector<std::pair<uint32_t, uint32_t>> ranges;
+        const double t0 = now_ms();
+        collect_chunks(p, r0, r1, row_cap, lists, ranges);
+        const double t1 = now_ms();
+        // phase B: sizes of every chunk, then the buffers (pointers become final)
+        std::vector<uint32_t> local(p->nodes.size());
+        pc.chunks.resize(lists.size());
+        std::vector<ChunkTmp> tmps(lists.size());
+        size_t cursor = 0, heavy_need = 16, max_nn = 1, max_cov = 1;
+        for (size_t c = 0; c < lists.size(); ++c) {
+            ChunkPlan &cp = pc.chunks[c];
+            cp.ri = ranges[c].first;
+            cp.rc = ranges[c].second;
+            fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, nullptr, local, nullptr, &cursor, &heavy_need, true,
+                       tmps[c]);
+            max_nn = std::max<size_t>(max_nn, cp.nrows);
+            max_cov = std::max<size_t>(max_cov, cp.ncov);
+        }
+        if ((st = grow(kb, s, w->rows, max_nn * row_bytes + 16, false))) return st;
+        if ((st = grow(kb, s, w->heavy, heavy_need, true))) return st;
+        if ((st = grow(kb, s, w->counts, max_cov * sizeof(hedl_counts), false))) return st;
+        if ((st = reserve_plan(pc, std::max<size_t>(cursor, 256)))) return st;
+        const double t2 = now_ms();
+        pc.r0 = r0; pc.r1 = r1; pc.bits = bits; pc.eflags = eflags;
+        pc.rows_base = w->rows.p;
+        pc.heavy_base = w->heavy.p;
+        // phase C + D interleaved: fill chunk c on the host while chunk c-1 runs on the GPU
+        for (size_t c = 0; c < lists.size(); ++c) {
+            ChunkPlan &cp = pc.chunks[c];
+            size_t cur = cp.blob_off;
+            fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, (uint32_t *)w->rows.p, local, (char *)pc.host, &cur,
+                       &heavy_need, false, tmps[c]);
+            ChunkTmp().need_row.swap(tmps[c].need_row);   // release the chunk's planning state
+            std::vector<uint32_t>().swap(tmps[c].slot);
+            HEDL_CUDA(kb, cudaMemcpyAsync((char *)pc.dev + cp.blob_off, (char *)pc.host + cp.blob_off, cp.blob_bytes,
+                                          cudaMemcpyHostToDevice, s));
+            count_io(cp.blob_bytes, 0);
+            if ((st = launch_chunk(kb, w, cp, r0, out_bits, counts_dev, s))) { invalidate_plan(pc); return st; }
+        }
+        pc.valid = true;
+        timing_note("plan: collect chunks", t1 - t0);
+        timing_note("plan: sizes+buffers", t2 - t1);
+        timing_note("plan: fill+upload+launch", now_ms() - t2);
+    } else {
+        for (const ChunkPlan &cp : pc.chunks)
+            if ((st = launch_chunk(kb, w, cp, r0, out_bits, counts_dev, s))) return st;
     }
     if (!w->done) HEDL_CUDA(kb, cudaEventCreateWithFlags(&w->done, cudaEventDisableTiming));
     HEDL_CUDA(kb, cudaEventRecord(w->done, s));
@@ -365,20 +517,21 @@ extern "C" hedl_status hedl_eval_batch(const hedl_kb *kb, hedl_program *p, uint3
     DeviceGuard dg(kb->device);
     cudaStream_t s = (cudaStream_t)stream;
     hedl_counts *dcounts = counts;
-    DevBuf out_stage;
-    if (!(flags & HEDL_EVAL_COUNTS_DEVICE)) {
-        cudaError_t e = cudaMallocAsync(&out_stage.p, (size_t)n * sizeof(hedl_counts), s);
+    void *stage = nullptr;
+    const bool host_out = !(flags & HEDL_EVAL_COUNTS_DEVICE);
+    if (host_out) {
+        cudaError_t e = cudaMallocAsync(&stage, (size_t)n * sizeof(hedl_counts), s);
         if (e != cudaSuccess) { cudaGetLastError(); return fail(HEDL_ERR_OOM, "count staging allocation failed"); }
-        dcounts = (hedl_counts *)out_stage.p;
+        dcounts = (hedl_counts *)stage;
     }
-    hedl_status st = run(kb, p, first, first + n, out_bits, dcounts, s, flags);
-    if (!(flags & HEDL_EVAL_COUNTS_DEVICE)) {
+    hedl_status st = run(kb, p, first, first + n, out_bits, dcounts, s, flags & ~HEDL_EVAL_COUNTS_DEVICE);
+    if (host_out) {
         if (st == HEDL_OK) {
             cudaError_t e = cudaMemcpyAsync(counts, dcounts, (size_t)n * sizeof(hedl_counts), cudaMemcpyDeviceToHost, s);
             count_io(0, (uint64_t)n * sizeof(hedl_counts));
             if (e != cudaSuccess) st = cuda_fail(kb, e, "count D2H");
         }
-        cudaFreeAsync(out_stage.p, s);
+        cudaFreeAsync(stage, s);
         if (st == HEDL_OK) {
             cudaError_t e = cudaStreamSynchronize(s);
             if (e != cudaSuccess) st = cuda_fail(kb, e, "eval_batch sync");
@@ -399,12 +552,9 @@ extern "C" hedl_status hedl_program_free(hedl_program *p) {
         Workspace *w = (Workspace *)p->ws;
         DeviceGuard dg(p->kb->device);
         if (w->done) cudaEventSynchronize(w->done);
-        for (DevBuf *b : {&w->rows, &w->heavy, &w->desc, &w->counts, &w->slice})
+        for (DevBuf *b : {&w->rows, &w->heavy, &w->counts, &w->slice})
             if (b->p) cudaFree(b->p);
-        for (int i = 0; i < 2; ++i) {
-            if (w->pinned[i]) cudaFreeHost(w->pinned[i]);
-            if (w->pinned_ev[i]) cudaEventDestroy(w->pinned_ev[i]);
-        }
+        release_plan(w->plan);
         if (w->done) cudaEventDestroy(w->done);
         delete w;
     }
@@ -414,6 +564,12 @@ extern "C" hedl_status hedl_program_free(hedl_program *p) {
 
 extern "C" hedl_status hedl_program_set_workspace_limit(hedl_program *p, uint64_t bytes) {
     if (!p || bytes < (1u << 20)) return fail(HEDL_ERR_INVALID_ARG, "null program or limit < 1 MiB");
+    std::lock_guard<std::mutex> lk(p->mu);
     p->ws_limit = bytes;
+    if (p->ws) {
+        Workspace *w = (Workspace *)p->ws;
+        if (w->done) cudaEventSynchronize(w->done);
+        invalidate_plan(w->plan);
+    }
     return HEDL_OK;
 }

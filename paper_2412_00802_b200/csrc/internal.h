@@ -112,7 +112,7 @@ struct hedl_program {
     size_t ws_bytes = 0;
     void *pinned = nullptr;
     size_t pinned_bytes = 0;
-    uint64_t ws_limit = 8ull << 30;
+    uint64_t ws_limit = 0;              // 0 = auto (half the free memory, <= 48 GiB)
     // planning scratch (host)
     std::vector<uint32_t> stamp;
     uint32_t stamp_gen = 0;
@@ -130,6 +130,11 @@ hedl_status cuda_fail(const hedl_kb *kb, cudaError_t e, const char *where);
         cudaError_t _e = (call);                             \
         if (_e != cudaSuccess) return hedl::cuda_fail(kb, _e, #call); \
     } while (0)
+
+// ---- host phase timing (HEDL_TIMING=1 prints to stderr) ---------------------------
+bool timing_enabled();
+double now_ms();
+void timing_note(const char *what, double ms);
 
 // ---- profiling -----------------------------------------------------------------
 enum KClass { KC_BOOL, KC_RESTRICT, KC_HEAVY, KC_DRANGE, KC_COVER_INIT, KC_GATHER,

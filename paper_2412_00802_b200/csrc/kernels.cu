@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(256) k_bool(KbDev kb, const BoolDesc *__restri
         acc.y = tail_word(acc.y, w0 + 1, kb.W, kb.N);
         acc.z = tail_word(acc.z, w0 + 2, kb.W, kb.N);
         acc.w = tail_word(acc.w, w0 + 3, kb.W, kb.N);
-        reinterpret_cast<uint4 *>(d.out)[i] = acc;
+        if (d.out) reinterpret_cast<uint4 *>(d.out)[i] = acc;   // null: root needed for counts only
         if (d.cover >= 0) {
             const uint4 p = __ldg(reinterpret_cast<const uint4 *>(kb.pos) + i);
             const uint4 q = __ldg(reinterpret_cast<const uint4 *>(kb.neg) + i);
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) k_restrict(KbDev kb, DirDev dir, const Re
             word = __ballot_sync(FULL, res);
         }
         if (lane == 0) {
-            d.out[w] = word;
+            if (d.out) d.out[w] = word;
             if (d.cover >= 0) {
                 tp = __popc(word & __ldg(kb.pos + w));
                 fp = __popc(word & __ldg(kb.neg + w));
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(256) k_restrict_heavy(KbDev kb, DirDev dir, co
         const uint32_t x = __ldg(dir.heavy_x + ch.x);
         if (pred_eval(d.pred, min(tot, d.sat), d.n)) {
             const uint32_t bit = 1u << (x & 31);
-            atomicOr(d.out + (x >> 5), bit);
+            if (d.out) atomicOr(d.out + (x >> 5), bit);
             if (d.cover >= 0) {
                 hedl_counts *cc = counts + d.cover;
                 if (__ldg(kb.pos + (x >> 5)) & bit) {
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(256) k_drange(KbDev kb, const uint32_t *__rest
             word = __ballot_sync(FULL, res);
         }
         if (lane == 0) {
-            d.out[w] = word;
+            if (d.out) d.out[w] = word;
             if (d.cover >= 0) {
                 tp = __popc(word & __ldg(kb.pos + w));
                 fp = __popc(word & __ldg(kb.neg + w));

@@ -89,38 +89,41 @@ __device__ void build_consts(PackConst &pc, const RestrictDesc *__restrict__ d, 
     __syncthreads();
 }
 
+// A thread owns HW = 4 words (128 lanes) of a row: the two threads of an
+// adjacent lane pair (lane & 1 = half) cover the 256 lanes and gather the two
+// 16 B halves of one 32 B sector of T[y] with one warp instruction.
+constexpr int HW = 4;
+
 template <bool COUNT>
 struct Acc {
-    uint32_t c[COUNT ? NPL : 1][LW];
+    uint32_t c[COUNT ? NPL : 1][HW];
     __device__ __forceinline__ void zero() {
 #pragma unroll
         for (int q = 0; q < (COUNT ? NPL : 1); ++q)
 #pragma unroll
-            for (int k = 0; k < LW; ++k) c[q][k] = 0;
+            for (int k = 0; k < HW; ++k) c[q][k] = 0;
     }
-    __device__ __forceinline__ void add(const uint32_t (&v)[LW]) {
+    __device__ __forceinline__ void add1(int k, uint32_t v) {
+        if (!COUNT) {
+            c[0][k] |= v;
+        } else {
+            uint32_t s = FULL;
 #pragma unroll
-        for (int k = 0; k < LW; ++k) {
-            if (!COUNT) {
-                c[0][k] |= v[k];
-            } else {
-                uint32_t s = FULL;
+            for (int q = 0; q < NPL; ++q) s &= c[q][k];
+            uint32_t carry = v & ~s;            // saturated lanes stay at 31
 #pragma unroll
-                for (int q = 0; q < NPL; ++q) s &= c[q][k];
-                uint32_t carry = v[k] & ~s;     // saturated lanes stay at 31
-#pragma unroll
-                for (int q = 0; q < NPL; ++q) {
-                    const uint32_t t = c[q][k] & carry;
-                    c[q][k] ^= carry;
-                    carry = t;
-                }
+            for (int q = 0; q < NPL; ++q) {
+                const uint32_t t = c[q][k] & carry;
+                c[q][k] ^= carry;
+                carry = t;
             }
         }
     }
+    __device__ __forceinline__ void add(const uint4 v) { add1(0, v.x); add1(1, v.y); add1(2, v.z); add1(3, v.w); }
     // saturating add of another accumulator (bit-sliced ripple-carry adder)
     __device__ __forceinline__ void merge(const Acc &o) {
 #pragma unroll
-        for (int k = 0; k < LW; ++k) {
+        for (int k = 0; k < HW; ++k) {
             if (!COUNT) {
                 c[0][k] |= o.c[0][k];
             } else {
@@ -136,72 +139,76 @@ struct Acc {
             }
         }
     }
-    __device__ __forceinline__ void warp_reduce() {
-        if (!COUNT) {
+    // combine the 16 pairs of a warp (lanes of equal parity); every lane gets its half's total
+    __device__ __forceinline__ void warp_reduce_pairs() {
 #pragma unroll
-            for (int k = 0; k < LW; ++k) c[0][k] = __reduce_or_sync(FULL, c[0][k]);
-        } else {
+        for (int off = 16; off >= 2; off >>= 1) {
+            Acc o;
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                Acc o;
+            for (int q = 0; q < (COUNT ? NPL : 1); ++q)
 #pragma unroll
-                for (int q = 0; q < NPL; ++q)
-#pragma unroll
-                    for (int k = 0; k < LW; ++k) o.c[q][k] = __shfl_xor_sync(FULL, c[q][k], off);
-                merge(o);
-            }
+                for (int k = 0; k < HW; ++k) o.c[q][k] = __shfl_xor_sync(FULL, c[q][k], off);
+            merge(o);
         }
     }
-    __device__ __forceinline__ uint32_t result(const PackConst &pc, int k) const {
-        if (!COUNT) return ((c[0][k] ^ pc.fl[k]) & pc.am[k]) | pc.om[k];
+    __device__ __forceinline__ uint32_t result(const PackConst &pc, int kk, int k) const {
+        if (!COUNT) return ((c[0][k] ^ pc.fl[kk]) & pc.am[kk]) | pc.om[kk];
         uint32_t gt = 0, eq = FULL, nz = 0;
 #pragma unroll
         for (int q = NPL - 1; q >= 0; --q) {
-            const uint32_t cq = c[q][k], nq = pc.nb[q][k];
+            const uint32_t cq = c[q][k], nq = pc.nb[q][kk];
             gt |= eq & cq & ~nq;
             eq &= ~(cq ^ nq);
             nz |= cq;
         }
         const uint32_t ge = gt | eq, le = ~gt;
-        return (ge & pc.mge[k]) | (le & pc.mle[k]) | (eq & pc.meq[k]) | (le & nz & pc.mlep[k]);
+        return (ge & pc.mge[kk]) | (le & pc.mle[kk]) | (eq & pc.meq[kk]) | (le & nz & pc.mlep[kk]);
     }
 };
 
-__device__ __forceinline__ void gather(const uint4 *__restrict__ T, uint32_t y, uint32_t (&v)[LW]) {
-    const uint4 a = __ldg(T + 2ull * y), b = __ldg(T + 2ull * y + 1);
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+// acc += T[y] (this thread's half) for the edges [e, b) with stride `step`, 4 gathers in flight
+template <bool COUNT>
+__device__ __forceinline__ void scan_edges(Acc<COUNT> &acc, const uint32_t *__restrict__ col, const uint4 *__restrict__ T,
+                                           uint32_t e, uint32_t b, uint32_t step, uint32_t half) {
+    for (; e + 3 * step < b; e += 4 * step) {
+        const uint32_t y0 = __ldg(col + e), y1 = __ldg(col + e + step);
+        const uint32_t y2 = __ldg(col + e + 2 * step), y3 = __ldg(col + e + 3 * step);
+        const uint4 v0 = __ldg(T + 2ull * y0 + half), v1 = __ldg(T + 2ull * y1 + half);
+        const uint4 v2 = __ldg(T + 2ull * y2 + half), v3 = __ldg(T + 2ull * y3 + half);
+        acc.add(v0);
+        acc.add(v1);
+        acc.add(v2);
+        acc.add(v3);
+    }
+    for (; e < b; e += step) acc.add(__ldg(T + 2ull * __ldg(col + e) + half));
 }
 
 // ------------------------------------------------------------------------------
-// T[y] for the pack: warp per 8 consecutive words (256 individuals).
+// T[y] for the pack: warp per 4 consecutive words (128 individuals).
 __global__ void __launch_bounds__(256) k_slice_pack(KbDev kb, const RestrictDesc *__restrict__ d, uint32_t count,
                                                     uint4 *__restrict__ T) {
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t w0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 8;
+    const uint32_t w0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 4;
     if (w0 >= kb.W4) return;
-    uint32_t v[LW][8];
+    uint4 v[LW];
 #pragma unroll
     for (int g = 0; g < LW; ++g) {
         const uint32_t j = g * 32 + lane;
-        uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
+        v[g] = make_uint4(0, 0, 0, 0);
         if (j < count) {
             const RestrictDesc r = d[j];
-            const uint4 *row = reinterpret_cast<const uint4 *>(r.child + w0);
-            a = __ldg(row);
-            if (w0 + 4 < kb.W4) b = __ldg(row + 1);
-            a.x ^= r.cmask; a.y ^= r.cmask; a.z ^= r.cmask; a.w ^= r.cmask;
-            b.x ^= r.cmask; b.y ^= r.cmask; b.z ^= r.cmask; b.w ^= r.cmask;
+            v[g] = __ldg(reinterpret_cast<const uint4 *>(r.child + w0));
+            v[g].x ^= r.cmask; v[g].y ^= r.cmask; v[g].z ^= r.cmask; v[g].w ^= r.cmask;
         }
-        v[g][0] = a.x; v[g][1] = a.y; v[g][2] = a.z; v[g][3] = a.w;
-        v[g][4] = b.x; v[g][5] = b.y; v[g][6] = b.z; v[g][7] = b.w;
     }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        if (w0 + k >= kb.W4) break;
+    for (int k = 0; k < 4; ++k) {
         uint32_t o[LW];
 #pragma unroll
-        for (int g = 0; g < LW; ++g) o[g] = warp_transpose(v[g][k], lane);
+        for (int g = 0; g < LW; ++g) {
+            const uint32_t x = k == 0 ? v[g].x : k == 1 ? v[g].y : k == 2 ? v[g].z : v[g].w;
+            o[g] = warp_transpose(x, lane);
+        }
         const uint64_t y = (uint64_t)(w0 + k) * 32 + lane;
         T[2 * y] = make_uint4(o[0], o[1], o[2], o[3]);
         T[2 * y + 1] = make_uint4(o[4], o[5], o[6], o[7]);
@@ -209,51 +216,47 @@ __global__ void __launch_bounds__(256) k_slice_pack(KbDev kb, const RestrictDesc
 }
 
 // ------------------------------------------------------------------------------
-// heavy rows: CTA (128 threads) per chunk of <= kHeavyChunk edges.
+// heavy rows: CTA (256 threads = 128 lane pairs) per chunk of <= kHeavyChunk edges.
 template <bool COUNT>
-__global__ void __launch_bounds__(128) k_slice_heavy(SliceDir dir, SliceScratch sc, const RestrictDesc *__restrict__ d,
+__global__ void __launch_bounds__(256) k_slice_heavy(SliceDir dir, SliceScratch sc, const RestrictDesc *__restrict__ d,
                                                      uint32_t count) {
     __shared__ PackConst pc;
-    __shared__ uint32_t red[4][COUNT ? NPL : 1][LW];
-    __shared__ uint32_t fin[COUNT ? NPL : 1][LW];
+    __shared__ uint32_t red[8][2][COUNT ? NPL : 1][HW];
+    __shared__ uint32_t fin[2][COUNT ? NPL : 1][HW];
+    __shared__ uint32_t outw[LW];
     __shared__ uint32_t s_last;
     const uint4 ch = dir.chunks[blockIdx.x];
     const uint32_t h = ch.x;
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, half = lane & 1;
     Acc<COUNT> acc;
     acc.zero();
-    uint32_t v[LW];
-    for (uint32_t e = ch.y + threadIdx.x; e < ch.z; e += 128) {
-        gather(sc.T, __ldg(dir.col + e), v);
-        acc.add(v);
-    }
-    acc.warp_reduce();
-    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (lane == 0)
+    scan_edges<COUNT>(acc, dir.col, sc.T, ch.y + (threadIdx.x >> 1), ch.z, 128, half);
+    acc.warp_reduce_pairs();
+    if (lane < 2)
         for (int q = 0; q < (COUNT ? NPL : 1); ++q)
-            for (int k = 0; k < LW; ++k) red[wid][q][k] = acc.c[q][k];
+            for (int k = 0; k < HW; ++k) red[wid][half][q][k] = acc.c[q][k];
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        Acc<COUNT> a, b;
+        for (int q = 0; q < (COUNT ? NPL : 1); ++q) for (int k = 0; k < HW; ++k) a.c[q][k] = red[0][threadIdx.x][q][k];
+        for (int w = 1; w < 8; ++w) {
+            for (int q = 0; q < (COUNT ? NPL : 1); ++q) for (int k = 0; k < HW; ++k) b.c[q][k] = red[w][threadIdx.x][q][k];
+            a.merge(b);
+        }
+        for (int q = 0; q < (COUNT ? NPL : 1); ++q) for (int k = 0; k < HW; ++k) fin[threadIdx.x][q][k] = a.c[q][k];
+    }
     __syncthreads();
     if (!COUNT) {
         if (threadIdx.x < LW) {
-            const uint32_t x = red[0][0][threadIdx.x] | red[1][0][threadIdx.x] | red[2][0][threadIdx.x] | red[3][0][threadIdx.x];
+            const uint32_t x = fin[threadIdx.x >> 2][0][threadIdx.x & 3];
             if (x) atomicOr(sc.hacc + (size_t)h * LW + threadIdx.x, x);
         }
     } else {
-        if (threadIdx.x == 0) {
-            Acc<true> a, b;
-            for (int q = 0; q < NPL; ++q) for (int k = 0; k < LW; ++k) a.c[q][k] = red[0][q][k];
-            for (int w = 1; w < 4; ++w) {
-                for (int q = 0; q < NPL; ++q) for (int k = 0; k < LW; ++k) b.c[q][k] = red[w][q][k];
-                a.merge(b);
-            }
-            for (int q = 0; q < NPL; ++q) for (int k = 0; k < LW; ++k) fin[q][k] = a.c[q][k];
-        }
-        __syncthreads();
-        for (uint32_t L = threadIdx.x; L < 256; L += 128) {
-            const uint32_t k = L >> 5, bit = L & 31;
-            uint32_t val = 0;
-            for (int q = 0; q < NPL; ++q) val |= ((fin[q][k] >> bit) & 1u) << q;
-            if (val) atomicAdd(sc.hcnt + (size_t)h * 256 + L, val);
-        }
+        const uint32_t L = threadIdx.x;                 // lane of the pack: half, word, bit
+        const uint32_t hh = L >> 7, k = (L >> 5) & 3, bit = L & 31;
+        uint32_t val = 0;
+        for (int q = 0; q < NPL; ++q) val |= ((fin[hh][q][k] >> bit) & 1u) << q;
+        if (val) atomicAdd(sc.hcnt + (size_t)h * 256 + L, val);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -272,23 +275,21 @@ __global__ void __launch_bounds__(128) k_slice_heavy(SliceDir dir, SliceScratch 
             sc.hout[(size_t)h * LW + k] = ((a ^ pc.fl[k]) & pc.am[k]) | pc.om[k];
         }
     } else {
-        __shared__ uint32_t outw[LW];
         if (threadIdx.x < LW) outw[threadIdx.x] = 0;
         __syncthreads();
-        for (uint32_t L = threadIdx.x; L < 256; L += 128) {
-            uint32_t c = atomicExch(sc.hcnt + (size_t)h * 256 + L, 0u);
-            c = c > 31u ? 31u : c;
-            const uint32_t k = L >> 5, bit = 1u << (L & 31);
-            uint32_t n = 0;
-            for (int q = 0; q < NPL; ++q) n |= ((pc.nb[q][k] & bit) ? 1u : 0u) << q;
-            bool r;
-            if (pc.mge[k] & bit) r = c >= n;
-            else if (pc.mle[k] & bit) r = c <= n;
-            else if (pc.meq[k] & bit) r = c == n;
-            else if (pc.mlep[k] & bit) r = c > 0 && c <= n;
-            else r = false;
-            if (r) atomicOr(&outw[k], bit);
-        }
+        const uint32_t L = threadIdx.x;
+        uint32_t c = atomicExch(sc.hcnt + (size_t)h * 256 + L, 0u);
+        c = c > 31u ? 31u : c;
+        const uint32_t k = L >> 5, bit = 1u << (L & 31);
+        uint32_t n = 0;
+        for (int q = 0; q < NPL; ++q) n |= ((pc.nb[q][k] & bit) ? 1u : 0u) << q;
+        bool r;
+        if (pc.mge[k] & bit) r = c >= n;
+        else if (pc.mle[k] & bit) r = c <= n;
+        else if (pc.meq[k] & bit) r = c == n;
+        else if (pc.mlep[k] & bit) r = c > 0 && c <= n;
+        else r = false;
+        if (r) atomicOr(&outw[k], bit);
         __syncthreads();
         if (threadIdx.x < LW) sc.hout[(size_t)h * LW + threadIdx.x] = outw[threadIdx.x];
     }
@@ -296,17 +297,17 @@ __global__ void __launch_bounds__(128) k_slice_heavy(SliceDir dir, SliceScratch 
 }
 
 // ------------------------------------------------------------------------------
-// tile of 1024 consecutive individuals per CTA (256 threads).
+// tile of 1024 consecutive individuals per CTA (256 threads = 128 lane pairs).
 template <bool COUNT>
-__global__ void __launch_bounds__(256) k_slice_tile(KbDev kb, SliceDir dir, SliceScratch sc,
-                                                    const RestrictDesc *__restrict__ d, uint32_t count,
-                                                    hedl_counts *counts) {
+__global__ void __launch_bounds__(256, COUNT ? 3 : 4) k_slice_tile(KbDev kb, SliceDir dir, SliceScratch sc,
+                                                                   const RestrictDesc *__restrict__ d, uint32_t count,
+                                                                   hedl_counts *counts) {
     extern __shared__ uint32_t smem[];
     PackConst &pc = *reinterpret_cast<PackConst *>(smem);
     uint32_t *ot = smem + sizeof(PackConst) / 4;          // [1024][TROW]
     const uint32_t t = blockIdx.x;
     const uint32_t x0 = t * 1024;
-    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, half = lane & 1;
     for (uint32_t i = threadIdx.x; i < 1024 * TROW; i += 256) ot[i] = 0;
     build_consts(pc, d, count);                           // (contains __syncthreads)
     const uint4 ti = dir.tiles[t];
@@ -316,46 +317,28 @@ __global__ void __launch_bounds__(256) k_slice_tile(KbDev kb, SliceDir dir, Slic
 #pragma unroll
         for (int k = 0; k < LW; ++k) ot[xl * TROW + k] = sc.hout[(size_t)h * LW + k];
     }
-    uint32_t v[LW];
-    // medium rows: warp per row
+    // medium rows: warp per row, the 16 lane pairs split its neighbours
     for (uint32_t m = wid; m < ti.y; m += 8) {
         const uint32_t x = __ldg(dir.order + ti.x + m);
         const uint32_t a = __ldg(dir.row_ptr + x), b = __ldg(dir.row_ptr + x + 1);
         Acc<COUNT> acc;
         acc.zero();
-        for (uint32_t e = a + lane; e < b; e += 32) {
-            gather(sc.T, __ldg(dir.col + e), v);
-            acc.add(v);
-        }
-        acc.warp_reduce();
-        if (lane < LW) {
-            uint32_t r = 0;
+        scan_edges<COUNT>(acc, dir.col, sc.T, a + (lane >> 1), b, 16, half);
+        acc.warp_reduce_pairs();
+        if (lane < 2) {
 #pragma unroll
-            for (int k = 0; k < LW; ++k) if (k == (int)lane) r = acc.result(pc, k);
-            ot[(x - x0) * TROW + lane] = r;
+            for (int k = 0; k < HW; ++k) ot[(x - x0) * TROW + half * HW + k] = acc.result(pc, half * HW + k, k);
         }
     }
-    // light rows: thread per row (rows sorted by degree, so a warp's trip counts agree)
-    for (uint32_t l = threadIdx.x; l < ti.z; l += 256) {
+    // light rows: lane pair per row (rows sorted by degree, so a warp's trip counts agree)
+    for (uint32_t l = threadIdx.x >> 1; l < ti.z; l += 128) {
         const uint32_t x = __ldg(dir.order + ti.x + ti.y + l);
         const uint32_t a = __ldg(dir.row_ptr + x), b = __ldg(dir.row_ptr + x + 1);
         Acc<COUNT> acc;
         acc.zero();
-        uint32_t e = a;
-        for (; e + 1 < b; e += 2) {
-            uint32_t v2[LW];
-            const uint32_t y0 = __ldg(dir.col + e), y1 = __ldg(dir.col + e + 1);
-            gather(sc.T, y0, v);
-            gather(sc.T, y1, v2);
-            acc.add(v);
-            acc.add(v2);
-        }
-        if (e < b) {
-            gather(sc.T, __ldg(dir.col + e), v);
-            acc.add(v);
-        }
+        scan_edges<COUNT>(acc, dir.col, sc.T, a, b, 1, half);
 #pragma unroll
-        for (int k = 0; k < LW; ++k) ot[(x - x0) * TROW + k] = acc.result(pc, k);
+        for (int k = 0; k < HW; ++k) ot[(x - x0) * TROW + half * HW + k] = acc.result(pc, half * HW + k, k);
     }
     __syncthreads();
     // transpose back: warp g writes lanes 32g..32g+31 (node rows), 4 words per store
@@ -372,7 +355,7 @@ __global__ void __launch_bounds__(256) k_slice_tile(KbDev kb, SliceDir dir, Slic
 #pragma unroll
         for (int q = 0; q < 4; ++q) o[q] = warp_transpose(ot[((wl + q) * 32 + lane) * TROW + g], lane);
         if (live) {
-            *reinterpret_cast<uint4 *>(r.out + w) = make_uint4(o[0], o[1], o[2], o[3]);
+            if (r.out) *reinterpret_cast<uint4 *>(r.out + w) = make_uint4(o[0], o[1], o[2], o[3]);
             if (r.cover >= 0) {
                 const uint4 p = __ldg(reinterpret_cast<const uint4 *>(kb.pos + w));
                 const uint4 n = __ldg(reinterpret_cast<const uint4 *>(kb.neg + w));
@@ -440,6 +423,8 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
     if (!attr_set) {
         cudaFuncSetAttribute(k_slice_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_slice_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_slice_tile<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_slice_tile<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr_set = true;
     }
     const double csr = 4.0 * (kb->N + 1) + 4.0 * dr.E;
@@ -451,13 +436,13 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             ++cnt;
         const RestrictDesc *dd = d_desc + off;
         prof_begin(s, KC_SLICE_IN);
-        k_slice_pack<<<cdiv(kb->W4, 64), 256, 0, s>>>(kd, dd, cnt, sc.T);
+        k_slice_pack<<<cdiv(kb->W4, 32), 256, 0, s>>>(kd, dd, cnt, sc.T);
         count_launch();
         prof_end(s, KC_SLICE_IN, 4.0 * kb->W * cnt + 32.0 * 32 * kb->W4);
         if (dr.n_chunks) {
             prof_begin(s, KC_SLICE_HEAVY);
-            if (cls == 0) k_slice_heavy<false><<<dr.n_chunks, 128, 0, s>>>(sd, sc, dd, cnt);
-            else k_slice_heavy<true><<<dr.n_chunks, 128, 0, s>>>(sd, sc, dd, cnt);
+            if (cls == 0) k_slice_heavy<false><<<dr.n_chunks, 256, 0, s>>>(sd, sc, dd, cnt);
+            else k_slice_heavy<true><<<dr.n_chunks, 256, 0, s>>>(sd, sc, dd, cnt);
             count_launch();
             prof_end(s, KC_SLICE_HEAVY, 4.0 * dr.E_heavy + 32.0 * dr.E_heavy);
         }

@@ -209,3 +209,28 @@ def test_errors_gpu():
     with pytest.raises(hedl.HedlError) as e:
         hedl.hedl_kb_load(bad, 0)
     assert e.value.code == 3
+
+
+def test_parallel_compile_equivalent():
+    """Sharded compile + lock-free merge (hedl_compile) == single-threaded compile, node for node in count,
+    and both equal the oracle; duplicates across shards are merged (global CSE)."""
+    import os
+    hedl = _hedl()
+    kb = abox.powerlaw_kb(30_000, 20, 2, 8.0, 2_000, 0.7, 1.0, 0.02, 31)
+    arrays = hyps.batch_arrays("c4", kb, 40_000, 31, chunk=10_000, workers=4)
+    nodes, kids, roots = arrays
+    k = hedl.hedl_kb_load(kb, 0)
+    infos, outs = [], []
+    for threads in ("1", "5", "16"):
+        os.environ["HEDL_COMPILE_THREADS"] = threads
+        try:
+            prog = hedl.hedl_compile(k, nodes, kids, roots)
+        finally:
+            del os.environ["HEDL_COMPILE_THREADS"]
+        infos.append(prog.info())
+        outs.append(hedl.hedl_eval_batch(k, prog, 0, len(roots))[1])
+    assert infos[0]["n_nodes"] == infos[1]["n_nodes"] == infos[2]["n_nodes"]
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    sample = np.arange(0, len(roots), 37)
+    _, oc = setsem.evaluate(kb, nodes, kids, roots[sample], threads=8, want_bits=False)
+    assert np.array_equal(outs[1][sample], oc)
