@@ -28,13 +28,14 @@ struct LaunchRec {
     uint8_t kind;          // NK_AND (AND+OR), NK_RESTRICT, NK_DRANGE
     uint16_t key;          // dir / prop
     bool slice;
+    bool proj;             // boolean group evaluated on example-projected rows
     uint32_t count, first_desc;
     double bytes, bytes2;
 };
 
 struct ChunkPlan {
     uint32_t ri, rc;       // roots [ri, rc) relative to the program
-    uint32_t nn, ncov, nrows;
+    uint32_t nn, ncov, nrows, nprows;
     size_t blob_off, blob_bytes;          // into PlanCache host/device blobs
     size_t off_bool, off_ops, off_res, off_dr, off_cov, off_rows;
     std::vector<LaunchRec> recs;
@@ -44,7 +45,7 @@ struct PlanCache {
     bool valid = false;
     uint32_t r0 = 0, r1 = 0, eflags = 0;
     bool bits = false;
-    void *rows_base = nullptr, *heavy_base = nullptr;
+    void *rows_base = nullptr, *heavy_base = nullptr, *prows_base = nullptr;
     std::vector<ChunkPlan> chunks;
     void *host = nullptr;                 // pinned descriptor blob
     void *dev = nullptr;                  // device descriptor blob
@@ -52,7 +53,7 @@ struct PlanCache {
 };
 
 struct Workspace {
-    DevBuf rows, heavy, counts, slice;
+    DevBuf rows, prows, heavy, counts, slice;
     PlanCache plan;
     cudaEvent_t done = nullptr;
     cudaStream_t last_stream = nullptr;
@@ -118,8 +119,9 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct Group {
     uint8_t kind;
     uint16_t key;
-    uint32_t first, count;
+    uint32_t first, count;   // into ChunkTmp::members (positions in the chunk list)
     bool slice = false;
+    bool proj = false;
 };
 
 // ---- planning -------------------------------------------------------------------
@@ -199,118 +201,164 @@ void collect_chunks(hedl_program *p, uint32_t r0, uint32_t r1, uint64_t row_cap,
 }
 
 struct ChunkTmp {            // per-chunk planning state kept between the sizing and filling passes
-    std::vector<uint32_t> slot, cover_of_root;
+    std::vector<uint32_t> slot, pslot, cover_of_root, members;
     std::vector<int32_t> cover_of_node;
-    std::vector<uint8_t> need_row;
+    std::vector<uint8_t> need_full, need_proj, pmode;
     std::vector<Group> groups;
 };
 
 // Phase C: descriptors of one chunk into `h` (host blob) with device addresses.
 // Called twice: sizes_only (fills tmp and the blob layout), then with the final buffers.
+//
+// Example projection: coverage only reads bits at P u N.  A boolean
+// node nobody needs in full (e.g. a root conjunction) runs on example-projected
+// rows (M bits instead of N); its operands then only need projected rows, which
+// atoms/TOP have precomputed and computed nodes emit as a scatter epilogue.
 void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> &list, ChunkPlan &cp,
-                bool out_bits, bool use_slice, bool force_slice, uint32_t *rows, std::vector<uint32_t> &local,
-                char *h_blob, size_t *blob_cursor, size_t *heavy_need, bool sizes_only, ChunkTmp &tmp) {
+                bool out_bits, bool use_slice, bool force_slice, uint32_t *rows, uint32_t *prows,
+                std::vector<uint32_t> &local, char *h_blob, size_t *blob_cursor, size_t *heavy_need, bool sizes_only,
+                ChunkTmp &tmp) {
     const uint32_t nn = (uint32_t)list.size();
     cp.nn = nn;
     for (uint32_t k = 0; k < nn; ++k) local[list[k]] = k;
     const uint32_t nroots = cp.rc - cp.ri;
-    std::vector<uint8_t> &need_row = tmp.need_row;
-    std::vector<uint32_t> &slot = tmp.slot;
-    std::vector<int32_t> &cover_of_node = tmp.cover_of_node;
-    std::vector<uint32_t> &cover_of_root = tmp.cover_of_root;
-    std::vector<Group> &groups = tmp.groups;
+    auto &need_full = tmp.need_full;
+    auto &need_proj = tmp.need_proj;
+    auto &pmode = tmp.pmode;
+    auto &slot = tmp.slot;
+    auto &pslot = tmp.pslot;
+    auto &cover_of_node = tmp.cover_of_node;
+    auto &cover_of_root = tmp.cover_of_root;
+    auto &groups = tmp.groups;
+    auto &members = tmp.members;
     if (sizes_only) {
-    need_row.assign(nn, 0);
-    for (uint32_t k = 0; k < nn; ++k) {
-        const CNode &n = p->nodes[list[k]];
-        for (uint32_t q = 0; q < n.op_count; ++q) {
-            const uint32_t o = p->ops[n.op_begin + q];
-            if (ref_type(o) == RT_NODE) need_row[local[ref_id(o)]] = 1;
+        cover_of_node.assign(nn, -1);
+        cover_of_root.resize(nroots);
+        uint32_t ncov = 0;
+        for (uint32_t k = 0; k < nroots; ++k) {
+            const uint32_t li = local[p->root_node[cp.ri + k]];
+            if (cover_of_node[li] < 0) cover_of_node[li] = (int32_t)ncov++;
+            cover_of_root[k] = (uint32_t)cover_of_node[li];
         }
-    }
-    if (out_bits)
-        for (uint32_t k = 0; k < nroots; ++k) need_row[local[p->root_node[cp.ri + k]]] = 1;
-    slot.assign(nn, 0);
-    uint32_t nrows = 0;
-    for (uint32_t k = 0; k < nn; ++k)
-        if (need_row[k]) slot[k] = nrows++;
-    cp.nrows = nrows;
-    cover_of_node.assign(nn, -1);
-    cover_of_root.resize(nroots);
-    uint32_t ncov = 0;
-    for (uint32_t k = 0; k < nroots; ++k) {
-        const uint32_t li = local[p->root_node[cp.ri + k]];
-        if (cover_of_node[li] < 0) cover_of_node[li] = (int32_t)ncov++;
-        cover_of_root[k] = (uint32_t)cover_of_node[li];
-    }
-    cp.ncov = ncov;
-    groups.clear();
-    for (uint32_t k = 0; k < nn;) {
-        const CNode &a = p->nodes[list[k]];
-        const uint8_t kind = (a.kind == NK_OR) ? NK_AND : a.kind;   // AND and OR share a launch
-        const uint16_t key = (kind == NK_AND) ? 0 : a.dir;
-        uint32_t e = k + 1;
-        while (e < nn) {
-            const CNode &b = p->nodes[list[e]];
-            const uint8_t kb2 = (b.kind == NK_OR) ? NK_AND : b.kind;
-            if (b.level != a.level || kb2 != kind || (kind != NK_AND && b.dir != key)) break;
-            ++e;
-        }
-        Group g{kind, key, k, e - k};
-        if (use_slice && kind == NK_RESTRICT) {
-            uint32_t ns = 0;   // leading lane-packable nodes (class 0/1 sort first)
-            while (ns < g.count) {
-                const CNode &c = p->nodes[list[k + ns]];
-                if (slice_class(c.pred, c.n, c.sat) == 2) break;
-                ++ns;
+        cp.ncov = ncov;
+        // demands, consumers first (the list is in ascending level order)
+        need_full.assign(nn, 0);
+        need_proj.assign(nn, 0);
+        pmode.assign(nn, 0);
+        if (out_bits)
+            for (uint32_t k = 0; k < nroots; ++k) need_full[local[p->root_node[cp.ri + k]]] = 1;
+        for (uint32_t k = nn; k-- > 0;) {
+            const CNode &n = p->nodes[list[k]];
+            const bool isbool = n.kind == NK_AND || n.kind == NK_OR;
+            pmode[k] = isbool && !need_full[k];
+            for (uint32_t q = 0; q < n.op_count; ++q) {
+                const uint32_t o = p->ops[n.op_begin + q];
+                if (ref_type(o) != RT_NODE) continue;
+                if (pmode[k]) need_proj[local[ref_id(o)]] = 1;
+                else need_full[local[ref_id(o)]] = 1;
             }
-            if (ns && slice_worthwhile(kb, ns, force_slice)) {
-                if (ns < g.count) {
-                    Group g1{kind, key, k, ns};
-                    g1.slice = true;
-                    groups.push_back(g1);
-                    g.first = k + ns;
-                    g.count -= ns;
-                } else {
-                    g.slice = true;
+        }
+        slot.assign(nn, 0);
+        pslot.assign(nn, 0);
+        uint32_t nrows = 0, nprows = 0;
+        for (uint32_t k = 0; k < nn; ++k) {
+            if (need_full[k]) slot[k] = nrows++;
+            if (need_proj[k]) pslot[k] = nprows++;
+        }
+        cp.nrows = nrows;
+        cp.nprows = nprows;
+        // launch groups: (level, kind, dir) runs of the list; boolean runs split by full/projected
+        groups.clear();
+        members.clear();
+        members.reserve(nn);
+        for (uint32_t k = 0; k < nn;) {
+            const CNode &a = p->nodes[list[k]];
+            const uint8_t kind = (a.kind == NK_OR) ? NK_AND : a.kind;   // AND and OR share a launch
+            const uint16_t key = (kind == NK_AND) ? 0 : a.dir;
+            uint32_t e = k + 1;
+            while (e < nn) {
+                const CNode &b = p->nodes[list[e]];
+                const uint8_t kb2 = (b.kind == NK_OR) ? NK_AND : b.kind;
+                if (b.level != a.level || kb2 != kind || (kind != NK_AND && b.dir != key)) break;
+                ++e;
+            }
+            if (kind == NK_AND) {
+                for (int pm = 0; pm < 2; ++pm) {
+                    Group g{kind, key, (uint32_t)members.size(), 0};
+                    g.proj = pm;
+                    for (uint32_t q = k; q < e; ++q)
+                        if (pmode[q] == pm) members.push_back(q);
+                    g.count = (uint32_t)members.size() - g.first;
+                    if (g.count) groups.push_back(g);
                 }
+            } else {
+                const uint32_t first = (uint32_t)members.size();
+                for (uint32_t q = k; q < e; ++q) members.push_back(q);
+                Group g{kind, key, first, e - k};
+                if (use_slice && kind == NK_RESTRICT) {
+                    uint32_t ns = 0;   // leading lane-packable nodes (class 0/1 sort first)
+                    while (ns < g.count) {
+                        const CNode &c = p->nodes[list[k + ns]];
+                        if (slice_class(c.pred, c.n, c.sat) == 2) break;
+                        ++ns;
+                    }
+                    if (ns && slice_worthwhile(kb, ns, force_slice)) {
+                        if (ns < g.count) {
+                            Group g1{kind, key, first, ns};
+                            g1.slice = true;
+                            groups.push_back(g1);
+                            g.first = first + ns;
+                            g.count -= ns;
+                        } else {
+                            g.slice = true;
+                        }
+                    }
+                }
+                groups.push_back(g);
+            }
+            k = e;
+        }
+        size_t n_ops = 0, n_bool = 0, n_res = 0, n_dr = 0;
+        for (const Group &g : groups) {
+            if (g.kind == NK_AND) {
+                n_bool += g.count;
+                for (uint32_t m = g.first; m < g.first + g.count; ++m) n_ops += p->nodes[list[members[m]]].op_count;
+            } else if (g.kind == NK_RESTRICT) {
+                n_res += g.count;
+                if (!g.slice) *heavy_need = std::max(*heavy_need, (size_t)g.count * kb->dirs[g.key].n_heavy * 8);
+            } else {
+                n_dr += g.count;
             }
         }
-        groups.push_back(g);
-        k = e;
-    }
-    size_t n_ops = 0, n_bool = 0, n_res = 0, n_dr = 0;
-    for (const Group &g : groups) {
-        if (g.kind == NK_AND) {
-            n_bool += g.count;
-            for (uint32_t k = g.first; k < g.first + g.count; ++k) n_ops += p->nodes[list[k]].op_count;
-        } else if (g.kind == NK_RESTRICT) {
-            n_res += g.count;
-            if (!g.slice) *heavy_need = std::max(*heavy_need, (size_t)g.count * kb->dirs[g.key].n_heavy * 8);
-        } else {
-            n_dr += g.count;
-        }
-    }
-    cp.off_bool = 0;
-    cp.off_ops = align_up(cp.off_bool + n_bool * sizeof(BoolDesc), 16);
-    cp.off_res = align_up(cp.off_ops + n_ops * sizeof(Operand), 16);
-    cp.off_dr = align_up(cp.off_res + n_res * sizeof(RestrictDesc), 16);
-    cp.off_cov = align_up(cp.off_dr + n_dr * sizeof(DrangeDesc), 16);
-    cp.off_rows = align_up(cp.off_cov + nroots * sizeof(uint32_t), 16);
-    cp.blob_bytes = align_up(cp.off_rows + (out_bits ? nroots * sizeof(void *) : 0), 256);
-    cp.blob_off = *blob_cursor;
-    *blob_cursor += cp.blob_bytes;
-    return;
+        cp.off_bool = 0;
+        cp.off_ops = align_up(cp.off_bool + n_bool * sizeof(BoolDesc), 16);
+        cp.off_res = align_up(cp.off_ops + n_ops * sizeof(Operand), 16);
+        cp.off_dr = align_up(cp.off_res + n_res * sizeof(RestrictDesc), 16);
+        cp.off_cov = align_up(cp.off_dr + n_dr * sizeof(DrangeDesc), 16);
+        cp.off_rows = align_up(cp.off_cov + nroots * sizeof(uint32_t), 16);
+        cp.blob_bytes = align_up(cp.off_rows + (out_bits ? nroots * sizeof(void *) : 0), 256);
+        cp.blob_off = *blob_cursor;
+        *blob_cursor += cp.blob_bytes;
+        return;
     }
 
     char *h = h_blob + cp.blob_off;
-    auto ptr_of = [&](uint32_t r) -> const uint32_t * {
+    auto ptr_of = [&](uint32_t r) -> const uint32_t * {        // full row of an operand
         switch (ref_type(r)) {
         case RT_NODE: return rows + (size_t)slot[local[ref_id(r)]] * kb->W4;
         case RT_ATOM: return kb->concepts + (size_t)ref_id(r) * kb->W4;
         default: return kb->ones;
         }
     };
+    auto pptr_of = [&](uint32_t r) -> const uint32_t * {       // projected row of an operand
+        switch (ref_type(r)) {
+        case RT_NODE: return prows + (size_t)pslot[local[ref_id(r)]] * kb->MW4;
+        case RT_ATOM: return kb->pconcepts + (size_t)ref_id(r) * kb->MW4;
+        default: return kb->pones;
+        }
+    };
+    auto out_of = [&](uint32_t k) { return need_full[k] ? rows + (size_t)slot[k] * kb->W4 : nullptr; };
+    auto proj_of = [&](uint32_t k) { return need_proj[k] ? prows + (size_t)pslot[k] * kb->MW4 : nullptr; };
     BoolDesc *hb = (BoolDesc *)(h + cp.off_bool);
     Operand *ho = (Operand *)(h + cp.off_ops);
     RestrictDesc *hr = (RestrictDesc *)(h + cp.off_res);
@@ -318,55 +366,67 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
     uint32_t ib = 0, io = 0, ir = 0, idr = 0;
     cp.recs.clear();
     for (const Group &g : groups) {
-        LaunchRec lr{g.kind, g.key, g.slice, g.count, 0, 0, 0};
+        LaunchRec lr{g.kind, g.key, g.slice, g.proj, g.count, 0, 0, 0};
         if (g.kind == NK_AND) {
             lr.first_desc = ib;
-            for (uint32_t k = g.first; k < g.first + g.count; ++k) {
+            const double wb = 4.0 * (g.proj ? kb->MW : kb->W);
+            for (uint32_t m = g.first; m < g.first + g.count; ++m) {
+                const uint32_t k = members[m];
                 const CNode &n = p->nodes[list[k]];
                 BoolDesc bd;
-                bd.out = need_row[k] ? rows + (size_t)slot[k] * kb->W4 : nullptr;
+                if (g.proj) {           // projected: the output (if any) is the projected row
+                    bd.out = proj_of(k);
+                    bd.proj = nullptr;
+                } else {
+                    bd.out = out_of(k);
+                    bd.proj = proj_of(k);
+                }
                 bd.op_first = io;
                 bd.op_count = n.op_count;
                 bd.is_or = n.kind == NK_OR;
                 bd.cover = cover_of_node[k];
                 for (uint32_t q = 0; q < n.op_count; ++q) {
                     const uint32_t o = p->ops[n.op_begin + q];
-                    ho[io++] = Operand{ptr_of(o), ref_comp(o) ? 0xffffffffu : 0u, 0};
+                    ho[io++] = Operand{g.proj ? pptr_of(o) : ptr_of(o), ref_comp(o) ? 0xffffffffu : 0u, 0};
                 }
                 hb[ib++] = bd;
-                lr.bytes += n.bytes + (bd.cover >= 0 ? 8.0 * kb->W : 0);
+                lr.bytes += wb * (n.op_count + (bd.out ? 1 : 0) + (bd.cover >= 0 ? 2 : 0));
             }
         } else if (g.kind == NK_RESTRICT) {
             lr.first_desc = ir;
             const hedl_dir &dr = kb->dirs[g.key];
-            for (uint32_t k = g.first; k < g.first + g.count; ++k) {
+            for (uint32_t m = g.first; m < g.first + g.count; ++m) {
+                const uint32_t k = members[m];
                 const CNode &n = p->nodes[list[k]];
                 const uint32_t c = p->ops[n.op_begin];
                 RestrictDesc rd;
                 rd.child = ptr_of(c);
-                rd.out = need_row[k] ? rows + (size_t)slot[k] * kb->W4 : nullptr;
+                rd.out = out_of(k);
+                rd.proj = proj_of(k);
                 rd.cmask = ref_comp(c) ? 0xffffffffu : 0u;
                 rd.pred = n.pred;
                 rd.n = n.n;
                 rd.sat = n.sat;
                 rd.cover = cover_of_node[k];
-                rd.heavy_slot = (k - g.first) * dr.n_heavy;
+                rd.heavy_slot = (m - g.first) * dr.n_heavy;
                 hr[ir++] = rd;
-                lr.bytes += 4.0 * (kb->N + 1) + 4.0 * (dr.E - dr.E_heavy) + 8.0 * kb->W + (rd.cover >= 0 ? 8.0 * kb->W : 0);
+                lr.bytes += 4.0 * (kb->N + 1) + 4.0 * (dr.E - dr.E_heavy) + 4.0 * kb->W * (1 + (rd.out ? 1 : 0) + (rd.cover >= 0 ? 2 : 0));
                 lr.bytes2 += 4.0 * dr.E_heavy;
             }
         } else {
             lr.first_desc = idr;
-            for (uint32_t k = g.first; k < g.first + g.count; ++k) {
+            for (uint32_t m = g.first; m < g.first + g.count; ++m) {
+                const uint32_t k = members[m];
                 const CNode &n = p->nodes[list[k]];
                 DrangeDesc dd;
-                dd.out = need_row[k] ? rows + (size_t)slot[k] * kb->W4 : nullptr;
+                dd.out = out_of(k);
+                dd.proj = proj_of(k);
                 dd.lo = n.lo;
                 dd.hi = n.hi;
                 dd.cover = cover_of_node[k];
                 dd.prop = n.dir;
                 hd[idr++] = dd;
-                lr.bytes += n.bytes + (dd.cover >= 0 ? 8.0 * kb->W : 0);
+                lr.bytes += kb->data_bytes[n.dir] + 4.0 * kb->W * ((dd.out ? 1 : 0) + (dd.cover >= 0 ? 2 : 0));
             }
         }
         cp.recs.push_back(lr);
@@ -381,15 +441,18 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
 // Phase D: the launches of one chunk.
 hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, uint32_t r0, uint32_t *out_bits,
                          hedl_counts *counts_dev, cudaStream_t s) {
-    const KbDev kd{kb->N, kb->W, kb->W4, kb->pos, kb->neg};
+    const KbDev kd{kb->N, kb->W, kb->W4, kb->pos, kb->neg, kb->ex_mask, kb->ex_base};
+    const KbDev kp{kb->M, kb->MW, kb->MW4, kb->ppos, kb->pneg, nullptr, nullptr};   // example-projected space
     const char *d = (const char *)w->plan.dev + cp.blob_off;
     const char *h = (const char *)w->plan.host + cp.blob_off;
     hedl_counts *cov = (hedl_counts *)w->counts.p;
     const uint32_t nroots = cp.rc - cp.ri;
     launch_cover_init(s, cov, cp.ncov, kb->npos, kb->nneg);
+    if (cp.nprows && kb->MW4)
+        HEDL_CUDA(kb, cudaMemsetAsync(w->prows.p, 0, (size_t)cp.nprows * kb->MW4 * 4, s));   // scatter targets
     for (const LaunchRec &lr : cp.recs) {
         if (lr.kind == NK_AND) {
-            launch_bool(s, kd, (const BoolDesc *)(d + cp.off_bool) + lr.first_desc, lr.count,
+            launch_bool(s, lr.proj ? kp : kd, (const BoolDesc *)(d + cp.off_bool) + lr.first_desc, lr.count,
                         (const Operand *)(d + cp.off_ops), cov, lr.bytes);
         } else if (lr.kind == NK_RESTRICT) {
             const hedl_dir &dr = kb->dirs[lr.key];
@@ -425,7 +488,7 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
     PlanCache &pc = w->plan;
     const bool bits = out_bits != nullptr;
     const bool hit = pc.valid && pc.r0 == r0 && pc.r1 == r1 && pc.bits == bits && pc.eflags == eflags &&
-                     pc.rows_base == w->rows.p && pc.heavy_base == w->heavy.p;
+                     pc.rows_base == w->rows.p && pc.heavy_base == w->heavy.p && pc.prows_base == w->prows.p;
     hedl_status st;
     if (!hit) {
         // the previous plan's blobs may still be read by queued work: wait, then reuse them
@@ -449,17 +512,19 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
         std::vector<uint32_t> local(p->nodes.size());
         pc.chunks.resize(lists.size());
         std::vector<ChunkTmp> tmps(lists.size());
-        size_t cursor = 0, heavy_need = 16, max_nn = 1, max_cov = 1;
+        size_t cursor = 0, heavy_need = 16, max_nn = 1, max_cov = 1, max_np = 1;
         for (size_t c = 0; c < lists.size(); ++c) {
             ChunkPlan &cp = pc.chunks[c];
             cp.ri = ranges[c].first;
             cp.rc = ranges[c].second;
-            fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, nullptr, local, nullptr, &cursor, &heavy_need, true,
-                       tmps[c]);
+            fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, nullptr, nullptr, local, nullptr, &cursor,
+                       &heavy_need, true, tmps[c]);
             max_nn = std::max<size_t>(max_nn, cp.nrows);
+            max_np = std::max<size_t>(max_np, cp.nprows);
             max_cov = std::max<size_t>(max_cov, cp.ncov);
         }
         if ((st = grow(kb, s, w->rows, max_nn * row_bytes + 16, false))) return st;
+        if ((st = grow(kb, s, w->prows, max_np * kb->MW4 * 4 + 16, false))) return st;
         if ((st = grow(kb, s, w->heavy, heavy_need, true))) return st;
         if ((st = grow(kb, s, w->counts, max_cov * sizeof(hedl_counts), false))) return st;
         if ((st = reserve_plan(pc, std::max<size_t>(cursor, 256)))) return st;
@@ -467,14 +532,14 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
         pc.r0 = r0; pc.r1 = r1; pc.bits = bits; pc.eflags = eflags;
         pc.rows_base = w->rows.p;
         pc.heavy_base = w->heavy.p;
+        pc.prows_base = w->prows.p;
         // phase C + D interleaved: fill chunk c on the host while chunk c-1 runs on the GPU
         for (size_t c = 0; c < lists.size(); ++c) {
             ChunkPlan &cp = pc.chunks[c];
             size_t cur = cp.blob_off;
-            fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, (uint32_t *)w->rows.p, local, (char *)pc.host, &cur,
-                       &heavy_need, false, tmps[c]);
-            ChunkTmp().need_row.swap(tmps[c].need_row);   // release the chunk's planning state
-            std::vector<uint32_t>().swap(tmps[c].slot);
+            fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, (uint32_t *)w->rows.p, (uint32_t *)w->prows.p, local,
+                       (char *)pc.host, &cur, &heavy_need, false, tmps[c]);
+            tmps[c] = ChunkTmp();   // release the chunk's planning state
             HEDL_CUDA(kb, cudaMemcpyAsync((char *)pc.dev + cp.blob_off, (char *)pc.host + cp.blob_off, cp.blob_bytes,
                                           cudaMemcpyHostToDevice, s));
             count_io(cp.blob_bytes, 0);
@@ -552,7 +617,7 @@ extern "C" hedl_status hedl_program_free(hedl_program *p) {
         Workspace *w = (Workspace *)p->ws;
         DeviceGuard dg(p->kb->device);
         if (w->done) cudaEventSynchronize(w->done);
-        for (DevBuf *b : {&w->rows, &w->heavy, &w->counts, &w->slice})
+        for (DevBuf *b : {&w->rows, &w->prows, &w->heavy, &w->counts, &w->slice})
             if (b->p) cudaFree(b->p);
         release_plan(w->plan);
         if (w->done) cudaEventDestroy(w->done);

@@ -89,6 +89,12 @@ struct hedl_kb {
     uint32_t *zeros = nullptr;     // device [W4]
     uint32_t *pos = nullptr, *neg = nullptr;  // device [W4]
     uint64_t npos = 0, nneg = 0;
+    // example projection: E = sorted P u N, M = |E|;
+    // a projected row holds bit r = membership of the r-th example (MW4 = ceil(M/32) padded to 4)
+    uint32_t M = 0, MW = 0, MW4 = 0;
+    uint32_t *ex_mask = nullptr, *ex_base = nullptr;    // device [W4]
+    uint32_t *pconcepts = nullptr;                      // device [C][MW4]
+    uint32_t *pones = nullptr, *ppos = nullptr, *pneg = nullptr;   // device [MW4]
     std::vector<hedl_dir> dirs;    // 2R
     std::vector<hedl_data> data;   // D
     std::vector<void *> allocs;
@@ -146,6 +152,7 @@ void prof_end(cudaStream_t s, int kc, double alg_bytes);
 // ---- kernels launchers (kernels.cu) -----------------------------------------
 struct BoolDesc {
     uint32_t *out;
+    uint32_t *proj;                // example-projected copy of the output (null = not needed)
     uint32_t op_first, op_count;   // into the operand table
     uint32_t is_or;
     int32_t cover;                 // counts slot or -1
@@ -158,6 +165,7 @@ struct Operand {
 struct RestrictDesc {
     const uint32_t *child;
     uint32_t *out;
+    uint32_t *proj;                // example-projected copy of the output (null = not needed)
     uint32_t cmask;                // 0 or ~0
     uint32_t pred, n, sat;
     int32_t cover;                 // counts slot or -1
@@ -165,6 +173,7 @@ struct RestrictDesc {
 };
 struct DrangeDesc {
     uint32_t *out;
+    uint32_t *proj;
     float lo, hi;
     int32_t cover;
     uint32_t prop;
@@ -180,8 +189,23 @@ struct DirDev {                   // passed by value
 struct KbDev {
     uint32_t N, W, W4;
     const uint32_t *pos, *neg;
+    const uint32_t *ex_mask, *ex_base;   // example projection: per word, example bits and rank of the first
 };
 
+#ifdef __CUDACC__
+// scatter the example bits of full-row word w into an example-projected row (atomicOr;
+// the projected row is zeroed before the launch)
+static __device__ __forceinline__ void proj_scatter(const KbDev &kb, uint32_t *proj, uint32_t w, uint32_t word) {
+    uint32_t m = __ldg(kb.ex_mask + w);
+    if (!m || !word) return;
+    uint32_t bits = 0, nb = 0;
+    for (; m; m &= m - 1, ++nb) bits |= ((word >> (__ffs(m) - 1)) & 1u) << nb;   // pext(word, mask)
+    if (!bits) return;
+    const uint32_t base = __ldg(kb.ex_base + w), sh = base & 31;
+    atomicOr(proj + (base >> 5), bits << sh);
+    if (sh && sh + nb > 32) atomicOr(proj + (base >> 5) + 1, bits >> (32 - sh));
+}
+#endif
 void launch_cover_init(cudaStream_t s, hedl_counts *counts, uint32_t n, uint64_t npos, uint64_t nneg);
 void launch_bool(cudaStream_t s, const KbDev &kb, const BoolDesc *d_desc, uint32_t n_desc,
                  const Operand *d_ops, hedl_counts *counts, double alg_bytes);

@@ -213,6 +213,34 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
         if ((s = upload(kb, st, &kb->pos, pos.data(), pos.size()))) return bail(s);
         if ((s = upload(kb, st, &kb->neg, neg.data(), neg.size()))) return bail(s);
         for (uint32_t w = 0; w < W4; ++w) { kb->npos += __builtin_popcount(pos[w]); kb->nneg += __builtin_popcount(neg[w]); }
+        // example projection: E = P u N in id order; rank r <-> r-th example
+        std::vector<uint32_t> exm(W4, 0), exb(W4, 0), ex;
+        uint32_t rank = 0;
+        for (uint32_t w = 0; w < W4; ++w) {
+            exm[w] = pos[w] | neg[w];
+            exb[w] = rank;
+            for (uint32_t m = exm[w]; m; m &= m - 1) ex.push_back(32 * w + __builtin_ctz(m));
+            rank += __builtin_popcount(exm[w]);
+        }
+        kb->M = rank;
+        kb->MW = (rank + 31) / 32;
+        kb->MW4 = (kb->MW + 3) & ~3u;
+        const uint32_t MW4 = kb->MW4;
+        std::vector<uint32_t> pc((uint64_t)C * MW4, 0), pon(MW4, 0), pp(MW4, 0), pn(MW4, 0);
+        for (uint32_t r = 0; r < rank; ++r) {
+            const uint32_t x = ex[r], bit = 1u << (r & 31);
+            pon[r >> 5] |= bit;
+            if (pos[x >> 5] >> (x & 31) & 1u) pp[r >> 5] |= bit;
+            if (neg[x >> 5] >> (x & 31) & 1u) pn[r >> 5] |= bit;
+            for (uint32_t c = 0; c < C; ++c)
+                if (desc->concept_bits[(uint64_t)c * W + (x >> 5)] >> (x & 31) & 1u) pc[(uint64_t)c * MW4 + (r >> 5)] |= bit;
+        }
+        if ((s = upload(kb, st, &kb->ex_mask, exm.data(), exm.size()))) return bail(s);
+        if ((s = upload(kb, st, &kb->ex_base, exb.data(), exb.size()))) return bail(s);
+        if ((s = upload(kb, st, &kb->pconcepts, pc.data(), pc.size()))) return bail(s);
+        if ((s = upload(kb, st, &kb->pones, pon.data(), pon.size()))) return bail(s);
+        if ((s = upload(kb, st, &kb->ppos, pp.data(), pp.size()))) return bail(s);
+        if ((s = upload(kb, st, &kb->pneg, pn.data(), pn.size()))) return bail(s);
         if (cudaStreamSynchronize(st) != cudaSuccess) return bail(fail(HEDL_ERR_CUDA, "upload failed"));
     }
     kb->dirs.resize(2 * R);

@@ -93,6 +93,12 @@ __global__ void __launch_bounds__(256) k_bool(KbDev kb, const BoolDesc *__restri
         acc.z = tail_word(acc.z, w0 + 2, kb.W, kb.N);
         acc.w = tail_word(acc.w, w0 + 3, kb.W, kb.N);
         if (d.out) reinterpret_cast<uint4 *>(d.out)[i] = acc;   // null: root needed for counts only
+        if (d.proj) {
+            proj_scatter(kb, d.proj, w0, acc.x);
+            proj_scatter(kb, d.proj, w0 + 1, acc.y);
+            proj_scatter(kb, d.proj, w0 + 2, acc.z);
+            proj_scatter(kb, d.proj, w0 + 3, acc.w);
+        }
         if (d.cover >= 0) {
             const uint4 p = __ldg(reinterpret_cast<const uint4 *>(kb.pos) + i);
             const uint4 q = __ldg(reinterpret_cast<const uint4 *>(kb.neg) + i);
@@ -159,6 +165,7 @@ __global__ void __launch_bounds__(256) k_restrict(KbDev kb, DirDev dir, const Re
         }
         if (lane == 0) {
             if (d.out) d.out[w] = word;
+            if (d.proj && w < kb.W) proj_scatter(kb, d.proj, w, word);
             if (d.cover >= 0) {
                 tp = __popc(word & __ldg(kb.pos + w));
                 fp = __popc(word & __ldg(kb.neg + w));
@@ -207,6 +214,7 @@ __global__ void __launch_bounds__(256) k_restrict_heavy(KbDev kb, DirDev dir, co
         if (pred_eval(d.pred, min(tot, d.sat), d.n)) {
             const uint32_t bit = 1u << (x & 31);
             if (d.out) atomicOr(d.out + (x >> 5), bit);
+            if (d.proj) proj_scatter(kb, d.proj, x >> 5, bit);
             if (d.cover >= 0) {
                 hedl_counts *cc = counts + d.cover;
                 if (__ldg(kb.pos + (x >> 5)) & bit) {
@@ -249,6 +257,7 @@ __global__ void __launch_bounds__(256) k_drange(KbDev kb, const uint32_t *__rest
             word = __ballot_sync(FULL, res);
         }
         if (lane == 0) {
+            if (d.proj && w < kb.W) proj_scatter(kb, d.proj, w, word);
             if (d.out) d.out[w] = word;
             if (d.cover >= 0) {
                 tp = __popc(word & __ldg(kb.pos + w));

@@ -356,6 +356,10 @@ __global__ void __launch_bounds__(256, COUNT ? 3 : 4) k_slice_tile(KbDev kb, Sli
         for (int q = 0; q < 4; ++q) o[q] = warp_transpose(ot[((wl + q) * 32 + lane) * TROW + g], lane);
         if (live) {
             if (r.out) *reinterpret_cast<uint4 *>(r.out + w) = make_uint4(o[0], o[1], o[2], o[3]);
+            if (r.proj) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) if (w + q < kb.W) proj_scatter(kb, r.proj, w + q, o[q]);
+            }
             if (r.cover >= 0) {
                 const uint4 p = __ldg(reinterpret_cast<const uint4 *>(kb.pos + w));
                 const uint4 n = __ldg(reinterpret_cast<const uint4 *>(kb.neg + w));

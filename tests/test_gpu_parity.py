@@ -36,11 +36,15 @@ def gpu_eval(kb, nodes, kids, roots, flags=0, bits=True, eflags=0, ws_limit=None
 
 
 def assert_parity(kb, trees=None, arrays=None, flags=0, eflags=0, ws_limit=None, tag=""):
+    """Bitsets + counts (bitsets requested) and counts alone (the example-projected path) vs the oracle."""
     nodes, kids, roots = arrays if arrays is not None else flatten(trees)
-    gb, gc, _ = gpu_eval(kb, nodes, kids, roots, flags, eflags=eflags, ws_limit=ws_limit)
+    gb, gc, (k, prog) = gpu_eval(kb, nodes, kids, roots, flags, eflags=eflags, ws_limit=ws_limit)
     ob, oc = setsem.evaluate(kb, nodes, kids, roots, flags=flags, threads=8)
     bad = np.nonzero((gb != ob).any(axis=1) | (gc != oc).any(axis=1))[0] if len(roots) else []
     assert len(bad) == 0, f"{tag}: {len(bad)} mismatching roots, first {bad[:5]}"
+    _, gc2 = _hedl().hedl_eval_batch(k, prog, 0, len(roots), want_bits=False, flags=eflags)
+    bad = np.nonzero((gc2 != oc).any(axis=1))[0] if len(roots) else []
+    assert len(bad) == 0, f"{tag} (counts only): {len(bad)} mismatching roots, first {bad[:5]}"
     return gb, gc
 
 
