@@ -36,7 +36,7 @@ hedl_status cuda_fail(const hedl_kb *kb, cudaError_t e, const char *where) {
 }
 
 const char *kKClassName[KC_N] = {"bool", "restrict", "restrict_heavy", "drange", "cover_init", "gather",
-                                 "slice_pack", "slice", "slice_heavy", "kb"};
+                                 "slice_pack", "slice", "slice_heavy", "kb", "slice_ex"};
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }

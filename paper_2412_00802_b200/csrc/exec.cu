@@ -29,6 +29,7 @@ struct LaunchRec {
     uint16_t key;          // dir / prop
     bool slice;
     bool proj;             // boolean group evaluated on example-projected rows
+    bool ex;               // restriction pack evaluated on example rows only
     uint32_t count, first_desc;
     double bytes, bytes2;
 };
@@ -122,6 +123,7 @@ struct Group {
     uint32_t first, count;   // into ChunkTmp::members (positions in the chunk list)
     bool slice = false;
     bool proj = false;
+    bool ex = false;
 };
 
 // ---- planning -------------------------------------------------------------------
@@ -291,30 +293,33 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                     g.count = (uint32_t)members.size() - g.first;
                     if (g.count) groups.push_back(g);
                 }
+            } else if (kind == NK_RESTRICT && use_slice) {
+                // lane-packable nodes (class 0/1 sort first) needed in full, then those needed only
+                // at the examples (EX packs), then the per-node rest
+                uint32_t ns = 0;
+                while (k + ns < e && slice_class(p->nodes[list[k + ns]].pred, p->nodes[list[k + ns]].n,
+                                                 p->nodes[list[k + ns]].sat) != 2)
+                    ++ns;
+                const bool packs = ns && slice_worthwhile(kb, ns, force_slice);
+                const uint32_t split = packs ? k + ns : k;
+                for (int demand = 0; demand < 2 && packs; ++demand) {     // 0: full rows, 1: examples only
+                    Group g{kind, key, (uint32_t)members.size(), 0};
+                    g.slice = true;
+                    g.ex = demand == 1;
+                    for (uint32_t q = k; q < split; ++q)
+                        if ((need_full[q] == 0) == (demand == 1)) members.push_back(q);
+                    g.count = (uint32_t)members.size() - g.first;
+                    if (g.count) groups.push_back(g);
+                }
+                if (split < e) {
+                    Group g{kind, key, (uint32_t)members.size(), e - split};
+                    for (uint32_t q = split; q < e; ++q) members.push_back(q);
+                    groups.push_back(g);
+                }
             } else {
                 const uint32_t first = (uint32_t)members.size();
                 for (uint32_t q = k; q < e; ++q) members.push_back(q);
-                Group g{kind, key, first, e - k};
-                if (use_slice && kind == NK_RESTRICT) {
-                    uint32_t ns = 0;   // leading lane-packable nodes (class 0/1 sort first)
-                    while (ns < g.count) {
-                        const CNode &c = p->nodes[list[k + ns]];
-                        if (slice_class(c.pred, c.n, c.sat) == 2) break;
-                        ++ns;
-                    }
-                    if (ns && slice_worthwhile(kb, ns, force_slice)) {
-                        if (ns < g.count) {
-                            Group g1{kind, key, first, ns};
-                            g1.slice = true;
-                            groups.push_back(g1);
-                            g.first = first + ns;
-                            g.count -= ns;
-                        } else {
-                            g.slice = true;
-                        }
-                    }
-                }
-                groups.push_back(g);
+                groups.push_back(Group{kind, key, first, e - k});
             }
             k = e;
         }
@@ -366,7 +371,7 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
     uint32_t ib = 0, io = 0, ir = 0, idr = 0;
     cp.recs.clear();
     for (const Group &g : groups) {
-        LaunchRec lr{g.kind, g.key, g.slice, g.proj, g.count, 0, 0, 0};
+        LaunchRec lr{g.kind, g.key, g.slice, g.proj, g.ex, g.count, 0, 0, 0};
         if (g.kind == NK_AND) {
             lr.first_desc = ib;
             const double wb = 4.0 * (g.proj ? kb->MW : kb->W);
@@ -459,7 +464,8 @@ hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, u
             const RestrictDesc *dd_desc = (const RestrictDesc *)(d + cp.off_res) + lr.first_desc;
             if (lr.slice) {
                 hedl_status st = slice_run(kb, &w->slice.p, &w->slice.bytes, s, kd, lr.key,
-                                           (const RestrictDesc *)(h + cp.off_res) + lr.first_desc, dd_desc, lr.count, cov);
+                                           (const RestrictDesc *)(h + cp.off_res) + lr.first_desc, dd_desc, lr.count, cov,
+                                           lr.ex);
                 if (st) return st;
             } else {
                 DirDev dd{dr.row_ptr, dr.col, dr.heavy_x, dr.heavy_nchunks, dr.chunks, dr.n_heavy, dr.n_chunks};

@@ -72,6 +72,14 @@ struct hedl_dir {                  // one role direction
     uint32_t n_tiles = 0;
     uint4 *tiles = nullptr;            // device [n_tiles + 1]
     uint32_t *order = nullptr;         // device [N - n_heavy]: per tile medium rows then light rows, degree-descending
+    // example-row ("EX") packs: the same over the example ranks, 128 ranks per block
+    uint32_t n_ex_blocks = 0;
+    uint4 *ex_tiles = nullptr;         // device [n_ex_blocks + 1] {order begin, n_medium, n_light, ex-heavy begin}
+    uint32_t *ex_order = nullptr;      // device: example ranks (medium then light, degree-descending per block)
+    uint32_t n_ex_heavy = 0, n_ex_chunks = 0;
+    uint32_t *ex_hx = nullptr, *ex_hrank = nullptr, *ex_hn = nullptr;   // heavy example rows: id, rank, #chunks
+    uint4 *ex_chunks = nullptr;        // {ex-heavy idx, e0, e1, 0}
+    uint64_t E_ex = 0, E_ex_heavy = 0; // edges of light/medium and of heavy example rows
 };
 
 struct hedl_data {
@@ -93,6 +101,8 @@ struct hedl_kb {
     // a projected row holds bit r = membership of the r-th example (MW4 = ceil(M/32) padded to 4)
     uint32_t M = 0, MW = 0, MW4 = 0;
     uint32_t *ex_mask = nullptr, *ex_base = nullptr;    // device [W4]
+    uint32_t *ex_ids = nullptr;                         // device [M]: the examples in rank order
+    std::vector<uint32_t> h_ex;                         // host copy of ex_ids
     uint32_t *pconcepts = nullptr;                      // device [C][MW4]
     uint32_t *pones = nullptr, *ppos = nullptr, *pneg = nullptr;   // device [MW4]
     std::vector<hedl_dir> dirs;    // 2R
@@ -144,7 +154,7 @@ void timing_note(const char *what, double ms);
 
 // ---- profiling -----------------------------------------------------------------
 enum KClass { KC_BOOL, KC_RESTRICT, KC_HEAVY, KC_DRANGE, KC_COVER_INIT, KC_GATHER,
-              KC_SLICE_IN, KC_SLICE, KC_SLICE_HEAVY, KC_KB, KC_N };
+              KC_SLICE_IN, KC_SLICE, KC_SLICE_HEAVY, KC_KB, KC_SLICE_EX, KC_N };
 extern const char *kKClassName[KC_N];
 void prof_begin(cudaStream_t s, int kc);
 void prof_end(cudaStream_t s, int kc, double alg_bytes);

@@ -223,6 +223,7 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
             rank += __builtin_popcount(exm[w]);
         }
         kb->M = rank;
+        kb->h_ex = ex;
         kb->MW = (rank + 31) / 32;
         kb->MW4 = (kb->MW + 3) & ~3u;
         const uint32_t MW4 = kb->MW4;
@@ -236,6 +237,7 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
                 if (desc->concept_bits[(uint64_t)c * W + (x >> 5)] >> (x & 31) & 1u) pc[(uint64_t)c * MW4 + (r >> 5)] |= bit;
         }
         if ((s = upload(kb, st, &kb->ex_mask, exm.data(), exm.size()))) return bail(s);
+        if ((s = upload(kb, st, &kb->ex_ids, ex.data(), ex.size()))) return bail(s);
         if ((s = upload(kb, st, &kb->ex_base, exb.data(), exb.size()))) return bail(s);
         if ((s = upload(kb, st, &kb->pconcepts, pc.data(), pc.size()))) return bail(s);
         if ((s = upload(kb, st, &kb->pones, pon.data(), pon.size()))) return bail(s);
@@ -302,6 +304,57 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
             }
             if ((s = upload(kb, st, &dr.tiles, tiles.data(), tiles.size()))) return bail(s);
             if ((s = upload(kb, st, &dr.order, order.data(), order.size()))) return bail(s);
+            // EX packs: example rows only (ranks of E), blocks of 128 ranks
+            {
+                const std::vector<uint32_t> &ex = kb->h_ex;
+                const uint32_t M = (uint32_t)ex.size();
+                dr.n_ex_blocks = (M + 127) / 128;
+                std::vector<uint4> et(dr.n_ex_blocks + 1);
+                std::vector<uint32_t> eo, ehx, ehr, ehn;
+                std::vector<uint4> ech;
+                std::vector<uint32_t> med, light;
+                auto degr = [&](uint32_t r) { return h.row_ptr[ex[r] + 1] - h.row_ptr[ex[r]]; };
+                for (uint32_t b = 0; b < dr.n_ex_blocks; ++b) {
+                    med.clear();
+                    light.clear();
+                    et[b].w = (uint32_t)ehx.size();
+                    for (uint32_t r = b * 128; r < std::min(M, b * 128 + 128); ++r) {
+                        const uint32_t d = degr(r);
+                        if (d > kHeavyDeg) {
+                            const uint32_t hi = (uint32_t)ehx.size();
+                            ehx.push_back(ex[r]);
+                            ehr.push_back(r);
+                            const uint32_t a = h.row_ptr[ex[r]], e = h.row_ptr[ex[r] + 1];
+                            uint32_t nc = 0;
+                            for (uint32_t q = a; q < e; q += kHeavyChunk, ++nc)
+                                ech.push_back(make_uint4(hi, q, std::min(e, q + kHeavyChunk), 0));
+                            ehn.push_back(nc);
+                            dr.E_ex_heavy += d;
+                        } else {
+                            (d > kLightDeg ? med : light).push_back(r);
+                            dr.E_ex += d;
+                        }
+                    }
+                    auto by_deg = [&](uint32_t a, uint32_t c) { return degr(a) != degr(c) ? degr(a) > degr(c) : a < c; };
+                    std::sort(med.begin(), med.end(), by_deg);
+                    std::sort(light.begin(), light.end(), by_deg);
+                    et[b].x = (uint32_t)eo.size();
+                    et[b].y = (uint32_t)med.size();
+                    et[b].z = (uint32_t)light.size();
+                    eo.insert(eo.end(), med.begin(), med.end());
+                    eo.insert(eo.end(), light.begin(), light.end());
+                }
+                et[dr.n_ex_blocks] = make_uint4((uint32_t)eo.size(), 0, 0, (uint32_t)ehx.size());
+                dr.n_ex_heavy = (uint32_t)ehx.size();
+                dr.n_ex_chunks = (uint32_t)ech.size();
+                if ((s = upload(kb, st, &dr.ex_tiles, et.data(), et.size()))) return bail(s);
+                if ((s = upload(kb, st, &dr.ex_order, eo.data(), eo.size()))) return bail(s);
+                if ((s = upload(kb, st, &dr.ex_hx, ehx.data(), ehx.size()))) return bail(s);
+                if ((s = upload(kb, st, &dr.ex_hrank, ehr.data(), ehr.size()))) return bail(s);
+                if ((s = upload(kb, st, &dr.ex_hn, ehn.data(), ehn.size()))) return bail(s);
+                if ((s = upload(kb, st, &dr.ex_chunks, ech.data(), ech.size()))) return bail(s);
+                if (cudaStreamSynchronize(st) != cudaSuccess) return bail(fail(HEDL_ERR_CUDA, "upload failed"));
+            }
             dr.n_heavy = (uint32_t)hx.size();
             dr.n_chunks = (uint32_t)chunks.size();
             if ((s = upload(kb, st, &dr.heavy_x, hx.data(), hx.size()))) return bail(s);

@@ -381,6 +381,81 @@ __global__ void __launch_bounds__(256, COUNT ? 3 : 4) k_slice_tile(KbDev kb, Sli
     }
 }
 
+// ------------------------------------------------------------------------------
+// EX packs: only the example rows (ranks of E); 128 ranks per CTA; the result goes
+// straight to the nodes' example-projected rows (4 projected words per CTA, owned:
+// plain stores) with fused coverage against the projected example masks.
+struct ExArgs {
+    const uint32_t *row_ptr, *col;
+    const uint4 *ex_tiles;
+    const uint32_t *ex_order, *ex_ids, *ex_hrank;
+    const uint32_t *ppos, *pneg;
+    uint32_t MW4;
+};
+
+template <bool COUNT>
+__global__ void __launch_bounds__(256, COUNT ? 3 : 4) k_slice_ex(ExArgs a, SliceScratch sc, const RestrictDesc *__restrict__ d,
+                                                                 uint32_t count, hedl_counts *counts) {
+    __shared__ PackConst pc;
+    __shared__ uint32_t ot[128 * TROW];
+    const uint32_t b = blockIdx.x, r0 = b * 128;
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, half = lane & 1;
+    for (uint32_t i = threadIdx.x; i < 128 * TROW; i += 256) ot[i] = 0;
+    build_consts(pc, d, count);                           // (contains __syncthreads)
+    const uint4 ti = a.ex_tiles[b];
+    const uint32_t hbeg = ti.w, hend = a.ex_tiles[b + 1].w;
+    for (uint32_t h = hbeg + threadIdx.x; h < hend; h += 256) {
+        const uint32_t rl = __ldg(a.ex_hrank + h) - r0;
+#pragma unroll
+        for (int k = 0; k < LW; ++k) ot[rl * TROW + k] = sc.hout[(size_t)h * LW + k];
+    }
+    for (uint32_t m = wid; m < ti.y; m += 8) {            // medium rows: warp per row
+        const uint32_t r = __ldg(a.ex_order + ti.x + m), x = __ldg(a.ex_ids + r);
+        const uint32_t e0 = __ldg(a.row_ptr + x), e1 = __ldg(a.row_ptr + x + 1);
+        Acc<COUNT> acc;
+        acc.zero();
+        scan_edges<COUNT>(acc, a.col, sc.T, e0 + (lane >> 1), e1, 16, half);
+        acc.warp_reduce_pairs();
+        if (lane < 2) {
+#pragma unroll
+            for (int k = 0; k < HW; ++k) ot[(r - r0) * TROW + half * HW + k] = acc.result(pc, half * HW + k, k);
+        }
+    }
+    for (uint32_t l = threadIdx.x >> 1; l < ti.z; l += 128) {   // light rows: lane pair per row
+        const uint32_t r = __ldg(a.ex_order + ti.x + ti.y + l), x = __ldg(a.ex_ids + r);
+        const uint32_t e0 = __ldg(a.row_ptr + x), e1 = __ldg(a.row_ptr + x + 1);
+        Acc<COUNT> acc;
+        acc.zero();
+        scan_edges<COUNT>(acc, a.col, sc.T, e0, e1, 1, half);
+#pragma unroll
+        for (int k = 0; k < HW; ++k) ot[(r - r0) * TROW + half * HW + k] = acc.result(pc, half * HW + k, k);
+    }
+    __syncthreads();
+    const uint32_t g = wid, j = g * 32 + lane;
+    uint32_t o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = warp_transpose(ot[(q * 32 + lane) * TROW + g], lane);
+    if (j >= count) return;                               // (after the warp-wide transposes)
+    const RestrictDesc r = d[j];
+    const uint32_t w = b * 4;
+    if (r.proj) *reinterpret_cast<uint4 *>(r.proj + w) = make_uint4(o[0], o[1], o[2], o[3]);
+    if (r.cover >= 0) {
+        const uint4 p = __ldg(reinterpret_cast<const uint4 *>(a.ppos + w));
+        const uint4 n = __ldg(reinterpret_cast<const uint4 *>(a.pneg + w));
+        const uint32_t tp = __popc(o[0] & p.x) + __popc(o[1] & p.y) + __popc(o[2] & p.z) + __popc(o[3] & p.w);
+        const uint32_t fp = __popc(o[0] & n.x) + __popc(o[1] & n.y) + __popc(o[2] & n.z) + __popc(o[3] & n.w);
+        hedl_counts *c = counts + r.cover;
+        if (tp) {
+            atomicAdd((unsigned long long *)&c->tp, (unsigned long long)tp);
+            atomicAdd((unsigned long long *)&c->fn, 0ull - tp);
+        }
+        if (fp) {
+            atomicAdd((unsigned long long *)&c->fp, (unsigned long long)fp);
+            atomicAdd((unsigned long long *)&c->tn, 0ull - fp);
+        }
+    }
+}
+
 inline uint32_t cdiv(uint64_t a, uint64_t b) { return (uint32_t)((a + b - 1) / b); }
 }  // namespace
 
@@ -396,7 +471,7 @@ uint32_t slice_class(uint32_t pred, uint32_t n, uint32_t sat) {
 }
 
 hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream_t s, const KbDev &kd, uint32_t dirid,
-                      const RestrictDesc *h_desc, const RestrictDesc *d_desc, uint32_t n, hedl_counts *counts) {
+                      const RestrictDesc *h_desc, const RestrictDesc *d_desc, uint32_t n, hedl_counts *counts, bool ex) {
     const hedl_dir &dr = kb->dirs[dirid];
     const size_t t_bytes = (size_t)kb->W4 * 32 * 32;
     // one fixed layout for every direction (sized by the largest heavy list), so the
@@ -422,6 +497,9 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
     sc.hout = sc.ticket + nh;
     SliceDir sd{dr.row_ptr, dr.col, dr.tiles, dr.order, dr.heavy_x, dr.heavy_nchunks, dr.chunks,
                 dr.n_heavy, dr.n_chunks, dr.n_tiles};
+    SliceDir sdx{dr.row_ptr, dr.col, nullptr, nullptr, dr.ex_hx, dr.ex_hn, dr.ex_chunks, dr.n_ex_heavy, dr.n_ex_chunks, 0};
+    const ExArgs xa{dr.row_ptr, dr.col, dr.ex_tiles, dr.ex_order, kb->ex_ids, dr.ex_hrank, kb->ppos, kb->pneg, kb->MW4};
+    if (ex && !kb->M) return HEDL_OK;                     // no examples: nothing to evaluate
     const size_t smem = sizeof(PackConst) + 1024 * TROW * 4;
     static bool attr_set = false;
     if (!attr_set) {
@@ -443,20 +521,31 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
         k_slice_pack<<<cdiv(kb->W4, 32), 256, 0, s>>>(kd, dd, cnt, sc.T);
         count_launch();
         prof_end(s, KC_SLICE_IN, 4.0 * kb->W * cnt + 32.0 * 32 * kb->W4);
-        if (dr.n_chunks) {
+        const SliceDir &hd = ex ? sdx : sd;
+        if (hd.n_chunks) {
             prof_begin(s, KC_SLICE_HEAVY);
-            if (cls == 0) k_slice_heavy<false><<<dr.n_chunks, 256, 0, s>>>(sd, sc, dd, cnt);
-            else k_slice_heavy<true><<<dr.n_chunks, 256, 0, s>>>(sd, sc, dd, cnt);
+            if (cls == 0) k_slice_heavy<false><<<hd.n_chunks, 256, 0, s>>>(hd, sc, dd, cnt);
+            else k_slice_heavy<true><<<hd.n_chunks, 256, 0, s>>>(hd, sc, dd, cnt);
             count_launch();
-            prof_end(s, KC_SLICE_HEAVY, 4.0 * dr.E_heavy + 32.0 * dr.E_heavy);
+            const double eh = ex ? (double)dr.E_ex_heavy : (double)dr.E_heavy;
+            prof_end(s, KC_SLICE_HEAVY, 4.0 * eh + 32.0 * eh);
         }
-        prof_begin(s, KC_SLICE);
-        if (cls == 0) k_slice_tile<false><<<dr.n_tiles, 256, smem, s>>>(kd, sd, sc, dd, cnt, counts);
-        else k_slice_tile<true><<<dr.n_tiles, 256, smem, s>>>(kd, sd, sc, dd, cnt, counts);
-        count_launch();
-        // minimal DRAM bytes of one lane-packed pass: CSR once + T once (32 B per individual)
-        // + the cnt output rows; the 32 B-per-edge T gathers are L2 traffic (DESIGN.md K-SLICE)
-        prof_end(s, KC_SLICE, csr + 32.0 * 32 * kb->W4 + 4.0 * kb->W * cnt);
+        if (ex) {
+            prof_begin(s, KC_SLICE_EX);
+            if (cls == 0) k_slice_ex<false><<<dr.n_ex_blocks, 256, 0, s>>>(xa, sc, dd, cnt, counts);
+            else k_slice_ex<true><<<dr.n_ex_blocks, 256, 0, s>>>(xa, sc, dd, cnt, counts);
+            count_launch();
+            // example rows only: their CSR rows + 32 B T gathers + the cnt projected rows
+            prof_end(s, KC_SLICE_EX, 8.0 * kb->M + 36.0 * dr.E_ex + 4.0 * kb->MW * cnt);
+        } else {
+            prof_begin(s, KC_SLICE);
+            if (cls == 0) k_slice_tile<false><<<dr.n_tiles, 256, smem, s>>>(kd, sd, sc, dd, cnt, counts);
+            else k_slice_tile<true><<<dr.n_tiles, 256, smem, s>>>(kd, sd, sc, dd, cnt, counts);
+            count_launch();
+            // minimal DRAM bytes of one lane-packed pass: CSR once + T once (32 B per individual)
+            // + the cnt output rows; the 32 B-per-edge T gathers are L2 traffic (DESIGN.md K-SLICE)
+            prof_end(s, KC_SLICE, csr + 32.0 * 32 * kb->W4 + 4.0 * kb->W * cnt);
+        }
         off += cnt;
     }
     return HEDL_OK;

@@ -14,5 +14,5 @@ uint32_t slice_class(uint32_t pred, uint32_t n, uint32_t sat);
 // until the stream reaches this point); d_desc: the same on the device.
 hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream_t s, const KbDev &kd,
                       uint32_t dir, const RestrictDesc *h_desc, const RestrictDesc *d_desc, uint32_t n,
-                      hedl_counts *counts);
+                      hedl_counts *counts, bool ex);
 }  // namespace hedl
