@@ -35,6 +35,46 @@ hedl_status cuda_fail(const hedl_kb *kb, cudaError_t e, const char *where) {
     return HEDL_ERR_CUDA;
 }
 
+void *pool_take(const hedl_kb *kb, int role, size_t need, size_t *got) {
+    std::lock_guard<std::mutex> lk(kb->pool_mu);
+    auto &v = kb->pool[role];
+    int best = -1;
+    for (int i = 0; i < (int)v.size(); ++i)
+        if (v[i].second >= need && (best < 0 || v[i].second < v[best].second)) best = i;
+    if (best < 0) return nullptr;
+    void *p = v[best].first;
+    *got = v[best].second;
+    v.erase(v.begin() + best);
+    return p;
+}
+
+static void pool_free_one(int role, void *p) {
+    if (role == PR_PLAN_HOST) cudaFreeHost(p);
+    else cudaFree(p);
+}
+
+void pool_give(const hedl_kb *kb, int role, void *p, size_t bytes) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(kb->pool_mu);
+    auto &v = kb->pool[role];
+    v.push_back({p, bytes});
+    while (v.size() > 2) {                    // keep the two largest
+        size_t mi = 0;
+        for (size_t i = 1; i < v.size(); ++i)
+            if (v[i].second < v[mi].second) mi = i;
+        pool_free_one(role, v[mi].first);
+        v.erase(v.begin() + mi);
+    }
+}
+
+void pool_release_all(hedl_kb *kb) {
+    std::lock_guard<std::mutex> lk(kb->pool_mu);
+    for (int r = 0; r < PR_N; ++r) {
+        for (auto &e : kb->pool[r]) pool_free_one(r, e.first);
+        kb->pool[r].clear();
+    }
+}
+
 const char *kKClassName[KC_N] = {"bool", "restrict", "restrict_heavy", "drange", "cover_init", "gather",
                                  "slice_pack", "slice", "slice_heavy", "kb", "slice_ex"};
 

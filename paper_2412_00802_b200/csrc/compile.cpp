@@ -157,6 +157,26 @@ struct Memo {
     }
 };
 
+// dense window over the ids a shard mostly touches (post-order flattened trees keep a
+// root's nodes just below it), with the hash memo for everything else
+struct WinMemo {
+    uint32_t lo = 0, hi = 0;
+    std::vector<uint32_t> vals;
+    std::vector<uint8_t> st;
+    Memo far;
+    WinMemo(uint32_t lo_, uint32_t hi_, uint64_t expect) : lo(lo_), hi(hi_), far(expect / 16 + 64) {
+        vals.assign((size_t)(hi - lo) + 1, 0);
+        st.assign((size_t)(hi - lo) + 1, 0);
+    }
+    bool in(uint32_t k) const { return k >= lo && k <= hi; }
+    uint8_t state(uint32_t k) { return in(k) ? st[k - lo] : far.state(k); }
+    void set(uint32_t k, uint8_t s, uint32_t v) {
+        if (in(k)) { st[k - lo] = s; vals[k - lo] = v; }
+        else far.set(k, s, v);
+    }
+    uint32_t val(uint32_t k) { return in(k) ? vals[k - lo] : far.val(k); }
+};
+
 struct Shard {
     LocalDag dag;
     std::vector<uint32_t> root_ref;   // canonical (local) reference of each root of the shard
@@ -185,7 +205,16 @@ void canon_shard(const Input &in, uint32_t r0, uint32_t r1, Shard &sh) {
     const uint64_t expect = (uint64_t)in.n_nodes * (r1 - r0) / std::max<uint32_t>(1, in.n_roots) + 64;
     D.nodes.reserve(expect / 3 + 16);
     D.ops.reserve(expect / 2 + 16);
-    Memo memo(expect);
+    uint32_t rmin = 0xffffffffu, rmax = 0;
+    for (uint32_t ri = r0; ri < r1; ++ri) {
+        rmin = std::min(rmin, in.roots[ri]);
+        rmax = std::max(rmax, in.roots[ri]);
+    }
+    const uint64_t per_root = (uint64_t)in.n_nodes / std::max<uint32_t>(1, in.n_roots) + 16;
+    const uint32_t wlo = rmin == 0xffffffffu ? 0 : (uint32_t)(rmin > 4 * per_root ? rmin - 4 * per_root : 0);
+    const uint32_t whi = rmin == 0xffffffffu ? 0 : std::min<uint32_t>(rmax, in.n_nodes ? in.n_nodes - 1 : 0);
+    const bool dense_ok = (uint64_t)whi - wlo <= 8 * expect + (1u << 16);   // else the window is not worth it
+    WinMemo memo(wlo, dense_ok ? whi : wlo, expect);
     std::vector<std::pair<uint32_t, uint32_t>> stack;
     std::vector<uint32_t> tmp;
     sh.root_ref.resize(r1 - r0);
@@ -316,12 +345,34 @@ struct Global {
     uint64_t mask = 0;
     std::atomic<uint32_t> n_count{0};
     std::atomic<uint64_t> ops_count{0};
+    static constexpr uint32_t kNodeBlock = 4096, kOpsBlock = 16384;
 
-    uint32_t intern(CNode n, const uint32_t *o) {
+    // per-thread allocation cursor: ids and operand slots come in private blocks, so
+    // threads neither contend on the counters nor false-share node cache lines
+    struct Cursor {
+        uint32_t next = 0, end = 0;
+        uint64_t onext = 0, oend = 0;
+    };
+
+    uint32_t intern(CNode n, const uint32_t *o, Cursor &cur) {
         uint32_t mine = 0xffffffffu;
         auto materialise = [&]() {
-            mine = n_count.fetch_add(1, std::memory_order_relaxed);
-            const uint64_t ob = ops_count.fetch_add(n.op_count, std::memory_order_relaxed);
+            if (cur.next == cur.end) {
+                cur.next = n_count.fetch_add(kNodeBlock, std::memory_order_relaxed);
+                cur.end = cur.next + kNodeBlock;
+            }
+            mine = cur.next++;
+            uint64_t ob;
+            if (n.op_count > kOpsBlock) {
+                ob = ops_count.fetch_add(n.op_count, std::memory_order_relaxed);
+            } else {
+                if (cur.onext + n.op_count > cur.oend) {
+                    cur.onext = ops_count.fetch_add(kOpsBlock, std::memory_order_relaxed);
+                    cur.oend = cur.onext + kOpsBlock;
+                }
+                ob = cur.onext;
+                cur.onext += n.op_count;
+            }
             std::copy(o, o + n.op_count, p->ops.begin() + ob);
             n.op_begin = (uint32_t)ob;
             uint32_t lvl = 0;
@@ -432,8 +483,17 @@ extern "C" hedl_status hedl_compile(const hedl_kb *kb, const hedl_node *nodes, u
             tot_ops += s.dag.ops.size();
             for (const CNode &n : s.dag.nodes) maxl = std::max(maxl, n.level);
         }
-        p->nodes.resize(tot_nodes);
-        p->ops.resize(tot_ops);
+        const double tm0 = now_ms();
+        // capacity: every local node + materialised roots + one partly used block per thread and phase
+        const uint64_t cap_nodes = tot_nodes + (uint64_t)T * (maxl + 2) * Global::kNodeBlock;
+        uint64_t max_ops = 0;
+        for (auto &s : sh)
+            for (const CNode &n : s.dag.nodes) max_ops = std::max<uint64_t>(max_ops, n.op_count);
+        const uint64_t cap_ops = 2 * tot_ops + (uint64_t)T * (maxl + 2) * Global::kOpsBlock + max_ops;
+        if (cap_nodes >= (1ull << 29)) { delete p; return fail(HEDL_ERR_INVALID_ARG, "program too large"); }
+        p->nodes.resize(cap_nodes);
+        p->ops.resize(cap_ops);
+        std::vector<Global::Cursor> cursors(T);
         Global G{p, kb, !(flags & HEDL_COMPILE_NO_CSE)};
         if (G.cse) {
             uint64_t cap = 1024;
@@ -460,6 +520,8 @@ extern "C" hedl_status hedl_compile(const hedl_kb *kb, const hedl_node *nodes, u
         auto remap = [&](unsigned t, uint32_t r) {
             return ref_type(r) == RT_NODE ? mkref(RT_NODE, gmap[t][ref_id(r)], ref_comp(r)) : r;
         };
+        const double tm1 = now_ms();
+        timing_note("compile: merge setup", tm1 - tm0);
         for (uint32_t l = 0; l <= maxl; ++l) {
             run_threads(T, [&](unsigned t) {
                 const LocalDag &D = sh[t].dag;
@@ -470,7 +532,7 @@ extern "C" hedl_status hedl_compile(const hedl_kb *kb, const hedl_node *nodes, u
                     tmp.resize(n.op_count);
                     for (uint32_t q = 0; q < n.op_count; ++q) tmp[q] = remap(t, D.ops[n.op_begin + q]);
                     if (rewrite && (n.kind == NK_AND || n.kind == NK_OR)) std::sort(tmp.begin(), tmp.end());
-                    gmap[t][li] = G.intern(n, tmp.data());
+                    gmap[t][li] = G.intern(n, tmp.data(), cursors[t]);
                 }
             });
         }
@@ -484,12 +546,16 @@ extern "C" hedl_status hedl_compile(const hedl_kb *kb, const hedl_node *nodes, u
                     CNode n{};
                     n.kind = NK_AND;
                     n.op_count = 1;
-                    p->root_node[a + k] = G.intern(n, &r);
+                    p->root_node[a + k] = G.intern(n, &r, cursors[t]);
                 }
             }
         });
-        p->nodes.resize(G.n_count.load());
-        p->ops.resize(G.ops_count.load());
+        // ids reserved in a cursor block but never used are holes
+        for (const Global::Cursor &c : cursors)
+            for (uint32_t i = c.next; i < c.end; ++i) p->nodes[i].kind = NK_DEAD;
+        p->nodes.resize(std::min<uint64_t>(G.n_count.load(), cap_nodes));
+        p->ops.resize(std::min<uint64_t>(G.ops_count.load(), cap_ops));
+        timing_note("compile: merge levels+roots", now_ms() - tm1);
     }
     uint32_t maxl = 0;
     bool any = false;

@@ -66,13 +66,19 @@ Workspace *ws_of(hedl_program *p) {
     return (Workspace *)p->ws;
 }
 
-hedl_status grow(const hedl_kb *kb, cudaStream_t s, DevBuf &b, size_t need, bool zero) {
+hedl_status grow(const hedl_kb *kb, cudaStream_t s, DevBuf &b, size_t need, bool zero, int role) {
     if (b.bytes >= need) return HEDL_OK;
     HEDL_CUDA(kb, cudaStreamSynchronize(s));
     size_t sz = std::max(need, b.bytes * 5 / 4);
     if (b.p) cudaFree(b.p);
     b.p = nullptr;
     b.bytes = 0;
+    size_t got = 0;
+    if (void *q = pool_take(kb, role, need, &got)) {   // pooled buffers come back self-cleaned
+        b.p = q;
+        b.bytes = got;
+        return HEDL_OK;
+    }
     sz = (sz + 255) & ~size_t(255);
     cudaError_t e = cudaMalloc(&b.p, sz);
     if (e != cudaSuccess) {
@@ -97,12 +103,22 @@ void release_plan(PlanCache &pc) {
     pc = PlanCache();
 }
 
-hedl_status reserve_plan(PlanCache &pc, size_t bytes) {
+hedl_status reserve_plan(const hedl_kb *kb, PlanCache &pc, size_t bytes) {
     if (pc.cap >= bytes) return HEDL_OK;
     if (pc.host) cudaFreeHost(pc.host);
     if (pc.dev) cudaFree(pc.dev);
     pc.host = pc.dev = nullptr;
     pc.cap = 0;
+    size_t gh = 0, gd = 0;
+    void *h = pool_take(kb, PR_PLAN_HOST, bytes, &gh);
+    void *d = h ? pool_take(kb, PR_PLAN_DEV, bytes, &gd) : nullptr;
+    if (h && d) {
+        pc.host = h;
+        pc.dev = d;
+        pc.cap = std::min(gh, gd);
+        return HEDL_OK;
+    }
+    if (h) pool_give(kb, PR_PLAN_HOST, h, gh);
     const size_t cap = std::max(bytes, (size_t)4096) * 5 / 4;
     if (cudaMallocHost(&pc.host, cap) != cudaSuccess) { cudaGetLastError(); pc.host = nullptr; return fail(HEDL_ERR_OOM, "pinned plan"); }
     if (cudaMalloc(&pc.dev, cap) != cudaSuccess) {
@@ -234,6 +250,7 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
     auto &groups = tmp.groups;
     auto &members = tmp.members;
     if (sizes_only) {
+        const double ts0 = now_ms();
         cover_of_node.assign(nn, -1);
         cover_of_root.resize(nroots);
         uint32_t ncov = 0;
@@ -260,6 +277,7 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                 else need_full[local[ref_id(o)]] = 1;
             }
         }
+        const double ts1 = now_ms();
         slot.assign(nn, 0);
         pslot.assign(nn, 0);
         uint32_t nrows = 0, nprows = 0;
@@ -344,6 +362,8 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
         cp.blob_bytes = align_up(cp.off_rows + (out_bits ? nroots * sizeof(void *) : 0), 256);
         cp.blob_off = *blob_cursor;
         *blob_cursor += cp.blob_bytes;
+        timing_note("plan: covers+demands", ts1 - ts0);
+        timing_note("plan: slots+groups", now_ms() - ts1);
         return;
     }
 
@@ -529,12 +549,14 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
             max_np = std::max<size_t>(max_np, cp.nprows);
             max_cov = std::max<size_t>(max_cov, cp.ncov);
         }
-        if ((st = grow(kb, s, w->rows, max_nn * row_bytes + 16, false))) return st;
-        if ((st = grow(kb, s, w->prows, max_np * kb->MW4 * 4 + 16, false))) return st;
-        if ((st = grow(kb, s, w->heavy, heavy_need, true))) return st;
-        if ((st = grow(kb, s, w->counts, max_cov * sizeof(hedl_counts), false))) return st;
-        if ((st = reserve_plan(pc, std::max<size_t>(cursor, 256)))) return st;
+        const double tb = now_ms();
+        if ((st = grow(kb, s, w->rows, max_nn * row_bytes + 16, false, PR_ROWS))) return st;
+        if ((st = grow(kb, s, w->prows, max_np * kb->MW4 * 4 + 16, false, PR_PROWS))) return st;
+        if ((st = grow(kb, s, w->heavy, heavy_need, true, PR_HEAVY))) return st;
+        if ((st = grow(kb, s, w->counts, max_cov * sizeof(hedl_counts), false, PR_COUNTS))) return st;
+        if ((st = reserve_plan(kb, pc, std::max<size_t>(cursor, 256)))) return st;
         const double t2 = now_ms();
+        timing_note("plan: buffers", t2 - tb);
         pc.r0 = r0; pc.r1 = r1; pc.bits = bits; pc.eflags = eflags;
         pc.rows_base = w->rows.p;
         pc.heavy_base = w->heavy.p;
@@ -546,6 +568,7 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
             fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, (uint32_t *)w->rows.p, (uint32_t *)w->prows.p, local,
                        (char *)pc.host, &cur, &heavy_need, false, tmps[c]);
             tmps[c] = ChunkTmp();   // release the chunk's planning state
+            timing_note("plan: fill chunk", now_ms() - t2);
             HEDL_CUDA(kb, cudaMemcpyAsync((char *)pc.dev + cp.blob_off, (char *)pc.host + cp.blob_off, cp.blob_bytes,
                                           cudaMemcpyHostToDevice, s));
             count_io(cp.blob_bytes, 0);
@@ -623,8 +646,12 @@ extern "C" hedl_status hedl_program_free(hedl_program *p) {
         Workspace *w = (Workspace *)p->ws;
         DeviceGuard dg(p->kb->device);
         if (w->done) cudaEventSynchronize(w->done);
-        for (DevBuf *b : {&w->rows, &w->prows, &w->heavy, &w->counts, &w->slice})
-            if (b->p) cudaFree(b->p);
+        const int roles[] = {PR_ROWS, PR_PROWS, PR_HEAVY, PR_COUNTS, PR_SLICE};
+        int ri = 0;
+        for (DevBuf *b : {&w->rows, &w->prows, &w->heavy, &w->counts, &w->slice}) pool_give(p->kb, roles[ri++], b->p, b->bytes);
+        pool_give(p->kb, PR_PLAN_HOST, w->plan.host, w->plan.cap);
+        pool_give(p->kb, PR_PLAN_DEV, w->plan.dev, w->plan.cap);
+        w->plan.host = w->plan.dev = nullptr;
         release_plan(w->plan);
         if (w->done) cudaEventDestroy(w->done);
         delete w;

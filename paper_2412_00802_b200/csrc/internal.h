@@ -110,6 +110,10 @@ struct hedl_kb {
     std::vector<void *> allocs;
     uint64_t device_bytes = 0;
     std::atomic<bool> poisoned{false};
+    // buffers released by freed programs, reused by the next ones (no cudaMalloc /
+    // cudaMallocHost / memset per program); accumulator buffers return self-cleaned
+    mutable std::mutex pool_mu;
+    mutable std::vector<std::pair<void *, size_t>> pool[8];
     std::vector<double> dir_bytes;  // 4(N+1) + 4E per direction
     std::vector<double> data_bytes; // 4(N+1) + 4V per property
 };
@@ -146,6 +150,12 @@ hedl_status cuda_fail(const hedl_kb *kb, cudaError_t e, const char *where);
         cudaError_t _e = (call);                             \
         if (_e != cudaSuccess) return hedl::cuda_fail(kb, _e, #call); \
     } while (0)
+
+// ---- workspace pool (per KB) ---------------------------------------------------
+enum PoolRole { PR_ROWS, PR_PROWS, PR_HEAVY, PR_COUNTS, PR_SLICE, PR_PLAN_DEV, PR_PLAN_HOST, PR_N };
+void *pool_take(const hedl_kb *kb, int role, size_t need, size_t *got);
+void pool_give(const hedl_kb *kb, int role, void *p, size_t bytes);
+void pool_release_all(hedl_kb *kb);
 
 // ---- host phase timing (HEDL_TIMING=1 prints to stderr) ---------------------------
 bool timing_enabled();

@@ -100,6 +100,7 @@ void free_kb(hedl_kb *kb) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(kb->device);
+    pool_release_all(kb);
     for (void *p : kb->allocs) cudaFree(p);
     cudaSetDevice(prev);
     delete kb;

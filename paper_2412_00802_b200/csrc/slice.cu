@@ -40,7 +40,21 @@ struct SliceScratch {
     uint32_t *hcnt;               // [n_heavy][256]   per-lane counts
     uint32_t *ticket;             // [n_heavy]
     uint32_t *hout;               // [n_heavy][8]     finished heavy rows
+    uint64_t t_stride;            // uint4 between the T of consecutive packs of one launch
+    uint64_t h_stride;            // heavy rows between the accumulators of consecutive packs
+    __device__ __forceinline__ SliceScratch at(uint32_t p) const {
+        SliceScratch r = *this;
+        r.T += p * t_stride;
+        r.hacc += p * h_stride * 8;
+        r.hcnt += p * h_stride * 256;
+        r.ticket += p * h_stride;
+        r.hout += p * h_stride * 8;
+        return r;
+    }
 };
+
+// pack p of a run of consecutive same-class descriptors: descs [256p, min(256p + 256, run))
+__device__ __forceinline__ uint32_t pack_count(uint32_t run, uint32_t p) { return min(256u, run - 256u * p); }
 
 // per-pack lane constants, built in shared memory from the node descriptors
 struct PackConst {
@@ -184,32 +198,48 @@ __device__ __forceinline__ void scan_edges(Acc<COUNT> &acc, const uint32_t *__re
 }
 
 // ------------------------------------------------------------------------------
-// T[y] for the pack: warp per 4 consecutive words (128 individuals).
-__global__ void __launch_bounds__(256) k_slice_pack(KbDev kb, const RestrictDesc *__restrict__ d, uint32_t count,
-                                                    uint4 *__restrict__ T) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t w0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 4;
-    if (w0 >= kb.W4) return;
-    uint4 v[LW];
-#pragma unroll
-    for (int g = 0; g < LW; ++g) {
-        const uint32_t j = g * 32 + lane;
-        v[g] = make_uint4(0, 0, 0, 0);
-        if (j < count) {
-            const RestrictDesc r = d[j];
-            v[g] = __ldg(reinterpret_cast<const uint4 *>(r.child + w0));
-            v[g].x ^= r.cmask; v[g].y ^= r.cmask; v[g].z ^= r.cmask; v[g].w ^= r.cmask;
+// T[y] for the packs of a run (blockIdx.y = pack): a CTA stages 256 child rows x 64
+// words (2048 individuals) in shared memory with coalesced 128 B row loads, then
+// warps transpose 32x32 bit blocks and write each individual's 32 B of T.
+constexpr uint32_t PK_WORDS = 64, PK_STRIDE = PK_WORDS + 1;
+
+__global__ void __launch_bounds__(256) k_slice_pack(KbDev kb, const RestrictDesc *__restrict__ d_run, uint32_t run,
+                                                    uint4 *__restrict__ T_base, uint64_t t_stride) {
+    extern __shared__ uint32_t sm[];                      // [256][PK_STRIDE]
+    __shared__ const uint32_t *s_row[256];
+    __shared__ uint32_t s_cm[256];
+    const uint32_t p = blockIdx.y;
+    const RestrictDesc *d = d_run + 256u * p;
+    const uint32_t count = pack_count(run, p);
+    uint4 *T = T_base + p * t_stride;
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t w0 = blockIdx.x * PK_WORDS;
+    // the 256 child rows first, so the row loads below are independent (no desc->row chain)
+    s_row[threadIdx.x] = threadIdx.x < count ? d[threadIdx.x].child : nullptr;
+    s_cm[threadIdx.x] = threadIdx.x < count ? d[threadIdx.x].cmask : 0u;
+    __syncthreads();
+    const bool lo_ok = w0 + lane < kb.W4, hi_ok = w0 + lane + 32 < kb.W4;
+#pragma unroll 8
+    for (uint32_t rr = 0; rr < 32; ++rr) {
+        const uint32_t r = wid * 32 + rr;
+        const uint32_t *row = s_row[r];
+        const uint32_t cm = s_cm[r];
+        uint32_t v0 = 0, v1 = 0;
+        if (row) {
+            if (lo_ok) v0 = __ldg(row + w0 + lane) ^ cm;
+            if (hi_ok) v1 = __ldg(row + w0 + lane + 32) ^ cm;
         }
+        sm[r * PK_STRIDE + lane] = v0;
+        sm[r * PK_STRIDE + lane + 32] = v1;
     }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    __syncthreads();
+    for (uint32_t k = 0; k < 8; ++k) {
+        const uint32_t wd = wid * 8 + k, w = w0 + wd;
+        if (w >= kb.W4) break;
         uint32_t o[LW];
 #pragma unroll
-        for (int g = 0; g < LW; ++g) {
-            const uint32_t x = k == 0 ? v[g].x : k == 1 ? v[g].y : k == 2 ? v[g].z : v[g].w;
-            o[g] = warp_transpose(x, lane);
-        }
-        const uint64_t y = (uint64_t)(w0 + k) * 32 + lane;
+        for (int g = 0; g < LW; ++g) o[g] = warp_transpose(sm[(g * 32 + lane) * PK_STRIDE + wd], lane);
+        const uint64_t y = (uint64_t)w * 32 + lane;
         T[2 * y] = make_uint4(o[0], o[1], o[2], o[3]);
         T[2 * y + 1] = make_uint4(o[4], o[5], o[6], o[7]);
     }
@@ -218,8 +248,11 @@ __global__ void __launch_bounds__(256) k_slice_pack(KbDev kb, const RestrictDesc
 // ------------------------------------------------------------------------------
 // heavy rows: CTA (256 threads = 128 lane pairs) per chunk of <= kHeavyChunk edges.
 template <bool COUNT>
-__global__ void __launch_bounds__(256) k_slice_heavy(SliceDir dir, SliceScratch sc, const RestrictDesc *__restrict__ d,
-                                                     uint32_t count) {
+__global__ void __launch_bounds__(256) k_slice_heavy(SliceDir dir, SliceScratch sc0, const RestrictDesc *__restrict__ d_run,
+                                                     uint32_t run) {
+    const SliceScratch sc = sc0.at(blockIdx.y);
+    const RestrictDesc *d = d_run + 256u * blockIdx.y;
+    const uint32_t count = pack_count(run, blockIdx.y);
     __shared__ PackConst pc;
     __shared__ uint32_t red[8][2][COUNT ? NPL : 1][HW];
     __shared__ uint32_t fin[2][COUNT ? NPL : 1][HW];
@@ -394,8 +427,11 @@ struct ExArgs {
 };
 
 template <bool COUNT>
-__global__ void __launch_bounds__(256, COUNT ? 3 : 4) k_slice_ex(ExArgs a, SliceScratch sc, const RestrictDesc *__restrict__ d,
-                                                                 uint32_t count, hedl_counts *counts) {
+__global__ void __launch_bounds__(256, COUNT ? 3 : 4) k_slice_ex(ExArgs a, SliceScratch sc0, const RestrictDesc *__restrict__ d_run,
+                                                                 uint32_t run, hedl_counts *counts) {
+    const SliceScratch sc = sc0.at(blockIdx.y);
+    const RestrictDesc *d = d_run + 256u * blockIdx.y;
+    const uint32_t count = pack_count(run, blockIdx.y);
     __shared__ PackConst pc;
     __shared__ uint32_t ot[128 * TROW];
     const uint32_t b = blockIdx.x, r0 = b * 128;
@@ -473,80 +509,109 @@ uint32_t slice_class(uint32_t pred, uint32_t n, uint32_t sat) {
 hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream_t s, const KbDev &kd, uint32_t dirid,
                       const RestrictDesc *h_desc, const RestrictDesc *d_desc, uint32_t n, hedl_counts *counts, bool ex) {
     const hedl_dir &dr = kb->dirs[dirid];
+    if (ex && !kb->M) return HEDL_OK;                     // no examples: nothing to evaluate
     const size_t t_bytes = (size_t)kb->W4 * 32 * 32;
-    // one fixed layout for every direction (sized by the largest heavy list), so the
-    // self-cleaning accumulators of one direction never alias another's results
-    size_t nh = 0;
-    for (const hedl_dir &x : kb->dirs) nh = std::max<size_t>(nh, x.n_heavy);
-    const size_t need = t_bytes + nh * (LW * 4 + 256 * 4 + 4 + LW * 4) + 256;
+    // one fixed layout for every direction (sized by the largest heavy lists), so the
+    // self-cleaning accumulators of one direction never alias another's results:
+    //   [T x kMaxBatch][full-pack heavy scratch (nh)][EX heavy scratch (kMaxBatch x nhx)]
+    size_t nh = 0, nhx = 0;
+    for (const hedl_dir &x : kb->dirs) {
+        nh = std::max<size_t>(nh, x.n_heavy);
+        nhx = std::max<size_t>(nhx, x.n_ex_heavy);
+    }
+    const size_t per_h = (LW + 256 + 1 + LW) * 4;
+    const uint32_t max_batch = (uint32_t)std::max<size_t>(1, std::min<size_t>(128, (4ull << 30) / std::max<size_t>(t_bytes, 1)));
+    const size_t off_hf = t_bytes * max_batch, off_hx = off_hf + nh * per_h;
+    const size_t need = off_hx + (size_t)max_batch * nhx * per_h + 256;
     if (*ws_bytes < need) {
         HEDL_CUDA(kb, cudaStreamSynchronize(s));
         if (*ws) cudaFree(*ws);
         *ws = nullptr;
         *ws_bytes = 0;
-        if (cudaMalloc(ws, need) != cudaSuccess) { cudaGetLastError(); *ws = nullptr; return fail(HEDL_ERR_OOM, "slice workspace"); }
-        HEDL_CUDA(kb, cudaMemsetAsync(*ws, 0, need, s));
-        *ws_bytes = need;
+        size_t got = 0;
+        if (void *q = pool_take(kb, PR_SLICE, need, &got)) {   // self-cleaned accumulators
+            *ws = q;
+            *ws_bytes = got;
+        } else {
+            if (cudaMalloc(ws, need) != cudaSuccess) { cudaGetLastError(); *ws = nullptr; return fail(HEDL_ERR_OOM, "slice workspace"); }
+            HEDL_CUDA(kb, cudaMemsetAsync(*ws, 0, need, s));
+            *ws_bytes = need;
+        }
     }
     char *base = (char *)*ws;
-    SliceScratch sc;
-    sc.T = (uint4 *)base;
-    sc.hacc = (uint32_t *)(base + t_bytes);
-    sc.hcnt = sc.hacc + nh * LW;
-    sc.ticket = sc.hcnt + nh * 256;
-    sc.hout = sc.ticket + nh;
+    // field-major accumulators with room for `npacks` packs of `nrows` heavy rows each
+    auto scratch = [&](size_t off, size_t nrows, size_t npacks) {
+        const size_t cap = nrows * npacks;
+        SliceScratch sc;
+        sc.T = (uint4 *)base;
+        sc.hacc = (uint32_t *)(base + off);
+        sc.hcnt = sc.hacc + cap * LW;
+        sc.ticket = sc.hcnt + cap * 256;
+        sc.hout = sc.ticket + cap;
+        sc.t_stride = t_bytes / 16;
+        sc.h_stride = 0;
+        return sc;
+    };
     SliceDir sd{dr.row_ptr, dr.col, dr.tiles, dr.order, dr.heavy_x, dr.heavy_nchunks, dr.chunks,
                 dr.n_heavy, dr.n_chunks, dr.n_tiles};
     SliceDir sdx{dr.row_ptr, dr.col, nullptr, nullptr, dr.ex_hx, dr.ex_hn, dr.ex_chunks, dr.n_ex_heavy, dr.n_ex_chunks, 0};
     const ExArgs xa{dr.row_ptr, dr.col, dr.ex_tiles, dr.ex_order, kb->ex_ids, dr.ex_hrank, kb->ppos, kb->pneg, kb->MW4};
-    if (ex && !kb->M) return HEDL_OK;                     // no examples: nothing to evaluate
     const size_t smem = sizeof(PackConst) + 1024 * TROW * 4;
+    const size_t pk_smem = 256 * PK_STRIDE * 4;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(k_slice_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_slice_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_slice_tile<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaFuncSetAttribute(k_slice_tile<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_slice_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pk_smem);
+        cudaFuncSetAttribute(k_slice_pack, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr_set = true;
     }
     const double csr = 4.0 * (kb->N + 1) + 4.0 * dr.E;
     for (uint32_t off = 0; off < n;) {
+        // a run of consecutive same-class descriptors: full packs go one pack per launch
+        // (T stays L2-resident for the tile sweep); EX packs go up to max_batch per launch
         const uint32_t cls = slice_class(h_desc[off].pred, h_desc[off].n, h_desc[off].sat);
-        uint32_t cnt = 1;
-        while (off + cnt < n && cnt < 256 &&
-               slice_class(h_desc[off + cnt].pred, h_desc[off + cnt].n, h_desc[off + cnt].sat) == cls)
-            ++cnt;
+        const uint32_t cap = ex ? 256u * max_batch : 256u;
+        uint32_t run = 1;
+        while (off + run < n && run < cap &&
+               slice_class(h_desc[off + run].pred, h_desc[off + run].n, h_desc[off + run].sat) == cls)
+            ++run;
+        const uint32_t packs = (run + 255) / 256;
         const RestrictDesc *dd = d_desc + off;
+        SliceScratch sc = ex ? scratch(off_hx, nhx, max_batch) : scratch(off_hf, nh, 1);
+        if (ex) sc.h_stride = nhx;
         prof_begin(s, KC_SLICE_IN);
-        k_slice_pack<<<cdiv(kb->W4, 32), 256, 0, s>>>(kd, dd, cnt, sc.T);
+        k_slice_pack<<<dim3(cdiv(kb->W4, PK_WORDS), packs), 256, pk_smem, s>>>(kd, dd, run, sc.T, sc.t_stride);
         count_launch();
-        prof_end(s, KC_SLICE_IN, 4.0 * kb->W * cnt + 32.0 * 32 * kb->W4);
+        prof_end(s, KC_SLICE_IN, 4.0 * kb->W * run + 32.0 * 32 * kb->W4 * packs);
         const SliceDir &hd = ex ? sdx : sd;
         if (hd.n_chunks) {
             prof_begin(s, KC_SLICE_HEAVY);
-            if (cls == 0) k_slice_heavy<false><<<hd.n_chunks, 256, 0, s>>>(hd, sc, dd, cnt);
-            else k_slice_heavy<true><<<hd.n_chunks, 256, 0, s>>>(hd, sc, dd, cnt);
+            if (cls == 0) k_slice_heavy<false><<<dim3(hd.n_chunks, packs), 256, 0, s>>>(hd, sc, dd, run);
+            else k_slice_heavy<true><<<dim3(hd.n_chunks, packs), 256, 0, s>>>(hd, sc, dd, run);
             count_launch();
             const double eh = ex ? (double)dr.E_ex_heavy : (double)dr.E_heavy;
-            prof_end(s, KC_SLICE_HEAVY, 4.0 * eh + 32.0 * eh);
+            prof_end(s, KC_SLICE_HEAVY, (4.0 * eh + 32.0 * eh) * packs);
         }
         if (ex) {
             prof_begin(s, KC_SLICE_EX);
-            if (cls == 0) k_slice_ex<false><<<dr.n_ex_blocks, 256, 0, s>>>(xa, sc, dd, cnt, counts);
-            else k_slice_ex<true><<<dr.n_ex_blocks, 256, 0, s>>>(xa, sc, dd, cnt, counts);
+            if (cls == 0) k_slice_ex<false><<<dim3(dr.n_ex_blocks, packs), 256, 0, s>>>(xa, sc, dd, run, counts);
+            else k_slice_ex<true><<<dim3(dr.n_ex_blocks, packs), 256, 0, s>>>(xa, sc, dd, run, counts);
             count_launch();
-            // example rows only: their CSR rows + 32 B T gathers + the cnt projected rows
-            prof_end(s, KC_SLICE_EX, 8.0 * kb->M + 36.0 * dr.E_ex + 4.0 * kb->MW * cnt);
+            // example rows only: their CSR rows + 32 B T gathers + the projected rows
+            prof_end(s, KC_SLICE_EX, (8.0 * kb->M + 36.0 * dr.E_ex) * packs + 4.0 * kb->MW * run);
         } else {
             prof_begin(s, KC_SLICE);
-            if (cls == 0) k_slice_tile<false><<<dr.n_tiles, 256, smem, s>>>(kd, sd, sc, dd, cnt, counts);
-            else k_slice_tile<true><<<dr.n_tiles, 256, smem, s>>>(kd, sd, sc, dd, cnt, counts);
+            if (cls == 0) k_slice_tile<false><<<dr.n_tiles, 256, smem, s>>>(kd, sd, sc, dd, run, counts);
+            else k_slice_tile<true><<<dr.n_tiles, 256, smem, s>>>(kd, sd, sc, dd, run, counts);
             count_launch();
             // minimal DRAM bytes of one lane-packed pass: CSR once + T once (32 B per individual)
-            // + the cnt output rows; the 32 B-per-edge T gathers are L2 traffic (DESIGN.md K-SLICE)
-            prof_end(s, KC_SLICE, csr + 32.0 * 32 * kb->W4 + 4.0 * kb->W * cnt);
+            // + the output rows; the 32 B-per-edge T gathers are L2 traffic (DESIGN.md K-SLICE)
+            prof_end(s, KC_SLICE, csr + 32.0 * 32 * kb->W4 + 4.0 * kb->W * run);
         }
-        off += cnt;
+        off += run;
     }
     return HEDL_OK;
 }

@@ -95,3 +95,23 @@ def test_slice_tail_sizes():
         rng = np.random.default_rng(n)
         trees = [hyps.random_tree(rng, abox.kb_shape(kb), depth=3, n_max=5) for _ in range(64)]
         assert_parity(kb, trees, eflags=FORCE, tag=f"slice N={n}")
+
+
+def test_slice_ex_batched_heavy_examples():
+    """EX packs batched several per launch, with heavy example rows (the hub is a positive example)."""
+    from synth.format import kb_from_sets
+    rng = np.random.default_rng(77)
+    n = 6000
+    concepts = [[i for i in range(n) if rng.random() < 0.4] for _ in range(12)]
+    pairs = [(0, int(y)) for y in rng.choice(n, 3000, replace=False)]          # heavy hub 0
+    pairs += [(1, int(y)) for y in rng.choice(n, 1500, replace=False)]         # heavy row 1
+    pairs += [(int(x), int(rng.integers(n))) for x in rng.integers(2, n, 30000)]
+    kb = kb_from_sets(n, concepts, [pairs], [], [0, 5, 7] + list(range(100, 160)), [1, 6] + list(range(200, 260)))
+    trees = []
+    for c in range(12):
+        for inv in (False, True):
+            for k in range(30):
+                child = ("AND", [("ATOM", c), ("ATOM", (c + k) % 12)]) if k % 2 else ("OR", [("ATOM", c), ("NOT", ("ATOM", k % 12))])
+                trees.append(("EXISTS", 0, inv, child) if k % 3 else ("MIN", k % 17, 0, inv, child))
+    assert len(trees) > 512
+    assert_parity(kb, trees, tag="ex batched heavy")
