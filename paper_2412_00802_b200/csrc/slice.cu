@@ -199,46 +199,55 @@ __device__ __forceinline__ void scan_edges(Acc<COUNT> &acc, const uint32_t *__re
 
 // ------------------------------------------------------------------------------
 // T[y] for the packs of a run (blockIdx.y = pack): a CTA stages 256 child rows x 64
-// words (2048 individuals) in shared memory with coalesced 128 B row loads, then
-// warps transpose 32x32 bit blocks and write each individual's 32 B of T.
-constexpr uint32_t PK_WORDS = 64, PK_STRIDE = PK_WORDS + 1;
+// words (2048 individuals) in shared memory with one TMA bulk copy per row
+// (cp.async.bulk, completion counted on an mbarrier), then warps transpose 32x32 bit
+// blocks (complement masks applied on the way) and write each individual's 32 B of T.
+constexpr uint32_t PK_WORDS = 64, PK_STRIDE = 68;        // 272 B rows: 16 B aligned for TMA
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
 
 __global__ void __launch_bounds__(256) k_slice_pack(KbDev kb, const RestrictDesc *__restrict__ d_run, uint32_t run,
                                                     uint4 *__restrict__ T_base, uint64_t t_stride) {
-    extern __shared__ uint32_t sm[];                      // [256][PK_STRIDE]
-    __shared__ const uint32_t *s_row[256];
+    extern __shared__ __align__(16) uint32_t sm[];        // [256][PK_STRIDE]
     __shared__ uint32_t s_cm[256];
+    __shared__ __align__(8) uint64_t mbar;
     const uint32_t p = blockIdx.y;
     const RestrictDesc *d = d_run + 256u * p;
     const uint32_t count = pack_count(run, p);
     uint4 *T = T_base + p * t_stride;
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t w0 = blockIdx.x * PK_WORDS;
-    // the 256 child rows first, so the row loads below are independent (no desc->row chain)
-    s_row[threadIdx.x] = threadIdx.x < count ? d[threadIdx.x].child : nullptr;
-    s_cm[threadIdx.x] = threadIdx.x < count ? d[threadIdx.x].cmask : 0u;
-    __syncthreads();
-    const bool lo_ok = w0 + lane < kb.W4, hi_ok = w0 + lane + 32 < kb.W4;
-#pragma unroll 8
-    for (uint32_t rr = 0; rr < 32; ++rr) {
-        const uint32_t r = wid * 32 + rr;
-        const uint32_t *row = s_row[r];
-        const uint32_t cm = s_cm[r];
-        uint32_t v0 = 0, v1 = 0;
-        if (row) {
-            if (lo_ok) v0 = __ldg(row + w0 + lane) ^ cm;
-            if (hi_ok) v1 = __ldg(row + w0 + lane + 32) ^ cm;
-        }
-        sm[r * PK_STRIDE + lane] = v0;
-        sm[r * PK_STRIDE + lane + 32] = v1;
+    const uint32_t nwords = min(PK_WORDS, kb.W4 - w0);    // multiple of 4 (W4 and w0 are)
+    const uint32_t seg = nwords * 4;
+    const uint32_t mb = smem_u32(&mbar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(seg * count) : "memory");
     }
-    __syncthreads();
+    const uint32_t t = threadIdx.x;
+    s_cm[t] = t < count ? d[t].cmask : 0u;
+    if (t >= count)
+        for (uint32_t i = 0; i < PK_WORDS; ++i) sm[t * PK_STRIDE + i] = 0u;
+    __syncthreads();                                      // barrier initialised and armed
+    if (t < count) {
+        const uint32_t *src = d[t].child + w0;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(smem_u32(sm + t * PK_STRIDE)), "l"(src), "r"(seg), "r"(mb) : "memory");
+    }
+    asm volatile("{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n @!P1 bra WAIT_%=;\n}"
+                 ::"r"(mb) : "memory");
     for (uint32_t k = 0; k < 8; ++k) {
         const uint32_t wd = wid * 8 + k, w = w0 + wd;
         if (w >= kb.W4) break;
         uint32_t o[LW];
 #pragma unroll
-        for (int g = 0; g < LW; ++g) o[g] = warp_transpose(sm[(g * 32 + lane) * PK_STRIDE + wd], lane);
+        for (int g = 0; g < LW; ++g) {
+            const uint32_t r = g * 32 + lane;
+            o[g] = warp_transpose(sm[r * PK_STRIDE + wd] ^ s_cm[r], lane);
+        }
         const uint64_t y = (uint64_t)w * 32 + lane;
         T[2 * y] = make_uint4(o[0], o[1], o[2], o[3]);
         T[2 * y + 1] = make_uint4(o[4], o[5], o[6], o[7]);
