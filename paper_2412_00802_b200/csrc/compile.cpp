@@ -63,8 +63,8 @@ double node_bytes(const hedl_kb *kb, const CNode &n) {
 
 // ---- single-threaded DAG of one shard ---------------------------------------------
 struct LocalDag {
-    std::vector<CNode> nodes;
-    std::vector<uint32_t> ops;
+    std::vector<CNode, NoInitAlloc<CNode>> nodes;
+    std::vector<uint32_t, NoInitAlloc<uint32_t>> ops;
     std::vector<uint32_t> table;   // open addressing: node id + 1, 0 = empty
     uint64_t mask = 0;
     bool cse = true;
@@ -341,7 +341,8 @@ struct Global {
     hedl_program *p;
     const hedl_kb *kb;
     bool cse;
-    std::unique_ptr<std::atomic<uint32_t>[]> table;
+    struct FreeDel { void operator()(std::atomic<uint32_t> *q) const { std::free(q); } };
+    std::unique_ptr<std::atomic<uint32_t>, FreeDel> table;
     uint64_t mask = 0;
     std::atomic<uint32_t> n_count{0};
     std::atomic<uint64_t> ops_count{0};
@@ -392,11 +393,11 @@ struct Global {
         }
         uint64_t h = hash_node(n, o) & mask;
         for (;;) {
-            uint32_t v = table[h].load(std::memory_order_acquire);
+            uint32_t v = table.get()[h].load(std::memory_order_acquire);
             if (v == 0) {
                 if (mine == 0xffffffffu) materialise();
                 uint32_t expected = 0;
-                if (table[h].compare_exchange_strong(expected, mine + 1, std::memory_order_acq_rel,
+                if (table.get()[h].compare_exchange_strong(expected, mine + 1, std::memory_order_acq_rel,
                                                      std::memory_order_acquire))
                     return mine;
                 v = expected;
@@ -498,8 +499,8 @@ extern "C" hedl_status hedl_compile(const hedl_kb *kb, const hedl_node *nodes, u
         if (G.cse) {
             uint64_t cap = 1024;
             while (cap < tot_nodes * 2) cap <<= 1;
-            G.table.reset(new std::atomic<uint32_t>[cap]);
-            for (uint64_t i = 0; i < cap; ++i) G.table[i].store(0, std::memory_order_relaxed);
+            // calloc: zero pages come lazily from the OS (first touch by the merging threads)
+            G.table.reset(reinterpret_cast<std::atomic<uint32_t> *>(std::calloc(cap, sizeof(uint32_t))));
             G.mask = cap - 1;
         }
         std::vector<std::vector<uint32_t>> gmap(T);

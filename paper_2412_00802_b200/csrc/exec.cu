@@ -11,6 +11,8 @@
 // kept device-resident in the program, and replayed by later calls.  Counts come
 // back with one D2H per call (the paper's single cudaMemcpyAsync).
 #include <algorithm>
+#include <atomic>
+#include <thread>
 
 #include "internal.h"
 #include "slice.h"
@@ -142,19 +144,105 @@ struct Group {
     bool ex = false;
 };
 
-// ---- planning -------------------------------------------------------------------
-// order key: level, kind, direction / property, lane-pack class, node id
-inline uint64_t order_key(const CNode &n, uint32_t id) {
-    const uint64_t cls = n.kind == NK_RESTRICT ? slice_class(n.pred, n.n, n.sat) : 0;
-    return ((uint64_t)std::min<uint32_t>(n.level, 4095) << 52) | ((uint64_t)(n.kind & 3) << 50) |
-           ((uint64_t)n.dir << 34) | (cls << 32) | id;
+// ---- planning (host threads, as the paper generates plans in parallel) ----
+unsigned plan_threads() {
+    static const unsigned t = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    return t;
 }
 
+// f(begin, end) over [0, n) in chunks of `grain`, dynamically scheduled over host threads
+template <class F>
+void par_for(size_t n, size_t grain, F f) {
+    const unsigned T = (unsigned)std::min<size_t>(plan_threads(), (n + grain - 1) / std::max<size_t>(grain, 1));
+    if (T <= 1) { if (n) f((size_t)0, n); return; }
+    std::atomic<size_t> next{0};
+    auto work = [&]() {
+        for (;;) {
+            const size_t b = next.fetch_add(grain);
+            if (b >= n) break;
+            f(b, std::min(n, b + grain));
+        }
+    };
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < T; ++t) th.emplace_back(work);
+    work();
+    for (auto &x : th) x.join();
+}
+
+// out[k] = rank of k among the k' < k with flag(k') (for flagged k); returns the count
+template <class Flag, class Out>
+uint32_t par_rank(size_t n, Flag flag, Out &out) {
+    const size_t C = 64;
+    std::vector<uint32_t> cnt(C + 1, 0);
+    par_for(C, 1, [&](size_t c0, size_t c1) {
+        for (size_t c = c0; c < c1; ++c)
+            for (size_t k = n * c / C; k < n * (c + 1) / C; ++k) cnt[c + 1] += flag(k) ? 1u : 0u;
+    });
+    for (size_t c = 0; c < C; ++c) cnt[c + 1] += cnt[c];
+    par_for(C, 1, [&](size_t c0, size_t c1) {
+        for (size_t c = c0; c < c1; ++c) {
+            uint32_t r = cnt[c];
+            for (size_t k = n * c / C; k < n * (c + 1) / C; ++k)
+                if (flag(k)) out[k] = r++;
+        }
+    });
+    return cnt[C];
+}
+
+// order key: level, kind, direction / property, lane-pack class (node id breaks ties)
+inline uint32_t group_key(const CNode &n) {
+    const uint32_t cls = n.kind == NK_RESTRICT ? slice_class(n.pred, n.n, n.sat) : 0;
+    return (std::min<uint32_t>(n.level, 4095) << 20) | ((uint32_t)(n.kind & 3) << 18) | ((uint32_t)n.dir << 2) | cls;
+}
+
+// stable bucket sort of `list` (ascending ids) by group_key: parallel histogram + scatter
 void sort_by_key(const hedl_program *p, std::vector<uint32_t> &list) {
-    std::vector<uint64_t> keys(list.size());
-    for (size_t k = 0; k < list.size(); ++k) keys[k] = order_key(p->nodes[list[k]], list[k]);
-    std::sort(keys.begin(), keys.end());
-    for (size_t k = 0; k < list.size(); ++k) list[k] = (uint32_t)keys[k];
+    const size_t n = list.size();
+    if (n < (1u << 15)) {
+        std::stable_sort(list.begin(), list.end(), [&](uint32_t a, uint32_t b) {
+            return group_key(p->nodes[a]) < group_key(p->nodes[b]);
+        });
+        return;
+    }
+    std::vector<uint32_t> key(n);
+    par_for(n, 1 << 14, [&](size_t a, size_t b) { for (size_t k = a; k < b; ++k) key[k] = group_key(p->nodes[list[k]]); });
+    std::vector<uint32_t> uk;                      // distinct keys (few: levels x kinds x directions x classes)
+    {
+        std::vector<uint32_t> tmp;
+        for (size_t k = 0; k < n; k += 97) tmp.push_back(key[k]);
+        std::sort(tmp.begin(), tmp.end());
+        tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+        uk = tmp;
+        for (size_t k = 0; k < n; ++k)
+            if (!std::binary_search(uk.begin(), uk.end(), key[k])) {
+                uk.insert(std::upper_bound(uk.begin(), uk.end(), key[k]), key[k]);
+            }
+    }
+    const size_t B = uk.size(), C = 64;            // C contiguous chunks of the list
+    std::vector<uint32_t> bk(n);
+    std::vector<uint64_t> hist(C * B, 0);
+    par_for(C, 1, [&](size_t c0, size_t c1) {
+        for (size_t c = c0; c < c1; ++c) {
+            const size_t a = n * c / C, b = n * (c + 1) / C;
+            for (size_t k = a; k < b; ++k) {
+                bk[k] = (uint32_t)(std::lower_bound(uk.begin(), uk.end(), key[k]) - uk.begin());
+                hist[c * B + bk[k]]++;
+            }
+        }
+    });
+    std::vector<uint64_t> off(C * B);
+    uint64_t acc = 0;
+    for (size_t b = 0; b < B; ++b)
+        for (size_t c = 0; c < C; ++c) { off[c * B + b] = acc; acc += hist[c * B + b]; }
+    std::vector<uint32_t> out(n);
+    par_for(C, 1, [&](size_t c0, size_t c1) {
+        for (size_t c = c0; c < c1; ++c) {
+            const size_t a = n * c / C, b = n * (c + 1) / C;
+            uint64_t *o = &off[c * B];
+            for (size_t k = a; k < b; ++k) out[o[bk[k]]++] = list[k];
+        }
+    });
+    list.swap(out);
 }
 
 // Phase A: the node list of every chunk (host only).  Rows are materialised only
@@ -164,13 +252,23 @@ void collect_chunks(hedl_program *p, uint32_t r0, uint32_t r1, uint64_t row_cap,
     if (p->stamp.size() < p->nodes.size()) p->stamp.assign(p->nodes.size(), 0);
     if (r0 == 0 && r1 == p->root_node.size()) {
         // the whole program: every live node is reachable from a root
-        uint64_t live = 0;
-        for (const CNode &n : p->nodes) live += n.kind <= NK_DRANGE;
+        const size_t NN = p->nodes.size(), C = 64;
+        std::vector<uint32_t> cnt(C + 1, 0);
+        par_for(C, 1, [&](size_t c0, size_t c1) {
+            for (size_t c = c0; c < c1; ++c)
+                for (size_t i = NN * c / C; i < NN * (c + 1) / C; ++i) cnt[c + 1] += p->nodes[i].kind <= NK_DRANGE;
+        });
+        for (size_t c = 0; c < C; ++c) cnt[c + 1] += cnt[c];
+        const uint64_t live = cnt[C];
         if (live - std::min<uint64_t>(live, r1) <= row_cap) {
-            std::vector<uint32_t> list;
-            list.reserve(live);
-            for (uint32_t i = 0; i < p->nodes.size(); ++i)
-                if (p->nodes[i].kind <= NK_DRANGE) list.push_back(i);
+            std::vector<uint32_t> list(live);
+            par_for(C, 1, [&](size_t c0, size_t c1) {
+                for (size_t c = c0; c < c1; ++c) {
+                    uint32_t o = cnt[c];
+                    for (size_t i = NN * c / C; i < NN * (c + 1) / C; ++i)
+                        if (p->nodes[i].kind <= NK_DRANGE) list[o++] = (uint32_t)i;
+                }
+            });
             sort_by_key(p, list);
             lists.push_back(std::move(list));
             ranges.push_back({r0, r1});
@@ -219,7 +317,7 @@ void collect_chunks(hedl_program *p, uint32_t r0, uint32_t r1, uint64_t row_cap,
 }
 
 struct ChunkTmp {            // per-chunk planning state kept between the sizing and filling passes
-    std::vector<uint32_t> slot, pslot, cover_of_root, members;
+    std::vector<uint32_t> slot, pslot, cover_of_root, members, gdesc, opbase;
     std::vector<int32_t> cover_of_node;
     std::vector<uint8_t> need_full, need_proj, pmode;
     std::vector<Group> groups;
@@ -238,7 +336,7 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                 ChunkTmp &tmp) {
     const uint32_t nn = (uint32_t)list.size();
     cp.nn = nn;
-    for (uint32_t k = 0; k < nn; ++k) local[list[k]] = k;
+    par_for(nn, 1 << 15, [&](size_t a, size_t b) { for (size_t k = a; k < b; ++k) local[list[k]] = (uint32_t)k; });
     const uint32_t nroots = cp.rc - cp.ri;
     auto &need_full = tmp.need_full;
     auto &need_proj = tmp.need_proj;
@@ -251,14 +349,17 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
     auto &members = tmp.members;
     if (sizes_only) {
         const double ts0 = now_ms();
+        // one count slot per distinct root node
         cover_of_node.assign(nn, -1);
         cover_of_root.resize(nroots);
-        uint32_t ncov = 0;
-        for (uint32_t k = 0; k < nroots; ++k) {
-            const uint32_t li = local[p->root_node[cp.ri + k]];
-            if (cover_of_node[li] < 0) cover_of_node[li] = (int32_t)ncov++;
-            cover_of_root[k] = (uint32_t)cover_of_node[li];
-        }
+        std::vector<uint8_t> isroot(nn, 0);
+        par_for(nroots, 1 << 15, [&](size_t a, size_t b) {
+            for (size_t k = a; k < b; ++k) isroot[local[p->root_node[cp.ri + k]]] = 1;
+        });
+        const uint32_t ncov = par_rank(nn, [&](size_t k) { return isroot[k] != 0; }, cover_of_node);
+        par_for(nroots, 1 << 15, [&](size_t a, size_t b) {
+            for (size_t k = a; k < b; ++k) cover_of_root[k] = (uint32_t)cover_of_node[local[p->root_node[cp.ri + k]]];
+        });
         cp.ncov = ncov;
         // demands, consumers first (the list is in ascending level order)
         need_full.assign(nn, 0);
@@ -266,25 +367,32 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
         pmode.assign(nn, 0);
         if (out_bits)
             for (uint32_t k = 0; k < nroots; ++k) need_full[local[p->root_node[cp.ri + k]]] = 1;
-        for (uint32_t k = nn; k-- > 0;) {
-            const CNode &n = p->nodes[list[k]];
-            const bool isbool = n.kind == NK_AND || n.kind == NK_OR;
-            pmode[k] = isbool && !need_full[k];
-            for (uint32_t q = 0; q < n.op_count; ++q) {
-                const uint32_t o = p->ops[n.op_begin + q];
-                if (ref_type(o) != RT_NODE) continue;
-                if (pmode[k]) need_proj[local[ref_id(o)]] = 1;
-                else need_full[local[ref_id(o)]] = 1;
-            }
+        // level by level from the top; within a level nodes are independent (operands sit at
+        // lower levels; concurrent writes of 1 to a shared operand flag are benign)
+        for (uint32_t hi = nn; hi > 0;) {
+            const uint32_t lvl = p->nodes[list[hi - 1]].level;
+            uint32_t lo = hi - 1;
+            while (lo > 0 && p->nodes[list[lo - 1]].level == lvl) --lo;
+            par_for(hi - lo, 1 << 13, [&](size_t a, size_t b) {
+                for (size_t kk = lo + a; kk < lo + b; ++kk) {
+                    const CNode &n = p->nodes[list[kk]];
+                    const bool isbool = n.kind == NK_AND || n.kind == NK_OR;
+                    pmode[kk] = isbool && !need_full[kk];
+                    for (uint32_t q = 0; q < n.op_count; ++q) {
+                        const uint32_t o = p->ops[n.op_begin + q];
+                        if (ref_type(o) != RT_NODE) continue;
+                        if (pmode[kk]) need_proj[local[ref_id(o)]] = 1;
+                        else need_full[local[ref_id(o)]] = 1;
+                    }
+                }
+            });
+            hi = lo;
         }
         const double ts1 = now_ms();
         slot.assign(nn, 0);
         pslot.assign(nn, 0);
-        uint32_t nrows = 0, nprows = 0;
-        for (uint32_t k = 0; k < nn; ++k) {
-            if (need_full[k]) slot[k] = nrows++;
-            if (need_proj[k]) pslot[k] = nprows++;
-        }
+        const uint32_t nrows = par_rank(nn, [&](size_t k) { return need_full[k] != 0; }, slot);
+        const uint32_t nprows = par_rank(nn, [&](size_t k) { return need_proj[k] != 0; }, pslot);
         cp.nrows = nrows;
         cp.nprows = nprows;
         // launch groups: (level, kind, dir) runs of the list; boolean runs split by full/projected
@@ -341,15 +449,25 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
             }
             k = e;
         }
+        // descriptor bases per group and operand bases per boolean member (for the parallel fill)
         size_t n_ops = 0, n_bool = 0, n_res = 0, n_dr = 0;
-        for (const Group &g : groups) {
+        tmp.gdesc.resize(groups.size());
+        tmp.opbase.assign(members.size(), 0);
+        for (size_t gi = 0; gi < groups.size(); ++gi) {
+            const Group &g = groups[gi];
             if (g.kind == NK_AND) {
+                tmp.gdesc[gi] = (uint32_t)n_bool;
                 n_bool += g.count;
-                for (uint32_t m = g.first; m < g.first + g.count; ++m) n_ops += p->nodes[list[members[m]]].op_count;
+                for (uint32_t m = g.first; m < g.first + g.count; ++m) {
+                    tmp.opbase[m] = (uint32_t)n_ops;
+                    n_ops += p->nodes[list[members[m]]].op_count;
+                }
             } else if (g.kind == NK_RESTRICT) {
+                tmp.gdesc[gi] = (uint32_t)n_res;
                 n_res += g.count;
                 if (!g.slice) *heavy_need = std::max(*heavy_need, (size_t)g.count * kb->dirs[g.key].n_heavy * 8);
             } else {
+                tmp.gdesc[gi] = (uint32_t)n_dr;
                 n_dr += g.count;
             }
         }
@@ -388,73 +506,88 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
     Operand *ho = (Operand *)(h + cp.off_ops);
     RestrictDesc *hr = (RestrictDesc *)(h + cp.off_res);
     DrangeDesc *hd = (DrangeDesc *)(h + cp.off_dr);
-    uint32_t ib = 0, io = 0, ir = 0, idr = 0;
-    cp.recs.clear();
-    for (const Group &g : groups) {
-        LaunchRec lr{g.kind, g.key, g.slice, g.proj, g.ex, g.count, 0, 0, 0};
-        if (g.kind == NK_AND) {
-            lr.first_desc = ib;
-            const double wb = 4.0 * (g.proj ? kb->MW : kb->W);
-            for (uint32_t m = g.first; m < g.first + g.count; ++m) {
-                const uint32_t k = members[m];
-                const CNode &n = p->nodes[list[k]];
-                BoolDesc bd;
-                if (g.proj) {           // projected: the output (if any) is the projected row
-                    bd.out = proj_of(k);
-                    bd.proj = nullptr;
-                } else {
-                    bd.out = out_of(k);
-                    bd.proj = proj_of(k);
+    // tasks: (group, member range); filled in parallel, each at precomputed offsets
+    struct Task { uint32_t g, m0, m1; double bytes, bytes2; };
+    std::vector<Task> tasks;
+    for (uint32_t gi = 0; gi < groups.size(); ++gi)
+        for (uint32_t m = groups[gi].first; m < groups[gi].first + groups[gi].count; m += 8192)
+            tasks.push_back({gi, m, std::min(m + 8192, groups[gi].first + groups[gi].count), 0, 0});
+    par_for(tasks.size(), 1, [&](size_t t0, size_t t1) {
+        for (size_t ti = t0; ti < t1; ++ti) {
+            Task &T = tasks[ti];
+            const Group &g = groups[T.g];
+            const uint32_t base = tmp.gdesc[T.g];
+            if (g.kind == NK_AND) {
+                const double wb = 4.0 * (g.proj ? kb->MW : kb->W);
+                for (uint32_t m = T.m0; m < T.m1; ++m) {
+                    const uint32_t k = members[m];
+                    const CNode &n = p->nodes[list[k]];
+                    BoolDesc bd;
+                    if (g.proj) {           // projected: the output (if any) is the projected row
+                        bd.out = proj_of(k);
+                        bd.proj = nullptr;
+                    } else {
+                        bd.out = out_of(k);
+                        bd.proj = proj_of(k);
+                    }
+                    uint32_t io = tmp.opbase[m];
+                    bd.op_first = io;
+                    bd.op_count = n.op_count;
+                    bd.is_or = n.kind == NK_OR;
+                    bd.cover = cover_of_node[k];
+                    for (uint32_t q = 0; q < n.op_count; ++q) {
+                        const uint32_t o = p->ops[n.op_begin + q];
+                        ho[io++] = Operand{g.proj ? pptr_of(o) : ptr_of(o), ref_comp(o) ? 0xffffffffu : 0u, 0};
+                    }
+                    hb[base + (m - g.first)] = bd;
+                    T.bytes += wb * (n.op_count + (bd.out ? 1 : 0) + (bd.cover >= 0 ? 2 : 0));
                 }
-                bd.op_first = io;
-                bd.op_count = n.op_count;
-                bd.is_or = n.kind == NK_OR;
-                bd.cover = cover_of_node[k];
-                for (uint32_t q = 0; q < n.op_count; ++q) {
-                    const uint32_t o = p->ops[n.op_begin + q];
-                    ho[io++] = Operand{g.proj ? pptr_of(o) : ptr_of(o), ref_comp(o) ? 0xffffffffu : 0u, 0};
+            } else if (g.kind == NK_RESTRICT) {
+                const hedl_dir &dr = kb->dirs[g.key];
+                for (uint32_t m = T.m0; m < T.m1; ++m) {
+                    const uint32_t k = members[m];
+                    const CNode &n = p->nodes[list[k]];
+                    const uint32_t c = p->ops[n.op_begin];
+                    RestrictDesc rd;
+                    rd.child = ptr_of(c);
+                    rd.out = out_of(k);
+                    rd.proj = proj_of(k);
+                    rd.cmask = ref_comp(c) ? 0xffffffffu : 0u;
+                    rd.pred = n.pred;
+                    rd.n = n.n;
+                    rd.sat = n.sat;
+                    rd.cover = cover_of_node[k];
+                    rd.heavy_slot = (m - g.first) * dr.n_heavy;
+                    hr[base + (m - g.first)] = rd;
+                    T.bytes += 4.0 * (kb->N + 1) + 4.0 * (dr.E - dr.E_heavy) +
+                               4.0 * kb->W * (1 + (rd.out ? 1 : 0) + (rd.cover >= 0 ? 2 : 0));
+                    T.bytes2 += 4.0 * dr.E_heavy;
                 }
-                hb[ib++] = bd;
-                lr.bytes += wb * (n.op_count + (bd.out ? 1 : 0) + (bd.cover >= 0 ? 2 : 0));
-            }
-        } else if (g.kind == NK_RESTRICT) {
-            lr.first_desc = ir;
-            const hedl_dir &dr = kb->dirs[g.key];
-            for (uint32_t m = g.first; m < g.first + g.count; ++m) {
-                const uint32_t k = members[m];
-                const CNode &n = p->nodes[list[k]];
-                const uint32_t c = p->ops[n.op_begin];
-                RestrictDesc rd;
-                rd.child = ptr_of(c);
-                rd.out = out_of(k);
-                rd.proj = proj_of(k);
-                rd.cmask = ref_comp(c) ? 0xffffffffu : 0u;
-                rd.pred = n.pred;
-                rd.n = n.n;
-                rd.sat = n.sat;
-                rd.cover = cover_of_node[k];
-                rd.heavy_slot = (m - g.first) * dr.n_heavy;
-                hr[ir++] = rd;
-                lr.bytes += 4.0 * (kb->N + 1) + 4.0 * (dr.E - dr.E_heavy) + 4.0 * kb->W * (1 + (rd.out ? 1 : 0) + (rd.cover >= 0 ? 2 : 0));
-                lr.bytes2 += 4.0 * dr.E_heavy;
-            }
-        } else {
-            lr.first_desc = idr;
-            for (uint32_t m = g.first; m < g.first + g.count; ++m) {
-                const uint32_t k = members[m];
-                const CNode &n = p->nodes[list[k]];
-                DrangeDesc dd;
-                dd.out = out_of(k);
-                dd.proj = proj_of(k);
-                dd.lo = n.lo;
-                dd.hi = n.hi;
-                dd.cover = cover_of_node[k];
-                dd.prop = n.dir;
-                hd[idr++] = dd;
-                lr.bytes += kb->data_bytes[n.dir] + 4.0 * kb->W * ((dd.out ? 1 : 0) + (dd.cover >= 0 ? 2 : 0));
+            } else {
+                for (uint32_t m = T.m0; m < T.m1; ++m) {
+                    const uint32_t k = members[m];
+                    const CNode &n = p->nodes[list[k]];
+                    DrangeDesc dd;
+                    dd.out = out_of(k);
+                    dd.proj = proj_of(k);
+                    dd.lo = n.lo;
+                    dd.hi = n.hi;
+                    dd.cover = cover_of_node[k];
+                    dd.prop = n.dir;
+                    hd[base + (m - g.first)] = dd;
+                    T.bytes += kb->data_bytes[n.dir] + 4.0 * kb->W * ((dd.out ? 1 : 0) + (dd.cover >= 0 ? 2 : 0));
+                }
             }
         }
-        cp.recs.push_back(lr);
+    });
+    cp.recs.clear();
+    for (uint32_t gi = 0; gi < groups.size(); ++gi) {
+        const Group &g = groups[gi];
+        cp.recs.push_back(LaunchRec{g.kind, g.key, g.slice, g.proj, g.ex, g.count, tmp.gdesc[gi], 0, 0});
+    }
+    for (const Task &T : tasks) {
+        cp.recs[T.g].bytes += T.bytes;
+        cp.recs[T.g].bytes2 += T.bytes2;
     }
     std::memcpy(h + cp.off_cov, cover_of_root.data(), nroots * sizeof(uint32_t));
     if (out_bits) {

@@ -15,6 +15,17 @@
 
 namespace hedl {
 
+// allocator that default-initialises (no zero fill) trivially constructible elements:
+// large planning arrays are written in parallel right after allocation
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+    template <class U> struct rebind { using other = NoInitAlloc<U>; };
+    NoInitAlloc() = default;
+    template <class U> NoInitAlloc(const NoInitAlloc<U> &) {}
+    template <class U> void construct(U *p) { ::new ((void *)p) U; }
+    template <class U, class... A> void construct(U *p, A &&...a) { ::new ((void *)p) U(std::forward<A>(a)...); }
+};
+
 // ---- degree bins ------------------------------------------
 // light  : deg <= kLightDeg      lane = individual, ballot builds the word
 // medium : deg <= kHeavyDeg      warp-cooperative, 32 neighbours per step
@@ -121,8 +132,8 @@ struct hedl_kb {
 struct hedl_program {
     const hedl_kb *kb = nullptr;
     uint32_t flags = 0;
-    std::vector<hedl::CNode> nodes;
-    std::vector<uint32_t> ops;
+    std::vector<hedl::CNode, hedl::NoInitAlloc<hedl::CNode>> nodes;
+    std::vector<uint32_t, hedl::NoInitAlloc<uint32_t>> ops;
     std::vector<uint32_t> root_node;   // per root: computed canonical node id
     std::vector<double> root_bytes;    // B(h)
     uint32_t n_levels = 0;
