@@ -204,12 +204,13 @@ const char *hedl_version(void);
 
 /* Kernel-level timing: when enabled, every kernel launch of the library is
  * bracketed by CUDA events on its launch stream; hedl_prof_read synchronises
- * and returns per kernel class {name, launches, total_ms, alg_bytes}. */
+ * and returns per kernel class {name, launches, total_ms, alg_bytes, units}. */
 typedef struct hedl_prof_entry {
     char name[32];
     uint64_t launches;
     double total_ms;
     double alg_bytes;
+    double units;          /* work units launched (nodes for per-node kernels, 256-lane packs for slice kernels) */
 } hedl_prof_entry;
 hedl_status hedl_prof_enable(int on);
 hedl_status hedl_prof_reset(void);

@@ -64,7 +64,7 @@ class _ProgInfo(C.Structure):
 
 class _ProfEntry(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("launches", C.c_uint64), ("total_ms", C.c_double),
-                ("alg_bytes", C.c_double)]
+                ("alg_bytes", C.c_double), ("units", C.c_double)]
 
 
 _lib = None
@@ -288,7 +288,7 @@ def prof_read() -> list:
     arr = (_ProfEntry * max(n, 1))()
     n = L.hedl_prof_read(arr, n)
     return [{"name": arr[i].name.decode(), "launches": arr[i].launches, "total_ms": arr[i].total_ms,
-             "alg_bytes": arr[i].alg_bytes} for i in range(n)]
+             "alg_bytes": arr[i].alg_bytes, "units": arr[i].units} for i in range(n)]
 
 
 def launch_count() -> int:

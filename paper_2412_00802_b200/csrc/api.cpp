@@ -76,7 +76,7 @@ void pool_release_all(hedl_kb *kb) {
 }
 
 const char *kKClassName[KC_N] = {"bool", "restrict", "restrict_heavy", "drange", "cover_init", "gather",
-                                 "slice_pack", "slice", "slice_heavy", "kb", "slice_ex"};
+                                 "slice_pack", "slice", "slice_heavy", "kb", "slice_ex", "interp"};
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -90,7 +90,7 @@ void count_io(uint64_t h2d, uint64_t d2h) {
 struct ProfRec {
     cudaEvent_t a, b;
     int kc;
-    double bytes;
+    double bytes, units;
 };
 static std::mutex g_prof_mu;
 static bool g_prof_on = false;
@@ -116,12 +116,12 @@ void prof_begin(cudaStream_t s, int) {
     cudaEventRecord(g_pending, s);
 }
 
-void prof_end(cudaStream_t s, int kc, double bytes) {
+void prof_end(cudaStream_t s, int kc, double bytes, double units) {
     if (!g_prof_on || !g_pending) return;
     std::lock_guard<std::mutex> lk(g_prof_mu);
     cudaEvent_t b = get_event();
     cudaEventRecord(b, s);
-    g_prof.push_back({g_pending, b, kc, bytes});
+    g_prof.push_back({g_pending, b, kc, bytes, units});
     g_pending = nullptr;
 }
 
@@ -167,6 +167,7 @@ extern "C" int hedl_prof_read(hedl_prof_entry *out, int max_entries) {
         acc[r.kc].launches++;
         acc[r.kc].total_ms += ms;
         acc[r.kc].alg_bytes += r.bytes;
+        acc[r.kc].units += r.units;
     }
     int n = 0;
     for (int k = 0; k < KC_N; ++k) {

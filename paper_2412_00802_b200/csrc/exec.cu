@@ -15,6 +15,7 @@
 #include <thread>
 
 #include "internal.h"
+#include "interp.h"
 #include "slice.h"
 
 using namespace hedl;
@@ -767,9 +768,92 @@ extern "C" hedl_status hedl_eval_batch(const hedl_kb *kb, hedl_program *p, uint3
     return st;
 }
 
+// Latency path: the root's sub-DAG (post-order, root last) as one interpreter launch
+// when it fits (<= kInterpMaxNodes nodes, rows in shared memory); else the batch path.
+static bool build_interp(const hedl_kb *kb, const hedl_program *p, uint32_t root_node, InterpProg &prog) {
+    std::vector<uint32_t> order, local_of;
+    std::vector<std::pair<uint32_t, uint32_t>> st;
+    std::vector<uint32_t> seen;
+    auto is_seen = [&](uint32_t id) { return std::find(seen.begin(), seen.end(), id) != seen.end(); };
+    st.push_back({root_node, 0});
+    seen.push_back(root_node);
+    while (!st.empty()) {
+        auto &top = st.back();
+        const CNode &n = p->nodes[top.first];
+        if (top.second < n.op_count) {
+            const uint32_t o = p->ops[n.op_begin + top.second++];
+            if (ref_type(o) == RT_NODE && !is_seen(ref_id(o))) {
+                if (seen.size() >= kInterpMaxNodes) return false;
+                seen.push_back(ref_id(o));
+                st.push_back({ref_id(o), 0});
+            }
+            continue;
+        }
+        order.push_back(top.first);
+        st.pop_back();
+    }
+    if ((size_t)order.size() * kb->W4 * 4 > interp_smem_limit()) return false;
+    prog.n_nodes = (uint32_t)order.size();
+    prog.n_ops = 0;
+    prog.npos = kb->npos;
+    prog.nneg = kb->nneg;
+    for (uint32_t i = 0; i < order.size(); ++i) {
+        const CNode &n = p->nodes[order[i]];
+        if (prog.n_ops + n.op_count > kInterpMaxOps) return false;
+        InterpNode &d = prog.nodes[i];
+        d.kind = n.kind; d.pred = n.pred; d.dir = n.dir; d.n = n.n; d.sat = n.sat; d.lo = n.lo; d.hi = n.hi;
+        d.op_begin = prog.n_ops;
+        d.op_count = n.op_count;
+        for (uint32_t q = 0; q < n.op_count; ++q) {
+            uint32_t o = p->ops[n.op_begin + q];
+            if (ref_type(o) == RT_NODE) {
+                const uint32_t li = (uint32_t)(std::find(order.begin(), order.end(), ref_id(o)) - order.begin());
+                o = mkref(RT_NODE, li, ref_comp(o));
+            }
+            prog.ops[prog.n_ops++] = o;
+        }
+    }
+    return true;
+}
+
 extern "C" hedl_status hedl_eval_one(const hedl_kb *kb, hedl_program *p, uint32_t root, uint32_t *out_bits,
                                      hedl_counts *out, void *stream) {
     if (!out) return fail(HEDL_ERR_INVALID_ARG, "null out");
+    if (!kb || !p) return fail(HEDL_ERR_INVALID_ARG, "null kb/program");
+    if (p->kb != kb) return fail(HEDL_ERR_INVALID_ARG, "program was compiled for another KB");
+    if (kb->poisoned) return fail(HEDL_ERR_CUDA, "KB handle is poisoned by an earlier CUDA error");
+    if (root >= p->root_node.size()) return fail(HEDL_ERR_OUT_OF_RANGE, "root out of range");
+    static thread_local InterpProg prog;   // ~5 KB: keep it off the stack
+    if (kb->N && build_interp(kb, p, p->root_node[root], prog)) {
+        std::lock_guard<std::mutex> lk(p->mu);
+        DeviceGuard dg(kb->device);
+        hedl_kb *mkb = const_cast<hedl_kb *>(kb);
+        {
+            std::lock_guard<std::mutex> lk2(mkb->interp_mu);
+            hedl_status st = interp_prepare(mkb);
+            if (st) return st;
+        }
+        if (!p->lat_host) {
+            if (cudaHostAlloc((void **)&p->lat_host, sizeof(hedl_counts), cudaHostAllocMapped) != cudaSuccess ||
+                cudaHostGetDevicePointer((void **)&p->lat_dev, p->lat_host, 0) != cudaSuccess) {
+                cudaGetLastError();
+                p->lat_host = nullptr;
+                return fail(HEDL_ERR_OOM, "mapped counts");
+            }
+        }
+        cudaStream_t s = (cudaStream_t)stream;
+        Workspace *w = ws_of(p);
+        if (w->used && w->done) HEDL_CUDA(kb, cudaStreamWaitEvent(s, w->done, 0));
+        hedl_status st = interp_launch(kb, prog, p->lat_dev, out_bits, s);
+        if (st) return st;
+        HEDL_CUDA(kb, cudaStreamSynchronize(s));
+        const volatile hedl_counts *vc = p->lat_host;
+        out->tp = vc->tp;
+        out->fp = vc->fp;
+        out->fn = vc->fn;
+        out->tn = vc->tn;
+        return HEDL_OK;
+    }
     return hedl_eval_batch(kb, p, root, 1, out_bits, out, stream, HEDL_EVAL_PER_NODE);
 }
 
@@ -787,6 +871,7 @@ extern "C" hedl_status hedl_program_free(hedl_program *p) {
         w->plan.host = w->plan.dev = nullptr;
         release_plan(w->plan);
         if (w->done) cudaEventDestroy(w->done);
+        if (p->lat_host) cudaFreeHost(p->lat_host);
         delete w;
     }
     delete p;

@@ -125,6 +125,8 @@ struct hedl_kb {
     // cudaMallocHost / memset per program); accumulator buffers return self-cleaned
     mutable std::mutex pool_mu;
     mutable std::vector<std::pair<void *, size_t>> pool[8];
+    const void **interp_ptrs = nullptr;  // device: per-direction row_ptr/col, per-property row_ptr/val
+    std::mutex interp_mu;
     std::vector<double> dir_bytes;  // 4(N+1) + 4E per direction
     std::vector<double> data_bytes; // 4(N+1) + 4V per property
 };
@@ -144,6 +146,8 @@ struct hedl_program {
     void *pinned = nullptr;
     size_t pinned_bytes = 0;
     uint64_t ws_limit = 0;              // 0 = auto (half the free memory, <= 48 GiB)
+    // latency path: mapped pinned counts (host pointer + device alias)
+    hedl_counts *lat_host = nullptr, *lat_dev = nullptr;
     // planning scratch (host)
     std::vector<uint32_t> stamp;
     uint32_t stamp_gen = 0;
@@ -175,10 +179,10 @@ void timing_note(const char *what, double ms);
 
 // ---- profiling -----------------------------------------------------------------
 enum KClass { KC_BOOL, KC_RESTRICT, KC_HEAVY, KC_DRANGE, KC_COVER_INIT, KC_GATHER,
-              KC_SLICE_IN, KC_SLICE, KC_SLICE_HEAVY, KC_KB, KC_SLICE_EX, KC_N };
+              KC_SLICE_IN, KC_SLICE, KC_SLICE_HEAVY, KC_KB, KC_SLICE_EX, KC_INTERP, KC_N };
 extern const char *kKClassName[KC_N];
 void prof_begin(cudaStream_t s, int kc);
-void prof_end(cudaStream_t s, int kc, double alg_bytes);
+void prof_end(cudaStream_t s, int kc, double alg_bytes, double units = 1);
 
 // ---- kernels launchers (kernels.cu) -----------------------------------------
 struct BoolDesc {

@@ -1,0 +1,171 @@
+// Latency path of hedl_eval_one (SURVEY 8(a) "small N": a single-launch bytecode
+// interpreter).  One CTA of 1024 threads walks the root's canonical sub-DAG in
+// topological order; every intermediate row lives in shared memory, the program
+// travels as a kernel parameter (no H2D copy), and the four counts are written
+// straight into mapped pinned host memory -- one launch and one stream sync per
+// hypothesis.  Semantics are those of the batch kernels (kernels.cu): the same
+// count-with-saturation predicates (Algs. 4, 6, 7-8), complement masks (Alg. 2),
+// float32 closed-interval ranges (Alg. 10, Q9) and Alg. 15 coverage.
+#include "interp.h"
+
+namespace hedl {
+
+namespace {
+constexpr uint32_t FULL = 0xffffffffu;
+
+__device__ __forceinline__ bool pred_ok(uint32_t pred, uint32_t cnt, uint32_t n) {
+    switch (pred) {
+    case P_GE: return cnt >= n;
+    case P_LE: return cnt <= n;
+    case P_EQ: return cnt == n;
+    default: return cnt > 0 && cnt <= n;
+    }
+}
+
+struct IKb {
+    uint32_t N, W, W4;
+    const uint32_t *concepts, *ones, *pos, *neg;
+    const uint32_t *const *row_ptr;   // per direction (device array of pointers)
+    const uint32_t *const *col;
+    const uint32_t *const *drow;      // per data property
+    const float *const *dval;
+};
+
+__device__ __forceinline__ const uint32_t *operand(const IKb &kb, const uint32_t *smem, uint32_t ref) {
+    const uint32_t id = ref >> 3;
+    switch ((ref >> 1) & 3u) {
+    case RT_NODE: return smem + (size_t)id * kb.W4;
+    case RT_ATOM: return kb.concepts + (size_t)id * kb.W4;
+    default: return kb.ones;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_interp(IKb kb, InterpProg prog, hedl_counts *counts, uint32_t *out_bits) {
+    extern __shared__ uint32_t srows[];
+    __shared__ uint32_t s_red[2][32];
+    const uint32_t tid = threadIdx.x, lane = tid & 31;
+    for (uint32_t i = 0; i < prog.n_nodes; ++i) {
+        const InterpNode nd = prog.nodes[i];
+        uint32_t *out = srows + (size_t)i * kb.W4;
+        if (nd.kind == NK_AND || nd.kind == NK_OR) {
+            for (uint32_t w = tid; w < kb.W4; w += blockDim.x) {
+                uint32_t acc = nd.kind == NK_OR ? 0u : FULL;
+                for (uint32_t q = 0; q < nd.op_count; ++q) {
+                    const uint32_t r = prog.ops[nd.op_begin + q];
+                    const uint32_t v = operand(kb, srows, r)[w] ^ ((r & 1u) ? FULL : 0u);
+                    acc = nd.kind == NK_OR ? (acc | v) : (acc & v);
+                }
+                if (w >= kb.W) acc = 0;
+                else if (w == kb.W - 1 && (kb.N & 31)) acc &= (1u << (kb.N & 31)) - 1u;
+                out[w] = acc;
+            }
+        } else if (nd.kind == NK_RESTRICT) {
+            const uint32_t r = prog.ops[nd.op_begin];
+            const uint32_t *child = operand(kb, srows, r);
+            const uint32_t cm = (r & 1u) ? FULL : 0u;
+            const uint32_t *rp = kb.row_ptr[nd.dir], *cl = kb.col[nd.dir];
+            // x = base + tid, the warp's 32 consecutive rows make one output word
+            for (uint32_t base = 0; base < kb.W4 * 32; base += blockDim.x) {
+                const uint32_t x = base + tid;
+                bool res = false;
+                if (x < kb.N) {
+                    const uint32_t a = __ldg(rp + x), b = __ldg(rp + x + 1);
+                    uint32_t cnt = 0;
+                    for (uint32_t e = a; e < b && cnt < nd.sat; ++e) {
+                        const uint32_t y = __ldg(cl + e);
+                        cnt += ((child[y >> 5] ^ cm) >> (y & 31)) & 1u;
+                    }
+                    res = pred_ok(nd.pred, min(cnt, nd.sat), nd.n);
+                }
+                const uint32_t word = __ballot_sync(FULL, res);
+                if (lane == 0 && (x >> 5) < kb.W4) out[x >> 5] = word;
+            }
+        } else {
+            const uint32_t *rp = kb.drow[nd.dir];
+            const float *val = kb.dval[nd.dir];
+            for (uint32_t base = 0; base < kb.W4 * 32; base += blockDim.x) {
+                const uint32_t x = base + tid;
+                bool res = false;
+                if (x < kb.N) {
+                    uint32_t lo = __ldg(rp + x), hi = __ldg(rp + x + 1);
+                    const uint32_t end = hi;
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (__ldg(val + mid) < nd.lo) lo = mid + 1; else hi = mid;
+                    }
+                    res = lo < end && __ldg(val + lo) <= nd.hi;
+                }
+                const uint32_t word = __ballot_sync(FULL, res);
+                if (lane == 0 && (x >> 5) < kb.W4) out[x >> 5] = word;
+            }
+        }
+        __syncthreads();
+    }
+    // Alg. 15 coverage of the root (the last node), one reduction, counts to mapped host memory
+    const uint32_t *root = srows + (size_t)(prog.n_nodes - 1) * kb.W4;
+    uint32_t tp = 0, fp = 0;
+    for (uint32_t w = tid; w < kb.W; w += blockDim.x) {
+        const uint32_t h = root[w];
+        tp += __popc(h & __ldg(kb.pos + w));
+        fp += __popc(h & __ldg(kb.neg + w));
+        if (out_bits) out_bits[w] = h;
+    }
+    tp = __reduce_add_sync(FULL, tp);
+    fp = __reduce_add_sync(FULL, fp);
+    if (lane == 0) { s_red[0][tid >> 5] = tp; s_red[1][tid >> 5] = fp; }
+    __syncthreads();
+    if (tid < 32) {
+        uint32_t a = tid < (blockDim.x >> 5) ? s_red[0][tid] : 0u, b = tid < (blockDim.x >> 5) ? s_red[1][tid] : 0u;
+        a = __reduce_add_sync(FULL, a);
+        b = __reduce_add_sync(FULL, b);
+        if (tid == 0) {
+            counts->tp = a;
+            counts->fp = b;
+            counts->fn = prog.npos - a;
+            counts->tn = prog.nneg - b;
+        }
+    }
+}
+}  // namespace
+
+size_t interp_smem_limit() { return 200u * 1024u; }
+
+hedl_status interp_prepare(hedl_kb *kb) {
+    // device arrays of per-direction / per-property pointers for the interpreter
+    if (kb->interp_ptrs || !kb->dirs.size() && !kb->data.size()) return HEDL_OK;
+    std::vector<const void *> h;
+    for (auto &d : kb->dirs) h.push_back(d.row_ptr);
+    for (auto &d : kb->dirs) h.push_back(d.col);
+    for (auto &d : kb->data) h.push_back(d.row_ptr);
+    for (auto &d : kb->data) h.push_back(d.val);
+    void *p = nullptr;
+    if (cudaMalloc(&p, h.size() * sizeof(void *)) != cudaSuccess) { cudaGetLastError(); return fail(HEDL_ERR_OOM, "interp pointers"); }
+    kb->allocs.push_back(p);
+    if (cudaMemcpy(p, h.data(), h.size() * sizeof(void *), cudaMemcpyHostToDevice) != cudaSuccess)
+        return cuda_fail(kb, cudaGetLastError(), "interp pointers");
+    kb->interp_ptrs = (const void **)p;
+    return HEDL_OK;
+}
+
+hedl_status interp_launch(const hedl_kb *kb, const InterpProg &prog, hedl_counts *counts_mapped, uint32_t *out_bits,
+                          cudaStream_t s) {
+    const size_t R = kb->dirs.size(), D = kb->data.size();
+    const void *const *pp = (const void *const *)kb->interp_ptrs;
+    IKb ik{kb->N, kb->W, kb->W4, kb->concepts, kb->ones, kb->pos, kb->neg,
+           (const uint32_t *const *)pp, (const uint32_t *const *)(pp + R),
+           (const uint32_t *const *)(pp + 2 * R), (const float *const *)(pp + 2 * R + D)};
+    const size_t smem = (size_t)prog.n_nodes * kb->W4 * 4;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)interp_smem_limit());
+        attr = true;
+    }
+    prof_begin(s, KC_INTERP);
+    k_interp<<<1, 1024, smem, s>>>(ik, prog, counts_mapped, out_bits);
+    count_launch();
+    prof_end(s, KC_INTERP, 0, prog.n_nodes);
+    HEDL_CUDA(kb, cudaGetLastError());
+    return HEDL_OK;
+}
+
+}  // namespace hedl

@@ -289,7 +289,7 @@ void launch_cover_init(cudaStream_t s, hedl_counts *counts, uint32_t n, uint64_t
     prof_begin(s, KC_COVER_INIT);
     k_cover_init<<<cdiv(n, 256), 256, 0, s>>>(counts, n, npos, nneg);
     count_launch();
-    prof_end(s, KC_COVER_INIT, 32.0 * n);
+    prof_end(s, KC_COVER_INIT, 32.0 * n, n);
 }
 
 void launch_bool(cudaStream_t s, const KbDev &kb, const BoolDesc *d_desc, uint32_t n_desc,
@@ -302,7 +302,7 @@ void launch_bool(cudaStream_t s, const KbDev &kb, const BoolDesc *d_desc, uint32
         prof_begin(s, KC_BOOL);
         k_bool<<<grid, 256, 0, s>>>(kb, d_desc + off, d_ops, counts);
         count_launch();
-        prof_end(s, KC_BOOL, alg_bytes * nd / n_desc);
+        prof_end(s, KC_BOOL, alg_bytes * nd / n_desc, nd);
     }
 }
 
@@ -316,12 +316,12 @@ void launch_restrict(cudaStream_t s, const KbDev &kb, const DirDev &dir, const R
         prof_begin(s, KC_RESTRICT);
         k_restrict<<<dim3(gx, nd), 256, 0, s>>>(kb, dir, d_desc + off, counts);
         count_launch();
-        prof_end(s, KC_RESTRICT, alg_light * nd / n_desc);
+        prof_end(s, KC_RESTRICT, alg_light * nd / n_desc, nd);
         if (dir.n_chunks) {
             prof_begin(s, KC_HEAVY);
             k_restrict_heavy<<<dim3(dir.n_chunks, nd), 256, 0, s>>>(kb, dir, d_desc + off, counts, heavy_scratch);
             count_launch();
-            prof_end(s, KC_HEAVY, alg_heavy * nd / n_desc);
+            prof_end(s, KC_HEAVY, alg_heavy * nd / n_desc, nd);
         }
     }
 }
@@ -335,7 +335,7 @@ void launch_drange(cudaStream_t s, const KbDev &kb, const uint32_t *row_ptr, con
         prof_begin(s, KC_DRANGE);
         k_drange<<<dim3(gx, nd), 256, 0, s>>>(kb, row_ptr, val, d_desc + off, counts);
         count_launch();
-        prof_end(s, KC_DRANGE, alg_bytes * nd / n_desc);
+        prof_end(s, KC_DRANGE, alg_bytes * nd / n_desc, nd);
     }
 }
 
@@ -345,7 +345,7 @@ void launch_gather_counts(cudaStream_t s, const hedl_counts *slots, const uint32
     prof_begin(s, KC_GATHER);
     k_gather_counts<<<cdiv(n, 256), 256, 0, s>>>(slots, slot_of, out, n);
     count_launch();
-    prof_end(s, KC_GATHER, 68.0 * n);
+    prof_end(s, KC_GATHER, 68.0 * n, n);
 }
 
 void launch_gather_bits(cudaStream_t s, const uint32_t *const *rows, uint32_t *out, uint32_t W, uint32_t n) {
@@ -355,7 +355,7 @@ void launch_gather_bits(cudaStream_t s, const uint32_t *const *rows, uint32_t *o
         prof_begin(s, KC_GATHER);
         k_gather_bits<<<dim3(cdiv(W, 256) < 32 ? cdiv(W, 256) : 32, nd), 256, 0, s>>>(rows + off, out + (uint64_t)off * W, W);
         count_launch();
-        prof_end(s, KC_GATHER, 8.0 * W * nd);
+        prof_end(s, KC_GATHER, 8.0 * W * nd, nd);
     }
 }
 

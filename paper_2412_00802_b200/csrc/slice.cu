@@ -594,7 +594,7 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
         prof_begin(s, KC_SLICE_IN);
         k_slice_pack<<<dim3(cdiv(kb->W4, PK_WORDS), packs), 256, pk_smem, s>>>(kd, dd, run, sc.T, sc.t_stride);
         count_launch();
-        prof_end(s, KC_SLICE_IN, 4.0 * kb->W * run + 32.0 * 32 * kb->W4 * packs);
+        prof_end(s, KC_SLICE_IN, 4.0 * kb->W * run + 32.0 * 32 * kb->W4 * packs, packs);
         const SliceDir &hd = ex ? sdx : sd;
         if (hd.n_chunks) {
             prof_begin(s, KC_SLICE_HEAVY);
@@ -602,7 +602,7 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             else k_slice_heavy<true><<<dim3(hd.n_chunks, packs), 256, 0, s>>>(hd, sc, dd, run);
             count_launch();
             const double eh = ex ? (double)dr.E_ex_heavy : (double)dr.E_heavy;
-            prof_end(s, KC_SLICE_HEAVY, (4.0 * eh + 32.0 * eh) * packs);
+            prof_end(s, KC_SLICE_HEAVY, (4.0 * eh + 32.0 * eh) * packs, packs);
         }
         if (ex) {
             prof_begin(s, KC_SLICE_EX);
@@ -610,7 +610,7 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             else k_slice_ex<true><<<dim3(dr.n_ex_blocks, packs), 256, 0, s>>>(xa, sc, dd, run, counts);
             count_launch();
             // example rows only: their CSR rows + 32 B T gathers + the projected rows
-            prof_end(s, KC_SLICE_EX, (8.0 * kb->M + 36.0 * dr.E_ex) * packs + 4.0 * kb->MW * run);
+            prof_end(s, KC_SLICE_EX, (8.0 * kb->M + 36.0 * dr.E_ex) * packs + 4.0 * kb->MW * run, packs);
         } else {
             prof_begin(s, KC_SLICE);
             if (cls == 0) k_slice_tile<false><<<dr.n_tiles, 256, smem, s>>>(kd, sd, sc, dd, run, counts);
@@ -618,7 +618,7 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             count_launch();
             // minimal DRAM bytes of one lane-packed pass: CSR once + T once (32 B per individual)
             // + the output rows; the 32 B-per-edge T gathers are L2 traffic (DESIGN.md K-SLICE)
-            prof_end(s, KC_SLICE, csr + 32.0 * 32 * kb->W4 + 4.0 * kb->W * run);
+            prof_end(s, KC_SLICE, csr + 32.0 * 32 * kb->W4 + 4.0 * kb->W * run, packs);
         }
         off += run;
     }

@@ -238,3 +238,27 @@ def test_parallel_compile_equivalent():
     sample = np.arange(0, len(roots), 37)
     _, oc = setsem.evaluate(kb, nodes, kids, roots[sample], threads=8, want_bits=False)
     assert np.array_equal(outs[1][sample], oc)
+
+
+def test_eval_one_latency_path():
+    """hedl_eval_one (single-launch interpreter when the sub-DAG fits in shared memory, else the
+    batch path) equals the oracle: C2 (all 256), random tiny KBs, a large-N fallback case."""
+    hedl = _hedl()
+    cases = [(abox.c2_kb(), hyps.c2_hypotheses(abox.c2_kb()))]
+    for seed in range(20):
+        kb = abox.random_tiny_kb(seed)
+        rng = np.random.default_rng(30_000 + seed)
+        cases.append((kb, [hyps.random_tree(rng, abox.kb_shape(kb), depth=4) for _ in range(12)]))
+    big = abox.powerlaw_kb(3_000_000, 4, 1, 4.0, 600, 0.5, 1.0, 0.001, 8)
+    cases.append((big, [("EXISTS", 0, False, ("ATOM", 1)), ("AND", [("ATOM", 0), ("MIN", 2, 0, True, ("ATOM", 2))])]))
+    for kb, trees in cases:
+        nodes, kids, roots = flatten(trees)
+        k = hedl.hedl_kb_load(kb, 0)
+        prog = hedl.hedl_compile(k, nodes, kids, roots)
+        ob, oc = setsem.evaluate(kb, nodes, kids, roots, threads=8)
+        for i in range(len(roots)):
+            b1, c1 = hedl.hedl_eval_one(k, prog, i, want_bits=True)
+            assert c1 == tuple(int(v) for v in oc[i]), (i, trees[i])
+            assert np.array_equal(b1.cpu().numpy().view(np.uint32), ob[i]), (i, trees[i])
+            _, c2 = hedl.hedl_eval_one(k, prog, i)
+            assert c2 == c1

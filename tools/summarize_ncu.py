@@ -33,7 +33,7 @@ def full_metrics(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hdr, units = rows[0], rows[1]
-    want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    want = ["launch__grid_size", "launch__grid_dim_y", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
             "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
             "sm__throughput.avg.pct_of_peak_sustained_elapsed", "lts__throughput.avg.pct_of_peak_sustained_elapsed"]
@@ -48,10 +48,18 @@ def full_metrics(rep):
     return res
 
 
+def to_bytes(v):
+    num, unit = v.split()[0], v.split()[1]
+    return float(num.replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+
+
 if __name__ == "__main__":
-    launches, rep, out_md, out_json = sys.argv[1:5]
+    launches, out_md, out_json = sys.argv[1:4]
+    reps = sys.argv[4:]
     sh = launch_shares(launches)
-    fm = full_metrics(rep)
+    fm = []
+    for rep in reps:
+        fm += full_metrics(rep)
     with open(out_md, "w") as f:
         f.write("# ncu summary\n\n## Launch list (gpu__time_duration.sum, --clock-control none; cold-cache, serialised)\n\n")
         f.write("| kernel | launches | total us | share |\n|---|---|---|---|\n")
@@ -62,22 +70,18 @@ if __name__ == "__main__":
         f.write("| " + " | ".join(keys) + " |\n|" + "---|" * len(keys) + "\n")
         for d in fm:
             f.write("| " + " | ".join(str(d.get(k, "")) for k in keys) + " |\n")
-    traffic = defaultdict(list)
+    name_map = {"k_slice_tile": "slice", "k_bool": "bool", "k_slice_pack": "slice_pack", "k_slice_ex": "slice_ex",
+                "k_slice_heavy": "slice_heavy", "k_restrict": "restrict", "k_restrict_heavy": "restrict_heavy",
+                "k_drange": "drange"}
+    tj = defaultdict(list)
     for d in fm:
         try:
-            rd = float(d["dram__bytes_read.sum"].split()[0].replace(",", ""))
-            wr = float(d["dram__bytes_write.sum"].split()[0].replace(",", ""))
-            unit = d["dram__bytes_read.sum"].split()[1]
-            sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-            traffic[d["kernel"]].append((rd + wr) * sc)
-        except Exception:
-            pass
-    name_map = {"k_slice_tile<0>": "slice", "k_slice_tile<1>": "slice", "k_bool": "bool", "k_slice_pack": "slice_pack",
-                "k_slice_heavy<0>": "slice_heavy", "k_slice_heavy<1>": "slice_heavy", "k_restrict": "restrict",
-                "k_restrict_heavy": "restrict_heavy", "k_drange": "drange"}
-    tj = defaultdict(list)
-    for k, v in traffic.items():
-        tj[name_map.get(k, k)] += v
-    json.dump({k: {"dram_bytes_per_launch": sum(v) / len(v), "captures": len(v)} for k, v in tj.items()},
+            tr = to_bytes(d["dram__bytes_read.sum"]) + to_bytes(d["dram__bytes_write.sum"])
+            gy = float(d.get("launch__grid_dim_y", "1 x").split()[0].replace(",", "") or 1)
+            tj[name_map.get(d["kernel"].split("<")[0], d["kernel"])].append((tr, gy))
+        except Exception as e:
+            print("skip", d.get("kernel"), e)
+    json.dump({k: {"dram_bytes_per_unit": sum(t for t, _ in v) / max(1.0, sum(g for _, g in v)),
+                   "captures": len(v), "units_captured": sum(g for _, g in v)} for k, v in tj.items()},
               open(out_json, "w"), indent=1)
     print(open(out_md).read())
