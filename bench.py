@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 (10M-individual) latency leg")
     ap.add_argument("--per-node", action="store_true", help="disable the lane-packed restriction path")
     ap.add_argument("--cache", default=os.environ.get("HEDL_CACHE", "/tmp/hedl_cache"))
     ap.add_argument("--seed", type=int, default=4)
@@ -235,6 +236,37 @@ def c2_latency(hedl, device):
             "p50_us_incl_compile": float(np.percentile(uc, 50)), "reps": len(us)}
 
 
+def c3_latency(hedl, device, cache):
+    """1-hypothesis latency on C3 (10^7 individuals, 1.6e8 assertions, power law to 1e5):
+    the 8 fixed nested exists/forall/inverse hypotheses, host wall time per hedl_eval_one
+    (KB loaded, hypothesis compiled), p50 over 20 reps, with each hypothesis' algorithmic
+    bytes B(h) and the HBM-roofline time B(h)/peak."""
+    from synth import abox, hyps
+    from synth.format import flatten
+    kb_np = _cached(cache, "c3kb_3", lambda: {k: np.asarray(v) for k, v in abox.c3_kb().items()})
+    kb_np["N"] = int(kb_np["N"])
+    nodes, kids, roots = flatten(hyps.c3_hypotheses())
+    k = hedl.hedl_kb_load(kb_np, device)
+    prog = hedl.hedl_compile(k, nodes, kids, roots)
+    rb = prog.root_bytes()
+    peak = measured_peaks().get("hbm_gbs", 6650.0) * 1e9
+    out = []
+    for i in range(len(roots)):
+        for _ in range(3):
+            hedl.hedl_eval_one(k, prog, i)
+        lat = []
+        for _ in range(20):
+            t0 = time.perf_counter()
+            hedl.hedl_eval_one(k, prog, i)
+            lat.append(time.perf_counter() - t0)
+        p50 = float(np.percentile(lat, 50)) * 1e6
+        out.append({"h": i, "p50_us": round(p50, 1), "alg_MB": round(rb[i] / 1e6, 1),
+                    "roofline_us": round(rb[i] / peak * 1e6, 1), "frac": round(rb[i] / peak * 1e6 / p50, 3)})
+    k.free()
+    return {"config": "C3 10M-individual power-law, 8 fixed hypotheses (H3a..)", "per_hypothesis": out,
+            "p50_us_median": float(np.median([o["p50_us"] for o in out]))}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -376,6 +408,14 @@ def main():
             lat = c2_latency(hedl, local)
         except Exception as e:  # latency is an extra; never hide the main number
             lat = {"error": str(e)}
+        if not args.no_c3:
+            try:
+                del prog
+                kb.free()
+                torch.cuda.empty_cache()
+                lat = {"c2": lat, "c3": c3_latency(hedl, local, args.cache)}
+            except Exception as e:
+                lat = {"c2": lat, "c3": {"error": str(e)}}
     line = {
         "metric": "hypotheses evaluated/sec", "value": value, "unit": "hyps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
