@@ -65,8 +65,9 @@ double node_bytes(const hedl_kb *kb, const CNode &n) {
 struct LocalDag {
     std::vector<CNode, NoInitAlloc<CNode>> nodes;
     std::vector<uint32_t, NoInitAlloc<uint32_t>> ops;
+    std::vector<uint8_t> rootonly;  // created for a root and kept out of the CSE table
     std::vector<uint32_t> table;   // open addressing: node id + 1, 0 = empty
-    uint64_t mask = 0;
+    uint64_t mask = 0, inserted = 0;
     bool cse = true;
 
     void grow() {
@@ -74,6 +75,7 @@ struct LocalDag {
         std::vector<uint32_t> t(cap, 0);
         const uint64_t m = cap - 1;
         for (uint32_t id = 0; id < nodes.size(); ++id) {
+            if (rootonly[id]) continue;
             uint64_t h = hash_node(nodes[id], ops.data() + nodes[id].op_begin) & m;
             while (t[h]) h = (h + 1) & m;
             t[h] = id + 1;
@@ -81,10 +83,13 @@ struct LocalDag {
         table.swap(t);
         mask = m;
     }
-    uint32_t intern(CNode n, const uint32_t *o) {
+    // nocse: a root's own node -- root conjunctions are almost never shared, so they skip
+    // the table here and in the global merge (a repeat only costs a duplicate count)
+    uint32_t intern(CNode n, const uint32_t *o, bool nocse = false) {
         uint64_t h = 0;
-        if (cse) {
-            if ((uint64_t)(nodes.size() + 1) * 2 > table.size()) grow();
+        const bool use = cse && !nocse;
+        if (use) {
+            if ((inserted + 1) * 2 > table.size()) grow();
             h = hash_node(n, o) & mask;
             while (table[h]) {
                 const uint32_t id = table[h] - 1;
@@ -104,7 +109,8 @@ struct LocalDag {
         n.level = has_node ? lvl + 1 : 0;
         const uint32_t id = (uint32_t)nodes.size();
         nodes.push_back(n);
-        if (cse) table[h] = id + 1;
+        rootonly.push_back(!use);
+        if (use) { table[h] = id + 1; ++inserted; }
         return id;
     }
 };
@@ -244,6 +250,7 @@ void canon_shard(const Input &in, uint32_t r0, uint32_t r1, Shard &sh) {
                     continue;
                 }
                 // all children are done: build the canonical reference of node i
+                const bool at_root = stack.size() == 1;      // the hypothesis' own node
                 const uint32_t *ch = in.child_idx + nd.child_begin;
                 const uint32_t cc = nd.child_count;
                 const bool is_role = nd.op >= HEDL_OP_EXISTS && nd.op <= HEDL_OP_EXACT;
@@ -290,7 +297,7 @@ void canon_shard(const Input &in, uint32_t r0, uint32_t r1, Shard &sh) {
                         CNode n{};
                         n.kind = kind;
                         n.op_count = (uint32_t)tmp.size();
-                        r = mkref(RT_NODE, D.intern(n, tmp.data()), 0);
+                        r = mkref(RT_NODE, D.intern(n, tmp.data(), at_root), 0);
                     }
                     break;
                 }
@@ -310,7 +317,7 @@ void canon_shard(const Input &in, uint32_t r0, uint32_t r1, Shard &sh) {
                     case HEDL_OP_MAX: n.pred = compat ? P_LEP : P_LE; n.n = nd.n; n.sat = nd.n + 1; break;
                     default: n.pred = P_EQ; n.n = nd.n; n.sat = nd.n + 1; break;             // EXACTLY
                     }
-                    r = mkref(RT_NODE, D.intern(n, &child), 0);
+                    r = mkref(RT_NODE, D.intern(n, &child, at_root), 0);
                     break;
                 }
                 case HEDL_OP_DRANGE: {
@@ -322,7 +329,7 @@ void canon_shard(const Input &in, uint32_t r0, uint32_t r1, Shard &sh) {
                     n.dir = (uint16_t)nd.arg;
                     n.lo = nd.lo;
                     n.hi = nd.hi;
-                    r = mkref(RT_NODE, D.intern(n, nullptr), 0);
+                    r = mkref(RT_NODE, D.intern(n, nullptr, at_root), 0);
                     break;
                 }
                 default:
@@ -355,7 +362,7 @@ struct Global {
         uint64_t onext = 0, oend = 0;
     };
 
-    uint32_t intern(CNode n, const uint32_t *o, Cursor &cur) {
+    uint32_t intern(CNode n, const uint32_t *o, Cursor &cur, bool nocse = false) {
         uint32_t mine = 0xffffffffu;
         auto materialise = [&]() {
             if (cur.next == cur.end) {
@@ -387,7 +394,7 @@ struct Global {
             n.bytes = node_bytes(kb, n);
             p->nodes[mine] = n;
         };
-        if (!cse) {
+        if (!cse || nocse) {
             materialise();
             return mine;
         }
@@ -468,7 +475,7 @@ extern "C" hedl_status hedl_compile(const hedl_kb *kb, const hedl_node *nodes, u
                 CNode n{};
                 n.kind = NK_AND;
                 n.op_count = 1;
-                const uint32_t id = D.intern(n, &r);
+                const uint32_t id = D.intern(n, &r, true);
                 D.nodes[id].bytes = node_bytes(kb, D.nodes[id]);
                 p->root_node[ri] = id;
             }
@@ -533,7 +540,7 @@ extern "C" hedl_status hedl_compile(const hedl_kb *kb, const hedl_node *nodes, u
                     tmp.resize(n.op_count);
                     for (uint32_t q = 0; q < n.op_count; ++q) tmp[q] = remap(t, D.ops[n.op_begin + q]);
                     if (rewrite && (n.kind == NK_AND || n.kind == NK_OR)) std::sort(tmp.begin(), tmp.end());
-                    gmap[t][li] = G.intern(n, tmp.data(), cursors[t]);
+                    gmap[t][li] = G.intern(n, tmp.data(), cursors[t], D.rootonly[li] != 0);
                 }
             });
         }
@@ -547,7 +554,7 @@ extern "C" hedl_status hedl_compile(const hedl_kb *kb, const hedl_node *nodes, u
                     CNode n{};
                     n.kind = NK_AND;
                     n.op_count = 1;
-                    p->root_node[a + k] = G.intern(n, &r, cursors[t]);
+                    p->root_node[a + k] = G.intern(n, &r, cursors[t], true);
                 }
             }
         });

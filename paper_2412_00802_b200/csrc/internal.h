@@ -83,6 +83,12 @@ struct hedl_dir {                  // one role direction
     uint32_t n_tiles = 0;
     uint4 *tiles = nullptr;            // device [n_tiles + 1]
     uint32_t *order = nullptr;         // device [N - n_heavy]: per tile medium rows then light rows, degree-descending
+    // light rows of each tile in SELL-16 slices (16 rows of similar degree, neighbours interleaved
+    // so the 16 row-pairs of a warp read 16 consecutive indices per step; pads = 0xffffffff)
+    uint32_t *tile_slice = nullptr;    // device [n_tiles + 1]: first slice of each tile
+    uint32_t *sell_off = nullptr;      // device [n_slices]: offset into sell_col
+    uint32_t *sell_w = nullptr;        // device [n_slices]: width (max degree) of the slice
+    uint32_t *sell_col = nullptr;      // device
     // example-row ("EX") packs: the same over the example ranks, 128 ranks per block
     uint32_t n_ex_blocks = 0;
     uint4 *ex_tiles = nullptr;         // device [n_ex_blocks + 1] {order begin, n_medium, n_light, ex-heavy begin}

@@ -305,6 +305,34 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
             }
             if ((s = upload(kb, st, &dr.tiles, tiles.data(), tiles.size()))) return bail(s);
             if ((s = upload(kb, st, &dr.order, order.data(), order.size()))) return bail(s);
+            {
+                std::vector<uint32_t> tslice(dr.n_tiles + 1), soff, sw, scol;
+                for (uint32_t t = 0; t < dr.n_tiles; ++t) {
+                    tslice[t] = (uint32_t)soff.size();
+                    const uint32_t l0 = tiles[t].x + tiles[t].y, nl = tiles[t].z;
+                    for (uint32_t a = 0; a < nl; a += 16) {
+                        const uint32_t x0 = order[l0 + a];
+                        // rows sorted: the first is widest; width padded to a multiple of 4 (4 gathers per step)
+                        const uint32_t wdt = (h.row_ptr[x0 + 1] - h.row_ptr[x0] + 3) & ~3u;
+                        soff.push_back((uint32_t)scol.size());
+                        sw.push_back(wdt);
+                        const size_t b = scol.size();
+                        scol.resize(b + (size_t)wdt * 16, 0xffffffffu);
+                        for (uint32_t i = 0; i < 16 && a + i < nl; ++i) {
+                            const uint32_t x = order[l0 + a + i];
+                            for (uint32_t k = 0, e = h.row_ptr[x]; e < h.row_ptr[x + 1]; ++e, ++k)
+                                scol[b + (size_t)k * 16 + i] = h.col[e];
+                        }
+                    }
+                }
+                tslice[dr.n_tiles] = (uint32_t)soff.size();
+                if (scol.size() >= 0xffffffffull) return bail(fail(HEDL_ERR_UNSUPPORTED, "SELL layout too large"));
+                if ((s = upload(kb, st, &dr.tile_slice, tslice.data(), tslice.size()))) return bail(s);
+                if ((s = upload(kb, st, &dr.sell_off, soff.data(), soff.size()))) return bail(s);
+                if ((s = upload(kb, st, &dr.sell_w, sw.data(), sw.size()))) return bail(s);
+                if ((s = upload(kb, st, &dr.sell_col, scol.data(), scol.size()))) return bail(s);
+                if (cudaStreamSynchronize(st) != cudaSuccess) return bail(fail(HEDL_ERR_CUDA, "upload failed"));
+            }
             // EX packs: example rows only (ranks of E), blocks of 128 ranks
             {
                 const std::vector<uint32_t> &ex = kb->h_ex;

@@ -16,6 +16,7 @@
 #include "slice.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace hedl {
 
@@ -29,6 +30,7 @@ struct SliceDir {
     const uint32_t *row_ptr, *col;
     const uint4 *tiles;           // [n_tiles + 1] {order begin, n_med, n_light, heavy begin}
     const uint32_t *order;
+    const uint32_t *tile_slice, *sell_off, *sell_w, *sell_col;   // SELL-16 light rows
     const uint32_t *heavy_x, *heavy_nchunks;
     const uint4 *chunks;
     uint32_t n_heavy, n_chunks, n_tiles;
@@ -77,28 +79,34 @@ __device__ __forceinline__ uint32_t warp_transpose(uint32_t x, uint32_t lane) {
     return x;
 }
 
-// every thread of the CTA calls; lanes >= count get "always 0" (am = om = 0, masks 0)
+// every thread of the CTA calls; lanes >= count get "always 0" (am = om = 0, masks 0).
+// Warp k builds the words of lanes 32k..32k+31 with ballots (no shared-memory atomics).
 __device__ void build_consts(PackConst &pc, const RestrictDesc *__restrict__ d, uint32_t count) {
-    uint32_t *w = reinterpret_cast<uint32_t *>(&pc);
-    for (uint32_t i = threadIdx.x; i < sizeof(PackConst) / 4; i += blockDim.x) w[i] = 0;
-    __syncthreads();
-    for (uint32_t j = threadIdx.x; j < count; j += blockDim.x) {
-        const RestrictDesc r = d[j];
-        const uint32_t k = j >> 5, bit = 1u << (j & 31);
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t k = threadIdx.x >> 5; k < LW; k += blockDim.x >> 5) {
+        const uint32_t j = k * 32 + lane;
+        uint32_t pred = 0xffu, n = 0;
+        if (j < count) {
+            pred = d[j].pred;
+            n = d[j].n;
+        }
         // OR class (sat <= 1): result is a function of b = (cnt >= 1)
         //   GE 0 -> 1 ; GE 1 -> b ; LE 0 / EQ 0 -> !b ; LEP 0 -> 0
-        bool am = false, fl = false, om = false;
-        if (r.pred == P_GE) { if (r.n == 0) om = true; else am = true; }
-        else if (r.pred == P_LE || r.pred == P_EQ) { am = true; fl = true; }
-        if (am) atomicOr(&pc.am[k], bit);
-        if (fl) atomicOr(&pc.fl[k], bit);
-        if (om) atomicOr(&pc.om[k], bit);
-        for (int q = 0; q < NPL; ++q)
-            if ((r.n >> q) & 1u) atomicOr(&pc.nb[q][k], bit);
-        if (r.pred == P_GE) atomicOr(&pc.mge[k], bit);
-        else if (r.pred == P_LE) atomicOr(&pc.mle[k], bit);
-        else if (r.pred == P_EQ) atomicOr(&pc.meq[k], bit);
-        else atomicOr(&pc.mlep[k], bit);
+        const bool ge = pred == P_GE, le = pred == P_LE, eq = pred == P_EQ, lep = pred == P_LEP;
+        const uint32_t am = __ballot_sync(FULL, (ge && n != 0) || le || eq);
+        const uint32_t fl = __ballot_sync(FULL, le || eq);
+        const uint32_t om = __ballot_sync(FULL, ge && n == 0);
+        const uint32_t mge = __ballot_sync(FULL, ge), mle = __ballot_sync(FULL, le);
+        const uint32_t meq = __ballot_sync(FULL, eq), mlep = __ballot_sync(FULL, lep);
+        uint32_t nb[NPL];
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) nb[q] = __ballot_sync(FULL, (n >> q) & 1u);
+        if (lane == 0) {
+            pc.am[k] = am; pc.fl[k] = fl; pc.om[k] = om;
+            pc.mge[k] = mge; pc.mle[k] = mle; pc.meq[k] = meq; pc.mlep[k] = mlep;
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) pc.nb[q][k] = nb[q];
+        }
     }
     __syncthreads();
 }
@@ -341,16 +349,32 @@ __global__ void __launch_bounds__(256) k_slice_heavy(SliceDir dir, SliceScratch 
 // ------------------------------------------------------------------------------
 // tile of 1024 consecutive individuals per CTA (256 threads = 128 lane pairs).
 template <bool COUNT>
-__global__ void __launch_bounds__(256, COUNT ? 3 : 4) k_slice_tile(KbDev kb, SliceDir dir, SliceScratch sc,
+__global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, SliceScratch sc,
                                                                    const RestrictDesc *__restrict__ d, uint32_t count,
-                                                                   hedl_counts *counts) {
+                                                                   hedl_counts *counts, uint32_t dbg) {
     extern __shared__ uint32_t smem[];
     PackConst &pc = *reinterpret_cast<PackConst *>(smem);
     uint32_t *ot = smem + sizeof(PackConst) / 4;          // [1024][TROW]
     const uint32_t t = blockIdx.x;
     const uint32_t x0 = t * 1024;
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, half = lane & 1;
-    for (uint32_t i = threadIdx.x; i < 1024 * TROW; i += 256) ot[i] = 0;
+    __shared__ uint32_t s_exm[32], s_exb[32];
+    if (x0 + 1024 > kb.N)                                  // only the last tile has rows >= N (left 0)
+        for (uint32_t i = threadIdx.x; i < 1024 * TROW; i += 256) ot[i] = 0;
+    if (threadIdx.x < 32) {
+        const uint32_t w = t * 32 + threadIdx.x;
+        s_exm[threadIdx.x] = w < kb.W ? __ldg(kb.ex_mask + w) : 0u;
+        s_exb[threadIdx.x] = w < kb.W ? __ldg(kb.ex_base + w) : 0u;
+    }
+    // this lane's node for the transpose-back phase, fetched early (its latency hides under the sweep)
+    const uint32_t jn = wid * 32 + lane;
+    uint32_t *r_out = nullptr, *r_proj = nullptr;
+    int32_t r_cover = -1;
+    if (jn < count) {
+        r_out = d[jn].out;
+        r_proj = d[jn].proj;
+        r_cover = d[jn].cover;
+    }
     build_consts(pc, d, count);                           // (contains __syncthreads)
     const uint4 ti = dir.tiles[t];
     const uint32_t hbeg = ti.w, hend = dir.tiles[t + 1].w;
@@ -360,7 +384,7 @@ __global__ void __launch_bounds__(256, COUNT ? 3 : 4) k_slice_tile(KbDev kb, Sli
         for (int k = 0; k < LW; ++k) ot[xl * TROW + k] = sc.hout[(size_t)h * LW + k];
     }
     // medium rows: warp per row, the 16 lane pairs split its neighbours
-    for (uint32_t m = wid; m < ti.y; m += 8) {
+    for (uint32_t m = wid; m < ((dbg & 2) ? 0u : ti.y); m += 8) {
         const uint32_t x = __ldg(dir.order + ti.x + m);
         const uint32_t a = __ldg(dir.row_ptr + x), b = __ldg(dir.row_ptr + x + 1);
         Acc<COUNT> acc;
@@ -372,37 +396,63 @@ __global__ void __launch_bounds__(256, COUNT ? 3 : 4) k_slice_tile(KbDev kb, Sli
             for (int k = 0; k < HW; ++k) ot[(x - x0) * TROW + half * HW + k] = acc.result(pc, half * HW + k, k);
         }
     }
-    // light rows: lane pair per row (rows sorted by degree, so a warp's trip counts agree)
-    for (uint32_t l = threadIdx.x >> 1; l < ti.z; l += 128) {
-        const uint32_t x = __ldg(dir.order + ti.x + ti.y + l);
-        const uint32_t a = __ldg(dir.row_ptr + x), b = __ldg(dir.row_ptr + x + 1);
+    // light rows: SELL-16 slices, a warp per slice, a lane pair per row; the 16 pairs read 16
+    // consecutive neighbour indices per step (coalesced), 4 steps of T gathers in flight
+    const uint32_t sbeg = __ldg(dir.tile_slice + t), send = __ldg(dir.tile_slice + t + 1);
+    for (uint32_t sl = sbeg + wid; sl < ((dbg & 1) ? sbeg : send); sl += 8) {
+        const uint32_t li = (sl - sbeg) * 16 + (lane >> 1);
+        const bool rv = li < ti.z;
+        const uint32_t x = rv ? __ldg(dir.order + ti.x + ti.y + li) : 0u;
+        const uint32_t *c = dir.sell_col + __ldg(dir.sell_off + sl) + (lane >> 1);
+        const uint32_t w = __ldg(dir.sell_w + sl);
         Acc<COUNT> acc;
         acc.zero();
-        scan_edges<COUNT>(acc, dir.col, sc.T, a, b, 1, half);
+        uint32_t k = 0;
+        for (; k + 4 <= w; k += 4) {
+            uint32_t y[4];
 #pragma unroll
-        for (int k = 0; k < HW; ++k) ot[(x - x0) * TROW + half * HW + k] = acc.result(pc, half * HW + k, k);
+            for (int u = 0; u < 4; ++u) y[u] = __ldg(c + (k + u) * 16);
+            uint4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                v[u] = y[u] != 0xffffffffu ? __ldg(sc.T + 2ull * y[u] + half) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc.add(v[u]);
+        }
+        if (rv) {
+#pragma unroll
+            for (int q = 0; q < HW; ++q) ot[(x - x0) * TROW + half * HW + q] = acc.result(pc, half * HW + q, q);
+        }
     }
     __syncthreads();
     // transpose back: warp g writes lanes 32g..32g+31 (node rows), 4 words per store
     const uint32_t g = wid;
-    const uint32_t j = g * 32 + lane;
-    const bool live = j < count;
-    RestrictDesc r{};
-    if (live) r = d[j];
+    const bool live = jn < count;
     uint32_t tp = 0, fp = 0;
-    for (uint32_t wl = 0; wl < 32; wl += 4) {
+    for (uint32_t wl = 0; wl < ((dbg & 4) ? 0u : 32u); wl += 4) {
         const uint32_t w = t * 32 + wl;
         if (w >= kb.W4) break;
         uint32_t o[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) o[q] = warp_transpose(ot[((wl + q) * 32 + lane) * TROW + g], lane);
         if (live) {
-            if (r.out) *reinterpret_cast<uint4 *>(r.out + w) = make_uint4(o[0], o[1], o[2], o[3]);
-            if (r.proj) {
+            if (r_out) *reinterpret_cast<uint4 *>(r_out + w) = make_uint4(o[0], o[1], o[2], o[3]);
+            if (r_proj) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) if (w + q < kb.W) proj_scatter(kb, r.proj, w + q, o[q]);
+                for (int q = 0; q < 4; ++q) {
+                    // example bits of word w+q -> the projected row (pext with the staged masks)
+                    uint32_t m = s_exm[wl + q];
+                    const uint32_t word = o[q];
+                    if (!m || !word) continue;
+                    uint32_t bits = 0, nb = 0;
+                    for (; m; m &= m - 1, ++nb) bits |= ((word >> (__ffs(m) - 1)) & 1u) << nb;
+                    if (!bits) continue;
+                    const uint32_t base = s_exb[wl + q], sh = base & 31;
+                    atomicOr(r_proj + (base >> 5), bits << sh);
+                    if (sh && sh + nb > 32) atomicOr(r_proj + (base >> 5) + 1, bits >> (32 - sh));
+                }
             }
-            if (r.cover >= 0) {
+            if (r_cover >= 0) {
                 const uint4 p = __ldg(reinterpret_cast<const uint4 *>(kb.pos + w));
                 const uint4 n = __ldg(reinterpret_cast<const uint4 *>(kb.neg + w));
                 tp += __popc(o[0] & p.x) + __popc(o[1] & p.y) + __popc(o[2] & p.z) + __popc(o[3] & p.w);
@@ -410,8 +460,8 @@ __global__ void __launch_bounds__(256, COUNT ? 3 : 4) k_slice_tile(KbDev kb, Sli
             }
         }
     }
-    if (live && r.cover >= 0 && (tp | fp)) {
-        hedl_counts *c = counts + r.cover;
+    if (live && r_cover >= 0 && (tp | fp)) {
+        hedl_counts *c = counts + r_cover;
         if (tp) {
             atomicAdd((unsigned long long *)&c->tp, (unsigned long long)tp);
             atomicAdd((unsigned long long *)&c->fn, 0ull - tp);
@@ -561,9 +611,10 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
         sc.h_stride = 0;
         return sc;
     };
-    SliceDir sd{dr.row_ptr, dr.col, dr.tiles, dr.order, dr.heavy_x, dr.heavy_nchunks, dr.chunks,
-                dr.n_heavy, dr.n_chunks, dr.n_tiles};
-    SliceDir sdx{dr.row_ptr, dr.col, nullptr, nullptr, dr.ex_hx, dr.ex_hn, dr.ex_chunks, dr.n_ex_heavy, dr.n_ex_chunks, 0};
+    SliceDir sd{dr.row_ptr, dr.col, dr.tiles, dr.order, dr.tile_slice, dr.sell_off, dr.sell_w, dr.sell_col,
+                dr.heavy_x, dr.heavy_nchunks, dr.chunks, dr.n_heavy, dr.n_chunks, dr.n_tiles};
+    SliceDir sdx{dr.row_ptr, dr.col, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                 dr.ex_hx, dr.ex_hn, dr.ex_chunks, dr.n_ex_heavy, dr.n_ex_chunks, 0};
     const ExArgs xa{dr.row_ptr, dr.col, dr.ex_tiles, dr.ex_order, kb->ex_ids, dr.ex_hrank, kb->ppos, kb->pneg, kb->MW4};
     const size_t smem = sizeof(PackConst) + 1024 * TROW * 4;
     const size_t pk_smem = 256 * PK_STRIDE * 4;
@@ -613,8 +664,9 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             prof_end(s, KC_SLICE_EX, (8.0 * kb->M + 36.0 * dr.E_ex) * packs + 4.0 * kb->MW * run, packs);
         } else {
             prof_begin(s, KC_SLICE);
-            if (cls == 0) k_slice_tile<false><<<dr.n_tiles, 256, smem, s>>>(kd, sd, sc, dd, run, counts);
-            else k_slice_tile<true><<<dr.n_tiles, 256, smem, s>>>(kd, sd, sc, dd, run, counts);
+            static const uint32_t dbg = getenv("HEDL_DBG_TILE") ? (uint32_t)atoi(getenv("HEDL_DBG_TILE")) : 0u;
+            if (cls == 0) k_slice_tile<false><<<dr.n_tiles, 256, smem, s>>>(kd, sd, sc, dd, run, counts, dbg);
+            else k_slice_tile<true><<<dr.n_tiles, 256, smem, s>>>(kd, sd, sc, dd, run, counts, dbg);
             count_launch();
             // minimal DRAM bytes of one lane-packed pass: CSR once + T once (32 B per individual)
             // + the output rows; the 32 B-per-edge T gathers are L2 traffic (DESIGN.md K-SLICE)
