@@ -143,9 +143,10 @@ class KB:
                 "heavy": list(inf.heavy[:2 * R])}
 
     def free(self):
-        if self._h:
+        """Release this handle (programs compiled against it keep the KB alive until freed)."""
+        if self._h and not getattr(self, "_released", False):
             lib().hedl_kb_free(self._h)
-            self._h = None
+            self._released = True
 
     def __del__(self):
         try:

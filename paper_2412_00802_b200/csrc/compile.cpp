@@ -571,6 +571,7 @@ extern "C" hedl_status hedl_compile(const hedl_kb *kb, const hedl_node *nodes, u
         if (n.kind != NK_DEAD) { maxl = std::max(maxl, n.level); any = true; }
     p->n_levels = any ? maxl + 1 : 0;
     p->stamp.assign(p->nodes.size(), 0);
+    const_cast<hedl_kb *>(kb)->refs.fetch_add(1);        // released by hedl_program_free
     timing_note("compile: shards", t1 - t0);
     timing_note("compile: total", now_ms() - t0);
     *out = p;

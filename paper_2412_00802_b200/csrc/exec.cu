@@ -11,6 +11,7 @@
 // kept device-resident in the program, and replayed by later calls.  Counts come
 // back with one D2H per call (the paper's single cudaMemcpyAsync).
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <thread>
 
@@ -57,7 +58,9 @@ struct PlanCache {
 };
 
 struct Workspace {
-    DevBuf rows, prows, heavy, counts, slice;
+    DevBuf rows, prows, heavy, counts, slice, stage;
+    hedl_counts *stage_host = nullptr;   // pinned staging of host-bound counts
+    size_t stage_host_n = 0;
     PlanCache plan;
     cudaEvent_t done = nullptr;
     cudaStream_t last_stream = nullptr;
@@ -173,6 +176,12 @@ void par_for(size_t n, size_t grain, F f) {
 // out[k] = rank of k among the k' < k with flag(k') (for flagged k); returns the count
 template <class Flag, class Out>
 uint32_t par_rank(size_t n, Flag flag, Out &out) {
+    if (n < (1u << 15)) {                          // small plans: no thread start-up
+        uint32_t r = 0;
+        for (size_t k = 0; k < n; ++k)
+            if (flag(k)) out[k] = r++;
+        return r;
+    }
     const size_t C = 64;
     std::vector<uint32_t> cnt(C + 1, 0);
     par_for(C, 1, [&](size_t c0, size_t c1) {
@@ -253,7 +262,7 @@ void collect_chunks(hedl_program *p, uint32_t r0, uint32_t r1, uint64_t row_cap,
     if (p->stamp.size() < p->nodes.size()) p->stamp.assign(p->nodes.size(), 0);
     if (r0 == 0 && r1 == p->root_node.size()) {
         // the whole program: every live node is reachable from a root
-        const size_t NN = p->nodes.size(), C = 64;
+        const size_t NN = p->nodes.size(), C = NN < (1u << 15) ? 1 : 64;
         std::vector<uint32_t> cnt(C + 1, 0);
         par_for(C, 1, [&](size_t c0, size_t c1) {
             for (size_t c = c0; c < c1; ++c)
@@ -513,7 +522,7 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
     for (uint32_t gi = 0; gi < groups.size(); ++gi)
         for (uint32_t m = groups[gi].first; m < groups[gi].first + groups[gi].count; m += 8192)
             tasks.push_back({gi, m, std::min(m + 8192, groups[gi].first + groups[gi].count), 0, 0});
-    par_for(tasks.size(), 1, [&](size_t t0, size_t t1) {
+    par_for(tasks.size(), nn < (1u << 15) ? tasks.size() : 1, [&](size_t t0, size_t t1) {
         for (size_t ti = t0; ti < t1; ++ti) {
             Task &T = tasks[ti];
             const Group &g = groups[T.g];
@@ -745,25 +754,33 @@ extern "C" hedl_status hedl_eval_batch(const hedl_kb *kb, hedl_program *p, uint3
     DeviceGuard dg(kb->device);
     cudaStream_t s = (cudaStream_t)stream;
     hedl_counts *dcounts = counts;
-    void *stage = nullptr;
     const bool host_out = !(flags & HEDL_EVAL_COUNTS_DEVICE);
-    if (host_out) {
-        cudaError_t e = cudaMallocAsync(&stage, (size_t)n * sizeof(hedl_counts), s);
-        if (e != cudaSuccess) { cudaGetLastError(); return fail(HEDL_ERR_OOM, "count staging allocation failed"); }
-        dcounts = (hedl_counts *)stage;
+    Workspace *w = ws_of(p);
+    const size_t cbytes = (size_t)n * sizeof(hedl_counts);
+    if (host_out) {                                   // device staging kept in the workspace
+        hedl_status st = grow(kb, s, w->stage, cbytes, false, PR_COUNTS);
+        if (st) return st;
+        dcounts = (hedl_counts *)w->stage.p;
+        if (w->stage_host_n < n && n <= (1u << 16)) {  // small results go through pinned memory
+            if (w->stage_host) cudaFreeHost(w->stage_host);
+            w->stage_host = nullptr;
+            w->stage_host_n = 0;
+            if (cudaMallocHost((void **)&w->stage_host, std::max<size_t>(cbytes, 4096)) == cudaSuccess)
+                w->stage_host_n = std::max<size_t>(cbytes, 4096) / sizeof(hedl_counts);
+            else
+                cudaGetLastError();
+        }
     }
     hedl_status st = run(kb, p, first, first + n, out_bits, dcounts, s, flags & ~HEDL_EVAL_COUNTS_DEVICE);
-    if (host_out) {
-        if (st == HEDL_OK) {
-            cudaError_t e = cudaMemcpyAsync(counts, dcounts, (size_t)n * sizeof(hedl_counts), cudaMemcpyDeviceToHost, s);
-            count_io(0, (uint64_t)n * sizeof(hedl_counts));
-            if (e != cudaSuccess) st = cuda_fail(kb, e, "count D2H");
-        }
-        cudaFreeAsync(stage, s);
-        if (st == HEDL_OK) {
-            cudaError_t e = cudaStreamSynchronize(s);
-            if (e != cudaSuccess) st = cuda_fail(kb, e, "eval_batch sync");
-        }
+    if (host_out && st == HEDL_OK) {
+        const bool pinned = w->stage_host && w->stage_host_n >= n;
+        cudaError_t e = cudaMemcpyAsync(pinned ? (void *)w->stage_host : (void *)counts, dcounts, cbytes,
+                                        cudaMemcpyDeviceToHost, s);
+        count_io(0, cbytes);
+        if (e != cudaSuccess) return cuda_fail(kb, e, "count D2H");
+        e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return cuda_fail(kb, e, "eval_batch sync");
+        if (pinned) std::memcpy(counts, w->stage_host, cbytes);
     }
     return st;
 }
@@ -824,7 +841,10 @@ extern "C" hedl_status hedl_eval_one(const hedl_kb *kb, hedl_program *p, uint32_
     if (kb->poisoned) return fail(HEDL_ERR_CUDA, "KB handle is poisoned by an earlier CUDA error");
     if (root >= p->root_node.size()) return fail(HEDL_ERR_OUT_OF_RANGE, "root out of range");
     static thread_local InterpProg prog;   // ~5 KB: keep it off the stack
-    if (kb->N && build_interp(kb, p, p->root_node[root], prog)) {
+    // a single CTA wins while launch/sync overheads dominate; above ~64k individuals the
+    // multi-CTA per-node kernels are faster (measured, tools/opbench.py)
+    static const bool no_interp = std::getenv("HEDL_NO_INTERP") != nullptr;
+    if (kb->N && kb->N <= kInterpMaxN && !no_interp && build_interp(kb, p, p->root_node[root], prog)) {
         std::lock_guard<std::mutex> lk(p->mu);
         DeviceGuard dg(kb->device);
         hedl_kb *mkb = const_cast<hedl_kb *>(kb);
@@ -866,6 +886,8 @@ extern "C" hedl_status hedl_program_free(hedl_program *p) {
         const int roles[] = {PR_ROWS, PR_PROWS, PR_HEAVY, PR_COUNTS, PR_SLICE};
         int ri = 0;
         for (DevBuf *b : {&w->rows, &w->prows, &w->heavy, &w->counts, &w->slice}) pool_give(p->kb, roles[ri++], b->p, b->bytes);
+        pool_give(p->kb, PR_COUNTS, w->stage.p, w->stage.bytes);
+        if (w->stage_host) cudaFreeHost(w->stage_host);
         pool_give(p->kb, PR_PLAN_HOST, w->plan.host, w->plan.cap);
         pool_give(p->kb, PR_PLAN_DEV, w->plan.dev, w->plan.cap);
         w->plan.host = w->plan.dev = nullptr;
@@ -873,8 +895,12 @@ extern "C" hedl_status hedl_program_free(hedl_program *p) {
         if (w->done) cudaEventDestroy(w->done);
         if (p->lat_host) cudaFreeHost(p->lat_host);
         delete w;
+    } else if (p->lat_host) {
+        cudaFreeHost(p->lat_host);
     }
+    const hedl_kb *kb = p->kb;
     delete p;
+    kb_release(kb);
     return HEDL_OK;
 }
 

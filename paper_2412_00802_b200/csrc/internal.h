@@ -127,6 +127,7 @@ struct hedl_kb {
     std::vector<void *> allocs;
     uint64_t device_bytes = 0;
     std::atomic<bool> poisoned{false};
+    std::atomic<int> refs{1};            // the handle itself + every live program compiled against it
     // buffers released by freed programs, reused by the next ones (no cudaMalloc /
     // cudaMallocHost / memset per program); accumulator buffers return self-cleaned
     mutable std::mutex pool_mu;
@@ -177,6 +178,7 @@ enum PoolRole { PR_ROWS, PR_PROWS, PR_HEAVY, PR_COUNTS, PR_SLICE, PR_PLAN_DEV, P
 void *pool_take(const hedl_kb *kb, int role, size_t need, size_t *got);
 void pool_give(const hedl_kb *kb, int role, void *p, size_t bytes);
 void pool_release_all(hedl_kb *kb);
+void kb_release(const hedl_kb *kb);     // drop one reference; frees the KB at zero
 
 // ---- host phase timing (HEDL_TIMING=1 prints to stderr) ---------------------------
 bool timing_enabled();

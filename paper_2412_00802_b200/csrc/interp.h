@@ -4,6 +4,7 @@
 
 namespace hedl {
 constexpr uint32_t kInterpMaxNodes = 96, kInterpMaxOps = 512;
+constexpr uint32_t kInterpMaxN = 1u << 16;   // individuals; larger KBs use the per-node kernels
 
 struct InterpNode {
     uint8_t kind, pred;

@@ -410,8 +410,16 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
     return HEDL_OK;
 }
 
+namespace hedl {
+void kb_release(const hedl_kb *kb) {
+    if (kb && const_cast<hedl_kb *>(kb)->refs.fetch_sub(1) == 1) free_kb(const_cast<hedl_kb *>(kb));
+}
+}  // namespace hedl
+
+// Programs keep their KB alive: the device memory goes when the handle and every
+// program compiled against it are freed (in any order).
 extern "C" hedl_status hedl_kb_free(hedl_kb *kb) {
-    free_kb(kb);
+    kb_release(kb);
     return HEDL_OK;
 }
 

@@ -262,3 +262,19 @@ def test_eval_one_latency_path():
             assert np.array_equal(b1.cpu().numpy().view(np.uint32), ob[i]), (i, trees[i])
             _, c2 = hedl.hedl_eval_one(k, prog, i)
             assert c2 == c1
+
+
+def test_free_order_kb_before_program():
+    """A program keeps its KB alive: freeing the KB handle first, then the program, leaves the
+    library healthy for the next KB (regression: use-after-free on the KB's device id)."""
+    hedl = _hedl()
+    kb = abox.c1_kb()
+    nodes, kids, roots = flatten(hyps.c1_hypotheses(kb))
+    for _ in range(3):
+        k = hedl.hedl_kb_load(kb, 0)
+        prog = hedl.hedl_compile(k, nodes, kids, roots)
+        _, c = hedl.hedl_eval_one(k, prog, 3)
+        k.free()                        # program still alive: evaluation must keep working
+        _, c2 = hedl.hedl_eval_batch(k, prog, 3, 1)
+        assert tuple(int(v) for v in c2[0]) == c
+        prog.free()
