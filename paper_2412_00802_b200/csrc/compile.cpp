@@ -83,8 +83,8 @@ struct LocalDag {
         table.swap(t);
         mask = m;
     }
-    // nocse: a root's own node -- root conjunctions are almost never shared, so they skip
-    // the table here and in the global merge (a repeat only costs a duplicate count)
+    // nocse: a root's own conjunction/disjunction -- almost never shared and cheap on the
+    // GPU (example-projected), so it skips the table here and in the global merge
     uint32_t intern(CNode n, const uint32_t *o, bool nocse = false) {
         uint64_t h = 0;
         const bool use = cse && !nocse;
@@ -317,7 +317,7 @@ void canon_shard(const Input &in, uint32_t r0, uint32_t r1, Shard &sh) {
                     case HEDL_OP_MAX: n.pred = compat ? P_LEP : P_LE; n.n = nd.n; n.sat = nd.n + 1; break;
                     default: n.pred = P_EQ; n.n = nd.n; n.sat = nd.n + 1; break;             // EXACTLY
                     }
-                    r = mkref(RT_NODE, D.intern(n, &child, at_root), 0);
+                    r = mkref(RT_NODE, D.intern(n, &child), 0);        // restrictions are always shared
                     break;
                 }
                 case HEDL_OP_DRANGE: {
@@ -329,7 +329,7 @@ void canon_shard(const Input &in, uint32_t r0, uint32_t r1, Shard &sh) {
                     n.dir = (uint16_t)nd.arg;
                     n.lo = nd.lo;
                     n.hi = nd.hi;
-                    r = mkref(RT_NODE, D.intern(n, nullptr, at_root), 0);
+                    r = mkref(RT_NODE, D.intern(n, nullptr), 0);
                     break;
                 }
                 default:
