@@ -111,7 +111,8 @@ void free_kb(hedl_kb *kb) {
 extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *stream, hedl_kb **out) {
     if (!desc || !out) return fail(HEDL_ERR_INVALID_ARG, "null desc/out");
     *out = nullptr;
-    const uint32_t N = desc->n_individuals, W = (N + 31) / 32, W4 = (W + 3) & ~3u;
+    // rows padded to 8 words (32 B = one L2 sector) so row segments start on sector boundaries
+    const uint32_t N = desc->n_individuals, W = (N + 31) / 32, W4 = (W + 7) & ~7u;
     const uint32_t C = desc->n_concepts, R = desc->n_roles, D = desc->n_data;
     if (R > 32) return fail(HEDL_ERR_INVALID_ARG, "at most 32 roles supported");
     if (C && W && !desc->concept_bits) return fail(HEDL_ERR_INVALID_ARG, "concept_bits is null");

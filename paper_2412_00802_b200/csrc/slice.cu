@@ -429,17 +429,22 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
     const uint32_t g = wid;
     const bool live = jn < count;
     uint32_t tp = 0, fp = 0;
-    for (uint32_t wl = 0; wl < ((dbg & 4) ? 0u : 32u); wl += 4) {
+    // 8 words per step: each lane writes one whole 32 B sector of its node's row
+    for (uint32_t wl = 0; wl < ((dbg & 4) ? 0u : 32u); wl += 8) {
         const uint32_t w = t * 32 + wl;
-        if (w >= kb.W4) break;
-        uint32_t o[4];
+        if (w >= kb.W4) break;                             // W4 is a multiple of 8
+        uint32_t o[8];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) o[q] = warp_transpose(ot[((wl + q) * 32 + lane) * TROW + g], lane);
+        for (int q = 0; q < 8; ++q) o[q] = warp_transpose(ot[((wl + q) * 32 + lane) * TROW + g], lane);
         if (live) {
-            if (r_out) *reinterpret_cast<uint4 *>(r_out + w) = make_uint4(o[0], o[1], o[2], o[3]);
+            if (r_out) {
+                uint4 *dst = reinterpret_cast<uint4 *>(r_out + w);
+                dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+                dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+            }
             if (r_proj) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < 8; ++q) {
                     // example bits of word w+q -> the projected row (pext with the staged masks)
                     uint32_t m = s_exm[wl + q];
                     const uint32_t word = o[q];
@@ -453,10 +458,15 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
                 }
             }
             if (r_cover >= 0) {
-                const uint4 p = __ldg(reinterpret_cast<const uint4 *>(kb.pos + w));
-                const uint4 n = __ldg(reinterpret_cast<const uint4 *>(kb.neg + w));
-                tp += __popc(o[0] & p.x) + __popc(o[1] & p.y) + __popc(o[2] & p.z) + __popc(o[3] & p.w);
-                fp += __popc(o[0] & n.x) + __popc(o[1] & n.y) + __popc(o[2] & n.z) + __popc(o[3] & n.w);
+                const uint4 *pp = reinterpret_cast<const uint4 *>(kb.pos + w);
+                const uint4 *nn = reinterpret_cast<const uint4 *>(kb.neg + w);
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const uint4 p = __ldg(pp + hh), n = __ldg(nn + hh);
+                    const uint32_t *oo = o + 4 * hh;
+                    tp += __popc(oo[0] & p.x) + __popc(oo[1] & p.y) + __popc(oo[2] & p.z) + __popc(oo[3] & p.w);
+                    fp += __popc(oo[0] & n.x) + __popc(oo[1] & n.y) + __popc(oo[2] & n.z) + __popc(oo[3] & n.w);
+                }
             }
         }
     }

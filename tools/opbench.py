@@ -60,18 +60,22 @@ def concepts_kb(n, k, seed):
             "pos_ids": np.sort(perm[:m]).astype(np.uint32), "neg_ids": np.sort(perm[m:2 * m]).astype(np.uint32)}
 
 
-def measure(kb_np, tree, reps, check):
+def measure(kb_np, tree, reps, check, bits=True):
+    """bits=True: the instance bitset is produced (full-row work, as the paper's operators);
+    bits=False: counts only (root conjunctions run on example-projected rows)."""
+    import torch
     k = hedl.hedl_kb_load(kb_np, 0)
     nodes, kids, roots = flatten([tree])
     prog = hedl.hedl_compile(k, nodes, kids, roots)
     for _ in range(3):
-        hedl.hedl_eval_one(k, prog, 0)
+        hedl.hedl_eval_one(k, prog, 0, want_bits=bits)
     lat, ker = [], []
     for _ in range(reps):
         hedl.prof_reset()
         hedl.prof_enable(True)
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
-        _, c = hedl.hedl_eval_one(k, prog, 0)
+        _, c = hedl.hedl_eval_one(k, prog, 0, want_bits=bits)
         lat.append(time.perf_counter() - t0)
         hedl.prof_enable(False)
         ker.append(sum(e["total_ms"] for e in hedl.prof_read()))
@@ -80,6 +84,7 @@ def measure(kb_np, tree, reps, check):
         b, c = hedl.hedl_eval_one(k, prog, 0, want_bits=True)
         ob, oc = setsem.evaluate(kb_np, nodes, kids, roots, threads=os.cpu_count())
         ok = bool(np.array_equal(b.cpu().numpy().view(np.uint32), ob[0]) and c == tuple(int(v) for v in oc[0]))
+    prog.free()
     k.free()
     return float(np.median(lat)) * 1e6, float(np.median(ker)) * 1e3, ok
 
@@ -98,6 +103,9 @@ def main():
             lat, ker, ok = measure(kb, tree, 30, n <= 1_000_000)
             rows.append({"op": name, "size": n, "latency_us": lat, "kernel_us": ker, "parity": ok,
                          "paper_gtx970_us": PAPER_GPU.get((name, n))})
+            lat, ker, _ = measure(kb, tree, 30, False, bits=False)
+            rows.append({"op": name + " (counts only)", "size": n, "latency_us": lat, "kernel_us": ker, "parity": None,
+                         "paper_gtx970_us": None})
     kb = concepts_kb(1_000_000, 32, 7)                        # Table 2: 10^6 individuals, 1..32 concepts
     for k in (1, 2, 4, 8, 16, 32):
         lat, ker, ok = measure(kb, ("AND", [A(i) for i in range(k)]) if k > 1 else ("AND", [A(0), ("TOP",)]), 30, True)
