@@ -13,6 +13,8 @@
 // Every output word is written exactly once by one warp (plus commutative
 // atomicOr of heavy bits), so results are deterministic (no paper-style
 // check-then-write race).
+#include <algorithm>
+
 #include "internal.h"
 
 namespace hedl {
@@ -298,7 +300,9 @@ void launch_bool(cudaStream_t s, const KbDev &kb, const BoolDesc *d_desc, uint32
         const uint32_t nd = n_desc - off < 65535 ? n_desc - off : 65535;
         const uint32_t gx = kb.W4 ? cdiv(kb.W4 / 4, 256) : 0;
         if (!gx) return;
-        dim3 grid(gx < 64 ? gx : 64, nd);
+        // enough CTAs to fill the 148 SMs even when the launch has few nodes
+        const uint32_t cap = std::max<uint32_t>(64, 148u * 8u / nd);
+        dim3 grid(gx < cap ? gx : cap, nd);
         prof_begin(s, KC_BOOL);
         k_bool<<<grid, 256, 0, s>>>(kb, d_desc + off, d_ops, counts);
         count_launch();
