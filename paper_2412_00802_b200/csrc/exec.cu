@@ -631,7 +631,8 @@ hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, u
                                            lr.ex);
                 if (st) return st;
             } else {
-                DirDev dd{dr.row_ptr, dr.col, dr.heavy_x, dr.heavy_nchunks, dr.chunks, dr.n_heavy, dr.n_chunks};
+                DirDev dd{dr.row_ptr, dr.col, dr.heavy_x, dr.heavy_nchunks, dr.chunks, dr.n_heavy, dr.n_chunks,
+                          dr.tiles, dr.order, dr.tile_slice, dr.sell_off, dr.sell_w, dr.sell_col, dr.n_tiles};
                 launch_restrict(s, kd, dd, dd_desc, lr.count, cov, (uint32_t *)w->heavy.p, lr.bytes, lr.bytes2);
             }
         } else {

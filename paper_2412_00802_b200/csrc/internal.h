@@ -228,6 +228,9 @@ struct DirDev {                   // passed by value
     const uint32_t *heavy_nchunks;
     const uint4 *chunks;
     uint32_t n_heavy, n_chunks;
+    const uint4 *tiles;             // per-tile row order (medium, light) and SELL-16 light slices
+    const uint32_t *order, *tile_slice, *sell_off, *sell_w, *sell_col;
+    uint32_t n_tiles;
 };
 struct KbDev {
     uint32_t N, W, W4;

@@ -2,10 +2,11 @@
 //
 //  k_bool           n-ary AND/OR with per-operand complement (Alg. 2),
 //                   128-bit words, tail mask, fused coverage (Alg. 15).
-//  k_restrict       exists / forall / >=n / <=n / =n over a role direction's CSR
+//  k_restrict_tile  exists / forall / >=n / <=n / =n over a role direction's CSR
 //                   (Algs. 4, 6, 8; inverse = transposed CSR):
-//                   light + medium degree bins, ballot-assembled output words,
-//                   saturating counts with early exit, fused coverage.
+//                   1,024-row tiles in degree order, light rows from SELL-16 slices,
+//                   warp-cooperative medium rows, saturating counts with early exit,
+//                   bits assembled in shared memory, fused coverage.
 //  k_restrict_heavy heavy rows (deg > kHeavyDeg) split over CTAs; the last CTA
 //                   of a row finalises its bit with atomicOr (no other atomics on rows).
 //  k_drange         exists d.[lo,hi] over sorted per-individual values (Alg. 10, Q9).
@@ -112,60 +113,63 @@ __global__ void __launch_bounds__(256) k_bool(KbDev kb, const BoolDesc *__restri
 }
 
 // ------------------------------------------------------------------------------
-// warp per output word (32 individuals); 8 warps per CTA; blockIdx.y = node.
-__global__ void __launch_bounds__(256) k_restrict(KbDev kb, DirDev dir, const RestrictDesc *__restrict__ descs,
-                                                  hedl_counts *counts) {
+// per-node restriction over 1,024-row tiles (blockIdx.x = tile, blockIdx.y = node):
+// rows in the tile's degree-descending order (no divergence between a warp's rows),
+// medium rows warp-cooperative, light rows from the SELL-16 slices (coalesced
+// neighbour indices, a lane pair per row taking alternate neighbours), results as
+// bits in shared memory, one store per output word.  Heavy rows: k_restrict_heavy.
+__global__ void __launch_bounds__(256) k_restrict_tile(KbDev kb, DirDev dir, const RestrictDesc *__restrict__ descs,
+                                                       hedl_counts *counts) {
     const RestrictDesc d = descs[blockIdx.y];
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t w = blockIdx.x * 8 + (threadIdx.x >> 5);
-    uint32_t tp = 0, fp = 0;
-    if (w < kb.W4) {
-        uint32_t word = 0;
-        if (w < kb.W) {
-            const uint32_t x = (w << 5) + lane;
-            const bool valid = x < kb.N;
-            uint32_t a = 0, b = 0;
-            if (valid) { a = __ldg(dir.row_ptr + x); b = __ldg(dir.row_ptr + x + 1); }
-            const uint32_t deg = b - a;
-            const uint32_t sat = d.sat;
-            uint32_t cnt = 0;
-            if (deg <= kLightDeg) {
-                // light: the lane scans its own neighbours, 4 probes in flight, early exit
-                for (uint32_t e = a; e < b && cnt < sat; e += 4) {
-                    uint32_t y0 = __ldg(dir.col + e);
-                    uint32_t y1 = e + 1 < b ? __ldg(dir.col + e + 1) : 0xffffffffu;
-                    uint32_t y2 = e + 2 < b ? __ldg(dir.col + e + 2) : 0xffffffffu;
-                    uint32_t y3 = e + 3 < b ? __ldg(dir.col + e + 3) : 0xffffffffu;
-                    uint32_t c = probe(d.child, y0, d.cmask);
-                    if (y1 != 0xffffffffu) c += probe(d.child, y1, d.cmask);
-                    if (y2 != 0xffffffffu) c += probe(d.child, y2, d.cmask);
-                    if (y3 != 0xffffffffu) c += probe(d.child, y3, d.cmask);
-                    cnt += c;
-                }
-            }
-            // medium: the whole warp scans one individual's neighbours, 128 per step
-            unsigned med = __ballot_sync(FULL, valid && deg > kLightDeg && deg <= kHeavyDeg);
-            while (med) {
-                const int l = __ffs(med) - 1;
-                med &= med - 1;
-                const uint32_t ma = __shfl_sync(FULL, a, l), mb = __shfl_sync(FULL, b, l);
-                uint32_t c = 0;
-                for (uint32_t e = ma; e < mb && c < sat; e += 128) {
-                    uint32_t bit[4];
+    __shared__ uint32_t sbits[32];
+    const uint32_t t = blockIdx.x, x0 = t * 1024;
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x < 32) sbits[threadIdx.x] = 0;
+    __syncthreads();
+    const uint4 ti = dir.tiles[t];
+    const uint32_t sat = d.sat;
+    for (uint32_t m = wid; m < ti.y; m += 8) {            // medium rows: warp per row
+        const uint32_t x = __ldg(dir.order + ti.x + m);
+        const uint32_t a = __ldg(dir.row_ptr + x), b = __ldg(dir.row_ptr + x + 1);
+        uint32_t c = 0;
+        for (uint32_t e = a; e < b && c < sat; e += 128) {
+            uint32_t bit[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const uint32_t k = e + u * 32 + lane;
-                        bit[u] = k < mb ? probe(d.child, __ldg(dir.col + k), d.cmask) : 0u;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) c += __popc(__ballot_sync(FULL, bit[u]));
-                }
-                if (lane == (uint32_t)l) cnt = c;
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t k = e + u * 32 + lane;
+                bit[u] = k < b ? probe(d.child, __ldg(dir.col + k), d.cmask) : 0u;
             }
-            const bool res = valid && deg <= kHeavyDeg && pred_eval(d.pred, min(cnt, sat), d.n);
-            word = __ballot_sync(FULL, res);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) c += __popc(__ballot_sync(FULL, bit[u]));
         }
-        if (lane == 0) {
+        if (lane == 0 && pred_eval(d.pred, min(c, sat), d.n))
+            atomicOr(&sbits[(x - x0) >> 5], 1u << ((x - x0) & 31));
+    }
+    const uint32_t sbeg = __ldg(dir.tile_slice + t), send = __ldg(dir.tile_slice + t + 1);
+    for (uint32_t sl = sbeg + wid; sl < send; sl += 8) {  // light rows: SELL-16 slices
+        const uint32_t li = (sl - sbeg) * 16 + (lane >> 1);
+        const bool rv = li < ti.z;
+        const uint32_t x = rv ? __ldg(dir.order + ti.x + ti.y + li) : 0u;
+        const uint32_t *cp = dir.sell_col + __ldg(dir.sell_off + sl) + (lane >> 1);
+        const uint32_t w = __ldg(dir.sell_w + sl);
+        uint32_t c = 0;
+        for (uint32_t k = lane & 1u; k < w && c < sat; k += 8) {
+            uint32_t y[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) y[u] = k + 2 * u < w ? __ldg(cp + (k + 2 * u) * 16) : 0xffffffffu;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) if (y[u] != 0xffffffffu) c += probe(d.child, y[u], d.cmask);
+        }
+        c += __shfl_xor_sync(FULL, c, 1);
+        if (rv && !(lane & 1u) && pred_eval(d.pred, min(c, sat), d.n))
+            atomicOr(&sbits[(x - x0) >> 5], 1u << ((x - x0) & 31));
+    }
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t w = t * 32 + lane;
+        uint32_t tp = 0, fp = 0;
+        if (w < kb.W4) {
+            const uint32_t word = sbits[lane];            // rows >= N were never set
             if (d.out) d.out[w] = word;
             if (d.proj && w < kb.W) proj_scatter(kb, d.proj, w, word);
             if (d.cover >= 0) {
@@ -173,8 +177,22 @@ __global__ void __launch_bounds__(256) k_restrict(KbDev kb, DirDev dir, const Re
                 fp = __popc(word & __ldg(kb.neg + w));
             }
         }
+        if (d.cover >= 0) {
+            tp = __reduce_add_sync(FULL, tp);
+            fp = __reduce_add_sync(FULL, fp);
+            if (lane == 0) {
+                hedl_counts *cc = counts + d.cover;
+                if (tp) {
+                    atomicAdd((unsigned long long *)&cc->tp, (unsigned long long)tp);
+                    atomicAdd((unsigned long long *)&cc->fn, 0ull - tp);
+                }
+                if (fp) {
+                    atomicAdd((unsigned long long *)&cc->fp, (unsigned long long)fp);
+                    atomicAdd((unsigned long long *)&cc->tn, 0ull - fp);
+                }
+            }
+        }
     }
-    if (d.cover >= 0) block_cover(counts, d.cover, tp, fp);
 }
 
 // ------------------------------------------------------------------------------
@@ -313,12 +331,12 @@ void launch_bool(cudaStream_t s, const KbDev &kb, const BoolDesc *d_desc, uint32
 void launch_restrict(cudaStream_t s, const KbDev &kb, const DirDev &dir, const RestrictDesc *d_desc,
                      uint32_t n_desc, hedl_counts *counts, uint32_t *heavy_scratch, double alg_light,
                      double alg_heavy) {
-    const uint32_t gx = cdiv(kb.W4, 8);
-    if (!gx) return;
+    const uint32_t gx = dir.n_tiles;
+    if (!gx || !kb.W4) return;
     for (uint32_t off = 0; off < n_desc; off += 65535) {
         const uint32_t nd = n_desc - off < 65535 ? n_desc - off : 65535;
         prof_begin(s, KC_RESTRICT);
-        k_restrict<<<dim3(gx, nd), 256, 0, s>>>(kb, dir, d_desc + off, counts);
+        k_restrict_tile<<<dim3(gx, nd), 256, 0, s>>>(kb, dir, d_desc + off, counts);
         count_launch();
         prof_end(s, KC_RESTRICT, alg_light * nd / n_desc, nd);
         if (dir.n_chunks) {
