@@ -12,6 +12,8 @@ UNA (§III-A):
   forall rho.C -> {x | every y in Delta: (x,y) in rho implies y in C}
   >=n/<=n/=n rho.C -> {x | #{y in Delta: (x,y) in rho, y in C} >= / <= / == n}
   exists d.[lo,hi] -> {x | some asserted (x,v): lo <= v <= hi} in float32
+  EQUAL s v   -> {x | some asserted (x,w) of s: w == v}      (Alg. 11)
+  CONTAIN s v -> {x | some asserted (x,w) of s: v substring of w}  (Alg. 13; empty v rejected)
   r^- = {(y,x) | (x,y) in r}.
 """
 from __future__ import annotations
@@ -19,7 +21,7 @@ from __future__ import annotations
 import numpy as np
 
 _OPS = ["TOP", "BOTTOM", "ATOM", "NOT", "AND", "OR", "EXISTS", "FORALL", "MIN", "MAX",
-        "EXACT", "DRANGE"]
+        "EXACT", "DRANGE", "SEQUAL", "SCONTAIN"]
 
 
 def _members(words, n):
@@ -43,6 +45,11 @@ class BruteKB:
         ds, dv = kb["data_subj"], np.asarray(kb["data_val"], dtype=np.float32)
         self.data = [list(zip(ds[doff[d]:doff[d + 1]].tolist(), dv[doff[d]:doff[d + 1]]))
                      for d in range(len(doff) - 1)]
+        from synth.format import string_fields
+        so, ss, sv, sb = string_fields(kb)
+        blob = bytes(sb)
+        self.strings = [[(int(ss[k]), blob[int(sv[k]):int(sv[k + 1])]) for k in range(int(so[r]), int(so[r + 1]))]
+                        for r in range(len(so) - 1)]
         self.pos = set(int(i) for i in kb["pos_ids"])
         self.neg = set(int(i) for i in kb["neg_ids"])
 
@@ -50,12 +57,12 @@ class BruteKB:
         rel = self.roles[r]
         return {(y, x) for (x, y) in rel} if inv else rel
 
-    def eval(self, nodes, kids, i, compat_paper_max=False):
+    def eval(self, nodes, kids, i, compat_paper_max=False, patterns=()):
         nd = nodes[i]
         op = _OPS[int(nd["op"])]
         ch = [int(k) for k in kids[int(nd["child_begin"]):int(nd["child_begin"]) + int(nd["child_count"])]]
         D = self.delta
-        ev = lambda j: self.eval(nodes, kids, j, compat_paper_max)
+        ev = lambda j: self.eval(nodes, kids, j, compat_paper_max, patterns)
         if op == "TOP":
             return set(D)
         if op == "BOTTOM":
@@ -74,6 +81,12 @@ class BruteKB:
             for j in ch:
                 out |= ev(j)
             return out
+        if op in ("SEQUAL", "SCONTAIN"):
+            pat = patterns[int(nd["n"])]
+            if op == "SCONTAIN" and not pat:
+                raise ValueError("empty CONTAIN pattern")
+            hit = (lambda w: w == pat) if op == "SEQUAL" else (lambda w: pat in w)
+            return {x for x in D if any(s == x and hit(w) for (s, w) in self.strings[int(nd["arg"])])}
         if op == "DRANGE":
             lo, hi = np.float32(nd["lo"]), np.float32(nd["hi"])
             return {x for x in D if any(s == x and lo <= v <= hi for (s, v) in self.data[int(nd["arg"])])}
@@ -98,12 +111,14 @@ class BruteKB:
         return tp, fp, len(self.pos) - tp, len(self.neg) - fp
 
 
-def evaluate(kb: dict, nodes, child_idx, roots, compat_paper_max=False):
+def evaluate(kb: dict, nodes, child_idx, roots, compat_paper_max=False, patterns=None):
     """-> list of (instance set, (tp, fp, fn, tn)) per root."""
+    if patterns is None:
+        patterns = list(getattr(nodes, "patterns", []) or [])
     b = BruteKB(kb)
     out = []
     for r in roots:
-        h = b.eval(nodes, child_idx, int(r), compat_paper_max)
+        h = b.eval(nodes, child_idx, int(r), compat_paper_max, patterns)
         out.append((h, b.coverage(h)))
     return out
 

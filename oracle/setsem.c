@@ -33,7 +33,7 @@
 
 /* node opcodes of the input format (synth/format.py) */
 enum { O_TOP, O_BOTTOM, O_ATOM, O_NOT, O_AND, O_OR, O_EXISTS, O_FORALL,
-       O_MIN, O_MAX, O_EXACT, O_DRANGE };
+       O_MIN, O_MAX, O_EXACT, O_DRANGE, O_SEQUAL, O_SCONTAIN };
 #define F_INV 1u
 #define CF_COMPAT_PAPER_MAX 4u
 
@@ -57,6 +57,11 @@ typedef struct {
     uint64_t *ndata;
     uint8_t *pos, *neg;                /* ExMat (Alg. 15 input) */
     uint64_t npos, nneg;
+    uint32_t S;                        /* string concrete roles (Algs. 11-14) */
+    const uint64_t *str_off;           /* borrowed: role s = assertions [str_off[s], str_off[s+1]) */
+    const uint32_t *str_subj;
+    const uint64_t *str_val_off;       /* assertion k's value = str_bytes[str_val_off[k] .. k+1) */
+    const uint8_t *str_bytes;
 } okb;
 
 static int cmp_u64(const void *a, const void *b) {
@@ -70,7 +75,8 @@ int oracle_kb_new(uint32_t N, uint32_t C, const uint32_t *concept_bits,
                   uint32_t R, const uint64_t *role_off, const uint32_t *esubj, const uint32_t *eobj,
                   uint32_t D, const uint64_t *data_off, const uint32_t *dsubj, const float *dval,
                   uint32_t npos, const uint32_t *pos, uint32_t nneg, const uint32_t *neg,
-                  okb **out) {
+                  uint32_t S, const uint64_t *str_off, const uint32_t *str_subj, const uint64_t *str_val_off,
+                  const uint8_t *str_bytes, okb **out) {
     okb *kb = (okb *)calloc(1, sizeof(okb));
     if (!kb) return R_OOM;
     kb->N = N; kb->W = (N + 31) / 32; kb->C = C; kb->R = R; kb->D = D;
@@ -118,6 +124,11 @@ int oracle_kb_new(uint32_t N, uint32_t C, const uint32_t *concept_bits,
         kb->neg[neg[i]] = 1;
     }
     for (uint32_t i = 0; i < N; i++) { kb->npos += kb->pos[i]; kb->nneg += kb->neg[i]; }
+    kb->S = S; kb->str_off = str_off; kb->str_subj = str_subj;
+    kb->str_val_off = str_val_off; kb->str_bytes = str_bytes;
+    for (uint32_t r = 0; r < S && rc == R_OK; r++)
+        for (uint64_t k = str_off[r]; k < str_off[r + 1]; k++)
+            if (str_subj[k] >= N) { rc = R_RANGE; break; }
     if (rc != R_OK) { oracle_kb_free(kb); return rc; }
     *out = kb;
     return R_OK;
@@ -138,7 +149,18 @@ typedef struct {
     const uint32_t *kids;
     uint64_t n_kids;
     uint32_t flags;
+    uint32_t n_pat;                    /* string patterns of SEQUAL / SCONTAIN (node.n) */
+    const uint64_t *pat_off;
+    const uint8_t *pat_bytes;
 } octx;
+
+/* does the byte string h[0..hn) contain p[0..pn) as a contiguous substring? */
+static int contains(const uint8_t *h, uint64_t hn, const uint8_t *p, uint64_t pn) {
+    if (pn > hn) return 0;
+    for (uint64_t i = 0; i + pn <= hn; i++)
+        if (memcmp(h + i, p, pn) == 0) return 1;
+    return 0;
+}
 
 /* eval(node) -> fresh row of N bytes in {0,1}; NULL on error (*rc set). */
 static uint8_t *eval(const octx *x, uint32_t id, int depth, int *rc) {
@@ -248,6 +270,25 @@ static uint8_t *eval(const octx *x, uint32_t id, int depth, int *rc) {
             if (nd->lo <= v[k] && v[k] <= nd->hi) res[s[k]] = 1;
         return res;
     }
+    case O_SEQUAL:
+    case O_SCONTAIN: {
+        /* EQUAL: some assertion's value equals the pattern (Alg. 11);
+           CONTAIN: some value contains the pattern as a substring (Alg. 13, PAPER.md:459-488,
+           SPEC.md:229 byte-wise, case-sensitive); an empty CONTAIN pattern is rejected (Q20) */
+        if (nd->child_count || (nd->flags & F_INV)) goto bad;
+        if (nd->arg >= kb->S || nd->n >= x->n_pat) { *rc = R_RANGE; free(res); return NULL; }
+        const uint8_t *pat = x->pat_bytes + x->pat_off[nd->n];
+        const uint64_t pn = x->pat_off[nd->n + 1] - x->pat_off[nd->n];
+        if (nd->op == O_SCONTAIN && pn == 0) goto bad;
+        memset(res, 0, N);
+        for (uint64_t k = kb->str_off[nd->arg]; k < kb->str_off[nd->arg + 1]; k++) {
+            const uint8_t *v = kb->str_bytes + kb->str_val_off[k];
+            const uint64_t vn = kb->str_val_off[k + 1] - kb->str_val_off[k];
+            const int hit = nd->op == O_SEQUAL ? (vn == pn && memcmp(v, pat, pn) == 0) : contains(v, vn, pat, pn);
+            if (hit) res[kb->str_subj[k]] = 1;
+        }
+        return res;
+    }
     default:
         goto bad;
     }
@@ -296,8 +337,9 @@ static void *run_job(void *arg) {
 int oracle_eval(const okb *kb, const onode *nodes, uint32_t n_nodes,
                 const uint32_t *kids, uint64_t n_kids,
                 const uint32_t *roots, uint32_t n_roots, uint32_t flags,
+                uint32_t n_pat, const uint64_t *pat_off, const uint8_t *pat_bytes,
                 uint32_t *out_bits, uint64_t *out_counts, int n_threads, uint32_t *bad_root) {
-    octx x = {kb, nodes, n_nodes, kids, n_kids, flags};
+    octx x = {kb, nodes, n_nodes, kids, n_kids, flags, n_pat, pat_off, pat_bytes};
     if (n_threads < 1) n_threads = 1;
     if ((uint32_t)n_threads > n_roots) n_threads = n_roots ? (int)n_roots : 1;
     ojob *jobs = (ojob *)calloc((size_t)n_threads, sizeof(ojob));

@@ -43,11 +43,11 @@ def _load():
         P = C.c_void_p
         lib.oracle_kb_new.argtypes = [C.c_uint32, C.c_uint32, P, C.c_uint32, P, P, P,
                                       C.c_uint32, P, P, P, C.c_uint32, P, C.c_uint32, P,
-                                      C.POINTER(C.c_void_p)]
+                                      C.c_uint32, P, P, P, P, C.POINTER(C.c_void_p)]
         lib.oracle_kb_new.restype = C.c_int
         lib.oracle_kb_free.argtypes = [P]
         lib.oracle_eval.argtypes = [P, P, C.c_uint32, P, C.c_uint64, P, C.c_uint32, C.c_uint32,
-                                    P, P, C.c_int, C.POINTER(C.c_uint32)]
+                                    C.c_uint32, P, P, P, P, C.c_int, C.POINTER(C.c_uint32)]
         lib.oracle_eval.restype = C.c_int
         _lib = lib
     return _lib
@@ -73,13 +73,17 @@ class OracleKB:
         ro, es, eo = arr("role_edge_off", np.uint64), arr("edge_subj", np.uint32), arr("edge_obj", np.uint32)
         do, ds, dv = arr("data_off", np.uint64), arr("data_subj", np.uint32), arr("data_val", np.float32)
         pos, neg = arr("pos_ids", np.uint32), arr("neg_ids", np.uint32)
+        from synth.format import string_fields
+        so, ss, sv, sb = string_fields(kb)
+        self._keep += [so, ss, sv, sb]
         self.N = int(kb["N"])
         self.W = (self.N + 31) // 32
         h = C.c_void_p()
         rc = lib.oracle_kb_new(self.N, cb.shape[0] if cb.ndim == 2 else 0, _p(cb),
                                len(ro) - 1, _p(ro), _p(es), _p(eo),
                                len(do) - 1, _p(do), _p(ds), _p(dv),
-                               len(pos), _p(pos), len(neg), _p(neg), C.byref(h))
+                               len(pos), _p(pos), len(neg), _p(neg),
+                               len(so) - 1, _p(so), _p(ss), _p(sv), _p(sb), C.byref(h))
         if rc:
             raise OracleError(rc)
         self._h = h
@@ -90,9 +94,14 @@ class OracleKB:
             self._h = None
 
     def evaluate(self, nodes, child_idx, roots, flags: int = 0, want_bits: bool = True,
-                 threads: int = 1):
-        """-> (bits [n_roots][W] u32 or None, counts [n_roots][4] u64 = tp, fp, fn, tn)."""
+                 threads: int = 1, patterns=None):
+        """-> (bits [n_roots][W] u32 or None, counts [n_roots][4] u64 = tp, fp, fn, tn).
+        `patterns`: string-restriction patterns (list of bytes; defaults to the table `nodes` carries)."""
         lib = _load()
+        from synth.format import node_patterns, pack_strings
+        if patterns is None:
+            patterns = node_patterns(nodes)
+        po, pb = pack_strings(patterns)
         nodes = np.ascontiguousarray(nodes)
         kids = np.ascontiguousarray(child_idx, dtype=np.uint32)
         roots = np.ascontiguousarray(roots, dtype=np.uint32)
@@ -101,12 +110,13 @@ class OracleKB:
         counts = np.zeros((n, 4), dtype=np.uint64)
         bad = C.c_uint32(0)
         rc = lib.oracle_eval(self._h, _p(nodes), len(nodes), _p(kids), len(kids), _p(roots), n,
-                             flags, _p(bits) if want_bits else None, _p(counts), threads,
-                             C.byref(bad))
+                             flags, len(po) - 1, _p(po), _p(pb), _p(bits) if want_bits else None, _p(counts),
+                             threads, C.byref(bad))
         if rc:
             raise OracleError(rc, bad.value)
         return bits, counts
 
 
-def evaluate(kb: dict, nodes, child_idx, roots, flags: int = 0, want_bits: bool = True, threads: int = 1):
-    return OracleKB(kb).evaluate(nodes, child_idx, roots, flags, want_bits, threads)
+def evaluate(kb: dict, nodes, child_idx, roots, flags: int = 0, want_bits: bool = True, threads: int = 1,
+             patterns=None):
+    return OracleKB(kb).evaluate(nodes, child_idx, roots, flags, want_bits, threads, patterns)

@@ -19,9 +19,9 @@ from typing import Dict, List, Sequence, Tuple
 import numpy as np
 
 # ---- opcodes (== hedl.h HEDL_OP_*) -----------------------------------------
-TOP, BOTTOM, ATOM, NOT, AND, OR, EXISTS, FORALL, MIN, MAX, EXACT, DRANGE = range(12)
+TOP, BOTTOM, ATOM, NOT, AND, OR, EXISTS, FORALL, MIN, MAX, EXACT, DRANGE, SEQUAL, SCONTAIN = range(14)
 OP_NAMES = ["TOP", "BOTTOM", "ATOM", "NOT", "AND", "OR", "EXISTS", "FORALL",
-            "MIN", "MAX", "EXACT", "DRANGE"]
+            "MIN", "MAX", "EXACT", "DRANGE", "SEQUAL", "SCONTAIN"]
 ROLE_OPS = (EXISTS, FORALL, MIN, MAX, EXACT)
 COUNT_OPS = (MIN, MAX, EXACT)
 
@@ -42,6 +42,14 @@ NODE_DTYPE = np.dtype([
 assert NODE_DTYPE.itemsize == 28
 
 
+def string_fields(kb: dict):
+    """The string concrete-role arrays of a KB dict (empty when the KB has none)."""
+    if "str_off" in kb:
+        return (np.asarray(kb["str_off"], np.uint64), np.asarray(kb["str_subj"], np.uint32),
+                np.asarray(kb["str_val_off"], np.uint64), np.asarray(kb["str_bytes"], np.uint8))
+    return (np.zeros(1, np.uint64), np.zeros(0, np.uint32), np.zeros(1, np.uint64), np.zeros(0, np.uint8))
+
+
 def words(n_individuals: int) -> int:
     """W = ceil(N/32): u32 words of one LSB-first bitset row."""
     return (n_individuals + 31) // 32
@@ -54,6 +62,27 @@ def words(n_individuals: int) -> int:
 #   ("MIN", n, r, inv, t) ("MAX", n, r, inv, t) ("EXACT", n, r, inv, t)
 #   ("DRANGE", d, lo, hi)
 
+class NodeArray(np.ndarray):
+    """A NODE_DTYPE array that carries its string-pattern table (`.patterns`, list of bytes,
+    indexed by node.n of SEQUAL / SCONTAIN nodes) through unpacking and slicing."""
+
+    def __array_finalize__(self, obj):
+        self.patterns = getattr(obj, "patterns", [])
+
+
+def node_patterns(nodes) -> list:
+    return list(getattr(nodes, "patterns", []) or [])
+
+
+class Flat(tuple):
+    """(nodes, child_idx, roots); `.patterns` = string-restriction patterns (list of bytes)
+    referenced by SEQUAL / SCONTAIN nodes through node.n (the hedl_patterns table)."""
+
+    @property
+    def patterns(self):
+        return node_patterns(self[0])
+
+
 def flatten(trees: Sequence[tuple], share: bool = False):
     """Post-order flatten trees into (nodes, child_idx, roots) arrays.
 
@@ -64,6 +93,7 @@ def flatten(trees: Sequence[tuple], share: bool = False):
     recs: List[tuple] = []
     kids: List[int] = []
     memo: Dict[tuple, int] = {}
+    patterns: List[bytes] = []
 
     def emit(t) -> int:
         if share:
@@ -87,6 +117,11 @@ def flatten(trees: Sequence[tuple], share: bool = False):
             n, arg, flags, ch = t[1], t[2], (FLAG_INV if t[3] else 0), [emit(t[4])]
         elif tag == "DRANGE":
             arg, lo, hi = t[1], t[2], t[3]
+        elif tag in ("SEQUAL", "SCONTAIN"):            # (tag, string role, pattern)
+            arg = t[1]
+            pat = t[2].encode() if isinstance(t[2], str) else bytes(t[2])
+            n = len(patterns)
+            patterns.append(pat)
         else:
             raise ValueError(tag)
         begin = len(kids)
@@ -98,8 +133,18 @@ def flatten(trees: Sequence[tuple], share: bool = False):
         return idx
 
     roots = [emit(t) for t in trees]
-    nodes = np.array(recs, dtype=NODE_DTYPE) if recs else np.zeros(0, NODE_DTYPE)
-    return nodes, np.array(kids, dtype=np.uint32), np.array(roots, dtype=np.uint32)
+    nodes = (np.array(recs, dtype=NODE_DTYPE) if recs else np.zeros(0, NODE_DTYPE)).view(NodeArray)
+    nodes.patterns = patterns
+    return Flat((nodes, np.array(kids, dtype=np.uint32), np.array(roots, dtype=np.uint32)))
+
+
+def pack_strings(strs: Sequence[bytes]):
+    """Byte strings -> (offsets u64[n+1], blob u8[]) (the hedl_patterns / string-value layout)."""
+    off = np.zeros(len(strs) + 1, dtype=np.uint64)
+    for i, b in enumerate(strs):
+        off[i + 1] = off[i] + len(b)
+    blob = np.frombuffer(b"".join(strs), dtype=np.uint8).copy() if strs else np.zeros(0, np.uint8)
+    return off, blob
 
 
 def _freeze(t):
@@ -113,7 +158,7 @@ def _freeze(t):
 def tree_depth(t) -> int:
     """Depth per SURVEY Q16: literals (A, not A, TOP, BOTTOM, DRANGE) are 1."""
     tag = t[0]
-    if tag in ("TOP", "BOTTOM", "ATOM", "DRANGE"):
+    if tag in ("TOP", "BOTTOM", "ATOM", "DRANGE", "SEQUAL", "SCONTAIN"):
         return 1
     if tag == "NOT":
         return 1 if t[1][0] == "ATOM" else 1 + tree_depth(t[1])
@@ -150,7 +195,16 @@ def tree_to_text(t, names=None) -> str:
     if tag == "DRANGE":
         d = dn[t[1]] if dn else f"d{t[1]}"
         return f"(DRANGE {d} {_fmt(t[2])} {_fmt(t[3])})"
+    if tag in ("SEQUAL", "SCONTAIN"):
+        sn = (names or {}).get("strings")
+        sr = sn[t[1]] if sn else f"s{t[1]}"
+        pat = t[2] if isinstance(t[2], str) else bytes(t[2]).decode("utf-8", "backslashreplace")
+        return f'(SSOME {sr} {"EQUAL" if tag == "SEQUAL" else "CONTAIN"} "{_esc(pat)}")'
     raise ValueError(tag)
+
+
+def _esc(s: str) -> str:
+    return s.replace("\\", "\\\\").replace('"', '\\"')
 
 
 def _fmt(x: float) -> str:
@@ -160,7 +214,7 @@ def _fmt(x: float) -> str:
 
 
 # ---- s-expression reader (SPEC.md:347-355 grammar, extended per SURVEY 8(b)) --
-_TOK = re.compile(r"\(|\)|[^\s()]+")
+_TOK = re.compile(r'"(?:[^"\\]|\\.)*"|\(|\)|[^\s()]+')
 
 
 def parse(text: str, names) -> tuple:
@@ -175,6 +229,7 @@ def parse(text: str, names) -> tuple:
     cidx = {s: i for i, s in enumerate(names.get("concepts", []))}
     ridx = {s: i for i, s in enumerate(names.get("roles", []))}
     didx = {s: i for i, s in enumerate(names.get("data", []))}
+    sidx = {s: i for i, s in enumerate(names.get("strings", []))}
 
     def nxt():
         if pos[0] >= len(toks):
@@ -237,6 +292,18 @@ def parse(text: str, names) -> tuple:
             if d not in didx:
                 raise KeyError(f"unknown data property {d!r}")
             e = ("DRANGE", didx[d], num(nxt()), num(nxt()))
+        elif kw == "SSOME":                       # SPEC.md:353 string restrictions
+            sr = nxt()
+            if sr not in sidx:
+                raise KeyError(f"unknown string role {sr!r}")
+            mode = nxt()
+            lit = nxt()
+            if not (lit.startswith('"') and lit.endswith('"')):
+                raise SyntaxError("string literal expected")
+            val = re.sub(r"\\(.)", r"\1", lit[1:-1])
+            if mode not in ("EQUAL", "CONTAIN"):
+                raise SyntaxError(f"unknown string restriction {mode!r}")
+            e = ("SEQUAL" if mode == "EQUAL" else "SCONTAIN", sidx[sr], val)
         else:
             raise SyntaxError(f"unknown constructor {kw!r}")
         expect(")")
@@ -253,7 +320,8 @@ def parse(text: str, names) -> tuple:
 def kb_from_sets(n: int, concepts: Sequence[Sequence[int]],
                  roles: Sequence[Sequence[Tuple[int, int]]],
                  data: Sequence[Sequence[Tuple[int, float]]],
-                 pos: Sequence[int], neg: Sequence[int]) -> dict:
+                 pos: Sequence[int], neg: Sequence[int],
+                 strings: Sequence[Sequence[Tuple[int, bytes]]] = ()) -> dict:
     """Assemble a KB dict (the hedl_kb_desc arrays) from explicit member lists.
 
     Packing a member list into LSB-first words is the input format itself
@@ -278,7 +346,18 @@ def kb_from_sets(n: int, concepts: Sequence[Sequence[int]],
             dsubj.append(s)
             dval.append(v)
         doff.append(len(dsubj))
+    soff, ssubj, svals = [0], [], []
+    for pairs in strings:
+        for s_, v in pairs:
+            ssubj.append(s_)
+            svals.append(v.encode() if isinstance(v, str) else bytes(v))
+        soff.append(len(ssubj))
+    vo, blob = pack_strings(svals)
     return {
+        "str_off": np.array(soff, dtype=np.uint64),
+        "str_subj": np.array(ssubj, dtype=np.uint32),
+        "str_val_off": vo,
+        "str_bytes": blob,
         "N": n,
         "concept_bits": cb,
         "role_edge_off": np.array(off, dtype=np.uint64),

@@ -19,15 +19,23 @@ INF = float("inf")
 # random trees (cover every constructor)
 
 
+STR_PATTERNS = ["Smith", "Alice Smith", "Bob", "b", "carbon", "c", "CARBON", "bond", "missing", "Ab", "a",
+                "\u00e9", '"', "tab\t", "Smithers", "xyz"]
+
+
 def random_tree(rng, shape: dict, depth: int = 4, n_max: int = 4, allow_drange=True):
     C, R, D = shape["C"], shape["R"], shape["D"]
+    S = shape.get("S", 0)
     leaf_kinds = ["TOP", "BOTTOM"] + (["ATOM"] * 4 if C else []) + \
-        (["DRANGE"] * 2 if (D and allow_drange) else [])
+        (["DRANGE"] * 2 if (D and allow_drange) else []) + (["STR"] * 2 if S else [])
     inner = ["NOT", "AND", "OR"] + (["EXISTS", "FORALL", "MIN", "MAX", "EXACT"] * 2 if R else [])
     if depth <= 1 or rng.random() < 0.25:
         k = leaf_kinds[int(rng.integers(len(leaf_kinds)))]
         if k == "ATOM":
             return ("ATOM", int(rng.integers(C)))
+        if k == "STR":
+            pat = STR_PATTERNS[int(rng.integers(len(STR_PATTERNS)))]
+            return ("SEQUAL" if rng.random() < 0.5 else "SCONTAIN", int(rng.integers(S)), pat)
         if k == "DRANGE":
             pool = [-INF, -2.0, -1.5, -0.0, 0.0, 0.5, 1.0, 2.25, 3.0, INF]
             lo = pool[int(rng.integers(len(pool)))]
@@ -317,12 +325,17 @@ def _gen_chunk(args):
 
 def concat_arrays(parts):
     """Concatenate several (nodes, child_idx, roots) triples into one."""
-    from .format import NODE_DTYPE
-    nodes_l, kids_l, roots_l = [], [], []
+    from .format import NODE_DTYPE, OP_NAMES, NodeArray, node_patterns
+    nodes_l, kids_l, roots_l, pats = [], [], [], []
     n_off = k_off = 0
+    s_ops = np.array([OP_NAMES.index("SEQUAL"), OP_NAMES.index("SCONTAIN")], dtype=np.uint8)
     for nodes, kids, roots in parts:
-        nd = nodes.copy()
+        nd = np.asarray(nodes).copy()
         nd["child_begin"] += np.uint32(k_off)
+        p = node_patterns(nodes)
+        if p:
+            nd["n"][np.isin(nd["op"], s_ops)] += np.uint32(len(pats))
+            pats += p
         nodes_l.append(nd)
         kids_l.append(kids + np.uint32(n_off))
         roots_l.append(roots + np.uint32(n_off))
@@ -330,7 +343,9 @@ def concat_arrays(parts):
         k_off += len(kids)
     if not parts:
         return np.zeros(0, NODE_DTYPE), np.zeros(0, np.uint32), np.zeros(0, np.uint32)
-    return np.concatenate(nodes_l), np.concatenate(kids_l), np.concatenate(roots_l)
+    nodes = np.concatenate(nodes_l).view(NodeArray)
+    nodes.patterns = pats
+    return nodes, np.concatenate(kids_l), np.concatenate(roots_l)
 
 
 def batch_arrays(kind: str, kb: dict, n: int, seed: int, chunk: int = 25_000,

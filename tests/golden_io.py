@@ -8,6 +8,8 @@ fixtures need):
   #concept-assertions   <concept> <individual>
   #role-assertions      <role> <subject> <object>
   #numeric-assertions   <numeric-role> <subject> <decimal>
+  #string-roles         names
+  #string-assertions    <string-role> <subject> "<literal>"   (\" escapes a quote)
   #examples             + <individual> | - <individual>
   #flags                compat_paper_max
   #hypotheses           <s-expr> => {i1, i2, ...} [tp fp fn tn]
@@ -25,8 +27,8 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 def load(path):
     sec = None
-    ind, con, rol, num = [], [], [], []
-    ca, ra, na, ex, hy = [], [], [], [], []
+    ind, con, rol, num, srl = [], [], [], [], []
+    ca, ra, na, sa, ex, hy = [], [], [], [], [], []
     flags = 0
     for raw in open(path):
         line = raw.strip()
@@ -43,6 +45,12 @@ def load(path):
             rol += line.split()
         elif sec == "numeric-roles":
             num += line.split()
+        elif sec == "string-roles":
+            srl += line.split()
+        elif sec == "string-assertions":
+            m = re.match(r'(\S+)\s+(\S+)\s+"((?:[^"\\]|\\.)*)"$', line)
+            assert m, line
+            sa.append((m.group(1), m.group(2), m.group(3).replace('\\"', '"').replace("\\\\", "\\")))
         elif sec == "concept-assertions":
             ca.append(line.split())
         elif sec == "role-assertions":
@@ -68,8 +76,11 @@ def load(path):
         data[num.index(d)].append((ii[s], float(np.float32(float(v)))))
     pos = [ii[a] for s, a in ex if s == "+"]
     neg = [ii[a] for s, a in ex if s == "-"]
-    kb = kb_from_sets(len(ind), concepts, roles, data, pos, neg)
-    names = {"concepts": con, "roles": rol, "data": num}
+    strings = [[] for _ in srl]
+    for r, s_, v in sa:
+        strings[srl.index(r)].append((ii[s_], v.encode()))
+    kb = kb_from_sets(len(ind), concepts, roles, data, pos, neg, strings)
+    names = {"concepts": con, "roles": rol, "data": num, "strings": srl}
     cases = []
     for line in hy:
         m = re.match(r"(.*)=>\s*\{([^}]*)\}\s*(.*)$", line)

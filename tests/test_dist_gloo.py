@@ -53,12 +53,17 @@ def _worker(rank, world, port, q):
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_counts_match_single_process(world):
     ctx = mp.get_context("spawn")
-    q = ctx.SimpleQueue()
+    q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got, ref, ranges = q.get()
+    try:
+        got, ref, ranges = q.get(timeout=180)
+    except Exception:
+        for p in procs:
+            p.kill()
+        raise
     for p in procs:
         p.join(60)
         assert p.exitcode == 0

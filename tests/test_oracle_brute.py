@@ -14,10 +14,11 @@ def _run(seed, flags):
     shape = abox.kb_shape(kb)
     rng = np.random.default_rng(10_000 + seed)
     trees = [hyps.random_tree(rng, shape, depth=4) for _ in range(8)]
-    nodes, kids, roots = flatten(trees)
-    bits, counts = setsem.evaluate(kb, nodes, kids, roots, flags=flags)
+    flat = flatten(trees)
+    nodes, kids, roots = flat
+    bits, counts = setsem.evaluate(kb, nodes, kids, roots, flags=flags, patterns=flat.patterns)
     res = brute.evaluate(kb, nodes, kids, roots,
-                         compat_paper_max=bool(flags & COMPILE_COMPAT_PAPER_MAX))
+                         compat_paper_max=bool(flags & COMPILE_COMPAT_PAPER_MAX), patterns=flat.patterns)
     for i, (h, c) in enumerate(res):
         assert (bits[i] == brute.to_words(h, kb["N"])).all(), (seed, i, trees[i])
         assert tuple(int(v) for v in counts[i]) == c, (seed, i)
@@ -30,7 +31,7 @@ def test_random_tiny_vs_brute():
         nodes = _run(seed, 0)
         seen |= {(int(o), int(f) & 1) for o, f in zip(nodes["op"], nodes["flags"])}
     # every opcode and both role directions were exercised
-    assert {o for o, _ in seen} == set(range(12))
+    assert {o for o, _ in seen} == set(range(14))
     assert {(o, 1) for o in (6, 7, 8, 9, 10)} <= seen
 
 

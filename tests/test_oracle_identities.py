@@ -51,12 +51,17 @@ def identity_pairs(shape, seed, k=6):
                     (C, ALL(r, not inv, EX(r, inv, C)), "sub"),              # ALCI tautology
                     (EX(r, inv, OR(C, D)), OR(EX(r, inv, C), EX(r, inv, D)), "eq"),
                     (ALL(r, inv, AND(C, D)), AND(ALL(r, inv, C), ALL(r, inv, D)), "eq")]
+        if shape.get("S"):
+            s_, v = int(rng.integers(shape["S"])), hyps.STR_PATTERNS[int(rng.integers(len(hyps.STR_PATTERNS)))]
+            out += [(("SEQUAL", s_, v), ("SCONTAIN", s_, v), "sub"),           # equality is a containment
+                    (("SCONTAIN", s_, v), ("SCONTAIN", s_, v[:1]), "sub"),     # shorter substring
+                    (("SCONTAIN", s_, v + "\x00never"), B, "eq")]              # no asserted value holds NUL
     return out
 
 
 def identity_kbs():
     out = [abox.random_tiny_kb(s) for s in range(40)]
-    out += [abox.random_tiny_kb(s, n=300, n_concepts=3, n_roles=2, n_data=1) for s in range(100, 106)]
+    out += [abox.random_tiny_kb(s, n=300, n_concepts=3, n_roles=2, n_data=1, n_strings=1) for s in range(100, 106)]
     out.append(abox.c1_kb())
     return out
 
