@@ -68,6 +68,16 @@ typedef struct hedl_program hedl_program;
  *                   and are dropped at load.
  *   pos_ids / neg_ids   host u32 lists of positive / negative examples
  *                  (ExMat); duplicates allowed; must be disjoint.
+ *   n_strings, str_off, str_subj, str_val_off, str_bytes   string concrete
+ *                  roles (PAPER.md:63 strConcretRoleMat, §III-B3 Algs. 11-14):
+ *                  role s's assertions are k in [str_off[s], str_off[s+1]), host
+ *                  u64[S+1]; assertion k is (str_subj[k], the byte string
+ *                  str_bytes[str_val_off[k] .. str_val_off[k+1])), str_val_off
+ *                  host u64[str_off[S]+1] ascending.  Values are raw bytes (no
+ *                  terminator, may be empty, compared byte-wise).  Duplicate
+ *                  (subject, value) pairs are removed; distinct values of a role
+ *                  are interned (the paper's stringValuesMapping).
+ *                  n_strings == 0 with null arrays is legal.
  * ------------------------------------------------------------------------- */
 typedef struct hedl_kb_desc {
     uint32_t n_individuals;
@@ -85,6 +95,11 @@ typedef struct hedl_kb_desc {
     const uint32_t *pos_ids;
     uint32_t n_neg;
     const uint32_t *neg_ids;
+    uint32_t n_strings;
+    const uint64_t *str_off;
+    const uint32_t *str_subj;
+    const uint64_t *str_val_off;
+    const uint8_t *str_bytes;
 } hedl_kb_desc;
 
 typedef struct hedl_kb_info {
@@ -93,6 +108,9 @@ typedef struct hedl_kb_info {
     uint64_t device_bytes;          /* bytes of device memory the KB holds */
     uint64_t edges[64];             /* distinct pairs per direction 2r (r) / 2r+1 (r^-), r < 32 */
     uint64_t heavy[64];             /* individuals above the heavy-degree threshold per direction */
+    uint32_t n_strings;
+    uint64_t str_pairs[32];         /* distinct (subject, value) pairs per string role, s < 32 */
+    uint64_t str_values[32];        /* distinct values (interned strings) per string role */
 } hedl_kb_info;
 
 /* Build the device layout on `device` (copying through `stream`; returns after
@@ -122,6 +140,10 @@ hedl_status hedl_kb_get_info(const hedl_kb *kb, hedl_kb_info *out);
 #define HEDL_OP_MAX 9      /* arg = role, n; <=n, 0 included          */
 #define HEDL_OP_EXACT 10   /* arg = role, n; ==n (Alg. 7 EXACTLY)   */
 #define HEDL_OP_DRANGE 11  /* arg = data property; exists v in [lo,hi] (Alg. 10) */
+#define HEDL_OP_SEQUAL 12  /* arg = string role, n = pattern id; exists value == pattern (Alg. 11-12) */
+#define HEDL_OP_SCONTAIN 13 /* arg = string role, n = pattern id; exists value containing the
+                              pattern as a contiguous byte substring (Alg. 13-14); the empty
+                              pattern is rejected (BAD_EXPR, Q20) */
 
 #define HEDL_FLAG_INV 1u   /* node.flags: the role is the inverse r^-  */
 
@@ -130,7 +152,7 @@ typedef struct hedl_node {
     uint8_t flags;
     uint16_t reserved;      /* must be 0 */
     uint32_t arg;
-    uint32_t n;             /* cardinality bound for MIN/MAX/EXACT; n <= 2^32-2 */
+    uint32_t n;             /* cardinality bound for MIN/MAX/EXACT (n <= 2^32-2); pattern id for SEQUAL/SCONTAIN */
     float lo, hi;           /* DRANGE closed float32 bounds; +-inf allowed, NaN rejected */
     uint32_t child_begin, child_count;
 } hedl_node;
@@ -149,6 +171,19 @@ hedl_status hedl_compile(const hedl_kb *kb, const hedl_node *nodes, uint32_t n_n
                          const uint32_t *child_idx, uint64_t n_child_idx,
                          const uint32_t *roots, uint32_t n_roots, uint32_t flags,
                          hedl_program **out);
+/* hedl_compile with a string-pattern table for SEQUAL / SCONTAIN nodes: pattern
+ * p is the bytes pat_bytes[pat_off[p] .. pat_off[p+1]) (host u64[n_patterns+1],
+ * ascending; copied).  SEQUAL resolves its pattern against the role's interned
+ * values at compile time; a pattern no assertion holds compiles to BOTTOM with
+ * no kernel work (the paper's short-circuit).  Errors as
+ * hedl_compile, plus OUT_OF_RANGE (pattern id >= n_patterns, string role >=
+ * n_strings) and BAD_EXPR (empty SCONTAIN pattern, children or INV flag on a
+ * string node).  hedl_compile == hedl_compile_ex with no patterns. */
+hedl_status hedl_compile_ex(const hedl_kb *kb, const hedl_node *nodes, uint32_t n_nodes,
+                            const uint32_t *child_idx, uint64_t n_child_idx,
+                            const uint32_t *roots, uint32_t n_roots, uint32_t flags,
+                            uint32_t n_patterns, const uint64_t *pat_off, const uint8_t *pat_bytes,
+                            hedl_program **out);
 hedl_status hedl_program_free(hedl_program *prog);
 
 typedef struct hedl_program_info {
@@ -158,6 +193,7 @@ typedef struct hedl_program_info {
     uint32_t n_bool, n_restrict, n_drange;
     double alg_bytes_total;       /* sum over roots of B(h) (per-hypothesis CSE only) */
     double alg_bytes_shared;      /* sum over canonical nodes (batch-wide CSE) */
+    uint32_t n_string;            /* string restriction nodes (after EQUAL short-circuit) */
 } hedl_program_info;
 hedl_status hedl_program_get_info(const hedl_program *prog, hedl_program_info *out);
 /* per-root algorithmic bytes B(h), host double[n] for roots [first, first+n) */

@@ -29,7 +29,8 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "OUT_OF_RANGE", 3: "EXAMPLE_CONFLICT", 4
           5: "PARSE", 6: "CUDA", 7: "OOM", 8: "UNSUPPORTED"}
 
 # every symbol include/hedl.h declares (checked by tests/test_abi.py)
-ABI_SYMBOLS = ["hedl_kb_load", "hedl_kb_free", "hedl_kb_get_info", "hedl_compile", "hedl_program_free",
+ABI_SYMBOLS = ["hedl_kb_load", "hedl_kb_free", "hedl_kb_get_info", "hedl_compile", "hedl_compile_ex",
+               "hedl_program_free",
                "hedl_program_get_info", "hedl_program_root_bytes", "hedl_eval_one", "hedl_eval_batch",
                "hedl_program_set_workspace_limit", "hedl_last_error", "hedl_version", "hedl_prof_enable",
                "hedl_prof_reset", "hedl_prof_read", "hedl_launch_count", "hedl_io_counters"]
@@ -46,20 +47,23 @@ class _KbDesc(C.Structure):
                 ("n_roles", C.c_uint32), ("role_edge_off", C.c_void_p), ("edge_subj", C.c_void_p),
                 ("edge_obj", C.c_void_p), ("n_data", C.c_uint32), ("data_off", C.c_void_p),
                 ("data_subj", C.c_void_p), ("data_val", C.c_void_p), ("n_pos", C.c_uint32),
-                ("pos_ids", C.c_void_p), ("n_neg", C.c_uint32), ("neg_ids", C.c_void_p)]
+                ("pos_ids", C.c_void_p), ("n_neg", C.c_uint32), ("neg_ids", C.c_void_p),
+                ("n_strings", C.c_uint32), ("str_off", C.c_void_p), ("str_subj", C.c_void_p),
+                ("str_val_off", C.c_void_p), ("str_bytes", C.c_void_p)]
 
 
 class _KbInfo(C.Structure):
     _fields_ = [("n_individuals", C.c_uint32), ("words", C.c_uint32), ("words_padded", C.c_uint32),
                 ("n_concepts", C.c_uint32), ("n_roles", C.c_uint32), ("n_data", C.c_uint32),
                 ("n_pos", C.c_uint64), ("n_neg", C.c_uint64), ("device_bytes", C.c_uint64),
-                ("edges", C.c_uint64 * 64), ("heavy", C.c_uint64 * 64)]
+                ("edges", C.c_uint64 * 64), ("heavy", C.c_uint64 * 64), ("n_strings", C.c_uint32),
+                ("str_pairs", C.c_uint64 * 32), ("str_values", C.c_uint64 * 32)]
 
 
 class _ProgInfo(C.Structure):
     _fields_ = [("n_roots", C.c_uint32), ("n_nodes", C.c_uint32), ("n_levels", C.c_uint32),
                 ("n_bool", C.c_uint32), ("n_restrict", C.c_uint32), ("n_drange", C.c_uint32),
-                ("alg_bytes_total", C.c_double), ("alg_bytes_shared", C.c_double)]
+                ("alg_bytes_total", C.c_double), ("alg_bytes_shared", C.c_double), ("n_string", C.c_uint32)]
 
 
 class _ProfEntry(C.Structure):
@@ -84,6 +88,7 @@ def lib():
         "hedl_kb_free": ([P], I32),
         "hedl_kb_get_info": ([P, C.POINTER(_KbInfo)], I32),
         "hedl_compile": ([P, P, U32, P, U64, P, U32, U32, C.POINTER(P)], I32),
+        "hedl_compile_ex": ([P, P, U32, P, U64, P, U32, U32, U32, P, P, C.POINTER(P)], I32),
         "hedl_program_free": ([P], I32),
         "hedl_program_get_info": ([P, C.POINTER(_ProgInfo)], I32),
         "hedl_program_root_bytes": ([P, U32, U32, P], I32),
@@ -203,6 +208,10 @@ def hedl_kb_load(kb: dict, device: int = 0, stream=None) -> KB:
         "data_val": np.ascontiguousarray(kb["data_val"], dtype=np.float32),
         "pos_ids": np.ascontiguousarray(kb["pos_ids"], dtype=np.uint32),
         "neg_ids": np.ascontiguousarray(kb["neg_ids"], dtype=np.uint32),
+        "str_off": np.ascontiguousarray(kb.get("str_off", np.zeros(1, np.uint64)), dtype=np.uint64),
+        "str_subj": np.ascontiguousarray(kb.get("str_subj", np.zeros(0, np.uint32)), dtype=np.uint32),
+        "str_val_off": np.ascontiguousarray(kb.get("str_val_off", np.zeros(1, np.uint64)), dtype=np.uint64),
+        "str_bytes": np.ascontiguousarray(kb.get("str_bytes", np.zeros(0, np.uint8)), dtype=np.uint8),
     }
     cb = arrs["concept_bits"]
     d = _KbDesc()
@@ -217,6 +226,9 @@ def hedl_kb_load(kb: dict, device: int = 0, stream=None) -> KB:
     d.data_subj, d.data_val = _ptr(arrs["data_subj"]), _ptr(arrs["data_val"])
     d.n_pos, d.pos_ids = len(arrs["pos_ids"]), _ptr(arrs["pos_ids"])
     d.n_neg, d.neg_ids = len(arrs["neg_ids"]), _ptr(arrs["neg_ids"])
+    d.n_strings = len(arrs["str_off"]) - 1
+    d.str_off, d.str_subj = _ptr(arrs["str_off"]), _ptr(arrs["str_subj"])
+    d.str_val_off, d.str_bytes = _ptr(arrs["str_val_off"]), _ptr(arrs["str_bytes"])
     h = C.c_void_p()
     if not torch.cuda.is_available():
         _check(L.hedl_kb_load(C.byref(d), device, None, C.byref(h)))
@@ -226,7 +238,13 @@ def hedl_kb_load(kb: dict, device: int = 0, stream=None) -> KB:
 
 
 def hedl_compile(kb: KB, nodes: np.ndarray, child_idx: np.ndarray, roots: np.ndarray,
-                 flags: int = 0) -> Program:
+                 flags: int = 0, patterns=None) -> Program:
+    """patterns: the SEQUAL / SCONTAIN pattern table (list of bytes); defaults to the table a
+    synth.format node array carries (`nodes.patterns`).  With patterns -> hedl_compile_ex."""
+    if patterns is None:
+        patterns = list(getattr(nodes, "patterns", None) or [])
+    if patterns:
+        return hedl_compile_ex(kb, nodes, child_idx, roots, flags, patterns)
     nodes = np.ascontiguousarray(nodes)
     assert nodes.dtype.itemsize == 28, "nodes must use synth.format.NODE_DTYPE (hedl_node)"
     kids = np.ascontiguousarray(child_idx, dtype=np.uint32)
@@ -234,6 +252,22 @@ def hedl_compile(kb: KB, nodes: np.ndarray, child_idx: np.ndarray, roots: np.nda
     h = C.c_void_p()
     _check(lib().hedl_compile(kb._h, _ptr(nodes), len(nodes), _ptr(kids), len(kids), _ptr(roots),
                               len(roots), flags, C.byref(h)))
+    return Program(h, kb, len(roots))
+
+
+def hedl_compile_ex(kb: KB, nodes: np.ndarray, child_idx: np.ndarray, roots: np.ndarray,
+                    flags: int = 0, patterns=()) -> Program:
+    nodes = np.ascontiguousarray(nodes)
+    assert nodes.dtype.itemsize == 28, "nodes must use synth.format.NODE_DTYPE (hedl_node)"
+    kids = np.ascontiguousarray(child_idx, dtype=np.uint32)
+    roots = np.ascontiguousarray(roots, dtype=np.uint32)
+    pats = [p.encode() if isinstance(p, str) else bytes(p) for p in patterns]
+    off = np.zeros(len(pats) + 1, dtype=np.uint64)
+    off[1:] = np.cumsum([len(p) for p in pats], dtype=np.uint64) if pats else []
+    blob = np.frombuffer(b"".join(pats), dtype=np.uint8).copy() if pats else np.zeros(0, np.uint8)
+    h = C.c_void_p()
+    _check(lib().hedl_compile_ex(kb._h, _ptr(nodes), len(nodes), _ptr(kids), len(kids), _ptr(roots),
+                                 len(roots), flags, len(pats), _ptr(off), _ptr(blob), C.byref(h)))
     return Program(h, kb, len(roots))
 
 

@@ -58,6 +58,10 @@ double node_bytes(const hedl_kb *kb, const CNode &n) {
     const double W4b = 4.0 * kb->W;
     if (n.kind == NK_AND || n.kind == NK_OR) return (n.op_count + 1) * W4b;
     if (n.kind == NK_RESTRICT) return kb->dir_bytes[n.dir] + 2 * W4b;
+    if (n.kind == NK_STRING) {     // pairs CSR (+ the role's interned values for CONTAIN) + output
+        const hedl_sdir &sd = kb->sdirs[n.dir];
+        return kb->str_bytes[n.dir] + (n.pred == SM_CONTAIN ? sd.dict_bytes + 8.0 * (sd.V + 1) : 0.0) + W4b;
+    }
     return kb->data_bytes[n.dir] + W4b;
 }
 
@@ -199,6 +203,10 @@ struct Input {
     const uint32_t *roots;
     uint32_t n_roots;
     uint32_t flags;
+    uint32_t n_pat;                       // string-pattern table (hedl_compile_ex)
+    const uint64_t *pat_off;
+    const uint8_t *pat_bytes;
+    const std::vector<uint32_t> *pat_canon;   // pattern id -> program pattern id (CONTAIN), or ~0
 };
 
 // canonicalise roots [r0, r1) into sh.dag (iterative post-order DFS, cycle check)
@@ -332,6 +340,30 @@ void canon_shard(const Input &in, uint32_t r0, uint32_t r1, Shard &sh) {
                     r = mkref(RT_NODE, D.intern(n, nullptr), 0);
                     break;
                 }
+                case HEDL_OP_SEQUAL:
+                case HEDL_OP_SCONTAIN: {
+                    if (cc) return bad(HEDL_ERR_BAD_EXPR, i, "string restriction takes no children");
+                    if (nd.arg >= kb->S) return bad(HEDL_ERR_OUT_OF_RANGE, i, "string role id out of range");
+                    if (nd.n >= in.n_pat) return bad(HEDL_ERR_OUT_OF_RANGE, i, "pattern id out of range");
+                    const uint64_t a = in.pat_off[nd.n], b = in.pat_off[nd.n + 1];
+                    CNode n{};
+                    n.kind = NK_STRING;
+                    n.dir = (uint16_t)nd.arg;
+                    if (nd.op == HEDL_OP_SEQUAL) {
+                        // interned-id compare; an absent value short-circuits to BOTTOM
+                        const auto &ids = kb->sdirs[nd.arg].ids;
+                        auto it = ids.find(std::string((const char *)in.pat_bytes + a, (const char *)in.pat_bytes + b));
+                        if (it == ids.end()) { r = mkref(RT_TOP, 0, 1); break; }
+                        n.pred = SM_EQUAL;
+                        n.n = it->second;
+                    } else {
+                        if (a == b) return bad(HEDL_ERR_BAD_EXPR, i, "empty CONTAIN pattern");
+                        n.pred = SM_CONTAIN;
+                        n.n = (*in.pat_canon)[nd.n];
+                    }
+                    r = mkref(RT_NODE, D.intern(n, nullptr), 0);
+                    break;
+                }
                 default:
                     return bad(HEDL_ERR_BAD_EXPR, i, "unknown opcode");
                 }
@@ -435,13 +467,44 @@ extern "C" hedl_status hedl_compile(const hedl_kb *kb, const hedl_node *nodes, u
                                     const uint32_t *child_idx, uint64_t n_child_idx,
                                     const uint32_t *roots, uint32_t n_roots, uint32_t flags,
                                     hedl_program **out) {
+    return hedl_compile_ex(kb, nodes, n_nodes, child_idx, n_child_idx, roots, n_roots, flags, 0, nullptr, nullptr, out);
+}
+
+extern "C" hedl_status hedl_compile_ex(const hedl_kb *kb, const hedl_node *nodes, uint32_t n_nodes,
+                                       const uint32_t *child_idx, uint64_t n_child_idx,
+                                       const uint32_t *roots, uint32_t n_roots, uint32_t flags,
+                                       uint32_t n_patterns, const uint64_t *pat_off, const uint8_t *pat_bytes,
+                                       hedl_program **out) {
     if (!kb || !out) return fail(HEDL_ERR_INVALID_ARG, "null kb/out");
     *out = nullptr;
     if ((n_nodes && !nodes) || (n_child_idx && !child_idx) || (n_roots && !roots))
         return fail(HEDL_ERR_INVALID_ARG, "null node/child/root array");
     if (n_nodes >= (1u << 28)) return fail(HEDL_ERR_INVALID_ARG, "too many nodes in one program (max 2^28)");
+    if (n_patterns && !pat_off) return fail(HEDL_ERR_INVALID_ARG, "null pattern offsets");
+    for (uint32_t q = 0; q < n_patterns; ++q)
+        if (pat_off[q + 1] < pat_off[q]) return fail(HEDL_ERR_INVALID_ARG, "pattern offsets not ascending");
+    if (n_patterns && pat_off[n_patterns] > pat_off[0] && !pat_bytes) return fail(HEDL_ERR_INVALID_ARG, "null pattern bytes");
     const double t0 = now_ms();
-    const Input in{kb, nodes, n_nodes, child_idx, n_child_idx, roots, n_roots, flags};
+    // CONTAIN patterns: deduplicated into the program's own table (equal patterns -> one node)
+    std::vector<uint32_t> pat_canon;
+    std::vector<std::string> prog_pats;
+    if (n_patterns) {
+        pat_canon.assign(n_patterns, ~0u);
+        std::unordered_map<std::string, uint32_t> seen;
+        for (uint32_t i = 0; i < n_nodes; ++i) {
+            if (nodes[i].op != HEDL_OP_SCONTAIN || nodes[i].n >= n_patterns || pat_canon[nodes[i].n] != ~0u) continue;
+            const uint32_t q = nodes[i].n;
+            std::string key((const char *)pat_bytes + pat_off[q], (const char *)pat_bytes + pat_off[q + 1]);
+            auto it = seen.find(key);
+            if (it == seen.end()) {
+                it = seen.emplace(key, (uint32_t)prog_pats.size()).first;
+                prog_pats.push_back(std::move(key));
+            }
+            pat_canon[q] = it->second;
+        }
+    }
+    const Input in{kb, nodes, n_nodes, child_idx, n_child_idx, roots, n_roots, flags,
+                   n_patterns, pat_off, pat_bytes, &pat_canon};
     unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     if (const char *e = std::getenv("HEDL_COMPILE_THREADS")) hw = std::max(1, std::atoi(e));   // tests / tuning
     const unsigned T = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>({(uint64_t)hw, 32ull, (uint64_t)n_roots / 4096}));
@@ -457,6 +520,7 @@ extern "C" hedl_status hedl_compile(const hedl_kb *kb, const hedl_node *nodes, u
     hedl_program *p = new hedl_program();
     p->kb = kb;
     p->flags = flags;
+    p->patterns.swap(prog_pats);
     p->root_node.resize(n_roots);
     if (T == 1) {
         // one shard: its DAG is the program
@@ -622,6 +686,7 @@ extern "C" hedl_status hedl_program_get_info(const hedl_program *p, hedl_program
         out->n_nodes++;
         if (n.kind == NK_AND || n.kind == NK_OR) out->n_bool++;
         else if (n.kind == NK_RESTRICT) out->n_restrict++;
+        else if (n.kind == NK_STRING) out->n_string++;
         else out->n_drange++;
         out->alg_bytes_shared += n.bytes;
     }

@@ -29,7 +29,7 @@ struct DevBuf {
 };
 
 struct LaunchRec {
-    uint8_t kind;          // NK_AND (AND+OR), NK_RESTRICT, NK_DRANGE
+    uint8_t kind;          // NK_AND (AND+OR), NK_RESTRICT, NK_DRANGE, NK_STRING
     uint16_t key;          // dir / prop
     bool slice;
     bool proj;             // boolean group evaluated on example-projected rows
@@ -42,7 +42,7 @@ struct ChunkPlan {
     uint32_t ri, rc;       // roots [ri, rc) relative to the program
     uint32_t nn, ncov, nrows, nprows;
     size_t blob_off, blob_bytes;          // into PlanCache host/device blobs
-    size_t off_bool, off_ops, off_res, off_dr, off_cov, off_rows;
+    size_t off_bool, off_ops, off_res, off_dr, off_str, off_cov, off_rows;
     std::vector<LaunchRec> recs;
 };
 
@@ -59,6 +59,8 @@ struct PlanCache {
 
 struct Workspace {
     DevBuf rows, prows, heavy, counts, slice, stage;
+    uint8_t *pats = nullptr;             // device copy of the program's CONTAIN patterns
+    std::vector<uint64_t> pat_off;       // their offsets
     hedl_counts *stage_host = nullptr;   // pinned staging of host-bound counts
     size_t stage_host_n = 0;
     PlanCache plan;
@@ -199,10 +201,11 @@ uint32_t par_rank(size_t n, Flag flag, Out &out) {
     return cnt[C];
 }
 
-// order key: level, kind, direction / property, lane-pack class (node id breaks ties)
-inline uint32_t group_key(const CNode &n) {
+// order key: level, kind, direction / property / string role, lane-pack class (node id breaks ties)
+inline uint64_t group_key(const CNode &n) {
     const uint32_t cls = n.kind == NK_RESTRICT ? slice_class(n.pred, n.n, n.sat) : 0;
-    return (std::min<uint32_t>(n.level, 4095) << 20) | ((uint32_t)(n.kind & 3) << 18) | ((uint32_t)n.dir << 2) | cls;
+    const uint32_t kind = n.kind == NK_OR ? NK_AND : n.kind;
+    return ((uint64_t)n.level << 24) | ((uint64_t)(kind & 7) << 20) | ((uint64_t)n.dir << 2) | cls;
 }
 
 // stable bucket sort of `list` (ascending ids) by group_key: parallel histogram + scatter
@@ -214,11 +217,11 @@ void sort_by_key(const hedl_program *p, std::vector<uint32_t> &list) {
         });
         return;
     }
-    std::vector<uint32_t> key(n);
+    std::vector<uint64_t> key(n);
     par_for(n, 1 << 14, [&](size_t a, size_t b) { for (size_t k = a; k < b; ++k) key[k] = group_key(p->nodes[list[k]]); });
-    std::vector<uint32_t> uk;                      // distinct keys (few: levels x kinds x directions x classes)
+    std::vector<uint64_t> uk;                      // distinct keys (few: levels x kinds x directions x classes)
     {
-        std::vector<uint32_t> tmp;
+        std::vector<uint64_t> tmp;
         for (size_t k = 0; k < n; k += 97) tmp.push_back(key[k]);
         std::sort(tmp.begin(), tmp.end());
         tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
@@ -266,7 +269,7 @@ void collect_chunks(hedl_program *p, uint32_t r0, uint32_t r1, uint64_t row_cap,
         std::vector<uint32_t> cnt(C + 1, 0);
         par_for(C, 1, [&](size_t c0, size_t c1) {
             for (size_t c = c0; c < c1; ++c)
-                for (size_t i = NN * c / C; i < NN * (c + 1) / C; ++i) cnt[c + 1] += p->nodes[i].kind <= NK_DRANGE;
+                for (size_t i = NN * c / C; i < NN * (c + 1) / C; ++i) cnt[c + 1] += p->nodes[i].kind <= NK_STRING;
         });
         for (size_t c = 0; c < C; ++c) cnt[c + 1] += cnt[c];
         const uint64_t live = cnt[C];
@@ -276,7 +279,7 @@ void collect_chunks(hedl_program *p, uint32_t r0, uint32_t r1, uint64_t row_cap,
                 for (size_t c = c0; c < c1; ++c) {
                     uint32_t o = cnt[c];
                     for (size_t i = NN * c / C; i < NN * (c + 1) / C; ++i)
-                        if (p->nodes[i].kind <= NK_DRANGE) list[o++] = (uint32_t)i;
+                        if (p->nodes[i].kind <= NK_STRING) list[o++] = (uint32_t)i;
                 }
             });
             sort_by_key(p, list);
@@ -460,7 +463,7 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
             k = e;
         }
         // descriptor bases per group and operand bases per boolean member (for the parallel fill)
-        size_t n_ops = 0, n_bool = 0, n_res = 0, n_dr = 0;
+        size_t n_ops = 0, n_bool = 0, n_res = 0, n_dr = 0, n_str = 0;
         tmp.gdesc.resize(groups.size());
         tmp.opbase.assign(members.size(), 0);
         for (size_t gi = 0; gi < groups.size(); ++gi) {
@@ -476,6 +479,9 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                 tmp.gdesc[gi] = (uint32_t)n_res;
                 n_res += g.count;
                 if (!g.slice) *heavy_need = std::max(*heavy_need, (size_t)g.count * kb->dirs[g.key].n_heavy * 8);
+            } else if (g.kind == NK_STRING) {
+                tmp.gdesc[gi] = (uint32_t)n_str;
+                n_str += g.count;
             } else {
                 tmp.gdesc[gi] = (uint32_t)n_dr;
                 n_dr += g.count;
@@ -485,7 +491,8 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
         cp.off_ops = align_up(cp.off_bool + n_bool * sizeof(BoolDesc), 16);
         cp.off_res = align_up(cp.off_ops + n_ops * sizeof(Operand), 16);
         cp.off_dr = align_up(cp.off_res + n_res * sizeof(RestrictDesc), 16);
-        cp.off_cov = align_up(cp.off_dr + n_dr * sizeof(DrangeDesc), 16);
+        cp.off_str = align_up(cp.off_dr + n_dr * sizeof(DrangeDesc), 16);
+        cp.off_cov = align_up(cp.off_str + n_str * sizeof(StringDesc), 16);
         cp.off_rows = align_up(cp.off_cov + nroots * sizeof(uint32_t), 16);
         cp.blob_bytes = align_up(cp.off_rows + (out_bits ? nroots * sizeof(void *) : 0), 256);
         cp.blob_off = *blob_cursor;
@@ -516,6 +523,8 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
     Operand *ho = (Operand *)(h + cp.off_ops);
     RestrictDesc *hr = (RestrictDesc *)(h + cp.off_res);
     DrangeDesc *hd = (DrangeDesc *)(h + cp.off_dr);
+    StringDesc *hs = (StringDesc *)(h + cp.off_str);
+    const Workspace *wsp = (const Workspace *)p->ws;
     // tasks: (group, member range); filled in parallel, each at precomputed offsets
     struct Task { uint32_t g, m0, m1; double bytes, bytes2; };
     std::vector<Task> tasks;
@@ -572,6 +581,25 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                     T.bytes += 4.0 * (kb->N + 1) + 4.0 * (dr.E - dr.E_heavy) +
                                4.0 * kb->W * (1 + (rd.out ? 1 : 0) + (rd.cover >= 0 ? 2 : 0));
                     T.bytes2 += 4.0 * dr.E_heavy;
+                }
+            } else if (g.kind == NK_STRING) {
+                for (uint32_t m = T.m0; m < T.m1; ++m) {
+                    const uint32_t k = members[m];
+                    const CNode &n = p->nodes[list[k]];
+                    StringDesc sd;
+                    sd.out = out_of(k);
+                    sd.proj = proj_of(k);
+                    sd.cover = cover_of_node[k];
+                    sd.mode = n.pred;
+                    sd.vid = n.pred == SM_EQUAL ? n.n : 0;
+                    sd.pat = nullptr;
+                    sd.pat_len = 0;
+                    if (n.pred == SM_CONTAIN) {
+                        sd.pat = wsp->pats + wsp->pat_off[n.n];
+                        sd.pat_len = (uint32_t)(wsp->pat_off[n.n + 1] - wsp->pat_off[n.n]);
+                    }
+                    hs[base + (m - g.first)] = sd;
+                    T.bytes += n.bytes - 4.0 * kb->W + 4.0 * kb->W * ((sd.out ? 1 : 0) + (sd.cover >= 0 ? 2 : 0));
                 }
             } else {
                 for (uint32_t m = T.m0; m < T.m1; ++m) {
@@ -635,6 +663,10 @@ hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, u
                           dr.tiles, dr.order, dr.tile_slice, dr.sell_off, dr.sell_w, dr.sell_col, dr.n_tiles};
                 launch_restrict(s, kd, dd, dd_desc, lr.count, cov, (uint32_t *)w->heavy.p, lr.bytes, lr.bytes2);
             }
+        } else if (lr.kind == NK_STRING) {
+            const hedl_sdir &sdr = kb->sdirs[lr.key];
+            launch_string(s, kd, StrDev{sdr.row_ptr, sdr.vid, sdr.dict_off, sdr.dict},
+                          (const StringDesc *)(d + cp.off_str) + lr.first_desc, lr.count, cov, lr.bytes);
         } else {
             const hedl_data &dp = kb->data[lr.key];
             launch_drange(s, kd, dp.row_ptr, dp.val, (const DrangeDesc *)(d + cp.off_dr) + lr.first_desc, lr.count, cov,
@@ -671,6 +703,21 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
             p->ws_limit = std::max<uint64_t>(1ull << 28, std::min<uint64_t>(fr / 2, 48ull << 30));
         }
         const uint64_t row_cap = std::max<uint64_t>(1, row_bytes ? p->ws_limit / row_bytes : (1ull << 22));
+        if (!p->patterns.empty() && !w->pats) {      // the program's CONTAIN patterns, uploaded once
+            std::vector<uint8_t> blob;
+            w->pat_off.assign(1, 0);
+            for (const std::string &q : p->patterns) {
+                blob.insert(blob.end(), q.begin(), q.end());
+                w->pat_off.push_back(blob.size());
+            }
+            if (cudaMalloc((void **)&w->pats, std::max<size_t>(blob.size(), 16)) != cudaSuccess) {
+                cudaGetLastError();
+                w->pats = nullptr;
+                return fail(HEDL_ERR_OOM, "pattern table");
+            }
+            HEDL_CUDA(kb, cudaMemcpy(w->pats, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+            count_io(blob.size(), 0);
+        }
         const bool use_slice = !(eflags & HEDL_EVAL_PER_NODE) && slice_enabled(kb);
         const bool force = eflags & HEDL_EVAL_FORCE_SLICE;
         std::vector<std::vector<uint32_t>> lists;
@@ -798,6 +845,7 @@ static bool build_interp(const hedl_kb *kb, const hedl_program *p, uint32_t root
     while (!st.empty()) {
         auto &top = st.back();
         const CNode &n = p->nodes[top.first];
+        if (n.kind == NK_STRING) return false;     // string restrictions run on the batch path
         if (top.second < n.op_count) {
             const uint32_t o = p->ops[n.op_begin + top.second++];
             if (ref_type(o) == RT_NODE && !is_seen(ref_id(o))) {
@@ -894,6 +942,7 @@ extern "C" hedl_status hedl_program_free(hedl_program *p) {
         w->plan.host = w->plan.dev = nullptr;
         release_plan(w->plan);
         if (w->done) cudaEventDestroy(w->done);
+        if (w->pats) cudaFree(w->pats);
         if (p->lat_host) cudaFreeHost(p->lat_host);
         delete w;
     } else if (p->lat_host) {

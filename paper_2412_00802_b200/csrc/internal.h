@@ -9,6 +9,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/hedl.h"
@@ -50,13 +51,14 @@ inline uint32_t ref_comp(uint32_t r) { return r & 1u; }
 inline RefType ref_type(uint32_t r) { return RefType((r >> 1) & 3u); }
 inline uint32_t ref_id(uint32_t r) { return r >> 3; }
 
-enum NodeKind : uint8_t { NK_AND = 0, NK_OR = 1, NK_RESTRICT = 2, NK_DRANGE = 3 };
+enum NodeKind : uint8_t { NK_AND = 0, NK_OR = 1, NK_RESTRICT = 2, NK_DRANGE = 3, NK_STRING = 4 };
+enum StrMode : uint8_t { SM_EQUAL = 0, SM_CONTAIN = 1 };
 
 struct CNode {
     uint8_t kind;        // NodeKind
-    uint8_t pred;        // restrict: Pred
-    uint16_t dir;        // restrict: 2*role + inverse ; drange: data property
-    uint32_t n;          // restrict: threshold
+    uint8_t pred;        // restrict: Pred ; string: StrMode
+    uint16_t dir;        // restrict: 2*role + inverse ; drange: data property ; string: string role
+    uint32_t n;          // restrict: threshold ; string: interned value id (EQUAL) / program pattern id (CONTAIN)
     uint32_t sat;        // restrict: saturation point of the count
     float lo, hi;        // drange
     uint32_t op_begin;   // operands in Program::ops
@@ -105,6 +107,15 @@ struct hedl_data {
     uint64_t V = 0;
 };
 
+struct hedl_sdir {                 // one string concrete role (Algs. 11-14)
+    uint32_t *row_ptr = nullptr;   // device [N+1]: subject -> its distinct value ids
+    uint32_t *vid = nullptr;       // device [E], ascending per subject
+    uint64_t *dict_off = nullptr;  // device [V+1]: interned value v = dict[dict_off[v] .. dict_off[v+1])
+    uint8_t *dict = nullptr;       // device
+    uint64_t E = 0, V = 0, dict_bytes = 0;
+    std::unordered_map<std::string, uint32_t> ids;   // host: value -> id (stringValuesMapping)
+};
+
 struct hedl_kb {
     int device = 0;
     int sm_count = 148;
@@ -124,6 +135,8 @@ struct hedl_kb {
     uint32_t *pones = nullptr, *ppos = nullptr, *pneg = nullptr;   // device [MW4]
     std::vector<hedl_dir> dirs;    // 2R
     std::vector<hedl_data> data;   // D
+    uint32_t S = 0;
+    std::vector<hedl_sdir> sdirs;  // S string roles
     std::vector<void *> allocs;
     uint64_t device_bytes = 0;
     std::atomic<bool> poisoned{false};
@@ -136,6 +149,7 @@ struct hedl_kb {
     std::mutex interp_mu;
     std::vector<double> dir_bytes;  // 4(N+1) + 4E per direction
     std::vector<double> data_bytes; // 4(N+1) + 4V per property
+    std::vector<double> str_bytes;  // 4(N+1) + 4E (+ dictionary for CONTAIN) per string role
 };
 
 struct hedl_program {
@@ -144,6 +158,7 @@ struct hedl_program {
     std::vector<hedl::CNode, hedl::NoInitAlloc<hedl::CNode>> nodes;
     std::vector<uint32_t, hedl::NoInitAlloc<uint32_t>> ops;
     std::vector<uint32_t> root_node;   // per root: computed canonical node id
+    std::vector<std::string> patterns; // CONTAIN patterns (deduplicated), CNode.n indexes them
     std::vector<double> root_bytes;    // B(h)
     uint32_t n_levels = 0;
     // evaluation workspace (device), grown on demand
@@ -187,7 +202,7 @@ void timing_note(const char *what, double ms);
 
 // ---- profiling -----------------------------------------------------------------
 enum KClass { KC_BOOL, KC_RESTRICT, KC_HEAVY, KC_DRANGE, KC_COVER_INIT, KC_GATHER,
-              KC_SLICE_IN, KC_SLICE, KC_SLICE_HEAVY, KC_KB, KC_SLICE_EX, KC_INTERP, KC_N };
+              KC_SLICE_IN, KC_SLICE, KC_SLICE_HEAVY, KC_KB, KC_SLICE_EX, KC_INTERP, KC_STRING, KC_N };
 extern const char *kKClassName[KC_N];
 void prof_begin(cudaStream_t s, int kc);
 void prof_end(cudaStream_t s, int kc, double alg_bytes, double units = 1);
@@ -220,6 +235,20 @@ struct DrangeDesc {
     float lo, hi;
     int32_t cover;
     uint32_t prop;
+};
+struct StringDesc {
+    uint32_t *out;
+    uint32_t *proj;
+    int32_t cover;
+    uint32_t mode;                 // StrMode
+    uint32_t vid;                  // EQUAL: interned value id
+    uint32_t pat_len;              // CONTAIN: pattern bytes pat[0 .. pat_len)
+    const uint8_t *pat;            // device (the plan's pattern blob)
+};
+struct StrDev {                   // one string role, passed by value
+    const uint32_t *row_ptr, *vid;
+    const uint64_t *dict_off;
+    const uint8_t *dict;
 };
 struct DirDev {                   // passed by value
     const uint32_t *row_ptr;
@@ -260,6 +289,8 @@ void launch_restrict(cudaStream_t s, const KbDev &kb, const DirDev &dir, const R
                      double alg_heavy);
 void launch_drange(cudaStream_t s, const KbDev &kb, const uint32_t *row_ptr, const float *val,
                    const DrangeDesc *d_desc, uint32_t n_desc, hedl_counts *counts, double alg_bytes);
+void launch_string(cudaStream_t s, const KbDev &kb, const StrDev &sd, const StringDesc *d_desc, uint32_t n_desc,
+                   hedl_counts *counts, double alg_bytes);
 void launch_gather_counts(cudaStream_t s, const hedl_counts *slots, const uint32_t *slot_of,
                           hedl_counts *out, uint32_t n);
 void launch_gather_bits(cudaStream_t s, const uint32_t *const *rows, uint32_t *out, uint32_t W,

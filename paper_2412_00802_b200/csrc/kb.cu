@@ -34,10 +34,13 @@ struct HostCSR {
 };
 
 // counting sort of (s, o) pairs by s, then sort + dedupe each row (sets)
-hedl_status build_forward(uint32_t N, const uint32_t *s, const uint32_t *o, uint64_t m, HostCSR &out) {
+// (objects < n_obj; n_obj = N for roles, the number of interned values for string roles)
+hedl_status build_forward(uint32_t N, const uint32_t *s, const uint32_t *o, uint64_t m, HostCSR &out,
+                          uint64_t n_obj = ~0ull) {
+    if (n_obj == ~0ull) n_obj = N;
     std::vector<uint64_t> cnt(N + 1, 0);
     for (uint64_t k = 0; k < m; ++k) {
-        if (s[k] >= N || o[k] >= N) return fail(HEDL_ERR_OUT_OF_RANGE, "role assertion id >= N at index " + std::to_string(k));
+        if (s[k] >= N || o[k] >= n_obj) return fail(HEDL_ERR_OUT_OF_RANGE, "role assertion id >= N at index " + std::to_string(k));
         cnt[s[k] + 1]++;
     }
     for (uint32_t i = 0; i < N; ++i) cnt[i + 1] += cnt[i];
@@ -118,6 +121,9 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
     if (C && W && !desc->concept_bits) return fail(HEDL_ERR_INVALID_ARG, "concept_bits is null");
     if (R && !desc->role_edge_off) return fail(HEDL_ERR_INVALID_ARG, "role_edge_off is null");
     if (D && !desc->data_off) return fail(HEDL_ERR_INVALID_ARG, "data_off is null");
+    const uint32_t S = desc->n_strings;
+    if (S > 0xffff) return fail(HEDL_ERR_INVALID_ARG, "at most 65535 string roles supported");
+    if (S && !desc->str_off) return fail(HEDL_ERR_INVALID_ARG, "str_off is null");
     if (desc->n_pos && !desc->pos_ids) return fail(HEDL_ERR_INVALID_ARG, "pos_ids is null");
     if (desc->n_neg && !desc->neg_ids) return fail(HEDL_ERR_INVALID_ARG, "neg_ids is null");
     // tail bits of every concept row must be 0
@@ -138,6 +144,18 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
         for (uint32_t d = 0; d < D; ++d)
             if (desc->data_off[d + 1] < desc->data_off[d]) return fail(HEDL_ERR_INVALID_ARG, "data_off not monotone");
         if (desc->data_off[D] && (!desc->data_subj || !desc->data_val)) return fail(HEDL_ERR_INVALID_ARG, "data arrays null");
+    }
+    if (S) {
+        if (desc->str_off[0] != 0) return fail(HEDL_ERR_INVALID_ARG, "str_off[0] != 0");
+        for (uint32_t r = 0; r < S; ++r)
+            if (desc->str_off[r + 1] < desc->str_off[r]) return fail(HEDL_ERR_INVALID_ARG, "str_off not monotone");
+        const uint64_t A = desc->str_off[S];
+        if (A && (!desc->str_subj || !desc->str_val_off)) return fail(HEDL_ERR_INVALID_ARG, "string arrays null");
+        if (A) {
+            for (uint64_t k = 0; k < A; ++k)
+                if (desc->str_val_off[k + 1] < desc->str_val_off[k]) return fail(HEDL_ERR_INVALID_ARG, "str_val_off not monotone");
+            if (desc->str_val_off[A] > desc->str_val_off[0] && !desc->str_bytes) return fail(HEDL_ERR_INVALID_ARG, "str_bytes is null");
+        }
     }
     // examples (P and N disjoint)
     std::vector<uint32_t> pos(W4, 0), neg(W4, 0);
@@ -189,6 +207,41 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
         parallel_ranges(N, [&](uint64_t x0, uint64_t x1) {
             for (uint64_t i = x0; i < x1; ++i) std::sort(v.begin() + rp[i], v.begin() + rp[i + 1]);
         });
+    }
+
+    // string roles: intern the distinct values of each role (stringValuesMapping),
+    // then a CSR subject -> ascending distinct value ids (duplicate pairs removed)
+    struct HostStr {
+        std::vector<uint32_t> row_ptr, vid;
+        std::vector<uint64_t> dict_off;
+        std::vector<uint8_t> dict;
+        std::unordered_map<std::string, uint32_t> ids;
+    };
+    std::vector<HostStr> hs(S);
+    for (uint32_t r = 0; r < S; ++r) {
+        HostStr &H = hs[r];
+        const uint64_t a = desc->str_off[r], b = desc->str_off[r + 1];
+        std::vector<uint32_t> kv(b - a);
+        H.dict_off.push_back(0);
+        for (uint64_t k = a; k < b; ++k) {
+            if (desc->str_subj[k] >= N) return fail(HEDL_ERR_OUT_OF_RANGE, "string subject id >= N");
+            const uint64_t v0 = desc->str_val_off[k], v1 = desc->str_val_off[k + 1];
+            std::string key((const char *)desc->str_bytes + v0, (const char *)desc->str_bytes + v1);
+            auto it = H.ids.find(key);
+            if (it == H.ids.end()) {
+                if (H.ids.size() >= 0xffffffffull) return fail(HEDL_ERR_INVALID_ARG, "string role has >= 2^32 values");
+                it = H.ids.emplace(std::move(key), (uint32_t)H.ids.size()).first;
+                H.dict.insert(H.dict.end(), desc->str_bytes + v0, desc->str_bytes + v1);
+                H.dict_off.push_back(H.dict.size());
+            }
+            kv[k - a] = it->second;
+        }
+        std::vector<uint32_t> subj(desc->str_subj + a, desc->str_subj + b);
+        HostCSR c;
+        hedl_status st = build_forward(N, subj.data(), kv.data(), b - a, c, H.ids.size());
+        if (st) return st;
+        H.row_ptr.swap(c.row_ptr);
+        H.vid.swap(c.col);
     }
 
     // ---- upload -------------------------------------------------------------------
@@ -406,6 +459,23 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
         kb->data_bytes[d] = 4.0 * (N + 1) + 4.0 * kb->data[d].V;
         if (cudaStreamSynchronize(st) != cudaSuccess) return bail(fail(HEDL_ERR_CUDA, "upload failed"));
     }
+    kb->S = S;
+    kb->sdirs.resize(S);
+    kb->str_bytes.resize(S);
+    for (uint32_t r = 0; r < S; ++r) {
+        hedl_sdir &sd = kb->sdirs[r];
+        HostStr &H = hs[r];
+        sd.E = H.vid.size();
+        sd.V = H.ids.size();
+        sd.dict_bytes = H.dict.size();
+        if ((s = upload(kb, st, &sd.row_ptr, H.row_ptr.data(), H.row_ptr.size()))) return bail(s);
+        if ((s = upload(kb, st, &sd.vid, H.vid.data(), H.vid.size()))) return bail(s);
+        if ((s = upload(kb, st, &sd.dict_off, H.dict_off.data(), H.dict_off.size()))) return bail(s);
+        if ((s = upload(kb, st, &sd.dict, H.dict.data(), H.dict.size()))) return bail(s);
+        kb->str_bytes[r] = 4.0 * (N + 1) + 4.0 * sd.E;
+        if (cudaStreamSynchronize(st) != cudaSuccess) return bail(fail(HEDL_ERR_CUDA, "upload failed"));
+        sd.ids.swap(H.ids);
+    }
     cudaSetDevice(prev_dev);
     *out = kb;
     return HEDL_OK;
@@ -434,6 +504,11 @@ extern "C" hedl_status hedl_kb_get_info(const hedl_kb *kb, hedl_kb_info *out) {
     for (size_t i = 0; i < kb->dirs.size() && i < 64; ++i) {
         out->edges[i] = kb->dirs[i].E;
         out->heavy[i] = kb->dirs[i].n_heavy;
+    }
+    out->n_strings = kb->S;
+    for (size_t i = 0; i < kb->sdirs.size() && i < 32; ++i) {
+        out->str_pairs[i] = kb->sdirs[i].E;
+        out->str_values[i] = kb->sdirs[i].V;
     }
     return HEDL_OK;
 }

@@ -10,6 +10,7 @@
 //  k_restrict_heavy heavy rows (deg > kHeavyDeg) split over CTAs; the last CTA
 //                   of a row finalises its bit with atomicOr (no other atomics on rows).
 //  k_drange         exists d.[lo,hi] over sorted per-individual values (Alg. 10, Q9).
+//  k_string         string EQUAL / CONTAIN restrictions (Algs. 11-14).
 //
 // Every output word is written exactly once by one warp (plus commutative
 // atomicOr of heavy bits), so results are deterministic (no paper-style
@@ -288,6 +289,84 @@ __global__ void __launch_bounds__(256) k_drange(KbDev kb, const uint32_t *__rest
     if (d.cover >= 0) block_cover(counts, d.cover, tp, fp);
 }
 
+// ------------------------------------------------------------------------------
+// String restrictions (Algs. 11-14).  Pull form: lane = subject x,
+// one warp per output word.  EQUAL compares interned ids (binary search of the
+// subject's ascending value ids); CONTAIN tests the subject's distinct values for
+// the pattern as a byte substring, lanes with many values scanned warp-cooperatively
+// with the paper's early exit (stop at the first matching assertion, Alg. 13).
+__device__ __forceinline__ bool str_contains(const uint8_t *__restrict__ t, uint64_t tl,
+                                             const uint8_t *__restrict__ p, uint32_t pl) {
+    if (pl > tl) return false;
+    const uint8_t p0 = __ldg(p);
+    for (uint64_t i = 0, last = tl - pl; i <= last; ++i) {
+        if (__ldg(t + i) != p0) continue;
+        uint32_t j = 1;
+        while (j < pl && __ldg(t + i + j) == __ldg(p + j)) ++j;
+        if (j == pl) return true;
+    }
+    return false;
+}
+
+__device__ __forceinline__ bool value_contains(const StrDev &sd, uint32_t v, const StringDesc &d) {
+    const uint64_t a = __ldg(sd.dict_off + v), b = __ldg(sd.dict_off + v + 1);
+    return str_contains(sd.dict + a, b - a, d.pat, d.pat_len);
+}
+
+constexpr uint32_t kStrLaneDeg = 8;   // CONTAIN rows longer than this are scanned by the whole warp
+
+__global__ void __launch_bounds__(256) k_string(KbDev kb, StrDev sd, const StringDesc *__restrict__ descs,
+                                                hedl_counts *counts) {
+    const StringDesc d = descs[blockIdx.y];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t w = blockIdx.x * 8 + (threadIdx.x >> 5);
+    uint32_t tp = 0, fp = 0;
+    if (w < kb.W4) {
+        uint32_t word = 0;
+        if (w < kb.W) {
+            const uint32_t x = (w << 5) + lane;
+            uint32_t e0 = 0, e1 = 0;
+            if (x < kb.N) {
+                e0 = __ldg(sd.row_ptr + x);
+                e1 = __ldg(sd.row_ptr + x + 1);
+            }
+            bool res = false;
+            if (d.mode == SM_EQUAL) {
+                uint32_t lo = e0, hi = e1;          // first id >= vid
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (__ldg(sd.vid + mid) < d.vid) lo = mid + 1; else hi = mid;
+                }
+                res = lo < e1 && __ldg(sd.vid + lo) == d.vid;
+                word = __ballot_sync(FULL, res);
+            } else {
+                const bool longrow = e1 - e0 > kStrLaneDeg;
+                if (!longrow)
+                    for (uint32_t e = e0; e < e1 && !res; ++e) res = value_contains(sd, __ldg(sd.vid + e), d);
+                word = __ballot_sync(FULL, res);
+                for (uint32_t m = __ballot_sync(FULL, longrow); m; m &= m - 1) {
+                    const uint32_t L = __ffs(m) - 1;
+                    const uint32_t a = __shfl_sync(FULL, e0, L), b = __shfl_sync(FULL, e1, L);
+                    for (uint32_t base = a; base < b; base += 32) {          // uniform trip count
+                        const uint32_t e = base + lane;
+                        const bool hit = e < b && value_contains(sd, __ldg(sd.vid + e), d);
+                        if (__any_sync(FULL, hit)) { word |= 1u << L; break; }
+                    }
+                }
+            }
+        }
+        if (lane == 0) {
+            if (d.proj && w < kb.W) proj_scatter(kb, d.proj, w, word);
+            if (d.out) d.out[w] = word;
+            if (d.cover >= 0) {
+                tp = __popc(word & __ldg(kb.pos + w));
+                fp = __popc(word & __ldg(kb.neg + w));
+            }
+        }
+    }
+    if (d.cover >= 0) block_cover(counts, d.cover, tp, fp);
+}
+
 __global__ void k_gather_counts(const hedl_counts *__restrict__ slots, const uint32_t *__restrict__ slot_of,
                                 hedl_counts *out, uint32_t n) {
     uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -358,6 +437,19 @@ void launch_drange(cudaStream_t s, const KbDev &kb, const uint32_t *row_ptr, con
         k_drange<<<dim3(gx, nd), 256, 0, s>>>(kb, row_ptr, val, d_desc + off, counts);
         count_launch();
         prof_end(s, KC_DRANGE, alg_bytes * nd / n_desc, nd);
+    }
+}
+
+void launch_string(cudaStream_t s, const KbDev &kb, const StrDev &sd, const StringDesc *d_desc, uint32_t n_desc,
+                   hedl_counts *counts, double alg_bytes) {
+    const uint32_t gx = cdiv(kb.W4, 8);
+    if (!gx) return;
+    for (uint32_t off = 0; off < n_desc; off += 65535) {
+        const uint32_t nd = n_desc - off < 65535 ? n_desc - off : 65535;
+        prof_begin(s, KC_STRING);
+        k_string<<<dim3(gx, nd), 256, 0, s>>>(kb, sd, d_desc + off, counts);
+        count_launch();
+        prof_end(s, KC_STRING, alg_bytes * nd / n_desc, nd);
     }
 }
 

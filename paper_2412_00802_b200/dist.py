@@ -26,7 +26,7 @@ def root_costs(nodes: np.ndarray, child_idx: np.ndarray, roots: np.ndarray) -> n
     balance shards before any rank compiles.
     """
     n = len(nodes)
-    heavy = np.isin(nodes["op"], ROLE_OPS + (11,)).astype(np.int64)
+    heavy = np.isin(nodes["op"], ROLE_OPS + (11, 12, 13)).astype(np.int64)
     cb = nodes["child_begin"].astype(np.int64)
     cc = nodes["child_count"].astype(np.int64)
     owner = np.repeat(np.arange(n), cc)                       # parent of each child slot

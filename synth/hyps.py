@@ -376,3 +376,46 @@ def batch_arrays(kind: str, kb: dict, n: int, seed: int, chunk: int = 25_000,
         with ProcessPoolExecutor(workers, mp_context=mp.get_context("fork")) as ex:
             parts = list(ex.map(_gen_chunk, jobs))
     return concat_arrays(parts)
+
+
+def string_hypotheses(kb: dict, n: int = 400, seed: int = 7) -> List[tuple]:
+    """Hypotheses over a string_kb: EQUAL on asserted values (hits) and on absent values
+    (the PAPER.md:457 short-circuit), CONTAIN on substrings of asserted values, on
+    absent substrings and on whole values, alone and composed with the other constructors."""
+    rng = np.random.default_rng(seed)
+    vocab = kb["_vocab"]
+    S = len(kb["str_off"]) - 1
+    R = len(kb["role_edge_off"]) - 1
+    C = kb["concept_bits"].shape[0]
+
+    def leaf():
+        s = int(rng.integers(S))
+        v = vocab[int(rng.integers(min(len(vocab), 50)))] if rng.random() < 0.5 else vocab[int(rng.integers(len(vocab)))]
+        u = rng.random()
+        if u < 0.3:
+            return ("SEQUAL", s, v)
+        if u < 0.4:
+            return ("SEQUAL", s, v + b"#absent")
+        if u < 0.85:
+            a = int(rng.integers(len(v)))
+            b = int(rng.integers(a + 1, len(v) + 1))
+            return ("SCONTAIN", s, v[a:b])
+        return ("SCONTAIN", s, b"#" + v[:3])
+
+    out = []
+    for _ in range(n):
+        k = int(rng.integers(6))
+        if k == 0:
+            t = leaf()
+        elif k == 1:
+            t = ("AND", [("ATOM", int(rng.integers(C))), leaf()])
+        elif k == 2:
+            t = ("OR", [leaf(), leaf()])
+        elif k == 3:
+            t = ("NOT", leaf())
+        elif k == 4 and R:
+            t = ("EXISTS", int(rng.integers(R)), bool(rng.integers(2)), leaf())
+        else:
+            t = ("AND", [("NOT", ("ATOM", int(rng.integers(C)))), ("OR", [leaf(), ("ATOM", 0)])])
+        out.append(t)
+    return out

@@ -4,7 +4,9 @@ Paper setup: conjunction / disjunction of 5 concepts over 10.
 individuals and of 1..32 concepts over 10^6 (Table 2); exists / forall over the
 "single subject" (one hub) and "unique subject" (degree <= 1) regimes with 10..10^7
 assertions (Table 4); MIN / MAX cardinality (card_role table); numeric
-existential restriction with every value one constant (Table 8).
+existential restriction with every value one constant and the string EQUAL / CONTAIN rows
+(Table 8; plus a distinct-values variant of ours, where interning cannot
+collapse the assertions).
 
 For each cell: the hypothesis is compiled once, then
   * latency_us : host wall time of hedl_eval_one (entry -> counts on the host), median of reps;
@@ -40,6 +42,10 @@ PAPER_GPU = {
     ("min_unique", 10000000): 2190, ("min_single", 10000000): 10525,
     ("max_unique", 10000000): 2191, ("max_single", 10000000): 10584,
     ("num_unique", 10000000): 1184, ("num_single", 10000000): 1042,
+    ("str_equal_single", 10000000): 957, ("str_contain_single", 10000000): 2346,
+    ("str_equal_unique", 10000000): 1102, ("str_contain_unique", 10000000): 12551,
+    ("str_equal_single", 1000000): 126, ("str_contain_single", 1000000): 287,
+    ("str_equal_unique", 1000000): 134, ("str_contain_unique", 1000000): 1459,
 }
 
 
@@ -65,7 +71,7 @@ def measure(kb_np, tree, reps, check, bits=True):
     bits=False: counts only (root conjunctions run on example-projected rows)."""
     import torch
     k = hedl.hedl_kb_load(kb_np, 0)
-    nodes, kids, roots = flatten([tree])
+    nodes, kids, roots = flatten([tree])      # nodes carry the string-pattern table
     prog = hedl.hedl_compile(k, nodes, kids, roots)
     for _ in range(3):
         hedl.hedl_eval_one(k, prog, 0, want_bits=bits)
@@ -113,14 +119,23 @@ def main():
                      "paper_gtx970_us": None})
     for n in [s for s in sizes if s >= 10]:                   # Tables 4 / card / 8: the two regimes
         for regime in ("unique", "single"):
-            kb = abox.regime_kb(regime, n, seed=n)
+            kb = abox.string_regime_kb(regime, n, seed=n)
             cases = [("exists", ("EXISTS", 0, False, A(0))), ("forall", ("FORALL", 0, False, A(0))),
                      ("min", ("MIN", 3, 0, False, A(0))), ("max", ("MAX", 3, 0, False, A(0))),
-                     ("num", ("DRANGE", 0, 1.0, np.inf))]
+                     ("num", ("DRANGE", 0, 1.0, np.inf)),
+                     ("str_equal", ("SEQUAL", 0, b"fixed string value")),
+                     ("str_contain", ("SCONTAIN", 0, b"string"))]
             for name, tree in cases:
                 lat, ker, ok = measure(kb, tree, 20, n <= 1_000_000)
                 rows.append({"op": f"{name}_{regime}", "size": n, "latency_us": lat, "kernel_us": ker, "parity": ok,
                              "paper_gtx970_us": PAPER_GPU.get((f"{name}_{regime}", n))})
+        for regime in ("unique", "single"):                    # distinct values: nothing to intern away
+            kb = abox.string_regime_kb(regime, n, seed=n, distinct=True)
+            for name, tree in (("str_equal", ("SEQUAL", 0, b"fixed string value0000000007")),
+                               ("str_contain", ("SCONTAIN", 0, b"value00000007"))):
+                lat, ker, ok = measure(kb, tree, 20, n <= 1_000_000)
+                rows.append({"op": f"{name}_{regime}_distinct", "size": n, "latency_us": lat, "kernel_us": ker,
+                             "parity": ok, "paper_gtx970_us": None})
     json.dump(rows, open(out_path, "w"), indent=1)
     print("| op | size | our eval_one latency us | our kernel us | parity | paper GTX 970 us |")
     print("|---|---|---|---|---|---|")
