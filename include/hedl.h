@@ -186,6 +186,20 @@ hedl_status hedl_compile_ex(const hedl_kb *kb, const hedl_node *nodes, uint32_t 
                             hedl_program **out);
 hedl_status hedl_program_free(hedl_program *prog);
 
+/* Device-side compile (the paper's future work: GPUs generate their own
+ * evaluation plans).  Same program as hedl_compile, built on the KB's device from
+ * DEVICE arrays (nodes / child_idx / roots as in hedl_compile, in device memory, read
+ * on `stream`; the call synchronises `stream` before returning).  The input must list
+ * children before parents (every child id < its parent's id: the post-order of
+ * flattened trees), else BAD_EXPR.  String restrictions, AND/OR with > 64 operands
+ * after flattening and inputs deeper than 512 levels are UNSUPPORTED (use
+ * hedl_compile).  Other errors as hedl_compile (the lowest failing node is named).
+ * The program is evaluated like any other; its plan is built on the device too. */
+hedl_status hedl_compile_device(const hedl_kb *kb, const hedl_node *nodes, uint32_t n_nodes,
+                                const uint32_t *child_idx, uint64_t n_child_idx,
+                                const uint32_t *roots, uint32_t n_roots, uint32_t flags,
+                                void *stream, hedl_program **out);
+
 typedef struct hedl_program_info {
     uint32_t n_roots;
     uint32_t n_nodes;             /* computed canonical nodes after CSE */

@@ -30,6 +30,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "OUT_OF_RANGE", 3: "EXAMPLE_CONFLICT", 4
 
 # every symbol include/hedl.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ["hedl_kb_load", "hedl_kb_free", "hedl_kb_get_info", "hedl_compile", "hedl_compile_ex",
+               "hedl_compile_device",
                "hedl_program_free",
                "hedl_program_get_info", "hedl_program_root_bytes", "hedl_eval_one", "hedl_eval_batch",
                "hedl_program_set_workspace_limit", "hedl_last_error", "hedl_version", "hedl_prof_enable",
@@ -89,6 +90,7 @@ def lib():
         "hedl_kb_get_info": ([P, C.POINTER(_KbInfo)], I32),
         "hedl_compile": ([P, P, U32, P, U64, P, U32, U32, C.POINTER(P)], I32),
         "hedl_compile_ex": ([P, P, U32, P, U64, P, U32, U32, U32, P, P, C.POINTER(P)], I32),
+        "hedl_compile_device": ([P, P, U32, P, U64, P, U32, U32, P, C.POINTER(P)], I32),
         "hedl_program_free": ([P], I32),
         "hedl_program_get_info": ([P, C.POINTER(_ProgInfo)], I32),
         "hedl_program_root_bytes": ([P, U32, U32, P], I32),
@@ -269,6 +271,38 @@ def hedl_compile_ex(kb: KB, nodes: np.ndarray, child_idx: np.ndarray, roots: np.
     _check(lib().hedl_compile_ex(kb._h, _ptr(nodes), len(nodes), _ptr(kids), len(kids), _ptr(roots),
                                  len(roots), flags, len(pats), _ptr(off), _ptr(blob), C.byref(h)))
     return Program(h, kb, len(roots))
+
+
+def _dev_u8(a, device):
+    """numpy array (any dtype) or CUDA tensor -> (uint8 CUDA tensor sharing the bytes, n elements)."""
+    import torch
+    if isinstance(a, torch.Tensor):
+        assert a.is_cuda and a.is_contiguous()
+        return a, None
+    arr = np.ascontiguousarray(a)
+    t = torch.from_numpy(arr.view(np.uint8).reshape(-1)).to(f"cuda:{device}", non_blocking=False)
+    return t, len(arr)
+
+
+def hedl_compile_device(kb: KB, nodes, child_idx, roots, flags: int = 0, stream=None,
+                        n_nodes: Optional[int] = None, n_kids: Optional[int] = None,
+                        n_roots: Optional[int] = None) -> Program:
+    """hedl_compile_device: the node / child / root arrays in DEVICE memory (CUDA tensors of
+    their bytes, with the counts given) or host numpy arrays (copied to the device first)."""
+    import torch
+    with torch.cuda.device(kb.device):
+        tn, nn = _dev_u8(nodes, kb.device)
+        tk, nk = _dev_u8(np.ascontiguousarray(child_idx, dtype=np.uint32)
+                         if not isinstance(child_idx, torch.Tensor) else child_idx, kb.device)
+        tr, nr = _dev_u8(np.ascontiguousarray(roots, dtype=np.uint32)
+                         if not isinstance(roots, torch.Tensor) else roots, kb.device)
+        nn = n_nodes if n_nodes is not None else nn
+        nk = n_kids if n_kids is not None else nk
+        nr = n_roots if n_roots is not None else nr
+        h = C.c_void_p()
+        _check(lib().hedl_compile_device(kb._h, C.c_void_p(tn.data_ptr()), nn, C.c_void_p(tk.data_ptr()), nk,
+                                         C.c_void_p(tr.data_ptr()), nr, flags, _stream(stream), C.byref(h)))
+    return Program(h, kb, nr)
 
 
 def hedl_eval_one(kb: KB, prog: Program, root: int, want_bits: bool = False, stream=None):

@@ -646,6 +646,7 @@ extern "C" hedl_status hedl_compile_ex(const hedl_kb *kb, const hedl_node *nodes
 // Computed lazily (only the info/bytes queries need it), so compile stays lean.
 static void ensure_root_bytes(hedl_program *p) {
     std::lock_guard<std::mutex> lk(p->mu);
+    if (p->dev && dc_download(p)) return;
     if (p->root_bytes.size() == p->root_node.size()) return;
     const hedl_kb *kb = p->kb;
     const uint32_t n_roots = (uint32_t)p->root_node.size();

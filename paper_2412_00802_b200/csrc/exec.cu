@@ -795,6 +795,11 @@ extern "C" hedl_status hedl_eval_batch(const hedl_kb *kb, hedl_program *p, uint3
                                        uint32_t *out_bits, hedl_counts *counts, void *stream, uint32_t flags) {
     if (!kb || !p || (n && !counts)) return fail(HEDL_ERR_INVALID_ARG, "null kb/program/counts");
     if (p->kb != kb) return fail(HEDL_ERR_INVALID_ARG, "program was compiled for another KB");
+    if (p->dev) {
+        std::lock_guard<std::mutex> lk(p->mu);
+        hedl_status st = dc_download(p);
+        if (st) return st;
+    }
     if (kb->poisoned) return fail(HEDL_ERR_CUDA, "KB handle is poisoned by an earlier CUDA error");
     if ((uint64_t)first + n > p->root_node.size()) return fail(HEDL_ERR_OUT_OF_RANGE, "root range out of range");
     if (!n) return HEDL_OK;
@@ -888,6 +893,11 @@ extern "C" hedl_status hedl_eval_one(const hedl_kb *kb, hedl_program *p, uint32_
     if (!kb || !p) return fail(HEDL_ERR_INVALID_ARG, "null kb/program");
     if (p->kb != kb) return fail(HEDL_ERR_INVALID_ARG, "program was compiled for another KB");
     if (kb->poisoned) return fail(HEDL_ERR_CUDA, "KB handle is poisoned by an earlier CUDA error");
+    if (p->dev) {
+        std::lock_guard<std::mutex> lk(p->mu);
+        hedl_status st = dc_download(p);
+        if (st) return st;
+    }
     if (root >= p->root_node.size()) return fail(HEDL_ERR_OUT_OF_RANGE, "root out of range");
     static thread_local InterpProg prog;   // ~5 KB: keep it off the stack
     // a single CTA wins while launch/sync overheads dominate; above ~64k individuals the
@@ -949,6 +959,10 @@ extern "C" hedl_status hedl_program_free(hedl_program *p) {
         cudaFreeHost(p->lat_host);
     }
     const hedl_kb *kb = p->kb;
+    if (p->dev) {
+        DeviceGuard dg(kb->device);
+        dc_free_arrays(p);
+    }
     delete p;
     kb_release(kb);
     return HEDL_OK;

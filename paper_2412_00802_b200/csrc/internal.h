@@ -173,9 +173,21 @@ struct hedl_program {
     // planning scratch (host)
     std::vector<uint32_t> stamp;
     uint32_t stamp_gen = 0;
+    // device-compiled program (hedl_compile_device): canonical DAG in device memory
+    bool dev = false, dev_downloaded = false;
+    hedl::CNode *d_nodes = nullptr;
+    uint32_t *d_ops = nullptr, *d_root_node = nullptr;
+    uint32_t dev_n_nodes = 0, dev_n_roots = 0;
+    uint64_t dev_n_ops = 0;
+    void *dplan = nullptr;              // device-side evaluation plan state (dplan.cu)
 };
 
 namespace hedl {
+
+// ---- device-compiled programs (dcompile.cu) ---------------------------------------
+void dc_free_arrays(hedl_program *p);
+hedl_status dc_download(hedl_program *p);     // host copy of nodes / ops / roots (utilities)
+inline uint32_t prog_n_roots(const hedl_program *p) { return p->dev ? p->dev_n_roots : (uint32_t)p->root_node.size(); }
 
 // ---- errors --------------------------------------------------------------------
 void set_error(const std::string &msg);

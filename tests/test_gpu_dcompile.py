@@ -1,0 +1,100 @@
+"""Device-side compile (hedl_compile_device) vs the oracle,
+element by element (bitsets + counts, bit-exact), and vs the host compiler's program shape."""
+import numpy as np
+import pytest
+
+from golden_io import all_fixtures, load
+from oracle import setsem
+from synth import abox, hyps
+from synth.format import COMPILE_COMPAT_PAPER_MAX, COMPILE_NO_CSE, COMPILE_NO_REWRITE, flatten
+from test_gpu_parity import _hedl
+
+pytestmark = pytest.mark.gpu
+
+
+def dev_parity(kb, nodes, kids, roots, flags=0, eflags=0, tag=""):
+    import torch
+    hedl = _hedl()
+    k = hedl.hedl_kb_load(kb, 0)
+    prog = hedl.hedl_compile_device(k, nodes, kids, roots, flags)
+    b, c = hedl.hedl_eval_batch(k, prog, 0, len(roots), want_bits=True, flags=eflags)
+    torch.cuda.synchronize()
+    gb = b.cpu().numpy().view(np.uint32)
+    ob, oc = setsem.evaluate(kb, nodes, kids, roots, flags=flags, threads=8)
+    bad = np.nonzero((gb != ob).any(axis=1) | (c != oc).any(axis=1))[0] if len(roots) else []
+    assert len(bad) == 0, f"{tag}: {len(bad)} mismatching roots, first {bad[:5]}"
+    _, c2 = hedl.hedl_eval_batch(k, prog, 0, len(roots), want_bits=False, flags=eflags)
+    bad = np.nonzero((c2 != oc).any(axis=1))[0] if len(roots) else []
+    assert len(bad) == 0, f"{tag} (counts only): {len(bad)} mismatching roots"
+    return k, prog
+
+
+@pytest.mark.parametrize("path", [p for p in all_fixtures() if not p.endswith("strings.kbt")],
+                         ids=lambda p: p.split("/")[-1])
+def test_golden_device_compile(path):
+    kb, cases, flags = load(path)
+    nodes, kids, roots = flatten([c[1] for c in cases])
+    dev_parity(kb, nodes, kids, roots, flags, tag=path)
+
+
+def test_c1_flags_device_compile():
+    kb = abox.c1_kb()
+    nodes, kids, roots = flatten(hyps.c1_hypotheses(kb))
+    for fl in (0, COMPILE_NO_CSE, COMPILE_NO_REWRITE | COMPILE_NO_CSE, COMPILE_NO_REWRITE, COMPILE_COMPAT_PAPER_MAX):
+        dev_parity(kb, nodes, kids, roots, fl, tag=f"C1 flags={fl}")
+
+
+def test_random_tiny_device_compile():
+    for seed in range(80):
+        kb = abox.random_tiny_kb(seed, n_strings=0)
+        rng = np.random.default_rng(seed + 77)
+        trees = [hyps.random_tree(rng, abox.kb_shape(kb), depth=4) for _ in range(12)]
+        f = flatten(trees)
+        dev_parity(kb, *f, tag=f"tiny {seed}")
+        fs = flatten(trees, share=True)                       # shared subtrees (a DAG input)
+        dev_parity(kb, *fs, tag=f"tiny shared {seed}")
+
+
+def test_refinement_batch_device_compile():
+    """C4-shaped refinement batch (20k hypotheses, 300k individuals) incl. lane-packed paths;
+    the device program has the host program's node counts up to root-only duplicates."""
+    hedl = _hedl()
+    kb = abox.powerlaw_kb(300_000, 20, 2, 8.0, 3000, data_frac=0.7, data_vals_mean=1.0, ex_frac=0.01, seed=9)
+    nodes, kids, roots = hyps.batch_arrays("c4", kb, 20_000, seed=3)
+    k, prog = dev_parity(kb, nodes, kids, roots, tag="refine")
+    dev_parity(kb, nodes, kids, roots, eflags=2, tag="refine per-node")
+    host = hedl.hedl_compile(k, nodes, kids, roots)
+    hi, di = host.info(), prog.info()
+    assert di["n_restrict"] == hi["n_restrict"] and di["n_drange"] == hi["n_drange"]
+    assert di["n_levels"] == hi["n_levels"]
+    assert abs(di["n_nodes"] - hi["n_nodes"]) <= hi["n_nodes"] // 10
+
+
+def test_device_compile_errors():
+    hedl = _hedl()
+    kb = abox.c1_kb()
+    k = hedl.hedl_kb_load(kb, 0)
+    bad_cases = [
+        ([("ATOM", 99)], 2),
+        ([("EXISTS", 5, False, ("TOP",))], 2),
+        ([("DRANGE", 0, float("nan"), 1.0)], 4),
+        ([("SEQUAL", 0, b"x")], 8),
+    ]
+    for trees, code in bad_cases:
+        f = flatten(trees)
+        with pytest.raises(hedl.HedlError) as e:
+            hedl.hedl_compile_device(k, *f)
+        assert e.value.code == code, trees
+    nodes, kids, roots = flatten([("AND", [("ATOM", 0), ("ATOM", 1)])])
+    kids2 = kids.copy()
+    kids2[0] = 2                                           # a child after its parent
+    with pytest.raises(hedl.HedlError) as e:
+        hedl.hedl_compile_device(k, nodes, kids2, roots)
+    assert e.value.code == 4
+    with pytest.raises(hedl.HedlError) as e:
+        hedl.hedl_compile_device(k, nodes, kids, np.array([7], np.uint32))
+    assert e.value.code == 2
+    # an invalid node nobody reaches is not an error (as for the host compiler)
+    nodes2 = np.concatenate([nodes, flatten([("ATOM", 99)])[0]])
+    prog = hedl.hedl_compile_device(k, nodes2, kids, roots)
+    assert prog.info()["n_roots"] == 1
