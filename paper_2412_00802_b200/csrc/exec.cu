@@ -15,59 +15,13 @@
 #include <atomic>
 #include <thread>
 
-#include "internal.h"
+#include "exec.h"
 #include "interp.h"
 #include "slice.h"
 
 using namespace hedl;
 
-namespace {
-
-struct DevBuf {
-    void *p = nullptr;
-    size_t bytes = 0;
-};
-
-struct LaunchRec {
-    uint8_t kind;          // NK_AND (AND+OR), NK_RESTRICT, NK_DRANGE, NK_STRING
-    uint16_t key;          // dir / prop
-    bool slice;
-    bool proj;             // boolean group evaluated on example-projected rows
-    bool ex;               // restriction pack evaluated on example rows only
-    uint32_t count, first_desc;
-    double bytes, bytes2;
-};
-
-struct ChunkPlan {
-    uint32_t ri, rc;       // roots [ri, rc) relative to the program
-    uint32_t nn, ncov, nrows, nprows;
-    size_t blob_off, blob_bytes;          // into PlanCache host/device blobs
-    size_t off_bool, off_ops, off_res, off_dr, off_str, off_cov, off_rows;
-    std::vector<LaunchRec> recs;
-};
-
-struct PlanCache {
-    bool valid = false;
-    uint32_t r0 = 0, r1 = 0, eflags = 0;
-    bool bits = false;
-    void *rows_base = nullptr, *heavy_base = nullptr, *prows_base = nullptr;
-    std::vector<ChunkPlan> chunks;
-    void *host = nullptr;                 // pinned descriptor blob
-    void *dev = nullptr;                  // device descriptor blob
-    size_t cap = 0;                       // capacity of both blobs
-};
-
-struct Workspace {
-    DevBuf rows, prows, heavy, counts, slice, stage;
-    uint8_t *pats = nullptr;             // device copy of the program's CONTAIN patterns
-    std::vector<uint64_t> pat_off;       // their offsets
-    hedl_counts *stage_host = nullptr;   // pinned staging of host-bound counts
-    size_t stage_host_n = 0;
-    PlanCache plan;
-    cudaEvent_t done = nullptr;
-    cudaStream_t last_stream = nullptr;
-    bool used = false;
-};
+namespace hedl {
 
 Workspace *ws_of(hedl_program *p) {
     if (!p->ws) p->ws = new Workspace();
@@ -139,7 +93,10 @@ hedl_status reserve_plan(const hedl_kb *kb, PlanCache &pc, size_t bytes) {
     return HEDL_OK;
 }
 
-inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+}  // namespace hedl
+
+namespace {
+
 
 struct Group {
     uint8_t kind;
@@ -634,6 +591,10 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
     }
 }
 
+}  // namespace
+
+namespace hedl {
+
 // Phase D: the launches of one chunk.
 hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, uint32_t r0, uint32_t *out_bits,
                          hedl_counts *counts_dev, cudaStream_t s) {
@@ -655,8 +616,8 @@ hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, u
             const RestrictDesc *dd_desc = (const RestrictDesc *)(d + cp.off_res) + lr.first_desc;
             if (lr.slice) {
                 hedl_status st = slice_run(kb, &w->slice.p, &w->slice.bytes, s, kd, lr.key,
-                                           (const RestrictDesc *)(h + cp.off_res) + lr.first_desc, dd_desc, lr.count, cov,
-                                           lr.ex);
+                                           lr.cls >= 0 ? nullptr : (const RestrictDesc *)(h + cp.off_res) + lr.first_desc,
+                                           dd_desc, lr.count, cov, lr.ex, lr.cls);
                 if (st) return st;
             } else {
                 DirDev dd{dr.row_ptr, dr.col, dr.heavy_x, dr.heavy_nchunks, dr.chunks, dr.n_heavy, dr.n_chunks,
@@ -680,6 +641,10 @@ hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, u
     HEDL_CUDA(kb, cudaGetLastError());
     return HEDL_OK;
 }
+
+}  // namespace hedl
+
+namespace {
 
 // Evaluate roots [r0, r1) of the program.  counts_dev: device hedl_counts[r1-r0];
 // out_bits: device [r1-r0][W] or null.
@@ -795,13 +760,8 @@ extern "C" hedl_status hedl_eval_batch(const hedl_kb *kb, hedl_program *p, uint3
                                        uint32_t *out_bits, hedl_counts *counts, void *stream, uint32_t flags) {
     if (!kb || !p || (n && !counts)) return fail(HEDL_ERR_INVALID_ARG, "null kb/program/counts");
     if (p->kb != kb) return fail(HEDL_ERR_INVALID_ARG, "program was compiled for another KB");
-    if (p->dev) {
-        std::lock_guard<std::mutex> lk(p->mu);
-        hedl_status st = dc_download(p);
-        if (st) return st;
-    }
     if (kb->poisoned) return fail(HEDL_ERR_CUDA, "KB handle is poisoned by an earlier CUDA error");
-    if ((uint64_t)first + n > p->root_node.size()) return fail(HEDL_ERR_OUT_OF_RANGE, "root range out of range");
+    if ((uint64_t)first + n > prog_n_roots(p)) return fail(HEDL_ERR_OUT_OF_RANGE, "root range out of range");
     if (!n) return HEDL_OK;
     std::lock_guard<std::mutex> lk(p->mu);
     DeviceGuard dg(kb->device);
@@ -824,7 +784,16 @@ extern "C" hedl_status hedl_eval_batch(const hedl_kb *kb, hedl_program *p, uint3
                 cudaGetLastError();
         }
     }
-    hedl_status st = run(kb, p, first, first + n, out_bits, dcounts, s, flags & ~HEDL_EVAL_COUNTS_DEVICE);
+    const uint32_t ef = flags & ~HEDL_EVAL_COUNTS_DEVICE;
+    hedl_status st;
+    if (p->dev && !p->dev_downloaded) {
+        // device-compiled program: plan on the device; a batch that needs several chunks
+        // goes to the host planner (one download of the program)
+        st = dplan_run(kb, p, first, first + n, out_bits, dcounts, s, ef);
+        if (st == HEDL_ERR_UNSUPPORTED && !(st = dc_download(p))) st = run(kb, p, first, first + n, out_bits, dcounts, s, ef);
+    } else {
+        st = run(kb, p, first, first + n, out_bits, dcounts, s, ef);
+    }
     if (host_out && st == HEDL_OK) {
         const bool pinned = w->stage_host && w->stage_host_n >= n;
         cudaError_t e = cudaMemcpyAsync(pinned ? (void *)w->stage_host : (void *)counts, dcounts, cbytes,
@@ -893,16 +862,16 @@ extern "C" hedl_status hedl_eval_one(const hedl_kb *kb, hedl_program *p, uint32_
     if (!kb || !p) return fail(HEDL_ERR_INVALID_ARG, "null kb/program");
     if (p->kb != kb) return fail(HEDL_ERR_INVALID_ARG, "program was compiled for another KB");
     if (kb->poisoned) return fail(HEDL_ERR_CUDA, "KB handle is poisoned by an earlier CUDA error");
-    if (p->dev) {
-        std::lock_guard<std::mutex> lk(p->mu);
-        hedl_status st = dc_download(p);
-        if (st) return st;
-    }
-    if (root >= p->root_node.size()) return fail(HEDL_ERR_OUT_OF_RANGE, "root out of range");
+    if (root >= prog_n_roots(p)) return fail(HEDL_ERR_OUT_OF_RANGE, "root out of range");
     static thread_local InterpProg prog;   // ~5 KB: keep it off the stack
     // a single CTA wins while launch/sync overheads dominate; above ~64k individuals the
     // multi-CTA per-node kernels are faster (measured, tools/opbench.py)
     static const bool no_interp = std::getenv("HEDL_NO_INTERP") != nullptr;
+    if (p->dev && kb->N && kb->N <= kInterpMaxN && !no_interp) {   // the interpreter reads the host program
+        std::lock_guard<std::mutex> lk(p->mu);
+        hedl_status st = dc_download(p);
+        if (st) return st;
+    }
     if (kb->N && kb->N <= kInterpMaxN && !no_interp && build_interp(kb, p, p->root_node[root], prog)) {
         std::lock_guard<std::mutex> lk(p->mu);
         DeviceGuard dg(kb->device);
@@ -961,6 +930,7 @@ extern "C" hedl_status hedl_program_free(hedl_program *p) {
     const hedl_kb *kb = p->kb;
     if (p->dev) {
         DeviceGuard dg(kb->device);
+        dplan_free(p);
         dc_free_arrays(p);
     }
     delete p;

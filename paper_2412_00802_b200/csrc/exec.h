@@ -1,0 +1,68 @@
+// Executor internals shared by the host planner (exec.cu) and the device planner (dplan.cu).
+#pragma once
+#include "internal.h"
+
+namespace hedl {
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+
+struct LaunchRec {
+    uint8_t kind;          // NK_AND (AND+OR), NK_RESTRICT, NK_DRANGE, NK_STRING
+    uint16_t key;          // dir / prop
+    bool slice;
+    bool proj;             // boolean group evaluated on example-projected rows
+    bool ex;               // restriction pack evaluated on example rows only
+    uint32_t count, first_desc;
+    double bytes, bytes2;
+    int8_t cls = -1;       // lane-pack class of the whole group (device plans), -1 = per descriptor
+};
+
+struct ChunkPlan {
+    uint32_t ri, rc;       // roots [ri, rc) relative to the program
+    uint32_t nn, ncov, nrows, nprows;
+    size_t blob_off, blob_bytes;          // into PlanCache host/device blobs
+    size_t off_bool, off_ops, off_res, off_dr, off_str, off_cov, off_rows;
+    std::vector<LaunchRec> recs;
+};
+
+struct PlanCache {
+    bool valid = false;
+    uint32_t r0 = 0, r1 = 0, eflags = 0;
+    bool bits = false;
+    void *rows_base = nullptr, *heavy_base = nullptr, *prows_base = nullptr;
+    std::vector<ChunkPlan> chunks;
+    void *host = nullptr;                 // pinned descriptor blob
+    void *dev = nullptr;                  // device descriptor blob
+    size_t cap = 0;                       // capacity of both blobs
+};
+
+struct Workspace {
+    DevBuf rows, prows, heavy, counts, slice, stage;
+    uint8_t *pats = nullptr;             // device copy of the program's CONTAIN patterns
+    std::vector<uint64_t> pat_off;       // their offsets
+    hedl_counts *stage_host = nullptr;   // pinned staging of host-bound counts
+    size_t stage_host_n = 0;
+    PlanCache plan;
+    cudaEvent_t done = nullptr;
+    cudaStream_t last_stream = nullptr;
+    bool used = false;
+};
+
+Workspace *ws_of(hedl_program *p);
+hedl_status grow(const hedl_kb *kb, cudaStream_t s, DevBuf &b, size_t need, bool zero, int role);
+void invalidate_plan(PlanCache &pc);
+void release_plan(PlanCache &pc);
+hedl_status reserve_plan(const hedl_kb *kb, PlanCache &pc, size_t bytes);
+hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, uint32_t r0, uint32_t *out_bits,
+                         hedl_counts *counts_dev, cudaStream_t s);
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+// device planner (dplan.cu): builds and launches the plan of a device-compiled program on
+// the device; HEDL_ERR_UNSUPPORTED = the batch does not fit one chunk (host planner then)
+hedl_status dplan_run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, uint32_t *out_bits,
+                      hedl_counts *counts_dev, cudaStream_t s, uint32_t eflags);
+void dplan_free(hedl_program *p);
+
+}  // namespace hedl

@@ -576,7 +576,8 @@ uint32_t slice_class(uint32_t pred, uint32_t n, uint32_t sat) {
 }
 
 hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream_t s, const KbDev &kd, uint32_t dirid,
-                      const RestrictDesc *h_desc, const RestrictDesc *d_desc, uint32_t n, hedl_counts *counts, bool ex) {
+                      const RestrictDesc *h_desc, const RestrictDesc *d_desc, uint32_t n, hedl_counts *counts, bool ex,
+                      int fixed_cls) {
     const hedl_dir &dr = kb->dirs[dirid];
     if (ex && !kb->M) return HEDL_OK;                     // no examples: nothing to evaluate
     const size_t t_bytes = (size_t)kb->W4 * 32 * 32;
@@ -642,12 +643,14 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
     for (uint32_t off = 0; off < n;) {
         // a run of consecutive same-class descriptors: full packs go one pack per launch
         // (T stays L2-resident for the tile sweep); EX packs go up to max_batch per launch
-        const uint32_t cls = slice_class(h_desc[off].pred, h_desc[off].n, h_desc[off].sat);
+        const uint32_t cls = fixed_cls >= 0 ? (uint32_t)fixed_cls : slice_class(h_desc[off].pred, h_desc[off].n, h_desc[off].sat);
         const uint32_t cap = ex ? 256u * max_batch : 256u;
         uint32_t run = 1;
-        while (off + run < n && run < cap &&
-               slice_class(h_desc[off + run].pred, h_desc[off + run].n, h_desc[off + run].sat) == cls)
-            ++run;
+        if (fixed_cls >= 0) run = std::min(n - off, cap);
+        else
+            while (off + run < n && run < cap &&
+                   slice_class(h_desc[off + run].pred, h_desc[off + run].n, h_desc[off + run].sat) == cls)
+                ++run;
         const uint32_t packs = (run + 255) / 256;
         const RestrictDesc *dd = d_desc + off;
         SliceScratch sc = ex ? scratch(off_hx, nhx, max_batch) : scratch(off_hf, nh, 1);

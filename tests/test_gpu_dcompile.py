@@ -98,3 +98,28 @@ def test_device_compile_errors():
     nodes2 = np.concatenate([nodes, flatten([("ATOM", 99)])[0]])
     prog = hedl.hedl_compile_device(k, nodes2, kids, roots)
     assert prog.info()["n_roots"] == 1
+
+
+def test_device_plan_subranges_and_fallback():
+    """Device plans for sub-ranges of the roots, eval_one above the interpreter's size, and the
+    host-planner fallback when the batch needs several chunks (tiny workspace limit)."""
+    import torch
+    hedl = _hedl()
+    kb = abox.powerlaw_kb(120_000, 12, 2, 6.0, 2000, data_frac=0.5, data_vals_mean=1.2, ex_frac=0.02, seed=5)
+    nodes, kids, roots = hyps.batch_arrays("c4", kb, 3000, seed=8)
+    ob, oc = setsem.evaluate(kb, nodes, kids, roots, threads=8)
+    k = hedl.hedl_kb_load(kb, 0)
+    prog = hedl.hedl_compile_device(k, nodes, kids, roots)
+    for a, b in ((0, 1), (5, 700), (2999, 3000), (100, 3000)):
+        bits, c = hedl.hedl_eval_batch(k, prog, a, b - a, want_bits=True)
+        assert np.array_equal(bits.cpu().numpy().view(np.uint32), ob[a:b]) and np.array_equal(c, oc[a:b]), (a, b)
+        _, c = hedl.hedl_eval_batch(k, prog, a, b - a, want_bits=False)
+        assert np.array_equal(c, oc[a:b]), (a, b)
+    for i in (0, 17, 2999):
+        b1, c1 = hedl.hedl_eval_one(k, prog, i, want_bits=True)
+        assert np.array_equal(b1.cpu().numpy().view(np.uint32), ob[i]) and c1 == tuple(int(v) for v in oc[i])
+    p2 = hedl.hedl_compile_device(k, nodes, kids, roots)
+    p2.set_workspace_limit(1 << 20)                      # 1 MiB: many chunks -> host planner
+    bits, c = hedl.hedl_eval_batch(k, p2, 0, 3000, want_bits=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits.cpu().numpy().view(np.uint32), ob) and np.array_equal(c, oc)
