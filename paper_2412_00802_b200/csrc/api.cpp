@@ -49,7 +49,7 @@ void *pool_take(const hedl_kb *kb, int role, size_t need, size_t *got) {
 }
 
 static void pool_free_one(int role, void *p) {
-    if (role == PR_PLAN_HOST) cudaFreeHost(p);
+    if (role == PR_PLAN_HOST || role == PR_DPLAN_HOST) cudaFreeHost(p);
     else cudaFree(p);
 }
 

@@ -105,34 +105,58 @@ __device__ bool d_same(const CNode &a, const uint32_t *aops, const CNode &b, con
 __global__ void k_dc_level(const hedl_node *__restrict__ nodes, uint32_t n, const uint32_t *__restrict__ kids,
                            uint64_t n_kids, uint32_t *lvl, uint8_t *bad, DcCounters *cnt) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const hedl_node nd = nodes[i];
-    uint32_t L = 0;
-    uint8_t b = 0;
-    if ((uint64_t)nd.child_begin + nd.child_count > n_kids) {
-        b = DE_CHILD_RANGE;
-    } else {
-        for (uint32_t k = 0; k < nd.child_count; ++k) {
-            const uint32_t c = kids[nd.child_begin + k];
-            if (c >= i) { b = c >= n ? DE_CHILD_RANGE : DE_CHILD_ORDER; break; }
-            L = max(L, ((volatile uint32_t *)lvl)[c] + 1);
+    bool changed = false;
+    if (i < n) {
+        const hedl_node nd = nodes[i];
+        uint32_t L = 0;
+        uint8_t b = 0;
+        if ((uint64_t)nd.child_begin + nd.child_count > n_kids) {
+            b = DE_CHILD_RANGE;
+        } else {
+            for (uint32_t k = 0; k < nd.child_count; ++k) {
+                const uint32_t c = kids[nd.child_begin + k];
+                if (c >= i) { b = c >= n ? DE_CHILD_RANGE : DE_CHILD_ORDER; break; }
+                L = max(L, ((volatile uint32_t *)lvl)[c] + 1);
+            }
+        }
+        if (b) { bad[i] = b; L = 0; }
+        if (L != lvl[i]) {
+            lvl[i] = L;
+            changed = true;
         }
     }
-    if (b) { bad[i] = b; L = 0; }
-    if (L != lvl[i]) {
-        lvl[i] = L;
-        cnt->changed = 1;
+    if (__any_sync(0xffffffffu, changed) && (threadIdx.x & 31) == 0) cnt->changed = 1;
+}
+
+// level histogram and scatter with block-level aggregation (few distinct levels: global
+// atomics on one counter per level would serialise millions of updates)
+__global__ void __launch_bounds__(1024) k_dc_hist(const uint32_t *__restrict__ lvl, uint32_t n, uint32_t *hist,
+                                                  uint32_t nkeys) {
+    extern __shared__ uint32_t sh[];
+    for (uint32_t k = threadIdx.x; k < nkeys; k += blockDim.x) sh[k] = 0;
+    __syncthreads();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) atomicAdd(sh + lvl[i], 1u);
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < nkeys; k += blockDim.x)
+        if (sh[k]) atomicAdd(hist + k, sh[k]);
+}
+
+__global__ void __launch_bounds__(1024) k_dc_scatter(const uint32_t *__restrict__ lvl, uint32_t n, uint32_t *cursor,
+                                                     uint32_t *list, uint32_t nkeys) {
+    extern __shared__ uint32_t sh[];          // [nkeys] local counts, then [nkeys] global bases
+    for (uint32_t k = threadIdx.x; k < 2 * nkeys; k += blockDim.x) sh[k] = 0;
+    __syncthreads();
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t key = 0, r = 0;
+    if (i < n) {
+        key = lvl[i];
+        r = atomicAdd(sh + key, 1u);
     }
-}
-
-__global__ void k_dc_hist(const uint32_t *__restrict__ lvl, uint32_t n, uint32_t *hist) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) atomicAdd(hist + lvl[i], 1u);
-}
-
-__global__ void k_dc_scatter(const uint32_t *__restrict__ lvl, uint32_t n, uint32_t *cursor, uint32_t *list) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) list[atomicAdd(cursor + lvl[i], 1u)] = i;
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < nkeys; k += blockDim.x)
+        if (sh[k]) sh[nkeys + k] = atomicAdd(cursor + k, sh[k]);
+    __syncthreads();
+    if (i < n) list[sh[nkeys + key] + r] = i;
 }
 
 // ---- 2. reachability ------------------------------------------------------------------
@@ -207,26 +231,43 @@ __device__ double d_node_bytes(const DcKb &kb, const CNode &n) {
 }
 
 __device__ uint32_t d_materialise(const DcOut &o, const DcKb &kb, CNode n, const uint32_t *ops, uint64_t node_err) {
-    const uint32_t id = atomicAdd(&o.cnt->n_nodes, 1u);
-    const unsigned long long ob = atomicAdd(&o.cnt->n_ops, (unsigned long long)n.op_count);
-    if (id >= o.node_cap || ob + n.op_count > o.ops_cap) {
-        dc_error(o.cnt, node_err, DE_OPS_CAP);
-        return 0xffffffffu;
-    }
     uint32_t lvl = 0;
     bool has_node = false;
-    for (uint32_t q = 0; q < n.op_count; ++q) {
-        o.ops[ob + q] = ops[q];
+    for (uint32_t q = 0; q < n.op_count; ++q)
         if (((ops[q] >> 1) & 3u) == RT_NODE) {
             has_node = true;
             lvl = max(lvl, o.nodes[ops[q] >> 3].level);
         }
-    }
-    n.op_begin = (uint32_t)ob;
     n.level = has_node ? lvl + 1 : 0;
+    // id, operand slots and the level maximum for every lane materialising now: one
+    // atomic each per warp (millions of same-address atomics would serialise in L2)
+    const uint32_t m = __activemask(), lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    const uint32_t below = m & ((1u << lane) - 1u);
+    uint32_t opre = 0, otot = 0;
+    for (uint32_t mm = m; mm; mm &= mm - 1) {
+        const uint32_t l = __ffs(mm) - 1;
+        const uint32_t c = __shfl_sync(m, n.op_count, l);
+        if (below & (1u << l)) opre += c;
+        otot += c;
+    }
+    const uint32_t lmax = __reduce_max_sync(m, n.level);
+    uint32_t idb = 0;
+    unsigned long long obb = 0;
+    if (lane == leader) {
+        idb = atomicAdd(&o.cnt->n_nodes, (uint32_t)__popc(m));
+        obb = atomicAdd(&o.cnt->n_ops, (unsigned long long)otot);
+        atomicMax(&o.cnt->max_level, lmax);
+    }
+    const uint32_t id = __shfl_sync(m, idb, leader) + __popc(below);
+    const unsigned long long ob = __shfl_sync(m, obb, leader) + opre;
+    if (id >= o.node_cap || ob + n.op_count > o.ops_cap) {
+        dc_error(o.cnt, node_err, DE_OPS_CAP);
+        return 0xffffffffu;
+    }
+    for (uint32_t q = 0; q < n.op_count; ++q) o.ops[ob + q] = ops[q];
+    n.op_begin = (uint32_t)ob;
     n.bytes = d_node_bytes(kb, n);
     o.nodes[id] = n;
-    atomicMax(&o.cnt->max_level, n.level);
     __threadfence();                 // content visible before the id is published
     return id;
 }
@@ -358,27 +399,36 @@ __global__ void k_dc_roots(const uint32_t *__restrict__ roots, uint32_t n_roots,
 
 inline uint32_t nblk(uint64_t n, uint32_t t) { return (uint32_t)((n + t - 1) / t); }
 
-struct DevMem {                      // scratch owned by one compile call
-    std::vector<void *> v;
-    ~DevMem() { for (void *p : v) cudaFree(p); }
-    template <class T> T *get(size_t n) {
-        void *p = nullptr;
-        if (cudaMalloc(&p, std::max<size_t>(n * sizeof(T), 16)) != cudaSuccess) { cudaGetLastError(); return nullptr; }
-        v.push_back(p);
-        return (T *)p;
-    }
-};
-
 }  // namespace
 
 void hedl::dc_free_arrays(hedl_program *p) {
-    if (p->d_nodes) cudaFree(p->d_nodes);
-    if (p->d_ops) cudaFree(p->d_ops);
-    if (p->d_root_node) cudaFree(p->d_root_node);
+    if (p->d_block) pool_give(p->kb, PR_DC_PROG, p->d_block, p->d_block_bytes);
+    p->d_block = nullptr;
+    p->d_block_bytes = 0;
     p->d_nodes = nullptr;
     p->d_ops = nullptr;
     p->d_root_node = nullptr;
 }
+
+namespace {
+// the program's three arrays in one pooled block
+bool dc_alloc_arrays(hedl_program *p, uint32_t node_cap, uint64_t ops_cap, uint32_t n_roots) {
+    Carver c;
+    c.take<CNode>(node_cap);
+    c.take<uint32_t>(ops_cap);
+    c.take<uint32_t>(std::max<uint32_t>(n_roots, 1));
+    size_t got = 0;
+    void *blk = pool_alloc(p->kb, PR_DC_PROG, c.off, &got);
+    if (!blk) return false;
+    p->d_block = blk;
+    p->d_block_bytes = got;
+    Carver d{(char *)blk, 0};
+    p->d_nodes = d.take<CNode>(node_cap);
+    p->d_ops = d.take<uint32_t>(ops_cap);
+    p->d_root_node = d.take<uint32_t>(std::max<uint32_t>(n_roots, 1));
+    return true;
+}
+}  // namespace
 
 extern "C" hedl_status hedl_compile_device(const hedl_kb *kb, const hedl_node *nodes, uint32_t n_nodes,
                                            const uint32_t *child_idx, uint64_t n_child_idx, const uint32_t *roots,
@@ -395,22 +445,50 @@ extern "C" hedl_status hedl_compile_device(const hedl_kb *kb, const hedl_node *n
     struct Restore { int d; ~Restore() { cudaSetDevice(d); } } restore{prev};
     const double t0 = now_ms();
     cudaStream_t s = (cudaStream_t)stream;
-    DevMem m;
     const uint32_t n = n_nodes;
-    uint32_t *lvl = m.get<uint32_t>(n), *hist = nullptr, *list = m.get<uint32_t>(n), *cref = m.get<uint32_t>(n);
-    uint8_t *bad = m.get<uint8_t>(n), *reach = m.get<uint8_t>(n);
-    DcCounters *cnt = m.get<DcCounters>(1);
-    double *kbytes = m.get<double>(2 * kb->R + kb->D + 1);
-    DcCounters *hc = nullptr;
-    if (!lvl || !list || !cref || !bad || !reach || !cnt || !kbytes) return fail(HEDL_ERR_OOM, "device compile scratch");
-    if (cudaMallocHost((void **)&hc, sizeof(DcCounters)) != cudaSuccess) { cudaGetLastError(); return fail(HEDL_ERR_OOM, "pinned"); }
-    struct FreeHost { void *p; ~FreeHost() { cudaFreeHost(p); } } fh{hc};
-    {
+    const uint32_t node_cap = n + n_roots + 1;
+    uint64_t tcap = 1024;
+    while (tcap < 2ull * node_cap) tcap <<= 1;
+    const bool cse = !(flags & HEDL_COMPILE_NO_CSE);
+    // scratch: one pooled block (no cudaMalloc / cudaFree per compile)
+    uint32_t *lvl, *list, *cref, *hist, *cursor, *table;
+    uint8_t *bad, *reach;
+    DcCounters *cnt;
+    double *kbytes;
+    size_t sgot = 0;
+    void *sblk = nullptr;
+    for (int pass = 0; pass < 2; ++pass) {
+        Carver c{(char *)sblk, 0};
+        lvl = c.take<uint32_t>(n);
+        list = c.take<uint32_t>(n);
+        cref = c.take<uint32_t>(n);
+        hist = c.take<uint32_t>(kDcMaxDepth + 3);
+        cursor = c.take<uint32_t>(kDcMaxDepth + 3);
+        table = c.take<uint32_t>(cse ? tcap : 1);
+        bad = c.take<uint8_t>(n);
+        reach = c.take<uint8_t>(n);
+        cnt = c.take<DcCounters>(1);
+        kbytes = c.take<double>(2 * kb->R + kb->D + 1);
+        if (pass == 0 && !(sblk = pool_alloc(kb, PR_DC_SCRATCH, c.off, &sgot))) return fail(HEDL_ERR_OOM, "device compile scratch");
+    }
+    struct GiveBack { const hedl_kb *kb; void *p; size_t b; ~GiveBack() { pool_give(kb, PR_DC_SCRATCH, p, b); } } gb{kb, sblk, sgot};
+    // pinned read-back word, one per host thread (no cudaMallocHost per compile)
+    struct PinnedCounters {
+        DcCounters *p = nullptr;
+        ~PinnedCounters() { if (p) cudaFreeHost(p); }
+    };
+    static thread_local PinnedCounters pinned;
+    if (!pinned.p && cudaMallocHost((void **)&pinned.p, sizeof(DcCounters)) != cudaSuccess) {
+        cudaGetLastError();
+        pinned.p = nullptr;
+        return fail(HEDL_ERR_OOM, "pinned");
+    }
+    DcCounters *hc = pinned.p;
+    {   // pageable source: the copy is staged before the call returns
         std::vector<double> kbb(kb->dir_bytes.begin(), kb->dir_bytes.end());
         kbb.insert(kbb.end(), kb->data_bytes.begin(), kb->data_bytes.end());
         kbb.push_back(0);
-        HEDL_CUDA(kb, cudaMemcpyAsync(kbytes, kbb.data(), kbb.size() * sizeof(double), cudaMemcpyHostToDevice, s));
-        HEDL_CUDA(kb, cudaStreamSynchronize(s));
+        HEDL_CUDA(kb, cudaMemcpy(kbytes, kbb.data(), kbb.size() * sizeof(double), cudaMemcpyHostToDevice));
     }
     const DcKb dk{kb->C, kb->R, kb->D, kb->W, kbytes, kbytes + 2 * kb->R};
     DcCounters init{0, 0, 0, ~0ull, 0, 0};
@@ -441,19 +519,17 @@ extern "C" hedl_status hedl_compile_device(const hedl_kb *kb, const hedl_node *n
         if ((st = read_counters())) return st;
         if (!hc->changed) break;
     }
+    timing_note("device compile: levels", now_ms() - t0);
     const uint32_t L = depth + 1;     // levels 0 .. depth-1 occur (depth passes changed something)
     // 2. level lists, reachability (top-down)
-    hist = m.get<uint32_t>(L + 1);
-    uint32_t *cursor = m.get<uint32_t>(L + 1);
-    if (!hist || !cursor) return fail(HEDL_ERR_OOM, "device compile scratch");
     HEDL_CUDA(kb, cudaMemsetAsync(hist, 0, (L + 1) * 4, s));
-    if (n) k_dc_hist<<<nblk(n, 256), 256, 0, s>>>(lvl, n, hist);
+    if (n) k_dc_hist<<<std::min<uint32_t>(nblk(n, 1024), 1184), 1024, (L + 1) * 4, s>>>(lvl, n, hist, L + 1);
     std::vector<uint32_t> h_hist(L + 1), h_off(L + 2, 0);
     HEDL_CUDA(kb, cudaMemcpyAsync(h_hist.data(), hist, (L + 1) * 4, cudaMemcpyDeviceToHost, s));
     HEDL_CUDA(kb, cudaStreamSynchronize(s));
     for (uint32_t l = 0; l <= L; ++l) h_off[l + 1] = h_off[l] + h_hist[l];
     HEDL_CUDA(kb, cudaMemcpyAsync(cursor, h_off.data(), (L + 1) * 4, cudaMemcpyHostToDevice, s));
-    if (n) k_dc_scatter<<<nblk(n, 256), 256, 0, s>>>(lvl, n, cursor, list);
+    if (n) k_dc_scatter<<<nblk(n, 1024), 1024, 2 * (L + 1) * 4, s>>>(lvl, n, cursor, list, L + 1);
     if (n_roots) k_dc_roots_mark<<<nblk(n_roots, 256), 256, 0, s>>>(roots, n_roots, n, reach, cnt);
     for (uint32_t l = L + 1; l-- > 1;)
         if (h_hist[l]) k_dc_reach<<<nblk(h_hist[l], 256), 256, 0, s>>>(list + h_off[l], h_hist[l], nodes, child_idx, bad, reach);
@@ -461,26 +537,17 @@ extern "C" hedl_status hedl_compile_device(const hedl_kb *kb, const hedl_node *n
     if (n) k_dc_validate<<<nblk(n, 256), 256, 0, s>>>(nodes, n, reach, bad, dk, cnt);
     if ((st = read_counters())) return st;
     if ((st = report())) return st;
+    timing_note("device compile: reach+validate", now_ms() - t0);
     // 4. canonicalisation, level by level up; 5. roots
     hedl_program *p = new hedl_program();
     p->kb = kb;
     p->flags = flags;
     p->dev = true;
     p->root_node.clear();
-    const uint32_t node_cap = n + n_roots + 1;
     uint64_t ops_cap = 2 * n_child_idx + n_roots + 1024;
-    uint32_t *table = nullptr;
-    uint64_t tcap = 1024;
-    while (tcap < 2ull * node_cap) tcap <<= 1;
-    const bool cse = !(flags & HEDL_COMPILE_NO_CSE);
-    if (cse && !(table = m.get<uint32_t>(tcap))) { delete p; return fail(HEDL_ERR_OOM, "device hash table"); }
     for (int attempt = 0; attempt < 2; ++attempt) {
         dc_free_arrays(p);
-        if (cudaMalloc((void **)&p->d_nodes, (size_t)node_cap * sizeof(CNode)) != cudaSuccess ||
-            cudaMalloc((void **)&p->d_ops, ops_cap * 4) != cudaSuccess ||
-            cudaMalloc((void **)&p->d_root_node, std::max<size_t>(n_roots, 1) * 4) != cudaSuccess) {
-            cudaGetLastError();
-            dc_free_arrays(p);
+        if (!dc_alloc_arrays(p, node_cap, ops_cap, n_roots)) {
             delete p;
             return fail(HEDL_ERR_OOM, "device program arrays");
         }
@@ -494,7 +561,7 @@ extern "C" hedl_status hedl_compile_device(const hedl_kb *kb, const hedl_node *n
                 count_launch();
             }
         if (n_roots) k_dc_roots<<<nblk(n_roots, 256), 256, 0, s>>>(roots, n_roots, cref, p->d_root_node, o, dk);
-        if ((st = read_counters())) { delete p; return st; }
+        if ((st = read_counters())) { dc_free_arrays(p); delete p; return st; }
         if (hc->err != ~0ull && (hc->err & 0xff) == DE_OPS_CAP && attempt == 0) {
             ops_cap = std::max<uint64_t>(ops_cap * 2, hc->n_ops + 1024);   // flattening grew the operand table
             continue;

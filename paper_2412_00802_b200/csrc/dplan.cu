@@ -100,13 +100,34 @@ __global__ void __launch_bounds__(1024) k_scan_add(uint32_t *out, uint32_t n, co
 inline uint32_t nblk(uint64_t n, uint32_t t) { return (uint32_t)((n + t - 1) / t); }
 
 // ---- live nodes, level lists -------------------------------------------------------------
-__global__ void k_dp_level_hist(const CNode *__restrict__ nodes, uint32_t nn, uint32_t *hist) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < nn && nodes[i].kind != NK_DEAD_D) atomicAdd(hist + nodes[i].level, 1u);
+__global__ void __launch_bounds__(1024) k_dp_level_hist(const CNode *__restrict__ nodes, uint32_t nn, uint32_t *hist,
+                                                        uint32_t nkeys) {
+    extern __shared__ uint32_t sh[];
+    for (uint32_t k = threadIdx.x; k < nkeys; k += blockDim.x) sh[k] = 0;
+    __syncthreads();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += gridDim.x * blockDim.x)
+        if (nodes[i].kind != NK_DEAD_D) atomicAdd(sh + nodes[i].level, 1u);
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < nkeys; k += blockDim.x)
+        if (sh[k]) atomicAdd(hist + k, sh[k]);
 }
-__global__ void k_dp_level_scatter(const CNode *__restrict__ nodes, uint32_t nn, uint32_t *cursor, uint32_t *list) {
+__global__ void __launch_bounds__(1024) k_dp_level_scatter(const CNode *__restrict__ nodes, uint32_t nn, uint32_t *cursor,
+                                                           uint32_t *list, uint32_t nkeys) {
+    extern __shared__ uint32_t sh[];
+    for (uint32_t k = threadIdx.x; k < 2 * nkeys; k += blockDim.x) sh[k] = 0;
+    __syncthreads();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < nn && nodes[i].kind != NK_DEAD_D) list[atomicAdd(cursor + nodes[i].level, 1u)] = i;
+    uint32_t key = 0, r = 0;
+    const bool on = i < nn && nodes[i].kind != NK_DEAD_D;
+    if (on) {
+        key = nodes[i].level;
+        r = atomicAdd(sh + key, 1u);
+    }
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < nkeys; k += blockDim.x)
+        if (sh[k]) sh[nkeys + k] = atomicAdd(cursor + k, sh[k]);
+    __syncthreads();
+    if (on) list[sh[nkeys + key] + r] = i;
 }
 
 __global__ void k_dp_init(const CNode *__restrict__ nodes, uint32_t nn, bool all, uint8_t *live, uint8_t *isroot,
@@ -325,28 +346,41 @@ __global__ void k_dp_root_tables(const uint32_t *__restrict__ root_node, uint32_
 
 // ---- per-program device-plan state ----------------------------------------------------------
 struct DPlan {
+    const hedl_kb *kb = nullptr;
     uint32_t nn = 0;
     bool lists = false;
     std::vector<uint32_t> lvl_off;             // host: level list offsets
     uint32_t *list = nullptr;                  // canonical nodes by level
     uint8_t *live = nullptr, *isroot = nullptr, *nfull = nullptr, *nproj = nullptr, *pmode = nullptr;
     uint32_t *cover = nullptr, *slot = nullptr, *pslot = nullptr, *bucket = nullptr, *rank_of = nullptr;
-    uint32_t *dnode = nullptr, *opfirst = nullptr, *bsum = nullptr, *totals = nullptr;
+    uint32_t *dnode = nullptr, *opfirst = nullptr, *bsum = nullptr, *totals = nullptr, *lhist = nullptr, *lcur = nullptr;
+    void *blk = nullptr;                       // pooled block holding the per-node arrays
+    size_t blk_bytes = 0;
     uint32_t *bstats = nullptr;                // 5 x nbuckets: count, ops, outs, cov, cursor
     uint32_t *bfirst = nullptr;
-    size_t bcap = 0;
-    uint32_t *h_stats = nullptr;               // pinned
+    void *bblk = nullptr;
+    size_t bcap = 0, bblk_bytes = 0;
+    uint32_t *h_stats = nullptr;               // pinned (pooled)
     size_t h_cap = 0;
-    std::vector<void *> allocs;
     ~DPlan() {
-        for (void *q : allocs) cudaFree(q);
-        if (h_stats) cudaFreeHost(h_stats);
+        if (blk) pool_give(kb, PR_DPLAN, blk, blk_bytes);
+        if (bblk) pool_give(kb, PR_DPLAN, bblk, bblk_bytes);
+        if (h_stats) pool_give(kb, PR_DPLAN_HOST, h_stats, h_cap);
     }
-    template <class T> T *get(size_t n) {
-        void *q = nullptr;
-        if (cudaMalloc(&q, std::max<size_t>(n * sizeof(T), 16)) != cudaSuccess) { cudaGetLastError(); return nullptr; }
-        allocs.push_back(q);
-        return (T *)q;
+    bool alloc(uint32_t n, uint32_t levels) {
+        for (int pass = 0; pass < 2; ++pass) {
+            Carver c{(char *)blk, 0};
+            list = c.take<uint32_t>(n);
+            live = c.take<uint8_t>(n); isroot = c.take<uint8_t>(n); nfull = c.take<uint8_t>(n);
+            nproj = c.take<uint8_t>(n); pmode = c.take<uint8_t>(n);
+            cover = c.take<uint32_t>(n); slot = c.take<uint32_t>(n); pslot = c.take<uint32_t>(n);
+            bucket = c.take<uint32_t>(n); rank_of = c.take<uint32_t>(n);
+            dnode = c.take<uint32_t>(n); opfirst = c.take<uint32_t>(n);
+            bsum = c.take<uint32_t>(nblk(n, 1024) + 1); totals = c.take<uint32_t>(8);
+            lhist = c.take<uint32_t>(levels + 2); lcur = c.take<uint32_t>(levels + 2);
+            if (pass == 0 && !(blk = pool_alloc(kb, PR_DPLAN, c.off, &blk_bytes))) return false;
+        }
+        return true;
     }
 };
 
@@ -388,38 +422,36 @@ hedl_status dplan_run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t 
         if (w->used && w->done) HEDL_CUDA(kb, cudaEventSynchronize(w->done));
         invalidate_plan(pc);
         const double t0 = now_ms();
-        if (!p->dplan) p->dplan = new DPlan();
-        DPlan &D = *(DPlan *)p->dplan;
         const uint32_t nn = p->dev_n_nodes;
-        if (D.nn != nn || !D.live) {
-            D.nn = nn;
-            D.list = D.get<uint32_t>(nn);
-            D.live = D.get<uint8_t>(nn); D.isroot = D.get<uint8_t>(nn); D.nfull = D.get<uint8_t>(nn);
-            D.nproj = D.get<uint8_t>(nn); D.pmode = D.get<uint8_t>(nn);
-            D.cover = D.get<uint32_t>(nn); D.slot = D.get<uint32_t>(nn); D.pslot = D.get<uint32_t>(nn);
-            D.bucket = D.get<uint32_t>(nn); D.rank_of = D.get<uint32_t>(nn);
-            D.dnode = D.get<uint32_t>(nn); D.opfirst = D.get<uint32_t>(nn);
-            D.bsum = D.get<uint32_t>(nblk(nn, 1024) + 1); D.totals = D.get<uint32_t>(8);
-            if (!D.list || !D.live || !D.isroot || !D.nfull || !D.nproj || !D.pmode || !D.cover || !D.slot || !D.pslot ||
-                !D.bucket || !D.rank_of || !D.dnode || !D.opfirst || !D.bsum || !D.totals)
-                return fail(HEDL_ERR_OOM, "device plan arrays");
-        }
         const uint32_t L = p->n_levels;
+        if (!p->dplan) {
+            DPlan *np = new DPlan();
+            np->kb = kb;
+            np->nn = nn;
+            if (!np->alloc(nn, L)) { delete np; return fail(HEDL_ERR_OOM, "device plan arrays"); }
+            p->dplan = np;
+        }
+        DPlan &D = *(DPlan *)p->dplan;
         if (!D.lists) {                              // canonical level lists (once per program)
-            uint32_t *hist = D.get<uint32_t>(L + 1), *cur = D.get<uint32_t>(L + 1);
-            if (!hist || !cur) return fail(HEDL_ERR_OOM, "device plan arrays");
+            uint32_t *hist = D.lhist, *cur = D.lcur;
             HEDL_CUDA(kb, cudaMemsetAsync(hist, 0, (L + 1) * 4, s));
-            if (nn) k_dp_level_hist<<<nblk(nn, 256), 256, 0, s>>>(p->d_nodes, nn, hist);
+            if (nn) k_dp_level_hist<<<std::min<uint32_t>(nblk(nn, 1024), 1184), 1024, (L + 1) * 4, s>>>(p->d_nodes, nn, hist, L + 1);
             std::vector<uint32_t> h(L + 1);
             HEDL_CUDA(kb, cudaMemcpyAsync(h.data(), hist, (L + 1) * 4, cudaMemcpyDeviceToHost, s));
             HEDL_CUDA(kb, cudaStreamSynchronize(s));
             D.lvl_off.assign(L + 2, 0);
             for (uint32_t l = 0; l <= L; ++l) D.lvl_off[l + 1] = D.lvl_off[l] + h[l];
             HEDL_CUDA(kb, cudaMemcpyAsync(cur, D.lvl_off.data(), (L + 1) * 4, cudaMemcpyHostToDevice, s));
-            if (nn) k_dp_level_scatter<<<nblk(nn, 256), 256, 0, s>>>(p->d_nodes, nn, cur, D.list);
+            if (nn) k_dp_level_scatter<<<nblk(nn, 1024), 1024, 2 * (L + 1) * 4, s>>>(p->d_nodes, nn, cur, D.list, L + 1);
             HEDL_CUDA(kb, cudaStreamSynchronize(s));     // `h` / lvl_off are host memory read by the copies
             D.lists = true;
         }
+        auto tsync = [&](const char *what) {          // phase timing (HEDL_TIMING=1 only)
+            if (!timing_enabled()) return;
+            cudaStreamSynchronize(s);
+            timing_note(what, now_ms() - t0);
+        };
+        tsync("device plan: lists");
         const bool all = r0 == 0 && r1 == p->dev_n_roots;
         // live nodes, roots, demands
         k_dp_init<<<nblk(std::max(nn, 1u), 256), 256, 0, s>>>(p->d_nodes, nn, all, D.live, D.isroot, D.nfull, D.nproj);
@@ -434,26 +466,40 @@ hedl_status dplan_run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t 
             if (m) k_dp_demand<<<nblk(m, 256), 256, 0, s>>>(D.list + D.lvl_off[l], m, p->d_nodes, p->d_ops, D.live,
                                                              D.nfull, D.nproj, D.pmode);
         }
+        tsync("device plan: live+demands");
         scan(s, D.isroot, nn, D.cover, D.bsum, D.totals + 0);
         scan(s, D.nfull, nn, D.slot, D.bsum, D.totals + 1);
         scan(s, D.nproj, nn, D.pslot, D.bsum, D.totals + 2);
+        tsync("device plan: scans");
         // groups
         uint32_t dirs = std::max<uint32_t>({1u, 2 * kb->R, kb->D, kb->S});
         const uint64_t nbk = (uint64_t)std::max<uint32_t>(L, 1) * kKinds * dirs * kSub;
         if (nbk > kMaxBuckets) return fail(HEDL_ERR_UNSUPPORTED, "device plan: too many launch groups");
         const BucketGeom g{dirs, (uint32_t)nbk};
         if (D.bcap < nbk) {
-            D.bstats = D.get<uint32_t>(nbk * 5);
-            D.bfirst = D.get<uint32_t>(nbk);
-            if (!D.bstats || !D.bfirst) return fail(HEDL_ERR_OOM, "device plan buckets");
+            if (D.bblk) pool_give(kb, PR_DPLAN, D.bblk, D.bblk_bytes);
+            D.bblk = pool_alloc(kb, PR_DPLAN, nbk * 6 * 4 + 256, &D.bblk_bytes);
+            if (!D.bblk) { D.bcap = 0; return fail(HEDL_ERR_OOM, "device plan buckets"); }
+            D.bstats = (uint32_t *)D.bblk;
+            D.bfirst = D.bstats + nbk * 5;
             D.bcap = nbk;
         }
         const size_t hbytes = nbk * 4 * 4 + 32;
         if (D.h_cap < hbytes) {
-            if (D.h_stats) cudaFreeHost(D.h_stats);
+            if (D.h_stats) pool_give(kb, PR_DPLAN_HOST, D.h_stats, D.h_cap);
             D.h_stats = nullptr;
-            if (cudaMallocHost((void **)&D.h_stats, hbytes) != cudaSuccess) { cudaGetLastError(); D.h_cap = 0; return fail(HEDL_ERR_OOM, "pinned"); }
-            D.h_cap = hbytes;
+            size_t got = 0;
+            if (void *q = pool_take(kb, PR_DPLAN_HOST, hbytes, &got)) {
+                D.h_stats = (uint32_t *)q;
+            } else if (cudaMallocHost((void **)&D.h_stats, hbytes) == cudaSuccess) {
+                got = hbytes;
+            } else {
+                cudaGetLastError();
+                D.h_stats = nullptr;
+                D.h_cap = 0;
+                return fail(HEDL_ERR_OOM, "pinned");
+            }
+            D.h_cap = got;
         }
         uint32_t *bc = D.bstats, *bo = bc + nbk, *bu = bo + nbk, *bv = bu + nbk, *bcur = bv + nbk;
         HEDL_CUDA(kb, cudaMemsetAsync(D.bstats, 0, nbk * 5 * 4, s));

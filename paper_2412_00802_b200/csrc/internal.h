@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cstring>
@@ -144,7 +145,7 @@ struct hedl_kb {
     // buffers released by freed programs, reused by the next ones (no cudaMalloc /
     // cudaMallocHost / memset per program); accumulator buffers return self-cleaned
     mutable std::mutex pool_mu;
-    mutable std::vector<std::pair<void *, size_t>> pool[8];
+    mutable std::vector<std::pair<void *, size_t>> pool[16];
     const void **interp_ptrs = nullptr;  // device: per-direction row_ptr/col, per-property row_ptr/val
     std::mutex interp_mu;
     std::vector<double> dir_bytes;  // 4(N+1) + 4E per direction
@@ -177,6 +178,8 @@ struct hedl_program {
     bool dev = false, dev_downloaded = false;
     hedl::CNode *d_nodes = nullptr;
     uint32_t *d_ops = nullptr, *d_root_node = nullptr;
+    void *d_block = nullptr;            // the pooled block holding the three arrays
+    size_t d_block_bytes = 0;
     uint32_t dev_n_nodes = 0, dev_n_roots = 0;
     uint64_t dev_n_ops = 0;
     void *dplan = nullptr;              // device-side evaluation plan state (dplan.cu)
@@ -201,10 +204,31 @@ hedl_status cuda_fail(const hedl_kb *kb, cudaError_t e, const char *where);
     } while (0)
 
 // ---- workspace pool (per KB) ---------------------------------------------------
-enum PoolRole { PR_ROWS, PR_PROWS, PR_HEAVY, PR_COUNTS, PR_SLICE, PR_PLAN_DEV, PR_PLAN_HOST, PR_N };
+enum PoolRole { PR_ROWS, PR_PROWS, PR_HEAVY, PR_COUNTS, PR_SLICE, PR_PLAN_DEV, PR_PLAN_HOST, PR_DC_SCRATCH, PR_DC_PROG,
+                PR_DPLAN, PR_DPLAN_HOST, PR_N };
 void *pool_take(const hedl_kb *kb, int role, size_t need, size_t *got);
 void pool_give(const hedl_kb *kb, int role, void *p, size_t bytes);
 void pool_release_all(hedl_kb *kb);
+// a device block from the pool (best fit) or cudaMalloc (25% headroom); null on OOM
+inline void *pool_alloc(const hedl_kb *kb, int role, size_t need, size_t *got) {
+    if (void *q = pool_take(kb, role, need, got)) return q;
+    void *q = nullptr;
+    const size_t sz = (need * 5 / 4 + 255) & ~size_t(255);
+    if (cudaMalloc(&q, sz) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    *got = sz;
+    return q;
+}
+// carves aligned sub-arrays out of one block (base == null: sizing pass)
+struct Carver {
+    char *base = nullptr;
+    size_t off = 0;
+    template <class T> T *take(size_t n) {
+        off = (off + 255) & ~size_t(255);
+        T *r = base ? (T *)(base + off) : nullptr;
+        off += std::max<size_t>(n * sizeof(T), 16);
+        return r;
+    }
+};
 void kb_release(const hedl_kb *kb);     // drop one reference; frees the KB at zero
 
 // ---- host phase timing (HEDL_TIMING=1 prints to stderr) ---------------------------

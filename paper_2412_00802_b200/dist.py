@@ -57,6 +57,35 @@ def shard_ranges(costs: np.ndarray, world: int) -> list:
     return [(int(cuts[r]), int(cuts[r + 1])) for r in range(world)]
 
 
+def local_arrays(nodes, child_idx, roots, lo, hi):
+    """Rank-local copy of the node arrays for roots [lo, hi) when the input is post-order
+    flattened trees stored root by root (every tree's nodes lie between the previous root
+    and its own root, children before parents): the node range (roots[lo-1], roots[hi-1]]
+    and its child slots, rebased to start at 0.  Returns None for any other layout."""
+    roots = np.asarray(roots)
+    if hi <= lo:
+        return None
+    a = int(roots[lo - 1]) + 1 if lo > 0 else 0
+    b = int(roots[hi - 1]) + 1
+    if lo > 0 and not np.all(np.diff(roots.astype(np.int64)) > 0):
+        return None
+    sub = nodes[a:b]
+    r = roots[lo:hi].astype(np.int64) - a
+    if len(sub) == 0 or r.min() < 0:
+        return None
+    cb = sub["child_begin"].astype(np.int64)
+    cc = sub["child_count"].astype(np.int64)
+    has = cc > 0
+    k0 = int(cb[has].min()) if has.any() else 0
+    k1 = int((cb + cc)[has].max()) if has.any() else 0
+    kids = np.asarray(child_idx)[k0:k1].astype(np.int64) - a
+    if len(kids) and (kids.min() < 0 or kids.max() >= len(sub)):
+        return None
+    out = sub.copy()
+    out["child_begin"] = np.where(has, cb - k0, 0).astype(np.uint32)
+    return out, kids.astype(np.uint32), r.astype(np.uint32)
+
+
 def subset_arrays(nodes, child_idx, roots, lo, hi):
     """The node arrays restricted to roots [lo, hi) (all nodes kept; roots sliced)."""
     return nodes, child_idx, roots[lo:hi]

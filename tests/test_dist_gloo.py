@@ -89,3 +89,27 @@ def test_root_costs_counts_restrictions():
              ("DRANGE", 0, 0.0, 1.0)]
     nodes, kids, roots = flatten(trees)
     assert hdist.root_costs(nodes, kids, roots).tolist() == [1, 33, 17]
+
+
+def test_local_arrays_rebased_equal_results():
+    """Rank-local rebased node arrays (post-order batches) give the oracle's counts for that range."""
+    from oracle import setsem
+    from synth import abox, hyps
+    from synth.format import flatten
+    kb = abox.random_tiny_kb(11, n=40, n_roles=2, n_data=1, n_strings=0)
+    rng = np.random.default_rng(2)
+    trees = [hyps.random_tree(rng, abox.kb_shape(kb), depth=4) for _ in range(50)]
+    nodes, kids, roots = flatten(trees)
+    _, ref = setsem.evaluate(kb, nodes, kids, roots, want_bits=False)
+    for lo, hi in ((0, 50), (0, 1), (7, 31), (49, 50)):
+        loc = hdist.local_arrays(nodes, kids, roots, lo, hi)
+        assert loc is not None
+        n2, k2, r2 = loc
+        assert len(n2) <= len(nodes)
+        _, c = setsem.evaluate(kb, n2, k2, r2, want_bits=False)
+        assert (c == ref[lo:hi]).all(), (lo, hi)
+    shared = flatten(trees, share=True)                  # DAG input: later trees reuse earlier nodes
+    loc = hdist.local_arrays(*shared, 3, 9)
+    if loc is not None:                                  # only when the range is self-contained
+        _, c = setsem.evaluate(kb, *loc, want_bits=False)
+        assert (c == ref[3:9]).all()
