@@ -241,6 +241,20 @@ hedl_status hedl_eval_batch(const hedl_kb *kb, hedl_program *prog, uint32_t firs
                             uint32_t n_roots, uint32_t *out_bits, hedl_counts *counts,
                             void *stream, uint32_t flags);
 
+/* Scores and top-k on the device (scoring for an on-GPU learner;
+ * definitions are reading Q14 -- the paper itself reports covered examples only):
+ *   HEDL_SCORE_ACCURACY  (tp + tn) / (tp + fp + fn + tn), 0 without examples
+ *   HEDL_SCORE_F1        2 tp / (2 tp + fp + fn), 0 when the denominator is 0
+ * in float64.  counts: DEVICE hedl_counts[n] (e.g. hedl_eval_batch with
+ * HEDL_EVAL_COUNTS_DEVICE).  scores: DEVICE double[n] or NULL.  top_idx / top_scores:
+ * DEVICE uint32[k] / double[k] (either may be NULL) = the k highest scores, descending,
+ * ties broken by the lower index.  Requires k <= n and k <= 4096.  Asynchronous on
+ * `stream` (device `device`).  Errors: INVALID_ARG, OOM, CUDA. */
+#define HEDL_SCORE_ACCURACY 0u
+#define HEDL_SCORE_F1 1u
+hedl_status hedl_score_topk(const hedl_counts *counts, uint32_t n, uint32_t metric, uint32_t k, double *scores,
+                            uint32_t *top_idx, double *top_scores, int device, void *stream);
+
 /* Device-memory cap for one program's evaluation workspace (default: half the
  * device memory free at first use, at most 48 GiB).  Larger caps give larger
  * chunks, i.e. fuller lane packs. */

@@ -30,7 +30,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "OUT_OF_RANGE", 3: "EXAMPLE_CONFLICT", 4
 
 # every symbol include/hedl.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ["hedl_kb_load", "hedl_kb_free", "hedl_kb_get_info", "hedl_compile", "hedl_compile_ex",
-               "hedl_compile_device",
+               "hedl_compile_device", "hedl_score_topk",
                "hedl_program_free",
                "hedl_program_get_info", "hedl_program_root_bytes", "hedl_eval_one", "hedl_eval_batch",
                "hedl_program_set_workspace_limit", "hedl_last_error", "hedl_version", "hedl_prof_enable",
@@ -91,6 +91,7 @@ def lib():
         "hedl_compile": ([P, P, U32, P, U64, P, U32, U32, C.POINTER(P)], I32),
         "hedl_compile_ex": ([P, P, U32, P, U64, P, U32, U32, U32, P, P, C.POINTER(P)], I32),
         "hedl_compile_device": ([P, P, U32, P, U64, P, U32, U32, P, C.POINTER(P)], I32),
+        "hedl_score_topk": ([P, U32, U32, U32, P, P, P, C.c_int, P], I32),
         "hedl_program_free": ([P], I32),
         "hedl_program_get_info": ([P, C.POINTER(_ProgInfo)], I32),
         "hedl_program_root_bytes": ([P, U32, U32, P], I32),
@@ -303,6 +304,30 @@ def hedl_compile_device(kb: KB, nodes, child_idx, roots, flags: int = 0, stream=
         _check(lib().hedl_compile_device(kb._h, C.c_void_p(tn.data_ptr()), nn, C.c_void_p(tk.data_ptr()), nk,
                                          C.c_void_p(tr.data_ptr()), nr, flags, _stream(stream), C.byref(h)))
     return Program(h, kb, nr)
+
+
+HEDL_SCORE_ACCURACY = 0
+HEDL_SCORE_F1 = 1
+
+
+def hedl_score_topk(counts, metric: int = HEDL_SCORE_ACCURACY, k: int = 0, want_scores: bool = True,
+                    stream=None):
+    """counts: CUDA int64 tensor [n][4] (tp, fp, fn, tn) -> (scores float64 [n] or None,
+    top_idx int32 [k], top_scores float64 [k]) on the same device."""
+    import torch
+    assert counts.is_cuda and counts.dtype == torch.int64 and counts.is_contiguous()
+    n = counts.shape[0]
+    dev = counts.device
+    with torch.cuda.device(dev):
+        sc = torch.empty(n, dtype=torch.float64, device=dev) if want_scores else None
+        ti = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+        ts = torch.empty(max(k, 1), dtype=torch.float64, device=dev)
+        _check(lib().hedl_score_topk(C.c_void_p(counts.data_ptr()), n, metric, k,
+                                     C.c_void_p(sc.data_ptr()) if sc is not None else None,
+                                     C.c_void_p(ti.data_ptr()), C.c_void_p(ts.data_ptr()),
+                                     dev.index if dev.index is not None else torch.cuda.current_device(),
+                                     _stream(stream)))
+    return sc, ti[:k], ts[:k]
 
 
 def hedl_eval_one(kb: KB, prog: Program, root: int, want_bits: bool = False, stream=None):

@@ -35,6 +35,7 @@ struct NoInitAlloc : std::allocator<T> {
 constexpr uint32_t kLightDeg = 32;
 constexpr uint32_t kHeavyDeg = 512;
 constexpr uint32_t kHeavyChunk = 4096;
+constexpr uint32_t kTopKMax = 4096;       // hedl_score_topk: k <= this
 
 // ---- restriction predicates ---------------------------------------------------
 // Every role restriction counts the neighbours y of x whose (possibly
