@@ -395,6 +395,29 @@ def main():
 
         e2e_steps(True)                                   # warm-up of the device-compile path
         e2e = e2e_steps(True)
+        # the learner's step on the GPU: device compile + plan + evaluate + F1 + top-1000,
+        # only the top-k indices / scores come back
+        if world == 1 and n_loc >= 1000:
+            lt = []
+            for it in range(args.warmup + args.steps):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                nodes_d.copy_(nodes_pin, non_blocking=True)
+                kids_d.copy_(kids_pin, non_blocking=True)
+                roots_d.copy_(roots_pin, non_blocking=True)
+                p3 = hedl.hedl_compile_device(kb, nodes_d, kids_d, roots_d, n_nodes=len(ln), n_kids=len(lk),
+                                              n_roots=len(lr))
+                _, cdev = hedl.hedl_eval_batch(kb, p3, 0, n_loc, counts_device=True, flags=eflags)
+                _, ti, ts = hedl.hedl_score_topk(cdev, hedl.HEDL_SCORE_F1, 1000, want_scores=False)
+                ti_h, ts_h = ti.cpu(), ts.cpu()
+                if it >= args.warmup:
+                    lt.append(time.perf_counter() - t0)
+                p3.free()
+            e2e["learner_step"] = {"value": n_loc / float(np.mean(lt)), "unit": "hyps/s",
+                                   "ms_per_step": 1000.0 * float(np.mean(lt)),
+                                   "what": "H2D of the batch + hedl_compile_device + device plan + evaluate + "
+                                           "F1 scores + top-1000 on the GPU; D2H of the top-1000 only",
+                                   "d2h_bytes_per_step": 12 * 1000}
         e2e["path"] = "hedl_compile_device + device plan (GPU-generated plans, PAPER.md:872)"
         e2e["host_compile"] = e2e_steps(False)
         e2e["host_compile"]["compile_ms"] = 1000.0 * compile_s
