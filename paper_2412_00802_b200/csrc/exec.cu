@@ -610,7 +610,7 @@ hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, u
     for (const LaunchRec &lr : cp.recs) {
         if (lr.kind == NK_AND) {
             launch_bool(s, lr.proj ? kp : kd, (const BoolDesc *)(d + cp.off_bool) + lr.first_desc, lr.count,
-                        (const Operand *)(d + cp.off_ops), cov, lr.bytes);
+                        (const Operand *)(d + cp.off_ops), cov, lr.bytes, kb->npos, kb->nneg);
         } else if (lr.kind == NK_RESTRICT) {
             const hedl_dir &dr = kb->dirs[lr.key];
             const RestrictDesc *dd_desc = (const RestrictDesc *)(d + cp.off_res) + lr.first_desc;

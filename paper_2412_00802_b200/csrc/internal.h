@@ -320,7 +320,7 @@ static __device__ __forceinline__ void proj_scatter(const KbDev &kb, uint32_t *p
 #endif
 void launch_cover_init(cudaStream_t s, hedl_counts *counts, uint32_t n, uint64_t npos, uint64_t nneg);
 void launch_bool(cudaStream_t s, const KbDev &kb, const BoolDesc *d_desc, uint32_t n_desc,
-                 const Operand *d_ops, hedl_counts *counts, double alg_bytes);
+                 const Operand *d_ops, hedl_counts *counts, double alg_bytes, uint64_t npos, uint64_t nneg);
 void launch_restrict(cudaStream_t s, const KbDev &kb, const DirDev &dir, const RestrictDesc *d_desc,
                      uint32_t n_desc, hedl_counts *counts, uint32_t *heavy_scratch, double alg_light,
                      double alg_heavy);

@@ -113,6 +113,57 @@ __global__ void __launch_bounds__(256) k_bool(KbDev kb, const BoolDesc *__restri
     if (d.cover >= 0) block_cover(counts, d.cover, tp, fp);
 }
 
+// Short rows (example-projected rows, small KBs): one warp per node, nodes strided over a
+// persistent grid.  One CTA per node would leave most of a 256-thread CTA idle and make
+// the launch CTA-scheduling bound (10^6 root conjunctions of 2.5 KB rows at C4); a warp
+// streams the node's k operand rows with 16 B loads, and writes its counts slot whole
+// (the node is never split across warps, so no atomics).
+constexpr uint32_t kBoolWarpMaxN4 = 1024;     // rows up to 4,096 words
+
+__global__ void __launch_bounds__(256) k_bool_warp(KbDev kb, const BoolDesc *__restrict__ descs, uint32_t n_desc,
+                                                   const Operand *__restrict__ ops, hedl_counts *counts,
+                                                   uint64_t npos, uint64_t nneg) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t n4 = kb.W4 >> 2;
+    for (uint32_t k = blockIdx.x * 8 + (threadIdx.x >> 5); k < n_desc; k += gridDim.x * 8) {
+        const BoolDesc d = descs[k];
+        uint32_t tp = 0, fp = 0;
+        for (uint32_t i = lane; i < n4; i += 32) {
+            uint4 acc = d.is_or ? make_uint4(0, 0, 0, 0) : make_uint4(FULL, FULL, FULL, FULL);
+            for (uint32_t j = 0; j < d.op_count; ++j) {
+                const Operand o = ops[d.op_first + j];
+                uint4 v = __ldg(reinterpret_cast<const uint4 *>(o.ptr) + i);
+                v.x ^= o.mask; v.y ^= o.mask; v.z ^= o.mask; v.w ^= o.mask;
+                if (d.is_or) { acc.x |= v.x; acc.y |= v.y; acc.z |= v.z; acc.w |= v.w; }
+                else { acc.x &= v.x; acc.y &= v.y; acc.z &= v.z; acc.w &= v.w; }
+            }
+            const uint32_t w0 = i << 2;
+            acc.x = tail_word(acc.x, w0, kb.W, kb.N);
+            acc.y = tail_word(acc.y, w0 + 1, kb.W, kb.N);
+            acc.z = tail_word(acc.z, w0 + 2, kb.W, kb.N);
+            acc.w = tail_word(acc.w, w0 + 3, kb.W, kb.N);
+            if (d.out) reinterpret_cast<uint4 *>(d.out)[i] = acc;
+            if (d.proj) {
+                proj_scatter(kb, d.proj, w0, acc.x);
+                proj_scatter(kb, d.proj, w0 + 1, acc.y);
+                proj_scatter(kb, d.proj, w0 + 2, acc.z);
+                proj_scatter(kb, d.proj, w0 + 3, acc.w);
+            }
+            if (d.cover >= 0) {
+                const uint4 p = __ldg(reinterpret_cast<const uint4 *>(kb.pos) + i);
+                const uint4 q = __ldg(reinterpret_cast<const uint4 *>(kb.neg) + i);
+                tp += __popc(acc.x & p.x) + __popc(acc.y & p.y) + __popc(acc.z & p.z) + __popc(acc.w & p.w);
+                fp += __popc(acc.x & q.x) + __popc(acc.y & q.y) + __popc(acc.z & q.z) + __popc(acc.w & q.w);
+            }
+        }
+        if (d.cover >= 0) {
+            tp = __reduce_add_sync(FULL, tp);
+            fp = __reduce_add_sync(FULL, fp);
+            if (lane == 0) counts[d.cover] = hedl_counts{tp, fp, npos - tp, nneg - fp};
+        }
+    }
+}
+
 // ------------------------------------------------------------------------------
 // per-node restriction over 1,024-row tiles (blockIdx.x = tile, blockIdx.y = node):
 // rows in the tile's degree-descending order (no divergence between a warp's rows),
@@ -392,7 +443,15 @@ void launch_cover_init(cudaStream_t s, hedl_counts *counts, uint32_t n, uint64_t
 }
 
 void launch_bool(cudaStream_t s, const KbDev &kb, const BoolDesc *d_desc, uint32_t n_desc,
-                 const Operand *d_ops, hedl_counts *counts, double alg_bytes) {
+                 const Operand *d_ops, hedl_counts *counts, double alg_bytes, uint64_t npos, uint64_t nneg) {
+    if (kb.W4 && (kb.W4 >> 2) <= kBoolWarpMaxN4 && n_desc >= 64) {
+        const uint32_t g = std::min<uint32_t>(cdiv(n_desc, 8), 148u * 16u);
+        prof_begin(s, KC_BOOL);
+        k_bool_warp<<<g, 256, 0, s>>>(kb, d_desc, n_desc, d_ops, counts, npos, nneg);
+        count_launch();
+        prof_end(s, KC_BOOL, alg_bytes, n_desc);
+        return;
+    }
     for (uint32_t off = 0; off < n_desc; off += 65535) {
         const uint32_t nd = n_desc - off < 65535 ? n_desc - off : 65535;
         const uint32_t gx = kb.W4 ? cdiv(kb.W4 / 4, 256) : 0;

@@ -139,6 +139,21 @@ extern "C" hedl_status hedl_score_topk(const hedl_counts *counts, uint32_t n, ui
     if (prev != device && cudaSetDevice(device) != cudaSuccess) { cudaGetLastError(); return fail(HEDL_ERR_UNSUPPORTED, "no such device"); }
     struct Restore { int d; ~Restore() { cudaSetDevice(d); } } restore{prev};
     cudaStream_t s = (cudaStream_t)stream;
+    {   // keep freed stream-ordered scratch mapped (the default release threshold of 0 would
+        // hand it back to the OS at every synchronisation and re-map it on the next call)
+        static std::mutex mu;
+        static uint64_t done_mask = 0;
+        std::lock_guard<std::mutex> lk(mu);
+        if (device < 64 && !(done_mask >> device & 1)) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+                uint64_t thr = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            cudaGetLastError();
+            done_mask |= 1ull << device;
+        }
+    }
     // stream-ordered scratch: keys, eq flags, ranks, candidates, block sums, state
     Carver c;
     c.take<unsigned long long>(n);
