@@ -101,6 +101,13 @@ struct hedl_dir {                  // one role direction
     uint32_t *ex_hx = nullptr, *ex_hrank = nullptr, *ex_hn = nullptr;   // heavy example rows: id, rank, #chunks
     uint4 *ex_chunks = nullptr;        // {ex-heavy idx, e0, e1, 0}
     uint64_t E_ex = 0, E_ex_heavy = 0; // edges of light/medium and of heavy example rows
+    // compact T for EX packs: U = sorted distinct neighbours of the example rows; an EX pack
+    // stores T only at U (32 B each) and the example rows' edges point into it
+    uint32_t n_u = 0;
+    uint32_t *ex_rp = nullptr;         // device [M+1]: edge range of example rank r
+    uint32_t *ex_ccol = nullptr;       // device: compact T index of each such edge's neighbour
+    uint32_t *ex_umask = nullptr;      // device [W4]: bit y&31 of word y>>5 set iff y in U
+    uint32_t *ex_ubase = nullptr;      // device [W4]: |U ∩ [0, 32w)|
 };
 
 struct hedl_data {

@@ -391,6 +391,31 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
             {
                 const std::vector<uint32_t> &ex = kb->h_ex;
                 const uint32_t M = (uint32_t)ex.size();
+                // example-row CSR over ranks with neighbours as compact T indices (U = distinct
+                // neighbours of the example rows, in id order)
+                std::vector<uint32_t> erp(M + 1, 0);
+                for (uint32_t r = 0; r < M; ++r) erp[r + 1] = erp[r] + (h.row_ptr[ex[r] + 1] - h.row_ptr[ex[r]]);
+                std::vector<uint32_t> umask(W4, 0), ubase(W4, 0), ecol(erp[M]);
+                for (uint32_t r = 0; r < M; ++r)
+                    for (uint32_t e = h.row_ptr[ex[r]]; e < h.row_ptr[ex[r] + 1]; ++e) {
+                        const uint32_t y = h.col[e];
+                        umask[y >> 5] |= 1u << (y & 31);
+                    }
+                uint32_t nu = 0;
+                for (uint32_t w = 0; w < W4; ++w) {
+                    ubase[w] = nu;
+                    nu += (uint32_t)__builtin_popcount(umask[w]);
+                }
+                for (uint32_t r = 0; r < M; ++r)
+                    for (uint32_t e = h.row_ptr[ex[r]], k = erp[r]; e < h.row_ptr[ex[r] + 1]; ++e, ++k) {
+                        const uint32_t y = h.col[e];
+                        ecol[k] = ubase[y >> 5] + (uint32_t)__builtin_popcount(umask[y >> 5] & ((1u << (y & 31)) - 1u));
+                    }
+                dr.n_u = nu;
+                if ((s = upload(kb, st, &dr.ex_rp, erp.data(), erp.size()))) return bail(s);
+                if ((s = upload(kb, st, &dr.ex_ccol, ecol.data(), ecol.size()))) return bail(s);
+                if ((s = upload(kb, st, &dr.ex_umask, umask.data(), umask.size()))) return bail(s);
+                if ((s = upload(kb, st, &dr.ex_ubase, ubase.data(), ubase.size()))) return bail(s);
                 dr.n_ex_blocks = (M + 127) / 128;
                 std::vector<uint4> et(dr.n_ex_blocks + 1);
                 std::vector<uint32_t> eo, ehx, ehr, ehn;
@@ -407,7 +432,7 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
                             const uint32_t hi = (uint32_t)ehx.size();
                             ehx.push_back(ex[r]);
                             ehr.push_back(r);
-                            const uint32_t a = h.row_ptr[ex[r]], e = h.row_ptr[ex[r] + 1];
+                            const uint32_t a = erp[r], e = erp[r + 1];     // in the example-row CSR
                             uint32_t nc = 0;
                             for (uint32_t q = a; q < e; q += kHeavyChunk, ++nc)
                                 ech.push_back(make_uint4(hi, q, std::min(e, q + kHeavyChunk), 0));

@@ -65,17 +65,27 @@ struct PackConst {
     uint32_t mge[LW], mle[LW], meq[LW], mlep[LW];
 };
 
-__device__ __forceinline__ uint32_t transpose_step(uint32_t x, uint32_t lane, int j, uint32_t m) {
-    const uint32_t y = __shfl_xor_sync(FULL, x, j);
-    return (lane & j) ? ((x & ~m) | ((y >> j) & m)) : ((x & m) | ((y & m) << j));
-}
-// 32x32 bit transpose across a warp: in lane r bit c = M[r][c]; out lane c bit r = M[r][c]
+// 32x32 bit transpose across a warp: in lane r bit c = M[r][c]; out lane c bit r = M[r][c].
+// Five butterfly stages; each lane keeps half of its word and takes the other half from its
+// partner.  The 16- and 8-bit stages are one byte permute (selector chosen per lane), the
+// 4/2/1-bit stages one rotate (left by j for the lower lane of a pair, right by j for the
+// upper one) and one LOP3 -- 13 instructions with the shuffles instead of ~30.
 __device__ __forceinline__ uint32_t warp_transpose(uint32_t x, uint32_t lane) {
-    x = transpose_step(x, lane, 16, 0x0000FFFFu);
-    x = transpose_step(x, lane, 8, 0x00FF00FFu);
-    x = transpose_step(x, lane, 4, 0x0F0F0F0Fu);
-    x = transpose_step(x, lane, 2, 0x33333333u);
-    x = transpose_step(x, lane, 1, 0x55555555u);
+    const bool lo16 = !(lane & 16), lo8 = !(lane & 8), lo4 = !(lane & 4), lo2 = !(lane & 2), lo1 = !(lane & 1);
+    uint32_t y = __shfl_xor_sync(FULL, x, 16);
+    x = __byte_perm(x, y, lo16 ? 0x5410u : 0x3276u);
+    y = __shfl_xor_sync(FULL, x, 8);
+    x = __byte_perm(x, y, lo8 ? 0x6240u : 0x3715u);
+    uint32_t k;
+    y = __shfl_xor_sync(FULL, x, 4);
+    k = lo4 ? 0x0F0F0F0Fu : 0xF0F0F0F0u;
+    x = (x & k) | (__funnelshift_l(y, y, lo4 ? 4 : 28) & ~k);
+    y = __shfl_xor_sync(FULL, x, 2);
+    k = lo2 ? 0x33333333u : 0xCCCCCCCCu;
+    x = (x & k) | (__funnelshift_l(y, y, lo2 ? 2 : 30) & ~k);
+    y = __shfl_xor_sync(FULL, x, 1);
+    k = lo1 ? 0x55555555u : 0xAAAAAAAAu;
+    x = (x & k) | (__funnelshift_l(y, y, lo1 ? 1 : 31) & ~k);
     return x;
 }
 
@@ -217,7 +227,8 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
 }
 
 __global__ void __launch_bounds__(256) k_slice_pack(KbDev kb, const RestrictDesc *__restrict__ d_run, uint32_t run,
-                                                    uint4 *__restrict__ T_base, uint64_t t_stride) {
+                                                    uint4 *__restrict__ T_base, uint64_t t_stride,
+                                                    const uint32_t *__restrict__ umask, const uint32_t *__restrict__ ubase) {
     extern __shared__ __align__(16) uint32_t sm[];        // [256][PK_STRIDE]
     __shared__ uint32_t s_cm[256];
     __shared__ __align__(8) uint64_t mbar;
@@ -245,20 +256,38 @@ __global__ void __launch_bounds__(256) k_slice_pack(KbDev kb, const RestrictDesc
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                      ::"r"(smem_u32(sm + t * PK_STRIDE)), "l"(src), "r"(seg), "r"(mb) : "memory");
     }
+    // EX packs: T only at the example rows' neighbours U, compacted (umask / ubase); the
+    // masks of this warp's 8 words are fetched while the bulk copies are in flight
+    uint32_t ums[8], ubs[8];
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) {
+        const uint32_t w = w0 + wid * 8 + k;
+        ums[k] = (umask && w < kb.W4) ? __ldg(umask + w) : FULL;
+        ubs[k] = (umask && w < kb.W4) ? __ldg(ubase + w) : 0u;
+    }
     asm volatile("{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n @!P1 bra WAIT_%=;\n}"
                  ::"r"(mb) : "memory");
+#pragma unroll
     for (uint32_t k = 0; k < 8; ++k) {
         const uint32_t wd = wid * 8 + k, w = w0 + wd;
         if (w >= kb.W4) break;
+        const uint32_t um = ums[k];
+        if (!um) continue;                                 // warp-uniform: no neighbour in this word
         uint32_t o[LW];
 #pragma unroll
         for (int g = 0; g < LW; ++g) {
             const uint32_t r = g * 32 + lane;
             o[g] = warp_transpose(sm[r * PK_STRIDE + wd] ^ s_cm[r], lane);
         }
-        const uint64_t y = (uint64_t)w * 32 + lane;
-        T[2 * y] = make_uint4(o[0], o[1], o[2], o[3]);
-        T[2 * y + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+        if (!umask) {
+            const uint64_t y = (uint64_t)w * 32 + lane;
+            T[2 * y] = make_uint4(o[0], o[1], o[2], o[3]);
+            T[2 * y + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+        } else if ((um >> lane) & 1u) {
+            const uint64_t t = ubs[k] + __popc(um & ((1u << lane) - 1u));
+            T[2 * t] = make_uint4(o[0], o[1], o[2], o[3]);
+            T[2 * t + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+        }
     }
 }
 
@@ -488,7 +517,7 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
 // straight to the nodes' example-projected rows (4 projected words per CTA, owned:
 // plain stores) with fused coverage against the projected example masks.
 struct ExArgs {
-    const uint32_t *row_ptr, *col;
+    const uint32_t *erp, *ecol;       // example-row CSR over ranks, neighbours as compact T indices
     const uint4 *ex_tiles;
     const uint32_t *ex_order, *ex_ids, *ex_hrank;
     const uint32_t *ppos, *pneg;
@@ -515,11 +544,11 @@ __global__ void __launch_bounds__(256, COUNT ? 3 : 4) k_slice_ex(ExArgs a, Slice
         for (int k = 0; k < LW; ++k) ot[rl * TROW + k] = sc.hout[(size_t)h * LW + k];
     }
     for (uint32_t m = wid; m < ti.y; m += 8) {            // medium rows: warp per row
-        const uint32_t r = __ldg(a.ex_order + ti.x + m), x = __ldg(a.ex_ids + r);
-        const uint32_t e0 = __ldg(a.row_ptr + x), e1 = __ldg(a.row_ptr + x + 1);
+        const uint32_t r = __ldg(a.ex_order + ti.x + m);
+        const uint32_t e0 = __ldg(a.erp + r), e1 = __ldg(a.erp + r + 1);
         Acc<COUNT> acc;
         acc.zero();
-        scan_edges<COUNT>(acc, a.col, sc.T, e0 + (lane >> 1), e1, 16, half);
+        scan_edges<COUNT>(acc, a.ecol, sc.T, e0 + (lane >> 1), e1, 16, half);
         acc.warp_reduce_pairs();
         if (lane < 2) {
 #pragma unroll
@@ -527,11 +556,11 @@ __global__ void __launch_bounds__(256, COUNT ? 3 : 4) k_slice_ex(ExArgs a, Slice
         }
     }
     for (uint32_t l = threadIdx.x >> 1; l < ti.z; l += 128) {   // light rows: lane pair per row
-        const uint32_t r = __ldg(a.ex_order + ti.x + ti.y + l), x = __ldg(a.ex_ids + r);
-        const uint32_t e0 = __ldg(a.row_ptr + x), e1 = __ldg(a.row_ptr + x + 1);
+        const uint32_t r = __ldg(a.ex_order + ti.x + ti.y + l);
+        const uint32_t e0 = __ldg(a.erp + r), e1 = __ldg(a.erp + r + 1);
         Acc<COUNT> acc;
         acc.zero();
-        scan_edges<COUNT>(acc, a.col, sc.T, e0, e1, 1, half);
+        scan_edges<COUNT>(acc, a.ecol, sc.T, e0, e1, 1, half);
 #pragma unroll
         for (int k = 0; k < HW; ++k) ot[(r - r0) * TROW + half * HW + k] = acc.result(pc, half * HW + k, k);
     }
@@ -580,7 +609,10 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
                       int fixed_cls) {
     const hedl_dir &dr = kb->dirs[dirid];
     if (ex && !kb->M) return HEDL_OK;                     // no examples: nothing to evaluate
-    const size_t t_bytes = (size_t)kb->W4 * 32 * 32;
+    const size_t t_bytes = (size_t)kb->W4 * 32 * 32;     // full packs: 32 B per individual
+    size_t nu_max = 0;
+    for (const hedl_dir &x : kb->dirs) nu_max = std::max<size_t>(nu_max, x.n_u);
+    const size_t tx_bytes = std::max<size_t>(nu_max * 32, 256);   // EX packs: 32 B per neighbour of an example
     // one fixed layout for every direction (sized by the largest heavy lists), so the
     // self-cleaning accumulators of one direction never alias another's results:
     //   [T x kMaxBatch][full-pack heavy scratch (nh)][EX heavy scratch (kMaxBatch x nhx)]
@@ -590,8 +622,8 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
         nhx = std::max<size_t>(nhx, x.n_ex_heavy);
     }
     const size_t per_h = (LW + 256 + 1 + LW) * 4;
-    const uint32_t max_batch = (uint32_t)std::max<size_t>(1, std::min<size_t>(128, (4ull << 30) / std::max<size_t>(t_bytes, 1)));
-    const size_t off_hf = t_bytes * max_batch, off_hx = off_hf + nh * per_h;
+    const uint32_t max_batch = (uint32_t)std::max<size_t>(1, std::min<size_t>(128, (4ull << 30) / tx_bytes));
+    const size_t off_hf = std::max(t_bytes, tx_bytes * max_batch), off_hx = off_hf + nh * per_h;
     const size_t need = off_hx + (size_t)max_batch * nhx * per_h + 256;
     if (*ws_bytes < need) {
         HEDL_CUDA(kb, cudaStreamSynchronize(s));
@@ -624,9 +656,9 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
     };
     SliceDir sd{dr.row_ptr, dr.col, dr.tiles, dr.order, dr.tile_slice, dr.sell_off, dr.sell_w, dr.sell_col,
                 dr.heavy_x, dr.heavy_nchunks, dr.chunks, dr.n_heavy, dr.n_chunks, dr.n_tiles};
-    SliceDir sdx{dr.row_ptr, dr.col, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+    SliceDir sdx{dr.ex_rp, dr.ex_ccol, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                  dr.ex_hx, dr.ex_hn, dr.ex_chunks, dr.n_ex_heavy, dr.n_ex_chunks, 0};
-    const ExArgs xa{dr.row_ptr, dr.col, dr.ex_tiles, dr.ex_order, kb->ex_ids, dr.ex_hrank, kb->ppos, kb->pneg, kb->MW4};
+    const ExArgs xa{dr.ex_rp, dr.ex_ccol, dr.ex_tiles, dr.ex_order, kb->ex_ids, dr.ex_hrank, kb->ppos, kb->pneg, kb->MW4};
     const size_t smem = sizeof(PackConst) + 1024 * TROW * 4;
     const size_t pk_smem = 256 * PK_STRIDE * 4;
     static bool attr_set = false;
@@ -654,11 +686,16 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
         const uint32_t packs = (run + 255) / 256;
         const RestrictDesc *dd = d_desc + off;
         SliceScratch sc = ex ? scratch(off_hx, nhx, max_batch) : scratch(off_hf, nh, 1);
-        if (ex) sc.h_stride = nhx;
+        if (ex) {
+            sc.h_stride = nhx;
+            sc.t_stride = tx_bytes / 16;
+        }
         prof_begin(s, KC_SLICE_IN);
-        k_slice_pack<<<dim3(cdiv(kb->W4, PK_WORDS), packs), 256, pk_smem, s>>>(kd, dd, run, sc.T, sc.t_stride);
+        k_slice_pack<<<dim3(cdiv(kb->W4, PK_WORDS), packs), 256, pk_smem, s>>>(kd, dd, run, sc.T, sc.t_stride,
+                                                                             ex ? dr.ex_umask : nullptr,
+                                                                             ex ? dr.ex_ubase : nullptr);
         count_launch();
-        prof_end(s, KC_SLICE_IN, 4.0 * kb->W * run + 32.0 * 32 * kb->W4 * packs, packs);
+        prof_end(s, KC_SLICE_IN, 4.0 * kb->W * run + 32.0 * (ex ? (double)dr.n_u : 32.0 * kb->W4) * packs, packs);
         const SliceDir &hd = ex ? sdx : sd;
         if (hd.n_chunks) {
             prof_begin(s, KC_SLICE_HEAVY);
