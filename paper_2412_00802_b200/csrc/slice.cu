@@ -267,26 +267,37 @@ __global__ void __launch_bounds__(256) k_slice_pack(KbDev kb, const RestrictDesc
     }
     asm volatile("{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n @!P1 bra WAIT_%=;\n}"
                  ::"r"(mb) : "memory");
+    // a quad of words per step: one conflict-free 16 B shared load per row group (the 68-word
+    // row stride makes 4 B column loads 4-way bank conflicted), four 32x32 transposes
+    uint32_t cms[LW];
 #pragma unroll
-    for (uint32_t k = 0; k < 8; ++k) {
-        const uint32_t wd = wid * 8 + k, w = w0 + wd;
-        if (w >= kb.W4) break;
-        const uint32_t um = ums[k];
-        if (!um) continue;                                 // warp-uniform: no neighbour in this word
-        uint32_t o[LW];
+    for (int g = 0; g < LW; ++g) cms[g] = s_cm[g * 32 + lane];
+#pragma unroll
+    for (uint32_t q = 0; q < 2; ++q) {
+        const uint32_t wq = wid * 8 + q * 4;
+        if (w0 + wq >= kb.W4) break;                       // W4 is a multiple of 8: whole quads
+        if (!(ums[4 * q] | ums[4 * q + 1] | ums[4 * q + 2] | ums[4 * q + 3])) continue;   // warp-uniform
+        uint32_t o[4][LW];
 #pragma unroll
         for (int g = 0; g < LW; ++g) {
-            const uint32_t r = g * 32 + lane;
-            o[g] = warp_transpose(sm[r * PK_STRIDE + wd] ^ s_cm[r], lane);
+            const uint4 v = *reinterpret_cast<const uint4 *>(sm + (g * 32 + lane) * PK_STRIDE + wq);
+            o[0][g] = warp_transpose(v.x ^ cms[g], lane);
+            o[1][g] = warp_transpose(v.y ^ cms[g], lane);
+            o[2][g] = warp_transpose(v.z ^ cms[g], lane);
+            o[3][g] = warp_transpose(v.w ^ cms[g], lane);
         }
-        if (!umask) {
-            const uint64_t y = (uint64_t)w * 32 + lane;
-            T[2 * y] = make_uint4(o[0], o[1], o[2], o[3]);
-            T[2 * y + 1] = make_uint4(o[4], o[5], o[6], o[7]);
-        } else if ((um >> lane) & 1u) {
-            const uint64_t t = ubs[k] + __popc(um & ((1u << lane) - 1u));
-            T[2 * t] = make_uint4(o[0], o[1], o[2], o[3]);
-            T[2 * t + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+#pragma unroll
+        for (uint32_t kk = 0; kk < 4; ++kk) {
+            const uint32_t w = w0 + wq + kk, um = ums[4 * q + kk];
+            if (!umask) {
+                const uint64_t y = (uint64_t)w * 32 + lane;
+                T[2 * y] = make_uint4(o[kk][0], o[kk][1], o[kk][2], o[kk][3]);
+                T[2 * y + 1] = make_uint4(o[kk][4], o[kk][5], o[kk][6], o[kk][7]);
+            } else if ((um >> lane) & 1u) {
+                const uint64_t t = ubs[4 * q + kk] + __popc(um & ((1u << lane) - 1u));
+                T[2 * t] = make_uint4(o[kk][0], o[kk][1], o[kk][2], o[kk][3]);
+                T[2 * t + 1] = make_uint4(o[kk][4], o[kk][5], o[kk][6], o[kk][7]);
+            }
         }
     }
 }

@@ -1,6 +1,6 @@
-"""From an ncu launch list (gpu__time_duration.sum CSV): the kernel with the largest total time and,
-for it, the invocation index (among launches of that kernel) with the largest grid.
-Prints: <kernel-name-regex> <invocation-index>"""
+"""From an ncu launch list (gpu__time_duration.sum CSV): the kernel with the largest total time
+(or the kernel named by argv[2]) and, for it, the invocation index (among launches of that
+kernel) with the largest grid.  Prints: <kernel-name-regex> <invocation-index>"""
 import csv
 import sys
 from collections import defaultdict
@@ -22,7 +22,7 @@ for r in body:
     tot[name] += v
     g = [int(x) for x in r[gi].strip("()").split(",")]
     launches[name].append(g[0] * g[1] * g[2])
-top = max(tot, key=tot.get)
+top = sys.argv[2] if len(sys.argv) > 2 else max(tot, key=tot.get)
 sizes = launches[top]
 idx = max(range(len(sizes)), key=lambda i: sizes[i])
 print(top, idx)
