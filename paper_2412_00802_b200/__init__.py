@@ -37,6 +37,12 @@ ABI_SYMBOLS = ["hedl_kb_load", "hedl_kb_free", "hedl_kb_get_info", "hedl_compile
                "hedl_prof_reset", "hedl_prof_read", "hedl_launch_count", "hedl_io_counters"]
 
 
+# the hedl_node record of include/hedl.h (28 bytes)
+HEDL_NODE_DTYPE = np.dtype({"names": ["op", "flags", "pad", "arg", "n", "lo", "hi", "child_begin", "child_count"],
+                            "formats": ["u1", "u1", "<u2", "<u4", "<u4", "<f4", "<f4", "<u4", "<u4"],
+                            "offsets": [0, 1, 2, 4, 8, 12, 16, 20, 24], "itemsize": 28})
+
+
 class HedlError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"hedl {STATUS.get(code, code)}: {msg}")

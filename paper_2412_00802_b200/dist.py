@@ -3,8 +3,9 @@
 One process per GPU (torchrun).  Every rank holds a full KB replica (the
 paper's "exact copy of knowledge representation matrixes" per device,
 PAPER.md:568 step 2).  The batch is cut into contiguous, cost-balanced index
-ranges (static scheduling as in PAPER.md:568/578, with estimated hypothesis
-cost replacing device speed: the B200s are identical).  Each rank compiles
+ranges (static scheduling as in PAPER.md:568/578, balanced by estimated hypothesis
+cost; on mixed-GPU boxes the paper's probe ratios, probe_ratios(), weight the
+shares).  Each rank compiles
 and evaluates only its range; the only collective is one all_gather of the
 per-hypothesis count vectors (NCCL over NVLink/NVSwitch on GPUs).  Rank 0
 un-pads into input order.
@@ -42,19 +43,72 @@ def root_costs(nodes: np.ndarray, child_idx: np.ndarray, roots: np.ndarray) -> n
     return 1 + 16 * sub[roots.astype(np.int64)]
 
 
-def shard_ranges(costs: np.ndarray, world: int) -> list:
-    """Contiguous [lo, hi) ranges with near-equal cost prefix sums (one per rank)."""
+def shard_ranges(costs: np.ndarray, world: int, weights: Optional[Sequence[float]] = None) -> list:
+    """Contiguous [lo, hi) ranges, one per rank, cutting the cost prefix sums at the ranks'
+    shares: equal shares by default, else proportional to `weights` (e.g. probe_ratios)."""
     n = len(costs)
     if world <= 1 or n == 0:
         return [(0, n)] + [(n, n)] * (world - 1)
+    if weights is None:
+        frac = np.arange(1, world, dtype=np.float64) / world
+    else:
+        w = np.asarray(weights, dtype=np.float64)
+        assert len(w) == world and (w > 0).all(), "one positive weight per rank"
+        frac = np.cumsum(w)[:-1] / w.sum()
     cum = np.cumsum(costs, dtype=np.float64)
     total = cum[-1]
     cuts = [0]
-    for r in range(1, world):
-        cuts.append(int(np.searchsorted(cum, total * r / world, side="left")) + 1)
+    for f in frac:
+        cuts.append(int(np.searchsorted(cum, total * f, side="left")) + 1)
     cuts.append(n)
     cuts = np.maximum.accumulate(np.clip(cuts, 0, n))
     return [(int(cuts[r]), int(cuts[r + 1])) for r in range(world)]
+
+
+def probe_ratios(kb=None, group=None, reps: int = 20, timer: Optional[Callable] = None) -> np.ndarray:
+    """The paper's device-capability probe (Fig. 5 steps 3-6): every rank times a
+    dummy hypothesis -- a conjunction of (up to) 5 concepts -- on its own device against the KB it
+    holds; the times are all-gathered and rank r's scheduling ratio is (1/t_r) / sum(1/t).
+    Computed once, then reused for every batch (static scheduling).  `timer` is a test seam
+    returning this rank's probe time in seconds (the gloo tests inject one)."""
+    import torch
+    import torch.distributed as dist
+    if timer is None:
+        timer = lambda: _probe_time(kb, reps)
+    t = float(timer())
+    world = dist.get_world_size(group)
+    dev = torch.device(f"cuda:{kb.device}") if kb is not None and dist.get_backend(group) == "nccl" else torch.device("cpu")
+    buf = torch.tensor([t], dtype=torch.float64, device=dev)
+    out = [torch.zeros_like(buf) for _ in range(world)]
+    dist.all_gather(out, buf, group=group)
+    times = np.array([float(x.item()) for x in out])
+    inv = 1.0 / np.maximum(times, 1e-12)
+    return inv / inv.sum()
+
+
+def _probe_time(kb, reps: int) -> float:
+    """Median device time of the probe hypothesis (AND of the first min(5, C) concepts)."""
+    import torch
+    import paper_2412_00802_b200 as hedl
+    c = min(5, kb.info()["C"])
+    nodes = np.zeros(c + 1, dtype=hedl.HEDL_NODE_DTYPE)       # ATOM 0 .. ATOM c-1, AND(all)
+    nodes["op"][:c] = 2
+    nodes["arg"][:c] = np.arange(c)
+    nodes["op"][c] = 4
+    nodes["child_count"][c] = c
+    kids = np.arange(c, dtype=np.uint32)
+    prog = hedl.hedl_compile(kb, nodes, kids, np.array([c], dtype=np.uint32))
+    ts = []
+    with torch.cuda.device(kb.device):
+        for _ in range(reps + 3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            hedl.hedl_eval_batch(kb, prog, 0, 1, counts_device=True)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) / 1000.0)
+    prog.free()
+    return float(np.median(ts[3:]))
 
 
 def local_arrays(nodes, child_idx, roots, lo, hi):
@@ -112,7 +166,8 @@ def gather_counts(local_counts, n_total: int, ranges, group=None, device=None):
 
 def eval_batch_sharded(kb, nodes: np.ndarray, child_idx: np.ndarray, roots: np.ndarray,
                        flags: int = 0, group=None,
-                       evaluator: Optional[Callable] = None) -> Tuple["object", dict]:
+                       evaluator: Optional[Callable] = None,
+                       weights: Optional[Sequence[float]] = None) -> Tuple["object", dict]:
     """Evaluate the batch across the ranks of `group`; returns (counts[n][4] int64 tensor, info).
 
     `kb` is this rank's replica (a paper_2412_00802_b200.KB).  `evaluator`
@@ -123,7 +178,7 @@ def eval_batch_sharded(kb, nodes: np.ndarray, child_idx: np.ndarray, roots: np.n
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     costs = root_costs(nodes, child_idx, roots)
-    ranges = shard_ranges(costs, world)
+    ranges = shard_ranges(costs, world, weights)
     lo, hi = ranges[rank]
     if evaluator is None:
         import paper_2412_00802_b200 as hedl

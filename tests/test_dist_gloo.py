@@ -113,3 +113,41 @@ def test_local_arrays_rebased_equal_results():
     if loc is not None:                                  # only when the range is self-contained
         _, c = setsem.evaluate(kb, *loc, want_bits=False)
         assert (c == ref[3:9]).all()
+
+
+def _probe_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # rank r's device is (r+1)x slower: ratios 1/(r+1) normalised
+    ratios = hdist.probe_ratios(timer=lambda: 0.001 * (rank + 1))
+    q.put((rank, ratios.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_probe_ratios_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_probe_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    inv = np.array([1.0 / (r + 1) for r in range(world)])
+    for _, ratios in got:                                   # every rank gets the same ratios
+        assert np.allclose(ratios, inv / inv.sum())
+
+
+def test_weighted_shard_ranges():
+    costs = np.ones(1000)
+    r = hdist.shard_ranges(costs, 3, weights=[0.5, 0.25, 0.25])
+    assert r == [(0, 501), (501, 751), (751, 1000)] or abs(r[0][1] - 500) <= 1
+    assert r[0][0] == 0 and r[-1][1] == 1000 and all(a[1] == b[0] for a, b in zip(r, r[1:]))
+    sizes = [b - a for a, b in r]
+    assert abs(sizes[0] - 500) <= 2 and abs(sizes[1] - 250) <= 2
