@@ -28,7 +28,8 @@ def test_probe_and_sharded_eval_world1():
     hedl = _hedl()
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(_port())
-    dist.init_process_group("gloo", rank=0, world_size=1)
+    import torch
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
     try:
         kb = abox.c1_kb()
         k = hedl.hedl_kb_load(kb, 0)
