@@ -105,6 +105,8 @@ struct Group {
     bool slice = false;
     bool proj = false;
     bool ex = false;
+    int16_t usp = -1;        // boolean group evaluated over U of direction usp
+    bool ucomp = false;      // EX pack whose fillers are U rows
 };
 
 // ---- planning (host threads, as the paper generates plans in parallel) ----
@@ -290,6 +292,9 @@ struct ChunkTmp {            // per-chunk planning state kept between the sizing
     std::vector<uint32_t> slot, pslot, cover_of_root, members, gdesc, opbase;
     std::vector<int32_t> cover_of_node;
     std::vector<uint8_t> need_full, need_proj, pmode;
+    std::vector<uint64_t> need_u;      // directions whose U rows of the node are read
+    std::vector<uint64_t> u_out;       // directions whose U rows the node (a boolean) computes
+    std::vector<uint32_t> ubase;       // first U-row slot of the node
     std::vector<Group> groups;
 };
 
@@ -301,7 +306,7 @@ struct ChunkTmp {            // per-chunk planning state kept between the sizing
 // rows (M bits instead of N); its operands then only need projected rows, which
 // atoms/TOP have precomputed and computed nodes emit as a scatter epilogue.
 void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> &list, ChunkPlan &cp,
-                bool out_bits, bool use_slice, bool force_slice, uint32_t *rows, uint32_t *prows,
+                bool out_bits, bool use_slice, bool force_slice, uint32_t *rows, uint32_t *prows, uint32_t *urows,
                 std::vector<uint32_t> &local, char *h_blob, size_t *blob_cursor, size_t *heavy_need, bool sizes_only,
                 ChunkTmp &tmp) {
     const uint32_t nn = (uint32_t)list.size();
@@ -335,10 +340,39 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
         need_full.assign(nn, 0);
         need_proj.assign(nn, 0);
         pmode.assign(nn, 0);
+        auto &need_u = tmp.need_u;
+        auto &u_out = tmp.u_out;
+        need_u.assign(nn, 0);
+        u_out.assign(nn, 0);
         if (out_bits)
             for (uint32_t k = 0; k < nroots; ++k) need_full[local[p->root_node[cp.ri + k]]] = 1;
+        // U rows: an EX-pack restriction in direction d reads its
+        // filler only at U_d (the example rows' neighbours).  A boolean over atoms / TOP /
+        // such booleans ("U-capable") demanded over U_d is evaluated over U_d (a row of |U_d|
+        // bits), besides any full or example-projected row it is needed as; other fillers are
+        // computed in full and the pack reads their full rows at U_d.
+        const bool use_u = use_slice && kb->M > 0;
+        std::vector<uint8_t> ucap(nn, 0);
+        if (use_u)
+            for (uint32_t lo = 0; lo < nn;) {                  // bottom-up, level by level
+                uint32_t hi = lo + 1;
+                while (hi < nn && p->nodes[list[hi]].level == p->nodes[list[lo]].level) ++hi;
+                par_for(hi - lo, 1 << 13, [&](size_t a, size_t b) {
+                    for (size_t kk = lo + a; kk < lo + b; ++kk) {
+                        const CNode &n = p->nodes[list[kk]];
+                        bool c = n.kind == NK_AND || n.kind == NK_OR;
+                        for (uint32_t q = 0; c && q < n.op_count; ++q) {
+                            const uint32_t o = p->ops[n.op_begin + q];
+                            if (ref_type(o) == RT_NODE && !ucap[local[ref_id(o)]]) c = false;
+                        }
+                        ucap[kk] = c;
+                    }
+                });
+                lo = hi;
+            }
         // level by level from the top; within a level nodes are independent (operands sit at
-        // lower levels; concurrent writes of 1 to a shared operand flag are benign)
+        // lower levels; concurrent writes of 1 to a shared operand flag are benign, U demands
+        // are atomic ORs)
         for (uint32_t hi = nn; hi > 0;) {
             const uint32_t lvl = p->nodes[list[hi - 1]].level;
             uint32_t lo = hi - 1;
@@ -347,12 +381,29 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                 for (size_t kk = lo + a; kk < lo + b; ++kk) {
                     const CNode &n = p->nodes[list[kk]];
                     const bool isbool = n.kind == NK_AND || n.kind == NK_OR;
-                    pmode[kk] = isbool && !need_full[kk];
+                    const uint64_t nu = need_u[kk];
+                    uint64_t uo = 0;
+                    if (nu) {
+                        if (ucap[kk]) uo = nu;
+                        else need_full[kk] = 1;                 // the packs read its full row
+                    }
+                    u_out[kk] = uo;
+                    pmode[kk] = isbool && !need_full[kk] && (need_proj[kk] || cover_of_node[kk] >= 0);
+                    const bool ex = use_u && n.kind == NK_RESTRICT && !need_full[kk] &&
+                                    slice_class(n.pred, n.n, n.sat) < 2;
                     for (uint32_t q = 0; q < n.op_count; ++q) {
                         const uint32_t o = p->ops[n.op_begin + q];
                         if (ref_type(o) != RT_NODE) continue;
-                        if (pmode[kk]) need_proj[local[ref_id(o)]] = 1;
-                        else need_full[local[ref_id(o)]] = 1;
+                        const uint32_t lo2 = local[ref_id(o)];
+                        if (ex) {
+                            __atomic_fetch_or(&need_u[lo2], 1ull << n.dir, __ATOMIC_RELAXED);
+                        } else if (!isbool) {
+                            need_full[lo2] = 1;
+                        } else {
+                            if (need_full[kk]) need_full[lo2] = 1;
+                            if (pmode[kk]) need_proj[lo2] = 1;
+                            if (uo) __atomic_fetch_or(&need_u[lo2], uo, __ATOMIC_RELAXED);
+                        }
                     }
                 }
             });
@@ -365,6 +416,15 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
         const uint32_t nprows = par_rank(nn, [&](size_t k) { return need_proj[k] != 0; }, pslot);
         cp.nrows = nrows;
         cp.nprows = nprows;
+        // U-row slots: one per direction a boolean computes a U row for
+        auto &ubase = tmp.ubase;
+        ubase.assign(nn, 0);
+        uint32_t nurows = 0;
+        for (uint32_t k = 0; k < nn; ++k) {
+            ubase[k] = nurows;
+            nurows += (uint32_t)__builtin_popcountll(u_out[k]);
+        }
+        cp.nurows = nurows;
         // launch groups: (level, kind, dir) runs of the list; boolean runs split by full/projected
         groups.clear();
         members.clear();
@@ -381,37 +441,69 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                 ++e;
             }
             if (kind == NK_AND) {
-                for (int pm = 0; pm < 2; ++pm) {
+                for (int pm = 0; pm < 2; ++pm) {               // full rows, example-projected rows
                     Group g{kind, key, (uint32_t)members.size(), 0};
                     g.proj = pm;
                     for (uint32_t q = k; q < e; ++q)
-                        if (pmode[q] == pm) members.push_back(q);
+                        if (pm ? pmode[q] != 0 : need_full[q] != 0) members.push_back(q);
                     g.count = (uint32_t)members.size() - g.first;
                     if (g.count) groups.push_back(g);
                 }
-            } else if (kind == NK_RESTRICT && use_slice) {
-                // lane-packable nodes (class 0/1 sort first) needed in full, then those needed only
-                // at the examples (EX packs), then the per-node rest
-                uint32_t ns = 0;
-                while (k + ns < e && slice_class(p->nodes[list[k + ns]].pred, p->nodes[list[k + ns]].n,
-                                                 p->nodes[list[k + ns]].sat) != 2)
-                    ++ns;
-                const bool packs = ns && slice_worthwhile(kb, ns, force_slice);
-                const uint32_t split = packs ? k + ns : k;
-                for (int demand = 0; demand < 2 && packs; ++demand) {     // 0: full rows, 1: examples only
+                uint64_t dirs_u = 0;                           // then one group per U direction
+                for (uint32_t q = k; q < e; ++q) dirs_u |= u_out[q];
+                for (; dirs_u; dirs_u &= dirs_u - 1) {
+                    const int d = __builtin_ctzll(dirs_u);
                     Group g{kind, key, (uint32_t)members.size(), 0};
-                    g.slice = true;
-                    g.ex = demand == 1;
-                    for (uint32_t q = k; q < split; ++q)
-                        if ((need_full[q] == 0) == (demand == 1)) members.push_back(q);
+                    g.usp = (int16_t)d;
+                    for (uint32_t q = k; q < e; ++q)
+                        if (u_out[q] >> d & 1) members.push_back(q);
                     g.count = (uint32_t)members.size() - g.first;
-                    if (g.count) groups.push_back(g);
-                }
-                if (split < e) {
-                    Group g{kind, key, (uint32_t)members.size(), e - split};
-                    for (uint32_t q = split; q < e; ++q) members.push_back(q);
                     groups.push_back(g);
                 }
+            } else if (kind == NK_RESTRICT && use_slice) {
+                // lane-packable nodes (class 0/1 sort first) needed in full -- packed when there
+                // are enough of them -- then those needed only at the examples (EX packs over U
+                // rows, always packed), then the per-node rest
+                uint32_t ns = 0, nf = 0;
+                while (k + ns < e && slice_class(p->nodes[list[k + ns]].pred, p->nodes[list[k + ns]].n,
+                                                 p->nodes[list[k + ns]].sat) != 2) {
+                    nf += need_full[k + ns] != 0;
+                    ++ns;
+                }
+                const bool full_packs = nf && slice_worthwhile(kb, nf, force_slice);
+                const uint32_t first_rest = (uint32_t)members.size();
+                if (full_packs) {
+                    Group g{kind, key, (uint32_t)members.size(), 0};
+                    g.slice = true;
+                    for (uint32_t q = k; q < k + ns; ++q)
+                        if (need_full[q]) members.push_back(q);
+                    g.count = (uint32_t)members.size() - g.first;
+                    groups.push_back(g);
+                }
+                // EX packs: fillers available as U rows of this direction (U-space booleans,
+                // atoms, TOP) in one group, fillers with full rows in another
+                auto u_filler = [&](uint32_t q) {
+                    const uint32_t c = p->ops[p->nodes[list[q]].op_begin];
+                    return use_u && (ref_type(c) != RT_NODE || (u_out[local[ref_id(c)]] >> key & 1));
+                };
+                for (int uc = 1; uc >= 0 && ns > nf; --uc) {
+                    Group g{kind, key, (uint32_t)members.size(), 0};
+                    g.slice = true;
+                    g.ex = true;
+                    g.ucomp = uc;
+                    for (uint32_t q = k; q < k + ns; ++q)
+                        if (!need_full[q] && u_filler(q) == (bool)uc) members.push_back(q);
+                    g.count = (uint32_t)members.size() - g.first;
+                    if (g.count) groups.push_back(g);
+                }
+                (void)first_rest;
+                Group g{kind, key, (uint32_t)members.size(), 0};
+                if (!full_packs)
+                    for (uint32_t q = k; q < k + ns; ++q)
+                        if (need_full[q]) members.push_back(q);
+                for (uint32_t q = k + ns; q < e; ++q) members.push_back(q);
+                g.count = (uint32_t)members.size() - g.first;
+                if (g.count) groups.push_back(g);
             } else {
                 const uint32_t first = (uint32_t)members.size();
                 for (uint32_t q = k; q < e; ++q) members.push_back(q);
@@ -475,6 +567,21 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
         }
     };
     auto out_of = [&](uint32_t k) { return need_full[k] ? rows + (size_t)slot[k] * kb->W4 : nullptr; };
+    // U rows: slot stride = the widest direction's UW4
+    const auto &u_out = tmp.u_out;
+    const auto &ubase = tmp.ubase;
+    uint32_t uw4max = 0;
+    for (const hedl_dir &x : kb->dirs) uw4max = std::max(uw4max, x.UW4);
+    auto urow_of = [&](uint32_t k, int d) -> uint32_t * {
+        return urows + (size_t)(ubase[k] + __builtin_popcountll(u_out[k] & ((1ull << d) - 1))) * uw4max;
+    };
+    auto uptr_of = [&](uint32_t r, int d) -> const uint32_t * {   // U row (direction d) of an operand
+        switch (ref_type(r)) {
+        case RT_NODE: return urow_of(local[ref_id(r)], d);
+        case RT_ATOM: return kb->dirs[d].uconcepts + (size_t)ref_id(r) * kb->dirs[d].UW4;
+        default: return kb->dirs[d].uones;
+        }
+    };
     auto proj_of = [&](uint32_t k) { return need_proj[k] ? prows + (size_t)pslot[k] * kb->MW4 : nullptr; };
     BoolDesc *hb = (BoolDesc *)(h + cp.off_bool);
     Operand *ho = (Operand *)(h + cp.off_ops);
@@ -493,7 +600,27 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
             Task &T = tasks[ti];
             const Group &g = groups[T.g];
             const uint32_t base = tmp.gdesc[T.g];
-            if (g.kind == NK_AND) {
+            if (g.kind == NK_AND && g.usp >= 0) {             // evaluated over U of direction usp
+                const double wb = 4.0 * kb->dirs[g.usp].UW;
+                for (uint32_t m = T.m0; m < T.m1; ++m) {
+                    const uint32_t k = members[m];
+                    const CNode &n = p->nodes[list[k]];
+                    BoolDesc bd;
+                    bd.out = urow_of(k, g.usp);
+                    bd.proj = nullptr;
+                    uint32_t io = tmp.opbase[m];
+                    bd.op_first = io;
+                    bd.op_count = n.op_count;
+                    bd.is_or = n.kind == NK_OR;
+                    bd.cover = -1;
+                    for (uint32_t q = 0; q < n.op_count; ++q) {
+                        const uint32_t o = p->ops[n.op_begin + q];
+                        ho[io++] = Operand{uptr_of(o, g.usp), ref_comp(o) ? 0xffffffffu : 0u, 0};
+                    }
+                    hb[base + (m - g.first)] = bd;
+                    T.bytes += wb * (n.op_count + 1);
+                }
+            } else if (g.kind == NK_AND) {
                 const double wb = 4.0 * (g.proj ? kb->MW : kb->W);
                 for (uint32_t m = T.m0; m < T.m1; ++m) {
                     const uint32_t k = members[m];
@@ -525,7 +652,7 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                     const CNode &n = p->nodes[list[k]];
                     const uint32_t c = p->ops[n.op_begin];
                     RestrictDesc rd;
-                    rd.child = ptr_of(c);
+                    rd.child = g.ucomp ? uptr_of(c, g.key) : ptr_of(c);
                     rd.out = out_of(k);
                     rd.proj = proj_of(k);
                     rd.cmask = ref_comp(c) ? 0xffffffffu : 0u;
@@ -578,7 +705,10 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
     cp.recs.clear();
     for (uint32_t gi = 0; gi < groups.size(); ++gi) {
         const Group &g = groups[gi];
-        cp.recs.push_back(LaunchRec{g.kind, g.key, g.slice, g.proj, g.ex, g.count, tmp.gdesc[gi], 0, 0});
+        LaunchRec lr{g.kind, g.key, g.slice, g.proj, g.ex, g.count, tmp.gdesc[gi], 0, 0};
+        lr.usp = g.usp;
+        lr.ucomp = g.ucomp;
+        cp.recs.push_back(lr);
     }
     for (const Task &T : tasks) {
         cp.recs[T.g].bytes += T.bytes;
@@ -609,15 +739,21 @@ hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, u
         HEDL_CUDA(kb, cudaMemsetAsync(w->prows.p, 0, (size_t)cp.nprows * kb->MW4 * 4, s));   // scatter targets
     for (const LaunchRec &lr : cp.recs) {
         if (lr.kind == NK_AND) {
-            launch_bool(s, lr.proj ? kp : kd, (const BoolDesc *)(d + cp.off_bool) + lr.first_desc, lr.count,
+            KbDev kx = lr.proj ? kp : kd;
+            if (lr.usp >= 0) {                                   // U space of one direction (no coverage)
+                const hedl_dir &du = kb->dirs[lr.usp];
+                kx = KbDev{du.n_u, du.UW, du.UW4, nullptr, nullptr, nullptr, nullptr};
+            }
+            launch_bool(s, kx, (const BoolDesc *)(d + cp.off_bool) + lr.first_desc, lr.count,
                         (const Operand *)(d + cp.off_ops), cov, lr.bytes, kb->npos, kb->nneg);
+
         } else if (lr.kind == NK_RESTRICT) {
             const hedl_dir &dr = kb->dirs[lr.key];
             const RestrictDesc *dd_desc = (const RestrictDesc *)(d + cp.off_res) + lr.first_desc;
             if (lr.slice) {
                 hedl_status st = slice_run(kb, &w->slice.p, &w->slice.bytes, s, kd, lr.key,
                                            lr.cls >= 0 ? nullptr : (const RestrictDesc *)(h + cp.off_res) + lr.first_desc,
-                                           dd_desc, lr.count, cov, lr.ex, lr.cls);
+                                           dd_desc, lr.count, cov, lr.ex, lr.cls, lr.ucomp);
                 if (st) return st;
             } else {
                 DirDev dd{dr.row_ptr, dr.col, dr.heavy_x, dr.heavy_nchunks, dr.chunks, dr.n_heavy, dr.n_chunks,
@@ -655,7 +791,8 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
     PlanCache &pc = w->plan;
     const bool bits = out_bits != nullptr;
     const bool hit = pc.valid && pc.r0 == r0 && pc.r1 == r1 && pc.bits == bits && pc.eflags == eflags &&
-                     pc.rows_base == w->rows.p && pc.heavy_base == w->heavy.p && pc.prows_base == w->prows.p;
+                     pc.rows_base == w->rows.p && pc.heavy_base == w->heavy.p && pc.prows_base == w->prows.p &&
+                     pc.urows_base == w->urows.p;
     hedl_status st;
     if (!hit) {
         // the previous plan's blobs may still be read by queued work: wait, then reuse them
@@ -694,20 +831,24 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
         std::vector<uint32_t> local(p->nodes.size());
         pc.chunks.resize(lists.size());
         std::vector<ChunkTmp> tmps(lists.size());
-        size_t cursor = 0, heavy_need = 16, max_nn = 1, max_cov = 1, max_np = 1;
+        size_t cursor = 0, heavy_need = 16, max_nn = 1, max_cov = 1, max_np = 1, max_nu = 1;
         for (size_t c = 0; c < lists.size(); ++c) {
             ChunkPlan &cp = pc.chunks[c];
             cp.ri = ranges[c].first;
             cp.rc = ranges[c].second;
-            fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, nullptr, nullptr, local, nullptr, &cursor,
+            fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, nullptr, nullptr, nullptr, local, nullptr, &cursor,
                        &heavy_need, true, tmps[c]);
             max_nn = std::max<size_t>(max_nn, cp.nrows);
             max_np = std::max<size_t>(max_np, cp.nprows);
+            max_nu = std::max<size_t>(max_nu, cp.nurows);
             max_cov = std::max<size_t>(max_cov, cp.ncov);
         }
         const double tb = now_ms();
         if ((st = grow(kb, s, w->rows, max_nn * row_bytes + 16, false, PR_ROWS))) return st;
         if ((st = grow(kb, s, w->prows, max_np * kb->MW4 * 4 + 16, false, PR_PROWS))) return st;
+        uint32_t uw4max = 0;
+        for (const hedl_dir &x : kb->dirs) uw4max = std::max(uw4max, x.UW4);
+        if ((st = grow(kb, s, w->urows, max_nu * uw4max * 4 + 16, false, PR_UROWS))) return st;
         if ((st = grow(kb, s, w->heavy, heavy_need, true, PR_HEAVY))) return st;
         if ((st = grow(kb, s, w->counts, max_cov * sizeof(hedl_counts), false, PR_COUNTS))) return st;
         if ((st = reserve_plan(kb, pc, std::max<size_t>(cursor, 256)))) return st;
@@ -717,12 +858,13 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
         pc.rows_base = w->rows.p;
         pc.heavy_base = w->heavy.p;
         pc.prows_base = w->prows.p;
+        pc.urows_base = w->urows.p;
         // phase C + D interleaved: fill chunk c on the host while chunk c-1 runs on the GPU
         for (size_t c = 0; c < lists.size(); ++c) {
             ChunkPlan &cp = pc.chunks[c];
             size_t cur = cp.blob_off;
-            fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, (uint32_t *)w->rows.p, (uint32_t *)w->prows.p, local,
-                       (char *)pc.host, &cur, &heavy_need, false, tmps[c]);
+            fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, (uint32_t *)w->rows.p, (uint32_t *)w->prows.p,
+                       (uint32_t *)w->urows.p, local, (char *)pc.host, &cur, &heavy_need, false, tmps[c]);
             tmps[c] = ChunkTmp();   // release the chunk's planning state
             timing_note("plan: fill chunk", now_ms() - t2);
             HEDL_CUDA(kb, cudaMemcpyAsync((char *)pc.dev + cp.blob_off, (char *)pc.host + cp.blob_off, cp.blob_bytes,
@@ -911,9 +1053,10 @@ extern "C" hedl_status hedl_program_free(hedl_program *p) {
         Workspace *w = (Workspace *)p->ws;
         DeviceGuard dg(p->kb->device);
         if (w->done) cudaEventSynchronize(w->done);
-        const int roles[] = {PR_ROWS, PR_PROWS, PR_HEAVY, PR_COUNTS, PR_SLICE};
+        const int roles[] = {PR_ROWS, PR_PROWS, PR_HEAVY, PR_COUNTS, PR_SLICE, PR_UROWS};
         int ri = 0;
-        for (DevBuf *b : {&w->rows, &w->prows, &w->heavy, &w->counts, &w->slice}) pool_give(p->kb, roles[ri++], b->p, b->bytes);
+        for (DevBuf *b : {&w->rows, &w->prows, &w->heavy, &w->counts, &w->slice, &w->urows})
+            pool_give(p->kb, roles[ri++], b->p, b->bytes);
         pool_give(p->kb, PR_COUNTS, w->stage.p, w->stage.bytes);
         if (w->stage_host) cudaFreeHost(w->stage_host);
         pool_give(p->kb, PR_PLAN_HOST, w->plan.host, w->plan.cap);

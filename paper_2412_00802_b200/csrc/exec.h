@@ -18,6 +18,8 @@ struct LaunchRec {
     uint32_t count, first_desc;
     double bytes, bytes2;
     int8_t cls = -1;       // lane-pack class of the whole group (device plans), -1 = per descriptor
+    int16_t usp = -1;      // boolean group over U of direction usp
+    bool ucomp = false;    // EX pack reading its fillers' U rows
 };
 
 struct ChunkPlan {
@@ -25,6 +27,7 @@ struct ChunkPlan {
     uint32_t nn, ncov, nrows, nprows;
     size_t blob_off, blob_bytes;          // into PlanCache host/device blobs
     size_t off_bool, off_ops, off_res, off_dr, off_str, off_cov, off_rows;
+    uint32_t nurows = 0;
     std::vector<LaunchRec> recs;
 };
 
@@ -32,7 +35,7 @@ struct PlanCache {
     bool valid = false;
     uint32_t r0 = 0, r1 = 0, eflags = 0;
     bool bits = false;
-    void *rows_base = nullptr, *heavy_base = nullptr, *prows_base = nullptr;
+    void *rows_base = nullptr, *heavy_base = nullptr, *prows_base = nullptr, *urows_base = nullptr;
     std::vector<ChunkPlan> chunks;
     void *host = nullptr;                 // pinned descriptor blob
     void *dev = nullptr;                  // device descriptor blob
@@ -40,7 +43,7 @@ struct PlanCache {
 };
 
 struct Workspace {
-    DevBuf rows, prows, heavy, counts, slice, stage;
+    DevBuf rows, prows, heavy, counts, slice, stage, urows;
     uint8_t *pats = nullptr;             // device copy of the program's CONTAIN patterns
     std::vector<uint64_t> pat_off;       // their offsets
     hedl_counts *stage_host = nullptr;   // pinned staging of host-bound counts

@@ -108,6 +108,11 @@ struct hedl_dir {                  // one role direction
     uint32_t *ex_ccol = nullptr;       // device: compact T index of each such edge's neighbour
     uint32_t *ex_umask = nullptr;      // device [W4]: bit y&31 of word y>>5 set iff y in U
     uint32_t *ex_ubase = nullptr;      // device [W4]: |U ∩ [0, 32w)|
+    // U-space rows: a row over U (bit t = individual U[t]),
+    // UW4 words (padded to 8); the fillers of EX-pack restrictions are evaluated / stored here
+    uint32_t UW = 0, UW4 = 0;
+    uint32_t *uconcepts = nullptr;     // device [C][UW4]
+    uint32_t *uones = nullptr;         // device [UW4], tail-masked TOP row over U
 };
 
 struct hedl_data {
@@ -213,7 +218,7 @@ hedl_status cuda_fail(const hedl_kb *kb, cudaError_t e, const char *where);
 
 // ---- workspace pool (per KB) ---------------------------------------------------
 enum PoolRole { PR_ROWS, PR_PROWS, PR_HEAVY, PR_COUNTS, PR_SLICE, PR_PLAN_DEV, PR_PLAN_HOST, PR_DC_SCRATCH, PR_DC_PROG,
-                PR_DPLAN, PR_DPLAN_HOST, PR_N };
+                PR_DPLAN, PR_DPLAN_HOST, PR_UROWS, PR_N };
 void *pool_take(const hedl_kb *kb, int role, size_t need, size_t *got);
 void pool_give(const hedl_kb *kb, int role, void *p, size_t bytes);
 void pool_release_all(hedl_kb *kb);

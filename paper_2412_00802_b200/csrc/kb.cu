@@ -412,6 +412,24 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
                         ecol[k] = ubase[y >> 5] + (uint32_t)__builtin_popcount(umask[y >> 5] & ((1u << (y & 31)) - 1u));
                     }
                 dr.n_u = nu;
+                dr.UW = (nu + 31) / 32;
+                dr.UW4 = (dr.UW + 7) & ~7u;
+                {
+                    std::vector<uint32_t> ul;
+                    ul.reserve(nu);
+                    for (uint32_t w = 0; w < W4; ++w)
+                        for (uint32_t m = umask[w]; m; m &= m - 1) ul.push_back(32 * w + __builtin_ctz(m));
+                    std::vector<uint32_t> uc((uint64_t)C * dr.UW4, 0), uon(dr.UW4, 0);
+                    for (uint32_t t = 0; t < nu; ++t) {
+                        const uint32_t y = ul[t], bit = 1u << (t & 31);
+                        uon[t >> 5] |= bit;
+                        for (uint32_t c = 0; c < C; ++c)
+                            if (desc->concept_bits[(uint64_t)c * W + (y >> 5)] >> (y & 31) & 1u) uc[(uint64_t)c * dr.UW4 + (t >> 5)] |= bit;
+                    }
+                    if ((s = upload(kb, st, &dr.uconcepts, uc.data(), uc.size()))) return bail(s);
+                    if ((s = upload(kb, st, &dr.uones, uon.data(), uon.size()))) return bail(s);
+                    if (cudaStreamSynchronize(st) != cudaSuccess) return bail(fail(HEDL_ERR_CUDA, "upload failed"));
+                }
                 if ((s = upload(kb, st, &dr.ex_rp, erp.data(), erp.size()))) return bail(s);
                 if ((s = upload(kb, st, &dr.ex_ccol, ecol.data(), ecol.size()))) return bail(s);
                 if ((s = upload(kb, st, &dr.ex_umask, umask.data(), umask.size()))) return bail(s);

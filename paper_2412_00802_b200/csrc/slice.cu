@@ -617,12 +617,12 @@ uint32_t slice_class(uint32_t pred, uint32_t n, uint32_t sat) {
 
 hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream_t s, const KbDev &kd, uint32_t dirid,
                       const RestrictDesc *h_desc, const RestrictDesc *d_desc, uint32_t n, hedl_counts *counts, bool ex,
-                      int fixed_cls) {
+                      int fixed_cls, bool ucomp) {
     const hedl_dir &dr = kb->dirs[dirid];
     if (ex && !kb->M) return HEDL_OK;                     // no examples: nothing to evaluate
     const size_t t_bytes = (size_t)kb->W4 * 32 * 32;     // full packs: 32 B per individual
     size_t nu_max = 0;
-    for (const hedl_dir &x : kb->dirs) nu_max = std::max<size_t>(nu_max, x.n_u);
+    for (const hedl_dir &x : kb->dirs) nu_max = std::max<size_t>({nu_max, (size_t)x.n_u, (size_t)x.UW4 * 32});
     const size_t tx_bytes = std::max<size_t>(nu_max * 32, 256);   // EX packs: 32 B per neighbour of an example
     // one fixed layout for every direction (sized by the largest heavy lists), so the
     // self-cleaning accumulators of one direction never alias another's results:
@@ -702,11 +702,22 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             sc.t_stride = tx_bytes / 16;
         }
         prof_begin(s, KC_SLICE_IN);
-        k_slice_pack<<<dim3(cdiv(kb->W4, PK_WORDS), packs), 256, pk_smem, s>>>(kd, dd, run, sc.T, sc.t_stride,
-                                                                             ex ? dr.ex_umask : nullptr,
-                                                                             ex ? dr.ex_ubase : nullptr);
-        count_launch();
-        prof_end(s, KC_SLICE_IN, 4.0 * kb->W * run + 32.0 * (ex ? (double)dr.n_u : 32.0 * kb->W4) * packs, packs);
+        if (ex && ucomp) {
+            // fillers are U rows: pack them whole (T index = U index), no compaction
+            KbDev ku = kd;
+            ku.W4 = dr.UW4;
+            if (dr.UW4)
+                k_slice_pack<<<dim3(cdiv(dr.UW4, PK_WORDS), packs), 256, pk_smem, s>>>(ku, dd, run, sc.T, sc.t_stride,
+                                                                                     nullptr, nullptr);
+            count_launch();
+            prof_end(s, KC_SLICE_IN, 4.0 * dr.UW * run + 32.0 * dr.n_u * packs, packs);
+        } else {
+            k_slice_pack<<<dim3(cdiv(kb->W4, PK_WORDS), packs), 256, pk_smem, s>>>(kd, dd, run, sc.T, sc.t_stride,
+                                                                                 ex ? dr.ex_umask : nullptr,
+                                                                                 ex ? dr.ex_ubase : nullptr);
+            count_launch();
+            prof_end(s, KC_SLICE_IN, 4.0 * kb->W * run + 32.0 * (ex ? (double)dr.n_u : 32.0 * kb->W4) * packs, packs);
+        }
         const SliceDir &hd = ex ? sdx : sd;
         if (hd.n_chunks) {
             prof_begin(s, KC_SLICE_HEAVY);

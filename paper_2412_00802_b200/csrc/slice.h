@@ -13,7 +13,9 @@ uint32_t slice_class(uint32_t pred, uint32_t n, uint32_t sat);
 // h_desc: host copies of the group's restriction descriptors (pinned, valid
 // until the stream reaches this point); d_desc: the same on the device.
 // fixed_cls >= 0: every descriptor has this class (h_desc may be null).
+// ucomp (EX packs): the descriptors' child rows are U rows of this direction (DESIGN.md
+// "U-projected rows"), else full rows compacted to U while packing.
 hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream_t s, const KbDev &kd,
                       uint32_t dir, const RestrictDesc *h_desc, const RestrictDesc *d_desc, uint32_t n,
-                      hedl_counts *counts, bool ex, int fixed_cls = -1);
+                      hedl_counts *counts, bool ex, int fixed_cls = -1, bool ucomp = false);
 }  // namespace hedl
