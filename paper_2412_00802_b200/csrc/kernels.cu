@@ -305,35 +305,50 @@ __global__ void __launch_bounds__(256) k_restrict_heavy(KbDev kb, DirDev dir, co
 }
 
 // ------------------------------------------------------------------------------
+// warp per 4 output words (lane = individual): the 4 words' row bounds and binary-search
+// probes are issued together (4 independent loads in flight per lane instead of 1)
+constexpr uint32_t kDrWords = 4;
+
 __global__ void __launch_bounds__(256) k_drange(KbDev kb, const uint32_t *__restrict__ row_ptr,
                                                 const float *__restrict__ val, const DrangeDesc *__restrict__ descs,
                                                 hedl_counts *counts) {
     const DrangeDesc d = descs[blockIdx.y];
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t w = blockIdx.x * 8 + (threadIdx.x >> 5);
-    uint32_t tp = 0, fp = 0;
-    if (w < kb.W4) {
-        uint32_t word = 0;
-        if (w < kb.W) {
-            const uint32_t x = (w << 5) + lane;
-            bool res = false;
-            if (x < kb.N) {
-                uint32_t lo = __ldg(row_ptr + x), hi = __ldg(row_ptr + x + 1);
-                // first value >= d.lo in the ascending segment, then test <= d.hi
-                while (lo < hi) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (__ldg(val + mid) < d.lo) lo = mid + 1; else hi = mid;
-                }
-                res = lo < __ldg(row_ptr + x + 1) && __ldg(val + lo) <= d.hi;
-            }
-            word = __ballot_sync(FULL, res);
+    const uint32_t w0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * kDrWords;
+    uint32_t lo[kDrWords], hi[kDrWords], end[kDrWords];
+#pragma unroll
+    for (uint32_t u = 0; u < kDrWords; ++u) {
+        const uint32_t x = ((w0 + u) << 5) + lane;
+        lo[u] = hi[u] = end[u] = 0;
+        if (w0 + u < kb.W && x < kb.N) {
+            lo[u] = __ldg(row_ptr + x);
+            hi[u] = end[u] = __ldg(row_ptr + x + 1);
         }
-        if (lane == 0) {
+    }
+    // first value >= d.lo in each ascending segment (interleaved binary searches)
+    for (;;) {
+        bool any = false;
+#pragma unroll
+        for (uint32_t u = 0; u < kDrWords; ++u)
+            if (lo[u] < hi[u]) {
+                any = true;
+                const uint32_t mid = (lo[u] + hi[u]) >> 1;
+                if (__ldg(val + mid) < d.lo) lo[u] = mid + 1; else hi[u] = mid;
+            }
+        if (!any) break;
+    }
+    uint32_t tp = 0, fp = 0;
+#pragma unroll
+    for (uint32_t u = 0; u < kDrWords; ++u) {
+        const uint32_t w = w0 + u;
+        const bool res = lo[u] < end[u] && __ldg(val + lo[u]) <= d.hi;
+        const uint32_t word = __ballot_sync(FULL, res);
+        if (lane == 0 && w < kb.W4) {
             if (d.proj && w < kb.W) proj_scatter(kb, d.proj, w, word);
             if (d.out) d.out[w] = word;
-            if (d.cover >= 0) {
-                tp = __popc(word & __ldg(kb.pos + w));
-                fp = __popc(word & __ldg(kb.neg + w));
+            if (d.cover >= 0 && w < kb.W) {
+                tp += __popc(word & __ldg(kb.pos + w));
+                fp += __popc(word & __ldg(kb.neg + w));
             }
         }
     }
@@ -370,48 +385,66 @@ __global__ void __launch_bounds__(256) k_string(KbDev kb, StrDev sd, const Strin
                                                 hedl_counts *counts) {
     const StringDesc d = descs[blockIdx.y];
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t w = blockIdx.x * 8 + (threadIdx.x >> 5);
-    uint32_t tp = 0, fp = 0;
-    if (w < kb.W4) {
-        uint32_t word = 0;
-        if (w < kb.W) {
-            const uint32_t x = (w << 5) + lane;
-            uint32_t e0 = 0, e1 = 0;
-            if (x < kb.N) {
-                e0 = __ldg(sd.row_ptr + x);
-                e1 = __ldg(sd.row_ptr + x + 1);
-            }
-            bool res = false;
-            if (d.mode == SM_EQUAL) {
-                uint32_t lo = e0, hi = e1;          // first id >= vid
-                while (lo < hi) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (__ldg(sd.vid + mid) < d.vid) lo = mid + 1; else hi = mid;
-                }
-                res = lo < e1 && __ldg(sd.vid + lo) == d.vid;
-                word = __ballot_sync(FULL, res);
-            } else {
-                const bool longrow = e1 - e0 > kStrLaneDeg;
-                if (!longrow)
-                    for (uint32_t e = e0; e < e1 && !res; ++e) res = value_contains(sd, __ldg(sd.vid + e), d);
-                word = __ballot_sync(FULL, res);
-                for (uint32_t m = __ballot_sync(FULL, longrow); m; m &= m - 1) {
-                    const uint32_t L = __ffs(m) - 1;
-                    const uint32_t a = __shfl_sync(FULL, e0, L), b = __shfl_sync(FULL, e1, L);
-                    for (uint32_t base = a; base < b; base += 32) {          // uniform trip count
-                        const uint32_t e = base + lane;
-                        const bool hit = e < b && value_contains(sd, __ldg(sd.vid + e), d);
-                        if (__any_sync(FULL, hit)) { word |= 1u << L; break; }
-                    }
-                }
-            }
+    const uint32_t w0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * kDrWords;   // 4 words per warp
+    uint32_t e0[kDrWords], e1[kDrWords];
+#pragma unroll
+    for (uint32_t u = 0; u < kDrWords; ++u) {
+        const uint32_t x = ((w0 + u) << 5) + lane;
+        e0[u] = e1[u] = 0;
+        if (w0 + u < kb.W && x < kb.N) {
+            e0[u] = __ldg(sd.row_ptr + x);
+            e1[u] = __ldg(sd.row_ptr + x + 1);
         }
-        if (lane == 0) {
-            if (d.proj && w < kb.W) proj_scatter(kb, d.proj, w, word);
-            if (d.out) d.out[w] = word;
-            if (d.cover >= 0) {
-                tp = __popc(word & __ldg(kb.pos + w));
-                fp = __popc(word & __ldg(kb.neg + w));
+    }
+    uint32_t words[kDrWords];
+    if (d.mode == SM_EQUAL) {
+        uint32_t lo[kDrWords], hi[kDrWords];
+#pragma unroll
+        for (uint32_t u = 0; u < kDrWords; ++u) { lo[u] = e0[u]; hi[u] = e1[u]; }
+        for (;;) {                                          // first id >= vid, searches interleaved
+            bool any = false;
+#pragma unroll
+            for (uint32_t u = 0; u < kDrWords; ++u)
+                if (lo[u] < hi[u]) {
+                    any = true;
+                    const uint32_t mid = (lo[u] + hi[u]) >> 1;
+                    if (__ldg(sd.vid + mid) < d.vid) lo[u] = mid + 1; else hi[u] = mid;
+                }
+            if (!any) break;
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < kDrWords; ++u)
+            words[u] = __ballot_sync(FULL, lo[u] < e1[u] && __ldg(sd.vid + lo[u]) == d.vid);
+    } else {
+#pragma unroll
+        for (uint32_t u = 0; u < kDrWords; ++u) {
+            bool res = false;
+            const bool longrow = e1[u] - e0[u] > kStrLaneDeg;
+            if (!longrow)
+                for (uint32_t e = e0[u]; e < e1[u] && !res; ++e) res = value_contains(sd, __ldg(sd.vid + e), d);
+            uint32_t word = __ballot_sync(FULL, res);
+            for (uint32_t m = __ballot_sync(FULL, longrow); m; m &= m - 1) {
+                const uint32_t L = __ffs(m) - 1;
+                const uint32_t a = __shfl_sync(FULL, e0[u], L), b = __shfl_sync(FULL, e1[u], L);
+                for (uint32_t base = a; base < b; base += 32) {          // uniform trip count
+                    const uint32_t e = base + lane;
+                    const bool hit = e < b && value_contains(sd, __ldg(sd.vid + e), d);
+                    if (__any_sync(FULL, hit)) { word |= 1u << L; break; }
+                }
+            }
+            words[u] = word;
+        }
+    }
+    uint32_t tp = 0, fp = 0;
+#pragma unroll
+    for (uint32_t u = 0; u < kDrWords; ++u) {
+        const uint32_t w = w0 + u;
+        if (lane == 0 && w < kb.W4) {
+            if (d.proj && w < kb.W) proj_scatter(kb, d.proj, w, words[u]);
+            if (d.out) d.out[w] = words[u];
+            if (d.cover >= 0 && w < kb.W) {
+                tp += __popc(words[u] & __ldg(kb.pos + w));
+                fp += __popc(words[u] & __ldg(kb.neg + w));
             }
         }
     }
@@ -488,7 +521,7 @@ void launch_restrict(cudaStream_t s, const KbDev &kb, const DirDev &dir, const R
 
 void launch_drange(cudaStream_t s, const KbDev &kb, const uint32_t *row_ptr, const float *val,
                    const DrangeDesc *d_desc, uint32_t n_desc, hedl_counts *counts, double alg_bytes) {
-    const uint32_t gx = cdiv(kb.W4, 8);
+    const uint32_t gx = cdiv(kb.W4, 8 * kDrWords);
     if (!gx) return;
     for (uint32_t off = 0; off < n_desc; off += 65535) {
         const uint32_t nd = n_desc - off < 65535 ? n_desc - off : 65535;
@@ -501,7 +534,7 @@ void launch_drange(cudaStream_t s, const KbDev &kb, const uint32_t *row_ptr, con
 
 void launch_string(cudaStream_t s, const KbDev &kb, const StrDev &sd, const StringDesc *d_desc, uint32_t n_desc,
                    hedl_counts *counts, double alg_bytes) {
-    const uint32_t gx = cdiv(kb.W4, 8);
+    const uint32_t gx = cdiv(kb.W4, 8 * kDrWords);
     if (!gx) return;
     for (uint32_t off = 0; off < n_desc; off += 65535) {
         const uint32_t nd = n_desc - off < 65535 ? n_desc - off : 65535;
