@@ -34,6 +34,7 @@ struct NoInitAlloc : std::allocator<T> {
 // heavy  : deg >  kHeavyDeg      CTA chunks of kHeavyChunk edges, atomics + last-CTA finalise
 constexpr uint32_t kLightDeg = 32;
 constexpr uint32_t kHeavyDeg = 512;
+constexpr uint32_t kMidDeg = 128;     // lane-packed sweep: medium rows up to this degree go 4 per warp
 constexpr uint32_t kHeavyChunk = 4096;
 constexpr uint32_t kTopKMax = 4096;       // hedl_score_topk: k <= this
 
@@ -87,6 +88,8 @@ struct hedl_dir {                  // one role direction
     uint32_t n_tiles = 0;
     uint4 *tiles = nullptr;            // device [n_tiles + 1]
     uint32_t *order = nullptr;         // device [N - n_heavy]: per tile medium rows then light rows, degree-descending
+    uint32_t *tile_rank = nullptr;     // device [n_tiles]: tiles in decreasing sweep cost (persistent scheduling)
+    uint32_t *tile_nbig = nullptr;     // device [n_tiles]: medium rows of the tile with deg > kMidDeg
     // light rows of each tile in SELL-16 slices (16 rows of similar degree, neighbours interleaved
     // so the 16 row-pairs of a warp read 16 consecutive indices per step; pads = 0xffffffff)
     uint32_t *tile_slice = nullptr;    // device [n_tiles + 1]: first slice of each tile

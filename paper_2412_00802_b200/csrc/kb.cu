@@ -360,6 +360,31 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
             if ((s = upload(kb, st, &dr.tiles, tiles.data(), tiles.size()))) return bail(s);
             if ((s = upload(kb, st, &dr.order, order.data(), order.size()))) return bail(s);
             {
+                // tiles in decreasing sweep cost (edges of their light and medium rows + a fixed
+                // share for the transpose-back): the persistent tile kernel takes them in this
+                // order, so the longest tiles start first (LPT) and the tail is short
+                std::vector<uint64_t> cost(dr.n_tiles);
+                std::vector<uint32_t> rank(dr.n_tiles);
+                for (uint32_t t = 0; t < dr.n_tiles; ++t) {
+                    uint64_t c = 2048;
+                    for (uint32_t i = tiles[t].x; i < tiles[t + 1].x; ++i)
+                        c += h.row_ptr[order[i] + 1] - h.row_ptr[order[i]];
+                    cost[t] = c;
+                    rank[t] = t;
+                }
+                std::stable_sort(rank.begin(), rank.end(), [&](uint32_t a, uint32_t b) { return cost[a] > cost[b]; });
+                if (dr.n_tiles && (s = upload(kb, st, &dr.tile_rank, rank.data(), rank.size()))) return bail(s);
+                // medium rows are degree-descending: the big ones (deg > kMidDeg) come first
+                std::vector<uint32_t> nbig(dr.n_tiles);
+                for (uint32_t t = 0; t < dr.n_tiles; ++t) {
+                    uint32_t nb = 0;
+                    for (uint32_t i = tiles[t].x; i < tiles[t].x + tiles[t].y; ++i)
+                        nb += h.row_ptr[order[i] + 1] - h.row_ptr[order[i]] > kMidDeg;
+                    nbig[t] = nb;
+                }
+                if (dr.n_tiles && (s = upload(kb, st, &dr.tile_nbig, nbig.data(), nbig.size()))) return bail(s);
+            }
+            {
                 std::vector<uint32_t> tslice(dr.n_tiles + 1), soff, sw, scol;
                 for (uint32_t t = 0; t < dr.n_tiles; ++t) {
                     tslice[t] = (uint32_t)soff.size();

@@ -30,6 +30,8 @@ struct SliceDir {
     const uint32_t *row_ptr, *col;
     const uint4 *tiles;           // [n_tiles + 1] {order begin, n_med, n_light, heavy begin}
     const uint32_t *order;
+    const uint32_t *tile_rank;    // [n_tiles] tiles in decreasing sweep cost
+    const uint32_t *tile_nbig;    // [n_tiles] medium rows with deg > kMidDeg (the first of the tile's medium rows)
     const uint32_t *tile_slice, *sell_off, *sell_w, *sell_col;   // SELL-16 light rows
     const uint32_t *heavy_x, *heavy_nchunks;
     const uint4 *chunks;
@@ -126,33 +128,77 @@ __device__ void build_consts(PackConst &pc, const RestrictDesc *__restrict__ d, 
 // 16 B halves of one 32 B sector of T[y] with one warp instruction.
 constexpr int HW = 4;
 
+// COUNT accumulators are 5 bit planes (count mod 32) plus a sticky overflow plane (count
+// >= 32 seen); fold() saturates the planes to 31 where it is set, so every predicate
+// sees min(cnt, 31) -- exact for n <= 30 (pred(min(cnt, sat)) == pred(cnt)).
 template <bool COUNT>
 struct Acc {
     uint32_t c[COUNT ? NPL : 1][HW];
+    uint32_t ov[COUNT ? HW : 1];
     __device__ __forceinline__ void zero() {
 #pragma unroll
         for (int q = 0; q < (COUNT ? NPL : 1); ++q)
 #pragma unroll
             for (int k = 0; k < HW; ++k) c[q][k] = 0;
+#pragma unroll
+        for (int k = 0; k < (COUNT ? HW : 1); ++k) ov[k] = 0;
     }
     __device__ __forceinline__ void add1(int k, uint32_t v) {
         if (!COUNT) {
             c[0][k] |= v;
         } else {
-            uint32_t s = FULL;
-#pragma unroll
-            for (int q = 0; q < NPL; ++q) s &= c[q][k];
-            uint32_t carry = v & ~s;            // saturated lanes stay at 31
+            uint32_t carry = v;                  // half-adder ripple, carry out -> overflow
 #pragma unroll
             for (int q = 0; q < NPL; ++q) {
                 const uint32_t t = c[q][k] & carry;
                 c[q][k] ^= carry;
                 carry = t;
             }
+            ov[k & (COUNT ? HW - 1 : 0)] |= carry;
         }
     }
     __device__ __forceinline__ void add(const uint4 v) { add1(0, v.x); add1(1, v.y); add1(2, v.z); add1(3, v.w); }
-    // saturating add of another accumulator (bit-sliced ripple-carry adder)
+    // four inputs per word with a carry-save tree: two full adders at weight 1, one at
+    // weight 2, then a half-adder ripple (13 LOP3-class ops per word instead of ~50)
+    __device__ __forceinline__ void add4w(int k, uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3) {
+        if (!COUNT) {
+            c[0][k] |= v0 | v1 | v2 | v3;
+        } else {
+            uint32_t s0 = c[0][k];
+            const uint32_t k1a = (s0 & v0) | (s0 & v1) | (v0 & v1);
+            s0 ^= v0 ^ v1;
+            const uint32_t k1b = (s0 & v2) | (s0 & v3) | (v2 & v3);
+            c[0][k] = s0 ^ v2 ^ v3;
+            const uint32_t s1 = c[1][k];
+            uint32_t carry = (s1 & k1a) | (s1 & k1b) | (k1a & k1b);
+            c[1][k] = s1 ^ k1a ^ k1b;
+#pragma unroll
+            for (int q = 2; q < NPL; ++q) {
+                const uint32_t t = c[q][k] & carry;
+                c[q][k] ^= carry;
+                carry = t;
+            }
+            ov[k & (COUNT ? HW - 1 : 0)] |= carry;
+        }
+    }
+    __device__ __forceinline__ void add4(const uint4 a, const uint4 b, const uint4 c4, const uint4 d) {
+        add4w(0, a.x, b.x, c4.x, d.x);
+        add4w(1, a.y, b.y, c4.y, d.y);
+        add4w(2, a.z, b.z, c4.z, d.z);
+        add4w(3, a.w, b.w, c4.w, d.w);
+    }
+    // saturate the planes where the overflow plane is set (planes then hold min(cnt, 31))
+    __device__ __forceinline__ void fold() {
+        if (COUNT) {
+#pragma unroll
+            for (int k = 0; k < HW; ++k) {
+#pragma unroll
+                for (int q = 0; q < NPL; ++q) c[q][k] |= ov[k & (COUNT ? HW - 1 : 0)];
+                ov[k & (COUNT ? HW - 1 : 0)] = 0;
+            }
+        }
+    }
+    // saturating add of another (folded) accumulator (bit-sliced ripple-carry adder)
     __device__ __forceinline__ void merge(const Acc &o) {
 #pragma unroll
         for (int k = 0; k < HW; ++k) {
@@ -171,10 +217,13 @@ struct Acc {
             }
         }
     }
-    // combine the 16 pairs of a warp (lanes of equal parity); every lane gets its half's total
+    // combine the TOP/2+... lane pairs of an aligned group of 2*TOP lanes (lanes of equal
+    // parity); every lane gets its half's total.  TOP = 16: the whole warp.
+    template <int TOP = 16>
     __device__ __forceinline__ void warp_reduce_pairs() {
+        fold();
 #pragma unroll
-        for (int off = 16; off >= 2; off >>= 1) {
+        for (int off = TOP; off >= 2; off >>= 1) {
             Acc o;
 #pragma unroll
             for (int q = 0; q < (COUNT ? NPL : 1); ++q)
@@ -185,10 +234,11 @@ struct Acc {
     }
     __device__ __forceinline__ uint32_t result(const PackConst &pc, int kk, int k) const {
         if (!COUNT) return ((c[0][k] ^ pc.fl[kk]) & pc.am[kk]) | pc.om[kk];
+        const uint32_t o = ov[k & (COUNT ? HW - 1 : 0)];
         uint32_t gt = 0, eq = FULL, nz = 0;
 #pragma unroll
         for (int q = NPL - 1; q >= 0; --q) {
-            const uint32_t cq = c[q][k], nq = pc.nb[q][kk];
+            const uint32_t cq = c[q][k] | o, nq = pc.nb[q][kk];
             gt |= eq & cq & ~nq;
             eq &= ~(cq ^ nq);
             nz |= cq;
@@ -207,10 +257,7 @@ __device__ __forceinline__ void scan_edges(Acc<COUNT> &acc, const uint32_t *__re
         const uint32_t y2 = __ldg(col + e + 2 * step), y3 = __ldg(col + e + 3 * step);
         const uint4 v0 = __ldg(T + 2ull * y0 + half), v1 = __ldg(T + 2ull * y1 + half);
         const uint4 v2 = __ldg(T + 2ull * y2 + half), v3 = __ldg(T + 2ull * y3 + half);
-        acc.add(v0);
-        acc.add(v1);
-        acc.add(v2);
-        acc.add(v3);
+        acc.add4(v0, v1, v2, v3);
     }
     for (; e < b; e += step) acc.add(__ldg(T + 2ull * __ldg(col + e) + half));
 }
@@ -321,7 +368,7 @@ __global__ void __launch_bounds__(256) k_slice_heavy(SliceDir dir, SliceScratch 
     Acc<COUNT> acc;
     acc.zero();
     scan_edges<COUNT>(acc, dir.col, sc.T, ch.y + (threadIdx.x >> 1), ch.z, 128, half);
-    acc.warp_reduce_pairs();
+    acc.template warp_reduce_pairs<16>();
     if (lane < 2)
         for (int q = 0; q < (COUNT ? NPL : 1); ++q)
             for (int k = 0; k < HW; ++k) red[wid][half][q][k] = acc.c[q][k];
@@ -387,26 +434,70 @@ __global__ void __launch_bounds__(256) k_slice_heavy(SliceDir dir, SliceScratch 
 }
 
 // ------------------------------------------------------------------------------
-// tile of 1024 consecutive individuals per CTA (256 threads = 128 lane pairs).
+// acc += T[y] over the neighbours of one row split across S lane pairs (this pair takes
+// edges e, e+S, e+2S, ... below b).  Software-pipelined: the next step's four neighbour
+// indices are loaded before this step's four T gathers, so the CSR stream (DRAM) and the
+// T gathers (L2) overlap instead of adding up.
+template <bool COUNT>
+__device__ __forceinline__ void scan_strided(Acc<COUNT> &acc, const uint32_t *__restrict__ col, const uint4 *__restrict__ T,
+                                             uint32_t e, uint32_t b, uint32_t S, uint32_t half) {
+    uint32_t y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) y[u] = e + S * u < b ? __ldg(col + e + S * u) : 0xffffffffu;
+    for (; e < b; e += 4 * S) {
+        uint32_t yn[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) yn[u] = e + S * (4 + u) < b ? __ldg(col + e + S * (4 + u)) : 0xffffffffu;
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = y[u] != 0xffffffffu ? __ldg(T + 2ull * y[u] + half) : make_uint4(0, 0, 0, 0);
+        acc.add4(v[0], v[1], v[2], v[3]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) y[u] = yn[u];
+    }
+}
+
+// one SELL-16 slice (16 rows of similar degree, neighbour k of row i at c[16k + i]), a lane
+// pair per row, the same software pipeline over the slice's width w (a multiple of 4)
+template <bool COUNT>
+__device__ __forceinline__ void scan_slice_pipelined(Acc<COUNT> &acc, const uint32_t *__restrict__ c, const uint4 *__restrict__ T,
+                                                     uint32_t w, uint32_t half) {
+    if (!w) return;
+    uint32_t y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) y[u] = __ldg(c + u * 16);
+    for (uint32_t k = 0; k < w; k += 4) {
+        uint32_t yn[4];
+        const bool more = k + 4 < w;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) yn[u] = more ? __ldg(c + (k + 4 + u) * 16) : 0xffffffffu;
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = y[u] != 0xffffffffu ? __ldg(T + 2ull * y[u] + half) : make_uint4(0, 0, 0, 0);
+        acc.add4(v[0], v[1], v[2], v[3]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) y[u] = yn[u];
+    }
+}
+
+// ------------------------------------------------------------------------------
+// Persistent sweep over 1024-individual tiles (256 threads = 128 lane pairs per CTA,
+// grid = resident CTAs).  CTAs take tiles from a global counter in decreasing-cost order
+// (dir.tile_rank, LPT), and inside a tile the warps take work items (medium rows, then
+// SELL slices, both degree-descending) from a shared counter, so neither the grid nor
+// the CTA waits on a statically unlucky share.  The counter pair `sched` is self-cleaning:
+// the last CTA to finish resets it for the next launch on the stream.
 template <bool COUNT>
 __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, SliceScratch sc,
                                                                    const RestrictDesc *__restrict__ d, uint32_t count,
-                                                                   hedl_counts *counts, uint32_t dbg) {
+                                                                   hedl_counts *counts, uint32_t *sched, uint32_t dbg) {
     extern __shared__ uint32_t smem[];
     PackConst &pc = *reinterpret_cast<PackConst *>(smem);
     uint32_t *ot = smem + sizeof(PackConst) / 4;          // [1024][TROW]
-    const uint32_t t = blockIdx.x;
-    const uint32_t x0 = t * 1024;
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, half = lane & 1;
     __shared__ uint32_t s_exm[32], s_exb[32];
-    if (x0 + 1024 > kb.N)                                  // only the last tile has rows >= N (left 0)
-        for (uint32_t i = threadIdx.x; i < 1024 * TROW; i += 256) ot[i] = 0;
-    if (threadIdx.x < 32) {
-        const uint32_t w = t * 32 + threadIdx.x;
-        s_exm[threadIdx.x] = w < kb.W ? __ldg(kb.ex_mask + w) : 0u;
-        s_exb[threadIdx.x] = w < kb.W ? __ldg(kb.ex_base + w) : 0u;
-    }
-    // this lane's node for the transpose-back phase, fetched early (its latency hides under the sweep)
+    __shared__ uint32_t s_tile, s_item;
+    // this lane's node for the transpose-back phase (fixed for the whole launch)
     const uint32_t jn = wid * 32 + lane;
     uint32_t *r_out = nullptr, *r_proj = nullptr;
     int32_t r_cover = -1;
@@ -416,100 +507,194 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
         r_cover = d[jn].cover;
     }
     build_consts(pc, d, count);                           // (contains __syncthreads)
-    const uint4 ti = dir.tiles[t];
-    const uint32_t hbeg = ti.w, hend = dir.tiles[t + 1].w;
-    for (uint32_t h = hbeg + threadIdx.x; h < hend; h += 256) {
-        const uint32_t xl = __ldg(dir.heavy_x + h) - x0;
-#pragma unroll
-        for (int k = 0; k < LW; ++k) ot[xl * TROW + k] = sc.hout[(size_t)h * LW + k];
-    }
-    // medium rows: warp per row, the 16 lane pairs split its neighbours
-    for (uint32_t m = wid; m < ((dbg & 2) ? 0u : ti.y); m += 8) {
-        const uint32_t x = __ldg(dir.order + ti.x + m);
-        const uint32_t a = __ldg(dir.row_ptr + x), b = __ldg(dir.row_ptr + x + 1);
-        Acc<COUNT> acc;
-        acc.zero();
-        scan_edges<COUNT>(acc, dir.col, sc.T, a + (lane >> 1), b, 16, half);
-        acc.warp_reduce_pairs();
-        if (lane < 2) {
-#pragma unroll
-            for (int k = 0; k < HW; ++k) ot[(x - x0) * TROW + half * HW + k] = acc.result(pc, half * HW + k, k);
-        }
-    }
-    // light rows: SELL-16 slices, a warp per slice, a lane pair per row; the 16 pairs read 16
-    // consecutive neighbour indices per step (coalesced), 4 steps of T gathers in flight
-    const uint32_t sbeg = __ldg(dir.tile_slice + t), send = __ldg(dir.tile_slice + t + 1);
-    for (uint32_t sl = sbeg + wid; sl < ((dbg & 1) ? sbeg : send); sl += 8) {
-        const uint32_t li = (sl - sbeg) * 16 + (lane >> 1);
-        const bool rv = li < ti.z;
-        const uint32_t x = rv ? __ldg(dir.order + ti.x + ti.y + li) : 0u;
-        const uint32_t *c = dir.sell_col + __ldg(dir.sell_off + sl) + (lane >> 1);
-        const uint32_t w = __ldg(dir.sell_w + sl);
-        Acc<COUNT> acc;
-        acc.zero();
-        uint32_t k = 0;
-        for (; k + 4 <= w; k += 4) {
-            uint32_t y[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) y[u] = __ldg(c + (k + u) * 16);
-            uint4 v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                v[u] = y[u] != 0xffffffffu ? __ldg(sc.T + 2ull * y[u] + half) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) acc.add(v[u]);
-        }
-        if (rv) {
-#pragma unroll
-            for (int q = 0; q < HW; ++q) ot[(x - x0) * TROW + half * HW + q] = acc.result(pc, half * HW + q, q);
-        }
-    }
-    __syncthreads();
-    // transpose back: warp g writes lanes 32g..32g+31 (node rows), 4 words per store
-    const uint32_t g = wid;
     const bool live = jn < count;
     uint32_t tp = 0, fp = 0;
-    // 8 words per step: each lane writes one whole 32 B sector of its node's row
-    for (uint32_t wl = 0; wl < ((dbg & 4) ? 0u : 32u); wl += 8) {
-        const uint32_t w = t * 32 + wl;
-        if (w >= kb.W4) break;                             // W4 is a multiple of 8
-        uint32_t o[8];
+    for (;;) {
+        __syncthreads();                                  // previous tile's transpose-back done
+        if (threadIdx.x == 0) {
+            s_tile = atomicAdd(sched, 1u);
+            s_item = 0;
+        }
+        __syncthreads();
+        const uint32_t tt = s_tile;
+        if (tt >= dir.n_tiles) break;
+        const uint32_t t = __ldg(dir.tile_rank + tt);
+        const uint32_t x0 = t * 1024;
+        if (x0 + 1024 > kb.N)                              // only the last tile has rows >= N (left 0)
+            for (uint32_t i = threadIdx.x; i < 1024 * TROW; i += 256) ot[i] = 0;
+        if (threadIdx.x < 32) {
+            const uint32_t w = t * 32 + threadIdx.x;
+            s_exm[threadIdx.x] = w < kb.W ? __ldg(kb.ex_mask + w) : 0u;
+            s_exb[threadIdx.x] = w < kb.W ? __ldg(kb.ex_base + w) : 0u;
+        }
+        const uint4 ti = dir.tiles[t];
+        const uint32_t hbeg = ti.w, hend = dir.tiles[t + 1].w;
+        if (x0 + 1024 > kb.N) __syncthreads();            // zero fill before the heavy rows land
+        for (uint32_t h = hbeg + threadIdx.x; h < hend; h += 256) {
+            const uint32_t xl = __ldg(dir.heavy_x + h) - x0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) o[q] = warp_transpose(ot[((wl + q) * 32 + lane) * TROW + g], lane);
-        if (live) {
-            if (r_out) {
-                uint4 *dst = reinterpret_cast<uint4 *>(r_out + w);
-                dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
-                dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
-            }
-            if (r_proj) {
+            for (int k = 0; k < LW; ++k) ot[xl * TROW + k] = sc.hout[(size_t)h * LW + k];
+        }
+        const uint32_t sbeg = __ldg(dir.tile_slice + t), send = __ldg(dir.tile_slice + t + 1);
+        // work items, in this order: big medium rows (deg > kMidDeg; a warp each), mid rows
+        // (4 per warp, 4 lane pairs each), light SELL slices (SPI per item)
+        constexpr uint32_t SPI = COUNT ? 1u : 2u;
+        const uint32_t n_big = (dbg & 2) ? 0u : __ldg(dir.tile_nbig + t);
+        const uint32_t n_med = (dbg & 2) ? 0u : ti.y, n_sl = (dbg & 1) ? 0u : send - sbeg;
+        const uint32_t i_light = n_big + (n_med - n_big + 3) / 4;
+        const uint32_t n_items = i_light + (n_sl + SPI - 1) / SPI;
+        uint32_t nxt = 0;
+        if (lane == 0) nxt = atomicAdd(&s_item, 1u);
+        nxt = __shfl_sync(FULL, nxt, 0);
+        while (nxt < n_items) {
+            const uint32_t it = nxt;
+            if (lane == 0) nxt = atomicAdd(&s_item, 1u);  // the next item, fetched under this one
+            Acc<COUNT> acc;
+            acc.zero();
+            if (it < n_big) {
+                // big medium row: warp per row, the 16 lane pairs split its neighbours
+                const uint32_t x = __ldg(dir.order + ti.x + it);
+                const uint32_t a = __ldg(dir.row_ptr + x), b = __ldg(dir.row_ptr + x + 1);
+                scan_strided<COUNT>(acc, dir.col, sc.T, a + (lane >> 1), b, 16, half);
+                acc.template warp_reduce_pairs<16>();
+                if (lane < 2) {
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    // example bits of word w+q -> the projected row (pext with the staged masks)
-                    uint32_t m = s_exm[wl + q];
-                    const uint32_t word = o[q];
-                    if (!m || !word) continue;
-                    uint32_t bits = 0, nb = 0;
-                    for (; m; m &= m - 1, ++nb) bits |= ((word >> (__ffs(m) - 1)) & 1u) << nb;
-                    if (!bits) continue;
-                    const uint32_t base = s_exb[wl + q], sh = base & 31;
-                    atomicOr(r_proj + (base >> 5), bits << sh);
-                    if (sh && sh + nb > 32) atomicOr(r_proj + (base >> 5) + 1, bits >> (32 - sh));
+                    for (int k = 0; k < HW; ++k) ot[(x - x0) * TROW + half * HW + k] = acc.result(pc, half * HW + k, k);
+                }
+            } else if (it < i_light) {
+                // mid rows: 4 per warp, the 4 lane pairs of each 8-lane group split one row
+                // (two reduction stages instead of four)
+                const uint32_t p = (lane >> 1) & 3u;
+                const uint32_t mi = n_big + (it - n_big) * 4 + (lane >> 3);
+                const bool rv = mi < n_med;
+                uint32_t x = 0, a = 0, b = 0;
+                if (rv) {
+                    x = __ldg(dir.order + ti.x + mi);
+                    a = __ldg(dir.row_ptr + x);
+                    b = __ldg(dir.row_ptr + x + 1);
+                }
+                scan_strided<COUNT>(acc, dir.col, sc.T, a + p, b, 4, half);
+                acc.template warp_reduce_pairs<4>();
+                if (rv && p == 0) {
+#pragma unroll
+                    for (int k = 0; k < HW; ++k) ot[(x - x0) * TROW + half * HW + k] = acc.result(pc, half * HW + k, k);
+                }
+            } else if (SPI == 1) {
+                // light rows: one SELL-16 slice, a lane pair per row; the 16 pairs read 16
+                // consecutive neighbour indices per step (coalesced)
+                const uint32_t sl = it - i_light;
+                const uint32_t li = sl * 16 + (lane >> 1);
+                const bool rv = li < ti.z;
+                const uint32_t x = rv ? __ldg(dir.order + ti.x + ti.y + li) : 0u;
+                const uint32_t *c = dir.sell_col + __ldg(dir.sell_off + sbeg + sl) + (lane >> 1);
+                scan_slice_pipelined<COUNT>(acc, c, sc.T, __ldg(dir.sell_w + sbeg + sl), half);
+                if (rv) {
+#pragma unroll
+                    for (int q = 0; q < HW; ++q) ot[(x - x0) * TROW + half * HW + q] = acc.result(pc, half * HW + q, q);
+                }
+            } else {
+                // light rows, OR class: two SELL-16 slices per step (their dependent load
+                // chains -- slice bounds, neighbour ids, T gathers -- overlap)
+                Acc<COUNT> acc2;
+                acc2.zero();
+                uint32_t x[2], w[2];
+                const uint32_t *cp[2];
+                bool rv[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t sl = (it - i_light) * 2 + h;
+                    const bool sv = sl < n_sl;
+                    const uint32_t li = sl * 16 + (lane >> 1);
+                    rv[h] = sv && li < ti.z;
+                    x[h] = rv[h] ? __ldg(dir.order + ti.x + ti.y + li) : 0u;
+                    cp[h] = sv ? dir.sell_col + __ldg(dir.sell_off + sbeg + sl) + (lane >> 1) : dir.sell_col;
+                    w[h] = sv ? __ldg(dir.sell_w + sbeg + sl) : 0u;
+                }
+                const uint32_t wm = max(w[0], w[1]);
+                for (uint32_t k = 0; k < wm; k += 4) {
+                    uint32_t y[2][4];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) y[h][u] = k < w[h] ? __ldg(cp[h] + (k + u) * 16) : 0xffffffffu;
+                    uint4 v[2][4];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            v[h][u] = y[h][u] != 0xffffffffu ? __ldg(sc.T + 2ull * y[h][u] + half) : make_uint4(0, 0, 0, 0);
+                    acc.add4(v[0][0], v[0][1], v[0][2], v[0][3]);
+                    acc2.add4(v[1][0], v[1][1], v[1][2], v[1][3]);
+                }
+                if (rv[0]) {
+#pragma unroll
+                    for (int q = 0; q < HW; ++q) ot[(x[0] - x0) * TROW + half * HW + q] = acc.result(pc, half * HW + q, q);
+                }
+                if (rv[1]) {
+#pragma unroll
+                    for (int q = 0; q < HW; ++q) ot[(x[1] - x0) * TROW + half * HW + q] = acc2.result(pc, half * HW + q, q);
                 }
             }
-            if (r_cover >= 0) {
-                const uint4 *pp = reinterpret_cast<const uint4 *>(kb.pos + w);
-                const uint4 *nn = reinterpret_cast<const uint4 *>(kb.neg + w);
+            nxt = __shfl_sync(FULL, nxt, 0);
+        }
+        __syncthreads();
+        // transpose back: warp g writes lanes 32g..32g+31 (node rows); each lane writes one
+        // whole 32 B sector of its node's row per 8 words
+        const uint32_t g = wid;
+        uint32_t pw = 0, pbits = 0;                       // pending projected word of this lane's node
+        for (uint32_t wl = 0; wl < ((dbg & 4) ? 0u : 32u); wl += 8) {
+            const uint32_t w = t * 32 + wl;
+            if (w >= kb.W4) break;                         // W4 is a multiple of 8
+            uint32_t o[8];
 #pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                    const uint4 p = __ldg(pp + hh), n = __ldg(nn + hh);
-                    const uint32_t *oo = o + 4 * hh;
-                    tp += __popc(oo[0] & p.x) + __popc(oo[1] & p.y) + __popc(oo[2] & p.z) + __popc(oo[3] & p.w);
-                    fp += __popc(oo[0] & n.x) + __popc(oo[1] & n.y) + __popc(oo[2] & n.z) + __popc(oo[3] & n.w);
+            for (int q = 0; q < 8; ++q) o[q] = warp_transpose(ot[((wl + q) * 32 + lane) * TROW + g], lane);
+            if (live) {
+                if (r_out) {
+                    uint4 *dst = reinterpret_cast<uint4 *>(r_out + w);
+                    dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+                    dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+                }
+                if (r_proj) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        // example bits of word w+q -> the projected row (pext with the staged
+                        // masks), gathered per projected word: one atomicOr per word touched
+                        uint32_t m = s_exm[wl + q];
+                        const uint32_t word = o[q];
+                        if (!m || !word) continue;
+                        uint32_t bits = 0, nb = 0;
+                        for (; m; m &= m - 1, ++nb) bits |= ((word >> (__ffs(m) - 1)) & 1u) << nb;
+                        if (!bits) continue;
+                        const uint32_t base = s_exb[wl + q], wi = base >> 5, sh = base & 31;
+                        if (wi != pw) {
+                            if (pbits) atomicOr(r_proj + pw, pbits);
+                            pw = wi;
+                            pbits = 0;
+                        }
+                        pbits |= bits << sh;
+                        if (sh + nb > 32) {
+                            atomicOr(r_proj + pw, pbits);
+                            pw = wi + 1;
+                            pbits = bits >> (32 - sh);
+                        }
+                    }
+                }
+                if (r_cover >= 0) {
+                    const uint4 *pp = reinterpret_cast<const uint4 *>(kb.pos + w);
+                    const uint4 *nn = reinterpret_cast<const uint4 *>(kb.neg + w);
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const uint4 p = __ldg(pp + hh), n = __ldg(nn + hh);
+                        const uint32_t *oo = o + 4 * hh;
+                        tp += __popc(oo[0] & p.x) + __popc(oo[1] & p.y) + __popc(oo[2] & p.z) + __popc(oo[3] & p.w);
+                        fp += __popc(oo[0] & n.x) + __popc(oo[1] & n.y) + __popc(oo[2] & n.z) + __popc(oo[3] & n.w);
+                    }
                 }
             }
         }
+        if (pbits) atomicOr(r_proj + pw, pbits);
     }
+    // coverage of this CTA's tiles, one atomic set per node per CTA
     if (live && r_cover >= 0 && (tp | fp)) {
         hedl_counts *c = counts + r_cover;
         if (tp) {
@@ -519,6 +704,15 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
         if (fp) {
             atomicAdd((unsigned long long *)&c->fp, (unsigned long long)fp);
             atomicAdd((unsigned long long *)&c->tn, 0ull - fp);
+        }
+    }
+    // self-cleaning scheduler: the last CTA out resets the counters for the next launch
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(sched + 1, 1u) == gridDim.x - 1) {
+            sched[0] = 0;
+            sched[1] = 0;
+            __threadfence();
         }
     }
 }
@@ -560,7 +754,7 @@ __global__ void __launch_bounds__(256, COUNT ? 3 : 4) k_slice_ex(ExArgs a, Slice
         Acc<COUNT> acc;
         acc.zero();
         scan_edges<COUNT>(acc, a.ecol, sc.T, e0 + (lane >> 1), e1, 16, half);
-        acc.warp_reduce_pairs();
+        acc.template warp_reduce_pairs<16>();
         if (lane < 2) {
 #pragma unroll
             for (int k = 0; k < HW; ++k) ot[(r - r0) * TROW + half * HW + k] = acc.result(pc, half * HW + k, k);
@@ -665,9 +859,9 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
         sc.h_stride = 0;
         return sc;
     };
-    SliceDir sd{dr.row_ptr, dr.col, dr.tiles, dr.order, dr.tile_slice, dr.sell_off, dr.sell_w, dr.sell_col,
+    SliceDir sd{dr.row_ptr, dr.col, dr.tiles, dr.order, dr.tile_rank, dr.tile_nbig, dr.tile_slice, dr.sell_off, dr.sell_w, dr.sell_col,
                 dr.heavy_x, dr.heavy_nchunks, dr.chunks, dr.n_heavy, dr.n_chunks, dr.n_tiles};
-    SliceDir sdx{dr.ex_rp, dr.ex_ccol, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+    SliceDir sdx{dr.ex_rp, dr.ex_ccol, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                  dr.ex_hx, dr.ex_hn, dr.ex_chunks, dr.n_ex_heavy, dr.n_ex_chunks, 0};
     const ExArgs xa{dr.ex_rp, dr.ex_ccol, dr.ex_tiles, dr.ex_order, kb->ex_ids, dr.ex_hrank, kb->ppos, kb->pneg, kb->MW4};
     const size_t smem = sizeof(PackConst) + 1024 * TROW * 4;
@@ -737,8 +931,19 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
         } else {
             prof_begin(s, KC_SLICE);
             static const uint32_t dbg = getenv("HEDL_DBG_TILE") ? (uint32_t)atoi(getenv("HEDL_DBG_TILE")) : 0u;
-            if (cls == 0) k_slice_tile<false><<<dr.n_tiles, 256, smem, s>>>(kd, sd, sc, dd, run, counts, dbg);
-            else k_slice_tile<true><<<dr.n_tiles, 256, smem, s>>>(kd, sd, sc, dd, run, counts, dbg);
+            // persistent grid: every resident CTA slot once (the tiles are taken dynamically)
+            static uint32_t resident[2] = {0, 0};
+            if (!resident[0]) {
+                int b0 = 0, b1 = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_slice_tile<false>, 256, smem);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_slice_tile<true>, 256, smem);
+                resident[0] = (uint32_t)std::max(1, b0) * std::max(1, kb->sm_count);
+                resident[1] = (uint32_t)std::max(1, b1) * std::max(1, kb->sm_count);
+            }
+            uint32_t *sched = (uint32_t *)(base + need - 256);   // self-cleaning {next tile, CTAs done}
+            const uint32_t grid = std::min(dr.n_tiles, resident[cls == 0 ? 0 : 1]);
+            if (cls == 0) k_slice_tile<false><<<grid, 256, smem, s>>>(kd, sd, sc, dd, run, counts, sched, dbg);
+            else k_slice_tile<true><<<grid, 256, smem, s>>>(kd, sd, sc, dd, run, counts, sched, dbg);
             count_launch();
             // minimal DRAM bytes of one lane-packed pass: CSR once + T once (32 B per individual)
             // + the output rows; the 32 B-per-edge T gathers are L2 traffic (DESIGN.md K-SLICE)
