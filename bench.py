@@ -391,7 +391,8 @@ def main():
             return {"value": len(roots) / (e_loc / args.steps), "unit": "hyps/s",
                     "h2d_bytes_per_step": int((h2d1 - h2d0) / args.steps) + extra,
                     "d2h_bytes_per_step": int((d2h1 - d2h0) / args.steps),
-                    "ms_per_step": 1000.0 * e_loc / args.steps}
+                    "ms_per_step": 1000.0 * e_loc / args.steps,
+                    "step_ms": [round(1000.0 * x, 2) for x in et]}
 
         e2e_steps(True)                                   # warm-up of the device-compile path
         e2e = e2e_steps(True)

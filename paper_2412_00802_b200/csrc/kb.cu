@@ -407,6 +407,7 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
                 tslice[dr.n_tiles] = (uint32_t)soff.size();
                 if (scol.size() >= 0xffffffffull) return bail(fail(HEDL_ERR_UNSUPPORTED, "SELL layout too large"));
                 if ((s = upload(kb, st, &dr.tile_slice, tslice.data(), tslice.size()))) return bail(s);
+                soff.push_back((uint32_t)scol.size());    // sentinel: slice s spans [sell_off[s], sell_off[s + 1])
                 if ((s = upload(kb, st, &dr.sell_off, soff.data(), soff.size()))) return bail(s);
                 if ((s = upload(kb, st, &dr.sell_w, sw.data(), sw.size()))) return bail(s);
                 if ((s = upload(kb, st, &dr.sell_col, scol.data(), scol.size()))) return bail(s);

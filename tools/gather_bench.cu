@@ -8,6 +8,7 @@
 #include <vector>
 #include <random>
 #include <algorithm>
+#include <cmath>
 #include <cuda_runtime.h>
 
 template <int UNROLL, bool PAIR>
@@ -90,6 +91,23 @@ int main() {
     run<4, false>("uniform", idx, T, E, out, 4, sms);
     run<4, false>("uniform", idx, T, E, out, 8, sms);
     run<8, false>("uniform", idx, T, E, out, 8, sms);
+    // skewed targets as in the C3/C4 generator: popularity ~ (rank+1)^-0.8 over a random
+    // permutation (a few individuals receive a large share of all gathers)
+    {
+        std::vector<double> cdf(N);
+        double acc = 0;
+        for (uint32_t k = 0; k < N; ++k) { acc += std::pow(k + 1.0, -0.8); cdf[k] = acc; }
+        std::vector<uint32_t> perm(N);
+        for (uint32_t k = 0; k < N; ++k) perm[k] = k;
+        std::shuffle(perm.begin(), perm.end(), rng);
+        std::uniform_real_distribution<double> U(0, acc);
+        std::vector<uint32_t> hs(E);
+        for (uint64_t e = 0; e < E; ++e) hs[e] = perm[std::lower_bound(cdf.begin(), cdf.end(), U(rng)) - cdf.begin()];
+        cudaMemcpy(idx, hs.data(), E * 4, cudaMemcpyHostToDevice);
+        run<4, true>("skewed", idx, T, E, out, 4, sms);
+        run<8, true>("skewed", idx, T, E, out, 4, sms);
+        cudaMemcpy(idx, h.data(), E * 4, cudaMemcpyHostToDevice);
+    }
     // sorted indices (best-case locality) for contrast
     std::sort(h.begin(), h.end());
     cudaMemcpy(idx, h.data(), E * 4, cudaMemcpyHostToDevice);
