@@ -115,3 +115,33 @@ def test_slice_ex_batched_heavy_examples():
                 trees.append(("EXISTS", 0, inv, child) if k % 3 else ("MIN", k % 17, 0, inv, child))
     assert len(trees) > 512
     assert_parity(kb, trees, tag="ex batched heavy")
+
+
+def test_slice_degree_ladder_dense():
+    """Every 1,024-row tile holds light (<= 32), mid (33..128), big (129..512) and heavy rows,
+    and the children are dense, so COUNT packs see counts far above 31 (overflow plane,
+    4-pair mid groups, warp-per-row big rows, 2-slice OR steps) against n in 0..30."""
+    from synth.format import kb_from_sets
+    rng = np.random.default_rng(4242)
+    n = 9000
+    deg = (np.arange(n, dtype=np.int64) * 7919) % 600
+    subj = np.repeat(np.arange(n), deg)
+    obj = np.concatenate([rng.choice(n, int(d), replace=False) for d in deg])
+    dens = (0.95, 0.5, 0.08, 0.99)
+    concepts = [np.flatnonzero(rng.random(n) < p).tolist() for p in dens]
+    kb = kb_from_sets(n, concepts, [list(zip(subj.tolist(), obj.tolist()))], [],
+                      list(range(0, n, 7)), [x for x in range(3, n, 11) if x % 7])
+    trees = []
+    for c in range(4):
+        for inv in (False, True):
+            trees += [("EXISTS", 0, inv, ("ATOM", c)), ("FORALL", 0, inv, ("ATOM", c)),
+                      ("EXISTS", 0, inv, ("NOT", ("ATOM", c))), ("FORALL", 0, inv, ("NOT", ("ATOM", c)))]
+            for nn in (0, 1, 2, 15, 29, 30):
+                for op in ("MIN", "MAX"):
+                    trees.append((op, nn, 0, inv, ("ATOM", c)))
+            trees.append(("EXACT", 30, 0, inv, ("ATOM", c)))
+    assert_parity(kb, trees, eflags=FORCE, tag="degree ladder (forced packs)")
+    assert_parity(kb, trees, tag="degree ladder (default)")
+    # without EXACT lanes (packs of GE / LE only)
+    trees2 = [t for t in trees if t[0] != "EXACT"]
+    assert_parity(kb, trees2, eflags=FORCE, tag="degree ladder GE/LE only")
