@@ -77,37 +77,64 @@ __global__ void k_cover_init(hedl_counts *c, uint32_t n, uint64_t npos, uint64_t
 }
 
 // ------------------------------------------------------------------------------
+// Full rows: blockIdx.y = node, blockIdx.x = a slice of its words.  Each thread owns BU
+// uint4 words (interleaved by the grid width, so every load instruction is coalesced) and
+// issues all BU loads of an operand before combining them; the node's operand table is
+// staged in shared memory once, so the operand loop has no dependent global load.
+constexpr int kBoolU = 4;
+constexpr uint32_t kBoolSmemOps = 64;
 __global__ void __launch_bounds__(256) k_bool(KbDev kb, const BoolDesc *__restrict__ descs,
                                               const Operand *__restrict__ ops, hedl_counts *counts) {
     const BoolDesc d = descs[blockIdx.y];
+    __shared__ Operand s_ops[kBoolSmemOps];
+    for (uint32_t j = threadIdx.x; j < d.op_count && j < kBoolSmemOps; j += blockDim.x) s_ops[j] = ops[d.op_first + j];
+    __syncthreads();
     const uint32_t n4 = kb.W4 >> 2;
+    const uint32_t gs = gridDim.x * blockDim.x;           // stride between a thread's words
     uint32_t tp = 0, fp = 0;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
-        uint4 acc = d.is_or ? make_uint4(0, 0, 0, 0) : make_uint4(FULL, FULL, FULL, FULL);
+    for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n4; i0 += gs * kBoolU) {
+        uint4 acc[kBoolU];
+#pragma unroll
+        for (int u = 0; u < kBoolU; ++u) acc[u] = d.is_or ? make_uint4(0, 0, 0, 0) : make_uint4(FULL, FULL, FULL, FULL);
         for (uint32_t j = 0; j < d.op_count; ++j) {
-            const Operand o = ops[d.op_first + j];
-            uint4 v = __ldg(reinterpret_cast<const uint4 *>(o.ptr) + i);
-            v.x ^= o.mask; v.y ^= o.mask; v.z ^= o.mask; v.w ^= o.mask;
-            if (d.is_or) { acc.x |= v.x; acc.y |= v.y; acc.z |= v.z; acc.w |= v.w; }
-            else { acc.x &= v.x; acc.y &= v.y; acc.z &= v.z; acc.w &= v.w; }
+            const Operand o = j < kBoolSmemOps ? s_ops[j] : ops[d.op_first + j];
+            const uint4 *src = reinterpret_cast<const uint4 *>(o.ptr);
+            uint4 v[kBoolU];
+#pragma unroll
+            for (int u = 0; u < kBoolU; ++u) {
+                const uint32_t i = i0 + u * gs;
+                v[u] = i < n4 ? __ldg(src + i) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < kBoolU; ++u) {
+                v[u].x ^= o.mask; v[u].y ^= o.mask; v[u].z ^= o.mask; v[u].w ^= o.mask;
+                if (d.is_or) { acc[u].x |= v[u].x; acc[u].y |= v[u].y; acc[u].z |= v[u].z; acc[u].w |= v[u].w; }
+                else { acc[u].x &= v[u].x; acc[u].y &= v[u].y; acc[u].z &= v[u].z; acc[u].w &= v[u].w; }
+            }
         }
-        const uint32_t w0 = i << 2;
-        acc.x = tail_word(acc.x, w0, kb.W, kb.N);
-        acc.y = tail_word(acc.y, w0 + 1, kb.W, kb.N);
-        acc.z = tail_word(acc.z, w0 + 2, kb.W, kb.N);
-        acc.w = tail_word(acc.w, w0 + 3, kb.W, kb.N);
-        if (d.out) reinterpret_cast<uint4 *>(d.out)[i] = acc;   // null: root needed for counts only
-        if (d.proj) {
-            proj_scatter(kb, d.proj, w0, acc.x);
-            proj_scatter(kb, d.proj, w0 + 1, acc.y);
-            proj_scatter(kb, d.proj, w0 + 2, acc.z);
-            proj_scatter(kb, d.proj, w0 + 3, acc.w);
-        }
-        if (d.cover >= 0) {
-            const uint4 p = __ldg(reinterpret_cast<const uint4 *>(kb.pos) + i);
-            const uint4 q = __ldg(reinterpret_cast<const uint4 *>(kb.neg) + i);
-            tp += __popc(acc.x & p.x) + __popc(acc.y & p.y) + __popc(acc.z & p.z) + __popc(acc.w & p.w);
-            fp += __popc(acc.x & q.x) + __popc(acc.y & q.y) + __popc(acc.z & q.z) + __popc(acc.w & q.w);
+#pragma unroll
+        for (int u = 0; u < kBoolU; ++u) {
+            const uint32_t i = i0 + u * gs;
+            if (i >= n4) break;
+            uint4 a = acc[u];
+            const uint32_t w0 = i << 2;
+            a.x = tail_word(a.x, w0, kb.W, kb.N);
+            a.y = tail_word(a.y, w0 + 1, kb.W, kb.N);
+            a.z = tail_word(a.z, w0 + 2, kb.W, kb.N);
+            a.w = tail_word(a.w, w0 + 3, kb.W, kb.N);
+            if (d.out) reinterpret_cast<uint4 *>(d.out)[i] = a;   // null: root needed for counts only
+            if (d.proj) {
+                proj_scatter(kb, d.proj, w0, a.x);
+                proj_scatter(kb, d.proj, w0 + 1, a.y);
+                proj_scatter(kb, d.proj, w0 + 2, a.z);
+                proj_scatter(kb, d.proj, w0 + 3, a.w);
+            }
+            if (d.cover >= 0) {
+                const uint4 p = __ldg(reinterpret_cast<const uint4 *>(kb.pos) + i);
+                const uint4 q = __ldg(reinterpret_cast<const uint4 *>(kb.neg) + i);
+                tp += __popc(a.x & p.x) + __popc(a.y & p.y) + __popc(a.z & p.z) + __popc(a.w & p.w);
+                fp += __popc(a.x & q.x) + __popc(a.y & q.y) + __popc(a.z & q.z) + __popc(a.w & q.w);
+            }
         }
     }
     if (d.cover >= 0) block_cover(counts, d.cover, tp, fp);
@@ -507,11 +534,13 @@ void launch_bool(cudaStream_t s, const KbDev &kb, const BoolDesc *d_desc, uint32
     }
     for (uint32_t off = 0; off < n_desc; off += 65535) {
         const uint32_t nd = n_desc - off < 65535 ? n_desc - off : 65535;
-        const uint32_t gx = kb.W4 ? cdiv(kb.W4 / 4, 256) : 0;
-        if (!gx) return;
-        // enough CTAs to fill the 148 SMs even when the launch has few nodes
-        const uint32_t cap = std::max<uint32_t>(64, 148u * 8u / nd);
-        dim3 grid(gx < cap ? gx : cap, nd);
+        const uint32_t g1 = kb.W4 ? cdiv(kb.W4 / 4, 256) : 0;         // one uint4 per thread
+        if (!g1) return;
+        const uint32_t gU = cdiv(kb.W4 / 4, 256 * kBoolU);              // kBoolU per thread
+        // kBoolU words per thread when the launch has enough nodes to fill the 148 SMs,
+        // more CTAs per node (down to one word per thread) when it has few
+        const uint32_t want = std::max<uint32_t>(gU, std::min<uint32_t>(g1, cdiv(148u * 8u, nd)));
+        dim3 grid(want, nd);
         prof_begin(s, KC_BOOL);
         k_bool<<<grid, 256, 0, s>>>(kb, d_desc + off, d_ops, counts);
         count_launch();
