@@ -252,14 +252,21 @@ struct Acc {
 template <bool COUNT>
 __device__ __forceinline__ void scan_edges(Acc<COUNT> &acc, const uint32_t *__restrict__ col, const uint4 *__restrict__ T,
                                            uint32_t e, uint32_t b, uint32_t step, uint32_t half) {
-    for (; e + 3 * step < b; e += 4 * step) {
-        const uint32_t y0 = __ldg(col + e), y1 = __ldg(col + e + step);
-        const uint32_t y2 = __ldg(col + e + 2 * step), y3 = __ldg(col + e + 3 * step);
-        const uint4 v0 = __ldg(T + 2ull * y0 + half), v1 = __ldg(T + 2ull * y1 + half);
-        const uint4 v2 = __ldg(T + 2ull * y2 + half), v3 = __ldg(T + 2ull * y3 + half);
-        acc.add4(v0, v1, v2, v3);
+    // software-pipelined: the next four neighbour ids are in flight during this step's gathers
+    uint32_t y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) y[u] = e + step * u < b ? __ldg(col + e + step * u) : 0xffffffffu;
+    for (; e < b; e += 4 * step) {
+        uint32_t yn[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) yn[u] = e + step * (4 + u) < b ? __ldg(col + e + step * (4 + u)) : 0xffffffffu;
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = y[u] != 0xffffffffu ? __ldg(T + 2ull * y[u] + half) : make_uint4(0, 0, 0, 0);
+        acc.add4(v[0], v[1], v[2], v[3]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) y[u] = yn[u];
     }
-    for (; e < b; e += step) acc.add(__ldg(T + 2ull * __ldg(col + e) + half));
 }
 
 // ------------------------------------------------------------------------------
