@@ -274,13 +274,14 @@ __device__ __forceinline__ void scan_edges(Acc<COUNT> &acc, const uint32_t *__re
 // words (2048 individuals) in shared memory with one TMA bulk copy per row
 // (cp.async.bulk, completion counted on an mbarrier), then warps transpose 32x32 bit
 // blocks (complement masks applied on the way) and write each individual's 32 B of T.
-constexpr uint32_t PK_WORDS = 64, PK_STRIDE = 68;        // 272 B rows: 16 B aligned for TMA
+constexpr uint32_t PK_WORDS = 32, PK_STRIDE = 36;        // 144 B rows: 16 B aligned for TMA, conflict-free quads
+constexpr uint32_t PK_WPW = PK_WORDS / 8;                 // words per warp
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-__global__ void __launch_bounds__(256) k_slice_pack(KbDev kb, const RestrictDesc *__restrict__ d_run, uint32_t run,
+__global__ void __launch_bounds__(256, 4) k_slice_pack(KbDev kb, const RestrictDesc *__restrict__ d_run, uint32_t run,
                                                     uint4 *__restrict__ T_base, uint64_t t_stride,
                                                     const uint32_t *__restrict__ umask, const uint32_t *__restrict__ ubase) {
     extern __shared__ __align__(16) uint32_t sm[];        // [256][PK_STRIDE]
@@ -311,24 +312,24 @@ __global__ void __launch_bounds__(256) k_slice_pack(KbDev kb, const RestrictDesc
                      ::"r"(smem_u32(sm + t * PK_STRIDE)), "l"(src), "r"(seg), "r"(mb) : "memory");
     }
     // EX packs: T only at the example rows' neighbours U, compacted (umask / ubase); the
-    // masks of this warp's 8 words are fetched while the bulk copies are in flight
-    uint32_t ums[8], ubs[8];
+    // masks of this warp's PK_WPW words are fetched while the bulk copies are in flight
+    uint32_t ums[PK_WPW], ubs[PK_WPW];
 #pragma unroll
-    for (uint32_t k = 0; k < 8; ++k) {
-        const uint32_t w = w0 + wid * 8 + k;
+    for (uint32_t k = 0; k < PK_WPW; ++k) {
+        const uint32_t w = w0 + wid * PK_WPW + k;
         ums[k] = (umask && w < kb.W4) ? __ldg(umask + w) : FULL;
         ubs[k] = (umask && w < kb.W4) ? __ldg(ubase + w) : 0u;
     }
     asm volatile("{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n @!P1 bra WAIT_%=;\n}"
                  ::"r"(mb) : "memory");
-    // a quad of words per step: one conflict-free 16 B shared load per row group (the 68-word
+    // a quad of words per step: one conflict-free 16 B shared load per row group (the 36-word
     // row stride makes 4 B column loads 4-way bank conflicted), four 32x32 transposes
     uint32_t cms[LW];
 #pragma unroll
     for (int g = 0; g < LW; ++g) cms[g] = s_cm[g * 32 + lane];
 #pragma unroll
-    for (uint32_t q = 0; q < 2; ++q) {
-        const uint32_t wq = wid * 8 + q * 4;
+    for (uint32_t q = 0; q < PK_WPW / 4; ++q) {
+        const uint32_t wq = wid * PK_WPW + q * 4;
         if (w0 + wq >= kb.W4) break;                       // W4 is a multiple of 8: whole quads
         if (!(ums[4 * q] | ums[4 * q + 1] | ums[4 * q + 2] | ums[4 * q + 3])) continue;   // warp-uniform
         uint32_t o[4][LW];
