@@ -92,36 +92,43 @@ __global__ void __launch_bounds__(256) k_bool(KbDev kb, const BoolDesc *__restri
     const uint32_t n4 = kb.W4 >> 2;
     const uint32_t gs = gridDim.x * blockDim.x;           // stride between a thread's words
     uint32_t tp = 0, fp = 0;
+    // one form for both: OR accumulates v ^ m; AND accumulates the complement, ~v ^ ~m ...
+    // = v ^ ~m, and complements at the end (De Morgan), so every operand word costs one LOP3
+    const uint32_t flip = d.is_or ? 0u : FULL;
     for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n4; i0 += gs * kBoolU) {
         uint4 acc[kBoolU];
 #pragma unroll
-        for (int u = 0; u < kBoolU; ++u) acc[u] = d.is_or ? make_uint4(0, 0, 0, 0) : make_uint4(FULL, FULL, FULL, FULL);
+        for (int u = 0; u < kBoolU; ++u) acc[u] = make_uint4(0, 0, 0, 0);
+        const bool full = i0 + (kBoolU - 1) * gs < n4;
         for (uint32_t j = 0; j < d.op_count; ++j) {
             const Operand o = j < kBoolSmemOps ? s_ops[j] : ops[d.op_first + j];
             const uint4 *src = reinterpret_cast<const uint4 *>(o.ptr);
+            const uint32_t m = o.mask ^ flip;
             uint4 v[kBoolU];
+            if (full) {
 #pragma unroll
-            for (int u = 0; u < kBoolU; ++u) {
-                const uint32_t i = i0 + u * gs;
-                v[u] = i < n4 ? __ldg(src + i) : make_uint4(0, 0, 0, 0);
+                for (int u = 0; u < kBoolU; ++u) v[u] = __ldg(src + i0 + u * gs);
+            } else {
+#pragma unroll
+                for (int u = 0; u < kBoolU; ++u) v[u] = i0 + u * gs < n4 ? __ldg(src + i0 + u * gs) : make_uint4(0, 0, 0, 0);
             }
 #pragma unroll
             for (int u = 0; u < kBoolU; ++u) {
-                v[u].x ^= o.mask; v[u].y ^= o.mask; v[u].z ^= o.mask; v[u].w ^= o.mask;
-                if (d.is_or) { acc[u].x |= v[u].x; acc[u].y |= v[u].y; acc[u].z |= v[u].z; acc[u].w |= v[u].w; }
-                else { acc[u].x &= v[u].x; acc[u].y &= v[u].y; acc[u].z &= v[u].z; acc[u].w &= v[u].w; }
+                acc[u].x |= v[u].x ^ m; acc[u].y |= v[u].y ^ m; acc[u].z |= v[u].z ^ m; acc[u].w |= v[u].w ^ m;
             }
         }
 #pragma unroll
         for (int u = 0; u < kBoolU; ++u) {
             const uint32_t i = i0 + u * gs;
             if (i >= n4) break;
-            uint4 a = acc[u];
+            uint4 a = make_uint4(acc[u].x ^ flip, acc[u].y ^ flip, acc[u].z ^ flip, acc[u].w ^ flip);
             const uint32_t w0 = i << 2;
-            a.x = tail_word(a.x, w0, kb.W, kb.N);
-            a.y = tail_word(a.y, w0 + 1, kb.W, kb.N);
-            a.z = tail_word(a.z, w0 + 2, kb.W, kb.N);
-            a.w = tail_word(a.w, w0 + 3, kb.W, kb.N);
+            if (w0 + 4 >= kb.W) {                          // the uint4 holding word W-1 and later
+                a.x = tail_word(a.x, w0, kb.W, kb.N);
+                a.y = tail_word(a.y, w0 + 1, kb.W, kb.N);
+                a.z = tail_word(a.z, w0 + 2, kb.W, kb.N);
+                a.w = tail_word(a.w, w0 + 3, kb.W, kb.N);
+            }
             if (d.out) reinterpret_cast<uint4 *>(d.out)[i] = a;   // null: root needed for counts only
             if (d.proj) {
                 proj_scatter(kb, d.proj, w0, a.x);

@@ -11,6 +11,6 @@ for rep in 1 2; do
 done
 for v in "$@"; do
   cp ab/$v/libhedl.so $LIB
-  timeout 600 python -m pytest tests/test_gpu_slice.py tests/test_gpu_fullsize.py -x -q > gpurun_out/ab_${v}_pytest.log 2>&1; echo "exit $?" >> gpurun_out/ab_${v}_pytest.log
+  timeout 600 python -m pytest tests/test_gpu_slice.py tests/test_gpu_fullsize.py tests/test_gpu_parity.py -x -q > gpurun_out/ab_${v}_pytest.log 2>&1; echo "exit $?" >> gpurun_out/ab_${v}_pytest.log
 done
 cp /tmp/base.so $LIB
