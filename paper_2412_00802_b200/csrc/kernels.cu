@@ -162,20 +162,35 @@ __global__ void __launch_bounds__(256) k_bool_warp(KbDev kb, const BoolDesc *__r
     for (uint32_t k = blockIdx.x * 8 + (threadIdx.x >> 5); k < n_desc; k += gridDim.x * 8) {
         const BoolDesc d = descs[k];
         uint32_t tp = 0, fp = 0;
+        // operand descriptors fetched together up front (no dependent descriptor load per
+        // word); the same one-LOP3 form as k_bool (AND = complemented OR of complements)
+        const uint32_t flip = d.is_or ? 0u : FULL;
+        Operand o4[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o4[j] = (uint32_t)j < d.op_count ? ops[d.op_first + j] : Operand{nullptr, 0u, 0u};
         for (uint32_t i = lane; i < n4; i += 32) {
-            uint4 acc = d.is_or ? make_uint4(0, 0, 0, 0) : make_uint4(FULL, FULL, FULL, FULL);
-            for (uint32_t j = 0; j < d.op_count; ++j) {
-                const Operand o = ops[d.op_first + j];
-                uint4 v = __ldg(reinterpret_cast<const uint4 *>(o.ptr) + i);
-                v.x ^= o.mask; v.y ^= o.mask; v.z ^= o.mask; v.w ^= o.mask;
-                if (d.is_or) { acc.x |= v.x; acc.y |= v.y; acc.z |= v.z; acc.w |= v.w; }
-                else { acc.x &= v.x; acc.y &= v.y; acc.z &= v.z; acc.w &= v.w; }
+            uint4 acc = make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if ((uint32_t)j >= d.op_count) break;
+                const uint4 v = __ldg(reinterpret_cast<const uint4 *>(o4[j].ptr) + i);
+                const uint32_t m = o4[j].mask ^ flip;
+                acc.x |= v.x ^ m; acc.y |= v.y ^ m; acc.z |= v.z ^ m; acc.w |= v.w ^ m;
             }
+            for (uint32_t j = 4; j < d.op_count; ++j) {
+                const Operand o = ops[d.op_first + j];
+                const uint4 v = __ldg(reinterpret_cast<const uint4 *>(o.ptr) + i);
+                const uint32_t m = o.mask ^ flip;
+                acc.x |= v.x ^ m; acc.y |= v.y ^ m; acc.z |= v.z ^ m; acc.w |= v.w ^ m;
+            }
+            acc.x ^= flip; acc.y ^= flip; acc.z ^= flip; acc.w ^= flip;
             const uint32_t w0 = i << 2;
-            acc.x = tail_word(acc.x, w0, kb.W, kb.N);
-            acc.y = tail_word(acc.y, w0 + 1, kb.W, kb.N);
-            acc.z = tail_word(acc.z, w0 + 2, kb.W, kb.N);
-            acc.w = tail_word(acc.w, w0 + 3, kb.W, kb.N);
+            if (w0 + 4 >= kb.W) {                          // the uint4 holding word W-1 and later
+                acc.x = tail_word(acc.x, w0, kb.W, kb.N);
+                acc.y = tail_word(acc.y, w0 + 1, kb.W, kb.N);
+                acc.z = tail_word(acc.z, w0 + 2, kb.W, kb.N);
+                acc.w = tail_word(acc.w, w0 + 3, kb.W, kb.N);
+            }
             if (d.out) reinterpret_cast<uint4 *>(d.out)[i] = acc;
             if (d.proj) {
                 proj_scatter(kb, d.proj, w0, acc.x);
