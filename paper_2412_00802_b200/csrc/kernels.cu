@@ -81,7 +81,7 @@ __global__ void k_cover_init(hedl_counts *c, uint32_t n, uint64_t npos, uint64_t
 // uint4 words (interleaved by the grid width, so every load instruction is coalesced) and
 // issues all BU loads of an operand before combining them; the node's operand table is
 // staged in shared memory once, so the operand loop has no dependent global load.
-constexpr int kBoolU = 4;
+constexpr int kBoolU = 8;
 constexpr uint32_t kBoolSmemOps = 64;
 __global__ void __launch_bounds__(256) k_bool(KbDev kb, const BoolDesc *__restrict__ descs,
                                               const Operand *__restrict__ ops, hedl_counts *counts) {
