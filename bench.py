@@ -416,6 +416,7 @@ def main():
                 p3.free()
             e2e["learner_step"] = {"value": n_loc / float(np.mean(lt)), "unit": "hyps/s",
                                    "ms_per_step": 1000.0 * float(np.mean(lt)),
+                                   "step_ms": [round(1000.0 * x, 2) for x in lt],
                                    "what": "H2D of the batch + hedl_compile_device + device plan + evaluate + "
                                            "F1 scores + top-1000 on the GPU; D2H of the top-1000 only",
                                    "d2h_bytes_per_step": 12 * 1000}
