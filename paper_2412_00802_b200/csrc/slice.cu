@@ -16,6 +16,7 @@
 #include "slice.h"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 namespace hedl {
@@ -876,12 +877,26 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
     const size_t pk_smem = 256 * PK_STRIDE * 4;
     static bool attr_set = false;
     if (!attr_set) {
+        // shared-memory carveout: just enough for 4 resident CTAs, the rest of the 256 KB
+        // L1/shared array stays L1 (the T gathers run at half rate with the minimum L1:
+        // tools/gather_bench.cu)
+        int dev = 0, maxsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        auto carve = [&](const void *f, size_t dyn, int ctas) {
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, f);
+            const double need = (double)ctas * (double)(dyn + fa.sharedSizeBytes + 1024);
+            int pct = maxsm > 0 ? (int)std::ceil(100.0 * need / maxsm) : 100;
+            pct = std::max(0, std::min(100, pct));
+            cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+        };
         cudaFuncSetAttribute(k_slice_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_slice_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_slice_tile<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaFuncSetAttribute(k_slice_tile<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        carve((const void *)k_slice_tile<false>, smem, 4);
+        carve((const void *)k_slice_tile<true>, smem, 4);
         cudaFuncSetAttribute(k_slice_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pk_smem);
-        cudaFuncSetAttribute(k_slice_pack, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        carve((const void *)k_slice_pack, pk_smem, 4);
         attr_set = true;
     }
     const double csr = 4.0 * (kb->N + 1) + 4.0 * dr.E;

@@ -50,23 +50,28 @@ __global__ void __launch_bounds__(256) k_gather(const uint32_t *__restrict__ idx
 }
 
 template <int U, bool P>
-void run(const char *name, const uint32_t *idx, const uint4 *T, uint64_t E, uint32_t *out, int blocks_per_sm, int sms) {
+void run(const char *name, const uint32_t *idx, const uint4 *T, uint64_t E, uint32_t *out, int blocks_per_sm, int sms,
+         int smem = 0) {
     const int grid = blocks_per_sm * sms;
+    if (smem) {
+        cudaFuncSetAttribute(k_gather<U, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_gather<U, P>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    for (int i = 0; i < 3; ++i) k_gather<U, P><<<grid, 256>>>(idx, T, E, out);
+    for (int i = 0; i < 3; ++i) k_gather<U, P><<<grid, 256, smem>>>(idx, T, E, out);
     cudaEventRecord(a);
     const int reps = 20;
-    for (int i = 0; i < reps; ++i) k_gather<U, P><<<grid, 256>>>(idx, T, E, out);
+    for (int i = 0; i < reps; ++i) k_gather<U, P><<<grid, 256, smem>>>(idx, T, E, out);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms = 0;
     cudaEventElapsedTime(&ms, a, b);
     const double s = ms / 1e3 / reps;
-    printf("{\"shape\": \"%s\", \"unroll\": %d, \"pair\": %d, \"ctas_per_sm\": %d, \"us\": %.1f, \"gsectors_per_s\": %.1f, "
-           "\"gather_gbs\": %.0f, \"idx_gbs\": %.0f}\n",
-           name, U, (int)P, blocks_per_sm, s * 1e6, E / s / 1e9, 32.0 * E / s / 1e9, 4.0 * E / s / 1e9);
+    printf("{\"shape\": \"%s\", \"unroll\": %d, \"pair\": %d, \"ctas_per_sm\": %d, \"smem_per_cta\": %d, \"us\": %.1f, "
+           "\"gsectors_per_s\": %.1f, \"gather_gbs\": %.0f, \"idx_gbs\": %.0f}\n",
+           name, U, (int)P, blocks_per_sm, smem, s * 1e6, E / s / 1e9, 32.0 * E / s / 1e9, 4.0 * E / s / 1e9);
 }
 
 int main() {
@@ -85,6 +90,7 @@ int main() {
     cudaMemcpy(idx, h.data(), E * 4, cudaMemcpyHostToDevice);
     cudaMemset(T, 0x5a, (size_t)N * 32);
     run<4, true>("uniform", idx, T, E, out, 4, sms);
+    run<4, true>("uniform", idx, T, E, out, 4, sms, 38400);
     run<8, true>("uniform", idx, T, E, out, 4, sms);
     run<4, true>("uniform", idx, T, E, out, 8, sms);
     run<8, true>("uniform", idx, T, E, out, 8, sms);
@@ -106,6 +112,9 @@ int main() {
         cudaMemcpy(idx, hs.data(), E * 4, cudaMemcpyHostToDevice);
         run<4, true>("skewed", idx, T, E, out, 4, sms);
         run<8, true>("skewed", idx, T, E, out, 4, sms);
+        // the tile kernel's shared-memory footprint (4 x 37.5 KB per SM) leaves less L1
+        run<4, true>("skewed", idx, T, E, out, 4, sms, 38400);
+        run<4, true>("skewed", idx, T, E, out, 4, sms, 54000);
         cudaMemcpy(idx, h.data(), E * 4, cudaMemcpyHostToDevice);
     }
     // sorted indices (best-case locality) for contrast
