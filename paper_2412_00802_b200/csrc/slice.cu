@@ -739,7 +739,7 @@ struct ExArgs {
 };
 
 template <bool COUNT>
-__global__ void __launch_bounds__(256, COUNT ? 3 : 4) k_slice_ex(ExArgs a, SliceScratch sc0, const RestrictDesc *__restrict__ d_run,
+__global__ void __launch_bounds__(256, COUNT ? 4 : 6) k_slice_ex(ExArgs a, SliceScratch sc0, const RestrictDesc *__restrict__ d_run,
                                                                  uint32_t run, hedl_counts *counts) {
     const SliceScratch sc = sc0.at(blockIdx.y);
     const RestrictDesc *d = d_run + 256u * blockIdx.y;
