@@ -115,8 +115,9 @@ typedef struct hedl_kb_info {
 
 /* Build the device layout on `device` (copying through `stream`; returns after
  * the upload completed).  Errors: INVALID_ARG (null arrays with non-zero
- * counts, tail bits set), OUT_OF_RANGE (id >= N), EXAMPLE_CONFLICT, OOM, CUDA,
- * UNSUPPORTED (device is not sm_100). */
+ * counts, tail bits set, more than 32 roles / 65535 data properties / 65535
+ * string roles / 2^29-1 concepts), OUT_OF_RANGE (id >= N), EXAMPLE_CONFLICT,
+ * OOM, CUDA, UNSUPPORTED (device is not sm_100). */
 hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *stream, hedl_kb **out);
 hedl_status hedl_kb_free(hedl_kb *kb);
 hedl_status hedl_kb_get_info(const hedl_kb *kb, hedl_kb_info *out);

@@ -247,6 +247,17 @@ struct Carver {
 };
 void kb_release(const hedl_kb *kb);     // drop one reference; frees the KB at zero
 
+// Function attributes (dynamic shared memory opt-in, carveout) belong to a device's
+// context, and KBs may live on any device of the process: run `f` once per device,
+// thread-safe.  Each call site owns its flag array.
+constexpr int kMaxDevices = 64;
+template <class F>
+inline void once_per_device(std::once_flag (&flags)[kMaxDevices], F f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::call_once(flags[(unsigned)dev % kMaxDevices], f);
+}
+
 // ---- host phase timing (HEDL_TIMING=1 prints to stderr) ---------------------------
 bool timing_enabled();
 double now_ms();

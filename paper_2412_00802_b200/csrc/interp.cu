@@ -155,11 +155,10 @@ hedl_status interp_launch(const hedl_kb *kb, const InterpProg &prog, hedl_counts
            (const uint32_t *const *)pp, (const uint32_t *const *)(pp + R),
            (const uint32_t *const *)(pp + 2 * R), (const float *const *)(pp + 2 * R + D)};
     const size_t smem = (size_t)prog.n_nodes * kb->W4 * 4;
-    static bool attr = false;
-    if (!attr) {
+    static std::once_flag attr[kMaxDevices];
+    once_per_device(attr, [] {
         cudaFuncSetAttribute(k_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)interp_smem_limit());
-        attr = true;
-    }
+    });
     prof_begin(s, KC_INTERP);
     k_interp<<<1, 1024, smem, s>>>(ik, prog, counts_mapped, out_bits);
     count_launch();

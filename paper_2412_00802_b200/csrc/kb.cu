@@ -118,6 +118,10 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
     const uint32_t N = desc->n_individuals, W = (N + 31) / 32, W4 = (W + 7) & ~7u;
     const uint32_t C = desc->n_concepts, R = desc->n_roles, D = desc->n_data;
     if (R > 32) return fail(HEDL_ERR_INVALID_ARG, "at most 32 roles supported");
+    // program nodes store a data property id in 16 bits and operand references a concept id
+    // in 29 bits (internal.h CNode.dir, mkref): larger ids would wrap silently
+    if (D > 0xffff) return fail(HEDL_ERR_INVALID_ARG, "at most 65535 data properties supported");
+    if (C >= (1u << 29)) return fail(HEDL_ERR_INVALID_ARG, "at most 2^29-1 concepts supported");
     if (C && W && !desc->concept_bits) return fail(HEDL_ERR_INVALID_ARG, "concept_bits is null");
     if (R && !desc->role_edge_off) return fail(HEDL_ERR_INVALID_ARG, "role_edge_off is null");
     if (D && !desc->data_off) return fail(HEDL_ERR_INVALID_ARG, "data_off is null");

@@ -500,6 +500,9 @@ template <bool COUNT>
 __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, SliceScratch sc,
                                                                    const RestrictDesc *__restrict__ d, uint32_t count,
                                                                    hedl_counts *counts, uint32_t *sched, uint32_t dbg) {
+#ifndef HEDL_DEBUG_TILE
+    dbg = 0;                                              // release builds: the debug switches fold away
+#endif
     extern __shared__ uint32_t smem[];
     PackConst &pc = *reinterpret_cast<PackConst *>(smem);
     uint32_t *ot = smem + sizeof(PackConst) / 4;          // [1024][TROW]
@@ -875,8 +878,8 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
     const ExArgs xa{dr.ex_rp, dr.ex_ccol, dr.ex_tiles, dr.ex_order, kb->ex_ids, dr.ex_hrank, kb->ppos, kb->pneg, kb->MW4};
     const size_t smem = sizeof(PackConst) + 1024 * TROW * 4;
     const size_t pk_smem = 256 * PK_STRIDE * 4;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::once_flag attr_set[kMaxDevices];
+    once_per_device(attr_set, [&] {
         // shared-memory carveout: just enough for 4 resident CTAs, the rest of the 256 KB
         // L1/shared array stays L1 (the T gathers run at half rate with the minimum L1:
         // tools/gather_bench.cu)
@@ -897,8 +900,7 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
         carve((const void *)k_slice_tile<true>, smem, 4);
         cudaFuncSetAttribute(k_slice_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pk_smem);
         carve((const void *)k_slice_pack, pk_smem, 4);
-        attr_set = true;
-    }
+    });
     const double csr = 4.0 * (kb->N + 1) + 4.0 * dr.E;
     for (uint32_t off = 0; off < n;) {
         // a run of consecutive same-class descriptors: full packs go one pack per launch
@@ -953,16 +955,27 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             prof_end(s, KC_SLICE_EX, (8.0 * kb->M + 36.0 * dr.E_ex) * packs + 4.0 * kb->MW * run, packs);
         } else {
             prof_begin(s, KC_SLICE);
+#ifdef HEDL_DEBUG_TILE
+            // timing experiments only (tools/dbg_tile.sh): skips sweep phases, results are WRONG
             static const uint32_t dbg = getenv("HEDL_DBG_TILE") ? (uint32_t)atoi(getenv("HEDL_DBG_TILE")) : 0u;
-            // persistent grid: every resident CTA slot once (the tiles are taken dynamically)
-            static uint32_t resident[2] = {0, 0};
-            if (!resident[0]) {
+#else
+            constexpr uint32_t dbg = 0u;
+#endif
+            // persistent grid: every resident CTA slot once (the tiles are taken dynamically);
+            // occupancy per device (the carveout above is set per device)
+            static std::once_flag occ_once[kMaxDevices];
+            static uint32_t occ[kMaxDevices][2];
+            int cur = 0;
+            cudaGetDevice(&cur);
+            once_per_device(occ_once, [&] {
                 int b0 = 0, b1 = 0;
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_slice_tile<false>, 256, smem);
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_slice_tile<true>, 256, smem);
-                resident[0] = (uint32_t)std::max(1, b0) * std::max(1, kb->sm_count);
-                resident[1] = (uint32_t)std::max(1, b1) * std::max(1, kb->sm_count);
-            }
+                occ[(unsigned)cur % kMaxDevices][0] = (uint32_t)std::max(1, b0);
+                occ[(unsigned)cur % kMaxDevices][1] = (uint32_t)std::max(1, b1);
+            });
+            const uint32_t resident[2] = {occ[(unsigned)cur % kMaxDevices][0] * std::max(1, kb->sm_count),
+                                          occ[(unsigned)cur % kMaxDevices][1] * std::max(1, kb->sm_count)};
             uint32_t *sched = (uint32_t *)(base + need - 256);   // self-cleaning {next tile, CTAs done}
             const uint32_t grid = std::min(dr.n_tiles, resident[cls == 0 ? 0 : 1]);
             if (cls == 0) k_slice_tile<false><<<grid, 256, smem, s>>>(kd, sd, sc, dd, run, counts, sched, dbg);

@@ -87,7 +87,9 @@ def probe_ratios(kb=None, group=None, reps: int = 20, timer: Optional[Callable] 
 
 
 def _probe_time(kb, reps: int) -> float:
-    """Median device time of the probe hypothesis (AND of the first min(5, C) concepts)."""
+    """Median device time of the probe hypothesis (AND of the first min(5, C) concepts).
+    Its bitset is requested, so the conjunction runs over full N-bit rows (a root without
+    requested bits would run on the example-projected rows and time launch latency only)."""
     import torch
     import paper_2412_00802_b200 as hedl
     c = min(5, kb.info()["C"])
@@ -100,10 +102,11 @@ def _probe_time(kb, reps: int) -> float:
     prog = hedl.hedl_compile(kb, nodes, kids, np.array([c], dtype=np.uint32))
     ts = []
     with torch.cuda.device(kb.device):
+        bits = torch.empty((1, max(kb.W, 1)), dtype=torch.int32, device=f"cuda:{kb.device}")
         for _ in range(reps + 3):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            hedl.hedl_eval_batch(kb, prog, 0, 1, counts_device=True)
+            hedl.hedl_eval_batch(kb, prog, 0, 1, counts_device=True, out_bits=bits)
             e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) / 1000.0)
@@ -119,13 +122,13 @@ def local_arrays(nodes, child_idx, roots, lo, hi):
     roots = np.asarray(roots)
     if hi <= lo:
         return None
+    if not np.all(np.diff(roots.astype(np.int64)) > 0):     # roots stored tree by tree, ascending
+        return None
     a = int(roots[lo - 1]) + 1 if lo > 0 else 0
     b = int(roots[hi - 1]) + 1
-    if lo > 0 and not np.all(np.diff(roots.astype(np.int64)) > 0):
-        return None
     sub = nodes[a:b]
     r = roots[lo:hi].astype(np.int64) - a
-    if len(sub) == 0 or r.min() < 0:
+    if len(sub) == 0 or r.min() < 0 or r.max() >= len(sub):
         return None
     cb = sub["child_begin"].astype(np.int64)
     cc = sub["child_count"].astype(np.int64)
@@ -138,11 +141,6 @@ def local_arrays(nodes, child_idx, roots, lo, hi):
     out = sub.copy()
     out["child_begin"] = np.where(has, cb - k0, 0).astype(np.uint32)
     return out, kids.astype(np.uint32), r.astype(np.uint32)
-
-
-def subset_arrays(nodes, child_idx, roots, lo, hi):
-    """The node arrays restricted to roots [lo, hi) (all nodes kept; roots sliced)."""
-    return nodes, child_idx, roots[lo:hi]
 
 
 def gather_counts(local_counts, n_total: int, ranges, group=None, device=None):

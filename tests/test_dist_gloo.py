@@ -115,6 +115,20 @@ def test_local_arrays_rebased_equal_results():
         assert (c == ref[3:9]).all()
 
 
+def test_local_arrays_rejects_unsorted_roots():
+    """Roots out of tree order (also for a range starting at 0) are not a post-order batch:
+    local_arrays returns None instead of a slice that cuts off later roots."""
+    from synth import abox, hyps
+    from synth.format import flatten
+    kb = abox.random_tiny_kb(12, n=40, n_roles=2, n_data=1, n_strings=0)
+    rng = np.random.default_rng(3)
+    nodes, kids, roots = flatten([hyps.random_tree(rng, abox.kb_shape(kb), depth=3) for _ in range(6)])
+    perm = roots[[0, 5, 1, 2, 3, 4]]
+    assert hdist.local_arrays(nodes, kids, perm, 0, 3) is None
+    assert hdist.local_arrays(nodes, kids, perm, 2, 5) is None
+    assert hdist.local_arrays(nodes, kids, roots, 0, 3) is not None
+
+
 def _probe_worker(rank, world, port, q):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
