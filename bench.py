@@ -1,22 +1,27 @@
 #!/usr/bin/env python
 """Benchmark of the HT-HEDL hot path on B200 (BASELINE.json metric: hypotheses evaluated/s).
 
-Workload (config C4 of SURVEY 8(d), BASELINE.json configs[3]): a 10^6-individual
-power-law ABox (50 concepts, 2 roles + inverses, 1 numeric property, 1%/1%
-examples) and a batch of 10^6 refinement-style hypotheses, KB replicated per
-GPU, batch sharded across ranks (weak scaling: per-GPU share fixed... the
-batch is the config's 10^6 at N=1 and 10^6 x N at N GPUs).
+Workloads:
+  c4 (default; BASELINE.json configs[3], the config the metric is quoted on): a 10^6-individual
+     power-law ABox (50 concepts, 2 roles + inverses, 1 numeric property, 1%/1% examples) and
+     10^6 refinement-style hypotheses per GPU;
+  c5 (configs[4]): 1.25*10^7 individuals, one 10^8-edge role + inverse, 10^5 cardinality /
+     datatype-heavy hypotheses per GPU.  The default run adds a G = 1 C5 leg under "c5".
+KB replicated per GPU; each rank generates and evaluates only its own slice of the batch
+(beams of 25k hypotheses, rank r takes the next n_hyps), weak scaling.
 
-One step = one pass of the whole hot path over the batch: every hypothesis
-evaluated to its instance set and TP/FP/FN/TN counts.
-  value : hyps/s with the KB and the compiled program resident on the device,
-          counts left on the device (+ the NCCL all_gather of counts at N>1).
-  e2e   : the same through the public API from host node arrays every step: the arrays
-          copied to the device, hedl_compile_device (the GPU builds the program and its
-          evaluation plan) + hedl_eval_batch with host counts; the host-compile variant
-          (hedl_compile) is reported beside it.
-`python bench.py --impl reference` times the oracle (the plain C set evaluator)
-on the same workload, on bounded samples (the tier's reference arm).
+One step = one pass of the whole hot path over the batch: every hypothesis evaluated to its
+instance set and TP/FP/FN/TN counts.
+  value : hyps/s with the KB and the compiled program resident on the device, counts left on
+          the device (+ the NCCL all_gather of counts at N>1).  Library profiling is OFF in
+          this timed region; a second, profiled pass of the same steps gives the per-class
+          kernel times (CUDA events on the launch stream) behind `roofline` / `kernels`.
+  e2e   : the same through the public C ABI from HOST arrays every step: hedl_compile_device
+          with HEDL_COMPILE_HOST_INPUT (the H2D of the batch, the GPU-built program and plan,
+          one call), hedl_eval_batch with host counts (D2H).  The host-compile variant
+          (hedl_compile: host canonicalisation + host plan) is reported beside it.
+`python bench.py --impl reference` times the oracle (the plain C set evaluator) on the same
+workload, on bounded samples (the tier's reference arm).
 """
 from __future__ import annotations
 
@@ -25,13 +30,20 @@ import json
 import os
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+
+CHUNK = 25_000          # hypotheses per generator beam (synth.hyps.batch_arrays)
+WORKLOADS = {
+    "c4": {"desc": "C4: 1M-individual power-law ABox x 1M refinement hypotheses per GPU", "n_hyps": 1_000_000,
+           "seed": 4},
+    "c5": {"desc": "C5: 12.5M-individual ABox, 10^8-edge role + inverse, 10^5 cardinality/datatype-heavy "
+                   "hypotheses per GPU", "n_hyps": 100_000, "seed": 5},
+}
 
 
 def parse():
@@ -40,21 +52,26 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="hedl", choices=["hedl", "reference"])
-    ap.add_argument("--n-hyps", type=int, default=1_000_000, help="hypotheses per GPU")
-    ap.add_argument("--n-individuals", type=int, default=1_000_000)
+    ap.add_argument("--workload", default="c4", choices=list(WORKLOADS))
+    ap.add_argument("--n-hyps", type=int, default=None, help="hypotheses per GPU (default: the workload's)")
+    ap.add_argument("--n-individuals", type=int, default=1_000_000, help="C4 only")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 (10M-individual) latency leg")
+    ap.add_argument("--no-c5", action="store_true", help="skip the G=1 C5 leg of the default C4 run")
+    ap.add_argument("--no-prof-pass", action="store_true", help="skip the profiled pass (per-class kernel times)")
     ap.add_argument("--per-node", action="store_true", help="disable the lane-packed restriction path")
     ap.add_argument("--cache", default=os.environ.get("HEDL_CACHE", "/tmp/hedl_cache"))
-    ap.add_argument("--seed", type=int, default=4)
+    ap.add_argument("--dry-run", action="store_true",
+                    help="multi-rank plumbing only (gloo, no GPU): per-rank inputs, shard ranges, count gather")
     return ap.parse_args()
 
 
 # ------------------------------------------------------------------------------ inputs
 def _cached(cache, name, fn):
-    """Optional disk cache of generated inputs (a speed-up only; regenerated when absent)."""
+    """Optional disk cache of generated inputs (a speed-up only; regenerated when absent).
+    Written through a per-process temporary, so concurrent ranks never share a partial file."""
     path = os.path.join(cache, name + ".npz") if cache else None
     if path and os.path.exists(path):
         try:
@@ -64,30 +81,52 @@ def _cached(cache, name, fn):
             pass
     d = fn()
     if path:
+        tmp = f"{path}.{os.getpid()}.tmp.npz"
         try:
             os.makedirs(cache, exist_ok=True)
-            np.savez(path + ".tmp.npz", **d)
-            os.replace(path + ".tmp.npz", path)
+            np.savez(tmp, **d)
+            os.replace(tmp, path)
         except Exception:
-            pass
+            try:
+                os.remove(tmp)
+            except OSError:
+                pass
     return d
 
 
-def c4_inputs(args, world):
-    from synth import abox, hyps
-    n_ind = args.n_individuals
-    kb = _cached(args.cache, f"c4kb_{n_ind}_{args.seed}",
-                 lambda: {k: np.asarray(v) for k, v in
-                          abox.powerlaw_kb(n_ind, 50, 2, 8.0, 10_000, 0.7, 1.0, 0.01, args.seed).items()})
+def workload_kb(kind, args):
+    from synth import abox
+    if kind == "c4":
+        n = args.n_individuals
+        kb = _cached(args.cache, f"c4kb_{n}_4",
+                     lambda: {k: np.asarray(v) for k, v in
+                              abox.powerlaw_kb(n, 50, 2, 8.0, 10_000, 0.7, 1.0, 0.01, 4).items()})
+    else:
+        kb = _cached(args.cache, "c5kb_5", lambda: {k: np.asarray(v) for k, v in abox.c5_kb().items()})
     kb["N"] = int(kb["N"])
-    total = args.n_hyps * world
+    return kb
+
+
+def rank_hyps(kind, kb, n_per, rank, args):
+    """This rank's slice of the global batch: beams [rank*B, rank*B + B) of the generator, B =
+    ceil(n_per / 25k) -- no rank generates (or holds) another rank's hypotheses.  The arrays
+    are post-order trees stored root by root, rank-local (ids start at 0)."""
+    from synth import hyps
+    first = rank * ((n_per + CHUNK - 1) // CHUNK)
+    seed = WORKLOADS[kind]["seed"]
 
     def gen():
-        nodes, kids, roots = hyps.batch_arrays("c4", kb, total, args.seed)
+        nodes, kids, roots = hyps.batch_arrays(kind, kb, n_per, seed, chunk=CHUNK, first_chunk=first)
         return {"nodes": nodes, "kids": kids, "roots": roots}
 
-    h = _cached(args.cache, f"c4hyps_{n_ind}_{total}_{args.seed}", gen)
-    return kb, h["nodes"], h["kids"], h["roots"]
+    h = _cached(args.cache, f"{kind}hyps_{kb['N']}_{n_per}_{seed}_b{first}", gen)
+    return h["nodes"], h["kids"], h["roots"]
+
+
+def c4_inputs(args, world):
+    """(kb, nodes, kids, roots) of the C4 batch at world size 1 (tests call this)."""
+    kb = workload_kb("c4", args)
+    return (kb,) + tuple(rank_hyps("c4", kb, args.n_hyps, 0, args))
 
 
 # ------------------------------------------------------------------------------ clocks
@@ -135,13 +174,19 @@ def measured_peaks():
         return {}
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of each kernel class from the committed `ncu --set full` summary."""
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+def ncu_traffic(kind):
+    """Measured DRAM bytes per launch / per step of each kernel class (tools/ncu_traffic.py:
+    an ncu capture of every launch of one bench step, committed under profiles/)."""
     try:
-        return json.load(open(path))
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(kind)
     except Exception:
-        return {}
+        return None
+
+
+# where each class's algorithmic bytes live (DESIGN.md section 7)
+CLASS_BOUND = {"bool": "hbm", "bool_l2": "l2", "slice_pack": "hbm", "slice": "l2", "slice_heavy": "l2",
+               "slice_ex": "l2", "restrict": "hbm", "restrict_heavy": "hbm", "drange": "hbm", "string": "hbm",
+               "cover_init": "hbm", "gather": "hbm", "interp": "l2"}
 
 
 # ------------------------------------------------------------------------------ oracle timing
@@ -168,8 +213,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    kb, nodes, kids, roots = c4_inputs(args, world)
+    kind = args.workload
+    n_per = args.n_hyps or WORKLOADS[kind]["n_hyps"]
+    kb = workload_kb(kind, args)
+    nodes, kids, roots = rank_hyps(kind, kb, n_per, 0, args)
     from oracle import setsem
     threads = os.cpu_count() or 1
     okb = setsem.OracleKB(kb)
@@ -195,18 +242,18 @@ def run_reference(args):
         "impl": "reference", "metric": "hypotheses evaluated/sec", "value": val, "unit": "hyps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": "C4: 1M-individual power-law ABox x 1M refinement hypotheses",
-                   "n_individuals": int(kb["N"]), "global_batch": int(len(roots)),
+        "config": {"workload": WORKLOADS[kind]["desc"], "n_individuals": int(kb["N"]),
+                   "global_batch": int(len(roots)) * args.gpus,
                    "parallelism": "oracle, hypothesis-parallel host threads"},
         "cpu_baseline": {"value": val, "unit": "hyps/s", "cores": threads, "kind": "oracle",
-                         "sample": f"{S} seeded-uniform hypotheses of the C4 batch per step"},
+                         "sample": f"{S} seeded-uniform hypotheses of the {kind.upper()} batch per step"},
         "e2e": {"value": val, "unit": "hyps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-# ------------------------------------------------------------------------------ main arm
+# ------------------------------------------------------------------------------ latency legs
 def c2_latency(hedl, device):
     """1-hypothesis latency (host wall time, eval_one entry -> counts on host), C2 config."""
     from synth import abox, hyps
@@ -264,74 +311,65 @@ def c3_latency(hedl, device, cache):
         p50 = float(np.percentile(lat, 50)) * 1e6
         out.append({"h": i, "p50_us": round(p50, 1), "alg_MB": round(rb[i] / 1e6, 1),
                     "roofline_us": round(rb[i] / peak * 1e6, 1), "frac": round(rb[i] / peak * 1e6 / p50, 3)})
+    prog.free()
     k.free()
     return {"config": "C3 10M-individual power-law, 8 fixed hypotheses (H3a..)", "per_hypothesis": out,
             "p50_us_median": float(np.median([o["p50_us"] for o in out]))}
 
 
-def main():
-    args = parse()
-    if args.impl == "reference":
-        return run_reference(args)
+# ------------------------------------------------------------------------------ one workload
+def run_workload(kind, args, hedl, rank, world, local, steps, warmup, cpu_budget_s):
+    """Time one workload: value (+ profiled pass), e2e, cpu baseline.  Returns the line's fields
+    (rank 0) or None (other ranks)."""
     import torch
     import torch.distributed as dist
-
-    import paper_2412_00802_b200 as hedl
     from paper_2412_00802_b200 import dist as hdist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     dev = torch.device(f"cuda:{local}")
-
-    kb_np, nodes, kids, roots = c4_inputs(args, world)
-    costs = hdist.root_costs(nodes, kids, roots)
-    ranges = hdist.shard_ranges(costs, world)
-    lo, hi = ranges[rank]
-    my_roots = np.ascontiguousarray(roots[lo:hi])
+    n_per = args.n_hyps or WORKLOADS[kind]["n_hyps"]
+    kb_np = workload_kb(kind, args)
+    nodes, kids, roots = rank_hyps(kind, kb_np, n_per, rank, args)
+    n_loc = len(roots)
+    ranges = [(r * n_per, (r + 1) * n_per) for r in range(world)]
+    total = n_per * world
     kb = hedl.hedl_kb_load(kb_np, local)
     t0 = time.perf_counter()
-    prog = hedl.hedl_compile(kb, nodes, kids, my_roots)
+    prog = hedl.hedl_compile(kb, nodes, kids, roots)
     compile_s = time.perf_counter() - t0
     pinfo = prog.info()
     eflags = hedl.HEDL_EVAL_PER_NODE if args.per_node else 0
-    n_loc = hi - lo
     counts_dev = torch.empty((max(n_loc, 1), 4), dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
 
     def step(c_out):
-        if n_loc:
-            hedl.hedl_eval_batch(kb, prog, 0, n_loc, counts_device=True, out_counts=c_out[:n_loc], flags=eflags)
+        hedl.hedl_eval_batch(kb, prog, 0, n_loc, counts_device=True, out_counts=c_out[:n_loc], flags=eflags)
         if world > 1:
-            hdist.gather_counts(c_out[:n_loc], len(roots), ranges, device=dev)
+            hdist.gather_counts(c_out[:n_loc], total, ranges, device=dev)
 
-    for _ in range(args.warmup):
+    def timed(n_steps):
+        times = []
+        for _ in range(n_steps):
+            flush.zero_()                                   # L2 flushed between timed steps
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            step(counts_dev)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        return times
+
+    for _ in range(warmup):
         step(counts_dev)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = ClockSampler(local)
     clocks.start()
-    hedl.prof_reset()
-    hedl.prof_enable(True)
     l0 = hedl.launch_count()
-    times = []
-    for _ in range(args.steps):
-        flush.zero_()                                   # L2 flushed between timed steps
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record(stream)
-        step(counts_dev)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1))
+    times = timed(steps)                                    # library profiling off
     launches = hedl.launch_count() - l0
-    hedl.prof_enable(False)
-    prof = hedl.prof_read()
     clk = clocks.stop()
     t_loc = float(np.sum(times))
     t_max = t_loc
@@ -339,45 +377,41 @@ def main():
         tt = torch.tensor([t_loc], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
-    ms_per_step = t_max / args.steps
-    value = len(roots) / (ms_per_step / 1000.0)
+    ms_per_step = t_max / steps
+    value = total / (ms_per_step / 1000.0)
+    # profiled pass: the same steps with per-launch CUDA events on the launch stream
+    prof, prof_ms = [], None
+    if not args.no_prof_pass:
+        hedl.prof_reset()
+        hedl.prof_enable(True)
+        pt = timed(steps)
+        hedl.prof_enable(False)
+        prof = hedl.prof_read()
+        prof_ms = float(np.mean(pt))
 
-    # ---- e2e through the public API from host arrays every step ----
-    # Each step: the rank's hypothesis arrays go host (pinned) -> device, the GPU compiles
-    # them (hedl_compile_device) and builds its own evaluation plan, then
-    # evaluates; the counts come back to host memory.  The host-compile variant
-    # (hedl_compile: host canonicalisation + host plan) is reported beside it.
+    # ---- e2e through the public C ABI from host arrays every step ----
     e2e = None
     if not args.no_e2e:
-        loc = hdist.local_arrays(nodes, kids, roots, lo, hi) if n_loc else None
-        ln, lk, lr = loc if loc is not None else (nodes, kids, my_roots)
-        nodes_pin = torch.from_numpy(np.ascontiguousarray(ln).view(np.uint8).reshape(-1)).pin_memory()
-        kids_pin = torch.from_numpy(np.ascontiguousarray(lk, dtype=np.uint32).view(np.uint8)).pin_memory()
-        roots_pin = torch.from_numpy(np.ascontiguousarray(lr, dtype=np.uint32).view(np.uint8)).pin_memory()
-        nodes_d = torch.empty_like(nodes_pin, device=dev)
-        kids_d = torch.empty_like(kids_pin, device=dev)
-        roots_d = torch.empty_like(roots_pin, device=dev)
-        in_bytes = nodes_pin.numel() + kids_pin.numel() + roots_pin.numel()
+        nodes_pin = torch.from_numpy(np.ascontiguousarray(nodes).view(np.uint8).reshape(-1)).pin_memory()
+        kids_pin = torch.from_numpy(np.ascontiguousarray(kids, dtype=np.uint32).view(np.uint8)).pin_memory()
+        roots_pin = torch.from_numpy(np.ascontiguousarray(roots, dtype=np.uint32).view(np.uint8)).pin_memory()
 
-        def e2e_steps(device_compile):
+        def e2e_steps(device_compile, n_steps):
             h2d0, d2h0 = hedl.io_counters()
             et = []
-            for _ in range(args.steps):
+            for _ in range(n_steps):
                 torch.cuda.synchronize()
                 if world > 1:
                     dist.barrier()
                 t0 = time.perf_counter()
-                if device_compile:
-                    nodes_d.copy_(nodes_pin, non_blocking=True)
-                    kids_d.copy_(kids_pin, non_blocking=True)
-                    roots_d.copy_(roots_pin, non_blocking=True)
-                    p2 = hedl.hedl_compile_device(kb, nodes_d, kids_d, roots_d, n_nodes=len(ln), n_kids=len(lk),
-                                                  n_roots=len(lr))
+                if device_compile:       # one call: H2D of the batch + GPU-built program
+                    p2 = hedl.hedl_compile_device(kb, nodes_pin, kids_pin, roots_pin, n_nodes=len(nodes),
+                                                  n_kids=len(kids), n_roots=n_loc)
                 else:
-                    p2 = hedl.hedl_compile(kb, ln, lk, lr)
+                    p2 = hedl.hedl_compile(kb, nodes, kids, roots)
                 _, c_host = hedl.hedl_eval_batch(kb, p2, 0, n_loc, flags=eflags)
                 if world > 1:
-                    hdist.gather_counts(torch.from_numpy(c_host.view(np.int64)).to(dev), len(roots), ranges, device=dev)
+                    hdist.gather_counts(torch.from_numpy(c_host.view(np.int64)).to(dev), total, ranges, device=dev)
                     torch.cuda.synchronize()
                 et.append(time.perf_counter() - t0)
                 p2.free()
@@ -387,109 +421,207 @@ def main():
                 tt = torch.tensor([e_loc], device=dev)
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
                 e_loc = float(tt.item())
-            extra = in_bytes if device_compile else 0
-            return {"value": len(roots) / (e_loc / args.steps), "unit": "hyps/s",
-                    "h2d_bytes_per_step": int((h2d1 - h2d0) / args.steps) + extra,
-                    "d2h_bytes_per_step": int((d2h1 - d2h0) / args.steps),
-                    "ms_per_step": 1000.0 * e_loc / args.steps,
+            return {"value": total / (e_loc / n_steps), "unit": "hyps/s",
+                    "h2d_bytes_per_step": int((h2d1 - h2d0) / n_steps),
+                    "d2h_bytes_per_step": int((d2h1 - d2h0) / n_steps),
+                    "ms_per_step": 1000.0 * e_loc / n_steps,
                     "step_ms": [round(1000.0 * x, 2) for x in et]}
 
-        e2e_steps(True)                                   # warm-up of the device-compile path
-        e2e = e2e_steps(True)
+        e2e_steps(True, max(1, warmup))                    # warm-up of the device-compile path
+        e2e = e2e_steps(True, steps)
+        e2e["path"] = ("hedl_compile_device(HEDL_COMPILE_HOST_INPUT: H2D inside the call) + device plan "
+                       "(GPU-generated plans, PAPER.md:872) + hedl_eval_batch (host counts)")
         # the learner's step on the GPU: device compile + plan + evaluate + F1 + top-1000,
         # only the top-k indices / scores come back
         if world == 1 and n_loc >= 1000:
             lt = []
-            for it in range(args.warmup + args.steps):
+            for it in range(warmup + steps):
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
-                nodes_d.copy_(nodes_pin, non_blocking=True)
-                kids_d.copy_(kids_pin, non_blocking=True)
-                roots_d.copy_(roots_pin, non_blocking=True)
-                p3 = hedl.hedl_compile_device(kb, nodes_d, kids_d, roots_d, n_nodes=len(ln), n_kids=len(lk),
-                                              n_roots=len(lr))
+                p3 = hedl.hedl_compile_device(kb, nodes_pin, kids_pin, roots_pin, n_nodes=len(nodes),
+                                              n_kids=len(kids), n_roots=n_loc)
                 _, cdev = hedl.hedl_eval_batch(kb, p3, 0, n_loc, counts_device=True, flags=eflags)
                 _, ti, ts = hedl.hedl_score_topk(cdev, hedl.HEDL_SCORE_F1, 1000, want_scores=False)
                 ti_h, ts_h = ti.cpu(), ts.cpu()
-                if it >= args.warmup:
+                if it >= warmup:
                     lt.append(time.perf_counter() - t0)
                 p3.free()
             e2e["learner_step"] = {"value": n_loc / float(np.mean(lt)), "unit": "hyps/s",
                                    "ms_per_step": 1000.0 * float(np.mean(lt)),
                                    "step_ms": [round(1000.0 * x, 2) for x in lt],
-                                   "what": "H2D of the batch + hedl_compile_device + device plan + evaluate + "
+                                   "what": "hedl_compile_device from host arrays + device plan + evaluate + "
                                            "F1 scores + top-1000 on the GPU; D2H of the top-1000 only",
                                    "d2h_bytes_per_step": 12 * 1000}
-        e2e["path"] = "hedl_compile_device + device plan (GPU-generated plans, PAPER.md:872)"
-        e2e["host_compile"] = e2e_steps(False)
+        e2e["host_compile"] = e2e_steps(False, steps)
         e2e["host_compile"]["compile_ms"] = 1000.0 * compile_s
 
+    if rank != 0:
+        prog.free()
+        kb.free()
+        return None
+
+    # ---- roofline: dominant class, every class, the step ----
+    peaks = measured_peaks()
+    peak = peaks.get("hbm_gbs")
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (copy, read+write)" if peak else "fallback"
+    peak = peak or 6650.0
+    traffic = ncu_traffic(kind)
+    tcls = (traffic or {}).get("classes", {})
+    classes = []
+    for e in prof:
+        ms = e["total_ms"] / steps
+        ach = e["alg_bytes"] / (e["total_ms"] / 1000.0) / 1e9 if e["total_ms"] else 0.0
+        t = tcls.get(e["name"], {})
+        classes.append({"name": e["name"], "bound": CLASS_BOUND.get(e["name"], "hbm"),
+                        "launches_per_step": e["launches"] / steps, "ms_per_step": ms,
+                        "alg_bytes_per_launch": e["alg_bytes"] / e["launches"], "alg_GBps": ach,
+                        "frac_of_hbm": ach / peak,
+                        "ncu_dram_bytes_per_launch": t.get("dram_bytes_per_launch"),
+                        "ncu_dram_GBps": (t["dram_bytes_per_step"] / (ms / 1000.0) / 1e9)
+                        if t.get("dram_bytes_per_step") and ms else None})
+    classes.sort(key=lambda c: -c["ms_per_step"])
+    roofline = None
+    top = next((c for c in classes if c["bound"] == "hbm"), None)
+    if top:
+        tr = tcls.get(top["name"], {}).get("dram_bytes_per_launch")
+        roofline = {"bound": "hbm", "kernel": top["name"], "achieved": top["alg_GBps"], "peak": peak, "unit": "GB/s",
+                    "frac": top["frac_of_hbm"], "traffic": tr, "peak_source": peak_src,
+                    "alg_bytes_per_launch": top["alg_bytes_per_launch"],
+                    "avg_launch_ms": top["ms_per_step"] / top["launches_per_step"],
+                    "share_of_step": top["ms_per_step"] / prof_ms if prof_ms else None,
+                    "traffic_source": "profiles/ncu_traffic.json (measured DRAM read+write per launch, every "
+                                      "launch of one step)" if tr is not None else None,
+                    "timing": "CUDA events on the launch stream, profiled pass of the same steps"}
+        if traffic and traffic.get("dram_bytes_per_step"):
+            db = traffic["dram_bytes_per_step"]
+            roofline["step_dram_bytes"] = db
+            roofline["step_dram_frac"] = db / (ms_per_step / 1000.0) / (peak * 1e9)
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        rate, S, cores, secs = oracle_rate(kb_np, nodes, kids, roots, budget_s=cpu_budget_s)
+        cpu = {"value": rate, "unit": "hyps/s", "cores": cores, "kind": "oracle",
+               "sample": f"{S} seeded-uniform hypotheses of the {kind.upper()} batch ({secs:.1f} s)"}
+    alg = pinfo["alg_bytes_total"] / max(1, n_loc)
+    res = {
+        "value": value, "ms_per_step": ms_per_step, "steps": steps, "warmup": warmup,
+        "config": {"workload": WORKLOADS[kind]["desc"], "n_individuals": int(kb_np["N"]),
+                   "global_batch": int(total), "hyps_per_gpu": int(n_loc),
+                   "parallelism": f"dp{world} (KB replicated, batch sharded)",
+                   "l2": "flushed (256 MB write) between timed steps; KB > L2",
+                   "path": "per-node" if args.per_node else "default",
+                   "canonical_nodes": pinfo["n_nodes"], "restrict_nodes": pinfo["n_restrict"],
+                   "levels": pinfo["n_levels"], "alg_bytes_per_hyp": alg},
+        "roofline": roofline,
+        "roofline_hyps": {"what": "SURVEY 8(d) unshared per-hypothesis byte model (no CSE / packing / "
+                                  "projection credit): a work-saving ratio, not a hardware fraction",
+                          "unshared_alg_bytes_per_hyp": alg,
+                          "roofline_hyps_per_s": world * peak * 1e9 / max(1.0, alg),
+                          "ratio": value / (world * peak * 1e9 / max(1.0, alg))},
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+        "kernels": classes, "profiled_ms_per_step": prof_ms,
+    }
+    prog.free()
+    kb.free()
+    return res
+
+
+def dry_run(args):
+    """The multi-rank path without a GPU (tests/test_dist_gloo.py runs it under torchrun on gloo):
+    every rank builds only its own slice of the batch, a per-root stand-in for its counts
+    (global root index, tree size, 0, 0) goes through the same all_gather + un-pad as the real
+    run, and rank 0 checks the gathered order."""
+    import torch
+    import torch.distributed as dist
+    from paper_2412_00802_b200 import dist as hdist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    kind = args.workload
+    n_per = args.n_hyps or WORKLOADS[kind]["n_hyps"]
+    kb = workload_kb(kind, args)
+    nodes, kids, roots = rank_hyps(kind, kb, n_per, rank, args)
+    ranges = [(r * n_per, (r + 1) * n_per) for r in range(world)]
+    sizes = np.diff(np.concatenate([[-1], roots.astype(np.int64)]))
+    local = torch.zeros((len(roots), 4), dtype=torch.int64)
+    local[:, 0] = torch.arange(ranges[rank][0], ranges[rank][1])
+    local[:, 1] = torch.from_numpy(sizes)
+    if world > 1:
+        allc = hdist.gather_counts(local, n_per * world, ranges)
+    else:
+        allc = local
+    ok = bool(torch.equal(allc[:, 0], torch.arange(n_per * world)))
+    digest = int(np.bitwise_xor.reduce(nodes.view(np.uint8).reshape(len(nodes), -1).view(np.uint32).ravel()))
+    digests = [None] * world
+    if world > 1:
+        dist.all_gather_object(digests, digest)
+    else:
+        digests = [digest]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "world": world, "workload": kind, "hyps_per_rank": n_per,
+                          "gather_in_order": ok, "tree_nodes_per_rank": [int(x) for x in
+                                                                         allc[:, 1].reshape(world, -1).sum(1)],
+                          "node_digest_per_rank": digests}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0 if ok else 1
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    if args.dry_run:
+        return dry_run(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2412_00802_b200 as hedl
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    main_res = run_workload(args.workload, args, hedl, rank, world, local, args.steps, args.warmup, 12.0)
+    side = {}
+    if args.workload == "c4" and world == 1 and not args.no_c5:
+        torch.cuda.empty_cache()
+        try:   # G = 1 leg of the cardinality / datatype-heavy config (BASELINE configs[4])
+            side["c5"] = run_workload("c5", args, hedl, 0, 1, local, min(args.steps, 3), min(args.warmup, 1), 10.0)
+        except Exception as e:   # an extra; never hide the main number
+            side["c5"] = {"error": repr(e)}
     if rank != 0:
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
         return 0
-
-    # ---- roofline of the dominant kernel class ----
-    peaks = measured_peaks()
-    peak = peaks.get("hbm_gbs")
-    peak_src = "measured" if peak else "fallback"
-    peak = peak or 6650.0
-    top = max(prof, key=lambda e: e["total_ms"]) if prof else None
-    traffic = ncu_traffic()
-    roofline = None
-    if top:
-        ach = top["alg_bytes"] / (top["total_ms"] / 1000.0) / 1e9
-        # ncu traffic is stored per work unit (grid.y: nodes or 256-lane packs) of the captured
-        # launch; scale to this run's average launch
-        tu = traffic.get(top["name"], {}).get("dram_bytes_per_unit") if traffic else None
-        tr = tu * top["units"] / top["launches"] if tu is not None else None
-        roofline = {"bound": "hbm", "kernel": top["name"], "achieved": ach, "peak": peak, "unit": "GB/s",
-                    "frac": ach / peak, "traffic": tr, "peak_source": peak_src,
-                    "alg_bytes_per_launch": top["alg_bytes"] / top["launches"],
-                    "avg_launch_ms": top["total_ms"] / top["launches"],
-                    "share_of_step": top["total_ms"] / t_loc}
-    cpu = None
-    if not args.no_cpu_baseline and world == 1:
-        rate, S, cores, secs = oracle_rate(kb_np, nodes, kids, roots, budget_s=12.0)
-        cpu = {"value": rate, "unit": "hyps/s", "cores": cores, "kind": "oracle",
-               "sample": f"{S} seeded-uniform hypotheses of the C4 batch ({secs:.1f} s)"}
     lat = None
-    if not args.no_latency and world == 1:
+    if not args.no_latency and world == 1 and args.workload == "c4":
+        torch.cuda.empty_cache()
         try:
             lat = c2_latency(hedl, local)
         except Exception as e:  # latency is an extra; never hide the main number
             lat = {"error": str(e)}
         if not args.no_c3:
             try:
-                del prog
-                kb.free()
                 torch.cuda.empty_cache()
                 lat = {"c2": lat, "c3": c3_latency(hedl, local, args.cache)}
             except Exception as e:
                 lat = {"c2": lat, "c3": {"error": str(e)}}
+    r = main_res
     line = {
-        "metric": "hypotheses evaluated/sec", "value": value, "unit": "hyps/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "metric": "hypotheses evaluated/sec", "value": r["value"], "unit": "hyps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": "C4: 1M-individual power-law ABox x 1M refinement hypotheses per GPU",
-                   "n_individuals": int(kb_np["N"]), "global_batch": int(len(roots)),
-                   "hyps_per_gpu": int(n_loc), "parallelism": f"dp{world} (KB replicated, batch sharded)",
-                   "l2": "flushed (256 MB write) between timed steps; KB 150 MB > L2",
-                   "path": "per-node" if args.per_node else "default",
-                   "canonical_nodes": pinfo["n_nodes"], "restrict_nodes": pinfo["n_restrict"],
-                   "levels": pinfo["n_levels"], "alg_bytes_per_hyp": pinfo["alg_bytes_total"] / max(1, n_loc)},
-        "roofline": roofline,
-        "roofline_hyps": {"unshared_alg_bytes_per_hyp": pinfo["alg_bytes_total"] / max(1, n_loc),
-                          "roofline_hyps_per_s": world * peak * 1e9 / max(1.0, pinfo["alg_bytes_total"] / max(1, n_loc)),
-                          "frac": value / (world * peak * 1e9 / max(1.0, pinfo["alg_bytes_total"] / max(1, n_loc)))},
-        "cpu_baseline": cpu,
-        "e2e": e2e,
-        "gpu_launches": int(launches),
-        "clocks": clk,
-        "kernels": prof,
-        "latency": lat,
+        "config": r["config"], "roofline": r["roofline"], "roofline_hyps": r["roofline_hyps"],
+        "cpu_baseline": r["cpu_baseline"], "e2e": r["e2e"], "gpu_launches": r["gpu_launches"], "clocks": r["clocks"],
+        "kernels": r["kernels"], "profiled_ms_per_step": r["profiled_ms_per_step"], "latency": lat,
     }
+    line.update(side)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -43,7 +43,7 @@ typedef int32_t hedl_status;
 #define HEDL_ERR_OUT_OF_RANGE 2    /* an id >= its count (individual, concept, role, data, root) */
 #define HEDL_ERR_EXAMPLE_CONFLICT 3 /* an individual is both positive and negative */
 #define HEDL_ERR_BAD_EXPR 4        /* arity, cycle, NaN bound, n > 2^32-2, inverse data property */
-#define HEDL_ERR_PARSE 5           /* reserved (text front end lives in the Python binding) */
+#define HEDL_ERR_PARSE 5           /* hedl_compile_text: syntax error, unknown name, negative n */
 #define HEDL_ERR_CUDA 6            /* CUDA runtime error; the KB handle is poisoned */
 #define HEDL_ERR_OOM 7             /* host or device allocation failed */
 #define HEDL_ERR_UNSUPPORTED 8     /* e.g. no sm_100 device */
@@ -162,6 +162,7 @@ typedef struct hedl_node {
 #define HEDL_COMPILE_NO_CSE 1u            /* do not merge identical subexpressions */
 #define HEDL_COMPILE_NO_REWRITE 2u        /* no flatten / sort / dedupe of AND-OR operands */
 #define HEDL_COMPILE_COMPAT_PAPER_MAX 4u  /* MAX as the paper's cVal>0 && cVal<=rVal */
+#define HEDL_COMPILE_HOST_INPUT 8u        /* hedl_compile_device: the three input arrays are HOST memory */
 
 /* Compile `roots` (indices into nodes) into a program: canonical DAG with
  * common-subexpression reuse across all roots, topological levels, per-node
@@ -187,10 +188,42 @@ hedl_status hedl_compile_ex(const hedl_kb *kb, const hedl_node *nodes, uint32_t 
                             hedl_program **out);
 hedl_status hedl_program_free(hedl_program *prog);
 
+/* Text front end (convenience and tests): SPEC.md:347-355's s-expression grammar
+ *   expr := NAME | "(" ("AND"|"OR") operand+ ")" | "(" ("SOME"|"ONLY") ROLE expr ")"
+ *         | "(" ("MIN"|"EXACTLY"|"MAX") INT ROLE expr ")"
+ *         | "(" "DSOME" NUMROLE (">="|"=="|"<=") DECIMAL ")"
+ *         | "(" "SSOME" STRROLE ("EQUAL"|"CONTAIN") STRING ")"
+ *   operand := expr | "(" "NOT" NAME ")" ;  ROLE := NAME | "(" "INV" NAME ")"
+ * extended with (NOT expr) for any expr (reading Q1), TOP, BOTTOM, empty
+ * AND / OR, (DRANGE NUMROLE lo hi) (closed float32 interval, reading Q9; >=v, ==v, <=v
+ * of DSOME are [v,+inf], [v,v], [-inf,v]) and nested (INV ROLE).  Numbers go through
+ * strtof (reading Q8); STRING is "..." with backslash escaping the next byte.
+ * `names` maps each kind of entity to its id (list index; NULL lists / NULL names =
+ * the spelling c<id>, r<id>, d<id>, s<id>).  The hypotheses become roots 0..n_exprs-1
+ * of one program, compiled as hedl_compile_ex (same flags).  Errors: HEDL_ERR_PARSE
+ * (syntax, unknown name, negative or > 2^32-1 cardinality) with *err_index = the
+ * hypothesis and *err_pos = the byte offset of the offending token (both only set on
+ * PARSE / a null hypothesis); otherwise hedl_compile_ex's errors. */
+typedef struct hedl_names {
+    uint32_t n_concepts;
+    const char *const *concepts;
+    uint32_t n_roles;
+    const char *const *roles;
+    uint32_t n_data;
+    const char *const *data;
+    uint32_t n_strings;
+    const char *const *strings;
+} hedl_names;
+hedl_status hedl_compile_text(const hedl_kb *kb, const hedl_names *names, const char *const *exprs, uint32_t n_exprs,
+                              uint32_t flags, hedl_program **out, uint32_t *err_index, uint32_t *err_pos);
+
 /* Device-side compile (the paper's future work: GPUs generate their own
  * evaluation plans).  Same program as hedl_compile, built on the KB's device from
  * DEVICE arrays (nodes / child_idx / roots as in hedl_compile, in device memory, read
- * on `stream`; the call synchronises `stream` before returning).  The input must list
+ * on `stream`; the call synchronises `stream` before returning).  With
+ * HEDL_COMPILE_HOST_INPUT the three arrays are HOST memory instead: the library
+ * copies them to its scratch on `stream` (DMA straight from page-locked memory), so
+ * host arrays -> program is one call (the e2e path of bench.py).  The input must list
  * children before parents (every child id < its parent's id: the post-order of
  * flattened trees), else BAD_EXPR.  String restrictions, AND/OR with > 64 operands
  * after flattening and inputs deeper than 512 levels are UNSUPPORTED (use
@@ -255,6 +288,48 @@ hedl_status hedl_eval_batch(const hedl_kb *kb, hedl_program *prog, uint32_t firs
 #define HEDL_SCORE_F1 1u
 hedl_status hedl_score_topk(const hedl_counts *counts, uint32_t n, uint32_t metric, uint32_t k, double *scores,
                             uint32_t *top_idx, double *top_scores, int device, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Device memory.  North_star: "PyTorch is used only for device memory, streams
+ * and process groups" -- the library never owns a device allocator of its own
+ * when the caller installs one.
+ *
+ * hedl_set_allocator: every device allocation of the library (KB arrays,
+ * program workspaces, plans, device-compile scratch, score scratch) goes through
+ * alloc(bytes, device, stream, ctx) -> device pointer (NULL = out of memory,
+ * the call then fails with HEDL_ERR_OOM) and is released through
+ * free(ptr, device, stream, ctx).  `device` is the CUDA device the block is for
+ * (it is current during the call), `stream` the cudaStream_t of the API call
+ * that needs it (blocks are used stream-ordered on that stream; a block is freed
+ * only after the library's work on it is complete, or on the stream that used it
+ * last).  Both NULL = the default, cudaMalloc / cudaFree.  The allocator can only
+ * change while no KB is alive (else INVALID_ARG), so every block is freed by the
+ * allocator that made it.  The Python binding installs torch's caching
+ * allocator (torch.cuda.caching_allocator_alloc / _delete).
+ * hedl_alloc_counters: device allocations / frees made so far (diagnostics and
+ * the "no allocation after warm-up" tests). */
+typedef void *(*hedl_dev_alloc_fn)(size_t bytes, int device, void *stream, void *ctx);
+typedef void (*hedl_dev_free_fn)(void *ptr, int device, void *stream, void *ctx);
+hedl_status hedl_set_allocator(hedl_dev_alloc_fn alloc, hedl_dev_free_fn free_fn, void *ctx);
+hedl_status hedl_alloc_counters(uint64_t *n_alloc, uint64_t *n_free);
+
+/* Caller-provided scratch (SURVEY 8(b) "Memory": latency calls never allocate).
+ * hedl_program_workspace_bytes: device bytes one hedl_eval_batch(kb, prog, first_root,
+ *   n_roots, ...) needs -- with_bits != 0 when out_bits will be requested, eval_flags
+ *   the call's HEDL_EVAL_* flags (PER_NODE / FORCE_SLICE change the plan) -- computed
+ *   by the planner's sizing pass, nothing launched.  hedl_eval_one needs the bytes of
+ *   (root, 1, with_bits, HEDL_EVAL_PER_NODE) (its single-CTA path needs none).
+ * hedl_program_set_workspace: `ptr` = DEVICE memory on the KB's device, `bytes` its
+ *   size (>= 4 KiB), owned by the caller and kept alive until the program is freed or
+ *   the workspace replaced (ptr NULL = back to library-allocated memory).  Every later
+ *   evaluation of the program carves its buffers (rows, counts staging, lane-pack
+ *   scratch, plan) out of this block and allocates no device memory; a call that needs
+ *   more returns HEDL_ERR_OOM naming the size.  Calls on one program serialise, so one
+ *   block serves any number of calls.  Both return HEDL_ERR_UNSUPPORTED for programs
+ *   from hedl_compile_device (they plan on the device from the KB's pool). */
+hedl_status hedl_program_workspace_bytes(const hedl_kb *kb, hedl_program *prog, uint32_t first_root,
+                                         uint32_t n_roots, int with_bits, uint32_t eval_flags, uint64_t *bytes);
+hedl_status hedl_program_set_workspace(hedl_program *prog, void *ptr, uint64_t bytes);
 
 /* Device-memory cap for one program's evaluation workspace (default: half the
  * device memory free at first use, at most 48 GiB).  Larger caps give larger

@@ -21,6 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libhedl.so")
 HEDL_COMPILE_NO_CSE = 1
 HEDL_COMPILE_NO_REWRITE = 2
 HEDL_COMPILE_COMPAT_PAPER_MAX = 4
+HEDL_COMPILE_HOST_INPUT = 8
 HEDL_EVAL_COUNTS_DEVICE = 1
 HEDL_EVAL_PER_NODE = 2
 HEDL_EVAL_FORCE_SLICE = 4
@@ -30,8 +31,9 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "OUT_OF_RANGE", 3: "EXAMPLE_CONFLICT", 4
 
 # every symbol include/hedl.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ["hedl_kb_load", "hedl_kb_free", "hedl_kb_get_info", "hedl_compile", "hedl_compile_ex",
-               "hedl_compile_device", "hedl_score_topk",
-               "hedl_program_free",
+               "hedl_compile_device", "hedl_compile_text", "hedl_score_topk",
+               "hedl_program_free", "hedl_set_allocator", "hedl_alloc_counters",
+               "hedl_program_workspace_bytes", "hedl_program_set_workspace",
                "hedl_program_get_info", "hedl_program_root_bytes", "hedl_eval_one", "hedl_eval_batch",
                "hedl_program_set_workspace_limit", "hedl_last_error", "hedl_version", "hedl_prof_enable",
                "hedl_prof_reset", "hedl_prof_read", "hedl_launch_count", "hedl_io_counters"]
@@ -73,12 +75,58 @@ class _ProgInfo(C.Structure):
                 ("alg_bytes_total", C.c_double), ("alg_bytes_shared", C.c_double), ("n_string", C.c_uint32)]
 
 
+class _Names(C.Structure):
+    _fields_ = [("n_concepts", C.c_uint32), ("concepts", C.c_void_p), ("n_roles", C.c_uint32),
+                ("roles", C.c_void_p), ("n_data", C.c_uint32), ("data", C.c_void_p),
+                ("n_strings", C.c_uint32), ("strings", C.c_void_p)]
+
+
 class _ProfEntry(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("launches", C.c_uint64), ("total_ms", C.c_double),
                 ("alg_bytes", C.c_double), ("units", C.c_double)]
 
 
 _lib = None
+
+# hedl_set_allocator callbacks: device memory of the library comes from torch's caching
+# allocator (north_star: PyTorch supplies device memory).  Kept referenced for the process.
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.c_void_p)
+_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p)
+
+
+def _torch_alloc(nbytes, device, stream, ctx):
+    try:
+        import torch
+        return torch.cuda.caching_allocator_alloc(int(nbytes), int(device), int(stream or 0))
+    except Exception:                  # out of memory (or torch unusable): the library reports OOM
+        return None
+
+
+def _torch_free(ptr, device, stream, ctx):
+    try:
+        import torch
+        torch.cuda.caching_allocator_delete(int(ptr))
+    except Exception:                  # interpreter shutdown: torch may already be torn down
+        pass
+
+
+_CALLBACKS = (_ALLOC_FN(_torch_alloc), _FREE_FN(_torch_free))
+
+
+def use_torch_allocator(on: bool = True):
+    """Route the library's device allocations through torch's caching allocator (the default
+    once the library is loaded) or back to cudaMalloc / cudaFree.  Only while no KB is alive."""
+    if on:
+        _check(lib().hedl_set_allocator(_CALLBACKS[0], _CALLBACKS[1], None))
+    else:
+        _check(lib().hedl_set_allocator(None, None, None))
+
+
+def alloc_counters() -> tuple:
+    """(device allocations, device frees) the library has made so far."""
+    a, b = C.c_uint64(), C.c_uint64()
+    _check(lib().hedl_alloc_counters(C.byref(a), C.byref(b)))
+    return int(a.value), int(b.value)
 
 
 def lib():
@@ -111,12 +159,19 @@ def lib():
         "hedl_prof_read": ([C.POINTER(_ProfEntry), C.c_int], C.c_int),
         "hedl_launch_count": ([], U64),
         "hedl_io_counters": ([C.POINTER(U64), C.POINTER(U64)], I32),
+        "hedl_set_allocator": ([_ALLOC_FN, _FREE_FN, P], I32),
+        "hedl_alloc_counters": ([C.POINTER(U64), C.POINTER(U64)], I32),
+        "hedl_program_workspace_bytes": ([P, P, U32, U32, C.c_int, U32, C.POINTER(U64)], I32),
+        "hedl_program_set_workspace": ([P, P, U64], I32),
+        "hedl_compile_text": ([P, C.POINTER(_Names), P, U32, U32, C.POINTER(P), C.POINTER(U32), C.POINTER(U32)], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
         f.argtypes = args
         f.restype = res
     _lib = L
+    if os.environ.get("HEDL_ALLOCATOR", "torch") == "torch":
+        _check(L.hedl_set_allocator(_CALLBACKS[0], _CALLBACKS[1], None))
     return L
 
 
@@ -190,6 +245,25 @@ class Program:
 
     def set_workspace_limit(self, nbytes: int):
         _check(lib().hedl_program_set_workspace_limit(self._h, int(nbytes)))
+
+    def workspace_bytes(self, first: int = 0, n: Optional[int] = None, with_bits: bool = False,
+                        flags: int = 0) -> int:
+        """hedl_program_workspace_bytes: device bytes one eval_batch(first, n) needs."""
+        n = self.n_roots - first if n is None else n
+        out = C.c_uint64()
+        _check(lib().hedl_program_workspace_bytes(self.kb._h, self._h, first, n, 1 if with_bits else 0, flags,
+                                                  C.byref(out)))
+        return int(out.value)
+
+    def set_workspace(self, buf):
+        """hedl_program_set_workspace over a CUDA tensor (kept referenced here), or None."""
+        self._ws = buf
+        if buf is None:
+            _check(lib().hedl_program_set_workspace(self._h, None, 0))
+        else:
+            assert buf.is_cuda and buf.is_contiguous()
+            _check(lib().hedl_program_set_workspace(self._h, C.c_void_p(buf.data_ptr()),
+                                                    buf.numel() * buf.element_size()))
 
     def free(self):
         if self._h:
@@ -280,6 +354,47 @@ def hedl_compile_ex(kb: KB, nodes: np.ndarray, child_idx: np.ndarray, roots: np.
     return Program(h, kb, len(roots))
 
 
+class ParseError(HedlError):
+    """HEDL_ERR_PARSE from hedl_compile_text: .index = hypothesis, .pos = byte offset."""
+
+    def __init__(self, code, msg, index, pos):
+        super().__init__(code, msg)
+        self.index = index
+        self.pos = pos
+
+
+def _cstr_array(names):
+    if names is None:
+        return 0, None, None
+    enc = [s.encode() if isinstance(s, str) else bytes(s) for s in names]
+    arr = (C.c_char_p * max(len(enc), 1))(*enc)
+    return len(enc), C.cast(arr, C.c_void_p), arr
+
+
+def hedl_compile_text(kb: KB, exprs, names: Optional[dict] = None, flags: int = 0) -> Program:
+    """hedl_compile_text: SPEC's s-expression hypotheses (list of str) -> one program.
+    names: {"concepts": [...], "roles": [...], "data": [...], "strings": [...]} (each optional;
+    a missing list means the spelling c<id> / r<id> / d<id> / s<id>)."""
+    names = names or {}
+    keep = []
+    nm = _Names()
+    for f in ("concepts", "roles", "data", "strings"):
+        n, p, arr = _cstr_array(names.get(f))
+        keep.append(arr)
+        setattr(nm, "n_" + f, n)
+        setattr(nm, f, p)
+    enc = [e.encode() if isinstance(e, str) else bytes(e) for e in exprs]
+    arr = (C.c_char_p * max(len(enc), 1))(*enc)
+    h = C.c_void_p()
+    ei, ep = C.c_uint32(0), C.c_uint32(0)
+    code = lib().hedl_compile_text(kb._h, C.byref(nm), C.cast(arr, C.c_void_p), len(enc), flags, C.byref(h),
+                                   C.byref(ei), C.byref(ep))
+    if code == 5:
+        raise ParseError(code, lib().hedl_last_error().decode(errors="replace"), int(ei.value), int(ep.value))
+    _check(code)
+    return Program(h, kb, len(enc))
+
+
 def _dev_u8(a, device):
     """numpy array (any dtype) or CUDA tensor -> (uint8 CUDA tensor sharing the bytes, n elements)."""
     import torch
@@ -295,8 +410,29 @@ def hedl_compile_device(kb: KB, nodes, child_idx, roots, flags: int = 0, stream=
                         n_nodes: Optional[int] = None, n_kids: Optional[int] = None,
                         n_roots: Optional[int] = None) -> Program:
     """hedl_compile_device: the node / child / root arrays in DEVICE memory (CUDA tensors of
-    their bytes, with the counts given) or host numpy arrays (copied to the device first)."""
+    their bytes, with the counts given), or all three in HOST memory (numpy arrays or CPU
+    tensors, ideally page-locked): then the library copies them itself
+    (HEDL_COMPILE_HOST_INPUT) -- host arrays to program in one C-ABI call."""
     import torch
+    host = [not (isinstance(a, torch.Tensor) and a.is_cuda) for a in (nodes, child_idx, roots)]
+    if all(host):
+        def hp(a, dt):
+            if isinstance(a, torch.Tensor):
+                assert a.is_contiguous()
+                return a, a.data_ptr(), None
+            arr = np.ascontiguousarray(a, dtype=dt) if dt is not None else np.ascontiguousarray(a)
+            return arr, arr.ctypes.data, len(arr)
+        an, pn, nn = hp(nodes, None)
+        ak, pk, nk = hp(child_idx, np.uint32)
+        ar, pr, nr = hp(roots, np.uint32)
+        nn = n_nodes if n_nodes is not None else nn
+        nk = n_kids if n_kids is not None else nk
+        nr = n_roots if n_roots is not None else nr
+        h = C.c_void_p()
+        with torch.cuda.device(kb.device):
+            _check(lib().hedl_compile_device(kb._h, C.c_void_p(pn), nn, C.c_void_p(pk), nk, C.c_void_p(pr), nr,
+                                             flags | HEDL_COMPILE_HOST_INPUT, _stream(stream), C.byref(h)))
+        return Program(h, kb, nr)
     with torch.cuda.device(kb.device):
         tn, nn = _dev_u8(nodes, kb.device)
         tk, nk = _dev_u8(np.ascontiguousarray(child_idx, dtype=np.uint32)

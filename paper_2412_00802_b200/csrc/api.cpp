@@ -48,9 +48,52 @@ void *pool_take(const hedl_kb *kb, int role, size_t need, size_t *got) {
     return p;
 }
 
+// ---- device memory (hedl_set_allocator) -------------------------------------------
+// Every device allocation of the library goes through dev_malloc / dev_free: the caller's
+// allocator when one is installed (the Python binding installs torch's caching allocator),
+// else cudaMalloc / cudaFree.  The allocator can only change while no KB is alive, so a
+// block is always freed by the allocator that made it.
+static std::mutex g_alloc_mu;
+static hedl_dev_alloc_fn g_alloc = nullptr;
+static hedl_dev_free_fn g_free = nullptr;
+static void *g_alloc_ctx = nullptr;
+static std::atomic<uint64_t> g_n_alloc{0}, g_n_free{0};
+static int g_live_kbs = 0;
+
+void live_kb_add(int d) {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    g_live_kbs += d;
+}
+
+cudaError_t dev_malloc(void **p, size_t bytes, cudaStream_t s) {
+    *p = nullptr;
+    g_n_alloc.fetch_add(1, std::memory_order_relaxed);
+    if (g_alloc) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        *p = g_alloc(bytes, dev, (void *)s, g_alloc_ctx);
+        return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+    }
+    return cudaMalloc(p, bytes);
+}
+
+bool dev_alloc_installed() { return g_alloc != nullptr; }
+
+void dev_free(void *p, cudaStream_t s) {
+    if (!p) return;
+    g_n_free.fetch_add(1, std::memory_order_relaxed);
+    if (g_free) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        g_free(p, dev, (void *)s, g_alloc_ctx);
+        return;
+    }
+    cudaFree(p);
+}
+
 static void pool_free_one(int role, void *p) {
     if (role == PR_PLAN_HOST || role == PR_DPLAN_HOST) cudaFreeHost(p);
-    else cudaFree(p);
+    else dev_free(p);
 }
 
 void pool_give(const hedl_kb *kb, int role, void *p, size_t bytes) {
@@ -76,7 +119,7 @@ void pool_release_all(hedl_kb *kb) {
 }
 
 const char *kKClassName[KC_N] = {"bool", "restrict", "restrict_heavy", "drange", "cover_init", "gather",
-                                 "slice_pack", "slice", "slice_heavy", "kb", "slice_ex", "interp", "string"};
+                                 "slice_pack", "slice", "slice_heavy", "kb", "slice_ex", "interp", "string", "bool_l2"};
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -136,6 +179,22 @@ extern "C" uint64_t hedl_launch_count(void) { return launches_total(); }
 extern "C" hedl_status hedl_io_counters(uint64_t *h2d, uint64_t *d2h) {
     if (h2d) *h2d = g_h2d.load();
     if (d2h) *d2h = g_d2h.load();
+    return HEDL_OK;
+}
+
+extern "C" hedl_status hedl_set_allocator(hedl_dev_alloc_fn alloc, hedl_dev_free_fn free_fn, void *ctx) {
+    if ((alloc == nullptr) != (free_fn == nullptr)) return fail(HEDL_ERR_INVALID_ARG, "alloc and free must both be set or both be null");
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    if (g_live_kbs > 0) return fail(HEDL_ERR_INVALID_ARG, "the allocator can only change while no KB is alive");
+    g_alloc = alloc;
+    g_free = free_fn;
+    g_alloc_ctx = ctx;
+    return HEDL_OK;
+}
+
+extern "C" hedl_status hedl_alloc_counters(uint64_t *n_alloc, uint64_t *n_free) {
+    if (n_alloc) *n_alloc = g_n_alloc.load();
+    if (n_free) *n_free = g_n_free.load();
     return HEDL_OK;
 }
 

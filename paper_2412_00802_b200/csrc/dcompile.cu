@@ -430,9 +430,13 @@ bool dc_alloc_arrays(hedl_program *p, uint32_t node_cap, uint64_t ops_cap, uint3
 }
 }  // namespace
 
-extern "C" hedl_status hedl_compile_device(const hedl_kb *kb, const hedl_node *nodes, uint32_t n_nodes,
-                                           const uint32_t *child_idx, uint64_t n_child_idx, const uint32_t *roots,
+extern "C" hedl_status hedl_compile_device(const hedl_kb *kb, const hedl_node *nodes_in, uint32_t n_nodes,
+                                           const uint32_t *child_in, uint64_t n_child_idx, const uint32_t *roots_in,
                                            uint32_t n_roots, uint32_t flags, void *stream, hedl_program **out) {
+    const bool host_input = flags & HEDL_COMPILE_HOST_INPUT;
+    flags &= ~HEDL_COMPILE_HOST_INPUT;
+    const hedl_node *nodes = nodes_in;
+    const uint32_t *child_idx = child_in, *roots = roots_in;
     if (!kb || !out) return fail(HEDL_ERR_INVALID_ARG, "null kb/out");
     *out = nullptr;
     if ((n_nodes && !nodes) || (n_child_idx && !child_idx) || (n_roots && !roots))
@@ -469,6 +473,11 @@ extern "C" hedl_status hedl_compile_device(const hedl_kb *kb, const hedl_node *n
         reach = c.take<uint8_t>(n);
         cnt = c.take<DcCounters>(1);
         kbytes = c.take<double>(2 * kb->R + kb->D + 1);
+        if (host_input) {          // device copies of the caller's host arrays (staged below)
+            nodes = c.take<hedl_node>(n);
+            child_idx = c.take<uint32_t>(n_child_idx);
+            roots = c.take<uint32_t>(n_roots);
+        }
         if (pass == 0 && !(sblk = pool_alloc(kb, PR_DC_SCRATCH, c.off, &sgot))) return fail(HEDL_ERR_OOM, "device compile scratch");
     }
     struct GiveBack { const hedl_kb *kb; void *p; size_t b; ~GiveBack() { pool_give(kb, PR_DC_SCRATCH, p, b); } } gb{kb, sblk, sgot};
@@ -489,6 +498,14 @@ extern "C" hedl_status hedl_compile_device(const hedl_kb *kb, const hedl_node *n
         kbb.insert(kbb.end(), kb->data_bytes.begin(), kb->data_bytes.end());
         kbb.push_back(0);
         HEDL_CUDA(kb, cudaMemcpy(kbytes, kbb.data(), kbb.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    if (host_input) {
+        // H2D of the batch on the call's stream: DMA straight from page-locked arrays (the
+        // e2e path of bench.py), staged by the driver from pageable ones
+        HEDL_CUDA(kb, cudaMemcpyAsync((void *)nodes, nodes_in, (size_t)n * sizeof(hedl_node), cudaMemcpyHostToDevice, s));
+        HEDL_CUDA(kb, cudaMemcpyAsync((void *)child_idx, child_in, n_child_idx * 4, cudaMemcpyHostToDevice, s));
+        HEDL_CUDA(kb, cudaMemcpyAsync((void *)roots, roots_in, (size_t)n_roots * 4, cudaMemcpyHostToDevice, s));
+        count_io((size_t)n * sizeof(hedl_node) + n_child_idx * 4 + (size_t)n_roots * 4, 0);
     }
     const DcKb dk{kb->C, kb->R, kb->D, kb->W, kbytes, kbytes + 2 * kb->R};
     DcCounters init{0, 0, 0, ~0ull, 0, 0};

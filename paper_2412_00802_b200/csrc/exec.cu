@@ -28,11 +28,29 @@ Workspace *ws_of(hedl_program *p) {
     return (Workspace *)p->ws;
 }
 
-hedl_status grow(const hedl_kb *kb, cudaStream_t s, DevBuf &b, size_t need, bool zero, int role) {
+// a sub-block of the caller's workspace (hedl_program_set_workspace); OOM when it is full
+static hedl_status carve(const hedl_kb *kb, cudaStream_t s, Workspace *w, void **p, size_t need, bool zero) {
+    const size_t a = align_up(need, 256);
+    if (w->ext_used + a > w->ext_bytes)
+        return fail(HEDL_ERR_OOM, "caller workspace too small (" + std::to_string(w->ext_bytes) +
+                                      " bytes; hedl_program_workspace_bytes gives the need)");
+    *p = w->ext + w->ext_used;
+    w->ext_used += a;
+    if (zero) HEDL_CUDA(kb, cudaMemsetAsync(*p, 0, need, s));
+    return HEDL_OK;
+}
+
+hedl_status grow(const hedl_kb *kb, cudaStream_t s, DevBuf &b, size_t need, bool zero, int role, Workspace *w) {
     if (b.bytes >= need) return HEDL_OK;
+    if (w && w->ext) {
+        hedl_status st = carve(kb, s, w, &b.p, need, zero);
+        b.bytes = st ? 0 : need;
+        if (st) b.p = nullptr;
+        return st;
+    }
     HEDL_CUDA(kb, cudaStreamSynchronize(s));
     size_t sz = std::max(need, b.bytes * 5 / 4);
-    if (b.p) cudaFree(b.p);
+    if (b.p) dev_free(b.p, s);
     b.p = nullptr;
     b.bytes = 0;
     size_t got = 0;
@@ -42,10 +60,10 @@ hedl_status grow(const hedl_kb *kb, cudaStream_t s, DevBuf &b, size_t need, bool
         return HEDL_OK;
     }
     sz = (sz + 255) & ~size_t(255);
-    cudaError_t e = cudaMalloc(&b.p, sz);
+    cudaError_t e = dev_malloc(&b.p, sz, s);
     if (e != cudaSuccess) {
         cudaGetLastError();
-        e = cudaMalloc(&b.p, need);
+        e = dev_malloc(&b.p, need, s);
         if (e != cudaSuccess) { cudaGetLastError(); b.p = nullptr; return fail(HEDL_ERR_OOM, "workspace allocation failed"); }
         sz = need;
     }
@@ -61,14 +79,30 @@ void invalidate_plan(PlanCache &pc) {
 
 void release_plan(PlanCache &pc) {
     if (pc.host) cudaFreeHost(pc.host);
-    if (pc.dev) cudaFree(pc.dev);
+    if (pc.dev) dev_free(pc.dev);
     pc = PlanCache();
 }
 
-hedl_status reserve_plan(const hedl_kb *kb, PlanCache &pc, size_t bytes) {
+hedl_status reserve_plan(const hedl_kb *kb, PlanCache &pc, size_t bytes, Workspace *w) {
     if (pc.cap >= bytes) return HEDL_OK;
+    if (w && w->ext) {      // device blob from the caller's block, pinned host blob from the library
+        const size_t cap = std::max(bytes, (size_t)4096);
+        if (pc.host_cap < cap) {
+            if (pc.host) cudaFreeHost(pc.host);
+            pc.host = nullptr;
+            pc.host_cap = 0;
+            if (cudaMallocHost(&pc.host, cap * 5 / 4) != cudaSuccess) { cudaGetLastError(); pc.host = nullptr; return fail(HEDL_ERR_OOM, "pinned plan"); }
+            pc.host_cap = cap * 5 / 4;
+        }
+        pc.dev = nullptr;
+        pc.cap = 0;
+        hedl_status st = carve(kb, nullptr, w, &pc.dev, cap, false);
+        if (st) return st;
+        pc.cap = cap;
+        return HEDL_OK;
+    }
     if (pc.host) cudaFreeHost(pc.host);
-    if (pc.dev) cudaFree(pc.dev);
+    if (pc.dev) dev_free(pc.dev);
     pc.host = pc.dev = nullptr;
     pc.cap = 0;
     size_t gh = 0, gd = 0;
@@ -83,7 +117,7 @@ hedl_status reserve_plan(const hedl_kb *kb, PlanCache &pc, size_t bytes) {
     if (h) pool_give(kb, PR_PLAN_HOST, h, gh);
     const size_t cap = std::max(bytes, (size_t)4096) * 5 / 4;
     if (cudaMallocHost(&pc.host, cap) != cudaSuccess) { cudaGetLastError(); pc.host = nullptr; return fail(HEDL_ERR_OOM, "pinned plan"); }
-    if (cudaMalloc(&pc.dev, cap) != cudaSuccess) {
+    if (dev_malloc(&pc.dev, cap) != cudaSuccess) {
         cudaGetLastError();
         cudaFreeHost(pc.host);
         pc.host = pc.dev = nullptr;
@@ -745,7 +779,7 @@ hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, u
                 kx = KbDev{du.n_u, du.UW, du.UW4, nullptr, nullptr, nullptr, nullptr};
             }
             launch_bool(s, kx, (const BoolDesc *)(d + cp.off_bool) + lr.first_desc, lr.count,
-                        (const Operand *)(d + cp.off_ops), cov, lr.bytes, kb->npos, kb->nneg);
+                        (const Operand *)(d + cp.off_ops), cov, lr.bytes, kb->npos, kb->nneg, !lr.proj && lr.usp < 0);
 
         } else if (lr.kind == NK_RESTRICT) {
             const hedl_dir &dr = kb->dirs[lr.key];
@@ -784,9 +818,17 @@ namespace {
 
 // Evaluate roots [r0, r1) of the program.  counts_dev: device hedl_counts[r1-r0];
 // out_bits: device [r1-r0][W] or null.
+// *counts_io == null: the counts go to the workspace's staging buffer (host-bound results),
+// whose address is returned in *counts_io.
 hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, uint32_t *out_bits,
-                hedl_counts *counts_dev, cudaStream_t s, uint32_t eflags) {
+                hedl_counts **counts_io, cudaStream_t s, uint32_t eflags) {
     Workspace *w = ws_of(p);
+    auto ensure_stage = [&]() -> hedl_status {
+        if (*counts_io) return HEDL_OK;
+        hedl_status st2 = grow(kb, s, w->stage, (size_t)(r1 - r0) * sizeof(hedl_counts), false, PR_COUNTS, w);
+        if (!st2) *counts_io = (hedl_counts *)w->stage.p;
+        return st2;
+    };
     if (w->used && w->last_stream != s && w->done) HEDL_CUDA(kb, cudaStreamWaitEvent(s, w->done, 0));
     PlanCache &pc = w->plan;
     const bool bits = out_bits != nullptr;
@@ -798,13 +840,25 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
         // the previous plan's blobs may still be read by queued work: wait, then reuse them
         if (w->used && w->done) HEDL_CUDA(kb, cudaEventSynchronize(w->done));
         invalidate_plan(pc);
+        if (w->ext) {
+            // caller's block: every buffer is re-carved from its start for the new plan (the
+            // queued work reading the old carve finished above); the staging of host-bound
+            // counts is always carved, so later calls of this range never need more
+            w->ext_used = 0;
+            for (DevBuf *b : {&w->rows, &w->prows, &w->heavy, &w->counts, &w->slice, &w->stage, &w->urows}) *b = DevBuf();
+            pc.dev = nullptr;
+            pc.cap = 0;
+            w->pats = nullptr;
+            if ((st = grow(kb, s, w->stage, (size_t)(r1 - r0) * sizeof(hedl_counts), false, PR_COUNTS, w))) return st;
+        }
         const size_t row_bytes = (size_t)kb->W4 * 4;
         if (!p->ws_limit) {            // default: half the free device memory, at most 48 GiB
             size_t fr = 0, tot = 0;
             cudaMemGetInfo(&fr, &tot);
             p->ws_limit = std::max<uint64_t>(1ull << 28, std::min<uint64_t>(fr / 2, 48ull << 30));
         }
-        const uint64_t row_cap = std::max<uint64_t>(1, row_bytes ? p->ws_limit / row_bytes : (1ull << 22));
+        const uint64_t lim = w->ext ? std::min<uint64_t>(p->ws_limit, w->ext_bytes) : p->ws_limit;
+        const uint64_t row_cap = std::max<uint64_t>(1, row_bytes ? lim / row_bytes : (1ull << 22));
         if (!p->patterns.empty() && !w->pats) {      // the program's CONTAIN patterns, uploaded once
             std::vector<uint8_t> blob;
             w->pat_off.assign(1, 0);
@@ -812,7 +866,9 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
                 blob.insert(blob.end(), q.begin(), q.end());
                 w->pat_off.push_back(blob.size());
             }
-            if (cudaMalloc((void **)&w->pats, std::max<size_t>(blob.size(), 16)) != cudaSuccess) {
+            if (w->ext) {
+                if ((st = carve(kb, s, w, (void **)&w->pats, std::max<size_t>(blob.size(), 16), false))) return st;
+            } else if (dev_malloc((void **)&w->pats, std::max<size_t>(blob.size(), 16), s) != cudaSuccess) {
                 cudaGetLastError();
                 w->pats = nullptr;
                 return fail(HEDL_ERR_OOM, "pattern table");
@@ -844,14 +900,20 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
             max_cov = std::max<size_t>(max_cov, cp.ncov);
         }
         const double tb = now_ms();
-        if ((st = grow(kb, s, w->rows, max_nn * row_bytes + 16, false, PR_ROWS))) return st;
-        if ((st = grow(kb, s, w->prows, max_np * kb->MW4 * 4 + 16, false, PR_PROWS))) return st;
+        if ((st = grow(kb, s, w->rows, max_nn * row_bytes + 16, false, PR_ROWS, w))) return st;
+        if ((st = grow(kb, s, w->prows, max_np * kb->MW4 * 4 + 16, false, PR_PROWS, w))) return st;
         uint32_t uw4max = 0;
         for (const hedl_dir &x : kb->dirs) uw4max = std::max(uw4max, x.UW4);
-        if ((st = grow(kb, s, w->urows, max_nu * uw4max * 4 + 16, false, PR_UROWS))) return st;
-        if ((st = grow(kb, s, w->heavy, heavy_need, true, PR_HEAVY))) return st;
-        if ((st = grow(kb, s, w->counts, max_cov * sizeof(hedl_counts), false, PR_COUNTS))) return st;
-        if ((st = reserve_plan(kb, pc, std::max<size_t>(cursor, 256)))) return st;
+        if ((st = grow(kb, s, w->urows, max_nu * uw4max * 4 + 16, false, PR_UROWS, w))) return st;
+        if ((st = grow(kb, s, w->heavy, heavy_need, true, PR_HEAVY, w))) return st;
+        if ((st = grow(kb, s, w->counts, max_cov * sizeof(hedl_counts), false, PR_COUNTS, w))) return st;
+        if ((st = reserve_plan(kb, pc, std::max<size_t>(cursor, 256), w))) return st;
+        bool any_slice = false;
+        for (const ChunkTmp &t : tmps)
+            for (const Group &g : t.groups) any_slice |= g.slice;
+        // lane-pack scratch: allocated lazily by slice_run, carved here in caller-workspace mode
+        if (w->ext && any_slice && (st = grow(kb, s, w->slice, slice_ws_bytes(kb), true, PR_SLICE, w))) return st;
+        if ((st = ensure_stage())) return st;
         const double t2 = now_ms();
         timing_note("plan: buffers", t2 - tb);
         pc.r0 = r0; pc.r1 = r1; pc.bits = bits; pc.eflags = eflags;
@@ -870,15 +932,16 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
             HEDL_CUDA(kb, cudaMemcpyAsync((char *)pc.dev + cp.blob_off, (char *)pc.host + cp.blob_off, cp.blob_bytes,
                                           cudaMemcpyHostToDevice, s));
             count_io(cp.blob_bytes, 0);
-            if ((st = launch_chunk(kb, w, cp, r0, out_bits, counts_dev, s))) { invalidate_plan(pc); return st; }
+            if ((st = launch_chunk(kb, w, cp, r0, out_bits, *counts_io, s))) { invalidate_plan(pc); return st; }
         }
         pc.valid = true;
         timing_note("plan: collect chunks", t1 - t0);
         timing_note("plan: sizes+buffers", t2 - t1);
         timing_note("plan: fill+upload+launch", now_ms() - t2);
     } else {
+        if ((st = ensure_stage())) return st;
         for (const ChunkPlan &cp : pc.chunks)
-            if ((st = launch_chunk(kb, w, cp, r0, out_bits, counts_dev, s))) return st;
+            if ((st = launch_chunk(kb, w, cp, r0, out_bits, *counts_io, s))) return st;
     }
     if (!w->done) HEDL_CUDA(kb, cudaEventCreateWithFlags(&w->done, cudaEventDisableTiming));
     HEDL_CUDA(kb, cudaEventRecord(w->done, s));
@@ -908,14 +971,11 @@ extern "C" hedl_status hedl_eval_batch(const hedl_kb *kb, hedl_program *p, uint3
     std::lock_guard<std::mutex> lk(p->mu);
     DeviceGuard dg(kb->device);
     cudaStream_t s = (cudaStream_t)stream;
-    hedl_counts *dcounts = counts;
     const bool host_out = !(flags & HEDL_EVAL_COUNTS_DEVICE);
+    hedl_counts *dcounts = host_out ? nullptr : counts;    // null: the workspace's device staging
     Workspace *w = ws_of(p);
     const size_t cbytes = (size_t)n * sizeof(hedl_counts);
-    if (host_out) {                                   // device staging kept in the workspace
-        hedl_status st = grow(kb, s, w->stage, cbytes, false, PR_COUNTS);
-        if (st) return st;
-        dcounts = (hedl_counts *)w->stage.p;
+    if (host_out) {
         if (w->stage_host_n < n && n <= (1u << 16)) {  // small results go through pinned memory
             if (w->stage_host) cudaFreeHost(w->stage_host);
             w->stage_host = nullptr;
@@ -931,10 +991,14 @@ extern "C" hedl_status hedl_eval_batch(const hedl_kb *kb, hedl_program *p, uint3
     if (p->dev && !p->dev_downloaded) {
         // device-compiled program: plan on the device; a batch that needs several chunks
         // goes to the host planner (one download of the program)
+        if (host_out) {
+            if ((st = grow(kb, s, w->stage, cbytes, false, PR_COUNTS))) return st;
+            dcounts = (hedl_counts *)w->stage.p;
+        }
         st = dplan_run(kb, p, first, first + n, out_bits, dcounts, s, ef);
-        if (st == HEDL_ERR_UNSUPPORTED && !(st = dc_download(p))) st = run(kb, p, first, first + n, out_bits, dcounts, s, ef);
+        if (st == HEDL_ERR_UNSUPPORTED && !(st = dc_download(p))) st = run(kb, p, first, first + n, out_bits, &dcounts, s, ef);
     } else {
-        st = run(kb, p, first, first + n, out_bits, dcounts, s, ef);
+        st = run(kb, p, first, first + n, out_bits, &dcounts, s, ef);
     }
     if (host_out && st == HEDL_OK) {
         const bool pinned = w->stage_host && w->stage_host_n >= n;
@@ -1053,18 +1117,22 @@ extern "C" hedl_status hedl_program_free(hedl_program *p) {
         Workspace *w = (Workspace *)p->ws;
         DeviceGuard dg(p->kb->device);
         if (w->done) cudaEventSynchronize(w->done);
-        const int roles[] = {PR_ROWS, PR_PROWS, PR_HEAVY, PR_COUNTS, PR_SLICE, PR_UROWS};
-        int ri = 0;
-        for (DevBuf *b : {&w->rows, &w->prows, &w->heavy, &w->counts, &w->slice, &w->urows})
-            pool_give(p->kb, roles[ri++], b->p, b->bytes);
-        pool_give(p->kb, PR_COUNTS, w->stage.p, w->stage.bytes);
+        if (w->ext) {                   // buffers carved from the caller's block: not ours
+            if (w->plan.host) cudaFreeHost(w->plan.host);
+        } else {
+            const int roles[] = {PR_ROWS, PR_PROWS, PR_HEAVY, PR_COUNTS, PR_SLICE, PR_UROWS};
+            int ri = 0;
+            for (DevBuf *b : {&w->rows, &w->prows, &w->heavy, &w->counts, &w->slice, &w->urows})
+                pool_give(p->kb, roles[ri++], b->p, b->bytes);
+            pool_give(p->kb, PR_COUNTS, w->stage.p, w->stage.bytes);
+            pool_give(p->kb, PR_PLAN_HOST, w->plan.host, w->plan.cap);
+            pool_give(p->kb, PR_PLAN_DEV, w->plan.dev, w->plan.cap);
+            if (w->pats) dev_free(w->pats);
+        }
         if (w->stage_host) cudaFreeHost(w->stage_host);
-        pool_give(p->kb, PR_PLAN_HOST, w->plan.host, w->plan.cap);
-        pool_give(p->kb, PR_PLAN_DEV, w->plan.dev, w->plan.cap);
         w->plan.host = w->plan.dev = nullptr;
         release_plan(w->plan);
         if (w->done) cudaEventDestroy(w->done);
-        if (w->pats) cudaFree(w->pats);
         if (p->lat_host) cudaFreeHost(p->lat_host);
         delete w;
     } else if (p->lat_host) {
@@ -1078,6 +1146,104 @@ extern "C" hedl_status hedl_program_free(hedl_program *p) {
     }
     delete p;
     kb_release(kb);
+    return HEDL_OK;
+}
+
+// Device bytes one hedl_eval_batch(first, n) of a host-compiled program needs from a caller's
+// workspace: the sizing pass of the planner (run(), phases A-B) without any launch.
+extern "C" hedl_status hedl_program_workspace_bytes(const hedl_kb *kb, hedl_program *p, uint32_t first, uint32_t n,
+                                                    int with_bits, uint32_t eflags, uint64_t *bytes) {
+    if (!kb || !p || !bytes) return fail(HEDL_ERR_INVALID_ARG, "null kb/program/bytes");
+    if (p->kb != kb) return fail(HEDL_ERR_INVALID_ARG, "program was compiled for another KB");
+    if (p->dev && !p->dev_downloaded) return fail(HEDL_ERR_UNSUPPORTED, "device-compiled programs plan on the device (use hedl_compile)");
+    if ((uint64_t)first + n > prog_n_roots(p)) return fail(HEDL_ERR_OUT_OF_RANGE, "root range out of range");
+    std::lock_guard<std::mutex> lk(p->mu);
+    DeviceGuard dg(kb->device);
+    eflags &= ~HEDL_EVAL_COUNTS_DEVICE;
+    size_t total = 0;
+    auto add = [&](size_t b) { total += align_up(std::max<size_t>(b, 1), 256); };
+    add((size_t)n * sizeof(hedl_counts));                                       // counts staging
+    if (!p->patterns.empty()) {
+        size_t pb = 0;
+        for (const std::string &q : p->patterns) pb += q.size();
+        add(std::max<size_t>(pb, 16));
+    }
+    if (n) {
+        if (!p->ws_limit) {
+            size_t fr = 0, tot = 0;
+            cudaMemGetInfo(&fr, &tot);
+            p->ws_limit = std::max<uint64_t>(1ull << 28, std::min<uint64_t>(fr / 2, 48ull << 30));
+        }
+        const size_t row_bytes = (size_t)kb->W4 * 4;
+        const uint64_t row_cap = std::max<uint64_t>(1, row_bytes ? p->ws_limit / row_bytes : (1ull << 22));
+        const bool use_slice = !(eflags & HEDL_EVAL_PER_NODE) && slice_enabled(kb);
+        std::vector<std::vector<uint32_t>> lists;
+        std::vector<std::pair<uint32_t, uint32_t>> ranges;
+        collect_chunks(p, first, first + n, row_cap, lists, ranges);
+        std::vector<uint32_t> local(p->nodes.size());
+        size_t cursor = 0, heavy_need = 16, max_nn = 1, max_cov = 1, max_np = 1, max_nu = 1;
+        bool any_slice = false;
+        for (size_t c = 0; c < lists.size(); ++c) {
+            ChunkPlan cp;
+            ChunkTmp tmp;
+            cp.ri = ranges[c].first;
+            cp.rc = ranges[c].second;
+            fill_chunk(kb, p, lists[c], cp, with_bits != 0, use_slice, eflags & HEDL_EVAL_FORCE_SLICE, nullptr, nullptr,
+                       nullptr, local, nullptr, &cursor, &heavy_need, true, tmp);
+            max_nn = std::max<size_t>(max_nn, cp.nrows);
+            max_np = std::max<size_t>(max_np, cp.nprows);
+            max_nu = std::max<size_t>(max_nu, cp.nurows);
+            max_cov = std::max<size_t>(max_cov, cp.ncov);
+            for (const Group &g : tmp.groups) any_slice |= g.slice;
+        }
+        uint32_t uw4max = 0;
+        for (const hedl_dir &x : kb->dirs) uw4max = std::max(uw4max, x.UW4);
+        add(max_nn * row_bytes + 16);
+        add(max_np * kb->MW4 * 4 + 16);
+        add(max_nu * uw4max * 4 + 16);
+        add(heavy_need);
+        add(max_cov * sizeof(hedl_counts));
+        add(std::max<size_t>(std::max<size_t>(cursor, 256), 4096));             // device plan blob
+        if (any_slice) add(slice_ws_bytes(kb));
+    }
+    *bytes = total;
+    return HEDL_OK;
+}
+
+// Caller-provided workspace: every later evaluation of `p` carves its device buffers out of
+// [ptr, ptr + bytes) and never allocates device memory (OOM when the block is too small).
+extern "C" hedl_status hedl_program_set_workspace(hedl_program *p, void *ptr, uint64_t bytes) {
+    if (!p) return fail(HEDL_ERR_INVALID_ARG, "null program");
+    if (ptr && bytes < 4096) return fail(HEDL_ERR_INVALID_ARG, "workspace smaller than 4 KiB");
+    if (p->dev && !p->dev_downloaded && ptr)
+        return fail(HEDL_ERR_UNSUPPORTED, "device-compiled programs plan on the device (use hedl_compile)");
+    std::lock_guard<std::mutex> lk(p->mu);
+    DeviceGuard dg(p->kb->device);
+    Workspace *w = ws_of(p);
+    if (w->done) cudaEventSynchronize(w->done);
+    invalidate_plan(w->plan);
+    if (w->ext) {                       // detach: carved buffers are not ours to free
+        for (DevBuf *b : {&w->rows, &w->prows, &w->heavy, &w->counts, &w->slice, &w->stage, &w->urows}) *b = DevBuf();
+        w->plan.dev = nullptr;
+        w->plan.cap = 0;
+        w->pats = nullptr;
+    } else {                            // library-owned buffers go back to the KB's pool
+        const int roles[] = {PR_ROWS, PR_PROWS, PR_HEAVY, PR_COUNTS, PR_SLICE, PR_UROWS, PR_COUNTS};
+        int ri = 0;
+        for (DevBuf *b : {&w->rows, &w->prows, &w->heavy, &w->counts, &w->slice, &w->urows, &w->stage}) {
+            pool_give(p->kb, roles[ri++], b->p, b->bytes);
+            *b = DevBuf();
+        }
+        if (w->plan.dev) pool_give(p->kb, PR_PLAN_DEV, w->plan.dev, w->plan.cap);
+        if (w->plan.host) pool_give(p->kb, PR_PLAN_HOST, w->plan.host, w->plan.cap);
+        w->plan.dev = w->plan.host = nullptr;
+        w->plan.cap = w->plan.host_cap = 0;
+        if (w->pats) dev_free(w->pats);
+        w->pats = nullptr;
+    }
+    w->ext = (char *)ptr;
+    w->ext_bytes = ptr ? bytes : 0;
+    w->ext_used = 0;
     return HEDL_OK;
 }
 

@@ -40,6 +40,7 @@ struct PlanCache {
     void *host = nullptr;                 // pinned descriptor blob
     void *dev = nullptr;                  // device descriptor blob
     size_t cap = 0;                       // capacity of both blobs
+    size_t host_cap = 0;                  // capacity of the host blob (caller-workspace mode)
 };
 
 struct Workspace {
@@ -52,13 +53,18 @@ struct Workspace {
     cudaEvent_t done = nullptr;
     cudaStream_t last_stream = nullptr;
     bool used = false;
+    // caller-provided device block (hedl_program_set_workspace): while set, every buffer
+    // above (and the device plan blob, the pattern table) is carved out of it, re-carved
+    // from its start whenever the plan is rebuilt; nothing is allocated or freed
+    char *ext = nullptr;
+    size_t ext_bytes = 0, ext_used = 0;
 };
 
 Workspace *ws_of(hedl_program *p);
-hedl_status grow(const hedl_kb *kb, cudaStream_t s, DevBuf &b, size_t need, bool zero, int role);
+hedl_status grow(const hedl_kb *kb, cudaStream_t s, DevBuf &b, size_t need, bool zero, int role, Workspace *w = nullptr);
 void invalidate_plan(PlanCache &pc);
 void release_plan(PlanCache &pc);
-hedl_status reserve_plan(const hedl_kb *kb, PlanCache &pc, size_t bytes);
+hedl_status reserve_plan(const hedl_kb *kb, PlanCache &pc, size_t bytes, Workspace *w = nullptr);
 hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, uint32_t r0, uint32_t *out_bits,
                          hedl_counts *counts_dev, cudaStream_t s);
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }

@@ -225,12 +225,17 @@ enum PoolRole { PR_ROWS, PR_PROWS, PR_HEAVY, PR_COUNTS, PR_SLICE, PR_PLAN_DEV, P
 void *pool_take(const hedl_kb *kb, int role, size_t need, size_t *got);
 void pool_give(const hedl_kb *kb, int role, void *p, size_t bytes);
 void pool_release_all(hedl_kb *kb);
-// a device block from the pool (best fit) or cudaMalloc (25% headroom); null on OOM
+// device memory: the caller's allocator (hedl_set_allocator) or cudaMalloc / cudaFree
+cudaError_t dev_malloc(void **p, size_t bytes, cudaStream_t s = nullptr);
+void dev_free(void *p, cudaStream_t s = nullptr);
+bool dev_alloc_installed();
+void live_kb_add(int d);                   // KBs alive (the allocator may change only at 0)
+// a device block from the pool (best fit) or dev_malloc (25% headroom); null on OOM
 inline void *pool_alloc(const hedl_kb *kb, int role, size_t need, size_t *got) {
     if (void *q = pool_take(kb, role, need, got)) return q;
     void *q = nullptr;
     const size_t sz = (need * 5 / 4 + 255) & ~size_t(255);
-    if (cudaMalloc(&q, sz) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    if (dev_malloc(&q, sz) != cudaSuccess) { cudaGetLastError(); return nullptr; }
     *got = sz;
     return q;
 }
@@ -265,7 +270,7 @@ void timing_note(const char *what, double ms);
 
 // ---- profiling -----------------------------------------------------------------
 enum KClass { KC_BOOL, KC_RESTRICT, KC_HEAVY, KC_DRANGE, KC_COVER_INIT, KC_GATHER,
-              KC_SLICE_IN, KC_SLICE, KC_SLICE_HEAVY, KC_KB, KC_SLICE_EX, KC_INTERP, KC_STRING, KC_N };
+              KC_SLICE_IN, KC_SLICE, KC_SLICE_HEAVY, KC_KB, KC_SLICE_EX, KC_INTERP, KC_STRING, KC_BOOL_L2, KC_N };
 extern const char *kKClassName[KC_N];
 void prof_begin(cudaStream_t s, int kc);
 void prof_end(cudaStream_t s, int kc, double alg_bytes, double units = 1);
@@ -346,7 +351,8 @@ static __device__ __forceinline__ void proj_scatter(const KbDev &kb, uint32_t *p
 #endif
 void launch_cover_init(cudaStream_t s, hedl_counts *counts, uint32_t n, uint64_t npos, uint64_t nneg);
 void launch_bool(cudaStream_t s, const KbDev &kb, const BoolDesc *d_desc, uint32_t n_desc,
-                 const Operand *d_ops, hedl_counts *counts, double alg_bytes, uint64_t npos, uint64_t nneg);
+                 const Operand *d_ops, hedl_counts *counts, double alg_bytes, uint64_t npos, uint64_t nneg,
+                 bool full_rows);
 void launch_restrict(cudaStream_t s, const KbDev &kb, const DirDev &dir, const RestrictDesc *d_desc,
                      uint32_t n_desc, hedl_counts *counts, uint32_t *heavy_scratch, double alg_light,
                      double alg_heavy);

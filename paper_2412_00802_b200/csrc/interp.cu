@@ -139,7 +139,7 @@ hedl_status interp_prepare(hedl_kb *kb) {
     for (auto &d : kb->data) h.push_back(d.row_ptr);
     for (auto &d : kb->data) h.push_back(d.val);
     void *p = nullptr;
-    if (cudaMalloc(&p, h.size() * sizeof(void *)) != cudaSuccess) { cudaGetLastError(); return fail(HEDL_ERR_OOM, "interp pointers"); }
+    if (dev_malloc(&p, h.size() * sizeof(void *)) != cudaSuccess) { cudaGetLastError(); return fail(HEDL_ERR_OOM, "interp pointers"); }
     kb->allocs.push_back(p);
     if (cudaMemcpy(p, h.data(), h.size() * sizeof(void *), cudaMemcpyHostToDevice) != cudaSuccess)
         return cuda_fail(kb, cudaGetLastError(), "interp pointers");

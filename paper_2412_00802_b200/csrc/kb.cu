@@ -88,9 +88,9 @@ template <class T>
 hedl_status upload(hedl_kb *kb, cudaStream_t st, T **dst, const T *src, size_t n) {
     size_t bytes = std::max<size_t>(n * sizeof(T), 16);
     void *p = nullptr;
-    cudaError_t e = cudaMalloc(&p, bytes);
+    cudaError_t e = dev_malloc(&p, bytes, st);
     if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? fail(HEDL_ERR_OOM, "device allocation failed")
-                                                                : cuda_fail(kb, e, "cudaMalloc");
+                                                                : cuda_fail(kb, e, "device allocation");
     kb->allocs.push_back(p);
     kb->device_bytes += bytes;
     if (n) HEDL_CUDA(kb, cudaMemcpyAsync(p, src, n * sizeof(T), cudaMemcpyHostToDevice, st));
@@ -104,9 +104,10 @@ void free_kb(hedl_kb *kb) {
     cudaGetDevice(&prev);
     cudaSetDevice(kb->device);
     pool_release_all(kb);
-    for (void *p : kb->allocs) cudaFree(p);
+    for (void *p : kb->allocs) dev_free(p);
     cudaSetDevice(prev);
     delete kb;
+    live_kb_add(-1);
 }
 
 }  // namespace
@@ -254,6 +255,7 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
     if (cudaSetDevice(device) != cudaSuccess) return fail(HEDL_ERR_CUDA, "cudaSetDevice failed");
     cudaStream_t st = (cudaStream_t)stream;
     hedl_kb *kb = new hedl_kb();
+    live_kb_add(1);
     kb->device = device;
     kb->sm_count = prop.multiProcessorCount;
     kb->N = N; kb->W = W; kb->W4 = W4; kb->C = C; kb->R = R; kb->D = D;

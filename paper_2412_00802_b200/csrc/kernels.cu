@@ -83,6 +83,9 @@ __global__ void k_cover_init(hedl_counts *c, uint32_t n, uint64_t npos, uint64_t
 // staged in shared memory once, so the operand loop has no dependent global load.
 constexpr int kBoolU = 8;
 constexpr uint32_t kBoolSmemOps = 64;
+// FULL: rows over all N individuals (else projected / U rows): the same code, instantiated twice
+// so profiles (ncu kernel names) tell the HBM-sized launches from the L2-sized ones
+template <bool FULL>
 __global__ void __launch_bounds__(256) k_bool(KbDev kb, const BoolDesc *__restrict__ descs,
                                               const Operand *__restrict__ ops, hedl_counts *counts) {
     const BoolDesc d = descs[blockIdx.y];
@@ -154,6 +157,7 @@ __global__ void __launch_bounds__(256) k_bool(KbDev kb, const BoolDesc *__restri
 // (the node is never split across warps, so no atomics).
 constexpr uint32_t kBoolWarpMaxN4 = 1024;     // rows up to 4,096 words
 
+template <bool FULL>
 __global__ void __launch_bounds__(256) k_bool_warp(KbDev kb, const BoolDesc *__restrict__ descs, uint32_t n_desc,
                                                    const Operand *__restrict__ ops, hedl_counts *counts,
                                                    uint64_t npos, uint64_t nneg) {
@@ -544,14 +548,19 @@ void launch_cover_init(cudaStream_t s, hedl_counts *counts, uint32_t n, uint64_t
     prof_end(s, KC_COVER_INIT, 32.0 * n, n);
 }
 
+// full_rows: the rows span all N individuals (HBM-sized); otherwise they are example-projected
+// or U rows (kilobytes per row, L2-resident) and the launch is profiled as its own class
 void launch_bool(cudaStream_t s, const KbDev &kb, const BoolDesc *d_desc, uint32_t n_desc,
-                 const Operand *d_ops, hedl_counts *counts, double alg_bytes, uint64_t npos, uint64_t nneg) {
+                 const Operand *d_ops, hedl_counts *counts, double alg_bytes, uint64_t npos, uint64_t nneg,
+                 bool full_rows) {
+    const int kc = full_rows ? KC_BOOL : KC_BOOL_L2;
     if (kb.W4 && (kb.W4 >> 2) <= kBoolWarpMaxN4 && n_desc >= 64) {
         const uint32_t g = std::min<uint32_t>(cdiv(n_desc, 8), 148u * 16u);
-        prof_begin(s, KC_BOOL);
-        k_bool_warp<<<g, 256, 0, s>>>(kb, d_desc, n_desc, d_ops, counts, npos, nneg);
+        prof_begin(s, kc);
+        if (full_rows) k_bool_warp<true><<<g, 256, 0, s>>>(kb, d_desc, n_desc, d_ops, counts, npos, nneg);
+        else k_bool_warp<false><<<g, 256, 0, s>>>(kb, d_desc, n_desc, d_ops, counts, npos, nneg);
         count_launch();
-        prof_end(s, KC_BOOL, alg_bytes, n_desc);
+        prof_end(s, kc, alg_bytes, n_desc);
         return;
     }
     for (uint32_t off = 0; off < n_desc; off += 65535) {
@@ -563,10 +572,11 @@ void launch_bool(cudaStream_t s, const KbDev &kb, const BoolDesc *d_desc, uint32
         // more CTAs per node (down to one word per thread) when it has few
         const uint32_t want = std::max<uint32_t>(gU, std::min<uint32_t>(g1, cdiv(148u * 8u, nd)));
         dim3 grid(want, nd);
-        prof_begin(s, KC_BOOL);
-        k_bool<<<grid, 256, 0, s>>>(kb, d_desc + off, d_ops, counts);
+        prof_begin(s, kc);
+        if (full_rows) k_bool<true><<<grid, 256, 0, s>>>(kb, d_desc + off, d_ops, counts);
+        else k_bool<false><<<grid, 256, 0, s>>>(kb, d_desc + off, d_ops, counts);
         count_launch();
-        prof_end(s, KC_BOOL, alg_bytes * nd / n_desc, nd);
+        prof_end(s, kc, alg_bytes * nd / n_desc, nd);
     }
 }
 

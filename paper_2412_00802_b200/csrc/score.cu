@@ -164,7 +164,8 @@ extern "C" hedl_status hedl_score_topk(const hedl_counts *counts, uint32_t n, ui
     c.take<uint32_t>(8);
     c.take<SelState>(1);
     void *blk = nullptr;
-    cudaError_t e = cudaMallocAsync(&blk, c.off, s);
+    // the caller's allocator when installed (hedl_set_allocator), else the stream-ordered pool
+    cudaError_t e = dev_alloc_installed() ? dev_malloc(&blk, c.off, s) : cudaMallocAsync(&blk, c.off, s);
     if (e != cudaSuccess) { cudaGetLastError(); return fail(HEDL_ERR_OOM, "top-k scratch"); }
     Carver d{(char *)blk, 0};
     unsigned long long *keys = d.take<unsigned long long>(n);
@@ -197,7 +198,8 @@ extern "C" hedl_status hedl_score_topk(const hedl_counts *counts, uint32_t n, ui
         k_sort_topk<<<1, 1024, smem, s>>>(cand, k, P, keys, top_idx, top_scores);
         for (int q = 0; q < 3; ++q) count_launch();
     }
-    cudaFreeAsync(blk, s);
+    if (dev_alloc_installed()) dev_free(blk, s);
+    else cudaFreeAsync(blk, s);
     e = cudaGetLastError();
     if (e != cudaSuccess) return fail(HEDL_ERR_CUDA, std::string("score_topk: ") + cudaGetErrorString(e));
     return HEDL_OK;

@@ -821,30 +821,48 @@ uint32_t slice_class(uint32_t pred, uint32_t n, uint32_t sat) {
     return 2;                                // per-node kernel
 }
 
+namespace {
+// One fixed scratch layout for every direction of the KB (sized by the largest heavy lists),
+// so the self-cleaning accumulators of one direction never alias another's results:
+//   [T x max_batch][full-pack heavy scratch (nh)][EX heavy scratch (max_batch x nhx)][sched]
+struct SliceLayout {
+    size_t t_bytes, tx_bytes, off_hf, off_hx, need, nh, nhx;
+    uint32_t max_batch;
+};
+SliceLayout slice_layout(const hedl_kb *kb) {
+    SliceLayout L;
+    L.t_bytes = (size_t)kb->W4 * 32 * 32;                 // full packs: 32 B per individual
+    size_t nu_max = 0;
+    for (const hedl_dir &x : kb->dirs) nu_max = std::max<size_t>({nu_max, (size_t)x.n_u, (size_t)x.UW4 * 32});
+    L.tx_bytes = std::max<size_t>(nu_max * 32, 256);      // EX packs: 32 B per neighbour of an example
+    L.nh = L.nhx = 0;
+    for (const hedl_dir &x : kb->dirs) {
+        L.nh = std::max<size_t>(L.nh, x.n_heavy);
+        L.nhx = std::max<size_t>(L.nhx, x.n_ex_heavy);
+    }
+    const size_t per_h = (LW + 256 + 1 + LW) * 4;
+    L.max_batch = (uint32_t)std::max<size_t>(1, std::min<size_t>(128, (4ull << 30) / L.tx_bytes));
+    L.off_hf = std::max(L.t_bytes, L.tx_bytes * L.max_batch);
+    L.off_hx = L.off_hf + L.nh * per_h;
+    L.need = L.off_hx + (size_t)L.max_batch * L.nhx * per_h + 256;
+    return L;
+}
+}  // namespace
+
+size_t slice_ws_bytes(const hedl_kb *kb) { return slice_layout(kb).need; }
+
 hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream_t s, const KbDev &kd, uint32_t dirid,
                       const RestrictDesc *h_desc, const RestrictDesc *d_desc, uint32_t n, hedl_counts *counts, bool ex,
                       int fixed_cls, bool ucomp) {
     const hedl_dir &dr = kb->dirs[dirid];
     if (ex && !kb->M) return HEDL_OK;                     // no examples: nothing to evaluate
-    const size_t t_bytes = (size_t)kb->W4 * 32 * 32;     // full packs: 32 B per individual
-    size_t nu_max = 0;
-    for (const hedl_dir &x : kb->dirs) nu_max = std::max<size_t>({nu_max, (size_t)x.n_u, (size_t)x.UW4 * 32});
-    const size_t tx_bytes = std::max<size_t>(nu_max * 32, 256);   // EX packs: 32 B per neighbour of an example
-    // one fixed layout for every direction (sized by the largest heavy lists), so the
-    // self-cleaning accumulators of one direction never alias another's results:
-    //   [T x kMaxBatch][full-pack heavy scratch (nh)][EX heavy scratch (kMaxBatch x nhx)]
-    size_t nh = 0, nhx = 0;
-    for (const hedl_dir &x : kb->dirs) {
-        nh = std::max<size_t>(nh, x.n_heavy);
-        nhx = std::max<size_t>(nhx, x.n_ex_heavy);
-    }
-    const size_t per_h = (LW + 256 + 1 + LW) * 4;
-    const uint32_t max_batch = (uint32_t)std::max<size_t>(1, std::min<size_t>(128, (4ull << 30) / tx_bytes));
-    const size_t off_hf = std::max(t_bytes, tx_bytes * max_batch), off_hx = off_hf + nh * per_h;
-    const size_t need = off_hx + (size_t)max_batch * nhx * per_h + 256;
+    const SliceLayout lay = slice_layout(kb);
+    const size_t t_bytes = lay.t_bytes, tx_bytes = lay.tx_bytes;
+    const size_t nh = lay.nh, nhx = lay.nhx, off_hf = lay.off_hf, off_hx = lay.off_hx, need = lay.need;
+    const uint32_t max_batch = lay.max_batch;
     if (*ws_bytes < need) {
         HEDL_CUDA(kb, cudaStreamSynchronize(s));
-        if (*ws) cudaFree(*ws);
+        if (*ws) dev_free(*ws, s);
         *ws = nullptr;
         *ws_bytes = 0;
         size_t got = 0;
@@ -852,7 +870,7 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             *ws = q;
             *ws_bytes = got;
         } else {
-            if (cudaMalloc(ws, need) != cudaSuccess) { cudaGetLastError(); *ws = nullptr; return fail(HEDL_ERR_OOM, "slice workspace"); }
+            if (dev_malloc(ws, need, s) != cudaSuccess) { cudaGetLastError(); *ws = nullptr; return fail(HEDL_ERR_OOM, "slice workspace"); }
             HEDL_CUDA(kb, cudaMemsetAsync(*ws, 0, need, s));
             *ws_bytes = need;
         }

@@ -349,11 +349,12 @@ def concat_arrays(parts):
 
 
 def batch_arrays(kind: str, kb: dict, n: int, seed: int, chunk: int = 25_000,
-                 workers: Optional[int] = None):
+                 workers: Optional[int] = None, first_chunk: int = 0):
     """Generate a C4/C5-style batch of n hypotheses as flat ABI arrays.
 
     The batch is cut into independent beams of `chunk` hypotheses (seed
-    (seed, i)); each beam keeps its sibling families contiguous.
+    (seed, i)); each beam keeps its sibling families contiguous.  `first_chunk` starts
+    at beam i = first_chunk, so a rank can generate just its own slice of a larger batch.
     """
     import os
     from concurrent.futures import ProcessPoolExecutor
@@ -366,7 +367,7 @@ def batch_arrays(kind: str, kb: dict, n: int, seed: int, chunk: int = 25_000,
     jobs = []
     i = 0
     while i * chunk < n:
-        jobs.append((kind, shape, dq, min(chunk, n - i * chunk), int(seed) * 100003 + i))
+        jobs.append((kind, shape, dq, min(chunk, n - i * chunk), int(seed) * 100003 + first_chunk + i))
         i += 1
     workers = workers or min(len(jobs), os.cpu_count() or 1, 32)
     if workers <= 1 or len(jobs) == 1:

@@ -94,3 +94,19 @@ def load(path):
 
 def all_fixtures():
     return sorted(os.path.join(GOLDEN, f) for f in os.listdir(GOLDEN) if f.endswith(".kbt"))
+
+
+def load_names(path):
+    """The fixture's declared names per kind (hedl_compile_text's name table)."""
+    sec, names = None, {"concepts": [], "roles": [], "data": [], "strings": []}
+    key = {"concepts": "concepts", "roles": "roles", "numeric-roles": "data", "string-roles": "strings"}
+    for raw in open(path):
+        line = raw.strip()
+        if not line or line.startswith(";"):
+            continue
+        if line.startswith("#"):
+            sec = line[1:]
+            continue
+        if sec in key:
+            names[key[sec]] += line.split()
+    return names

@@ -165,3 +165,26 @@ def test_weighted_shard_ranges():
     assert r[0][0] == 0 and r[-1][1] == 1000 and all(a[1] == b[0] for a, b in zip(r, r[1:]))
     sizes = [b - a for a, b in r]
     assert abs(sizes[0] - 500) <= 2 and abs(sizes[1] - 250) <= 2
+
+
+def test_bench_multirank_dry_run(tmp_path):
+    """bench.py's multi-rank path under torchrun (world 2, gloo, no GPU): each rank builds only its
+    own beams of the batch (their node arrays differ), caches are written race-free, and the count
+    all_gather returns every root in global order."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "bench.py"),
+           "--dry-run", "--gpus", "2", "--n-hyps", "2000", "--n-individuals", "20000", "--cache", str(tmp_path)]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["dry_run"] and line["world"] == 2 and line["gather_in_order"]
+    assert line["node_digest_per_rank"][0] != line["node_digest_per_rank"][1]
+    assert not [f for f in os.listdir(tmp_path) if ".tmp" in f]
