@@ -122,6 +122,20 @@ hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *stream, hed
 hedl_status hedl_kb_free(hedl_kb *kb);
 hedl_status hedl_kb_get_info(const hedl_kb *kb, hedl_kb_info *out);
 
+/* Overwrite concept rows [first, first + n) with rows the caller supplies (SURVEY 8(f)
+ * NEXT-4: one hypothesis split across GPUs by individual range; the
+ * ranks all_gather their word segments of each restriction filler and install the
+ * complete rows as "scratch" concepts reserved at load, see
+ * paper_2412_00802_b200/dist.py eval_split).  src: DEVICE u32 [parts][n][part_words] --
+ * row i is the concatenation over p of src[p][i][0 .. part_words), cut to W words
+ * (parts * part_words >= W); bits above N are cleared.  The rows' derived copies
+ * (example-projected and per-direction U rows) are rebuilt too.  Asynchronous on
+ * `stream`.  This is the one call that mutates a KB: no evaluation on the KB may run
+ * concurrently, and later evaluations on other streams must be ordered after it.
+ * Errors: INVALID_ARG, OUT_OF_RANGE (first + n > n_concepts), CUDA. */
+hedl_status hedl_kb_set_concept_rows(hedl_kb *kb, uint32_t first, uint32_t n, const uint32_t *src, uint32_t parts,
+                                     uint32_t part_words, void *stream);
+
 /* ---------------------------------------------------------------------------
  * Hypotheses (§IV: "a series of (potentially) nested DL
  * operations", stored contiguously; an "evaluation plan ... determines the

@@ -33,7 +33,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "OUT_OF_RANGE", 3: "EXAMPLE_CONFLICT", 4
 ABI_SYMBOLS = ["hedl_kb_load", "hedl_kb_free", "hedl_kb_get_info", "hedl_compile", "hedl_compile_ex",
                "hedl_compile_device", "hedl_compile_text", "hedl_score_topk",
                "hedl_program_free", "hedl_set_allocator", "hedl_alloc_counters",
-               "hedl_program_workspace_bytes", "hedl_program_set_workspace",
+               "hedl_program_workspace_bytes", "hedl_program_set_workspace", "hedl_kb_set_concept_rows",
                "hedl_program_get_info", "hedl_program_root_bytes", "hedl_eval_one", "hedl_eval_batch",
                "hedl_program_set_workspace_limit", "hedl_last_error", "hedl_version", "hedl_prof_enable",
                "hedl_prof_reset", "hedl_prof_read", "hedl_launch_count", "hedl_io_counters"]
@@ -117,7 +117,7 @@ def use_torch_allocator(on: bool = True):
     """Route the library's device allocations through torch's caching allocator (the default
     once the library is loaded) or back to cudaMalloc / cudaFree.  Only while no KB is alive."""
     if on:
-        _check(lib().hedl_set_allocator(_CALLBACKS[0], _CALLBACKS[1], None))
+        _check(lib().hedl_set_allocator(C.cast(_CALLBACKS[0], C.c_void_p), C.cast(_CALLBACKS[1], C.c_void_p), None))
     else:
         _check(lib().hedl_set_allocator(None, None, None))
 
@@ -159,10 +159,11 @@ def lib():
         "hedl_prof_read": ([C.POINTER(_ProfEntry), C.c_int], C.c_int),
         "hedl_launch_count": ([], U64),
         "hedl_io_counters": ([C.POINTER(U64), C.POINTER(U64)], I32),
-        "hedl_set_allocator": ([_ALLOC_FN, _FREE_FN, P], I32),
+        "hedl_set_allocator": ([P, P, P], I32),
         "hedl_alloc_counters": ([C.POINTER(U64), C.POINTER(U64)], I32),
         "hedl_program_workspace_bytes": ([P, P, U32, U32, C.c_int, U32, C.POINTER(U64)], I32),
         "hedl_program_set_workspace": ([P, P, U64], I32),
+        "hedl_kb_set_concept_rows": ([P, U32, U32, P, U32, U32, P], I32),
         "hedl_compile_text": ([P, C.POINTER(_Names), P, U32, U32, C.POINTER(P), C.POINTER(U32), C.POINTER(U32)], I32),
     }
     for name, (args, res) in sig.items():
@@ -171,7 +172,7 @@ def lib():
         f.restype = res
     _lib = L
     if os.environ.get("HEDL_ALLOCATOR", "torch") == "torch":
-        _check(L.hedl_set_allocator(_CALLBACKS[0], _CALLBACKS[1], None))
+        _check(L.hedl_set_allocator(C.cast(_CALLBACKS[0], C.c_void_p), C.cast(_CALLBACKS[1], C.c_void_p), None))
     return L
 
 
@@ -198,6 +199,7 @@ class KB:
 
     def __init__(self, handle, device: int, n: int):
         self._h = handle
+        self._pid = os.getpid()          # a forked child (e.g. a generator pool) never frees it
         self.device = device
         self.N = n
         self.W = (n + 31) // 32
@@ -211,9 +213,20 @@ class KB:
                 "device_bytes": inf.device_bytes, "edges": list(inf.edges[:2 * R]),
                 "heavy": list(inf.heavy[:2 * R])}
 
+    def set_concept_rows(self, first: int, rows, parts: int = 1, part_words: Optional[int] = None, stream=None):
+        """hedl_kb_set_concept_rows: rows = CUDA int32/uint32 tensor [parts][n][part_words] (or
+        [n][W] with parts = 1) holding the complete rows of concepts first .. first+n-1."""
+        import torch
+        assert rows.is_cuda and rows.is_contiguous() and rows.element_size() == 4
+        pw = part_words if part_words is not None else rows.shape[-1]
+        n = rows.numel() // (parts * pw) if pw else 0
+        with torch.cuda.device(self.device):
+            _check(lib().hedl_kb_set_concept_rows(self._h, first, n, C.c_void_p(rows.data_ptr()), parts, pw,
+                                                  _stream(stream)))
+
     def free(self):
         """Release this handle (programs compiled against it keep the KB alive until freed)."""
-        if self._h and not getattr(self, "_released", False):
+        if self._h and not getattr(self, "_released", False) and getattr(self, "_pid", None) == os.getpid():
             lib().hedl_kb_free(self._h)
             self._released = True
 
@@ -229,6 +242,7 @@ class Program:
 
     def __init__(self, handle, kb: KB, n_roots: int):
         self._h = handle
+        self._pid = os.getpid()
         self.kb = kb
         self.n_roots = n_roots
 
@@ -266,9 +280,9 @@ class Program:
                                                     buf.numel() * buf.element_size()))
 
     def free(self):
-        if self._h:
+        if self._h and getattr(self, "_pid", None) == os.getpid():
             lib().hedl_program_free(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         try:

@@ -83,9 +83,9 @@ __global__ void k_cover_init(hedl_counts *c, uint32_t n, uint64_t npos, uint64_t
 // staged in shared memory once, so the operand loop has no dependent global load.
 constexpr int kBoolU = 8;
 constexpr uint32_t kBoolSmemOps = 64;
-// FULL: rows over all N individuals (else projected / U rows): the same code, instantiated twice
-// so profiles (ncu kernel names) tell the HBM-sized launches from the L2-sized ones
-template <bool FULL>
+// FULL_ROWS: rows over all N individuals (else projected / U rows): the same code, instantiated
+// twice so profiles (ncu kernel names) tell the HBM-sized launches from the L2-sized ones
+template <bool FULL_ROWS>
 __global__ void __launch_bounds__(256) k_bool(KbDev kb, const BoolDesc *__restrict__ descs,
                                               const Operand *__restrict__ ops, hedl_counts *counts) {
     const BoolDesc d = descs[blockIdx.y];
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(256) k_bool(KbDev kb, const BoolDesc *__restri
 // (the node is never split across warps, so no atomics).
 constexpr uint32_t kBoolWarpMaxN4 = 1024;     // rows up to 4,096 words
 
-template <bool FULL>
+template <bool FULL_ROWS>
 __global__ void __launch_bounds__(256) k_bool_warp(KbDev kb, const BoolDesc *__restrict__ descs, uint32_t n_desc,
                                                    const Operand *__restrict__ ops, hedl_counts *counts,
                                                    uint64_t npos, uint64_t nneg) {
