@@ -255,6 +255,7 @@ __global__ void k_dp_fill(FillArgs a) {
         d.sat = n.sat;
         d.cover = cover;
         d.heavy_slot = a.rank_of[k] * a.n_heavy[n.dir & 63];
+        d.op_first = d.op_n = 0;
         a.rd[pos - a.nb] = d;
     } else {
         DrangeDesc d;

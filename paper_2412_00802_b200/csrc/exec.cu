@@ -326,6 +326,9 @@ struct ChunkTmp {            // per-chunk planning state kept between the sizing
     std::vector<uint32_t> slot, pslot, cover_of_root, members, gdesc, opbase;
     std::vector<int32_t> cover_of_node;
     std::vector<uint8_t> need_full, need_proj, pmode;
+    // boolean fillers fused into the packs: a full row only lane packs
+    // read is never materialised; the pack kernel combines the node's operand rows itself
+    std::vector<uint8_t> by_pack, by_other, fused;
     std::vector<uint64_t> need_u;      // directions whose U rows of the node are read
     std::vector<uint64_t> u_out;       // directions whose U rows the node (a boolean) computes
     std::vector<uint32_t> ubase;       // first U-row slot of the node
@@ -374,12 +377,18 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
         need_full.assign(nn, 0);
         need_proj.assign(nn, 0);
         pmode.assign(nn, 0);
+        auto &by_pack = tmp.by_pack;
+        auto &by_other = tmp.by_other;
+        auto &fused = tmp.fused;
+        by_pack.assign(nn, 0);
+        by_other.assign(nn, 0);
+        fused.assign(nn, 0);
         auto &need_u = tmp.need_u;
         auto &u_out = tmp.u_out;
         need_u.assign(nn, 0);
         u_out.assign(nn, 0);
         if (out_bits)
-            for (uint32_t k = 0; k < nroots; ++k) need_full[local[p->root_node[cp.ri + k]]] = 1;
+            for (uint32_t k = 0; k < nroots; ++k) need_full[local[p->root_node[cp.ri + k]]] = by_other[local[p->root_node[cp.ri + k]]] = 1;
         // U rows: an EX-pack restriction in direction d reads its
         // filler only at U_d (the example rows' neighbours).  A boolean over atoms / TOP /
         // such booleans ("U-capable") demanded over U_d is evaluated over U_d (a row of |U_d|
@@ -411,6 +420,16 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
             const uint32_t lvl = p->nodes[list[hi - 1]].level;
             uint32_t lo = hi - 1;
             while (lo > 0 && p->nodes[list[lo - 1]].level == lvl) --lo;
+            // this level's demands are final: restrictions an EX pack reads as full-row fillers
+            // are needed in full; then which (level, direction) groups run as full lane packs
+            // (the same rule the grouping below applies), so their fillers' demand is a pack's
+            uint32_t nfull_dir[64] = {0};
+            for (uint32_t kk = lo; kk < hi; ++kk) {
+                const CNode &n = p->nodes[list[kk]];
+                if (n.kind != NK_RESTRICT) continue;
+                if (need_u[kk]) need_full[kk] = 1;
+                if (need_full[kk] && slice_class(n.pred, n.n, n.sat) < 2) nfull_dir[n.dir & 63]++;
+            }
             par_for(hi - lo, 1 << 13, [&](size_t a, size_t b) {
                 for (size_t kk = lo + a; kk < lo + b; ++kk) {
                     const CNode &n = p->nodes[list[kk]];
@@ -419,12 +438,20 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                     uint64_t uo = 0;
                     if (nu) {
                         if (ucap[kk]) uo = nu;
-                        else need_full[kk] = 1;                 // the packs read its full row
+                        else need_full[kk] = by_pack[kk] = 1;   // the EX packs read its full row
                     }
                     u_out[kk] = uo;
                     pmode[kk] = isbool && !need_full[kk] && (need_proj[kk] || cover_of_node[kk] >= 0);
                     const bool ex = use_u && n.kind == NK_RESTRICT && !need_full[kk] &&
                                     slice_class(n.pred, n.n, n.sat) < 2;
+                    // a full-row restriction that runs in a lane pack (else: the per-node kernel)
+                    const bool packed = n.kind == NK_RESTRICT && need_full[kk] && use_slice &&
+                                        slice_class(n.pred, n.n, n.sat) < 2 &&
+                                        slice_worthwhile(kb, nfull_dir[n.dir & 63], force_slice);
+                    // a boolean only lane packs read in full: fused into those packs, no row
+                    const bool fuse = isbool && need_full[kk] && by_pack[kk] && !by_other[kk] && !need_proj[kk] &&
+                                      cover_of_node[kk] < 0 && n.op_count >= 1 && n.op_count <= kFuseMaxOps;
+                    fused[kk] = fuse;
                     for (uint32_t q = 0; q < n.op_count; ++q) {
                         const uint32_t o = p->ops[n.op_begin + q];
                         if (ref_type(o) != RT_NODE) continue;
@@ -433,8 +460,10 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                             __atomic_fetch_or(&need_u[lo2], 1ull << n.dir, __ATOMIC_RELAXED);
                         } else if (!isbool) {
                             need_full[lo2] = 1;
+                            if (packed) by_pack[lo2] = 1;
+                            else by_other[lo2] = 1;
                         } else {
-                            if (need_full[kk]) need_full[lo2] = 1;
+                            if (need_full[kk]) need_full[lo2] = by_other[lo2] = 1;
                             if (pmode[kk]) need_proj[lo2] = 1;
                             if (uo) __atomic_fetch_or(&need_u[lo2], uo, __ATOMIC_RELAXED);
                         }
@@ -443,6 +472,11 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
             });
             hi = lo;
         }
+        // fused booleans have no row of their own (their operands' rows were demanded above)
+        par_for(nn, 1 << 15, [&](size_t a, size_t b) {
+            for (size_t k = a; k < b; ++k)
+                if (fused[k]) need_full[k] = 0;
+        });
         const double ts1 = now_ms();
         slot.assign(nn, 0);
         pslot.assign(nn, 0);
@@ -562,6 +596,13 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                 tmp.gdesc[gi] = (uint32_t)n_res;
                 n_res += g.count;
                 if (!g.slice) *heavy_need = std::max(*heavy_need, (size_t)g.count * kb->dirs[g.key].n_heavy * 8);
+                if (g.slice && !g.ucomp)            // fused fillers: their operands, read by the pack
+                    for (uint32_t m = g.first; m < g.first + g.count; ++m) {
+                        const uint32_t c = p->ops[p->nodes[list[members[m]]].op_begin];
+                        if (ref_type(c) != RT_NODE || !tmp.fused[local[ref_id(c)]]) continue;
+                        tmp.opbase[m] = (uint32_t)n_ops;
+                        n_ops += p->nodes[ref_id(c)].op_count;
+                    }
             } else if (g.kind == NK_STRING) {
                 tmp.gdesc[gi] = (uint32_t)n_str;
                 n_str += g.count;
@@ -686,7 +727,22 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                     const CNode &n = p->nodes[list[k]];
                     const uint32_t c = p->ops[n.op_begin];
                     RestrictDesc rd;
-                    rd.child = g.ucomp ? uptr_of(c, g.key) : ptr_of(c);
+                    rd.op_first = rd.op_n = 0;
+                    if (!g.ucomp && ref_type(c) == RT_NODE && tmp.fused[local[ref_id(c)]]) {
+                        // fused filler: the pack combines its operand rows (k-ary AND / OR with
+                        // complement masks, Alg. 1-2) instead of reading a materialised row
+                        const CNode &f = p->nodes[ref_id(c)];
+                        uint32_t io = tmp.opbase[m];
+                        rd.child = nullptr;
+                        rd.op_first = io;
+                        rd.op_n = f.op_count | (f.kind == NK_OR ? 0x80000000u : 0u);
+                        for (uint32_t q = 0; q < f.op_count; ++q) {
+                            const uint32_t o = p->ops[f.op_begin + q];
+                            ho[io++] = Operand{ptr_of(o), ref_comp(o) ? 0xffffffffu : 0u, 0};
+                        }
+                    } else {
+                        rd.child = g.ucomp ? uptr_of(c, g.key) : ptr_of(c);
+                    }
                     rd.out = out_of(k);
                     rd.proj = proj_of(k);
                     rd.cmask = ref_comp(c) ? 0xffffffffu : 0u;
@@ -787,7 +843,8 @@ hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, u
             if (lr.slice) {
                 hedl_status st = slice_run(kb, &w->slice.p, &w->slice.bytes, s, kd, lr.key,
                                            lr.cls >= 0 ? nullptr : (const RestrictDesc *)(h + cp.off_res) + lr.first_desc,
-                                           dd_desc, lr.count, cov, lr.ex, lr.cls, lr.ucomp);
+                                           dd_desc, lr.count, cov, lr.ex, lr.cls, lr.ucomp,
+                                           (const Operand *)(d + cp.off_ops));
                 if (st) return st;
             } else {
                 DirDev dd{dr.row_ptr, dr.col, dr.heavy_x, dr.heavy_nchunks, dr.chunks, dr.n_heavy, dr.n_chunks,

@@ -296,7 +296,11 @@ struct RestrictDesc {
     uint32_t pred, n, sat;
     int32_t cover;                 // counts slot or -1
     uint32_t heavy_slot;           // scratch base index for heavy counters of this node
+    // fused filler (lane packs only; child == null): the filler is the AND (OR if bit 31 of
+    // op_n) of operands [op_first, op_first + (op_n & 0x7fffffff)) of the plan's operand table
+    uint32_t op_first, op_n;
 };
+constexpr uint32_t kFuseMaxOps = 8;   // operands of a boolean filler the pack kernel combines
 struct DrangeDesc {
     uint32_t *out;
     uint32_t *proj;

@@ -284,7 +284,8 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
 
 __global__ void __launch_bounds__(256, 4) k_slice_pack(KbDev kb, const RestrictDesc *__restrict__ d_run, uint32_t run,
                                                     uint4 *__restrict__ T_base, uint64_t t_stride,
-                                                    const uint32_t *__restrict__ umask, const uint32_t *__restrict__ ubase) {
+                                                    const uint32_t *__restrict__ umask, const uint32_t *__restrict__ ubase,
+                                                    const Operand *__restrict__ ops) {
     extern __shared__ __align__(16) uint32_t sm[];        // [256][PK_STRIDE]
     __shared__ uint32_t s_cm[256];
     __shared__ __align__(8) uint64_t mbar;
@@ -297,20 +298,58 @@ __global__ void __launch_bounds__(256, 4) k_slice_pack(KbDev kb, const RestrictD
     const uint32_t nwords = min(PK_WORDS, kb.W4 - w0);    // multiple of 4 (W4 and w0 are)
     const uint32_t seg = nwords * 4;
     const uint32_t mb = smem_u32(&mbar);
+    const uint32_t t = threadIdx.x;
+    // lane t: a materialised filler row (one TMA bulk copy of its segment) or a fused boolean
+    // filler (this thread combines the operand segments itself)
+    const uint32_t *child = t < count ? d[t].child : nullptr;
+    const bool tma = child != nullptr;
+    const uint32_t ntma = __syncthreads_count(tma);
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(seg * count) : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(seg * ntma) : "memory");
     }
-    const uint32_t t = threadIdx.x;
     s_cm[t] = t < count ? d[t].cmask : 0u;
     if (t >= count)
         for (uint32_t i = 0; i < PK_WORDS; ++i) sm[t * PK_STRIDE + i] = 0u;
     __syncthreads();                                      // barrier initialised and armed
-    if (t < count) {
-        const uint32_t *src = d[t].child + w0;
+    if (tma) {
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     ::"r"(smem_u32(sm + t * PK_STRIDE)), "l"(src), "r"(seg), "r"(mb) : "memory");
+                     ::"r"(smem_u32(sm + t * PK_STRIDE)), "l"(child + w0), "r"(seg), "r"(mb) : "memory");
+    } else if (t < count) {
+        // k-ary AND / OR with complement masks over this segment, one LOP3 per operand word as
+        // in k_bool (an AND is the complemented OR of the complements); 16 B loads
+        const uint32_t on = d[t].op_n, nop = on & 0x7fffffffu, of = d[t].op_first;
+        const uint32_t flip = (on >> 31) ? 0u : FULL;
+        uint4 acc[PK_WORDS / 4];
+#pragma unroll
+        for (uint32_t q = 0; q < PK_WORDS / 4; ++q) acc[q] = make_uint4(0, 0, 0, 0);
+        for (uint32_t j = 0; j < nop; ++j) {
+            const Operand o = ops[of + j];
+            const uint4 *src = reinterpret_cast<const uint4 *>(o.ptr + w0);
+            const uint32_t m = o.mask ^ flip;
+#pragma unroll
+            for (uint32_t q = 0; q < PK_WORDS / 4; ++q) {
+                if (4 * q < nwords) {
+                    const uint4 v = __ldg(src + q);
+                    acc[q].x |= v.x ^ m; acc[q].y |= v.y ^ m; acc[q].z |= v.z ^ m; acc[q].w |= v.w ^ m;
+                }
+            }
+        }
+        // tail words (>= W) stay 0: the operands are tail-masked rows, AND of complements is not
+        const uint32_t lim = kb.W > w0 ? kb.W - w0 : 0u;
+        const uint32_t tail = (kb.N & 31) ? (1u << (kb.N & 31)) - 1u : FULL;
+#pragma unroll
+        for (uint32_t q = 0; q < PK_WORDS / 4; ++q) {
+            uint32_t v4[4] = {acc[q].x ^ flip, acc[q].y ^ flip, acc[q].z ^ flip, acc[q].w ^ flip};
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k) {
+                const uint32_t wl = 4 * q + k;
+                uint32_t v = wl < lim ? v4[k] : 0u;
+                if (wl + 1 == lim && w0 + wl + 1 == kb.W) v &= tail;
+                if (wl < nwords) sm[t * PK_STRIDE + wl] = v;
+            }
+        }
     }
     // EX packs: T only at the example rows' neighbours U, compacted (umask / ubase); the
     // masks of this warp's PK_WPW words are fetched while the bulk copies are in flight
@@ -323,6 +362,7 @@ __global__ void __launch_bounds__(256, 4) k_slice_pack(KbDev kb, const RestrictD
     }
     asm volatile("{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n @!P1 bra WAIT_%=;\n}"
                  ::"r"(mb) : "memory");
+    if (ntma < min(count, 256u)) __syncthreads();          // fused lanes' rows (generic-proxy stores) visible
     // a quad of words per step: one conflict-free 16 B shared load per row group (the 36-word
     // row stride makes 4 B column loads 4-way bank conflicted), four 32x32 transposes
     uint32_t cms[LW];
@@ -853,7 +893,7 @@ size_t slice_ws_bytes(const hedl_kb *kb) { return slice_layout(kb).need; }
 
 hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream_t s, const KbDev &kd, uint32_t dirid,
                       const RestrictDesc *h_desc, const RestrictDesc *d_desc, uint32_t n, hedl_counts *counts, bool ex,
-                      int fixed_cls, bool ucomp) {
+                      int fixed_cls, bool ucomp, const Operand *d_ops) {
     const hedl_dir &dr = kb->dirs[dirid];
     if (ex && !kb->M) return HEDL_OK;                     // no examples: nothing to evaluate
     const SliceLayout lay = slice_layout(kb);
@@ -945,15 +985,20 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             ku.W4 = dr.UW4;
             if (dr.UW4)
                 k_slice_pack<<<dim3(cdiv(dr.UW4, PK_WORDS), packs), 256, pk_smem, s>>>(ku, dd, run, sc.T, sc.t_stride,
-                                                                                     nullptr, nullptr);
+                                                                                     nullptr, nullptr, nullptr);
             count_launch();
             prof_end(s, KC_SLICE_IN, 4.0 * dr.UW * run + 32.0 * dr.n_u * packs, packs);
         } else {
             k_slice_pack<<<dim3(cdiv(kb->W4, PK_WORDS), packs), 256, pk_smem, s>>>(kd, dd, run, sc.T, sc.t_stride,
                                                                                  ex ? dr.ex_umask : nullptr,
-                                                                                 ex ? dr.ex_ubase : nullptr);
+                                                                                 ex ? dr.ex_ubase : nullptr, d_ops);
             count_launch();
-            prof_end(s, KC_SLICE_IN, 4.0 * kb->W * run + 32.0 * (ex ? (double)dr.n_u : 32.0 * kb->W4) * packs, packs);
+            // rows read: one per materialised filler, the operand rows of a fused one
+            double rows_read = run;
+            if (h_desc)
+                for (uint32_t j = 0; j < run; ++j)
+                    if (!h_desc[off + j].child) rows_read += (double)(h_desc[off + j].op_n & 0x7fffffffu) - 1.0;
+            prof_end(s, KC_SLICE_IN, 4.0 * kb->W * rows_read + 32.0 * (ex ? (double)dr.n_u : 32.0 * kb->W4) * packs, packs);
         }
         const SliceDir &hd = ex ? sdx : sd;
         if (hd.n_chunks) {

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 
 def _kb():
-    return abox.powerlaw_kb(120_000, 12, 2, 8.0, 3000, 0.7, 1.0, 0.01, seed=21)
+    return abox.powerlaw_kb(120_000, 50, 2, 8.0, 3000, 0.7, 1.0, 0.01, seed=21)
 
 
 def _trees(kb, n=40, seed=4):
