@@ -343,7 +343,7 @@ struct ChunkTmp {            // per-chunk planning state kept between the sizing
 // rows (M bits instead of N); its operands then only need projected rows, which
 // atoms/TOP have precomputed and computed nodes emit as a scatter epilogue.
 void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> &list, ChunkPlan &cp,
-                bool out_bits, bool use_slice, bool force_slice, uint32_t *rows, uint32_t *prows, uint32_t *urows,
+                bool out_bits, bool use_slice, bool force_slice, bool allow_fuse, uint32_t *rows, uint32_t *prows, uint32_t *urows,
                 std::vector<uint32_t> &local, char *h_blob, size_t *blob_cursor, size_t *heavy_need, bool sizes_only,
                 ChunkTmp &tmp) {
     const uint32_t nn = (uint32_t)list.size();
@@ -449,7 +449,7 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                                         slice_class(n.pred, n.n, n.sat) < 2 &&
                                         slice_worthwhile(kb, nfull_dir[n.dir & 63], force_slice);
                     // a boolean only lane packs read in full: fused into those packs, no row
-                    const bool fuse = isbool && need_full[kk] && by_pack[kk] && !by_other[kk] && !need_proj[kk] &&
+                    const bool fuse = allow_fuse && isbool && need_full[kk] && by_pack[kk] && !by_other[kk] && !need_proj[kk] &&
                                       cover_of_node[kk] < 0 && n.op_count >= 1 && n.op_count <= kFuseMaxOps;
                     fused[kk] = fuse;
                     for (uint32_t q = 0; q < n.op_count; ++q) {
@@ -949,7 +949,8 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
             ChunkPlan &cp = pc.chunks[c];
             cp.ri = ranges[c].first;
             cp.rc = ranges[c].second;
-            fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, nullptr, nullptr, nullptr, local, nullptr, &cursor,
+            fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, !(eflags & HEDL_EVAL_NO_FUSE), nullptr, nullptr, nullptr,
+                       local, nullptr, &cursor,
                        &heavy_need, true, tmps[c]);
             max_nn = std::max<size_t>(max_nn, cp.nrows);
             max_np = std::max<size_t>(max_np, cp.nprows);
@@ -982,7 +983,8 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
         for (size_t c = 0; c < lists.size(); ++c) {
             ChunkPlan &cp = pc.chunks[c];
             size_t cur = cp.blob_off;
-            fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, (uint32_t *)w->rows.p, (uint32_t *)w->prows.p,
+            fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, !(eflags & HEDL_EVAL_NO_FUSE), (uint32_t *)w->rows.p,
+                       (uint32_t *)w->prows.p,
                        (uint32_t *)w->urows.p, local, (char *)pc.host, &cur, &heavy_need, false, tmps[c]);
             tmps[c] = ChunkTmp();   // release the chunk's planning state
             timing_note("plan: fill chunk", now_ms() - t2);
@@ -1245,7 +1247,8 @@ extern "C" hedl_status hedl_program_workspace_bytes(const hedl_kb *kb, hedl_prog
             ChunkTmp tmp;
             cp.ri = ranges[c].first;
             cp.rc = ranges[c].second;
-            fill_chunk(kb, p, lists[c], cp, with_bits != 0, use_slice, eflags & HEDL_EVAL_FORCE_SLICE, nullptr, nullptr,
+            fill_chunk(kb, p, lists[c], cp, with_bits != 0, use_slice, eflags & HEDL_EVAL_FORCE_SLICE,
+                       !(eflags & HEDL_EVAL_NO_FUSE), nullptr, nullptr,
                        nullptr, local, nullptr, &cursor, &heavy_need, true, tmp);
             max_nn = std::max<size_t>(max_nn, cp.nrows);
             max_np = std::max<size_t>(max_np, cp.nprows);

@@ -300,7 +300,7 @@ struct RestrictDesc {
     // op_n) of operands [op_first, op_first + (op_n & 0x7fffffff)) of the plan's operand table
     uint32_t op_first, op_n;
 };
-constexpr uint32_t kFuseMaxOps = 8;   // operands of a boolean filler the pack kernel combines
+constexpr uint32_t kFuseMaxOps = 4;   // operands of a boolean filler the pack kernel combines
 struct DrangeDesc {
     uint32_t *out;
     uint32_t *proj;

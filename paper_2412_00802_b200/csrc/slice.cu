@@ -286,8 +286,9 @@ __global__ void __launch_bounds__(256, 4) k_slice_pack(KbDev kb, const RestrictD
                                                     uint4 *__restrict__ T_base, uint64_t t_stride,
                                                     const uint32_t *__restrict__ umask, const uint32_t *__restrict__ ubase,
                                                     const Operand *__restrict__ ops) {
-    extern __shared__ __align__(16) uint32_t sm[];        // [256][PK_STRIDE]
-    __shared__ uint32_t s_cm[256];
+    extern __shared__ __align__(16) uint32_t sm[];        // [256][PK_STRIDE] lane rows
+    __shared__ uint32_t s_cm[256], s_on[256];
+    __shared__ uint64_t s_optab[256 * kFuseMaxOps];       // fused lanes' operand rows | complement
     __shared__ __align__(8) uint64_t mbar;
     const uint32_t p = blockIdx.y;
     const RestrictDesc *d = d_run + 256u * p;
@@ -300,10 +301,11 @@ __global__ void __launch_bounds__(256, 4) k_slice_pack(KbDev kb, const RestrictD
     const uint32_t mb = smem_u32(&mbar);
     const uint32_t t = threadIdx.x;
     // lane t: a materialised filler row (one TMA bulk copy of its segment) or a fused boolean
-    // filler (this thread combines the operand segments itself)
+    // filler (the CTA combines the operand segments itself)
     const uint32_t *child = t < count ? d[t].child : nullptr;
     const bool tma = child != nullptr;
     const uint32_t ntma = __syncthreads_count(tma);
+    const bool any_fused = ntma < min(count, 256u);
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -312,42 +314,72 @@ __global__ void __launch_bounds__(256, 4) k_slice_pack(KbDev kb, const RestrictD
     s_cm[t] = t < count ? d[t].cmask : 0u;
     if (t >= count)
         for (uint32_t i = 0; i < PK_WORDS; ++i) sm[t * PK_STRIDE + i] = 0u;
+    if (any_fused) {
+        // lane t's operand rows (32 B aligned) with the complement flag in bit 0; all descriptor
+        // loads independent, so the combine has no dependent load per operand
+        const uint32_t on_t = (t < count && !tma) ? d[t].op_n : 0u;
+        s_on[t] = on_t;
+        if (on_t) {
+            const Operand *op = ops + d[t].op_first;
+            const uint32_t n_t = min(on_t & 0x7fffffffu, kFuseMaxOps);
+#pragma unroll
+            for (uint32_t j = 0; j < kFuseMaxOps; ++j)
+                if (j < n_t) {
+                    const Operand o = op[j];
+                    s_optab[t * kFuseMaxOps + j] = reinterpret_cast<uint64_t>(o.ptr) | (o.mask & 1u);
+                }
+        }
+    }
     __syncthreads();                                      // barrier initialised and armed
-    if (tma) {
+    if (tma)
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                      ::"r"(smem_u32(sm + t * PK_STRIDE)), "l"(child + w0), "r"(seg), "r"(mb) : "memory");
-    } else if (t < count) {
-        // k-ary AND / OR with complement masks over this segment, one LOP3 per operand word as
-        // in k_bool (an AND is the complemented OR of the complements); 16 B loads
-        const uint32_t on = d[t].op_n, nop = on & 0x7fffffffu, of = d[t].op_first;
-        const uint32_t flip = (on >> 31) ? 0u : FULL;
-        uint4 acc[PK_WORDS / 4];
-#pragma unroll
-        for (uint32_t q = 0; q < PK_WORDS / 4; ++q) acc[q] = make_uint4(0, 0, 0, 0);
-        for (uint32_t j = 0; j < nop; ++j) {
-            const Operand o = ops[of + j];
-            const uint4 *src = reinterpret_cast<const uint4 *>(o.ptr + w0);
-            const uint32_t m = o.mask ^ flip;
-#pragma unroll
-            for (uint32_t q = 0; q < PK_WORDS / 4; ++q) {
-                if (4 * q < nwords) {
-                    const uint4 v = __ldg(src + q);
-                    acc[q].x |= v.x ^ m; acc[q].y |= v.y ^ m; acc[q].z |= v.z ^ m; acc[q].w |= v.w ^ m;
-                }
-            }
-        }
-        // tail words (>= W) stay 0: the operands are tail-masked rows, AND of complements is not
-        const uint32_t lim = kb.W > w0 ? kb.W - w0 : 0u;
+    if (any_fused) {
+        // fused fillers, CTA-cooperative while the bulk copies fly: a lane's 32-word segment is 8 quads, thread t takes quad
+        // t & 7 of lanes (t >> 3) + 32 r (128 contiguous bytes per lane and operand, coalesced /
+        // conflict-free).  k-ary AND / OR with complement masks as in k_bool: an AND is the
+        // complemented OR of the complements, one LOP3 per operand word.
+        const uint32_t wq = 4 * (t & 7);
+        const uint32_t lim = kb.W > w0 ? kb.W - w0 : 0u;       // valid words of this segment
         const uint32_t tail = (kb.N & 31) ? (1u << (kb.N & 31)) - 1u : FULL;
 #pragma unroll
-        for (uint32_t q = 0; q < PK_WORDS / 4; ++q) {
-            uint32_t v4[4] = {acc[q].x ^ flip, acc[q].y ^ flip, acc[q].z ^ flip, acc[q].w ^ flip};
+        for (uint32_t half = 0; half < 2; ++half) {
+            uint32_t on[4], flip[4];
+            uint4 acc[4];
+            uint32_t jmax = 0;
 #pragma unroll
-            for (uint32_t k = 0; k < 4; ++k) {
-                const uint32_t wl = 4 * q + k;
-                uint32_t v = wl < lim ? v4[k] : 0u;
-                if (wl + 1 == lim && w0 + wl + 1 == kb.W) v &= tail;
-                if (wl < nwords) sm[t * PK_STRIDE + wl] = v;
+            for (uint32_t r = 0; r < 4; ++r) {
+                const uint32_t L = (t >> 3) + 32 * (4 * half + r);
+                on[r] = min(s_on[L] & 0x7fffffffu, kFuseMaxOps);
+                flip[r] = (s_on[L] >> 31) ? 0u : FULL;
+                acc[r] = make_uint4(0, 0, 0, 0);
+                jmax = max(jmax, on[r]);
+            }
+            if (wq >= nwords) jmax = 0;
+            for (uint32_t jo = 0; jo < jmax; ++jo) {
+#pragma unroll
+                for (uint32_t r = 0; r < 4; ++r) {
+                    if (jo < on[r]) {
+                        const uint32_t L = (t >> 3) + 32 * (4 * half + r);
+                        const uint64_t e = s_optab[L * kFuseMaxOps + jo];
+                        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(e & ~uint64_t(1)) + ((w0 + wq) >> 2));
+                        const uint32_t m = ((e & 1u) ? FULL : 0u) ^ flip[r];
+                        acc[r].x |= v.x ^ m; acc[r].y |= v.y ^ m; acc[r].z |= v.z ^ m; acc[r].w |= v.w ^ m;
+                    }
+                }
+            }
+#pragma unroll
+            for (uint32_t r = 0; r < 4; ++r) {
+                if (!on[r] || wq >= nwords) continue;
+                const uint32_t L = (t >> 3) + 32 * (4 * half + r);
+                uint32_t v4[4] = {acc[r].x ^ flip[r], acc[r].y ^ flip[r], acc[r].z ^ flip[r], acc[r].w ^ flip[r]};
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k) {       // tail bits (>= N) and padding words stay 0
+                    const uint32_t wl = wq + k;
+                    if (wl >= lim) v4[k] = 0u;
+                    else if (w0 + wl + 1 == kb.W) v4[k] &= tail;
+                }
+                *reinterpret_cast<uint4 *>(sm + L * PK_STRIDE + wq) = make_uint4(v4[0], v4[1], v4[2], v4[3]);
             }
         }
     }
@@ -362,7 +394,7 @@ __global__ void __launch_bounds__(256, 4) k_slice_pack(KbDev kb, const RestrictD
     }
     asm volatile("{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n @!P1 bra WAIT_%=;\n}"
                  ::"r"(mb) : "memory");
-    if (ntma < min(count, 256u)) __syncthreads();          // fused lanes' rows (generic-proxy stores) visible
+    if (any_fused) __syncthreads();                       // fused rows (generic-proxy stores) visible
     // a quad of words per step: one conflict-free 16 B shared load per row group (the 36-word
     // row stride makes 4 B column loads 4-way bank conflicted), four 32x32 transposes
     uint32_t cms[LW];

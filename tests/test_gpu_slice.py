@@ -14,6 +14,7 @@ from test_gpu_parity import assert_parity, gpu_eval
 pytestmark = pytest.mark.gpu
 FORCE = 4       # HEDL_EVAL_FORCE_SLICE
 PER_NODE = 2    # HEDL_EVAL_PER_NODE
+NO_FUSE = 8     # HEDL_EVAL_NO_FUSE
 
 
 def test_slice_random_tiny():
@@ -22,6 +23,8 @@ def test_slice_random_tiny():
         rng = np.random.default_rng(20_000 + seed)
         trees = [hyps.random_tree(rng, abox.kb_shape(kb), depth=4, n_max=6) for _ in range(40)]
         assert_parity(kb, trees, eflags=FORCE, tag=f"slice seed {seed}")
+        if seed % 4 == 0:               # boolean fillers materialised instead of fused into the packs
+            assert_parity(kb, trees, eflags=FORCE | NO_FUSE, tag=f"slice no-fuse {seed}")
         if seed % 10 == 0:
             assert_parity(kb, trees, flags=COMPILE_COMPAT_PAPER_MAX, eflags=FORCE, tag=f"slice compat {seed}")
 
@@ -86,6 +89,7 @@ def test_slice_c4_shape():
     kb = abox.powerlaw_kb(300_000, 50, 2, 8.0, 10_000, 0.7, 1.0, 0.01, 4)
     arrays = hyps.batch_arrays("c4", kb, 20_000, 4, chunk=5000, workers=4)
     assert_parity(kb, arrays=arrays, tag="slice c4-shape")
+    assert_parity(kb, arrays=arrays, eflags=NO_FUSE, tag="slice c4-shape, fillers materialised")
 
 
 def test_slice_tail_sizes():
