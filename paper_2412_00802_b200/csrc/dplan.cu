@@ -256,6 +256,8 @@ __global__ void k_dp_fill(FillArgs a) {
         d.cover = cover;
         d.heavy_slot = a.rank_of[k] * a.n_heavy[n.dir & 63];
         d.op_first = d.op_n = 0;
+        d.uout = nullptr;
+        d.udirs = d.pad_ = 0;
         a.rd[pos - a.nb] = d;
     } else {
         DrangeDesc d;

@@ -343,7 +343,7 @@ struct ChunkTmp {            // per-chunk planning state kept between the sizing
 // rows (M bits instead of N); its operands then only need projected rows, which
 // atoms/TOP have precomputed and computed nodes emit as a scatter epilogue.
 void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> &list, ChunkPlan &cp,
-                bool out_bits, bool use_slice, bool force_slice, bool allow_fuse, uint32_t *rows, uint32_t *prows, uint32_t *urows,
+                bool out_bits, bool use_slice, bool force_slice, bool allow_fuse, bool allow_urestr, uint32_t *rows, uint32_t *prows, uint32_t *urows,
                 std::vector<uint32_t> &local, char *h_blob, size_t *blob_cursor, size_t *heavy_need, bool sizes_only,
                 ChunkTmp &tmp) {
     const uint32_t nn = (uint32_t)list.size();
@@ -395,6 +395,9 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
         // bits), besides any full or example-projected row it is needed as; other fillers are
         // computed in full and the pack reads their full rows at U_d.
         const bool use_u = use_slice && kb->M > 0;
+        // restrictions in full lane packs emit U rows from the tile epilogue (DESIGN.md "U rows
+        // of restrictions"), so booleans over them are U-capable too
+        const bool u_restr = use_u && allow_urestr && kb->dirs.size() <= kMaxUDirs;
         std::vector<uint8_t> ucap(nn, 0);
         if (use_u)
             for (uint32_t lo = 0; lo < nn;) {                  // bottom-up, level by level
@@ -403,6 +406,10 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                 par_for(hi - lo, 1 << 13, [&](size_t a, size_t b) {
                     for (size_t kk = lo + a; kk < lo + b; ++kk) {
                         const CNode &n = p->nodes[list[kk]];
+                        if (n.kind == NK_RESTRICT) {
+                            ucap[kk] = u_restr && slice_class(n.pred, n.n, n.sat) < 2;
+                            continue;
+                        }
                         bool c = n.kind == NK_AND || n.kind == NK_OR;
                         for (uint32_t q = 0; c && q < n.op_count; ++q) {
                             const uint32_t o = p->ops[n.op_begin + q];
@@ -423,12 +430,16 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
             // this level's demands are final: restrictions an EX pack reads as full-row fillers
             // are needed in full; then which (level, direction) groups run as full lane packs
             // (the same rule the grouping below applies), so their fillers' demand is a pack's
+            // (restrictions emitting U rows run in full packs too, and force their group's packing)
             uint32_t nfull_dir[64] = {0};
+            uint64_t uforce = 0;
             for (uint32_t kk = lo; kk < hi; ++kk) {
                 const CNode &n = p->nodes[list[kk]];
                 if (n.kind != NK_RESTRICT) continue;
-                if (need_u[kk]) need_full[kk] = 1;
-                if (need_full[kk] && slice_class(n.pred, n.n, n.sat) < 2) nfull_dir[n.dir & 63]++;
+                if (need_u[kk] && !ucap[kk]) need_full[kk] = 1;
+                if ((need_full[kk] || (need_u[kk] && ucap[kk])) && slice_class(n.pred, n.n, n.sat) < 2)
+                    nfull_dir[n.dir & 63]++;
+                if (need_u[kk] && ucap[kk]) uforce |= 1ull << (n.dir & 63);
             }
             par_for(hi - lo, 1 << 13, [&](size_t a, size_t b) {
                 for (size_t kk = lo + a; kk < lo + b; ++kk) {
@@ -442,12 +453,13 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                     }
                     u_out[kk] = uo;
                     pmode[kk] = isbool && !need_full[kk] && (need_proj[kk] || cover_of_node[kk] >= 0);
-                    const bool ex = use_u && n.kind == NK_RESTRICT && !need_full[kk] &&
+                    const bool ex = use_u && n.kind == NK_RESTRICT && !need_full[kk] && !uo &&
                                     slice_class(n.pred, n.n, n.sat) < 2;
                     // a full-row restriction that runs in a lane pack (else: the per-node kernel)
-                    const bool packed = n.kind == NK_RESTRICT && need_full[kk] && use_slice &&
+                    const bool packed = n.kind == NK_RESTRICT && (need_full[kk] || uo) && use_slice &&
                                         slice_class(n.pred, n.n, n.sat) < 2 &&
-                                        slice_worthwhile(kb, nfull_dir[n.dir & 63], force_slice);
+                                        (slice_worthwhile(kb, nfull_dir[n.dir & 63], force_slice) ||
+                                         (uforce >> (n.dir & 63) & 1));
                     // a boolean only lane packs read in full: fused into those packs, no row
                     const bool fuse = allow_fuse && isbool && need_full[kk] && by_pack[kk] && !by_other[kk] && !need_proj[kk] &&
                                       cover_of_node[kk] < 0 && n.op_count >= 1 && n.op_count <= kFuseMaxOps;
@@ -488,9 +500,13 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
         auto &ubase = tmp.ubase;
         ubase.assign(nn, 0);
         uint32_t nurows = 0;
-        for (uint32_t k = 0; k < nn; ++k) {
-            ubase[k] = nurows;
-            nurows += (uint32_t)__builtin_popcountll(u_out[k]);
+        for (int pass = 0; pass < 2; ++pass) {      // restrictions' U rows first: zeroed per chunk
+            for (uint32_t k = 0; k < nn; ++k) {
+                if ((p->nodes[list[k]].kind == NK_RESTRICT) != (pass == 0)) continue;
+                ubase[k] = nurows;
+                nurows += (uint32_t)__builtin_popcountll(u_out[k]);
+            }
+            if (pass == 0) cp.nurows_r = nurows;
         }
         cp.nurows = nurows;
         // launch groups: (level, kind, dir) runs of the list; boolean runs split by full/projected
@@ -533,18 +549,20 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                 // are enough of them -- then those needed only at the examples (EX packs over U
                 // rows, always packed), then the per-node rest
                 uint32_t ns = 0, nf = 0;
+                bool any_u = false;
                 while (k + ns < e && slice_class(p->nodes[list[k + ns]].pred, p->nodes[list[k + ns]].n,
                                                  p->nodes[list[k + ns]].sat) != 2) {
-                    nf += need_full[k + ns] != 0;
+                    nf += (need_full[k + ns] || u_out[k + ns]) != 0;
+                    any_u |= u_out[k + ns] != 0;
                     ++ns;
                 }
-                const bool full_packs = nf && slice_worthwhile(kb, nf, force_slice);
+                const bool full_packs = nf && (slice_worthwhile(kb, nf, force_slice) || any_u);
                 const uint32_t first_rest = (uint32_t)members.size();
                 if (full_packs) {
                     Group g{kind, key, (uint32_t)members.size(), 0};
                     g.slice = true;
                     for (uint32_t q = k; q < k + ns; ++q)
-                        if (need_full[q]) members.push_back(q);
+                        if (need_full[q] || u_out[q]) members.push_back(q);
                     g.count = (uint32_t)members.size() - g.first;
                     groups.push_back(g);
                 }
@@ -554,13 +572,13 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                     const uint32_t c = p->ops[p->nodes[list[q]].op_begin];
                     return use_u && (ref_type(c) != RT_NODE || (u_out[local[ref_id(c)]] >> key & 1));
                 };
-                for (int uc = 1; uc >= 0 && ns > nf; --uc) {
+                for (int uc = 1; uc >= 0 && ns > nf; --uc) {      // (nf counts the full-pack members)
                     Group g{kind, key, (uint32_t)members.size(), 0};
                     g.slice = true;
                     g.ex = true;
                     g.ucomp = uc;
                     for (uint32_t q = k; q < k + ns; ++q)
-                        if (!need_full[q] && u_filler(q) == (bool)uc) members.push_back(q);
+                        if (!need_full[q] && !u_out[q] && u_filler(q) == (bool)uc) members.push_back(q);
                     g.count = (uint32_t)members.size() - g.first;
                     if (g.count) groups.push_back(g);
                 }
@@ -728,6 +746,12 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                     const uint32_t c = p->ops[n.op_begin];
                     RestrictDesc rd;
                     rd.op_first = rd.op_n = 0;
+                    rd.uout = nullptr;
+                    rd.udirs = rd.pad_ = 0;
+                    if (u_out[k]) {                          // full pack: U rows from the epilogue
+                        rd.uout = urow_of(k, __builtin_ctzll(u_out[k]));
+                        rd.udirs = (uint32_t)u_out[k];
+                    }
                     if (!g.ucomp && ref_type(c) == RT_NODE && tmp.fused[local[ref_id(c)]]) {
                         // fused filler: the pack combines its operand rows (k-ary AND / OR with
                         // complement masks, Alg. 1-2) instead of reading a materialised row
@@ -827,6 +851,11 @@ hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, u
     launch_cover_init(s, cov, cp.ncov, kb->npos, kb->nneg);
     if (cp.nprows && kb->MW4)
         HEDL_CUDA(kb, cudaMemsetAsync(w->prows.p, 0, (size_t)cp.nprows * kb->MW4 * 4, s));   // scatter targets
+    if (cp.nurows_r) {                                  // restrictions' U rows: atomicOr targets too
+        uint32_t uw4max = 0;
+        for (const hedl_dir &x : kb->dirs) uw4max = std::max(uw4max, x.UW4);
+        HEDL_CUDA(kb, cudaMemsetAsync(w->urows.p, 0, (size_t)cp.nurows_r * uw4max * 4, s));
+    }
     for (const LaunchRec &lr : cp.recs) {
         if (lr.kind == NK_AND) {
             KbDev kx = lr.proj ? kp : kd;
@@ -949,7 +978,8 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
             ChunkPlan &cp = pc.chunks[c];
             cp.ri = ranges[c].first;
             cp.rc = ranges[c].second;
-            fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, !(eflags & HEDL_EVAL_NO_FUSE), nullptr, nullptr, nullptr,
+            fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, !(eflags & HEDL_EVAL_NO_FUSE),
+                       !(eflags & HEDL_EVAL_NO_RESTRICT_U), nullptr, nullptr, nullptr,
                        local, nullptr, &cursor,
                        &heavy_need, true, tmps[c]);
             max_nn = std::max<size_t>(max_nn, cp.nrows);
@@ -983,7 +1013,8 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
         for (size_t c = 0; c < lists.size(); ++c) {
             ChunkPlan &cp = pc.chunks[c];
             size_t cur = cp.blob_off;
-            fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, !(eflags & HEDL_EVAL_NO_FUSE), (uint32_t *)w->rows.p,
+            fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, !(eflags & HEDL_EVAL_NO_FUSE),
+                       !(eflags & HEDL_EVAL_NO_RESTRICT_U), (uint32_t *)w->rows.p,
                        (uint32_t *)w->prows.p,
                        (uint32_t *)w->urows.p, local, (char *)pc.host, &cur, &heavy_need, false, tmps[c]);
             tmps[c] = ChunkTmp();   // release the chunk's planning state
@@ -1248,7 +1279,7 @@ extern "C" hedl_status hedl_program_workspace_bytes(const hedl_kb *kb, hedl_prog
             cp.ri = ranges[c].first;
             cp.rc = ranges[c].second;
             fill_chunk(kb, p, lists[c], cp, with_bits != 0, use_slice, eflags & HEDL_EVAL_FORCE_SLICE,
-                       !(eflags & HEDL_EVAL_NO_FUSE), nullptr, nullptr,
+                       !(eflags & HEDL_EVAL_NO_FUSE), !(eflags & HEDL_EVAL_NO_RESTRICT_U), nullptr, nullptr,
                        nullptr, local, nullptr, &cursor, &heavy_need, true, tmp);
             max_nn = std::max<size_t>(max_nn, cp.nrows);
             max_np = std::max<size_t>(max_np, cp.nprows);

@@ -27,7 +27,7 @@ struct ChunkPlan {
     uint32_t nn, ncov, nrows, nprows;
     size_t blob_off, blob_bytes;          // into PlanCache host/device blobs
     size_t off_bool, off_ops, off_res, off_dr, off_str, off_cov, off_rows;
-    uint32_t nurows = 0;
+    uint32_t nurows = 0, nurows_r = 0;   // U rows; the first nurows_r are restrictions' (zeroed per chunk)
     std::vector<LaunchRec> recs;
 };
 

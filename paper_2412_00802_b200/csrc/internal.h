@@ -299,7 +299,13 @@ struct RestrictDesc {
     // fused filler (lane packs only; child == null): the filler is the AND (OR if bit 31 of
     // op_n) of operands [op_first, op_first + (op_n & 0x7fffffff)) of the plan's operand table
     uint32_t op_first, op_n;
+    // U rows this restriction emits from its full-pack epilogue (DESIGN.md "U rows of
+    // restrictions"): direction d (bit d of udirs, d < kMaxUDirs) -> uout + rank of d in udirs
+    // x the U-row stride; zeroed before the chunk, filled with atomicOr
+    uint32_t *uout;
+    uint32_t udirs, pad_;
 };
+constexpr uint32_t kMaxUDirs = 4;     // role directions whose U rows restrictions can emit
 constexpr uint32_t kFuseMaxOps = 4;   // operands of a boolean filler the pack kernel combines
 struct DrangeDesc {
     uint32_t *out;

@@ -39,6 +39,14 @@ struct SliceDir {
     uint32_t n_heavy, n_chunks, n_tiles;
 };
 
+// per-direction U masks for the restriction U-row epilogue (directions < kMaxUDirs)
+struct UTab {
+    const uint32_t *um[kMaxUDirs], *ub[kMaxUDirs];   // ex_umask / ex_ubase of direction d
+    uint32_t nu[kMaxUDirs];                           // |U_d|
+    uint32_t stride;                                  // words between a node's consecutive U rows
+};
+
+
 struct SliceScratch {
     uint4 *T;                     // [W4*32][2] : 32 B per individual
     uint32_t *hacc;               // [n_heavy][8]     OR accumulators
@@ -90,6 +98,35 @@ __device__ __forceinline__ uint32_t warp_transpose(uint32_t x, uint32_t lane) {
     k = lo1 ? 0x55555555u : 0xAAAAAAAAu;
     x = (x & k) | (__funnelshift_l(y, y, lo1 ? 1 : 31) & ~k);
     return x;
+}
+
+// The bits of `word` selected by `m` (pext), destined for bit positions base .. of a packed
+// row (a projected or U row), gathered per destination word: one write per word touched.
+// (pw, pbits) is the caller's pending destination word; flush with pack_flush at the end.
+// Destination words in [own_lo, own_hi) receive bits from this caller only: a plain store;
+// the others (shared with a neighbouring tile) an atomicOr into the zeroed row.
+__device__ __forceinline__ void pack_flush(uint32_t *row, uint32_t pw, uint32_t pbits, uint32_t own_lo, uint32_t own_hi) {
+    if (pw >= own_lo && pw < own_hi) row[pw] = pbits;
+    else if (pbits) atomicOr(row + pw, pbits);
+}
+__device__ __forceinline__ void pack_bits(uint32_t m, uint32_t word, uint32_t base, uint32_t *row, uint32_t &pw,
+                                          uint32_t &pbits, uint32_t own_lo = 0, uint32_t own_hi = 0) {
+    if (!m || !word) return;
+    uint32_t bits = 0, nb = 0;
+    for (; m; m &= m - 1, ++nb) bits |= ((word >> (__ffs(m) - 1)) & 1u) << nb;
+    if (!bits) return;                    // (words never written stay 0: the row was zeroed)
+    const uint32_t wi = base >> 5, sh = base & 31;
+    if (wi != pw) {
+        if (pbits) pack_flush(row, pw, pbits, own_lo, own_hi);
+        pw = wi;
+        pbits = 0;
+    }
+    pbits |= bits << sh;
+    if (sh + nb > 32) {
+        pack_flush(row, pw, pbits, own_lo, own_hi);
+        pw = wi + 1;
+        pbits = bits >> (32 - sh);
+    }
 }
 
 // every thread of the CTA calls; lanes >= count get "always 0" (am = om = 0, masks 0).
@@ -569,7 +606,7 @@ __device__ __forceinline__ void scan_slice_pipelined(Acc<COUNT> &acc, const uint
 // the CTA waits on a statically unlucky share.  The counter pair `sched` is self-cleaning:
 // the last CTA to finish resets it for the next launch on the stream.
 template <bool COUNT>
-__global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, SliceScratch sc,
+__global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, SliceScratch sc, UTab ut,
                                                                    const RestrictDesc *__restrict__ d, uint32_t count,
                                                                    hedl_counts *counts, uint32_t *sched, uint32_t dbg) {
 #ifndef HEDL_DEBUG_TILE
@@ -581,15 +618,23 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, half = lane & 1;
     __shared__ uint32_t s_exm[32], s_exb[32];
     __shared__ uint32_t s_tile, s_item;
+    __shared__ uint16_t s_uix[1024];                      // the tile's members of U_d (row indices)
+    __shared__ uint32_t s_unt, s_ubl, s_udirs;
     // this lane's node for the transpose-back phase (fixed for the whole launch)
     const uint32_t jn = wid * 32 + lane;
-    uint32_t *r_out = nullptr, *r_proj = nullptr;
+    uint32_t *r_out = nullptr, *r_proj = nullptr, *r_uout = nullptr;
+    uint32_t r_udirs = 0;
     int32_t r_cover = -1;
     if (jn < count) {
         r_out = d[jn].out;
         r_proj = d[jn].proj;
         r_cover = d[jn].cover;
+        r_uout = d[jn].uout;
+        r_udirs = r_uout ? d[jn].udirs : 0u;
     }
+    if (threadIdx.x == 0) s_udirs = 0;
+    __syncthreads();
+    if (r_udirs) atomicOr(&s_udirs, r_udirs);            // directions some node of the pack emits
     build_consts(pc, d, count);                           // (contains __syncthreads)
     const bool live = jn < count;
     uint32_t tp = 0, fp = 0;
@@ -739,29 +784,9 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
                     dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
                 }
                 if (r_proj) {
+                    // example bits of word w+q -> the projected row (pext with the staged masks)
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        // example bits of word w+q -> the projected row (pext with the staged
-                        // masks), gathered per projected word: one atomicOr per word touched
-                        uint32_t m = s_exm[wl + q];
-                        const uint32_t word = o[q];
-                        if (!m || !word) continue;
-                        uint32_t bits = 0, nb = 0;
-                        for (; m; m &= m - 1, ++nb) bits |= ((word >> (__ffs(m) - 1)) & 1u) << nb;
-                        if (!bits) continue;
-                        const uint32_t base = s_exb[wl + q], wi = base >> 5, sh = base & 31;
-                        if (wi != pw) {
-                            if (pbits) atomicOr(r_proj + pw, pbits);
-                            pw = wi;
-                            pbits = 0;
-                        }
-                        pbits |= bits << sh;
-                        if (sh + nb > 32) {
-                            atomicOr(r_proj + pw, pbits);
-                            pw = wi + 1;
-                            pbits = bits >> (32 - sh);
-                        }
-                    }
+                    for (int q = 0; q < 8; ++q) pack_bits(s_exm[wl + q], o[q], s_exb[wl + q], r_proj, pw, pbits);
                 }
                 if (r_cover >= 0) {
                     const uint4 *pp = reinterpret_cast<const uint4 *>(kb.pos + w);
@@ -777,6 +802,49 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
             }
         }
         if (pbits) atomicOr(r_proj + pw, pbits);
+        // U rows: for each direction d some node of the pack
+        // emits, the tile's members of U_d (the example rows' neighbours in direction d) are
+        // consecutive U positions [bl, bl + k); 32 of them at a time, their result rows (ot) go
+        // through one more warp transpose, and lane j of warp g holds node 32g + j's U word.
+        // Interior U words are written whole, the two seam words shared with the neighbouring
+        // tiles by atomicOr into the zeroed row.
+#pragma unroll
+        for (uint32_t dd = 0; dd < kMaxUDirs; ++dd) {
+            if (!((s_udirs >> dd) & 1u)) continue;                        // block-uniform
+            if (wid == 0) {                                               // member list of the tile
+                const uint32_t w = t * 32 + lane;
+                const uint32_t m = w < kb.W4 ? __ldg(ut.um[dd] + w) : 0u;
+                const uint32_t c = __popc(m);
+                uint32_t pre = c;
+#pragma unroll
+                for (int o2 = 1; o2 < 32; o2 <<= 1) {
+                    const uint32_t v = __shfl_up_sync(FULL, pre, o2);
+                    if (lane >= (uint32_t)o2) pre += v;
+                }
+                uint32_t at = pre - c;
+                for (uint32_t mm = m; mm; mm &= mm - 1) s_uix[at++] = (uint16_t)(lane * 32 + __ffs(mm) - 1);
+                if (lane == 31) s_unt = pre;
+                if (lane == 0) s_ubl = __ldg(ut.ub[dd] + t * 32);
+            }
+            __syncthreads();
+            const uint32_t k = s_unt, bl = s_ubl;
+            if (k) {
+                const bool mine = live && ((r_udirs >> dd) & 1u);
+                uint32_t *urow = mine ? r_uout + __popc(r_udirs & ((1u << dd) - 1u)) * ut.stride : nullptr;
+                const uint32_t c0 = bl >> 5, c1 = (bl + k - 1) >> 5;
+                for (uint32_t cw = c0; cw <= c1; ++cw) {
+                    const int32_t idx = (int32_t)(cw * 32 + lane) - (int32_t)bl;
+                    const uint32_t v = (idx >= 0 && (uint32_t)idx < k) ? ot[(uint32_t)s_uix[idx] * TROW + g] : 0u;
+                    const uint32_t x = warp_transpose(v, lane);
+                    if (mine) {
+                        const bool seam = (cw == c0 && (bl & 31)) || (cw == c1 && ((bl + k) & 31));
+                        if (seam) { if (x) atomicOr(urow + cw, x); }
+                        else urow[cw] = x;
+                    }
+                }
+            }
+            __syncthreads();                                              // before the list is rebuilt
+        }
     }
     // coverage of this CTA's tiles, one atomic set per node per CTA
     if (live && r_cover >= 0 && (tp | fp)) {
@@ -1073,8 +1141,17 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
                                           occ[(unsigned)cur % kMaxDevices][1] * std::max(1, kb->sm_count)};
             uint32_t *sched = (uint32_t *)(base + need - 256);   // self-cleaning {next tile, CTAs done}
             const uint32_t grid = std::min(dr.n_tiles, resident[cls == 0 ? 0 : 1]);
-            if (cls == 0) k_slice_tile<false><<<grid, 256, smem, s>>>(kd, sd, sc, dd, run, counts, sched, dbg);
-            else k_slice_tile<true><<<grid, 256, smem, s>>>(kd, sd, sc, dd, run, counts, sched, dbg);
+            UTab ut{};
+            uint32_t uw4max = 0;
+            for (const hedl_dir &x : kb->dirs) uw4max = std::max(uw4max, x.UW4);
+            ut.stride = uw4max;
+            for (uint32_t q = 0; q < kMaxUDirs && q < kb->dirs.size(); ++q) {
+                ut.um[q] = kb->dirs[q].ex_umask;
+                ut.ub[q] = kb->dirs[q].ex_ubase;
+                ut.nu[q] = kb->dirs[q].n_u;
+            }
+            if (cls == 0) k_slice_tile<false><<<grid, 256, smem, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
+            else k_slice_tile<true><<<grid, 256, smem, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
             count_launch();
             // minimal DRAM bytes of one lane-packed pass: CSR once + T once (32 B per individual)
             // + the output rows; the 32 B-per-edge T gathers are L2 traffic (DESIGN.md K-SLICE)

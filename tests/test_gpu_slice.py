@@ -15,6 +15,7 @@ pytestmark = pytest.mark.gpu
 FORCE = 4       # HEDL_EVAL_FORCE_SLICE
 PER_NODE = 2    # HEDL_EVAL_PER_NODE
 NO_FUSE = 8     # HEDL_EVAL_NO_FUSE
+NO_RESTRICT_U = 16  # HEDL_EVAL_NO_RESTRICT_U
 
 
 def test_slice_random_tiny():
@@ -25,6 +26,8 @@ def test_slice_random_tiny():
         assert_parity(kb, trees, eflags=FORCE, tag=f"slice seed {seed}")
         if seed % 4 == 0:               # boolean fillers materialised instead of fused into the packs
             assert_parity(kb, trees, eflags=FORCE | NO_FUSE, tag=f"slice no-fuse {seed}")
+        if seed % 4 == 1:               # no U rows from restrictions: booleans over them in full
+            assert_parity(kb, trees, eflags=FORCE | NO_RESTRICT_U, tag=f"slice no-restrict-U {seed}")
         if seed % 10 == 0:
             assert_parity(kb, trees, flags=COMPILE_COMPAT_PAPER_MAX, eflags=FORCE, tag=f"slice compat {seed}")
 
@@ -90,6 +93,7 @@ def test_slice_c4_shape():
     arrays = hyps.batch_arrays("c4", kb, 20_000, 4, chunk=5000, workers=4)
     assert_parity(kb, arrays=arrays, tag="slice c4-shape")
     assert_parity(kb, arrays=arrays, eflags=NO_FUSE, tag="slice c4-shape, fillers materialised")
+    assert_parity(kb, arrays=arrays, eflags=NO_FUSE | NO_RESTRICT_U, tag="slice c4-shape, round-1 planner")
 
 
 def test_slice_tail_sizes():
