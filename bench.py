@@ -62,6 +62,7 @@ def parse():
     ap.add_argument("--no-c5", action="store_true", help="skip the G=1 C5 leg of the default C4 run")
     ap.add_argument("--no-prof-pass", action="store_true", help="skip the profiled pass (per-class kernel times)")
     ap.add_argument("--per-node", action="store_true", help="disable the lane-packed restriction path")
+    ap.add_argument("--eval-flags", type=int, default=0, help="extra HEDL_EVAL_* flags (A/B experiments)")
     ap.add_argument("--cache", default=os.environ.get("HEDL_CACHE", "/tmp/hedl_cache"))
     ap.add_argument("--dry-run", action="store_true",
                     help="multi-rank plumbing only (gloo, no GPU): per-rank inputs, shard ranges, count gather")
@@ -337,7 +338,7 @@ def run_workload(kind, args, hedl, rank, world, local, steps, warmup, cpu_budget
     prog = hedl.hedl_compile(kb, nodes, kids, roots)
     compile_s = time.perf_counter() - t0
     pinfo = prog.info()
-    eflags = hedl.HEDL_EVAL_PER_NODE if args.per_node else 0
+    eflags = (hedl.HEDL_EVAL_PER_NODE if args.per_node else 0) | args.eval_flags
     counts_dev = torch.empty((max(n_loc, 1), 4), dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()

@@ -410,6 +410,10 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                             ucap[kk] = u_restr && slice_class(n.pred, n.n, n.sat) < 2;
                             continue;
                         }
+                        if (n.kind == NK_DRANGE) {           // ranges are evaluated at U members directly
+                            ucap[kk] = use_u && allow_urestr;
+                            continue;
+                        }
                         bool c = n.kind == NK_AND || n.kind == NK_OR;
                         for (uint32_t q = 0; c && q < n.op_count; ++q) {
                             const uint32_t o = p->ops[n.op_begin + q];
@@ -590,6 +594,24 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                 for (uint32_t q = k + ns; q < e; ++q) members.push_back(q);
                 g.count = (uint32_t)members.size() - g.first;
                 if (g.count) groups.push_back(g);
+            } else if (kind == NK_DRANGE) {
+                // ranges needed in full / projected / as roots, then one group per U direction
+                Group g{kind, key, (uint32_t)members.size(), 0};
+                for (uint32_t q = k; q < e; ++q)
+                    if (need_full[q] || need_proj[q] || cover_of_node[q] >= 0 || !u_out[q]) members.push_back(q);
+                g.count = (uint32_t)members.size() - g.first;
+                if (g.count) groups.push_back(g);
+                uint64_t dirs_u = 0;
+                for (uint32_t q = k; q < e; ++q) dirs_u |= u_out[q];
+                for (; dirs_u; dirs_u &= dirs_u - 1) {
+                    const int d = __builtin_ctzll(dirs_u);
+                    Group gu{kind, key, (uint32_t)members.size(), 0};
+                    gu.usp = (int16_t)d;
+                    for (uint32_t q = k; q < e; ++q)
+                        if (u_out[q] >> d & 1) members.push_back(q);
+                    gu.count = (uint32_t)members.size() - gu.first;
+                    groups.push_back(gu);
+                }
             } else {
                 const uint32_t first = (uint32_t)members.size();
                 for (uint32_t q = k; q < e; ++q) members.push_back(q);
@@ -641,6 +663,34 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
         *blob_cursor += cp.blob_bytes;
         timing_note("plan: covers+demands", ts1 - ts0);
         timing_note("plan: slots+groups", now_ms() - ts1);
+        if (timing_enabled()) {            // plan statistics (HEDL_TIMING=1): lanes per pack kind
+            uint64_t full_rows = 0, full_u_only = 0, full_any = 0, ex_u = 0, ex_full = 0, per_node = 0, fused_n = 0;
+            uint64_t bool_full = 0, bool_proj = 0, bool_u = 0, restr_fillers_full = 0;
+            for (const Group &g : groups)
+                for (uint32_t m = g.first; m < g.first + g.count; ++m) {
+                    const uint32_t q = members[m];
+                    if (g.kind == NK_RESTRICT) {
+                        if (g.slice && !g.ex) {
+                            ++full_any;
+                            if (need_full[q]) ++full_rows; else ++full_u_only;
+                        } else if (g.ex) { if (g.ucomp) ++ex_u; else ++ex_full; }
+                        else ++per_node;
+                    } else if (g.kind == NK_AND) {
+                        if (g.usp >= 0) ++bool_u; else if (g.proj) ++bool_proj; else ++bool_full;
+                    }
+                }
+            for (uint32_t k = 0; k < nn; ++k) {
+                fused_n += tmp.fused[k];
+                if (p->nodes[list[k]].kind == NK_RESTRICT && tmp.by_pack[k] && need_full[k]) ++restr_fillers_full;
+            }
+            std::fprintf(stderr, "[hedl plan] restrict: full-pack %llu (full row %llu, U rows only %llu), EX over U %llu, "
+                                 "EX over full rows %llu, per-node %llu; bool: full %llu, projected %llu, U %llu, fused %llu; "
+                                 "restrictions read in full by packs %llu\n",
+                         (unsigned long long)full_any, (unsigned long long)full_rows, (unsigned long long)full_u_only,
+                         (unsigned long long)ex_u, (unsigned long long)ex_full, (unsigned long long)per_node,
+                         (unsigned long long)bool_full, (unsigned long long)bool_proj, (unsigned long long)bool_u,
+                         (unsigned long long)fused_n, (unsigned long long)restr_fillers_full);
+        }
         return;
     }
 
@@ -804,14 +854,22 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                     const uint32_t k = members[m];
                     const CNode &n = p->nodes[list[k]];
                     DrangeDesc dd;
-                    dd.out = out_of(k);
-                    dd.proj = proj_of(k);
                     dd.lo = n.lo;
                     dd.hi = n.hi;
-                    dd.cover = cover_of_node[k];
                     dd.prop = n.dir;
+                    if (g.usp >= 0) {                    // evaluated at the members of U_usp
+                        const hedl_dir &du = kb->dirs[g.usp];
+                        dd.out = urow_of(k, g.usp);
+                        dd.proj = nullptr;
+                        dd.cover = -1;
+                        T.bytes += 4.0 * du.n_u * 3 + 4.0 * du.UW;   // U list + two row pointers + values, U row
+                    } else {
+                        dd.out = out_of(k);
+                        dd.proj = proj_of(k);
+                        dd.cover = cover_of_node[k];
+                        T.bytes += kb->data_bytes[n.dir] + 4.0 * kb->W * ((dd.out ? 1 : 0) + (dd.cover >= 0 ? 2 : 0));
+                    }
                     hd[base + (m - g.first)] = dd;
-                    T.bytes += kb->data_bytes[n.dir] + 4.0 * kb->W * ((dd.out ? 1 : 0) + (dd.cover >= 0 ? 2 : 0));
                 }
             }
         }
@@ -886,8 +944,15 @@ hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, u
                           (const StringDesc *)(d + cp.off_str) + lr.first_desc, lr.count, cov, lr.bytes);
         } else {
             const hedl_data &dp = kb->data[lr.key];
-            launch_drange(s, kd, dp.row_ptr, dp.val, (const DrangeDesc *)(d + cp.off_dr) + lr.first_desc, lr.count, cov,
-                          lr.bytes);
+            if (lr.usp >= 0) {
+                const hedl_dir &du = kb->dirs[lr.usp];
+                const KbDev ku{du.n_u, du.UW, du.UW4, nullptr, nullptr, nullptr, nullptr};
+                launch_drange(s, ku, dp.row_ptr, dp.val, (const DrangeDesc *)(d + cp.off_dr) + lr.first_desc, lr.count,
+                              cov, lr.bytes, du.ulist);
+            } else {
+                launch_drange(s, kd, dp.row_ptr, dp.val, (const DrangeDesc *)(d + cp.off_dr) + lr.first_desc, lr.count,
+                              cov, lr.bytes);
+            }
         }
     }
     launch_gather_counts(s, cov, (const uint32_t *)(d + cp.off_cov), counts_dev + (cp.ri - r0), nroots);

@@ -116,6 +116,7 @@ struct hedl_dir {                  // one role direction
     uint32_t UW = 0, UW4 = 0;
     uint32_t *uconcepts = nullptr;     // device [C][UW4]
     uint32_t *uones = nullptr;         // device [UW4], tail-masked TOP row over U
+    uint32_t *ulist = nullptr;         // device [n_u]: the members of U in order (U position -> individual)
 };
 
 struct hedl_data {
@@ -366,8 +367,10 @@ void launch_bool(cudaStream_t s, const KbDev &kb, const BoolDesc *d_desc, uint32
 void launch_restrict(cudaStream_t s, const KbDev &kb, const DirDev &dir, const RestrictDesc *d_desc,
                      uint32_t n_desc, hedl_counts *counts, uint32_t *heavy_scratch, double alg_light,
                      double alg_heavy);
+// xmap != null: U space of a direction (kb = {|U|, UW, UW4}); position p is individual xmap[p]
 void launch_drange(cudaStream_t s, const KbDev &kb, const uint32_t *row_ptr, const float *val,
-                   const DrangeDesc *d_desc, uint32_t n_desc, hedl_counts *counts, double alg_bytes);
+                   const DrangeDesc *d_desc, uint32_t n_desc, hedl_counts *counts, double alg_bytes,
+                   const uint32_t *xmap = nullptr);
 void launch_string(cudaStream_t s, const KbDev &kb, const StrDev &sd, const StringDesc *d_desc, uint32_t n_desc,
                    hedl_counts *counts, double alg_bytes);
 void launch_gather_counts(cudaStream_t s, const hedl_counts *slots, const uint32_t *slot_of,

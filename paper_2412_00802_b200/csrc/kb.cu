@@ -460,6 +460,7 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
                     }
                     if ((s = upload(kb, st, &dr.uconcepts, uc.data(), uc.size()))) return bail(s);
                     if ((s = upload(kb, st, &dr.uones, uon.data(), uon.size()))) return bail(s);
+                    if ((s = upload(kb, st, &dr.ulist, ul.data(), ul.size()))) return bail(s);
                     if (cudaStreamSynchronize(st) != cudaSuccess) return bail(fail(HEDL_ERR_CUDA, "upload failed"));
                 }
                 if ((s = upload(kb, st, &dr.ex_rp, erp.data(), erp.size()))) return bail(s);

@@ -382,18 +382,22 @@ __global__ void __launch_bounds__(256) k_restrict_heavy(KbDev kb, DirDev dir, co
 // probes are issued together (4 independent loads in flight per lane instead of 1)
 constexpr uint32_t kDrWords = 4;
 
+// UMAP: evaluated over the U space of one direction: position p of the
+// output row is the individual xmap[p]; no projection / coverage there
+template <bool UMAP>
 __global__ void __launch_bounds__(256) k_drange(KbDev kb, const uint32_t *__restrict__ row_ptr,
                                                 const float *__restrict__ val, const DrangeDesc *__restrict__ descs,
-                                                hedl_counts *counts) {
+                                                hedl_counts *counts, const uint32_t *__restrict__ xmap) {
     const DrangeDesc d = descs[blockIdx.y];
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t w0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * kDrWords;
     uint32_t lo[kDrWords], hi[kDrWords], end[kDrWords];
 #pragma unroll
     for (uint32_t u = 0; u < kDrWords; ++u) {
-        const uint32_t x = ((w0 + u) << 5) + lane;
+        const uint32_t pos = ((w0 + u) << 5) + lane;
         lo[u] = hi[u] = end[u] = 0;
-        if (w0 + u < kb.W && x < kb.N) {
+        if (w0 + u < kb.W && pos < kb.N) {
+            const uint32_t x = UMAP ? __ldg(xmap + pos) : pos;
             lo[u] = __ldg(row_ptr + x);
             hi[u] = end[u] = __ldg(row_ptr + x + 1);
         }
@@ -417,15 +421,15 @@ __global__ void __launch_bounds__(256) k_drange(KbDev kb, const uint32_t *__rest
         const bool res = lo[u] < end[u] && __ldg(val + lo[u]) <= d.hi;
         const uint32_t word = __ballot_sync(FULL, res);
         if (lane == 0 && w < kb.W4) {
-            if (d.proj && w < kb.W) proj_scatter(kb, d.proj, w, word);
+            if (!UMAP && d.proj && w < kb.W) proj_scatter(kb, d.proj, w, word);
             if (d.out) d.out[w] = word;
-            if (d.cover >= 0 && w < kb.W) {
+            if (!UMAP && d.cover >= 0 && w < kb.W) {
                 tp += __popc(word & __ldg(kb.pos + w));
                 fp += __popc(word & __ldg(kb.neg + w));
             }
         }
     }
-    if (d.cover >= 0) block_cover(counts, d.cover, tp, fp);
+    if (!UMAP && d.cover >= 0) block_cover(counts, d.cover, tp, fp);
 }
 
 // ------------------------------------------------------------------------------
@@ -601,13 +605,15 @@ void launch_restrict(cudaStream_t s, const KbDev &kb, const DirDev &dir, const R
 }
 
 void launch_drange(cudaStream_t s, const KbDev &kb, const uint32_t *row_ptr, const float *val,
-                   const DrangeDesc *d_desc, uint32_t n_desc, hedl_counts *counts, double alg_bytes) {
+                   const DrangeDesc *d_desc, uint32_t n_desc, hedl_counts *counts, double alg_bytes,
+                   const uint32_t *xmap) {
     const uint32_t gx = cdiv(kb.W4, 8 * kDrWords);
     if (!gx) return;
     for (uint32_t off = 0; off < n_desc; off += 65535) {
         const uint32_t nd = n_desc - off < 65535 ? n_desc - off : 65535;
         prof_begin(s, KC_DRANGE);
-        k_drange<<<dim3(gx, nd), 256, 0, s>>>(kb, row_ptr, val, d_desc + off, counts);
+        if (xmap) k_drange<true><<<dim3(gx, nd), 256, 0, s>>>(kb, row_ptr, val, d_desc + off, counts, xmap);
+        else k_drange<false><<<dim3(gx, nd), 256, 0, s>>>(kb, row_ptr, val, d_desc + off, counts, nullptr);
         count_launch();
         prof_end(s, KC_DRANGE, alg_bytes * nd / n_desc, nd);
     }
