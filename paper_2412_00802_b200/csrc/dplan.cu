@@ -567,6 +567,7 @@ hedl_status dplan_run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t 
         const bool u_restr = use_u && !(eflags & HEDL_EVAL_NO_RESTRICT_U);
         const bool all = r0 == 0 && r1 == p->dev_n_roots;
         // live nodes, roots, U capability (bottom up), demands (top down)
+        HEDL_CUDA(kb, cudaMemsetAsync(D.totals, 0, 8 * 4, s));   // (all 8 are read back below)
         k_dp_init<<<nblk(std::max(nn, 1u), 256), 256, 0, s>>>(p->d_nodes, nn, all, D.live, D.isroot, D.nfull, D.nproj);
         if (nn) {
             HEDL_CUDA(kb, cudaMemsetAsync(D.needu, 0, (size_t)nn * 8, s));
@@ -742,7 +743,7 @@ hedl_status dplan_run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t 
                         if (lr.slice) {
                             lr.cls = (int8_t)cls;
                         } else {
-                            heavy_need = std::max(heavy_need, (size_t)cnt * dr.n_heavy * 8);
+                            heavy_need = std::max(heavy_need, restrict_scratch_bytes(kb, dir, cnt));
                             lr.bytes = cnt * (4.0 * (kb->N + 1) + 4.0 * (dr.E - dr.E_heavy)) + 4.0 * W * (cnt + hu[b] + 2.0 * hv[b]);
                             lr.bytes2 = cnt * 4.0 * dr.E_heavy;
                         }

@@ -635,7 +635,7 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
             } else if (g.kind == NK_RESTRICT) {
                 tmp.gdesc[gi] = (uint32_t)n_res;
                 n_res += g.count;
-                if (!g.slice) *heavy_need = std::max(*heavy_need, (size_t)g.count * kb->dirs[g.key].n_heavy * 8);
+                if (!g.slice) *heavy_need = std::max(*heavy_need, restrict_scratch_bytes(kb, g.key, g.count));
                 if (g.slice && !g.ucomp)            // fused fillers: their operands, read by the pack
                     for (uint32_t m = g.first; m < g.first + g.count; ++m) {
                         const uint32_t c = p->ops[p->nodes[list[members[m]]].op_begin];
@@ -936,7 +936,16 @@ hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, u
             } else {
                 DirDev dd{dr.row_ptr, dr.col, dr.heavy_x, dr.heavy_nchunks, dr.chunks, dr.n_heavy, dr.n_chunks,
                           dr.tiles, dr.order, dr.tile_slice, dr.sell_off, dr.sell_w, dr.sell_col, dr.n_tiles};
-                launch_restrict(s, kd, dd, dd_desc, lr.count, cov, (uint32_t *)w->heavy.p, lr.bytes, lr.bytes2);
+                if (restrict_push(kb, lr.count)) {       // direction-optimising (push) candidates
+                    const hedl_dir &iv = kb->dirs[lr.key ^ 1];
+                    DirDev di{iv.row_ptr, iv.col, iv.heavy_x, iv.heavy_nchunks, iv.chunks, iv.n_heavy, iv.n_chunks,
+                              iv.tiles, iv.order, iv.tile_slice, iv.sell_off, iv.sell_w, iv.sell_col, iv.n_tiles};
+                    uint32_t *push = (uint32_t *)((char *)w->heavy.p + restrict_heavy_bytes(kb, lr.key, lr.count));
+                    launch_restrict(s, kd, dd, dd_desc, lr.count, cov, (uint32_t *)w->heavy.p, lr.bytes, lr.bytes2, &di,
+                                    push, push_scratch_words(kb->N, kb->W4, true));
+                } else {
+                    launch_restrict(s, kd, dd, dd_desc, lr.count, cov, (uint32_t *)w->heavy.p, lr.bytes, lr.bytes2);
+                }
             }
         } else if (lr.kind == NK_STRING) {
             const hedl_sdir &sdr = kb->sdirs[lr.key];

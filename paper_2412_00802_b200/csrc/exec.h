@@ -68,6 +68,17 @@ hedl_status reserve_plan(const hedl_kb *kb, PlanCache &pc, size_t bytes, Workspa
 hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, uint32_t r0, uint32_t *out_bits,
                          hedl_counts *counts_dev, cudaStream_t s);
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+// scratch of a per-node restriction group of `count` nodes in direction `dir`: the heavy-row
+// counters, then (small groups on large KBs) the push-direction scratch of each node
+inline bool restrict_push(const hedl_kb *kb, uint32_t count) { return count <= kPushMaxNodes && kb->N >= kPushMinN; }
+inline size_t restrict_heavy_bytes(const hedl_kb *kb, uint32_t dir, uint32_t count) {
+    return align_up((size_t)count * kb->dirs[dir].n_heavy * 8, 256);
+}
+inline size_t restrict_scratch_bytes(const hedl_kb *kb, uint32_t dir, uint32_t count) {
+    size_t b = restrict_heavy_bytes(kb, dir, count);
+    if (restrict_push(kb, count)) b += (size_t)count * push_scratch_words(kb->N, kb->W4, true) * 4;
+    return b;
+}
 // device planner (dplan.cu): builds and launches the plan of a device-compiled program on
 // the device; HEDL_ERR_UNSUPPORTED = the batch does not fit one chunk (host planner then)
 hedl_status dplan_run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, uint32_t *out_bits,

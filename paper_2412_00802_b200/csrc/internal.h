@@ -364,9 +364,14 @@ void launch_cover_init(cudaStream_t s, hedl_counts *counts, uint32_t n, uint64_t
 void launch_bool(cudaStream_t s, const KbDev &kb, const BoolDesc *d_desc, uint32_t n_desc,
                  const Operand *d_ops, hedl_counts *counts, double alg_bytes, uint64_t npos, uint64_t nneg,
                  bool full_rows);
+// inv / push (nullable): the inverse direction and self-cleaning scratch of push_stride words
+// per node -- groups of <= kPushMaxNodes nodes then pick push or pull per node on the device
 void launch_restrict(cudaStream_t s, const KbDev &kb, const DirDev &dir, const RestrictDesc *d_desc,
                      uint32_t n_desc, hedl_counts *counts, uint32_t *heavy_scratch, double alg_light,
-                     double alg_heavy);
+                     double alg_heavy, const DirDev *inv = nullptr, uint32_t *push = nullptr, size_t push_stride = 0);
+constexpr uint32_t kPushMaxNodes = 8;      // per-node groups this small consider the push direction
+constexpr uint32_t kPushMinN = 1u << 18;   // ... on KBs at least this large (below, the pull is cheap)
+size_t push_scratch_words(uint32_t N, uint32_t W4, bool counting);
 // xmap != null: U space of a direction (kb = {|U|, UW, UW4}); position p is individual xmap[p]
 void launch_drange(cudaStream_t s, const KbDev &kb, const uint32_t *row_ptr, const float *val,
                    const DrangeDesc *d_desc, uint32_t n_desc, hedl_counts *counts, double alg_bytes,

@@ -224,7 +224,9 @@ __global__ void __launch_bounds__(256) k_bool_warp(KbDev kb, const BoolDesc *__r
 // neighbour indices, a lane pair per row taking alternate neighbours), results as
 // bits in shared memory, one store per output word.  Heavy rows: k_restrict_heavy.
 __global__ void __launch_bounds__(256) k_restrict_tile(KbDev kb, DirDev dir, const RestrictDesc *__restrict__ descs,
-                                                       hedl_counts *counts) {
+                                                       hedl_counts *counts, const uint32_t *__restrict__ push_mode,
+                                                       uint32_t push_stride) {
+    if (push_mode && push_mode[(size_t)blockIdx.y * push_stride]) return;   // evaluated by the push kernels
     const RestrictDesc d = descs[blockIdx.y];
     __shared__ uint32_t sbits[32];
     const uint32_t t = blockIdx.x, x0 = t * 1024;
@@ -323,7 +325,9 @@ __global__ void __launch_bounds__(256) k_restrict_tile(KbDev kb, DirDev dir, con
 // ------------------------------------------------------------------------------
 // heavy rows: blockIdx.x = chunk of <= kHeavyChunk edges, blockIdx.y = node.
 __global__ void __launch_bounds__(256) k_restrict_heavy(KbDev kb, DirDev dir, const RestrictDesc *__restrict__ descs,
-                                                        hedl_counts *counts, uint32_t *scratch) {
+                                                        hedl_counts *counts, uint32_t *scratch,
+                                                        const uint32_t *__restrict__ push_mode, uint32_t push_stride) {
+    if (push_mode && push_mode[(size_t)blockIdx.y * push_stride]) return;
     const RestrictDesc d = descs[blockIdx.y];
     const uint4 ch = dir.chunks[blockIdx.x];
     uint32_t *cp = scratch + 2ull * (d.heavy_slot + ch.x);   // {count, ticket}
@@ -375,6 +379,130 @@ __global__ void __launch_bounds__(256) k_restrict_heavy(KbDev kb, DirDev dir, co
         cp[0] = 0;   // self-clean: the scratch is zero again for the next launch
         cp[1] = 0;
     }
+}
+
+// ------------------------------------------------------------------------------
+// Direction-optimising restriction (latency path): when the counted set
+// S = child ^ cmask is sparse, walk S's members y and their neighbours x through the inverse
+// direction's CSR ((x, y) in rho  <=>  x in rho^-(y)) instead of probing the
+// child bit of every edge of every x.  Work |S| x mean degree instead of E.  Per node j of the
+// launch: scratch push + j*stride words = {S count, mode} then the flag row (W4 words,
+// "x has an S-neighbour", enough when the count saturates at 1) and, for counting predicates,
+// N u32 counters.  Both directions are launched; each node runs in exactly one of them (the
+// pull kernels return for push nodes, the push kernels for pull nodes).  Flags and counters
+// are read and zeroed by the finishing kernel (self-cleaning); the header is reset per launch.
+__device__ __forceinline__ uint32_t *push_flags(uint32_t *base, uint32_t W4) { return base + 16; }
+__device__ __forceinline__ uint32_t *push_cnts(uint32_t *base, uint32_t W4) { return base + 16 + W4; }
+
+__global__ void __launch_bounds__(256) k_push_count(KbDev kb, const RestrictDesc *__restrict__ descs, uint32_t *push,
+                                                    uint32_t stride) {
+    const RestrictDesc d = descs[blockIdx.y];
+    uint32_t *hdr = push + (size_t)blockIdx.y * stride;
+    uint32_t c = 0;
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < kb.W; w += gridDim.x * blockDim.x) {
+        uint32_t v = __ldg(d.child + w) ^ d.cmask;
+        if (w == kb.W - 1 && (kb.N & 31)) v &= (1u << (kb.N & 31)) - 1u;
+        c += __popc(v);
+    }
+    c = __reduce_add_sync(FULL, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(hdr, c);
+}
+
+// mode: push iff |S| <= N / 4 (below that density the pull's probes outnumber the push's edges
+// even with its early exit); written by one thread per node before the other kernels run
+__global__ void k_push_mode(KbDev kb, uint32_t *push, uint32_t stride, uint32_t nd) {
+    const uint32_t j = threadIdx.x;
+    if (j >= nd) return;
+    uint32_t *hdr = push + (size_t)j * stride;
+    hdr[1] = (uint64_t)hdr[0] * 4 <= kb.N ? 1u : 0u;
+    hdr[0] = 0;                                           // (the count is not needed any more)
+}
+
+// light members: warp per 32 words of S, the warp walks each member's inverse row (lanes stride)
+__global__ void __launch_bounds__(256) k_push_scatter(KbDev kb, DirDev inv, const RestrictDesc *__restrict__ descs,
+                                                      uint32_t *push, uint32_t stride) {
+    uint32_t *hdr = push + (size_t)blockIdx.y * stride;
+    if (!hdr[1]) return;
+    const RestrictDesc d = descs[blockIdx.y];
+    const bool bitmode = d.sat <= 1;
+    uint32_t *flags = push_flags(hdr, kb.W4), *cnts = push_cnts(hdr, kb.W4);
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t wbase = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
+    for (uint32_t wi = 0; wi < 32; ++wi) {
+        const uint32_t w = wbase + wi;
+        if (w >= kb.W) break;
+        uint32_t v = __ldg(d.child + w) ^ d.cmask;
+        if (w == kb.W - 1 && (kb.N & 31)) v &= (1u << (kb.N & 31)) - 1u;
+        for (; v; v &= v - 1) {
+            const uint32_t y = 32 * w + __ffs(v) - 1;
+            const uint32_t a = __ldg(inv.row_ptr + y), b = __ldg(inv.row_ptr + y + 1);
+            if (b - a > kHeavyDeg) continue;             // heavy rows: k_push_heavy
+            for (uint32_t e = a + lane; e < b; e += 32) {
+                const uint32_t x = __ldg(inv.col + e);
+                if (bitmode) atomicOr(flags + (x >> 5), 1u << (x & 31));
+                else atomicAdd(cnts + x, 1u);
+            }
+        }
+    }
+}
+
+// heavy members: the inverse direction's heavy rows in 4,096-edge chunks, a CTA per chunk
+__global__ void __launch_bounds__(256) k_push_heavy(KbDev kb, DirDev inv, const RestrictDesc *__restrict__ descs,
+                                                    uint32_t *push, uint32_t stride) {
+    uint32_t *hdr = push + (size_t)blockIdx.y * stride;
+    if (!hdr[1]) return;
+    const RestrictDesc d = descs[blockIdx.y];
+    const uint4 ch = inv.chunks[blockIdx.x];
+    const uint32_t y = __ldg(inv.heavy_x + ch.x);
+    if (!((((__ldg(d.child + (y >> 5)) ^ d.cmask) >> (y & 31)) & 1u))) return;
+    const bool bitmode = d.sat <= 1;
+    uint32_t *flags = push_flags(hdr, kb.W4), *cnts = push_cnts(hdr, kb.W4);
+    for (uint32_t e = ch.y + threadIdx.x; e < ch.z; e += blockDim.x) {
+        const uint32_t x = __ldg(inv.col + e);
+        if (bitmode) atomicOr(flags + (x >> 5), 1u << (x & 31));
+        else atomicAdd(cnts + x, 1u);
+    }
+}
+
+// result words of push nodes: predicate on the flag (count saturating at 1) or the counter,
+// tail masked, then the same epilogue as the pull kernels (row, projection, coverage)
+__global__ void __launch_bounds__(256) k_push_finish(KbDev kb, const RestrictDesc *__restrict__ descs, uint32_t *push,
+                                                     uint32_t stride, hedl_counts *counts) {
+    uint32_t *hdr = push + (size_t)blockIdx.y * stride;
+    if (!hdr[1]) return;
+    const RestrictDesc d = descs[blockIdx.y];
+    const bool bitmode = d.sat <= 1;
+    uint32_t *flags = push_flags(hdr, kb.W4), *cnts = push_cnts(hdr, kb.W4);
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t v1 = pred_eval(d.pred, 1u, d.n) ? FULL : 0u, v0 = pred_eval(d.pred, 0u, d.n) ? FULL : 0u;
+    uint32_t tp = 0, fp = 0;
+    for (uint32_t w = blockIdx.x * 8 + (threadIdx.x >> 5); w < kb.W4; w += gridDim.x * 8) {
+        uint32_t word;
+        if (bitmode) {
+            const uint32_t f = flags[w];
+            if (lane == 0 && f) flags[w] = 0;             // self-clean
+            word = (f & v1) | (~f & v0);
+        } else {
+            const uint32_t x = 32 * w + lane;
+            uint32_t c = 0;
+            if (x < kb.N) {
+                c = cnts[x];
+                if (c) cnts[x] = 0;
+            }
+            word = __ballot_sync(FULL, pred_eval(d.pred, min(c, d.sat), d.n));
+        }
+        if (w >= kb.W) word = 0;
+        else if (w == kb.W - 1 && (kb.N & 31)) word &= (1u << (kb.N & 31)) - 1u;
+        if (lane == 0) {
+            if (d.out) d.out[w] = word;
+            if (d.proj && w < kb.W) proj_scatter(kb, d.proj, w, word);
+            if (d.cover >= 0 && w < kb.W) {
+                tp += __popc(word & __ldg(kb.pos + w));
+                fp += __popc(word & __ldg(kb.neg + w));
+            }
+        }
+    }
+    if (d.cover >= 0) block_cover(counts, d.cover, tp, fp);
 }
 
 // ------------------------------------------------------------------------------
@@ -584,20 +712,41 @@ void launch_bool(cudaStream_t s, const KbDev &kb, const BoolDesc *d_desc, uint32
     }
 }
 
+size_t push_scratch_words(uint32_t N, uint32_t W4, bool counting) {
+    return (size_t)16 + W4 + (counting ? (size_t)N : 0) + 16;
+}
+
 void launch_restrict(cudaStream_t s, const KbDev &kb, const DirDev &dir, const RestrictDesc *d_desc,
                      uint32_t n_desc, hedl_counts *counts, uint32_t *heavy_scratch, double alg_light,
-                     double alg_heavy) {
+                     double alg_heavy, const DirDev *inv, uint32_t *push, size_t push_stride) {
     const uint32_t gx = dir.n_tiles;
     if (!gx || !kb.W4) return;
+    const bool use_push = inv && push && n_desc <= kPushMaxNodes;
+    if (use_push) {
+        // direction decision on the device: |S| per node, then each node runs push or pull
+        const uint32_t stride = (uint32_t)push_stride;
+        for (uint32_t j = 0; j < n_desc; ++j) cudaMemsetAsync(push + (size_t)j * stride, 0, 8, s);
+        prof_begin(s, KC_RESTRICT);
+        k_push_count<<<dim3(std::min<uint32_t>(cdiv(kb.W, 256), 148u * 4u), n_desc), 256, 0, s>>>(kb, d_desc, push, stride);
+        k_push_mode<<<1, 32, 0, s>>>(kb, push, stride, n_desc);
+        k_push_scatter<<<dim3(cdiv(kb.W, 256), n_desc), 256, 0, s>>>(kb, *inv, d_desc, push, stride);
+        if (inv->n_chunks) k_push_heavy<<<dim3(inv->n_chunks, n_desc), 256, 0, s>>>(kb, *inv, d_desc, push, stride);
+        k_push_finish<<<dim3(std::min<uint32_t>(cdiv(kb.W4, 8), 148u * 8u), n_desc), 256, 0, s>>>(kb, d_desc, push, stride,
+                                                                                                counts);
+        for (int q = 0; q < 5; ++q) count_launch();
+        prof_end(s, KC_RESTRICT, 0, n_desc);
+    }
+    const uint32_t *pm = use_push ? push + 1 : nullptr;
     for (uint32_t off = 0; off < n_desc; off += 65535) {
         const uint32_t nd = n_desc - off < 65535 ? n_desc - off : 65535;
         prof_begin(s, KC_RESTRICT);
-        k_restrict_tile<<<dim3(gx, nd), 256, 0, s>>>(kb, dir, d_desc + off, counts);
+        k_restrict_tile<<<dim3(gx, nd), 256, 0, s>>>(kb, dir, d_desc + off, counts, pm, (uint32_t)push_stride);
         count_launch();
         prof_end(s, KC_RESTRICT, alg_light * nd / n_desc, nd);
         if (dir.n_chunks) {
             prof_begin(s, KC_HEAVY);
-            k_restrict_heavy<<<dim3(dir.n_chunks, nd), 256, 0, s>>>(kb, dir, d_desc + off, counts, heavy_scratch);
+            k_restrict_heavy<<<dim3(dir.n_chunks, nd), 256, 0, s>>>(kb, dir, d_desc + off, counts, heavy_scratch, pm,
+                                                                    (uint32_t)push_stride);
             count_launch();
             prof_end(s, KC_HEAVY, alg_heavy * nd / n_desc, nd);
         }

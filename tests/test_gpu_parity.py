@@ -264,6 +264,40 @@ def test_eval_one_latency_path():
             assert c2 == c1
 
 
+def test_push_direction_latency_path():
+    """Direction-optimising restrictions: on a KB above kPushMinN individuals
+    the latency path evaluates a restriction whose counted set S = child ^ cmask holds at most
+    N/4 members by walking S through the inverse CSR, else by the pull sweep.  Fillers from
+    empty to full density, complemented ones (FORALL counts the complement), every predicate,
+    inverse roles, heavy inverse rows (hubs of degree 4,000), nested restrictions: every
+    result equals the oracle, bitsets and counts, through hedl_eval_one and a small batch."""
+    hedl = _hedl()
+    kb = abox.powerlaw_kb(400_000, 12, 2, 8.0, 4000, 0.7, 1.0, 0.01, seed=31)
+    A = lambda i: ("ATOM", i)
+    trees = []
+    for r in range(2):
+        for inv in (False, True):
+            for c in (A(0), A(5), A(11), ("NOT", A(3)), ("TOP",), ("BOTTOM",), ("AND", [A(1), A(2)])):
+                trees += [("EXISTS", r, inv, c), ("FORALL", r, inv, c), ("MIN", 2, r, inv, c), ("MAX", 1, r, inv, c),
+                          ("EXACT", 3, r, inv, c), ("MIN", 0, r, inv, c)]
+    trees += [("EXISTS", 0, False, ("AND", [A(1), ("FORALL", 1, True, ("OR", [A(2), ("NOT", A(3))]))])),
+              ("MIN", 2, 0, True, ("EXISTS", 1, False, A(4))), ("FORALL", 0, False, ("OR", [("EXISTS", 0, False, A(5)),
+                                                                                             ("DRANGE", 0, 0.5, np.inf)]))]
+    nodes, kids, roots = flatten(trees)
+    k = hedl.hedl_kb_load(kb, 0)
+    prog = hedl.hedl_compile(k, nodes, kids, roots)
+    ob, oc = setsem.evaluate(kb, nodes, kids, roots, threads=8)
+    for i in range(len(roots)):
+        b1, c1 = hedl.hedl_eval_one(k, prog, i, want_bits=True)
+        assert c1 == tuple(int(v) for v in oc[i]), (i, trees[i])
+        assert np.array_equal(b1.cpu().numpy().view(np.uint32), ob[i]), (i, trees[i])
+    for first in range(0, len(roots), 6):          # groups of <= 8 nodes on the batch path too
+        n = min(6, len(roots) - first)
+        b, c = hedl.hedl_eval_batch(k, prog, first, n, want_bits=True, flags=2)
+        assert np.array_equal(c, oc[first:first + n]) and np.array_equal(b.cpu().numpy().view(np.uint32),
+                                                                         ob[first:first + n]), first
+
+
 def test_free_order_kb_before_program():
     """A program keeps its KB alive: freeing the KB handle first, then the program, leaves the
     library healthy for the next KB (regression: use-after-free on the KB's device id)."""
