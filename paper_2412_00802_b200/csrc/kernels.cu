@@ -383,21 +383,26 @@ __global__ void __launch_bounds__(256) k_restrict_heavy(KbDev kb, DirDev dir, co
 
 // ------------------------------------------------------------------------------
 // Direction-optimising restriction (latency path): when the counted set
-// S = child ^ cmask is sparse, walk S's members y and their neighbours x through the inverse
-// direction's CSR ((x, y) in rho  <=>  x in rho^-(y)) instead of probing the
-// child bit of every edge of every x.  Work |S| x mean degree instead of E.  Per node j of the
-// launch: scratch push + j*stride words = {S count, mode} then the flag row (W4 words,
-// "x has an S-neighbour", enough when the count saturates at 1) and, for counting predicates,
-// N u32 counters.  Both directions are launched; each node runs in exactly one of them (the
-// pull kernels return for push nodes, the push kernels for pull nodes).  Flags and counters
-// are read and zeroed by the finishing kernel (self-cleaning); the header is reset per launch.
+// S = child ^ cmask -- or its complement -- is sparse, walk its members y and their neighbours
+// x through the inverse direction's CSR ((x, y) in rho  <=>  x in rho^-(y))
+// instead of probing the child bit of every edge of every x: work |S| x mean degree instead
+// of E.  Modes, decided on the device per node: 1 = push S (the flag "x has an S-neighbour"
+// when the count saturates at 1, else per-x counters), 2 = push the complement of S into
+// counters, cnt_S(x) = deg(x) - cnt_notS(x), 0 = the pull sweep.  Per node j of the launch:
+// scratch push + j*stride words = {S count, mode, ticket} then the flag row (W4 words) and N
+// u32 counters.  Both directions are launched; each node runs in exactly one (the pull
+// kernels return for push nodes, the push kernels for pull nodes).  Flags and counters are
+// read and zeroed by the finishing kernel, the header by k_push_reset (all zero between
+// launches: another group's heavy-row counters may reuse the bytes).
 __device__ __forceinline__ uint32_t *push_flags(uint32_t *base, uint32_t W4) { return base + 16; }
 __device__ __forceinline__ uint32_t *push_cnts(uint32_t *base, uint32_t W4) { return base + 16 + W4; }
 
+// |S| per node, the last block to finish picks the mode
 __global__ void __launch_bounds__(256) k_push_count(KbDev kb, const RestrictDesc *__restrict__ descs, uint32_t *push,
                                                     uint32_t stride) {
     const RestrictDesc d = descs[blockIdx.y];
     uint32_t *hdr = push + (size_t)blockIdx.y * stride;
+    __shared__ uint32_t s_red[8];
     uint32_t c = 0;
     for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < kb.W; w += gridDim.x * blockDim.x) {
         uint32_t v = __ldg(d.child + w) ^ d.cmask;
@@ -405,44 +410,64 @@ __global__ void __launch_bounds__(256) k_push_count(KbDev kb, const RestrictDesc
         c += __popc(v);
     }
     c = __reduce_add_sync(FULL, c);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(hdr, c);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int q = 0; q < 8; ++q) t += s_red[q];
+        if (t) atomicAdd(hdr, t);
+        __threadfence();
+        if (atomicAdd(hdr + 2, 1u) == gridDim.x - 1) {    // last block: the total is final
+            __threadfence();
+            const uint64_t cs = atomicAdd(hdr, 0u);
+            // below N/4 members the push walks fewer edges than the pull probes, even with
+            // the pull's early exit
+            hdr[1] = cs * 4 <= kb.N ? 1u : ((uint64_t)kb.N - cs) * 4 <= kb.N ? 2u : 0u;
+        }
+    }
 }
 
-// mode: push iff |S| <= N / 4 (below that density the pull's probes outnumber the push's edges
-// even with its early exit); written by one thread per node before the other kernels run
-__global__ void k_push_mode(KbDev kb, uint32_t *push, uint32_t stride, uint32_t nd) {
+__global__ void k_push_reset(uint32_t *push, uint32_t stride, uint32_t nd) {
     const uint32_t j = threadIdx.x;
-    if (j >= nd) return;
-    uint32_t *hdr = push + (size_t)j * stride;
-    hdr[1] = (uint64_t)hdr[0] * 4 <= kb.N ? 1u : 0u;
-    hdr[0] = 0;                                           // (the count is not needed any more)
+    if (j < nd) {
+        uint32_t *h = push + (size_t)j * stride;
+        h[0] = h[1] = h[2] = 0;
+    }
 }
 
-// light members: warp per 32 words of S, the warp walks each member's inverse row (lanes stride)
+__device__ __forceinline__ void push_edge(bool bitmode, uint32_t *flags, uint32_t *cnts, uint32_t x) {
+    if (bitmode) atomicOr(flags + (x >> 5), 1u << (x & 31));
+    else atomicAdd(cnts + x, 1u);
+}
+
+// light and medium members: lane per word of the pushed set, each lane walks its members'
+// inverse rows (32 independent chains per warp); heavy rows are k_push_heavy's
 __global__ void __launch_bounds__(256) k_push_scatter(KbDev kb, DirDev inv, const RestrictDesc *__restrict__ descs,
                                                       uint32_t *push, uint32_t stride) {
     uint32_t *hdr = push + (size_t)blockIdx.y * stride;
-    if (!hdr[1]) return;
+    const uint32_t mode = hdr[1];
+    if (!mode) return;
     const RestrictDesc d = descs[blockIdx.y];
-    const bool bitmode = d.sat <= 1;
+    const bool bitmode = mode == 1 && d.sat <= 1;
+    const uint32_t flip = mode == 2 ? FULL : 0u;
     uint32_t *flags = push_flags(hdr, kb.W4), *cnts = push_cnts(hdr, kb.W4);
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t wbase = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
-    for (uint32_t wi = 0; wi < 32; ++wi) {
-        const uint32_t w = wbase + wi;
-        if (w >= kb.W) break;
-        uint32_t v = __ldg(d.child + w) ^ d.cmask;
-        if (w == kb.W - 1 && (kb.N & 31)) v &= (1u << (kb.N & 31)) - 1u;
-        for (; v; v &= v - 1) {
-            const uint32_t y = 32 * w + __ffs(v) - 1;
-            const uint32_t a = __ldg(inv.row_ptr + y), b = __ldg(inv.row_ptr + y + 1);
-            if (b - a > kHeavyDeg) continue;             // heavy rows: k_push_heavy
-            for (uint32_t e = a + lane; e < b; e += 32) {
-                const uint32_t x = __ldg(inv.col + e);
-                if (bitmode) atomicOr(flags + (x >> 5), 1u << (x & 31));
-                else atomicAdd(cnts + x, 1u);
-            }
+    const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= kb.W) return;
+    uint32_t v = __ldg(d.child + w) ^ d.cmask ^ flip;
+    if (w == kb.W - 1 && (kb.N & 31)) v &= (1u << (kb.N & 31)) - 1u;
+    for (; v; v &= v - 1) {
+        const uint32_t y = 32 * w + __ffs(v) - 1;
+        const uint32_t a = __ldg(inv.row_ptr + y), b = __ldg(inv.row_ptr + y + 1);
+        if (b - a > kHeavyDeg) continue;
+        uint32_t e = a;
+        for (; e + 4 <= b; e += 4) {                     // four neighbour ids in flight
+            uint32_t x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = __ldg(inv.col + e + u);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) push_edge(bitmode, flags, cnts, x[u]);
         }
+        for (; e < b; ++e) push_edge(bitmode, flags, cnts, __ldg(inv.col + e));
     }
 }
 
@@ -450,55 +475,64 @@ __global__ void __launch_bounds__(256) k_push_scatter(KbDev kb, DirDev inv, cons
 __global__ void __launch_bounds__(256) k_push_heavy(KbDev kb, DirDev inv, const RestrictDesc *__restrict__ descs,
                                                     uint32_t *push, uint32_t stride) {
     uint32_t *hdr = push + (size_t)blockIdx.y * stride;
-    if (!hdr[1]) return;
+    const uint32_t mode = hdr[1];
+    if (!mode) return;
     const RestrictDesc d = descs[blockIdx.y];
     const uint4 ch = inv.chunks[blockIdx.x];
     const uint32_t y = __ldg(inv.heavy_x + ch.x);
-    if (!((((__ldg(d.child + (y >> 5)) ^ d.cmask) >> (y & 31)) & 1u))) return;
-    const bool bitmode = d.sat <= 1;
+    const uint32_t in_s = (((__ldg(d.child + (y >> 5)) ^ d.cmask) >> (y & 31)) & 1u);
+    if (in_s == (mode == 2 ? 1u : 0u)) return;           // y is not in the pushed set
+    const bool bitmode = mode == 1 && d.sat <= 1;
     uint32_t *flags = push_flags(hdr, kb.W4), *cnts = push_cnts(hdr, kb.W4);
-    for (uint32_t e = ch.y + threadIdx.x; e < ch.z; e += blockDim.x) {
-        const uint32_t x = __ldg(inv.col + e);
-        if (bitmode) atomicOr(flags + (x >> 5), 1u << (x & 31));
-        else atomicAdd(cnts + x, 1u);
-    }
+    for (uint32_t e = ch.y + threadIdx.x; e < ch.z; e += blockDim.x) push_edge(bitmode, flags, cnts, __ldg(inv.col + e));
 }
 
-// result words of push nodes: predicate on the flag (count saturating at 1) or the counter,
-// tail masked, then the same epilogue as the pull kernels (row, projection, coverage)
-__global__ void __launch_bounds__(256) k_push_finish(KbDev kb, const RestrictDesc *__restrict__ descs, uint32_t *push,
-                                                     uint32_t stride, hedl_counts *counts) {
+// result words of push nodes: predicate on the flag (count saturating at 1), the counter, or
+// deg - the complement's counter; tail masked; the pull kernels' epilogue (row, projection,
+// coverage).  Bit mode: lane per word; counters: lane per individual, ballot per word.
+__global__ void __launch_bounds__(256) k_push_finish(KbDev kb, DirDev dir, const RestrictDesc *__restrict__ descs,
+                                                     uint32_t *push, uint32_t stride, hedl_counts *counts) {
     uint32_t *hdr = push + (size_t)blockIdx.y * stride;
-    if (!hdr[1]) return;
+    const uint32_t mode = hdr[1];
+    if (!mode) return;
     const RestrictDesc d = descs[blockIdx.y];
-    const bool bitmode = d.sat <= 1;
+    const bool bitmode = mode == 1 && d.sat <= 1;
     uint32_t *flags = push_flags(hdr, kb.W4), *cnts = push_cnts(hdr, kb.W4);
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t v1 = pred_eval(d.pred, 1u, d.n) ? FULL : 0u, v0 = pred_eval(d.pred, 0u, d.n) ? FULL : 0u;
     uint32_t tp = 0, fp = 0;
-    for (uint32_t w = blockIdx.x * 8 + (threadIdx.x >> 5); w < kb.W4; w += gridDim.x * 8) {
-        uint32_t word;
-        if (bitmode) {
+    if (bitmode) {
+        const uint32_t v1 = pred_eval(d.pred, 1u, d.n) ? FULL : 0u, v0 = pred_eval(d.pred, 0u, d.n) ? FULL : 0u;
+        for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < kb.W4; w += gridDim.x * blockDim.x) {
             const uint32_t f = flags[w];
-            if (lane == 0 && f) flags[w] = 0;             // self-clean
-            word = (f & v1) | (~f & v0);
-        } else {
-            const uint32_t x = 32 * w + lane;
-            uint32_t c = 0;
-            if (x < kb.N) {
-                c = cnts[x];
-                if (c) cnts[x] = 0;
-            }
-            word = __ballot_sync(FULL, pred_eval(d.pred, min(c, d.sat), d.n));
-        }
-        if (w >= kb.W) word = 0;
-        else if (w == kb.W - 1 && (kb.N & 31)) word &= (1u << (kb.N & 31)) - 1u;
-        if (lane == 0) {
+            if (f) flags[w] = 0;                          // self-clean
+            uint32_t word = (f & v1) | (~f & v0);
+            if (w >= kb.W) word = 0;
+            else if (w == kb.W - 1 && (kb.N & 31)) word &= (1u << (kb.N & 31)) - 1u;
             if (d.out) d.out[w] = word;
             if (d.proj && w < kb.W) proj_scatter(kb, d.proj, w, word);
             if (d.cover >= 0 && w < kb.W) {
                 tp += __popc(word & __ldg(kb.pos + w));
                 fp += __popc(word & __ldg(kb.neg + w));
+            }
+        }
+    } else {
+        for (uint32_t w = blockIdx.x * 8 + (threadIdx.x >> 5); w < kb.W4; w += gridDim.x * 8) {
+            const uint32_t x = 32 * w + lane;
+            bool r = false;
+            if (x < kb.N) {
+                uint32_t c = cnts[x];
+                if (c) cnts[x] = 0;
+                if (mode == 2) c = __ldg(dir.row_ptr + x + 1) - __ldg(dir.row_ptr + x) - c;
+                r = pred_eval(d.pred, min(c, d.sat), d.n);
+            }
+            const uint32_t word = __ballot_sync(FULL, r);
+            if (lane == 0) {
+                if (d.out) d.out[w] = word;
+                if (d.proj && w < kb.W) proj_scatter(kb, d.proj, w, word);
+                if (d.cover >= 0 && w < kb.W) {
+                    tp += __popc(word & __ldg(kb.pos + w));
+                    fp += __popc(word & __ldg(kb.neg + w));
+                }
             }
         }
     }
@@ -725,15 +759,14 @@ void launch_restrict(cudaStream_t s, const KbDev &kb, const DirDev &dir, const R
     if (use_push) {
         // direction decision on the device: |S| per node, then each node runs push or pull
         const uint32_t stride = (uint32_t)push_stride;
-        for (uint32_t j = 0; j < n_desc; ++j) cudaMemsetAsync(push + (size_t)j * stride, 0, 8, s);
+        // (the headers are zero: k_push_reset cleans them after every launch)
         prof_begin(s, KC_RESTRICT);
         k_push_count<<<dim3(std::min<uint32_t>(cdiv(kb.W, 256), 148u * 4u), n_desc), 256, 0, s>>>(kb, d_desc, push, stride);
-        k_push_mode<<<1, 32, 0, s>>>(kb, push, stride, n_desc);
         k_push_scatter<<<dim3(cdiv(kb.W, 256), n_desc), 256, 0, s>>>(kb, *inv, d_desc, push, stride);
         if (inv->n_chunks) k_push_heavy<<<dim3(inv->n_chunks, n_desc), 256, 0, s>>>(kb, *inv, d_desc, push, stride);
-        k_push_finish<<<dim3(std::min<uint32_t>(cdiv(kb.W4, 8), 148u * 8u), n_desc), 256, 0, s>>>(kb, d_desc, push, stride,
-                                                                                                counts);
-        for (int q = 0; q < 5; ++q) count_launch();
+        k_push_finish<<<dim3(std::min<uint32_t>(cdiv(kb.W4, 256), 148u * 8u), n_desc), 256, 0, s>>>(kb, dir, d_desc, push,
+                                                                                                 stride, counts);
+        for (int q = 0; q < 4; ++q) count_launch();
         prof_end(s, KC_RESTRICT, 0, n_desc);
     }
     const uint32_t *pm = use_push ? push + 1 : nullptr;
@@ -750,6 +783,10 @@ void launch_restrict(cudaStream_t s, const KbDev &kb, const DirDev &dir, const R
             count_launch();
             prof_end(s, KC_HEAVY, alg_heavy * nd / n_desc, nd);
         }
+    }
+    if (use_push) {
+        k_push_reset<<<1, 32, 0, s>>>(push, (uint32_t)push_stride, n_desc);
+        count_launch();
     }
 }
 
