@@ -489,15 +489,17 @@ def hedl_score_topk(counts, metric: int = HEDL_SCORE_ACCURACY, k: int = 0, want_
 
 
 def hedl_eval_one(kb: KB, prog: Program, root: int, want_bits: bool = False, stream=None):
-    """-> (bits int32 tensor [W] on the KB's device or None, (tp, fp, fn, tn))."""
+    """-> (bits int32 tensor [W] on the KB's device or None, (tp, fp, fn, tn)).
+    The latency path: the library switches to the KB's device itself, so no torch device
+    context is entered here (it costs microseconds per call)."""
     import torch
     out = np.zeros(4, dtype=np.uint64)
     bits = None
-    with torch.cuda.device(kb.device):
-        if want_bits:
-            bits = torch.empty(max(kb.W, 1), dtype=torch.int32, device=f"cuda:{kb.device}")
-        _check(lib().hedl_eval_one(kb._h, prog._h, root, C.c_void_p(bits.data_ptr()) if want_bits else None,
-                                   _ptr(out), _stream(stream)))
+    if want_bits:
+        bits = torch.empty(max(kb.W, 1), dtype=torch.int32, device=f"cuda:{kb.device}")
+    st = stream if stream is not None else torch.cuda.current_stream(kb.device)
+    _check(lib().hedl_eval_one(kb._h, prog._h, root, C.c_void_p(bits.data_ptr()) if want_bits else None,
+                               out.ctypes.data, C.c_void_p(st.cuda_stream)))
     return (bits[:kb.W] if want_bits else None), tuple(int(v) for v in out)
 
 

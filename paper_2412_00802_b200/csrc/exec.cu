@@ -1219,6 +1219,7 @@ static bool build_interp(const hedl_kb *kb, const hedl_program *p, uint32_t root
             if (ref_type(o) == RT_NODE) {
                 const uint32_t li = (uint32_t)(std::find(order.begin(), order.end(), ref_id(o)) - order.begin());
                 o = mkref(RT_NODE, li, ref_comp(o));
+                if (n.kind == NK_RESTRICT) prog.nodes[li].kind |= 0x80;   // read at any individual
             }
             prog.ops[prog.n_ops++] = o;
         }

@@ -5,9 +5,11 @@
 namespace hedl {
 constexpr uint32_t kInterpMaxNodes = 96, kInterpMaxOps = 512;
 constexpr uint32_t kInterpMaxN = 1u << 16;   // individuals; larger KBs use the per-node kernels
+constexpr uint32_t kInterpCl = 8;            // CTAs of the cluster interpreter
+constexpr uint32_t kInterpClusterMinW4 = 256;   // rows of at least this many words use it
 
 struct InterpNode {
-    uint8_t kind, pred;
+    uint8_t kind, pred;     // kind bit 7: a restriction reads this row at any individual
     uint16_t dir;
     uint32_t n, sat;
     float lo, hi;
