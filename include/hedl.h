@@ -281,6 +281,7 @@ hedl_status hedl_eval_one(const hedl_kb *kb, hedl_program *prog, uint32_t root,
 #define HEDL_EVAL_FORCE_SLICE 4u     /* lane-pack every eligible restriction group, however small (tests) */
 #define HEDL_EVAL_NO_FUSE 8u         /* materialise boolean fillers of lane packs instead of fusing them (A/B, tests) */
 #define HEDL_EVAL_NO_RESTRICT_U 16u  /* restrictions never emit U rows: booleans over them run in full (A/B, tests) */
+#define HEDL_EVAL_NO_USWEEP 32u      /* restrictions needed over one U set are swept over all rows (A/B, tests) */
 
 /* Throughput path: evaluate roots [first_root, first_root + n_roots) of prog.
  * Output position i <-> root first_root + i (input order).

@@ -27,6 +27,7 @@ HEDL_EVAL_PER_NODE = 2
 HEDL_EVAL_FORCE_SLICE = 4
 HEDL_EVAL_NO_FUSE = 8
 HEDL_EVAL_NO_RESTRICT_U = 16
+HEDL_EVAL_NO_USWEEP = 32
 
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "OUT_OF_RANGE", 3: "EXAMPLE_CONFLICT", 4: "BAD_EXPR",
           5: "PARSE", 6: "CUDA", 7: "OOM", 8: "UNSUPPORTED"}

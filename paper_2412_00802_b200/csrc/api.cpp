@@ -119,7 +119,7 @@ void pool_release_all(hedl_kb *kb) {
 }
 
 const char *kKClassName[KC_N] = {"bool", "restrict", "restrict_heavy", "drange", "cover_init", "gather",
-                                 "slice_pack", "slice", "slice_heavy", "kb", "slice_ex", "interp", "string", "bool_l2"};
+                                 "slice_pack", "slice", "slice_heavy", "kb", "slice_ex", "interp", "string", "bool_l2", "slice_u"};
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }

@@ -141,6 +141,7 @@ struct Group {
     bool ex = false;
     int16_t usp = -1;        // boolean group evaluated over U of direction usp
     bool ucomp = false;      // EX pack whose fillers are U rows
+    int8_t usw = -1;         // U-sweep pack: rows of U_usw only, results to U rows
 };
 
 // ---- planning (host threads, as the paper generates plans in parallel) ----
@@ -329,6 +330,7 @@ struct ChunkTmp {            // per-chunk planning state kept between the sizing
     // boolean fillers fused into the packs: a full row only lane packs
     // read is never materialised; the pack kernel combines the node's operand rows itself
     std::vector<uint8_t> by_pack, by_other, fused;
+    std::vector<int8_t> uswd;          // U-sweep direction of a restriction (-1: full pack / EX / per-node)
     std::vector<uint64_t> need_u;      // directions whose U rows of the node are read
     std::vector<uint64_t> u_out;       // directions whose U rows the node (a boolean) computes
     std::vector<uint32_t> ubase;       // first U-row slot of the node
@@ -343,7 +345,7 @@ struct ChunkTmp {            // per-chunk planning state kept between the sizing
 // rows (M bits instead of N); its operands then only need projected rows, which
 // atoms/TOP have precomputed and computed nodes emit as a scatter epilogue.
 void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> &list, ChunkPlan &cp,
-                bool out_bits, bool use_slice, bool force_slice, bool allow_fuse, bool allow_urestr, uint32_t *rows, uint32_t *prows, uint32_t *urows,
+                bool out_bits, bool use_slice, bool force_slice, bool allow_fuse, bool allow_urestr, bool allow_usw, uint32_t *rows, uint32_t *prows, uint32_t *urows,
                 std::vector<uint32_t> &local, char *h_blob, size_t *blob_cursor, size_t *heavy_need, bool sizes_only,
                 ChunkTmp &tmp) {
     const uint32_t nn = (uint32_t)list.size();
@@ -383,6 +385,8 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
         by_pack.assign(nn, 0);
         by_other.assign(nn, 0);
         fused.assign(nn, 0);
+        auto &uswd = tmp.uswd;
+        uswd.assign(nn, -1);
         auto &need_u = tmp.need_u;
         auto &u_out = tmp.u_out;
         need_u.assign(nn, 0);
@@ -398,6 +402,17 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
         // restrictions in full lane packs emit U rows from the tile epilogue (DESIGN.md "U rows
         // of restrictions"), so booleans over them are U-capable too
         const bool u_restr = use_u && allow_urestr && kb->dirs.size() <= kMaxUDirs;
+        // a restriction needed only as one U row (not in full, not projected, not a root) is
+        // swept over the rows of that U set only
+        const bool use_usw = u_restr && allow_usw;
+        auto usw_of = [&](size_t kk, uint64_t uo) -> int {
+            if (!use_usw || !uo || need_full[kk] || need_proj[kk] || cover_of_node[kk] >= 0) return -1;
+            if (__builtin_popcountll(uo) != 1) return -1;
+            const CNode &n = p->nodes[list[kk]];
+            if (n.kind != NK_RESTRICT || slice_class(n.pred, n.n, n.sat) >= 2) return -1;
+            const int d = __builtin_ctzll(uo);
+            return (d < (int)kMaxUDirs && kb->dirs[n.dir].usw[d].n_rows) ? d : -1;
+        };
         std::vector<uint8_t> ucap(nn, 0);
         if (use_u)
             for (uint32_t lo = 0; lo < nn;) {                  // bottom-up, level by level
@@ -437,13 +452,56 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
             // (restrictions emitting U rows run in full packs too, and force their group's packing)
             uint32_t nfull_dir[64] = {0};
             uint64_t uforce = 0;
+            // U sweeps: per (direction, class) the candidates of each U set
+            // either get packs of their own (rows of U_d only) or join the full packs; the cheaper
+            // split by a per-pack cost model (full pack: T build + heavy rows + full sweep = 1.42;
+            // U pack: T build + heavy / sweep at the U set's edge fraction f = 0.20 + 1.22 f)
+            if (use_usw) {
+                uint32_t F[64][2] = {{0}}, Lc[64][2][kMaxUDirs] = {{{0}}};
+                for (uint32_t kk = lo; kk < hi; ++kk) {
+                    const CNode &n = p->nodes[list[kk]];
+                    if (n.kind != NK_RESTRICT) continue;
+                    const uint32_t cls = slice_class(n.pred, n.n, n.sat);
+                    if (cls >= 2) continue;
+                    const uint64_t uo = (need_u[kk] && ucap[kk]) ? need_u[kk] : 0;
+                    const int c = usw_of(kk, uo);
+                    if (c >= 0) Lc[n.dir & 63][cls][c]++;
+                    else if (need_full[kk] || need_u[kk]) F[n.dir & 63][cls]++;
+                }
+                uint32_t pick[64][2] = {{0}};                 // bit d: U_d candidates get their own packs
+                for (uint32_t dd = 0; dd < kb->dirs.size() && dd < 64; ++dd)
+                    for (int cls = 0; cls < 2; ++cls) {
+                        double best = 1e300;
+                        for (uint32_t sub = 0; sub < (1u << kMaxUDirs); ++sub) {
+                            double cost = 0;
+                            uint32_t joined = F[dd][cls];
+                            for (uint32_t d = 0; d < kMaxUDirs; ++d) {
+                                if (!Lc[dd][cls][d]) continue;
+                                if (sub >> d & 1) cost += ((Lc[dd][cls][d] + 255) / 256) * (0.20 + 1.22 * kb->dirs[dd].usw[d].frac);
+                                else joined += Lc[dd][cls][d];
+                            }
+                            cost += ((joined + 255) / 256) * 1.42;
+                            if (cost < best - 1e-9) { best = cost; pick[dd][cls] = sub; }
+                        }
+                    }
+                for (uint32_t kk = lo; kk < hi; ++kk) {
+                    const CNode &n = p->nodes[list[kk]];
+                    if (n.kind != NK_RESTRICT) continue;
+                    const uint32_t cls = slice_class(n.pred, n.n, n.sat);
+                    if (cls >= 2) continue;
+                    const uint64_t uo = (need_u[kk] && ucap[kk]) ? need_u[kk] : 0;
+                    const int c = usw_of(kk, uo);
+                    if (c >= 0 && (pick[n.dir & 63][cls] >> c & 1)) uswd[kk] = (int8_t)c;
+                }
+            }
             for (uint32_t kk = lo; kk < hi; ++kk) {
                 const CNode &n = p->nodes[list[kk]];
                 if (n.kind != NK_RESTRICT) continue;
                 if (need_u[kk] && !ucap[kk]) need_full[kk] = 1;
-                if ((need_full[kk] || (need_u[kk] && ucap[kk])) && slice_class(n.pred, n.n, n.sat) < 2)
-                    nfull_dir[n.dir & 63]++;
-                if (need_u[kk] && ucap[kk]) uforce |= 1ull << (n.dir & 63);
+                const uint64_t uo = (need_u[kk] && ucap[kk]) ? need_u[kk] : 0;
+                const bool swept = uswd[kk] >= 0;             // U sweeps are always packed, separately
+                if ((need_full[kk] || (uo && !swept)) && slice_class(n.pred, n.n, n.sat) < 2) nfull_dir[n.dir & 63]++;
+                if (uo && !swept) uforce |= 1ull << (n.dir & 63);
             }
             par_for(hi - lo, 1 << 13, [&](size_t a, size_t b) {
                 for (size_t kk = lo + a; kk < lo + b; ++kk) {
@@ -462,7 +520,7 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                     // a full-row restriction that runs in a lane pack (else: the per-node kernel)
                     const bool packed = n.kind == NK_RESTRICT && (need_full[kk] || uo) && use_slice &&
                                         slice_class(n.pred, n.n, n.sat) < 2 &&
-                                        (slice_worthwhile(kb, nfull_dir[n.dir & 63], force_slice) ||
+                                        (uswd[kk] >= 0 || slice_worthwhile(kb, nfull_dir[n.dir & 63], force_slice) ||
                                          (uforce >> (n.dir & 63) & 1));
                     // a boolean only lane packs read in full: fused into those packs, no row
                     const bool fuse = allow_fuse && isbool && need_full[kk] && by_pack[kk] && !by_other[kk] && !need_proj[kk] &&
@@ -554,10 +612,12 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                 // rows, always packed), then the per-node rest
                 uint32_t ns = 0, nf = 0;
                 bool any_u = false;
+                auto in_full = [&](uint32_t q) { return need_full[q] || (u_out[q] && tmp.uswd[q] < 0); };
                 while (k + ns < e && slice_class(p->nodes[list[k + ns]].pred, p->nodes[list[k + ns]].n,
                                                  p->nodes[list[k + ns]].sat) != 2) {
-                    nf += (need_full[k + ns] || u_out[k + ns]) != 0;
-                    any_u |= u_out[k + ns] != 0;
+                    const uint32_t q = k + ns;
+                    nf += in_full(q);
+                    any_u |= u_out[q] && tmp.uswd[q] < 0;
                     ++ns;
                 }
                 const bool full_packs = nf && (slice_worthwhile(kb, nf, force_slice) || any_u);
@@ -566,9 +626,18 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                     Group g{kind, key, (uint32_t)members.size(), 0};
                     g.slice = true;
                     for (uint32_t q = k; q < k + ns; ++q)
-                        if (need_full[q] || u_out[q]) members.push_back(q);
+                        if (in_full(q)) members.push_back(q);
                     g.count = (uint32_t)members.size() - g.first;
                     groups.push_back(g);
+                }
+                for (int d = 0; d < (int)kMaxUDirs; ++d) {     // U sweeps, one group per U direction
+                    Group g{kind, key, (uint32_t)members.size(), 0};
+                    g.slice = true;
+                    g.usw = (int8_t)d;
+                    for (uint32_t q = k; q < k + ns; ++q)
+                        if (!need_full[q] && u_out[q] && tmp.uswd[q] == d) members.push_back(q);
+                    g.count = (uint32_t)members.size() - g.first;
+                    if (g.count) groups.push_back(g);
                 }
                 // EX packs: fillers available as U rows of this direction (U-space booleans,
                 // atoms, TOP) in one group, fillers with full rows in another
@@ -664,13 +733,15 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
         timing_note("plan: covers+demands", ts1 - ts0);
         timing_note("plan: slots+groups", now_ms() - ts1);
         if (timing_enabled()) {            // plan statistics (HEDL_TIMING=1): lanes per pack kind
-            uint64_t full_rows = 0, full_u_only = 0, full_any = 0, ex_u = 0, ex_full = 0, per_node = 0, fused_n = 0;
+            uint64_t full_rows = 0, full_u_only = 0, full_any = 0, ex_u = 0, ex_full = 0, per_node = 0, fused_n = 0, swept = 0;
             uint64_t bool_full = 0, bool_proj = 0, bool_u = 0, restr_fillers_full = 0;
             for (const Group &g : groups)
                 for (uint32_t m = g.first; m < g.first + g.count; ++m) {
                     const uint32_t q = members[m];
                     if (g.kind == NK_RESTRICT) {
-                        if (g.slice && !g.ex) {
+                        if (g.usw >= 0) {
+                            ++swept;
+                        } else if (g.slice && !g.ex) {
                             ++full_any;
                             if (need_full[q]) ++full_rows; else ++full_u_only;
                         } else if (g.ex) { if (g.ucomp) ++ex_u; else ++ex_full; }
@@ -683,6 +754,21 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                 fused_n += tmp.fused[k];
                 if (p->nodes[list[k]].kind == NK_RESTRICT && tmp.by_pack[k] && need_full[k]) ++restr_fillers_full;
             }
+            if (std::getenv("HEDL_PLAN_GROUPS"))   // per full-pack group: level dir class lanes (U-only lanes by dir mask)
+                for (const Group &g : groups) {
+                    if (g.kind != NK_RESTRICT || !g.slice || g.ex) continue;
+                    uint32_t byu[16] = {0}, nfr = 0;
+                    const CNode &n0 = p->nodes[list[members[g.first]]];
+                    for (uint32_t m = g.first; m < g.first + g.count; ++m) {
+                        const uint32_t q = members[m];
+                        if (need_full[q]) ++nfr; else byu[tmp.u_out[q] & 15]++;
+                    }
+                    std::fprintf(stderr, "[hedl group] level %u dir %u lanes %u full %u U-only by mask:", n0.level, g.key,
+                                 g.count, nfr);
+                    for (int b = 1; b < 16; ++b) if (byu[b]) std::fprintf(stderr, " %x:%u", b, byu[b]);
+                    std::fprintf(stderr, "\n");
+                }
+            std::fprintf(stderr, "[hedl plan] U sweeps %llu\n", (unsigned long long)swept);
             std::fprintf(stderr, "[hedl plan] restrict: full-pack %llu (full row %llu, U rows only %llu), EX over U %llu, "
                                  "EX over full rows %llu, per-node %llu; bool: full %llu, projected %llu, U %llu, fused %llu; "
                                  "restrictions read in full by packs %llu\n",
@@ -798,7 +884,7 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                     rd.op_first = rd.op_n = 0;
                     rd.uout = nullptr;
                     rd.udirs = rd.pad_ = 0;
-                    if (u_out[k]) {                          // full pack: U rows from the epilogue
+                    if (u_out[k] && g.usw < 0) {             // full pack: U rows from the epilogue
                         rd.uout = urow_of(k, __builtin_ctzll(u_out[k]));
                         rd.udirs = (uint32_t)u_out[k];
                     }
@@ -824,6 +910,7 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
                     rd.n = n.n;
                     rd.sat = n.sat;
                     rd.cover = cover_of_node[k];
+                    if (g.usw >= 0) rd.proj = urow_of(k, g.usw);   // U sweep: the U row is its output
                     rd.heavy_slot = (m - g.first) * dr.n_heavy;
                     hr[base + (m - g.first)] = rd;
                     T.bytes += 4.0 * (kb->N + 1) + 4.0 * (dr.E - dr.E_heavy) +
@@ -880,6 +967,7 @@ void fill_chunk(const hedl_kb *kb, hedl_program *p, const std::vector<uint32_t> 
         LaunchRec lr{g.kind, g.key, g.slice, g.proj, g.ex, g.count, tmp.gdesc[gi], 0, 0};
         lr.usp = g.usp;
         lr.ucomp = g.ucomp;
+        lr.usw = g.usw;
         cp.recs.push_back(lr);
     }
     for (const Task &T : tasks) {
@@ -931,7 +1019,7 @@ hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, u
                 hedl_status st = slice_run(kb, &w->slice.p, &w->slice.bytes, s, kd, lr.key,
                                            lr.cls >= 0 ? nullptr : (const RestrictDesc *)(h + cp.off_res) + lr.first_desc,
                                            dd_desc, lr.count, cov, lr.ex, lr.cls, lr.ucomp,
-                                           (const Operand *)(d + cp.off_ops));
+                                           (const Operand *)(d + cp.off_ops), lr.usw);
                 if (st) return st;
             } else {
                 DirDev dd{dr.row_ptr, dr.col, dr.heavy_x, dr.heavy_nchunks, dr.chunks, dr.n_heavy, dr.n_chunks,
@@ -1053,7 +1141,7 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
             cp.ri = ranges[c].first;
             cp.rc = ranges[c].second;
             fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, !(eflags & HEDL_EVAL_NO_FUSE),
-                       !(eflags & HEDL_EVAL_NO_RESTRICT_U), nullptr, nullptr, nullptr,
+                       !(eflags & HEDL_EVAL_NO_RESTRICT_U), !(eflags & HEDL_EVAL_NO_USWEEP), nullptr, nullptr, nullptr,
                        local, nullptr, &cursor,
                        &heavy_need, true, tmps[c]);
             max_nn = std::max<size_t>(max_nn, cp.nrows);
@@ -1088,7 +1176,7 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
             ChunkPlan &cp = pc.chunks[c];
             size_t cur = cp.blob_off;
             fill_chunk(kb, p, lists[c], cp, bits, use_slice, force, !(eflags & HEDL_EVAL_NO_FUSE),
-                       !(eflags & HEDL_EVAL_NO_RESTRICT_U), (uint32_t *)w->rows.p,
+                       !(eflags & HEDL_EVAL_NO_RESTRICT_U), !(eflags & HEDL_EVAL_NO_USWEEP), (uint32_t *)w->rows.p,
                        (uint32_t *)w->prows.p,
                        (uint32_t *)w->urows.p, local, (char *)pc.host, &cur, &heavy_need, false, tmps[c]);
             tmps[c] = ChunkTmp();   // release the chunk's planning state
@@ -1354,7 +1442,7 @@ extern "C" hedl_status hedl_program_workspace_bytes(const hedl_kb *kb, hedl_prog
             cp.ri = ranges[c].first;
             cp.rc = ranges[c].second;
             fill_chunk(kb, p, lists[c], cp, with_bits != 0, use_slice, eflags & HEDL_EVAL_FORCE_SLICE,
-                       !(eflags & HEDL_EVAL_NO_FUSE), !(eflags & HEDL_EVAL_NO_RESTRICT_U), nullptr, nullptr,
+                       !(eflags & HEDL_EVAL_NO_FUSE), !(eflags & HEDL_EVAL_NO_RESTRICT_U), !(eflags & HEDL_EVAL_NO_USWEEP), nullptr, nullptr,
                        nullptr, local, nullptr, &cursor, &heavy_need, true, tmp);
             max_nn = std::max<size_t>(max_nn, cp.nrows);
             max_np = std::max<size_t>(max_np, cp.nprows);

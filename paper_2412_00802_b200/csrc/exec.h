@@ -20,6 +20,7 @@ struct LaunchRec {
     int8_t cls = -1;       // lane-pack class of the whole group (device plans), -1 = per descriptor
     int16_t usp = -1;      // boolean group over U of direction usp
     bool ucomp = false;    // EX pack reading its fillers' U rows
+    int8_t usw = -1;       // U-sweep pack (rows of U_usw only)
 };
 
 struct ChunkPlan {

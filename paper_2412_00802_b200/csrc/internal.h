@@ -37,6 +37,7 @@ constexpr uint32_t kHeavyDeg = 512;
 constexpr uint32_t kMidDeg = 128;     // lane-packed sweep: medium rows up to this degree go 4 per warp
 constexpr uint32_t kHeavyChunk = 4096;
 constexpr uint32_t kTopKMax = 4096;       // hedl_score_topk: k <= this
+constexpr uint32_t kMaxUDirs = 4;         // role directions whose U rows restrictions can emit / U sweeps
 
 // ---- restriction predicates ---------------------------------------------------
 // Every role restriction counts the neighbours y of x whose (possibly
@@ -73,6 +74,19 @@ struct CNode {
 }  // namespace hedl
 
 // ---- handles -------------------------------------------------------------------
+// a row subset of one direction's CSR, in the layout of the example-row (EX) sweep: rows
+// ("ranks") in blocks of 128, medium then light rows per block by degree, heavy rows in
+// 4,096-edge chunks, neighbours as individual ids
+struct hedl_rowset {
+    uint32_t n_rows = 0, n_blocks = 0, n_heavy = 0, n_chunks = 0;
+    uint64_t E = 0, E_heavy = 0;
+    double frac = 1.0;                             // (E + E_heavy) / the direction's E: sweep cost ratio
+    uint32_t *rp = nullptr, *col = nullptr;        // device [n_rows+1], [E + E_heavy]
+    uint4 *tiles = nullptr;                        // device [n_blocks+1] {order begin, n_med, n_light, heavy begin}
+    uint32_t *order = nullptr, *hx = nullptr, *hrank = nullptr, *hn = nullptr;
+    uint4 *chunks = nullptr;
+};
+
 struct hedl_dir {                  // one role direction
     uint32_t *row_ptr = nullptr;   // device [N+1]
     uint32_t *col = nullptr;       // device [E], sorted per row
@@ -117,6 +131,9 @@ struct hedl_dir {                  // one role direction
     uint32_t *uconcepts = nullptr;     // device [C][UW4]
     uint32_t *uones = nullptr;         // device [UW4], tail-masked TOP row over U
     uint32_t *ulist = nullptr;         // device [n_u]: the members of U in order (U position -> individual)
+    // U sweeps: this direction's rows restricted to U_d' (for restrictions needed only over
+    // one U_d'), per d' < kMaxUDirs (empty without examples or with more directions)
+    hedl_rowset usw[hedl::kMaxUDirs];
 };
 
 struct hedl_data {
@@ -271,7 +288,7 @@ void timing_note(const char *what, double ms);
 
 // ---- profiling -----------------------------------------------------------------
 enum KClass { KC_BOOL, KC_RESTRICT, KC_HEAVY, KC_DRANGE, KC_COVER_INIT, KC_GATHER,
-              KC_SLICE_IN, KC_SLICE, KC_SLICE_HEAVY, KC_KB, KC_SLICE_EX, KC_INTERP, KC_STRING, KC_BOOL_L2, KC_N };
+              KC_SLICE_IN, KC_SLICE, KC_SLICE_HEAVY, KC_KB, KC_SLICE_EX, KC_INTERP, KC_STRING, KC_BOOL_L2, KC_SLICE_U, KC_N };
 extern const char *kKClassName[KC_N];
 void prof_begin(cudaStream_t s, int kc);
 void prof_end(cudaStream_t s, int kc, double alg_bytes, double units = 1);
@@ -306,7 +323,7 @@ struct RestrictDesc {
     uint32_t *uout;
     uint32_t udirs, pad_;
 };
-constexpr uint32_t kMaxUDirs = 4;     // role directions whose U rows restrictions can emit
+
 constexpr uint32_t kFuseMaxOps = 4;   // operands of a boolean filler the pack kernel combines
 struct DrangeDesc {
     uint32_t *out;

@@ -306,6 +306,21 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
         if ((s = upload(kb, st, &kb->pneg, pn.data(), pn.size()))) return bail(s);
         if (cudaStreamSynchronize(st) != cudaSuccess) return bail(fail(HEDL_ERR_CUDA, "upload failed"));
     }
+    // U_d per direction (the distinct neighbours of the example rows, in id order): the rows of
+    // the U sweeps, built with every direction below
+    std::vector<std::vector<uint32_t>> ulists;
+    if (kb->M && 2 * R <= kMaxUDirs) {
+        ulists.resize(2 * R);
+        std::vector<uint8_t> mark(N);
+        for (uint32_t d = 0; d < 2 * R; ++d) {
+            const HostCSR &h = (d & 1) ? tr[d >> 1] : fw[d >> 1];
+            std::fill(mark.begin(), mark.end(), 0);
+            for (uint32_t x : kb->h_ex)
+                for (uint32_t e = h.row_ptr[x]; e < h.row_ptr[x + 1]; ++e) mark[h.col[e]] = 1;
+            for (uint32_t y = 0; y < N; ++y)
+                if (mark[y]) ulists[d].push_back(y);
+        }
+    }
     kb->dirs.resize(2 * R);
     kb->dir_bytes.resize(2 * R);
     for (uint32_t r = 0; r < R; ++r) {
@@ -512,6 +527,64 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
                 if ((s = upload(kb, st, &dr.ex_hrank, ehr.data(), ehr.size()))) return bail(s);
                 if ((s = upload(kb, st, &dr.ex_hn, ehn.data(), ehn.size()))) return bail(s);
                 if ((s = upload(kb, st, &dr.ex_chunks, ech.data(), ech.size()))) return bail(s);
+                if (cudaStreamSynchronize(st) != cudaSuccess) return bail(fail(HEDL_ERR_CUDA, "upload failed"));
+            }
+            // U sweeps of this direction: its rows restricted to U_d' for every d'
+            for (uint32_t du = 0; du < ulists.size(); ++du) {
+                const std::vector<uint32_t> &rows = ulists[du];
+                hedl_rowset &rs = dr.usw[du];
+                const uint32_t n = (uint32_t)rows.size();
+                rs.n_rows = n;
+                rs.n_blocks = (n + 127) / 128;
+                std::vector<uint32_t> rp(n + 1, 0), cl;
+                for (uint32_t q = 0; q < n; ++q) rp[q + 1] = rp[q] + (h.row_ptr[rows[q] + 1] - h.row_ptr[rows[q]]);
+                cl.reserve(rp[n]);
+                for (uint32_t q = 0; q < n; ++q)
+                    for (uint32_t e = h.row_ptr[rows[q]]; e < h.row_ptr[rows[q] + 1]; ++e) cl.push_back(h.col[e]);
+                std::vector<uint4> tb(rs.n_blocks + 1), chs;
+                std::vector<uint32_t> ord, rhx, rhr, rhn, med, light;
+                auto deg = [&](uint32_t q) { return rp[q + 1] - rp[q]; };
+                for (uint32_t b = 0; b < rs.n_blocks; ++b) {
+                    med.clear();
+                    light.clear();
+                    tb[b].w = (uint32_t)rhx.size();
+                    for (uint32_t q = b * 128; q < std::min(n, b * 128 + 128); ++q) {
+                        const uint32_t dq = deg(q);
+                        if (dq > kHeavyDeg) {
+                            const uint32_t hi = (uint32_t)rhx.size();
+                            rhx.push_back(rows[q]);
+                            rhr.push_back(q);
+                            uint32_t nc = 0;
+                            for (uint32_t e = rp[q]; e < rp[q + 1]; e += kHeavyChunk, ++nc)
+                                chs.push_back(make_uint4(hi, e, std::min(rp[q + 1], e + kHeavyChunk), 0));
+                            rhn.push_back(nc);
+                            rs.E_heavy += dq;
+                        } else {
+                            (dq > kLightDeg ? med : light).push_back(q);
+                            rs.E += dq;
+                        }
+                    }
+                    auto by_deg = [&](uint32_t a, uint32_t c) { return deg(a) != deg(c) ? deg(a) > deg(c) : a < c; };
+                    std::sort(med.begin(), med.end(), by_deg);
+                    std::sort(light.begin(), light.end(), by_deg);
+                    tb[b].x = (uint32_t)ord.size();
+                    tb[b].y = (uint32_t)med.size();
+                    tb[b].z = (uint32_t)light.size();
+                    ord.insert(ord.end(), med.begin(), med.end());
+                    ord.insert(ord.end(), light.begin(), light.end());
+                }
+                tb[rs.n_blocks] = make_uint4((uint32_t)ord.size(), 0, 0, (uint32_t)rhx.size());
+                rs.n_heavy = (uint32_t)rhx.size();
+                rs.n_chunks = (uint32_t)chs.size();
+                rs.frac = h.col.empty() ? 1.0 : (double)(rs.E + rs.E_heavy) / (double)h.col.size();
+                if ((s = upload(kb, st, &rs.rp, rp.data(), rp.size()))) return bail(s);
+                if ((s = upload(kb, st, &rs.col, cl.data(), cl.size()))) return bail(s);
+                if ((s = upload(kb, st, &rs.tiles, tb.data(), tb.size()))) return bail(s);
+                if ((s = upload(kb, st, &rs.order, ord.data(), ord.size()))) return bail(s);
+                if ((s = upload(kb, st, &rs.hx, rhx.data(), rhx.size()))) return bail(s);
+                if ((s = upload(kb, st, &rs.hrank, rhr.data(), rhr.size()))) return bail(s);
+                if ((s = upload(kb, st, &rs.hn, rhn.data(), rhn.size()))) return bail(s);
+                if ((s = upload(kb, st, &rs.chunks, chs.data(), chs.size()))) return bail(s);
                 if (cudaStreamSynchronize(st) != cudaSuccess) return bail(fail(HEDL_ERR_CUDA, "upload failed"));
             }
             dr.n_heavy = (uint32_t)hx.size();

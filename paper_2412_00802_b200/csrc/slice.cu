@@ -979,6 +979,7 @@ SliceLayout slice_layout(const hedl_kb *kb) {
     for (const hedl_dir &x : kb->dirs) {
         L.nh = std::max<size_t>(L.nh, x.n_heavy);
         L.nhx = std::max<size_t>(L.nhx, x.n_ex_heavy);
+        for (const hedl_rowset &rs : x.usw) L.nhx = std::max<size_t>(L.nhx, rs.n_heavy);
     }
     const size_t per_h = (LW + 256 + 1 + LW) * 4;
     L.max_batch = (uint32_t)std::max<size_t>(1, std::min<size_t>(128, (4ull << 30) / L.tx_bytes));
@@ -993,7 +994,7 @@ size_t slice_ws_bytes(const hedl_kb *kb) { return slice_layout(kb).need; }
 
 hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream_t s, const KbDev &kd, uint32_t dirid,
                       const RestrictDesc *h_desc, const RestrictDesc *d_desc, uint32_t n, hedl_counts *counts, bool ex,
-                      int fixed_cls, bool ucomp, const Operand *d_ops) {
+                      int fixed_cls, bool ucomp, const Operand *d_ops, int usw) {
     const hedl_dir &dr = kb->dirs[dirid];
     if (ex && !kb->M) return HEDL_OK;                     // no examples: nothing to evaluate
     const SliceLayout lay = slice_layout(kb);
@@ -1064,7 +1065,9 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
         // a run of consecutive same-class descriptors: full packs go one pack per launch
         // (T stays L2-resident for the tile sweep); EX packs go up to max_batch per launch
         const uint32_t cls = fixed_cls >= 0 ? (uint32_t)fixed_cls : slice_class(h_desc[off].pred, h_desc[off].n, h_desc[off].sat);
-        const uint32_t cap = ex ? 256u * max_batch : 256u;
+        // U sweeps: full T per pack, as many packs per launch as the T area holds
+        const uint32_t usw_batch = (uint32_t)std::max<size_t>(1, std::min<size_t>(max_batch, off_hf / std::max<size_t>(t_bytes, 1)));
+        const uint32_t cap = ex ? 256u * max_batch : usw >= 0 ? 256u * usw_batch : 256u;
         uint32_t run = 1;
         if (fixed_cls >= 0) run = std::min(n - off, cap);
         else
@@ -1073,10 +1076,12 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
                 ++run;
         const uint32_t packs = (run + 255) / 256;
         const RestrictDesc *dd = d_desc + off;
-        SliceScratch sc = ex ? scratch(off_hx, nhx, max_batch) : scratch(off_hf, nh, 1);
+        SliceScratch sc = (ex || usw >= 0) ? scratch(off_hx, nhx, max_batch) : scratch(off_hf, nh, 1);
         if (ex) {
             sc.h_stride = nhx;
             sc.t_stride = tx_bytes / 16;
+        } else if (usw >= 0) {
+            sc.h_stride = nhx;                            // (t_stride: one full T per pack)
         }
         prof_begin(s, KC_SLICE_IN);
         if (ex && ucomp) {
@@ -1099,6 +1104,32 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
                 for (uint32_t j = 0; j < run; ++j)
                     if (!h_desc[off + j].child) rows_read += (double)(h_desc[off + j].op_n & 0x7fffffffu) - 1.0;
             prof_end(s, KC_SLICE_IN, 4.0 * kb->W * rows_read + 32.0 * (ex ? (double)dr.n_u : 32.0 * kb->W4) * packs, packs);
+        }
+        if (usw >= 0) {
+            // U sweep: the pack's nodes are needed only over U_usw, so only
+            // the rows of U_usw are swept -- the example-row sweep over that row set, writing the
+            // nodes' U rows (RestrictDesc.proj) instead of projected rows
+            const hedl_rowset &rs = dr.usw[usw];
+            const SliceDir su{rs.rp, rs.col, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                              rs.hx, rs.hn, rs.chunks, rs.n_heavy, rs.n_chunks, 0};
+            const ExArgs ua{rs.rp, rs.col, rs.tiles, rs.order, kb->dirs[usw].ulist, rs.hrank, nullptr, nullptr,
+                            kb->dirs[usw].UW4};
+            if (rs.n_chunks) {
+                prof_begin(s, KC_SLICE_HEAVY);
+                if (cls == 0) k_slice_heavy<false><<<dim3(rs.n_chunks, packs), 256, 0, s>>>(su, sc, dd, run);
+                else k_slice_heavy<true><<<dim3(rs.n_chunks, packs), 256, 0, s>>>(su, sc, dd, run);
+                count_launch();
+                prof_end(s, KC_SLICE_HEAVY, 36.0 * rs.E_heavy * packs, packs);
+            }
+            if (rs.n_blocks) {
+                prof_begin(s, KC_SLICE_U);
+                if (cls == 0) k_slice_ex<false><<<dim3(rs.n_blocks, packs), 256, 0, s>>>(ua, sc, dd, run, counts);
+                else k_slice_ex<true><<<dim3(rs.n_blocks, packs), 256, 0, s>>>(ua, sc, dd, run, counts);
+                count_launch();
+                prof_end(s, KC_SLICE_U, (8.0 * rs.n_rows + 36.0 * rs.E) * packs + 4.0 * kb->dirs[usw].UW * run, packs);
+            }
+            off += run;
+            continue;
         }
         const SliceDir &hd = ex ? sdx : sd;
         if (hd.n_chunks) {

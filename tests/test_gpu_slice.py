@@ -16,6 +16,7 @@ FORCE = 4       # HEDL_EVAL_FORCE_SLICE
 PER_NODE = 2    # HEDL_EVAL_PER_NODE
 NO_FUSE = 8     # HEDL_EVAL_NO_FUSE
 NO_RESTRICT_U = 16  # HEDL_EVAL_NO_RESTRICT_U
+NO_USWEEP = 32  # HEDL_EVAL_NO_USWEEP
 
 
 def test_slice_random_tiny():
@@ -28,6 +29,8 @@ def test_slice_random_tiny():
             assert_parity(kb, trees, eflags=FORCE | NO_FUSE, tag=f"slice no-fuse {seed}")
         if seed % 4 == 1:               # no U rows from restrictions: booleans over them in full
             assert_parity(kb, trees, eflags=FORCE | NO_RESTRICT_U, tag=f"slice no-restrict-U {seed}")
+        if seed % 4 == 2:               # U-only restrictions swept over all rows
+            assert_parity(kb, trees, eflags=FORCE | NO_USWEEP, tag=f"slice no-U-sweep {seed}")
         if seed % 10 == 0:
             assert_parity(kb, trees, flags=COMPILE_COMPAT_PAPER_MAX, eflags=FORCE, tag=f"slice compat {seed}")
 
@@ -94,6 +97,7 @@ def test_slice_c4_shape():
     assert_parity(kb, arrays=arrays, tag="slice c4-shape")
     assert_parity(kb, arrays=arrays, eflags=NO_FUSE, tag="slice c4-shape, fillers materialised")
     assert_parity(kb, arrays=arrays, eflags=NO_FUSE | NO_RESTRICT_U, tag="slice c4-shape, round-1 planner")
+    assert_parity(kb, arrays=arrays, eflags=NO_USWEEP, tag="slice c4-shape, no U sweeps")
 
 
 def test_slice_tail_sizes():
