@@ -42,6 +42,7 @@ struct SliceDir {
 // per-direction U masks for the restriction U-row epilogue (directions < kMaxUDirs)
 struct UTab {
     const uint32_t *um[kMaxUDirs], *ub[kMaxUDirs];   // ex_umask / ex_ubase of direction d
+    const uint32_t *ul[kMaxUDirs];                    // ulist of direction d (U position -> individual)
     uint32_t nu[kMaxUDirs];                           // |U_d|
     uint32_t stride;                                  // words between a node's consecutive U rows
 };
@@ -618,8 +619,7 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, half = lane & 1;
     __shared__ uint32_t s_exm[32], s_exb[32];
     __shared__ uint32_t s_tile, s_item;
-    __shared__ uint16_t s_uix[1024];                      // the tile's members of U_d (row indices)
-    __shared__ uint32_t s_unt, s_ubl, s_udirs;
+    __shared__ uint32_t s_udirs;
     // this lane's node for the transpose-back phase (fixed for the whole launch)
     const uint32_t jn = wid * 32 + lane;
     uint32_t *r_out = nullptr, *r_proj = nullptr, *r_uout = nullptr;
@@ -803,47 +803,31 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
         }
         if (pbits) atomicOr(r_proj + pw, pbits);
         // U rows: for each direction d some node of the pack
-        // emits, the tile's members of U_d (the example rows' neighbours in direction d) are
-        // consecutive U positions [bl, bl + k); 32 of them at a time, their result rows (ot) go
-        // through one more warp transpose, and lane j of warp g holds node 32g + j's U word.
-        // Interior U words are written whole, the two seam words shared with the neighbouring
-        // tiles by atomicOr into the zeroed row.
+        // emits, the tile's members of U_d (the example rows' neighbours in direction d) are the
+        // consecutive U positions [bl, bh) whose individuals ulist_d gives; 32 of them at a time,
+        // their result rows (ot) go through one more warp transpose, and lane j of warp g holds
+        // node 32g + j's U word.  Interior U words are written whole, the two seam words shared
+        // with the neighbouring tiles by atomicOr into the zeroed row.  (No block barrier: ot is
+        // stable until the next tile's first __syncthreads.)
 #pragma unroll
         for (uint32_t dd = 0; dd < kMaxUDirs; ++dd) {
             if (!((s_udirs >> dd) & 1u)) continue;                        // block-uniform
-            if (wid == 0) {                                               // member list of the tile
-                const uint32_t w = t * 32 + lane;
-                const uint32_t m = w < kb.W4 ? __ldg(ut.um[dd] + w) : 0u;
-                const uint32_t c = __popc(m);
-                uint32_t pre = c;
-#pragma unroll
-                for (int o2 = 1; o2 < 32; o2 <<= 1) {
-                    const uint32_t v = __shfl_up_sync(FULL, pre, o2);
-                    if (lane >= (uint32_t)o2) pre += v;
-                }
-                uint32_t at = pre - c;
-                for (uint32_t mm = m; mm; mm &= mm - 1) s_uix[at++] = (uint16_t)(lane * 32 + __ffs(mm) - 1);
-                if (lane == 31) s_unt = pre;
-                if (lane == 0) s_ubl = __ldg(ut.ub[dd] + t * 32);
-            }
-            __syncthreads();
-            const uint32_t k = s_unt, bl = s_ubl;
-            if (k) {
-                const bool mine = live && ((r_udirs >> dd) & 1u);
-                uint32_t *urow = mine ? r_uout + __popc(r_udirs & ((1u << dd) - 1u)) * ut.stride : nullptr;
-                const uint32_t c0 = bl >> 5, c1 = (bl + k - 1) >> 5;
-                for (uint32_t cw = c0; cw <= c1; ++cw) {
-                    const int32_t idx = (int32_t)(cw * 32 + lane) - (int32_t)bl;
-                    const uint32_t v = (idx >= 0 && (uint32_t)idx < k) ? ot[(uint32_t)s_uix[idx] * TROW + g] : 0u;
-                    const uint32_t x = warp_transpose(v, lane);
-                    if (mine) {
-                        const bool seam = (cw == c0 && (bl & 31)) || (cw == c1 && ((bl + k) & 31));
-                        if (seam) { if (x) atomicOr(urow + cw, x); }
-                        else urow[cw] = x;
-                    }
+            const uint32_t bl = __ldg(ut.ub[dd] + t * 32);
+            const uint32_t bh = t * 32 + 32 < kb.W4 ? __ldg(ut.ub[dd] + t * 32 + 32) : ut.nu[dd];
+            if (bh <= bl) continue;
+            const bool mine = live && ((r_udirs >> dd) & 1u);
+            uint32_t *urow = mine ? r_uout + __popc(r_udirs & ((1u << dd) - 1u)) * ut.stride : nullptr;
+            const uint32_t c0 = bl >> 5, c1 = (bh - 1) >> 5;
+            for (uint32_t cw = c0; cw <= c1; ++cw) {
+                const uint32_t pos = cw * 32 + lane;
+                const uint32_t v = (pos >= bl && pos < bh) ? ot[(__ldg(ut.ul[dd] + pos) - x0) * TROW + g] : 0u;
+                const uint32_t x = warp_transpose(v, lane);
+                if (mine) {
+                    const bool seam = (cw == c0 && (bl & 31)) || (cw == c1 && (bh & 31));
+                    if (seam) { if (x) atomicOr(urow + cw, x); }
+                    else urow[cw] = x;
                 }
             }
-            __syncthreads();                                              // before the list is rebuilt
         }
     }
     // coverage of this CTA's tiles, one atomic set per node per CTA
@@ -1180,6 +1164,7 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
                 ut.um[q] = kb->dirs[q].ex_umask;
                 ut.ub[q] = kb->dirs[q].ex_ubase;
                 ut.nu[q] = kb->dirs[q].n_u;
+                ut.ul[q] = kb->dirs[q].ulist;
             }
             if (cls == 0) k_slice_tile<false><<<grid, 256, smem, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
             else k_slice_tile<true><<<grid, 256, smem, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
