@@ -123,6 +123,7 @@ const char *kKClassName[KC_N] = {"bool", "restrict", "restrict_heavy", "drange",
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void count_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 uint64_t launches_total() { return g_launches.load(); }
 static std::atomic<uint64_t> g_h2d{0}, g_d2h{0};
 void count_io(uint64_t h2d, uint64_t d2h) {
@@ -151,6 +152,8 @@ static cudaEvent_t get_event() {
     cudaEventCreate(&e);
     return e;
 }
+
+bool prof_active() { return g_prof_on; }
 
 void prof_begin(cudaStream_t s, int) {
     if (!g_prof_on) return;

@@ -524,8 +524,7 @@ hedl_status dplan_run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t 
                      pc.urows_base == w->urows.p;
     hedl_status st;
     if (hit) {
-        for (const ChunkPlan &cp : pc.chunks)
-            if ((st = launch_chunk(kb, w, cp, r0, out_bits, counts_dev, s))) return st;
+        if ((st = replay_plan(kb, w, r0, out_bits, counts_dev, s))) return st;
     } else {
         if (w->used && w->done) HEDL_CUDA(kb, cudaEventSynchronize(w->done));
         invalidate_plan(pc);

@@ -72,12 +72,84 @@ hedl_status grow(const hedl_kb *kb, cudaStream_t s, DevBuf &b, size_t need, bool
     return HEDL_OK;
 }
 
+void drop_graph(PlanCache &pc) {
+    if (pc.graph) cudaGraphExecDestroy(pc.graph);
+    pc.graph = nullptr;
+    pc.g_counts = pc.g_bits = nullptr;
+    pc.g_calls = 0;
+}
+
 void invalidate_plan(PlanCache &pc) {
     pc.valid = false;
     pc.chunks.clear();
+    drop_graph(pc);
+}
+
+// Replays of a cached plan go through a CUDA graph of its launches (captured on the second
+// replay with the same output buffers; the plan's descriptors, workspace and outputs are all
+// fixed addresses then), on the library's own stream between two events.  Not while library
+// profiling is on (its events are per launch), not with HEDL_NO_GRAPH set; a failed capture
+// falls back to plain launches on the caller's stream.
+hedl_status replay_plan(const hedl_kb *kb, Workspace *w, uint32_t r0, uint32_t *out_bits, hedl_counts *counts_dev,
+                        cudaStream_t s) {
+    PlanCache &pc = w->plan;
+    static const bool no_graph = std::getenv("HEDL_NO_GRAPH") != nullptr;
+    hedl_status st = HEDL_OK;
+    auto direct = [&](cudaStream_t on) -> hedl_status {
+        for (const ChunkPlan &cp : pc.chunks)
+            if ((st = launch_chunk(kb, w, cp, r0, out_bits, counts_dev, on))) return st;
+        return HEDL_OK;
+    };
+    if (no_graph || prof_active()) return direct(s);
+    if (pc.g_counts != counts_dev || pc.g_bits != out_bits) {
+        drop_graph(pc);
+        pc.g_counts = counts_dev;
+        pc.g_bits = out_bits;
+    }
+    if (!pc.graph && ++pc.g_calls < 2) return direct(s);    // capture once the outputs repeat
+    if (!pc.gstream) {
+        if (cudaStreamCreateWithFlags(&pc.gstream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&pc.gev_in, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&pc.gev_out, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            return direct(s);
+        }
+    }
+    HEDL_CUDA(kb, cudaEventRecord(pc.gev_in, s));
+    HEDL_CUDA(kb, cudaStreamWaitEvent(pc.gstream, pc.gev_in, 0));
+    if (!pc.graph) {
+        cudaGraph_t g = nullptr;
+        if (cudaStreamBeginCapture(pc.gstream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+            cudaGetLastError();
+            return direct(s);
+        }
+        const uint64_t l0 = launches_total();
+        const hedl_status cs = direct(pc.gstream);
+        const cudaError_t ce = cudaStreamEndCapture(pc.gstream, &g);
+        pc.g_launches = launches_total() - l0;
+        cudaGraphExec_t ex = nullptr;
+        const bool ok = !cs && ce == cudaSuccess && g && cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
+        if (g) cudaGraphDestroy(g);
+        if (!ok) {
+            cudaGetLastError();
+            pc.g_calls = 0;
+            return direct(s);
+        }
+        pc.graph = ex;
+    } else {
+        count_launches(pc.g_launches);
+    }
+    HEDL_CUDA(kb, cudaGraphLaunch(pc.graph, pc.gstream));
+    HEDL_CUDA(kb, cudaEventRecord(pc.gev_out, pc.gstream));
+    HEDL_CUDA(kb, cudaStreamWaitEvent(s, pc.gev_out, 0));
+    return HEDL_OK;
 }
 
 void release_plan(PlanCache &pc) {
+    drop_graph(pc);
+    if (pc.gstream) cudaStreamDestroy(pc.gstream);
+    if (pc.gev_in) cudaEventDestroy(pc.gev_in);
+    if (pc.gev_out) cudaEventDestroy(pc.gev_out);
     if (pc.host) cudaFreeHost(pc.host);
     if (pc.dev) dev_free(pc.dev);
     pc = PlanCache();
@@ -1192,8 +1264,7 @@ hedl_status run(const hedl_kb *kb, hedl_program *p, uint32_t r0, uint32_t r1, ui
         timing_note("plan: fill+upload+launch", now_ms() - t2);
     } else {
         if ((st = ensure_stage())) return st;
-        for (const ChunkPlan &cp : pc.chunks)
-            if ((st = launch_chunk(kb, w, cp, r0, out_bits, *counts_io, s))) return st;
+        if ((st = replay_plan(kb, w, r0, out_bits, *counts_io, s))) return st;
     }
     if (!w->done) HEDL_CUDA(kb, cudaEventCreateWithFlags(&w->done, cudaEventDisableTiming));
     HEDL_CUDA(kb, cudaEventRecord(w->done, s));

@@ -42,6 +42,16 @@ struct PlanCache {
     void *dev = nullptr;                  // device descriptor blob
     size_t cap = 0;                       // capacity of both blobs
     size_t host_cap = 0;                  // capacity of the host blob (caller-workspace mode)
+    // the plan's launches captured as a CUDA graph (replayed by later calls with the same
+    // output buffers): one graph launch instead of ~250 kernel launches per C4 step
+    cudaGraphExec_t graph = nullptr;
+    const void *g_counts = nullptr, *g_bits = nullptr;
+    uint32_t g_calls = 0;                 // replays seen: capture from the second one on
+    uint64_t g_launches = 0;              // kernels in the graph (the launch counter's share)
+    // the graph runs on the library's own stream, ordered after / before the caller's stream by
+    // events (the legacy default stream a caller usually passes cannot be captured)
+    cudaStream_t gstream = nullptr;
+    cudaEvent_t gev_in = nullptr, gev_out = nullptr;
 };
 
 struct Workspace {
@@ -68,6 +78,10 @@ void release_plan(PlanCache &pc);
 hedl_status reserve_plan(const hedl_kb *kb, PlanCache &pc, size_t bytes, Workspace *w = nullptr);
 hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, uint32_t r0, uint32_t *out_bits,
                          hedl_counts *counts_dev, cudaStream_t s);
+// the launches of a valid plan: its captured graph when possible, else launch_chunk per chunk
+hedl_status replay_plan(const hedl_kb *kb, Workspace *w, uint32_t r0, uint32_t *out_bits, hedl_counts *counts_dev,
+                        cudaStream_t s);
+void drop_graph(PlanCache &pc);
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 // scratch of a per-node restriction group of `count` nodes in direction `dir`: the heavy-row
 // counters, then (small groups on large KBs) the push-direction scratch of each node

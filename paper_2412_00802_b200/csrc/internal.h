@@ -291,6 +291,7 @@ enum KClass { KC_BOOL, KC_RESTRICT, KC_HEAVY, KC_DRANGE, KC_COVER_INIT, KC_GATHE
               KC_SLICE_IN, KC_SLICE, KC_SLICE_HEAVY, KC_KB, KC_SLICE_EX, KC_INTERP, KC_STRING, KC_BOOL_L2, KC_SLICE_U, KC_N };
 extern const char *kKClassName[KC_N];
 void prof_begin(cudaStream_t s, int kc);
+bool prof_active();
 void prof_end(cudaStream_t s, int kc, double alg_bytes, double units = 1);
 
 // ---- kernels launchers (kernels.cu) -----------------------------------------
@@ -402,6 +403,7 @@ void launch_gather_bits(cudaStream_t s, const uint32_t *const *rows, uint32_t *o
 void launch_kb_build(cudaStream_t s);
 uint64_t launches_total();
 void count_launch();
+void count_launches(uint64_t n);
 void count_io(uint64_t h2d, uint64_t d2h);
 
 }  // namespace hedl
