@@ -157,62 +157,91 @@ __global__ void __launch_bounds__(256) k_bool(KbDev kb, const BoolDesc *__restri
 // (the node is never split across warps, so no atomics).
 constexpr uint32_t kBoolWarpMaxN4 = 1024;     // rows up to 4,096 words
 
+#ifndef HEDL_BOOLW_MINB
+#define HEDL_BOOLW_MINB 4
+#endif
 template <bool FULL_ROWS>
-__global__ void __launch_bounds__(256) k_bool_warp(KbDev kb, const BoolDesc *__restrict__ descs, uint32_t n_desc,
+__global__ void __launch_bounds__(256, HEDL_BOOLW_MINB) k_bool_warp(KbDev kb, const BoolDesc *__restrict__ descs, uint32_t n_desc,
                                                    const Operand *__restrict__ ops, hedl_counts *counts,
                                                    uint64_t npos, uint64_t nneg) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t n4 = kb.W4 >> 2;
-    for (uint32_t k = blockIdx.x * 8 + (threadIdx.x >> 5); k < n_desc; k += gridDim.x * 8) {
-        const BoolDesc d = descs[k];
-        uint32_t tp = 0, fp = 0;
-        // operand descriptors fetched together up front (no dependent descriptor load per
-        // word); the same one-LOP3 form as k_bool (AND = complemented OR of complements)
-        const uint32_t flip = d.is_or ? 0u : FULL;
-        Operand o4[4];
+    const uint32_t stride = gridDim.x * 8;
+    uint32_t k = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (k >= n_desc) return;
+    // a node's descriptor and its first four operand descriptors are fetched while the warp
+    // works on the previous node (the dependent descriptor loads leave the critical path)
+    BoolDesc d = descs[k];
+    Operand o4[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) o4[j] = (uint32_t)j < d.op_count ? ops[d.op_first + j] : Operand{nullptr, 0u, 0u};
-        for (uint32_t i = lane; i < n4; i += 32) {
-            uint4 acc = make_uint4(0, 0, 0, 0);
+    for (int j = 0; j < 4; ++j) o4[j] = (uint32_t)j < d.op_count ? ops[d.op_first + j] : Operand{nullptr, 0u, 0u};
+    for (; k < n_desc; k += stride) {
+        const uint32_t kn = k + stride;
+        BoolDesc dn{};
+        if (kn < n_desc) dn = descs[kn];
+        uint32_t tp = 0, fp = 0;
+        // the same one-LOP3 form as k_bool (AND = complemented OR of complements); two uint4
+        // per lane in flight per operand
+        const uint32_t flip = d.is_or ? 0u : FULL;
+        for (uint32_t i0 = lane; i0 < n4; i0 += 64) {
+            uint4 acc[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+            const bool two = i0 + 32 < n4;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 if ((uint32_t)j >= d.op_count) break;
-                const uint4 v = __ldg(reinterpret_cast<const uint4 *>(o4[j].ptr) + i);
+                const uint4 *src = reinterpret_cast<const uint4 *>(o4[j].ptr);
+                const uint4 v0 = __ldg(src + i0);
+                const uint4 v1 = two ? __ldg(src + i0 + 32) : make_uint4(0, 0, 0, 0);
                 const uint32_t m = o4[j].mask ^ flip;
-                acc.x |= v.x ^ m; acc.y |= v.y ^ m; acc.z |= v.z ^ m; acc.w |= v.w ^ m;
+                acc[0].x |= v0.x ^ m; acc[0].y |= v0.y ^ m; acc[0].z |= v0.z ^ m; acc[0].w |= v0.w ^ m;
+                acc[1].x |= v1.x ^ m; acc[1].y |= v1.y ^ m; acc[1].z |= v1.z ^ m; acc[1].w |= v1.w ^ m;
             }
             for (uint32_t j = 4; j < d.op_count; ++j) {
                 const Operand o = ops[d.op_first + j];
-                const uint4 v = __ldg(reinterpret_cast<const uint4 *>(o.ptr) + i);
+                const uint4 *src = reinterpret_cast<const uint4 *>(o.ptr);
+                const uint4 v0 = __ldg(src + i0);
+                const uint4 v1 = two ? __ldg(src + i0 + 32) : make_uint4(0, 0, 0, 0);
                 const uint32_t m = o.mask ^ flip;
-                acc.x |= v.x ^ m; acc.y |= v.y ^ m; acc.z |= v.z ^ m; acc.w |= v.w ^ m;
+                acc[0].x |= v0.x ^ m; acc[0].y |= v0.y ^ m; acc[0].z |= v0.z ^ m; acc[0].w |= v0.w ^ m;
+                acc[1].x |= v1.x ^ m; acc[1].y |= v1.y ^ m; acc[1].z |= v1.z ^ m; acc[1].w |= v1.w ^ m;
             }
-            acc.x ^= flip; acc.y ^= flip; acc.z ^= flip; acc.w ^= flip;
-            const uint32_t w0 = i << 2;
-            if (w0 + 4 >= kb.W) {                          // the uint4 holding word W-1 and later
-                acc.x = tail_word(acc.x, w0, kb.W, kb.N);
-                acc.y = tail_word(acc.y, w0 + 1, kb.W, kb.N);
-                acc.z = tail_word(acc.z, w0 + 2, kb.W, kb.N);
-                acc.w = tail_word(acc.w, w0 + 3, kb.W, kb.N);
-            }
-            if (d.out) reinterpret_cast<uint4 *>(d.out)[i] = acc;
-            if (d.proj) {
-                proj_scatter(kb, d.proj, w0, acc.x);
-                proj_scatter(kb, d.proj, w0 + 1, acc.y);
-                proj_scatter(kb, d.proj, w0 + 2, acc.z);
-                proj_scatter(kb, d.proj, w0 + 3, acc.w);
-            }
-            if (d.cover >= 0) {
-                const uint4 p = __ldg(reinterpret_cast<const uint4 *>(kb.pos) + i);
-                const uint4 q = __ldg(reinterpret_cast<const uint4 *>(kb.neg) + i);
-                tp += __popc(acc.x & p.x) + __popc(acc.y & p.y) + __popc(acc.z & p.z) + __popc(acc.w & p.w);
-                fp += __popc(acc.x & q.x) + __popc(acc.y & q.y) + __popc(acc.z & q.z) + __popc(acc.w & q.w);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t i = i0 + 32 * h;
+                if (h && !two) break;
+                uint4 a = acc[h];
+                a.x ^= flip; a.y ^= flip; a.z ^= flip; a.w ^= flip;
+                const uint32_t w0 = i << 2;
+                if (w0 + 4 >= kb.W) {                      // the uint4 holding word W-1 and later
+                    a.x = tail_word(a.x, w0, kb.W, kb.N);
+                    a.y = tail_word(a.y, w0 + 1, kb.W, kb.N);
+                    a.z = tail_word(a.z, w0 + 2, kb.W, kb.N);
+                    a.w = tail_word(a.w, w0 + 3, kb.W, kb.N);
+                }
+                if (d.out) reinterpret_cast<uint4 *>(d.out)[i] = a;
+                if (d.proj) {
+                    proj_scatter(kb, d.proj, w0, a.x);
+                    proj_scatter(kb, d.proj, w0 + 1, a.y);
+                    proj_scatter(kb, d.proj, w0 + 2, a.z);
+                    proj_scatter(kb, d.proj, w0 + 3, a.w);
+                }
+                if (d.cover >= 0) {
+                    const uint4 p = __ldg(reinterpret_cast<const uint4 *>(kb.pos) + i);
+                    const uint4 q = __ldg(reinterpret_cast<const uint4 *>(kb.neg) + i);
+                    tp += __popc(a.x & p.x) + __popc(a.y & p.y) + __popc(a.z & p.z) + __popc(a.w & p.w);
+                    fp += __popc(a.x & q.x) + __popc(a.y & q.y) + __popc(a.z & q.z) + __popc(a.w & q.w);
+                }
             }
         }
         if (d.cover >= 0) {
             tp = __reduce_add_sync(FULL, tp);
             fp = __reduce_add_sync(FULL, fp);
             if (lane == 0) counts[d.cover] = hedl_counts{tp, fp, npos - tp, nneg - fp};
+        }
+        if (kn < n_desc) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o4[j] = (uint32_t)j < dn.op_count ? ops[dn.op_first + j] : Operand{nullptr, 0u, 0u};
+            d = dn;
         }
     }
 }

@@ -2,7 +2,7 @@
 # Same-box A/B of libhedl.so variants: ab/<name>/libhedl.so vs the in-tree build, run in
 # ABAB order (kernel-only bench, 5 timed steps), then the slice parity tests per variant.
 # Usage: bash tools/ab.sh name [name ...]
-B="python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-latency"
+B="python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-latency --no-c5"
 LIB=paper_2412_00802_b200/libhedl.so
 cp $LIB /tmp/base.so
 for rep in 1 2; do
