@@ -33,16 +33,11 @@ def bfs_order(kb):
     s, o = kb["edge_subj"].astype(np.int64), kb["edge_obj"].astype(np.int64)
     A = sp.csr_matrix((np.ones(2 * len(s), np.int8), (np.concatenate([s, o]), np.concatenate([o, s]))), shape=(N, N))
     deg = np.diff(A.indptr)
+    by_deg = np.argsort(-deg, kind="stable")
+    comp = breadth_first_order(A, int(by_deg[0]), directed=False, return_predecessors=False)
     seen = np.zeros(N, bool)
-    out = []
-    for v in np.argsort(-deg, kind="stable"):
-        if seen[v]:
-            continue
-        comp = breadth_first_order(A, v, directed=False, return_predecessors=False)
-        comp = comp[~seen[comp]]
-        seen[comp] = True
-        out.append(comp)
-    return np.concatenate(out)
+    seen[comp] = True
+    return np.concatenate([comp, by_deg[~seen[by_deg]]])   # the giant component, then the rest by degree
 
 
 def permute_bits(rows, N, order):
