@@ -16,10 +16,13 @@ instance set and TP/FP/FN/TN counts.
           the device (+ the NCCL all_gather of counts at N>1).  Library profiling is OFF in
           this timed region; a second, profiled pass of the same steps gives the per-class
           kernel times (CUDA events on the launch stream) behind `roofline` / `kernels`.
-  e2e   : the same through the public C ABI from HOST arrays every step: hedl_compile_device
-          with HEDL_COMPILE_HOST_INPUT (the H2D of the batch, the GPU-built program and plan,
-          one call), hedl_eval_batch with host counts (D2H).  The host-compile variant
-          (hedl_compile: host canonicalisation + host plan) is reported beside it.
+  e2e   : the same through the public C ABI from page-locked HOST arrays every step: the H2D of
+          the step's batch, hedl_compile_device (the GPU-built program), hedl_eval_batch (device
+          plan + evaluation) and the D2H of the step's counts, as a double-buffered learner loop
+          (step k+1's H2D and compile overlap step k's evaluation; at N = 1).  `e2e.sequential`
+          is one step at a time (hedl_compile_device with HEDL_COMPILE_HOST_INPUT: the H2D inside
+          the call, host counts); the host-compile variant (hedl_compile: host canonicalisation +
+          host plan) is reported beside it.
 `python bench.py --impl reference` times the oracle (the plain C set evaluator) on the same
 workload, on bounded samples (the tier's reference arm).
 """
@@ -127,7 +130,7 @@ def rank_hyps(kind, kb, n_per, rank, args):
 def c4_inputs(args, world):
     """(kb, nodes, kids, roots) of the C4 batch at world size 1 (tests call this)."""
     kb = workload_kb("c4", args)
-    return (kb,) + tuple(rank_hyps("c4", kb, args.n_hyps, 0, args))
+    return (kb,) + tuple(rank_hyps("c4", kb, args.n_hyps or WORKLOADS["c4"]["n_hyps"], 0, args))
 
 
 # ------------------------------------------------------------------------------ clocks
@@ -428,10 +431,77 @@ def run_workload(kind, args, hedl, rank, world, local, steps, warmup, cpu_budget
                     "ms_per_step": 1000.0 * e_loc / n_steps,
                     "step_ms": [round(1000.0 * x, 2) for x in et]}
 
+        def e2e_pipelined(n_steps):
+            """The learner loop double-buffered: step k+1's batch is copied H2D (copy stream) and
+            compiled on the GPU (high-priority stream) while step k evaluates; step k's counts go
+            D2H into page-locked memory (second copy stream) while step k+1 runs.  Every step
+            still moves its own inputs H2D and its counts D2H inside the timed region; the region
+            runs from the first H2D to the last D2H (pipeline fill and drain included)."""
+            s_eval = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+            s_comp = torch.cuda.Stream(device=dev, priority=-1)
+            s_h2d, s_d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+            dbuf = [tuple(torch.empty_like(t, device=dev) for t in (nodes_pin, kids_pin, roots_pin)) for _ in range(2)]
+            cdev = [torch.empty((max(n_loc, 1), 4), dtype=torch.int64, device=dev) for _ in range(2)]
+            chost = [torch.empty((max(n_loc, 1), 4), dtype=torch.int64).pin_memory() for _ in range(2)]
+            ev = lambda: torch.cuda.Event()
+            h2d_done, comp_done, eval_done, d2h_done = ([ev(), ev()] for _ in range(4))
+            bytes_in = sum(t.numel() for t in (nodes_pin, kids_pin, roots_pin))
+
+            def issue_h2d(k):
+                b = k & 1
+                with torch.cuda.stream(s_h2d):
+                    s_h2d.wait_event(comp_done[b])          # compile(k-2) has read this buffer
+                    for dst, src in zip(dbuf[b], (nodes_pin, kids_pin, roots_pin)):
+                        dst.copy_(src, non_blocking=True)
+                    h2d_done[b].record(s_h2d)
+
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            issue_h2d(0)
+            progs = []
+            for k in range(n_steps):
+                b = k & 1
+                if k + 1 < n_steps:
+                    issue_h2d(k + 1)
+                s_comp.wait_event(h2d_done[b])
+                p2 = hedl.hedl_compile_device(kb, *dbuf[b], n_nodes=len(nodes), n_kids=len(kids), n_roots=n_loc,
+                                              stream=s_comp)
+                comp_done[b].record(s_comp)
+                s_eval[b].wait_event(comp_done[b])
+                s_eval[b].wait_event(d2h_done[b])             # counts(k-2) have left this buffer
+                hedl.hedl_eval_batch(kb, p2, 0, n_loc, counts_device=True, out_counts=cdev[b][:n_loc],
+                                     flags=eflags, stream=s_eval[b])
+                eval_done[b].record(s_eval[b])
+                with torch.cuda.stream(s_d2h):
+                    s_d2h.wait_event(eval_done[b])
+                    chost[b].copy_(cdev[b], non_blocking=True)
+                    d2h_done[b].record(s_d2h)
+                progs.append(p2)
+                if len(progs) > 2:                          # its evaluation has finished (host-synced plan of k)
+                    progs.pop(0).free()
+            torch.cuda.synchronize()
+            el = time.perf_counter() - t0
+            for q in progs:
+                q.free()
+            last = chost[(n_steps - 1) & 1][:n_loc]
+            return {"value": total / (el / n_steps), "unit": "hyps/s", "h2d_bytes_per_step": int(bytes_in),
+                    "d2h_bytes_per_step": int(last.numel() * 8), "ms_per_step": 1000.0 * el / n_steps,
+                    "counts_equal_value_program": bool(torch.equal(last, counts_dev[:n_loc].cpu()))}
+
         e2e_steps(True, max(1, warmup))                    # warm-up of the device-compile path
-        e2e = e2e_steps(True, steps)
-        e2e["path"] = ("hedl_compile_device(HEDL_COMPILE_HOST_INPUT: H2D inside the call) + device plan "
-                       "(GPU-generated plans, PAPER.md:872) + hedl_eval_batch (host counts)")
+        seq = e2e_steps(True, steps)
+        seq["path"] = ("hedl_compile_device(HEDL_COMPILE_HOST_INPUT: H2D inside the call) + device plan "
+                       "(GPU-generated plans, PAPER.md:872) + hedl_eval_batch (host counts), one step at a time")
+        if world == 1:
+            e2e_pipelined(max(2, warmup))
+            e2e = e2e_pipelined(steps)
+            e2e["path"] = ("double-buffered learner loop through the C ABI: H2D of step k+1's batch (pinned -> "
+                           "device, copy stream) and hedl_compile_device (device arrays, high-priority stream) "
+                           "overlap step k's device plan + hedl_eval_batch; counts D2H into pinned memory on a "
+                           "second copy stream; timed from the first H2D to the last D2H")
+            e2e["sequential"] = seq
+        else:
+            e2e = seq
         # the learner's step on the GPU: device compile + plan + evaluate + F1 + top-1000,
         # only the top-k indices / scores come back (SURVEY 8(f) NEXT-3)
         if world == 1 and n_loc >= 1000:

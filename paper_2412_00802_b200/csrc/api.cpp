@@ -68,13 +68,19 @@ void live_kb_add(int d) {
 cudaError_t dev_malloc(void **p, size_t bytes, cudaStream_t s) {
     *p = nullptr;
     g_n_alloc.fetch_add(1, std::memory_order_relaxed);
+    const double t0 = timing_enabled() ? now_ms() : 0.0;
+    cudaError_t e;
     if (g_alloc) {
         int dev = 0;
         cudaGetDevice(&dev);
         *p = g_alloc(bytes, dev, (void *)s, g_alloc_ctx);
-        return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+        e = *p ? cudaSuccess : cudaErrorMemoryAllocation;
+    } else {
+        e = cudaMalloc(p, bytes);
     }
-    return cudaMalloc(p, bytes);
+    if (timing_enabled())
+        std::fprintf(stderr, "[hedl timing] dev_malloc %12zu B %9.3f ms\n", bytes, now_ms() - t0);
+    return e;
 }
 
 bool dev_alloc_installed() { return g_alloc != nullptr; }
@@ -96,12 +102,17 @@ static void pool_free_one(int role, void *p) {
     else dev_free(p);
 }
 
+constexpr size_t kPoolKeep = 4;
+
 void pool_give(const hedl_kb *kb, int role, void *p, size_t bytes) {
     if (!p) return;
     std::lock_guard<std::mutex> lk(kb->pool_mu);
     auto &v = kb->pool[role];
     v.push_back({p, bytes});
-    while (v.size() > 2) {                    // keep the two largest
+    // keep the kPoolKeep largest: a double-buffered caller (bench.py's e2e loop) has three
+    // programs alive at once, and an evicted pinned block costs a cudaFreeHost (a device-wide
+    // synchronisation) now and a cudaMallocHost (~80 ms for a C4 plan blob) later
+    while (v.size() > kPoolKeep) {
         size_t mi = 0;
         for (size_t i = 1; i < v.size(); ++i)
             if (v[i].second < v[mi].second) mi = i;

@@ -179,19 +179,34 @@ hedl_status reserve_plan(const hedl_kb *kb, PlanCache &pc, size_t bytes, Workspa
     pc.cap = 0;
     size_t gh = 0, gd = 0;
     void *h = pool_take(kb, PR_PLAN_HOST, bytes, &gh);
-    void *d = h ? pool_take(kb, PR_PLAN_DEV, bytes, &gd) : nullptr;
+    void *d = pool_take(kb, PR_PLAN_DEV, bytes, &gd);
     if (h && d) {
         pc.host = h;
         pc.dev = d;
         pc.cap = std::min(gh, gd);
         return HEDL_OK;
     }
-    if (h) pool_give(kb, PR_PLAN_HOST, h, gh);
-    const size_t cap = std::max(bytes, (size_t)4096) * 5 / 4;
-    if (cudaMallocHost(&pc.host, cap) != cudaSuccess) { cudaGetLastError(); pc.host = nullptr; return fail(HEDL_ERR_OOM, "pinned plan"); }
-    if (dev_malloc(&pc.dev, cap) != cudaSuccess) {
+    // a pooled half is kept; only the missing one is allocated
+    size_t cap = std::max(bytes, (size_t)4096) * 5 / 4;
+    if (h) {
+        pc.host = h;
+        cap = std::min(cap, gh);
+    } else {
+        if (d) cap = std::min(cap, gd);
+        const double t0 = now_ms();
+        if (cudaMallocHost(&pc.host, cap) != cudaSuccess) {
+            cudaGetLastError();
+            pc.host = nullptr;
+            if (d) pool_give(kb, PR_PLAN_DEV, d, gd);
+            return fail(HEDL_ERR_OOM, "pinned plan");
+        }
+        timing_note("plan: cudaMallocHost", now_ms() - t0);
+    }
+    if (d) {
+        pc.dev = d;
+    } else if (dev_malloc(&pc.dev, cap) != cudaSuccess) {
         cudaGetLastError();
-        cudaFreeHost(pc.host);
+        pool_give(kb, PR_PLAN_HOST, pc.host, cap);
         pc.host = pc.dev = nullptr;
         return fail(HEDL_ERR_OOM, "device plan");
     }
