@@ -12,10 +12,11 @@ for i, r in enumerate(rows):
         hdr, body = r, rows[i + 1:]
         break
 ki, vi, gi = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Grid Size")
+mi = hdr.index("Metric Name") if "Metric Name" in hdr else None
 tot = defaultdict(float)
 launches = defaultdict(list)
 for r in body:
-    if len(r) <= vi:
+    if len(r) <= vi or (mi is not None and r[mi] != "gpu__time_duration.sum"):
         continue
     name = r[ki].split("(")[0].replace("void ", "").split("::")[-1].split("<")[0]
     v = float(r[vi].replace(",", ""))
