@@ -65,7 +65,48 @@ void live_kb_add(int d) {
     g_live_kbs += d;
 }
 
+#ifdef HEDL_CHECKED
+// Checked build: every device block gets kGuard bytes of 0xA5 on both sides; dev_free checks
+// them (after a device synchronise) and aborts with the block's size if a kernel wrote there.
+constexpr size_t kGuard = 4096;
+static std::mutex g_guard_mu;
+static std::unordered_map<void *, size_t> g_guarded;       // user pointer -> requested bytes
+static std::atomic<uint64_t> g_guard_checked{0};
+static bool guard_check(void *p, size_t bytes) {
+    const size_t pad = (bytes + 255) & ~size_t(255);
+    std::vector<unsigned char> h(kGuard);
+    bool ok = true;
+    for (char *g : {(char *)p - kGuard, (char *)p + pad}) {
+        if (cudaMemcpy(h.data(), g, kGuard, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+        for (unsigned char c : h) ok &= c == 0xA5;
+    }
+    g_guard_checked.fetch_add(1);
+    return ok;
+}
+static struct GuardReport {
+    ~GuardReport() {
+        std::fprintf(stderr, "[hedl checked] guard zones verified on %llu freed device blocks, none corrupted\n",
+                     (unsigned long long)g_guard_checked.load());
+    }
+} g_guard_report;
+#endif
+
 cudaError_t dev_malloc(void **p, size_t bytes, cudaStream_t s) {
+#ifdef HEDL_CHECKED
+    {
+        const size_t pad = (bytes + 255) & ~size_t(255);
+        void *base = nullptr;
+        cudaError_t e = cudaMalloc(&base, pad + 2 * kGuard);
+        if (e != cudaSuccess) { *p = nullptr; return e; }
+        cudaMemset(base, 0xA5, pad + 2 * kGuard);               // guards, and garbage in the block
+        cudaDeviceSynchronize();
+        *p = (char *)base + kGuard;
+        std::lock_guard<std::mutex> lk(g_guard_mu);
+        g_guarded[*p] = bytes;
+        (void)s;
+        return cudaSuccess;
+    }
+#endif
     *p = nullptr;
     g_n_alloc.fetch_add(1, std::memory_order_relaxed);
     const double t0 = timing_enabled() ? now_ms() : 0.0;
@@ -87,6 +128,26 @@ bool dev_alloc_installed() { return g_alloc != nullptr; }
 
 void dev_free(void *p, cudaStream_t s) {
     if (!p) return;
+#ifdef HEDL_CHECKED
+    {
+        cudaDeviceSynchronize();
+        size_t bytes = 0;
+        {
+            std::lock_guard<std::mutex> lk(g_guard_mu);
+            auto it = g_guarded.find(p);
+            if (it == g_guarded.end()) { std::fprintf(stderr, "[hedl checked] free of an unknown block %p\n", p); std::abort(); }
+            bytes = it->second;
+            g_guarded.erase(it);
+        }
+        if (!guard_check(p, bytes)) {
+            std::fprintf(stderr, "[hedl checked] guard zone of a %zu-byte device block corrupted\n", bytes);
+            std::abort();
+        }
+        cudaFree((char *)p - kGuard);
+        (void)s;
+        return;
+    }
+#endif
     g_n_free.fetch_add(1, std::memory_order_relaxed);
     if (g_free) {
         int dev = 0;

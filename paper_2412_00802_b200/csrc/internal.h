@@ -365,6 +365,23 @@ struct KbDev {
 };
 
 #ifdef __CUDACC__
+// Checked build (-DHEDL_CHECKED, tools/checked.sh): device-side bounds / invariant traps in the
+// hot kernels and guard zones around every device block (api.cpp).  Compiled out otherwise.
+#ifdef HEDL_CHECKED
+#define HCHECK(c)                                                                                 \
+    do {                                                                                          \
+        if (!(c)) {                                                                               \
+            printf("HCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, blockIdx.x, \
+                   threadIdx.x, #c);                                                              \
+            __trap();                                                                             \
+        }                                                                                         \
+    } while (0)
+#else
+#define HCHECK(c) ((void)0)
+#endif
+#endif
+
+#ifdef __CUDACC__
 // scatter the example bits of full-row word w into an example-projected row (atomicOr;
 // the projected row is zeroed before the launch)
 static __device__ __forceinline__ void proj_scatter(const KbDev &kb, uint32_t *proj, uint32_t w, uint32_t word) {

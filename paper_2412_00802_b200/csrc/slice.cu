@@ -56,6 +56,7 @@ struct SliceScratch {
     uint32_t *hout;               // [n_heavy][8]     finished heavy rows
     uint64_t t_stride;            // uint4 between the T of consecutive packs of one launch
     uint64_t h_stride;            // heavy rows between the accumulators of consecutive packs
+    uint64_t t_cap;               // uint4 of one pack's T region (HCHECK bound of the gathers)
     __device__ __forceinline__ SliceScratch at(uint32_t p) const {
         SliceScratch r = *this;
         r.T += p * t_stride;
@@ -70,12 +71,15 @@ struct SliceScratch {
 // pack p of a run of consecutive same-class descriptors: descs [256p, min(256p + 256, run))
 __device__ __forceinline__ uint32_t pack_count(uint32_t run, uint32_t p) { return min(256u, run - 256u * p); }
 
-// per-pack lane constants, built in shared memory from the node descriptors
-struct PackConst {
-    uint32_t fl[LW], am[LW], om[LW];              // OR class: out = ((acc ^ fl) & am) | om
-    uint32_t nb[NPL][LW];                         // COUNT class: bit planes of n
-    uint32_t mge[LW], mle[LW], meq[LW], mlep[LW];
+// per-pack lane constants, built in shared memory from the node descriptors; NP packs of one
+// pass: word kk of the 8*NP covers lanes 32kk .. 32kk+31
+template <int NP>
+struct PackConstN {
+    uint32_t fl[NP * LW], am[NP * LW], om[NP * LW];   // OR class: out = ((acc ^ fl) & am) | om
+    uint32_t nb[NPL][NP * LW];                         // COUNT class: bit planes of n
+    uint32_t mge[NP * LW], mle[NP * LW], meq[NP * LW], mlep[NP * LW];
 };
+using PackConst = PackConstN<1>;
 
 // 32x32 bit transpose across a warp: in lane r bit c = M[r][c]; out lane c bit r = M[r][c].
 // Five butterfly stages; each lane keeps half of its word and takes the other half from its
@@ -132,9 +136,10 @@ __device__ __forceinline__ void pack_bits(uint32_t m, uint32_t word, uint32_t ba
 
 // every thread of the CTA calls; lanes >= count get "always 0" (am = om = 0, masks 0).
 // Warp k builds the words of lanes 32k..32k+31 with ballots (no shared-memory atomics).
-__device__ void build_consts(PackConst &pc, const RestrictDesc *__restrict__ d, uint32_t count) {
+template <int NP>
+__device__ void build_consts(PackConstN<NP> &pc, const RestrictDesc *__restrict__ d, uint32_t count) {
     const uint32_t lane = threadIdx.x & 31;
-    for (uint32_t k = threadIdx.x >> 5; k < LW; k += blockDim.x >> 5) {
+    for (uint32_t k = threadIdx.x >> 5; k < NP * LW; k += blockDim.x >> 5) {
         const uint32_t j = k * 32 + lane;
         uint32_t pred = 0xffu, n = 0;
         if (j < count) {
@@ -256,13 +261,14 @@ struct Acc {
             }
         }
     }
-    // combine the TOP/2+... lane pairs of an aligned group of 2*TOP lanes (lanes of equal
-    // parity); every lane gets its half's total.  TOP = 16: the whole warp.
-    template <int TOP = 16>
+    // combine the lane groups of G lanes (G = 2: pairs, 4: quads) of an aligned block of 2*TOP
+    // lanes (lanes equal mod G); every lane gets its group position's total.  TOP = 16: the
+    // whole warp.
+    template <int TOP = 16, int G = 2>
     __device__ __forceinline__ void warp_reduce_pairs() {
         fold();
 #pragma unroll
-        for (int off = TOP; off >= 2; off >>= 1) {
+        for (int off = TOP; off >= G; off >>= 1) {
             Acc o;
 #pragma unroll
             for (int q = 0; q < (COUNT ? NPL : 1); ++q)
@@ -271,7 +277,8 @@ struct Acc {
             merge(o);
         }
     }
-    __device__ __forceinline__ uint32_t result(const PackConst &pc, int kk, int k) const {
+    template <class PC>
+    __device__ __forceinline__ uint32_t result(const PC &pc, int kk, int k) const {
         if (!COUNT) return ((c[0][k] ^ pc.fl[kk]) & pc.am[kk]) | pc.om[kk];
         const uint32_t o = ov[k & (COUNT ? HW - 1 : 0)];
         uint32_t gt = 0, eq = FULL, nz = 0;
@@ -287,10 +294,11 @@ struct Acc {
     }
 };
 
-// acc += T[y] (this thread's half) for the edges [e, b) with stride `step`, 4 gathers in flight
-template <bool COUNT>
+// acc += T[y] (this thread's 16 B of the R x 16 B record, `half` = its index) for the edges
+// [e, b) with stride `step`, 4 gathers in flight
+template <bool COUNT, int R = 2>
 __device__ __forceinline__ void scan_edges(Acc<COUNT> &acc, const uint32_t *__restrict__ col, const uint4 *__restrict__ T,
-                                           uint32_t e, uint32_t b, uint32_t step, uint32_t half) {
+                                           uint32_t e, uint32_t b, uint32_t step, uint32_t half, uint64_t cap) {
     // software-pipelined: the next four neighbour ids are in flight during this step's gathers
     uint32_t y[4];
 #pragma unroll
@@ -301,7 +309,10 @@ __device__ __forceinline__ void scan_edges(Acc<COUNT> &acc, const uint32_t *__re
         for (int u = 0; u < 4; ++u) yn[u] = e + step * (4 + u) < b ? __ldg(col + e + step * (4 + u)) : 0xffffffffu;
         uint4 v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = y[u] != 0xffffffffu ? __ldg(T + 2ull * y[u] + half) : make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < 4; ++u) {
+            HCHECK(y[u] == 0xffffffffu || (uint64_t)R * y[u] + R <= cap);
+            v[u] = y[u] != 0xffffffffu ? __ldg(T + (uint64_t)R * y[u] + half) : make_uint4(0, 0, 0, 0);
+        }
         acc.add4(v[0], v[1], v[2], v[3]);
 #pragma unroll
         for (int u = 0; u < 4; ++u) y[u] = yn[u];
@@ -323,7 +334,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
 __global__ void __launch_bounds__(256, 4) k_slice_pack(KbDev kb, const RestrictDesc *__restrict__ d_run, uint32_t run,
                                                     uint4 *__restrict__ T_base, uint64_t t_stride,
                                                     const uint32_t *__restrict__ umask, const uint32_t *__restrict__ ubase,
-                                                    const Operand *__restrict__ ops) {
+                                                    const Operand *__restrict__ ops, uint32_t rec) {
     extern __shared__ __align__(16) uint32_t sm[];        // [256][PK_STRIDE] lane rows
     __shared__ uint32_t s_cm[256], s_on[256];
     __shared__ uint64_t s_optab[256 * kFuseMaxOps];       // fused lanes' operand rows | complement
@@ -331,7 +342,10 @@ __global__ void __launch_bounds__(256, 4) k_slice_pack(KbDev kb, const RestrictD
     const uint32_t p = blockIdx.y;
     const RestrictDesc *d = d_run + 256u * p;
     const uint32_t count = pack_count(run, p);
-    uint4 *T = T_base + p * t_stride;
+    // rec = uint4 per individual: 2 (one pack's 32 B T per region of t_stride uint4), or 4 (a
+    // pack pair: the two packs' 32 B interleaved in one 64 B record;
+    // t_stride = the whole region)
+    uint4 *T = rec == 4 ? T_base + 2 * p : T_base + p * t_stride;
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t w0 = blockIdx.x * PK_WORDS;
     const uint32_t nwords = min(PK_WORDS, kb.W4 - w0);    // multiple of 4 (W4 and w0 are)
@@ -457,10 +471,12 @@ __global__ void __launch_bounds__(256, 4) k_slice_pack(KbDev kb, const RestrictD
             const uint32_t w = w0 + wq + kk, um = ums[4 * q + kk];
             if (!umask) {
                 const uint64_t y = (uint64_t)w * 32 + lane;
-                T[2 * y] = make_uint4(o[kk][0], o[kk][1], o[kk][2], o[kk][3]);
-                T[2 * y + 1] = make_uint4(o[kk][4], o[kk][5], o[kk][6], o[kk][7]);
+                HCHECK(rec * y + rec <= t_stride);
+                T[rec * y] = make_uint4(o[kk][0], o[kk][1], o[kk][2], o[kk][3]);
+                T[rec * y + 1] = make_uint4(o[kk][4], o[kk][5], o[kk][6], o[kk][7]);
             } else if ((um >> lane) & 1u) {
                 const uint64_t t = ubs[4 * q + kk] + __popc(um & ((1u << lane) - 1u));
+                HCHECK(2 * t + 2 <= t_stride);
                 T[2 * t] = make_uint4(o[kk][0], o[kk][1], o[kk][2], o[kk][3]);
                 T[2 * t + 1] = make_uint4(o[kk][4], o[kk][5], o[kk][6], o[kk][7]);
             }
@@ -469,50 +485,59 @@ __global__ void __launch_bounds__(256, 4) k_slice_pack(KbDev kb, const RestrictD
 }
 
 // ------------------------------------------------------------------------------
-// heavy rows: CTA (256 threads = 128 lane pairs) per chunk of <= kHeavyChunk edges.
-template <bool COUNT>
+// heavy rows: CTA (256 threads) per chunk of <= kHeavyChunk edges.  NP packs per pass: the
+// threads form groups of G = 2 NP (lane pairs for one pack, quads for a pack pair), thread q of
+// a group owns words 4q .. 4q+3 of the 8 NP-word lane record (pack q >> 1).
+template <bool COUNT, int NP>
 __global__ void __launch_bounds__(256) k_slice_heavy(SliceDir dir, SliceScratch sc0, const RestrictDesc *__restrict__ d_run,
                                                      uint32_t run) {
-    const SliceScratch sc = sc0.at(blockIdx.y);
-    const RestrictDesc *d = d_run + 256u * blockIdx.y;
-    const uint32_t count = pack_count(run, blockIdx.y);
-    __shared__ PackConst pc;
-    __shared__ uint32_t red[8][2][COUNT ? NPL : 1][HW];
-    __shared__ uint32_t fin[2][COUNT ? NPL : 1][HW];
-    __shared__ uint32_t outw[LW];
+    constexpr int G = 2 * NP, NG = 256 / G;
+    const uint32_t p0 = blockIdx.y * NP;                  // first pack of this pass
+    const SliceScratch sc = sc0.at(p0);
+    const RestrictDesc *d = d_run + 256u * p0;
+    const uint32_t count = min(256u * NP, run - 256u * p0);
+    __shared__ PackConstN<NP> pc;
+    __shared__ uint32_t red[8][G][COUNT ? NPL : 1][HW];
+    __shared__ uint32_t fin[G][COUNT ? NPL : 1][HW];
+    __shared__ uint32_t outw[NP * LW];
     __shared__ uint32_t s_last;
     const uint4 ch = dir.chunks[blockIdx.x];
     const uint32_t h = ch.x;
-    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, half = lane & 1;
+    HCHECK(h < dir.n_heavy && ch.y <= ch.z);
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, q = lane & (G - 1);
     Acc<COUNT> acc;
     acc.zero();
-    scan_edges<COUNT>(acc, dir.col, sc.T, ch.y + (threadIdx.x >> 1), ch.z, 128, half);
-    acc.template warp_reduce_pairs<16>();
-    if (lane < 2)
-        for (int q = 0; q < (COUNT ? NPL : 1); ++q)
-            for (int k = 0; k < HW; ++k) red[wid][half][q][k] = acc.c[q][k];
+    scan_edges<COUNT, G>(acc, dir.col, sc.T, ch.y + threadIdx.x / G, ch.z, NG, q, sc.t_cap);
+    acc.template warp_reduce_pairs<16, G>();
+    if (lane < G)
+        for (int c = 0; c < (COUNT ? NPL : 1); ++c)
+            for (int k = 0; k < HW; ++k) red[wid][q][c][k] = acc.c[c][k];
     __syncthreads();
-    if (threadIdx.x < 2) {
+    if (threadIdx.x < G) {
         Acc<COUNT> a, b;
-        for (int q = 0; q < (COUNT ? NPL : 1); ++q) for (int k = 0; k < HW; ++k) a.c[q][k] = red[0][threadIdx.x][q][k];
+        for (int c = 0; c < (COUNT ? NPL : 1); ++c) for (int k = 0; k < HW; ++k) a.c[c][k] = red[0][threadIdx.x][c][k];
         for (int w = 1; w < 8; ++w) {
-            for (int q = 0; q < (COUNT ? NPL : 1); ++q) for (int k = 0; k < HW; ++k) b.c[q][k] = red[w][threadIdx.x][q][k];
+            for (int c = 0; c < (COUNT ? NPL : 1); ++c) for (int k = 0; k < HW; ++k) b.c[c][k] = red[w][threadIdx.x][c][k];
             a.merge(b);
         }
-        for (int q = 0; q < (COUNT ? NPL : 1); ++q) for (int k = 0; k < HW; ++k) fin[threadIdx.x][q][k] = a.c[q][k];
+        for (int c = 0; c < (COUNT ? NPL : 1); ++c) for (int k = 0; k < HW; ++k) fin[threadIdx.x][c][k] = a.c[c][k];
     }
     __syncthreads();
     if (!COUNT) {
-        if (threadIdx.x < LW) {
-            const uint32_t x = fin[threadIdx.x >> 2][0][threadIdx.x & 3];
-            if (x) atomicOr(sc.hacc + (size_t)h * LW + threadIdx.x, x);
+        if (threadIdx.x < NP * LW) {                      // word kk of the pass: pack kk / 8, word kk % 8
+            const uint32_t kk = threadIdx.x;
+            const uint32_t x = fin[kk >> 2][0][kk & 3];
+            if (x) atomicOr(sc0.at(p0 + (kk >> 3)).hacc + (size_t)h * LW + (kk & 7), x);
         }
     } else {
-        const uint32_t L = threadIdx.x;                 // lane of the pack: half, word, bit
-        const uint32_t hh = L >> 7, k = (L >> 5) & 3, bit = L & 31;
-        uint32_t val = 0;
-        for (int q = 0; q < NPL; ++q) val |= ((fin[hh][q][k] >> bit) & 1u) << q;
-        if (val) atomicAdd(sc.hcnt + (size_t)h * 256 + L, val);
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) {
+            const uint32_t L = threadIdx.x;             // lane of pack pp: half, word, bit
+            const uint32_t g = 2 * pp + (L >> 7), k = (L >> 5) & 3, bit = L & 31;
+            uint32_t val = 0;
+            for (int c = 0; c < NPL; ++c) val |= ((fin[g][c][k] >> bit) & 1u) << c;
+            if (val) atomicAdd(sc0.at(p0 + pp).hcnt + (size_t)h * 256 + L, val);
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -525,29 +550,33 @@ __global__ void __launch_bounds__(256) k_slice_heavy(SliceDir dir, SliceScratch 
     __threadfence();
     build_consts(pc, d, count);
     if (!COUNT) {
-        if (threadIdx.x < LW) {
-            const uint32_t k = threadIdx.x;
-            const uint32_t a = atomicExch(sc.hacc + (size_t)h * LW + k, 0u);   // read + self-clean
-            sc.hout[(size_t)h * LW + k] = ((a ^ pc.fl[k]) & pc.am[k]) | pc.om[k];
+        if (threadIdx.x < NP * LW) {
+            const uint32_t kk = threadIdx.x;
+            const SliceScratch sp = sc0.at(p0 + (kk >> 3));
+            const uint32_t a = atomicExch(sp.hacc + (size_t)h * LW + (kk & 7), 0u);   // read + self-clean
+            sp.hout[(size_t)h * LW + (kk & 7)] = ((a ^ pc.fl[kk]) & pc.am[kk]) | pc.om[kk];
         }
     } else {
-        if (threadIdx.x < LW) outw[threadIdx.x] = 0;
+        if (threadIdx.x < NP * LW) outw[threadIdx.x] = 0;
         __syncthreads();
-        const uint32_t L = threadIdx.x;
-        uint32_t c = atomicExch(sc.hcnt + (size_t)h * 256 + L, 0u);
-        c = c > 31u ? 31u : c;
-        const uint32_t k = L >> 5, bit = 1u << (L & 31);
-        uint32_t n = 0;
-        for (int q = 0; q < NPL; ++q) n |= ((pc.nb[q][k] & bit) ? 1u : 0u) << q;
-        bool r;
-        if (pc.mge[k] & bit) r = c >= n;
-        else if (pc.mle[k] & bit) r = c <= n;
-        else if (pc.meq[k] & bit) r = c == n;
-        else if (pc.mlep[k] & bit) r = c > 0 && c <= n;
-        else r = false;
-        if (r) atomicOr(&outw[k], bit);
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) {
+            const uint32_t L = threadIdx.x;
+            uint32_t c = atomicExch(sc0.at(p0 + pp).hcnt + (size_t)h * 256 + L, 0u);
+            c = c > 31u ? 31u : c;
+            const uint32_t k = pp * LW + (L >> 5), bit = 1u << (L & 31);
+            uint32_t n = 0;
+            for (int cq = 0; cq < NPL; ++cq) n |= ((pc.nb[cq][k] & bit) ? 1u : 0u) << cq;
+            bool r;
+            if (pc.mge[k] & bit) r = c >= n;
+            else if (pc.mle[k] & bit) r = c <= n;
+            else if (pc.meq[k] & bit) r = c == n;
+            else if (pc.mlep[k] & bit) r = c > 0 && c <= n;
+            else r = false;
+            if (r) atomicOr(&outw[k], bit);
+        }
         __syncthreads();
-        if (threadIdx.x < LW) sc.hout[(size_t)h * LW + threadIdx.x] = outw[threadIdx.x];
+        if (threadIdx.x < NP * LW) sc0.at(p0 + (threadIdx.x >> 3)).hout[(size_t)h * LW + (threadIdx.x & 7)] = outw[threadIdx.x];
     }
     if (threadIdx.x == 0) sc.ticket[h] = 0;
 }
@@ -557,9 +586,9 @@ __global__ void __launch_bounds__(256) k_slice_heavy(SliceDir dir, SliceScratch 
 // edges e, e+S, e+2S, ... below b).  Software-pipelined: the next step's four neighbour
 // indices are loaded before this step's four T gathers, so the CSR stream (DRAM) and the
 // T gathers (L2) overlap instead of adding up.
-template <bool COUNT>
+template <bool COUNT, int R = 2>
 __device__ __forceinline__ void scan_strided(Acc<COUNT> &acc, const uint32_t *__restrict__ col, const uint4 *__restrict__ T,
-                                             uint32_t e, uint32_t b, uint32_t S, uint32_t half) {
+                                             uint32_t e, uint32_t b, uint32_t S, uint32_t half, uint64_t cap) {
     uint32_t y[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) y[u] = e + S * u < b ? __ldg(col + e + S * u) : 0xffffffffu;
@@ -569,7 +598,10 @@ __device__ __forceinline__ void scan_strided(Acc<COUNT> &acc, const uint32_t *__
         for (int u = 0; u < 4; ++u) yn[u] = e + S * (4 + u) < b ? __ldg(col + e + S * (4 + u)) : 0xffffffffu;
         uint4 v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = y[u] != 0xffffffffu ? __ldg(T + 2ull * y[u] + half) : make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < 4; ++u) {
+            HCHECK(y[u] == 0xffffffffu || (uint64_t)R * y[u] + R <= cap);
+            v[u] = y[u] != 0xffffffffu ? __ldg(T + (uint64_t)R * y[u] + half) : make_uint4(0, 0, 0, 0);
+        }
         acc.add4(v[0], v[1], v[2], v[3]);
 #pragma unroll
         for (int u = 0; u < 4; ++u) y[u] = yn[u];
@@ -578,9 +610,9 @@ __device__ __forceinline__ void scan_strided(Acc<COUNT> &acc, const uint32_t *__
 
 // one SELL-16 slice (16 rows of similar degree, neighbour k of row i at c[16k + i]), a lane
 // pair per row, the same software pipeline over the slice's width w (a multiple of 4)
-template <bool COUNT>
+template <bool COUNT, int R = 2>
 __device__ __forceinline__ void scan_slice_pipelined(Acc<COUNT> &acc, const uint32_t *__restrict__ c, const uint4 *__restrict__ T,
-                                                     uint32_t w, uint32_t half) {
+                                                     uint32_t w, uint32_t half, uint64_t cap) {
     if (!w) return;
     uint32_t y[4];
 #pragma unroll
@@ -592,7 +624,10 @@ __device__ __forceinline__ void scan_slice_pipelined(Acc<COUNT> &acc, const uint
         for (int u = 0; u < 4; ++u) yn[u] = more ? __ldg(c + (k + 4 + u) * 16) : 0xffffffffu;
         uint4 v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = y[u] != 0xffffffffu ? __ldg(T + 2ull * y[u] + half) : make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < 4; ++u) {
+            HCHECK(y[u] == 0xffffffffu || (uint64_t)R * y[u] + R <= cap);
+            v[u] = y[u] != 0xffffffffu ? __ldg(T + (uint64_t)R * y[u] + half) : make_uint4(0, 0, 0, 0);
+        }
         acc.add4(v[0], v[1], v[2], v[3]);
 #pragma unroll
         for (int u = 0; u < 4; ++u) y[u] = yn[u];
@@ -600,23 +635,28 @@ __device__ __forceinline__ void scan_slice_pipelined(Acc<COUNT> &acc, const uint
 }
 
 // ------------------------------------------------------------------------------
-// Persistent sweep over 1024-individual tiles (256 threads = 128 lane pairs per CTA,
-// grid = resident CTAs).  CTAs take tiles from a global counter in decreasing-cost order
-// (dir.tile_rank, LPT), and inside a tile the warps take work items (medium rows, then
-// SELL slices, both degree-descending) from a shared counter, so neither the grid nor
-// the CTA waits on a statically unlucky share.  The counter pair `sched` is self-cleaning:
-// the last CTA to finish resets it for the next launch on the stream.
-template <bool COUNT>
-__global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, SliceScratch sc, UTab ut,
-                                                                   const RestrictDesc *__restrict__ d, uint32_t count,
-                                                                   hedl_counts *counts, uint32_t *sched, uint32_t dbg) {
+// Persistent sweep over 1024-individual tiles (grid = resident CTAs).  NP packs per pass
+// (DESIGN.md "Pack pairs"): 256 NP threads per CTA, a group of G = 2 NP threads per row, thread
+// q of a group owning words 4q .. 4q+3 of the row's 8 NP-word lane record (T record of 16 G
+// bytes, one gather per edge and thread group).  CTAs take tiles from a global counter in
+// decreasing-cost order (dir.tile_rank, LPT), and inside a tile the warps take work items
+// (medium rows, then SELL slices, both degree-descending) from a shared counter, so neither
+// the grid nor the CTA waits on a statically unlucky share.  The counter pair `sched` is
+// self-cleaning: the last CTA to finish resets it for the next launch on the stream.
+template <bool COUNT, int NP>
+__global__ void __launch_bounds__(256 * NP, 4 / NP) k_slice_tile(KbDev kb, SliceDir dir, SliceScratch sc, UTab ut,
+                                                                 const RestrictDesc *__restrict__ d, uint32_t count,
+                                                                 hedl_counts *counts, uint32_t *sched, uint32_t dbg) {
 #ifndef HEDL_DEBUG_TILE
     dbg = 0;                                              // release builds: the debug switches fold away
 #endif
+    constexpr int G = 2 * NP;                             // threads per row (one 16 B quarter each)
+    constexpr uint32_t TR = NP * LW + 1;                  // ot row stride (bank-conflict-free transposes)
+    constexpr uint32_t NT = 256 * NP;
     extern __shared__ uint32_t smem[];
-    PackConst &pc = *reinterpret_cast<PackConst *>(smem);
-    uint32_t *ot = smem + sizeof(PackConst) / 4;          // [1024][TROW]
-    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, half = lane & 1;
+    PackConstN<NP> &pc = *reinterpret_cast<PackConstN<NP> *>(smem);
+    uint32_t *ot = smem + sizeof(PackConstN<NP>) / 4;     // [1024][TR]
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, q = lane & (G - 1);
     __shared__ uint32_t s_exm[32], s_exb[32];
     __shared__ uint32_t s_tile, s_item;
     __shared__ uint32_t s_udirs;
@@ -634,7 +674,7 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
     }
     if (threadIdx.x == 0) s_udirs = 0;
     __syncthreads();
-    if (r_udirs) atomicOr(&s_udirs, r_udirs);            // directions some node of the pack emits
+    if (r_udirs) atomicOr(&s_udirs, r_udirs);            // directions some node of the pass emits
     build_consts(pc, d, count);                           // (contains __syncthreads)
     const bool live = jn < count;
     uint32_t tp = 0, fp = 0;
@@ -650,7 +690,7 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
         const uint32_t t = __ldg(dir.tile_rank + tt);
         const uint32_t x0 = t * 1024;
         if (x0 + 1024 > kb.N)                              // only the last tile has rows >= N (left 0)
-            for (uint32_t i = threadIdx.x; i < 1024 * TROW; i += 256) ot[i] = 0;
+            for (uint32_t i = threadIdx.x; i < 1024 * TR; i += NT) ot[i] = 0;
         if (threadIdx.x < 32) {
             const uint32_t w = t * 32 + threadIdx.x;
             s_exm[threadIdx.x] = w < kb.W ? __ldg(kb.ex_mask + w) : 0u;
@@ -659,15 +699,21 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
         const uint4 ti = dir.tiles[t];
         const uint32_t hbeg = ti.w, hend = dir.tiles[t + 1].w;
         if (x0 + 1024 > kb.N) __syncthreads();            // zero fill before the heavy rows land
-        for (uint32_t h = hbeg + threadIdx.x; h < hend; h += 256) {
+        for (uint32_t h = hbeg + threadIdx.x; h < hend; h += NT) {
             const uint32_t xl = __ldg(dir.heavy_x + h) - x0;
+            HCHECK(xl < 1024u);
 #pragma unroll
-            for (int k = 0; k < LW; ++k) ot[xl * TROW + k] = sc.hout[(size_t)h * LW + k];
+            for (int pp = 0; pp < NP; ++pp) {
+                const uint32_t *ho = sc.at(pp).hout + (size_t)h * LW;
+#pragma unroll
+                for (int k = 0; k < LW; ++k) ot[xl * TR + pp * LW + k] = ho[k];
+            }
         }
         const uint32_t sbeg = __ldg(dir.tile_slice + t), send = __ldg(dir.tile_slice + t + 1);
         // work items, in this order: big medium rows (deg > kMidDeg; a warp each), mid rows
-        // (4 per warp, 4 lane pairs each), light SELL slices (SPI per item)
-        constexpr uint32_t SPI = COUNT ? 1u : 2u;
+        // (4 per warp, 8 lanes each), light SELL-16 slices (SPI per item; for a pack pair a
+        // slice's 16 rows are two 8-row halves of the warp)
+        constexpr uint32_t SPI = (COUNT || NP == 2) ? 1u : 2u;
         const uint32_t n_big = (dbg & 2) ? 0u : __ldg(dir.tile_nbig + t);
         const uint32_t n_med = (dbg & 2) ? 0u : ti.y, n_sl = (dbg & 1) ? 0u : send - sbeg;
         const uint32_t i_light = n_big + (n_med - n_big + 3) / 4;
@@ -681,49 +727,72 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
             Acc<COUNT> acc;
             acc.zero();
             if (it < n_big) {
-                // big medium row: warp per row, the 16 lane pairs split its neighbours
+                // big medium row: warp per row, the 32 / G thread groups split its neighbours
                 const uint32_t x = __ldg(dir.order + ti.x + it);
+                HCHECK(x - x0 < 1024u);
                 const uint32_t a = __ldg(dir.row_ptr + x), b = __ldg(dir.row_ptr + x + 1);
-                scan_strided<COUNT>(acc, dir.col, sc.T, a + (lane >> 1), b, 16, half);
-                acc.template warp_reduce_pairs<16>();
-                if (lane < 2) {
+                scan_strided<COUNT, G>(acc, dir.col, sc.T, a + lane / G, b, 32 / G, q, sc.t_cap);
+                acc.template warp_reduce_pairs<16, G>();
+                if (lane < G) {
 #pragma unroll
-                    for (int k = 0; k < HW; ++k) ot[(x - x0) * TROW + half * HW + k] = acc.result(pc, half * HW + k, k);
+                    for (int k = 0; k < HW; ++k) ot[(x - x0) * TR + q * HW + k] = acc.result(pc, q * HW + k, k);
                 }
             } else if (it < i_light) {
-                // mid rows: 4 per warp, the 4 lane pairs of each 8-lane group split one row
-                // (two reduction stages instead of four)
-                const uint32_t p = (lane >> 1) & 3u;
+                // mid rows: 4 per warp, the 8 / G groups of each 8-lane block split one row
+                const uint32_t p = (lane / G) & (8 / G - 1);
                 const uint32_t mi = n_big + (it - n_big) * 4 + (lane >> 3);
                 const bool rv = mi < n_med;
                 uint32_t x = 0, a = 0, b = 0;
                 if (rv) {
                     x = __ldg(dir.order + ti.x + mi);
+                    HCHECK(x - x0 < 1024u);
                     a = __ldg(dir.row_ptr + x);
                     b = __ldg(dir.row_ptr + x + 1);
                 }
-                scan_strided<COUNT>(acc, dir.col, sc.T, a + p, b, 4, half);
-                acc.template warp_reduce_pairs<4>();
+                scan_strided<COUNT, G>(acc, dir.col, sc.T, a + p, b, 8 / G, q, sc.t_cap);
+                acc.template warp_reduce_pairs<4, G>();
                 if (rv && p == 0) {
 #pragma unroll
-                    for (int k = 0; k < HW; ++k) ot[(x - x0) * TROW + half * HW + k] = acc.result(pc, half * HW + k, k);
+                    for (int k = 0; k < HW; ++k) ot[(x - x0) * TR + q * HW + k] = acc.result(pc, q * HW + k, k);
                 }
-            } else if (SPI == 1) {
+            } else if (NP == 1 && SPI == 1) {
                 // light rows: one SELL-16 slice, a lane pair per row; the 16 pairs read 16
                 // consecutive neighbour indices per step (coalesced)
                 const uint32_t sl = it - i_light;
                 const uint32_t li = sl * 16 + (lane >> 1);
                 const bool rv = li < ti.z;
                 const uint32_t x = rv ? __ldg(dir.order + ti.x + ti.y + li) : 0u;
+                HCHECK(!rv || x - x0 < 1024u);
                 const uint32_t *c = dir.sell_col + __ldg(dir.sell_off + sbeg + sl) + (lane >> 1);
-                scan_slice_pipelined<COUNT>(acc, c, sc.T, __ldg(dir.sell_w + sbeg + sl), half);
+                scan_slice_pipelined<COUNT, G>(acc, c, sc.T, __ldg(dir.sell_w + sbeg + sl), q, sc.t_cap);
                 if (rv) {
 #pragma unroll
-                    for (int q = 0; q < HW; ++q) ot[(x - x0) * TROW + half * HW + q] = acc.result(pc, half * HW + q, q);
+                    for (int k = 0; k < HW; ++k) ot[(x - x0) * TR + q * HW + k] = acc.result(pc, q * HW + k, k);
+                }
+            } else if (NP == 2 && COUNT) {
+                // light rows of a pack pair, COUNT class: one SELL-16 slice, a quad per row, the
+                // two 8-row halves one after the other (register budget)
+                const uint32_t sl = it - i_light;
+                const uint32_t *cb = dir.sell_col + __ldg(dir.sell_off + sbeg + sl) + (lane >> 2);
+                const uint32_t wdt = __ldg(dir.sell_w + sbeg + sl);
+#pragma unroll 1
+                for (uint32_t hh = 0; hh < 2; ++hh) {
+                    const uint32_t li = sl * 16 + hh * 8 + (lane >> 2);
+                    const bool rv = li < ti.z;
+                    const uint32_t x = rv ? __ldg(dir.order + ti.x + ti.y + li) : 0u;
+                    HCHECK(!rv || x - x0 < 1024u);
+                    if (hh) acc.zero();
+                    scan_slice_pipelined<COUNT, G>(acc, cb + hh * 8, sc.T, wdt, q, sc.t_cap);
+                    if (rv) {
+#pragma unroll
+                        for (int k = 0; k < HW; ++k) ot[(x - x0) * TR + q * HW + k] = acc.result(pc, q * HW + k, k);
+                    }
                 }
             } else {
-                // light rows, OR class: two SELL-16 slices per step (their dependent load
-                // chains -- slice bounds, neighbour ids, T gathers -- overlap)
+                // light rows, OR class: two row sets per step, their dependent load chains (slice
+                // bounds, neighbour ids, T gathers) overlapping -- one pack: two SELL-16 slices,
+                // a lane pair per row; a pack pair: the two 8-row halves of one slice, a quad
+                // per row
                 Acc<COUNT> acc2;
                 acc2.zero();
                 uint32_t x[2], w[2];
@@ -731,12 +800,14 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
                 bool rv[2];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const uint32_t sl = (it - i_light) * 2 + h;
+                    const uint32_t sl = NP == 1 ? (it - i_light) * 2 + h : it - i_light;
                     const bool sv = sl < n_sl;
-                    const uint32_t li = sl * 16 + (lane >> 1);
+                    const uint32_t li = NP == 1 ? sl * 16 + (lane >> 1) : sl * 16 + h * 8 + (lane >> 2);
                     rv[h] = sv && li < ti.z;
                     x[h] = rv[h] ? __ldg(dir.order + ti.x + ti.y + li) : 0u;
-                    cp[h] = sv ? dir.sell_col + __ldg(dir.sell_off + sbeg + sl) + (lane >> 1) : dir.sell_col;
+                    HCHECK(!rv[h] || x[h] - x0 < 1024u);
+                    const uint32_t col0 = NP == 1 ? (lane >> 1) : h * 8 + (lane >> 2);
+                    cp[h] = sv ? dir.sell_col + __ldg(dir.sell_off + sbeg + sl) + col0 : dir.sell_col;
                     w[h] = sv ? __ldg(dir.sell_w + sbeg + sl) : 0u;
                 }
                 const uint32_t wm = max(w[0], w[1]);
@@ -750,18 +821,20 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
 #pragma unroll
                     for (int h = 0; h < 2; ++h)
 #pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            v[h][u] = y[h][u] != 0xffffffffu ? __ldg(sc.T + 2ull * y[h][u] + half) : make_uint4(0, 0, 0, 0);
+                        for (int u = 0; u < 4; ++u) {
+                            HCHECK(y[h][u] == 0xffffffffu || (uint64_t)G * y[h][u] + G <= sc.t_cap);
+                            v[h][u] = y[h][u] != 0xffffffffu ? __ldg(sc.T + (uint64_t)G * y[h][u] + q) : make_uint4(0, 0, 0, 0);
+                        }
                     acc.add4(v[0][0], v[0][1], v[0][2], v[0][3]);
                     acc2.add4(v[1][0], v[1][1], v[1][2], v[1][3]);
                 }
                 if (rv[0]) {
 #pragma unroll
-                    for (int q = 0; q < HW; ++q) ot[(x[0] - x0) * TROW + half * HW + q] = acc.result(pc, half * HW + q, q);
+                    for (int k = 0; k < HW; ++k) ot[(x[0] - x0) * TR + q * HW + k] = acc.result(pc, q * HW + k, k);
                 }
                 if (rv[1]) {
 #pragma unroll
-                    for (int q = 0; q < HW; ++q) ot[(x[1] - x0) * TROW + half * HW + q] = acc2.result(pc, half * HW + q, q);
+                    for (int k = 0; k < HW; ++k) ot[(x[1] - x0) * TR + q * HW + k] = acc2.result(pc, q * HW + k, k);
                 }
             }
             nxt = __shfl_sync(FULL, nxt, 0);
@@ -776,7 +849,7 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
             if (w >= kb.W4) break;                         // W4 is a multiple of 8
             uint32_t o[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) o[q] = warp_transpose(ot[((wl + q) * 32 + lane) * TROW + g], lane);
+            for (int k = 0; k < 8; ++k) o[k] = warp_transpose(ot[((wl + k) * 32 + lane) * TR + g], lane);
             if (live) {
                 if (r_out) {
                     uint4 *dst = reinterpret_cast<uint4 *>(r_out + w);
@@ -784,31 +857,32 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
                     dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
                 }
                 if (r_proj) {
-                    // example bits of word w+q -> the projected row (pext with the staged masks)
+                    // example bits of word w+k -> the projected row (pext with the staged masks)
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) pack_bits(s_exm[wl + q], o[q], s_exb[wl + q], r_proj, pw, pbits);
+                    for (int k = 0; k < 8; ++k) pack_bits(s_exm[wl + k], o[k], s_exb[wl + k], r_proj, pw, pbits);
                 }
                 if (r_cover >= 0) {
                     const uint4 *pp = reinterpret_cast<const uint4 *>(kb.pos + w);
                     const uint4 *nn = reinterpret_cast<const uint4 *>(kb.neg + w);
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh) {
-                        const uint4 p = __ldg(pp + hh), n = __ldg(nn + hh);
+                        const uint4 pv = __ldg(pp + hh), nv = __ldg(nn + hh);
                         const uint32_t *oo = o + 4 * hh;
-                        tp += __popc(oo[0] & p.x) + __popc(oo[1] & p.y) + __popc(oo[2] & p.z) + __popc(oo[3] & p.w);
-                        fp += __popc(oo[0] & n.x) + __popc(oo[1] & n.y) + __popc(oo[2] & n.z) + __popc(oo[3] & n.w);
+                        tp += __popc(oo[0] & pv.x) + __popc(oo[1] & pv.y) + __popc(oo[2] & pv.z) + __popc(oo[3] & pv.w);
+                        fp += __popc(oo[0] & nv.x) + __popc(oo[1] & nv.y) + __popc(oo[2] & nv.z) + __popc(oo[3] & nv.w);
                     }
                 }
             }
         }
         if (pbits) atomicOr(r_proj + pw, pbits);
-        // U rows: for each direction d some node of the pack
+        // U rows: for each direction d some node of the pass
         // emits, the tile's members of U_d (the example rows' neighbours in direction d) are the
         // consecutive U positions [bl, bh) whose individuals ulist_d gives; 32 of them at a time,
         // their result rows (ot) go through one more warp transpose, and lane j of warp g holds
         // node 32g + j's U word.  Interior U words are written whole, the two seam words shared
         // with the neighbouring tiles by atomicOr into the zeroed row.  (No block barrier: ot is
-        // stable until the next tile's first __syncthreads.)
+        // stable until the next tile's first __syncthreads.  Selecting the members from the
+        // tile's U-mask words with warp scans instead of the ulist loads measured 2% slower.)
 #pragma unroll
         for (uint32_t dd = 0; dd < kMaxUDirs; ++dd) {
             if (!((s_udirs >> dd) & 1u)) continue;                        // block-uniform
@@ -820,7 +894,8 @@ __global__ void __launch_bounds__(256, 4) k_slice_tile(KbDev kb, SliceDir dir, S
             const uint32_t c0 = bl >> 5, c1 = (bh - 1) >> 5;
             for (uint32_t cw = c0; cw <= c1; ++cw) {
                 const uint32_t pos = cw * 32 + lane;
-                const uint32_t v = (pos >= bl && pos < bh) ? ot[(__ldg(ut.ul[dd] + pos) - x0) * TROW + g] : 0u;
+                HCHECK(!(pos >= bl && pos < bh) || (pos < ut.nu[dd] && __ldg(ut.ul[dd] + pos) - x0 < 1024u));
+                const uint32_t v = (pos >= bl && pos < bh) ? ot[(__ldg(ut.ul[dd] + pos) - x0) * TR + g] : 0u;
                 const uint32_t x = warp_transpose(v, lane);
                 if (mine) {
                     const bool seam = (cw == c0 && (bl & 31)) || (cw == c1 && (bh & 31));
@@ -881,15 +956,17 @@ __global__ void __launch_bounds__(256, COUNT ? 4 : 6) k_slice_ex(ExArgs a, Slice
     const uint32_t hbeg = ti.w, hend = a.ex_tiles[b + 1].w;
     for (uint32_t h = hbeg + threadIdx.x; h < hend; h += 256) {
         const uint32_t rl = __ldg(a.ex_hrank + h) - r0;
+        HCHECK(rl < 128u);
 #pragma unroll
         for (int k = 0; k < LW; ++k) ot[rl * TROW + k] = sc.hout[(size_t)h * LW + k];
     }
     for (uint32_t m = wid; m < ti.y; m += 8) {            // medium rows: warp per row
         const uint32_t r = __ldg(a.ex_order + ti.x + m);
+        HCHECK(r - r0 < 128u);
         const uint32_t e0 = __ldg(a.erp + r), e1 = __ldg(a.erp + r + 1);
         Acc<COUNT> acc;
         acc.zero();
-        scan_edges<COUNT>(acc, a.ecol, sc.T, e0 + (lane >> 1), e1, 16, half);
+        scan_edges<COUNT>(acc, a.ecol, sc.T, e0 + (lane >> 1), e1, 16, half, sc.t_cap);
         acc.template warp_reduce_pairs<16>();
         if (lane < 2) {
 #pragma unroll
@@ -898,10 +975,11 @@ __global__ void __launch_bounds__(256, COUNT ? 4 : 6) k_slice_ex(ExArgs a, Slice
     }
     for (uint32_t l = threadIdx.x >> 1; l < ti.z; l += 128) {   // light rows: lane pair per row
         const uint32_t r = __ldg(a.ex_order + ti.x + ti.y + l);
+        HCHECK(r - r0 < 128u);
         const uint32_t e0 = __ldg(a.erp + r), e1 = __ldg(a.erp + r + 1);
         Acc<COUNT> acc;
         acc.zero();
-        scan_edges<COUNT>(acc, a.ecol, sc.T, e0, e1, 1, half);
+        scan_edges<COUNT>(acc, a.ecol, sc.T, e0, e1, 1, half, sc.t_cap);
 #pragma unroll
         for (int k = 0; k < HW; ++k) ot[(r - r0) * TROW + half * HW + k] = acc.result(pc, half * HW + k, k);
     }
@@ -967,8 +1045,9 @@ SliceLayout slice_layout(const hedl_kb *kb) {
     }
     const size_t per_h = (LW + 256 + 1 + LW) * 4;
     L.max_batch = (uint32_t)std::max<size_t>(1, std::min<size_t>(128, (4ull << 30) / L.tx_bytes));
-    L.off_hf = std::max(L.t_bytes, L.tx_bytes * L.max_batch);
-    L.off_hx = L.off_hf + L.nh * per_h;
+    // full packs go in pairs: room for two packs' T and heavy scratch
+    L.off_hf = std::max(2 * L.t_bytes, L.tx_bytes * L.max_batch);
+    L.off_hx = L.off_hf + 2 * L.nh * per_h;
     L.need = L.off_hx + (size_t)L.max_batch * L.nhx * per_h + 256;
     return L;
 }
@@ -1011,6 +1090,7 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
         sc.ticket = sc.hcnt + cap * 256;
         sc.hout = sc.ticket + cap;
         sc.t_stride = t_bytes / 16;
+        sc.t_cap = t_bytes / 16;
         sc.h_stride = 0;
         return sc;
     };
@@ -1020,6 +1100,7 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
                  dr.ex_hx, dr.ex_hn, dr.ex_chunks, dr.n_ex_heavy, dr.n_ex_chunks, 0};
     const ExArgs xa{dr.ex_rp, dr.ex_ccol, dr.ex_tiles, dr.ex_order, kb->ex_ids, dr.ex_hrank, kb->ppos, kb->pneg, kb->MW4};
     const size_t smem = sizeof(PackConst) + 1024 * TROW * 4;
+    const size_t smem2 = sizeof(PackConstN<2>) + 1024 * (2 * LW + 1) * 4;   // pack pairs (2 CTAs/SM)
     const size_t pk_smem = 256 * PK_STRIDE * 4;
     static std::once_flag attr_set[kMaxDevices];
     once_per_device(attr_set, [&] {
@@ -1037,10 +1118,14 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             pct = std::max(0, std::min(100, pct));
             cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
         };
-        cudaFuncSetAttribute(k_slice_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_slice_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        carve((const void *)k_slice_tile<false>, smem, 4);
-        carve((const void *)k_slice_tile<true>, smem, 4);
+        cudaFuncSetAttribute(k_slice_tile<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_slice_tile<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        carve((const void *)k_slice_tile<false, 1>, smem, 4);
+        carve((const void *)k_slice_tile<true, 1>, smem, 4);
+        cudaFuncSetAttribute(k_slice_tile<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+        cudaFuncSetAttribute(k_slice_tile<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+        carve((const void *)k_slice_tile<false, 2>, smem2, 2);
+        carve((const void *)k_slice_tile<true, 2>, smem2, 2);
         cudaFuncSetAttribute(k_slice_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pk_smem);
         carve((const void *)k_slice_pack, pk_smem, 4);
     });
@@ -1051,7 +1136,9 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
         const uint32_t cls = fixed_cls >= 0 ? (uint32_t)fixed_cls : slice_class(h_desc[off].pred, h_desc[off].n, h_desc[off].sat);
         // U sweeps: full T per pack, as many packs per launch as the T area holds
         const uint32_t usw_batch = (uint32_t)std::max<size_t>(1, std::min<size_t>(max_batch, off_hf / std::max<size_t>(t_bytes, 1)));
-        const uint32_t cap = ex ? 256u * max_batch : usw >= 0 ? 256u * usw_batch : 256u;
+        // full packs: two per CSR pass (pack pairs) unless HEDL_NO_PAIR (A/B)
+        static const bool no_pair = std::getenv("HEDL_NO_PAIR") != nullptr;
+        const uint32_t cap = ex ? 256u * max_batch : usw >= 0 ? 256u * usw_batch : (no_pair ? 256u : 512u);
         uint32_t run = 1;
         if (fixed_cls >= 0) run = std::min(n - off, cap);
         else
@@ -1060,10 +1147,17 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
                 ++run;
         const uint32_t packs = (run + 255) / 256;
         const RestrictDesc *dd = d_desc + off;
-        SliceScratch sc = (ex || usw >= 0) ? scratch(off_hx, nhx, max_batch) : scratch(off_hf, nh, 1);
+        SliceScratch sc = (ex || usw >= 0) ? scratch(off_hx, nhx, max_batch) : scratch(off_hf, nh, 2);
+        const bool pair = !ex && usw < 0 && packs == 2;
+        if (pair) {
+            sc.h_stride = nh;                             // the two packs' heavy accumulators
+            sc.t_stride = 2 * t_bytes / 16;               // one interleaved region of 64 B records
+            sc.t_cap = 2 * t_bytes / 16;
+        }
         if (ex) {
             sc.h_stride = nhx;
             sc.t_stride = tx_bytes / 16;
+            sc.t_cap = tx_bytes / 16;
         } else if (usw >= 0) {
             sc.h_stride = nhx;                            // (t_stride: one full T per pack)
         }
@@ -1074,13 +1168,14 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             ku.W4 = dr.UW4;
             if (dr.UW4)
                 k_slice_pack<<<dim3(cdiv(dr.UW4, PK_WORDS), packs), 256, pk_smem, s>>>(ku, dd, run, sc.T, sc.t_stride,
-                                                                                     nullptr, nullptr, nullptr);
+                                                                                     nullptr, nullptr, nullptr, 2u);
             count_launch();
             prof_end(s, KC_SLICE_IN, 4.0 * dr.UW * run + 32.0 * dr.n_u * packs, packs);
         } else {
             k_slice_pack<<<dim3(cdiv(kb->W4, PK_WORDS), packs), 256, pk_smem, s>>>(kd, dd, run, sc.T, sc.t_stride,
                                                                                  ex ? dr.ex_umask : nullptr,
-                                                                                 ex ? dr.ex_ubase : nullptr, d_ops);
+                                                                                 ex ? dr.ex_ubase : nullptr, d_ops,
+                                                                                 pair ? 4u : 2u);
             count_launch();
             // rows read: one per materialised filler, the operand rows of a fused one
             double rows_read = run;
@@ -1100,8 +1195,8 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
                             kb->dirs[usw].UW4};
             if (rs.n_chunks) {
                 prof_begin(s, KC_SLICE_HEAVY);
-                if (cls == 0) k_slice_heavy<false><<<dim3(rs.n_chunks, packs), 256, 0, s>>>(su, sc, dd, run);
-                else k_slice_heavy<true><<<dim3(rs.n_chunks, packs), 256, 0, s>>>(su, sc, dd, run);
+                if (cls == 0) k_slice_heavy<false, 1><<<dim3(rs.n_chunks, packs), 256, 0, s>>>(su, sc, dd, run);
+                else k_slice_heavy<true, 1><<<dim3(rs.n_chunks, packs), 256, 0, s>>>(su, sc, dd, run);
                 count_launch();
                 prof_end(s, KC_SLICE_HEAVY, 36.0 * rs.E_heavy * packs, packs);
             }
@@ -1118,11 +1213,16 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
         const SliceDir &hd = ex ? sdx : sd;
         if (hd.n_chunks) {
             prof_begin(s, KC_SLICE_HEAVY);
-            if (cls == 0) k_slice_heavy<false><<<dim3(hd.n_chunks, packs), 256, 0, s>>>(hd, sc, dd, run);
-            else k_slice_heavy<true><<<dim3(hd.n_chunks, packs), 256, 0, s>>>(hd, sc, dd, run);
+            if (pair) {
+                if (cls == 0) k_slice_heavy<false, 2><<<dim3(hd.n_chunks, 1), 256, 0, s>>>(hd, sc, dd, run);
+                else k_slice_heavy<true, 2><<<dim3(hd.n_chunks, 1), 256, 0, s>>>(hd, sc, dd, run);
+            } else {
+                if (cls == 0) k_slice_heavy<false, 1><<<dim3(hd.n_chunks, packs), 256, 0, s>>>(hd, sc, dd, run);
+                else k_slice_heavy<true, 1><<<dim3(hd.n_chunks, packs), 256, 0, s>>>(hd, sc, dd, run);
+            }
             count_launch();
             const double eh = ex ? (double)dr.E_ex_heavy : (double)dr.E_heavy;
-            prof_end(s, KC_SLICE_HEAVY, (4.0 * eh + 32.0 * eh) * packs, packs);
+            prof_end(s, KC_SLICE_HEAVY, 4.0 * eh * (pair ? 1 : packs) + 32.0 * eh * packs, packs);   // a pair: one CSR pass
         }
         if (ex) {
             prof_begin(s, KC_SLICE_EX);
@@ -1142,20 +1242,21 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             // persistent grid: every resident CTA slot once (the tiles are taken dynamically);
             // occupancy per device (the carveout above is set per device)
             static std::once_flag occ_once[kMaxDevices];
-            static uint32_t occ[kMaxDevices][2];
+            static uint32_t occ[kMaxDevices][4];
             int cur = 0;
             cudaGetDevice(&cur);
             once_per_device(occ_once, [&] {
-                int b0 = 0, b1 = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_slice_tile<false>, 256, smem);
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_slice_tile<true>, 256, smem);
-                occ[(unsigned)cur % kMaxDevices][0] = (uint32_t)std::max(1, b0);
-                occ[(unsigned)cur % kMaxDevices][1] = (uint32_t)std::max(1, b1);
+                int b[4] = {0, 0, 0, 0};
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[0], k_slice_tile<false, 1>, 256, smem);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[1], k_slice_tile<true, 1>, 256, smem);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[2], k_slice_tile<false, 2>, 512, smem2);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[3], k_slice_tile<true, 2>, 512, smem2);
+                for (int i = 0; i < 4; ++i) occ[(unsigned)cur % kMaxDevices][i] = (uint32_t)std::max(1, b[i]);
             });
-            const uint32_t resident[2] = {occ[(unsigned)cur % kMaxDevices][0] * std::max(1, kb->sm_count),
-                                          occ[(unsigned)cur % kMaxDevices][1] * std::max(1, kb->sm_count)};
+            const uint32_t oi = (pair ? 2u : 0u) + (cls == 0 ? 0u : 1u);
+            const uint32_t resident = occ[(unsigned)cur % kMaxDevices][oi] * std::max(1, kb->sm_count);
             uint32_t *sched = (uint32_t *)(base + need - 256);   // self-cleaning {next tile, CTAs done}
-            const uint32_t grid = std::min(dr.n_tiles, resident[cls == 0 ? 0 : 1]);
+            const uint32_t grid = std::min(dr.n_tiles, resident);
             UTab ut{};
             uint32_t uw4max = 0;
             for (const hedl_dir &x : kb->dirs) uw4max = std::max(uw4max, x.UW4);
@@ -1166,12 +1267,17 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
                 ut.nu[q] = kb->dirs[q].n_u;
                 ut.ul[q] = kb->dirs[q].ulist;
             }
-            if (cls == 0) k_slice_tile<false><<<grid, 256, smem, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
-            else k_slice_tile<true><<<grid, 256, smem, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
+            if (pair) {
+                if (cls == 0) k_slice_tile<false, 2><<<grid, 512, smem2, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
+                else k_slice_tile<true, 2><<<grid, 512, smem2, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
+            } else {
+                if (cls == 0) k_slice_tile<false, 1><<<grid, 256, smem, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
+                else k_slice_tile<true, 1><<<grid, 256, smem, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
+            }
             count_launch();
             // minimal DRAM bytes of one lane-packed pass: CSR once + T once (32 B per individual)
             // + the output rows; the 32 B-per-edge T gathers are L2 traffic (DESIGN.md K-SLICE)
-            prof_end(s, KC_SLICE, csr + 32.0 * 32 * kb->W4 + 4.0 * kb->W * run, packs);
+            prof_end(s, KC_SLICE, csr + 32.0 * 32 * kb->W4 * packs + 4.0 * kb->W * run, packs);
         }
         off += run;
     }

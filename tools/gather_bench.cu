@@ -49,6 +49,50 @@ __global__ void __launch_bounds__(256) k_gather(const uint32_t *__restrict__ idx
     if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x12345678u) out[0] = 1;
 }
 
+
+// QUAD: a lane quad reads the four 16 B quarters of one 64 B record (two packs' 32 B T rows
+// interleaved per individual): the 2-pack sweep's access pattern, 64 B per gather
+template <int UNROLL>
+__global__ void __launch_bounds__(256) k_gather64(const uint32_t *__restrict__ idx, const uint4 *__restrict__ T, uint64_t E,
+                                                  uint32_t *__restrict__ out) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    const uint64_t pr = tid >> 2, npr = nthr >> 2;
+    const uint32_t q = tid & 3;
+    uint64_t e = pr;
+    for (; e + (UNROLL - 1) * npr < E; e += UNROLL * npr) {
+        uint32_t y[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) y[u] = __ldg(idx + e + u * npr);
+        uint4 v[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) v[u] = __ldg(T + 4ull * y[u] + q);
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) { acc.x |= v[u].x; acc.y |= v[u].y; acc.z |= v[u].z; acc.w |= v[u].w; }
+    }
+    if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x12345678u) out[0] = 1;
+}
+
+template <int U>
+void run64(const char *name, const uint32_t *idx, const uint4 *T, uint64_t E, uint32_t *out, int blocks_per_sm, int sms) {
+    const int grid = blocks_per_sm * sms;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    for (int i = 0; i < 3; ++i) k_gather64<U><<<grid, 256>>>(idx, T, E, out);
+    cudaEventRecord(a);
+    const int reps = 20;
+    for (int i = 0; i < reps; ++i) k_gather64<U><<<grid, 256>>>(idx, T, E, out);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    const double s = ms / 1e3 / reps;
+    printf("{\"shape\": \"%s\", \"bytes_per_gather\": 64, \"unroll\": %d, \"ctas_per_sm\": %d, \"us\": %.1f, "
+           "\"ggathers_per_s\": %.1f, \"gather_gbs\": %.0f}\n", name, U, blocks_per_sm, s * 1e6, E / s / 1e9, 64.0 * E / s / 1e9);
+}
+
 template <int U, bool P>
 void run(const char *name, const uint32_t *idx, const uint4 *T, uint64_t E, uint32_t *out, int blocks_per_sm, int sms,
          int smem = 0) {
@@ -85,11 +129,15 @@ int main() {
     uint32_t *idx, *out;
     uint4 *T;
     cudaMalloc(&idx, E * 4);
-    cudaMalloc(&T, (size_t)N * 32);
+    cudaMalloc(&T, (size_t)N * 64);
     cudaMalloc(&out, 4);
     cudaMemcpy(idx, h.data(), E * 4, cudaMemcpyHostToDevice);
-    cudaMemset(T, 0x5a, (size_t)N * 32);
+    cudaMemset(T, 0x5a, (size_t)N * 64);
     run<4, true>("uniform", idx, T, E, out, 4, sms);
+    run<8, true>("uniform", idx, T, E, out, 4, sms);
+    run64<4>("uniform", idx, T, E, out, 4, sms);
+    run64<8>("uniform", idx, T, E, out, 4, sms);
+    run64<8>("uniform", idx, T, E, out, 8, sms);
     run<4, true>("uniform", idx, T, E, out, 4, sms, 38400);
     run<8, true>("uniform", idx, T, E, out, 4, sms);
     run<4, true>("uniform", idx, T, E, out, 8, sms);
@@ -112,6 +160,8 @@ int main() {
         cudaMemcpy(idx, hs.data(), E * 4, cudaMemcpyHostToDevice);
         run<4, true>("skewed", idx, T, E, out, 4, sms);
         run<8, true>("skewed", idx, T, E, out, 4, sms);
+        run64<4>("skewed", idx, T, E, out, 4, sms);
+        run64<8>("skewed", idx, T, E, out, 4, sms);
         // the tile kernel's shared-memory footprint (4 x 37.5 KB per SM) leaves less L1
         run<4, true>("skewed", idx, T, E, out, 4, sms, 38400);
         run<4, true>("skewed", idx, T, E, out, 4, sms, 54000);
