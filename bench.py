@@ -188,6 +188,25 @@ def ncu_traffic(kind):
 
 
 # where each class's algorithmic bytes live
+# lane-packed sweep classes: hedl_prof_entry.units = bytes of T records gathered (32 B per edge
+# and pack, from L2 at C4); their ceiling is the measured gather rate of the same access pattern
+SWEEP_CLASSES = ("slice", "slice_heavy", "slice_ex", "slice_u")
+
+
+def gather_ceiling():
+    """Best gather rate tools/gather_bench.cu measured on B200 (profiles/r02_gather_micro.jsonl):
+    GB/s of gathered records at random indices from an L2-resident table."""
+    best = None
+    try:
+        for line in open(os.path.join(ROOT, "profiles", "r02_gather_micro.jsonl")):
+            d = json.loads(line)
+            if d.get("shape") in ("uniform", "skewed"):
+                best = max(best or 0.0, float(d["gather_gbs"]))
+    except (OSError, ValueError, KeyError):
+        return None
+    return best
+
+
 CLASS_BOUND = {"bool": "hbm", "bool_l2": "l2", "slice_pack": "hbm", "slice": "l2", "slice_heavy": "l2",
                "slice_ex": "l2", "restrict": "hbm", "restrict_heavy": "hbm", "drange": "hbm", "string": "hbm",
                "cover_init": "hbm", "gather": "hbm", "interp": "l2"}
@@ -543,7 +562,10 @@ def run_workload(kind, args, hedl, rank, world, local, steps, warmup, cpu_budget
         ms = e["total_ms"] / steps
         ach = e["alg_bytes"] / (e["total_ms"] / 1000.0) / 1e9 if e["total_ms"] else 0.0
         t = tcls.get(e["name"], {})
+        gb = e["units"] if e["name"] in SWEEP_CLASSES else 0.0       # T-gather bytes (hedl.h)
         classes.append({"name": e["name"], "bound": CLASS_BOUND.get(e["name"], "hbm"),
+                        "l2_gather_bytes_per_launch": gb / e["launches"] if gb else None,
+                        "l2_gather_GBps": gb / (e["total_ms"] / 1000.0) / 1e9 if gb and e["total_ms"] else None,
                         "launches_per_step": e["launches"] / steps, "ms_per_step": ms,
                         "alg_bytes_per_launch": e["alg_bytes"] / e["launches"], "alg_GBps": ach,
                         "frac_of_hbm": ach / peak,
@@ -567,6 +589,14 @@ def run_workload(kind, args, hedl, rank, world, local, steps, warmup, cpu_budget
                     "traffic_source": "profiles/ncu_traffic.json (measured DRAM read+write per launch, every "
                                       "launch of one step)" if tr is not None else None,
                     "timing": "CUDA events on the launch stream, profiled pass of the same steps"}
+        gc = gather_ceiling()
+        if top.get("l2_gather_GBps") and gc:
+            roofline["l2_gather"] = {"achieved": top["l2_gather_GBps"], "ceiling": gc, "unit": "GB/s",
+                                     "frac": top["l2_gather_GBps"] / gc,
+                                     "ceiling_source": "profiles/r02_gather_micro.jsonl (tools/gather_bench.cu: best "
+                                                       "measured rate of 32/64 B record gathers at random indices "
+                                                       "from an L2-resident table, B200)",
+                                     "what": "the sweep's T-record gathers (32 B per edge and pack) per second"}
         if traffic and traffic.get("dram_bytes_per_step"):
             db = traffic["dram_bytes_per_step"]
             roofline["step_dram_bytes"] = db

@@ -367,7 +367,9 @@ typedef struct hedl_prof_entry {
     uint64_t launches;
     double total_ms;
     double alg_bytes;
-    double units;          /* work units launched (nodes for per-node kernels, 256-lane packs for slice kernels) */
+    double units;          /* work units launched: nodes for per-node kernels and packs; for the lane-packed
+                              sweeps (slice, slice_heavy, slice_ex, slice_u) the bytes of T gathered,
+                              32 B per swept edge and pack (the L2-gather traffic of the sweep) */
 } hedl_prof_entry;
 hedl_status hedl_prof_enable(int on);
 hedl_status hedl_prof_reset(void);

@@ -1198,14 +1198,14 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
                 if (cls == 0) k_slice_heavy<false, 1><<<dim3(rs.n_chunks, packs), 256, 0, s>>>(su, sc, dd, run);
                 else k_slice_heavy<true, 1><<<dim3(rs.n_chunks, packs), 256, 0, s>>>(su, sc, dd, run);
                 count_launch();
-                prof_end(s, KC_SLICE_HEAVY, 36.0 * rs.E_heavy * packs, packs);
+                prof_end(s, KC_SLICE_HEAVY, 36.0 * rs.E_heavy * packs, 32.0 * rs.E_heavy * packs);
             }
             if (rs.n_blocks) {
                 prof_begin(s, KC_SLICE_U);
                 if (cls == 0) k_slice_ex<false><<<dim3(rs.n_blocks, packs), 256, 0, s>>>(ua, sc, dd, run, counts);
                 else k_slice_ex<true><<<dim3(rs.n_blocks, packs), 256, 0, s>>>(ua, sc, dd, run, counts);
                 count_launch();
-                prof_end(s, KC_SLICE_U, (8.0 * rs.n_rows + 36.0 * rs.E) * packs + 4.0 * kb->dirs[usw].UW * run, packs);
+                prof_end(s, KC_SLICE_U, (8.0 * rs.n_rows + 36.0 * rs.E) * packs + 4.0 * kb->dirs[usw].UW * run, 32.0 * rs.E * packs);
             }
             off += run;
             continue;
@@ -1222,7 +1222,7 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             }
             count_launch();
             const double eh = ex ? (double)dr.E_ex_heavy : (double)dr.E_heavy;
-            prof_end(s, KC_SLICE_HEAVY, 4.0 * eh * (pair ? 1 : packs) + 32.0 * eh * packs, packs);   // a pair: one CSR pass
+            prof_end(s, KC_SLICE_HEAVY, 4.0 * eh * (pair ? 1 : packs) + 32.0 * eh * packs, 32.0 * eh * packs);   // a pair: one CSR pass
         }
         if (ex) {
             prof_begin(s, KC_SLICE_EX);
@@ -1230,7 +1230,7 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             else k_slice_ex<true><<<dim3(dr.n_ex_blocks, packs), 256, 0, s>>>(xa, sc, dd, run, counts);
             count_launch();
             // example rows only: their CSR rows + 32 B T gathers + the projected rows
-            prof_end(s, KC_SLICE_EX, (8.0 * kb->M + 36.0 * dr.E_ex) * packs + 4.0 * kb->MW * run, packs);
+            prof_end(s, KC_SLICE_EX, (8.0 * kb->M + 36.0 * dr.E_ex) * packs + 4.0 * kb->MW * run, 32.0 * dr.E_ex * packs);
         } else {
             prof_begin(s, KC_SLICE);
 #ifdef HEDL_DEBUG_TILE
@@ -1277,7 +1277,7 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             count_launch();
             // minimal DRAM bytes of one lane-packed pass: CSR once + T once (32 B per individual)
             // + the output rows; the 32 B-per-edge T gathers are L2 traffic (DESIGN.md K-SLICE)
-            prof_end(s, KC_SLICE, csr + 32.0 * 32 * kb->W4 * packs + 4.0 * kb->W * run, packs);
+            prof_end(s, KC_SLICE, csr + 32.0 * 32 * kb->W4 * packs + 4.0 * kb->W * run, 32.0 * (double)(dr.E - dr.E_heavy) * packs);
         }
         off += run;
     }

@@ -21,7 +21,7 @@ def main():
     kids_pin = torch.from_numpy(np.ascontiguousarray(kids, dtype=np.uint32).view(np.uint8)).pin_memory()
     roots_pin = torch.from_numpy(np.ascontiguousarray(roots, dtype=np.uint32).view(np.uint8)).pin_memory()
     nd, kd, rd = (torch.empty_like(t, device=dev) for t in (nodes_pin, kids_pin, roots_pin))
-    for it in range(8):
+    for it in range(int(os.environ.get("E2E_ITERS", "8"))):
         T = {}
         torch.cuda.synchronize()
         t = time.perf_counter()
