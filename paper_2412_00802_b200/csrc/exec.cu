@@ -48,7 +48,7 @@ hedl_status grow(const hedl_kb *kb, cudaStream_t s, DevBuf &b, size_t need, bool
         if (st) b.p = nullptr;
         return st;
     }
-    HEDL_CUDA(kb, cudaStreamSynchronize(s));
+    if (b.p) HEDL_CUDA(kb, cudaStreamSynchronize(s));  // the old buffer may still be in use
     size_t sz = std::max(need, b.bytes * 5 / 4);
     if (b.p) dev_free(b.p, s);
     b.p = nullptr;
@@ -1089,7 +1089,16 @@ hedl_status launch_chunk(const hedl_kb *kb, Workspace *w, const ChunkPlan &cp, u
         for (const hedl_dir &x : kb->dirs) uw4max = std::max(uw4max, x.UW4);
         HEDL_CUDA(kb, cudaMemsetAsync(w->urows.p, 0, (size_t)cp.nurows_r * uw4max * 4, s));
     }
+    const bool tm = timing_enabled();
+    double t_rec = tm ? now_ms() : 0.0;
     for (const LaunchRec &lr : cp.recs) {
+        if (tm) {                                        // host time of the previous record's launches
+            const double t = now_ms();
+            if (t - t_rec > 1.0)
+                std::fprintf(stderr, "[hedl timing] launch record %zu (kind %d, %u nodes) took %.3f ms of host time\n",
+                             (size_t)(&lr - cp.recs.data()) - 1, (int)(&lr - 1)->kind, (&lr - 1)->count, t - t_rec);
+            t_rec = t;
+        }
         if (lr.kind == NK_AND) {
             KbDev kx = lr.proj ? kp : kd;
             if (lr.usp >= 0) {                                   // U space of one direction (no coverage)

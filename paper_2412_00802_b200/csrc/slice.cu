@@ -1065,8 +1065,12 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
     const size_t nh = lay.nh, nhx = lay.nhx, off_hf = lay.off_hf, off_hx = lay.off_hx, need = lay.need;
     const uint32_t max_batch = lay.max_batch;
     if (*ws_bytes < need) {
-        HEDL_CUDA(kb, cudaStreamSynchronize(s));
-        if (*ws) dev_free(*ws, s);
+        // a buffer being replaced may still be read by launched kernels; a fresh one (the first
+        // evaluation of a program) needs no synchronisation -- the launches keep streaming
+        if (*ws) {
+            HEDL_CUDA(kb, cudaStreamSynchronize(s));
+            dev_free(*ws, s);
+        }
         *ws = nullptr;
         *ws_bytes = 0;
         size_t got = 0;

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+T=${TAG:-e2f}
+HEDL_TIMING=1 timeout 600 python tools/time_e2e.py --no-latency --no-c5 2>&1 | grep -v dev_malloc > gpurun_out/${T}_time.log
+timeout 900 python bench.py > gpurun_out/${T}_bench.log 2>&1; echo bench=$? >> gpurun_out/${T}_bench.log
+timeout 1500 python -m pytest tests -m gpu -q -x -rf > gpurun_out/${T}_pytest.log 2>&1; echo pytest=$? >> gpurun_out/${T}_pytest.log
