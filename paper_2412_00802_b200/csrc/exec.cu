@@ -1436,7 +1436,8 @@ extern "C" hedl_status hedl_eval_one(const hedl_kb *kb, hedl_program *p, uint32_
             if (st) return st;
         }
         if (!p->lat_host) {
-            if (cudaHostAlloc((void **)&p->lat_host, sizeof(hedl_counts), cudaHostAllocMapped) != cudaSuccess ||
+            // [0] the counts, [1].tp the completion sequence number the kernel writes after them
+            if (cudaHostAlloc((void **)&p->lat_host, 2 * sizeof(hedl_counts), cudaHostAllocMapped) != cudaSuccess ||
                 cudaHostGetDevicePointer((void **)&p->lat_dev, p->lat_host, 0) != cudaSuccess) {
                 cudaGetLastError();
                 p->lat_host = nullptr;
@@ -1446,9 +1447,24 @@ extern "C" hedl_status hedl_eval_one(const hedl_kb *kb, hedl_program *p, uint32_
         cudaStream_t s = (cudaStream_t)stream;
         Workspace *w = ws_of(p);
         if (w->used && w->done) HEDL_CUDA(kb, cudaStreamWaitEvent(s, w->done, 0));
+        // completion: the kernel writes the counts, then (system-scope fence) this call's sequence
+        // number into mapped host memory; spinning on it returns ~µs earlier than a stream
+        // synchronisation.  The stream is still queried now and then, so a failed launch
+        // surfaces as an error; HEDL_LAT_SYNC=1 synchronises the stream instead (A/B).
+        static const bool lat_sync = std::getenv("HEDL_LAT_SYNC") != nullptr;
+        prog.seq = ++p->lat_seq;
+        volatile uint64_t *flag = &p->lat_host[1].tp;
         hedl_status st = interp_launch(kb, prog, p->lat_dev, out_bits, s);
         if (st) return st;
-        HEDL_CUDA(kb, cudaStreamSynchronize(s));
+        bool done = false;
+        if (!lat_sync) {
+            for (uint32_t spin = 1; !(done = (*flag == prog.seq)); ++spin)
+                if (!(spin & 1023) && cudaStreamQuery(s) != cudaErrorNotReady) {
+                    done = *flag == prog.seq;
+                    break;
+                }
+        }
+        if (!done) HEDL_CUDA(kb, cudaStreamSynchronize(s));
         const volatile hedl_counts *vc = p->lat_host;
         out->tp = vc->tp;
         out->fp = vc->fp;

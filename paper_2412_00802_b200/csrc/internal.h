@@ -204,7 +204,8 @@ struct hedl_program {
     size_t pinned_bytes = 0;
     uint64_t ws_limit = 0;              // 0 = auto (half the free memory, <= 48 GiB)
     // latency path: mapped pinned counts (host pointer + device alias)
-    hedl_counts *lat_host = nullptr, *lat_dev = nullptr;
+    hedl_counts *lat_host = nullptr, *lat_dev = nullptr;   // [2]: counts, completion sequence
+    uint64_t lat_seq = 0;
     // planning scratch (host)
     std::vector<uint32_t> stamp;
     uint32_t stamp_gen = 0;

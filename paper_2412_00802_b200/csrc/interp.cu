@@ -130,6 +130,8 @@ __global__ void __launch_bounds__(1024) k_interp(IKb kb, InterpProg prog, hedl_c
             counts->fp = b;
             counts->fn = prog.npos - a;
             counts->tn = prog.nneg - b;
+            __threadfence_system();                       // counts (and the row) before the flag
+            *(volatile unsigned long long *)&counts[1].tp = prog.seq;
         }
     }
 }
@@ -245,6 +247,8 @@ __global__ void __cluster_dims__(kInterpCl, 1, 1) __launch_bounds__(1024)
         counts->fp = b;
         counts->fn = prog.npos - a;
         counts->tn = prog.nneg - b;
+        __threadfence_system();                           // counts (and the row) before the flag
+        *(volatile unsigned long long *)&counts[1].tp = prog.seq;
     }
     cl.sync();                                            // keep shared memory alive for rank 0
 }

@@ -19,6 +19,7 @@ struct InterpNode {
 struct InterpProg {
     uint32_t n_nodes, n_ops;
     uint64_t npos, nneg;
+    uint64_t seq;              // written to counts[1].tp (mapped host memory) after the counts
     InterpNode nodes[kInterpMaxNodes];
     uint32_t ops[kInterpMaxOps];
 };
