@@ -861,7 +861,10 @@ void launch_gather_bits(cudaStream_t s, const uint32_t *const *rows, uint32_t *o
     for (uint32_t off = 0; off < n; off += 65535) {
         const uint32_t nd = n - off < 65535 ? n - off : 65535;
         prof_begin(s, KC_GATHER);
-        k_gather_bits<<<dim3(cdiv(W, 256) < 32 ? cdiv(W, 256) : 32, nd), 256, 0, s>>>(rows + off, out + (uint64_t)off * W, W);
+        // about 16 CTAs per SM over all rows of the launch, each thread ~4 words (one 10^7-bit
+        // row is 1.25 MB: 32 CTAs per row took 18 us)
+        const uint32_t gx = std::max<uint32_t>(1, std::min<uint32_t>(cdiv(W, 1024), cdiv(2368, nd)));
+        k_gather_bits<<<dim3(gx, nd), 256, 0, s>>>(rows + off, out + (uint64_t)off * W, W);
         count_launch();
         prof_end(s, KC_GATHER, 8.0 * W * nd, nd);
     }

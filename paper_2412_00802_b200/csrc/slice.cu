@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 namespace hedl {
@@ -342,9 +343,9 @@ __global__ void __launch_bounds__(256, 4) k_slice_pack(KbDev kb, const RestrictD
     const uint32_t p = blockIdx.y;
     const RestrictDesc *d = d_run + 256u * p;
     const uint32_t count = pack_count(run, p);
-    // rec = uint4 per individual: 2 (one pack's 32 B T per region of t_stride uint4), or 4 (a
-    // pack pair: the two packs' 32 B interleaved in one 64 B record;
-    // t_stride = the whole region)
+    // rec = uint4 per individual: 2 (one pack's 32 B T per region of t_stride uint4), 4 (a pack
+    // pair: the two packs' 32 B interleaved in one 64 B record;
+    // t_stride = the whole region) or 1 (a narrow pack of <= 128 nodes: lanes 0..127, 16 B)
     uint4 *T = rec == 4 ? T_base + 2 * p : T_base + p * t_stride;
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t w0 = blockIdx.x * PK_WORDS;
@@ -460,6 +461,7 @@ __global__ void __launch_bounds__(256, 4) k_slice_pack(KbDev kb, const RestrictD
         uint32_t o[4][LW];
 #pragma unroll
         for (int g = 0; g < LW; ++g) {
+            if (rec == 1 && g >= 4) break;                 // a narrow pack: lanes 128.. are empty
             const uint4 v = *reinterpret_cast<const uint4 *>(sm + (g * 32 + lane) * PK_STRIDE + wq);
             o[0][g] = warp_transpose(v.x ^ cms[g], lane);
             o[1][g] = warp_transpose(v.y ^ cms[g], lane);
@@ -473,7 +475,7 @@ __global__ void __launch_bounds__(256, 4) k_slice_pack(KbDev kb, const RestrictD
                 const uint64_t y = (uint64_t)w * 32 + lane;
                 HCHECK(rec * y + rec <= t_stride);
                 T[rec * y] = make_uint4(o[kk][0], o[kk][1], o[kk][2], o[kk][3]);
-                T[rec * y + 1] = make_uint4(o[kk][4], o[kk][5], o[kk][6], o[kk][7]);
+                if (rec != 1) T[rec * y + 1] = make_uint4(o[kk][4], o[kk][5], o[kk][6], o[kk][7]);
             } else if ((um >> lane) & 1u) {
                 const uint64_t t = ubs[4 * q + kk] + __popc(um & ((1u << lane) - 1u));
                 HCHECK(2 * t + 2 <= t_stride);
@@ -485,13 +487,13 @@ __global__ void __launch_bounds__(256, 4) k_slice_pack(KbDev kb, const RestrictD
 }
 
 // ------------------------------------------------------------------------------
-// heavy rows: CTA (256 threads) per chunk of <= kHeavyChunk edges.  NP packs per pass: the
-// threads form groups of G = 2 NP (lane pairs for one pack, quads for a pack pair), thread q of
-// a group owns words 4q .. 4q+3 of the 8 NP-word lane record (pack q >> 1).
-template <bool COUNT, int NP>
+// heavy rows: CTA (256 threads) per chunk of <= kHeavyChunk edges.  The threads form groups of
+// G (1: a narrow pack of <= 128 nodes, 2: lane pairs for one pack, 4: quads for a pack pair),
+// thread q of a group owns words 4q .. 4q+3 of the 4G-word lane record (pack q >> 1).
+template <bool COUNT, int G>
 __global__ void __launch_bounds__(256) k_slice_heavy(SliceDir dir, SliceScratch sc0, const RestrictDesc *__restrict__ d_run,
                                                      uint32_t run) {
-    constexpr int G = 2 * NP, NG = 256 / G;
+    constexpr int NP = G < 2 ? 1 : G / 2, NG = 256 / G, RW = 4 * G;   // packs per pass, groups, record words
     const uint32_t p0 = blockIdx.y * NP;                  // first pack of this pass
     const SliceScratch sc = sc0.at(p0);
     const RestrictDesc *d = d_run + 256u * p0;
@@ -524,7 +526,7 @@ __global__ void __launch_bounds__(256) k_slice_heavy(SliceDir dir, SliceScratch 
     }
     __syncthreads();
     if (!COUNT) {
-        if (threadIdx.x < NP * LW) {                      // word kk of the pass: pack kk / 8, word kk % 8
+        if (threadIdx.x < RW) {                           // word kk of the pass: pack kk / 8, word kk % 8
             const uint32_t kk = threadIdx.x;
             const uint32_t x = fin[kk >> 2][0][kk & 3];
             if (x) atomicOr(sc0.at(p0 + (kk >> 3)).hacc + (size_t)h * LW + (kk & 7), x);
@@ -532,8 +534,9 @@ __global__ void __launch_bounds__(256) k_slice_heavy(SliceDir dir, SliceScratch 
     } else {
 #pragma unroll
         for (int pp = 0; pp < NP; ++pp) {
-            const uint32_t L = threadIdx.x;             // lane of pack pp: half, word, bit
-            const uint32_t g = 2 * pp + (L >> 7), k = (L >> 5) & 3, bit = L & 31;
+            const uint32_t L = threadIdx.x, LL = pp * 256 + L;   // lane of pack pp: half, word, bit
+            if (LL >= 128u * G) continue;
+            const uint32_t g = LL >> 7, k = (L >> 5) & 3, bit = L & 31;
             uint32_t val = 0;
             for (int c = 0; c < NPL; ++c) val |= ((fin[g][c][k] >> bit) & 1u) << c;
             if (val) atomicAdd(sc0.at(p0 + pp).hcnt + (size_t)h * 256 + L, val);
@@ -550,7 +553,7 @@ __global__ void __launch_bounds__(256) k_slice_heavy(SliceDir dir, SliceScratch 
     __threadfence();
     build_consts(pc, d, count);
     if (!COUNT) {
-        if (threadIdx.x < NP * LW) {
+        if (threadIdx.x < RW) {
             const uint32_t kk = threadIdx.x;
             const SliceScratch sp = sc0.at(p0 + (kk >> 3));
             const uint32_t a = atomicExch(sp.hacc + (size_t)h * LW + (kk & 7), 0u);   // read + self-clean
@@ -562,6 +565,7 @@ __global__ void __launch_bounds__(256) k_slice_heavy(SliceDir dir, SliceScratch 
 #pragma unroll
         for (int pp = 0; pp < NP; ++pp) {
             const uint32_t L = threadIdx.x;
+            if (pp * 256 + L >= 128u * G) continue;
             uint32_t c = atomicExch(sc0.at(p0 + pp).hcnt + (size_t)h * 256 + L, 0u);
             c = c > 31u ? 31u : c;
             const uint32_t k = pp * LW + (L >> 5), bit = 1u << (L & 31);
@@ -576,7 +580,7 @@ __global__ void __launch_bounds__(256) k_slice_heavy(SliceDir dir, SliceScratch 
             if (r) atomicOr(&outw[k], bit);
         }
         __syncthreads();
-        if (threadIdx.x < NP * LW) sc0.at(p0 + (threadIdx.x >> 3)).hout[(size_t)h * LW + (threadIdx.x & 7)] = outw[threadIdx.x];
+        if (threadIdx.x < RW) sc0.at(p0 + (threadIdx.x >> 3)).hout[(size_t)h * LW + (threadIdx.x & 7)] = outw[threadIdx.x];
     }
     if (threadIdx.x == 0) sc.ticket[h] = 0;
 }
@@ -635,24 +639,25 @@ __device__ __forceinline__ void scan_slice_pipelined(Acc<COUNT> &acc, const uint
 }
 
 // ------------------------------------------------------------------------------
-// Persistent sweep over 1024-individual tiles (grid = resident CTAs).  NP packs per pass
-// (DESIGN.md "Pack pairs"): 256 NP threads per CTA, a group of G = 2 NP threads per row, thread
-// q of a group owning words 4q .. 4q+3 of the row's 8 NP-word lane record (T record of 16 G
-// bytes, one gather per edge and thread group).  CTAs take tiles from a global counter in
+// Persistent sweep over 1024-individual tiles (grid = resident CTAs).  G threads per row
+// ("Narrow packs"): thread q of a row's group owns words 4q .. 4q+3 of
+// the row's 4G-word lane record (T record of 16 G bytes, one gather per edge and group):
+// G = 1 a narrow pack (<= 128 nodes), 2 one pack, 4 a pack pair (512-thread CTAs).  CTAs take tiles from a global counter in
 // decreasing-cost order (dir.tile_rank, LPT), and inside a tile the warps take work items
 // (medium rows, then SELL slices, both degree-descending) from a shared counter, so neither
 // the grid nor the CTA waits on a statically unlucky share.  The counter pair `sched` is
 // self-cleaning: the last CTA to finish resets it for the next launch on the stream.
-template <bool COUNT, int NP>
-__global__ void __launch_bounds__(256 * NP, 4 / NP) k_slice_tile(KbDev kb, SliceDir dir, SliceScratch sc, UTab ut,
+template <bool COUNT, int G>
+__global__ void __launch_bounds__(G == 4 ? 512 : 256, G == 4 ? 2 : 4) k_slice_tile(KbDev kb, SliceDir dir, SliceScratch sc, UTab ut,
                                                                  const RestrictDesc *__restrict__ d, uint32_t count,
                                                                  hedl_counts *counts, uint32_t *sched, uint32_t dbg) {
 #ifndef HEDL_DEBUG_TILE
     dbg = 0;                                              // release builds: the debug switches fold away
 #endif
-    constexpr int G = 2 * NP;                             // threads per row (one 16 B quarter each)
-    constexpr uint32_t TR = NP * LW + 1;                  // ot row stride (bank-conflict-free transposes)
-    constexpr uint32_t NT = 256 * NP;
+    constexpr int NP = G < 2 ? 1 : G / 2;                 // packs of the pass
+    constexpr uint32_t RW = 4 * G;                        // record words (lanes / 32)
+    constexpr uint32_t TR = RW + 1;                       // ot row stride (bank-conflict-free transposes)
+    constexpr uint32_t NT = G == 4 ? 512 : 256;
     extern __shared__ uint32_t smem[];
     PackConstN<NP> &pc = *reinterpret_cast<PackConstN<NP> *>(smem);
     uint32_t *ot = smem + sizeof(PackConstN<NP>) / 4;     // [1024][TR]
@@ -660,8 +665,9 @@ __global__ void __launch_bounds__(256 * NP, 4 / NP) k_slice_tile(KbDev kb, Slice
     __shared__ uint32_t s_exm[32], s_exb[32];
     __shared__ uint32_t s_tile, s_item;
     __shared__ uint32_t s_udirs;
-    // this lane's node for the transpose-back phase (fixed for the whole launch)
-    const uint32_t jn = wid * 32 + lane;
+    // this lane's node for the transpose-back phase (fixed for the whole launch): warp g takes
+    // record word (column) g; a narrow pack's 4 columns go to warps w and w + 4 (word halves)
+    const uint32_t jn = (G == 1 ? (wid & 3) : wid) * 32 + lane;
     uint32_t *r_out = nullptr, *r_proj = nullptr, *r_uout = nullptr;
     uint32_t r_udirs = 0;
     int32_t r_cover = -1;
@@ -706,14 +712,14 @@ __global__ void __launch_bounds__(256 * NP, 4 / NP) k_slice_tile(KbDev kb, Slice
             for (int pp = 0; pp < NP; ++pp) {
                 const uint32_t *ho = sc.at(pp).hout + (size_t)h * LW;
 #pragma unroll
-                for (int k = 0; k < LW; ++k) ot[xl * TR + pp * LW + k] = ho[k];
+                for (int k = 0; k < (RW < LW ? (int)RW : LW); ++k) ot[xl * TR + pp * LW + k] = ho[k];
             }
         }
         const uint32_t sbeg = __ldg(dir.tile_slice + t), send = __ldg(dir.tile_slice + t + 1);
         // work items, in this order: big medium rows (deg > kMidDeg; a warp each), mid rows
         // (4 per warp, 8 lanes each), light SELL-16 slices (SPI per item; for a pack pair a
         // slice's 16 rows are two 8-row halves of the warp)
-        constexpr uint32_t SPI = (COUNT || NP == 2) ? 1u : 2u;
+        constexpr uint32_t SPI = G == 1 ? 2u : (COUNT || G == 4) ? 1u : 2u;
         const uint32_t n_big = (dbg & 2) ? 0u : __ldg(dir.tile_nbig + t);
         const uint32_t n_med = (dbg & 2) ? 0u : ti.y, n_sl = (dbg & 1) ? 0u : send - sbeg;
         const uint32_t i_light = n_big + (n_med - n_big + 3) / 4;
@@ -755,7 +761,22 @@ __global__ void __launch_bounds__(256 * NP, 4 / NP) k_slice_tile(KbDev kb, Slice
 #pragma unroll
                     for (int k = 0; k < HW; ++k) ot[(x - x0) * TR + q * HW + k] = acc.result(pc, q * HW + k, k);
                 }
-            } else if (NP == 1 && SPI == 1) {
+            } else if (G == 1) {
+                // light rows of a narrow pack: a thread per row, the warp's halves on two SELL-16
+                // slices (16 consecutive neighbour indices per half and step, coalesced)
+                const uint32_t sl = (it - i_light) * 2 + (lane >> 4);
+                const bool sv = sl < n_sl;
+                const uint32_t li = sl * 16 + (lane & 15);
+                const bool rv = sv && li < ti.z;
+                const uint32_t x = rv ? __ldg(dir.order + ti.x + ti.y + li) : 0u;
+                HCHECK(!rv || x - x0 < 1024u);
+                const uint32_t *c = sv ? dir.sell_col + __ldg(dir.sell_off + sbeg + sl) + (lane & 15) : dir.sell_col;
+                scan_slice_pipelined<COUNT, G>(acc, c, sc.T, sv ? __ldg(dir.sell_w + sbeg + sl) : 0u, 0u, sc.t_cap);
+                if (rv) {
+#pragma unroll
+                    for (int k = 0; k < HW; ++k) ot[(x - x0) * TR + k] = acc.result(pc, k, k);
+                }
+            } else if (G == 2 && SPI == 1) {
                 // light rows: one SELL-16 slice, a lane pair per row; the 16 pairs read 16
                 // consecutive neighbour indices per step (coalesced)
                 const uint32_t sl = it - i_light;
@@ -769,7 +790,7 @@ __global__ void __launch_bounds__(256 * NP, 4 / NP) k_slice_tile(KbDev kb, Slice
 #pragma unroll
                     for (int k = 0; k < HW; ++k) ot[(x - x0) * TR + q * HW + k] = acc.result(pc, q * HW + k, k);
                 }
-            } else if (NP == 2 && COUNT) {
+            } else if (G == 4 && COUNT) {
                 // light rows of a pack pair, COUNT class: one SELL-16 slice, a quad per row, the
                 // two 8-row halves one after the other (register budget)
                 const uint32_t sl = it - i_light;
@@ -800,13 +821,13 @@ __global__ void __launch_bounds__(256 * NP, 4 / NP) k_slice_tile(KbDev kb, Slice
                 bool rv[2];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const uint32_t sl = NP == 1 ? (it - i_light) * 2 + h : it - i_light;
+                    const uint32_t sl = G == 2 ? (it - i_light) * 2 + h : it - i_light;
                     const bool sv = sl < n_sl;
-                    const uint32_t li = NP == 1 ? sl * 16 + (lane >> 1) : sl * 16 + h * 8 + (lane >> 2);
+                    const uint32_t li = G == 2 ? sl * 16 + (lane >> 1) : sl * 16 + h * 8 + (lane >> 2);
                     rv[h] = sv && li < ti.z;
                     x[h] = rv[h] ? __ldg(dir.order + ti.x + ti.y + li) : 0u;
                     HCHECK(!rv[h] || x[h] - x0 < 1024u);
-                    const uint32_t col0 = NP == 1 ? (lane >> 1) : h * 8 + (lane >> 2);
+                    const uint32_t col0 = G == 2 ? (lane >> 1) : h * 8 + (lane >> 2);
                     cp[h] = sv ? dir.sell_col + __ldg(dir.sell_off + sbeg + sl) + col0 : dir.sell_col;
                     w[h] = sv ? __ldg(dir.sell_w + sbeg + sl) : 0u;
                 }
@@ -841,10 +862,12 @@ __global__ void __launch_bounds__(256 * NP, 4 / NP) k_slice_tile(KbDev kb, Slice
         }
         __syncthreads();
         // transpose back: warp g writes lanes 32g..32g+31 (node rows); each lane writes one
-        // whole 32 B sector of its node's row per 8 words
-        const uint32_t g = wid;
+        // whole 32 B sector of its node's row per 8 words (a narrow pack: warps g and g + 4 take
+        // the two 16-word halves of the tile)
+        const uint32_t g = G == 1 ? (wid & 3) : wid;
+        const uint32_t wl0 = G == 1 ? (wid >> 2) * 16 : 0u, wl1 = G == 1 ? wl0 + 16 : 32u;
         uint32_t pw = 0, pbits = 0;                       // pending projected word of this lane's node
-        for (uint32_t wl = 0; wl < ((dbg & 4) ? 0u : 32u); wl += 8) {
+        for (uint32_t wl = wl0; wl < ((dbg & 4) ? 0u : wl1); wl += 8) {
             const uint32_t w = t * 32 + wl;
             if (w >= kb.W4) break;                         // W4 is a multiple of 8
             uint32_t o[8];
@@ -886,6 +909,7 @@ __global__ void __launch_bounds__(256 * NP, 4 / NP) k_slice_tile(KbDev kb, Slice
 #pragma unroll
         for (uint32_t dd = 0; dd < kMaxUDirs; ++dd) {
             if (!((s_udirs >> dd) & 1u)) continue;                        // block-uniform
+            if (G == 1 && wid >= 4) break;                                // a narrow pack: 4 columns
             const uint32_t bl = __ldg(ut.ub[dd] + t * 32);
             const uint32_t bh = t * 32 + 32 < kb.W4 ? __ldg(ut.ub[dd] + t * 32 + 32) : ut.nu[dd];
             if (bh <= bl) continue;
@@ -1105,6 +1129,7 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
     const ExArgs xa{dr.ex_rp, dr.ex_ccol, dr.ex_tiles, dr.ex_order, kb->ex_ids, dr.ex_hrank, kb->ppos, kb->pneg, kb->MW4};
     const size_t smem = sizeof(PackConst) + 1024 * TROW * 4;
     const size_t smem2 = sizeof(PackConstN<2>) + 1024 * (2 * LW + 1) * 4;   // pack pairs (2 CTAs/SM)
+    const size_t smem1 = sizeof(PackConst) + 1024 * (LW / 2 + 1) * 4;        // narrow packs
     const size_t pk_smem = 256 * PK_STRIDE * 4;
     static std::once_flag attr_set[kMaxDevices];
     once_per_device(attr_set, [&] {
@@ -1122,14 +1147,16 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             pct = std::max(0, std::min(100, pct));
             cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
         };
-        cudaFuncSetAttribute(k_slice_tile<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_slice_tile<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        carve((const void *)k_slice_tile<false, 1>, smem, 4);
-        carve((const void *)k_slice_tile<true, 1>, smem, 4);
-        cudaFuncSetAttribute(k_slice_tile<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-        cudaFuncSetAttribute(k_slice_tile<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-        carve((const void *)k_slice_tile<false, 2>, smem2, 2);
-        carve((const void *)k_slice_tile<true, 2>, smem2, 2);
+        cudaFuncSetAttribute(k_slice_tile<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_slice_tile<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        carve((const void *)k_slice_tile<false, 2>, smem, 4);
+        carve((const void *)k_slice_tile<true, 2>, smem, 4);
+        cudaFuncSetAttribute(k_slice_tile<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+        cudaFuncSetAttribute(k_slice_tile<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+        carve((const void *)k_slice_tile<false, 4>, smem2, 2);
+        carve((const void *)k_slice_tile<true, 4>, smem2, 2);
+        carve((const void *)k_slice_tile<false, 1>, smem1, 4);
+        carve((const void *)k_slice_tile<true, 1>, smem1, 4);
         cudaFuncSetAttribute(k_slice_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pk_smem);
         carve((const void *)k_slice_pack, pk_smem, 4);
     });
@@ -1153,10 +1180,17 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
         const RestrictDesc *dd = d_desc + off;
         SliceScratch sc = (ex || usw >= 0) ? scratch(off_hx, nhx, max_batch) : scratch(off_hf, nh, 2);
         const bool pair = !ex && usw < 0 && packs == 2;
+        // narrow packs: a full pack of <= 128 nodes sweeps with one
+        // thread per row and 16 B T records; HEDL_NO_NARROW=1 disables (A/B)
+        static const bool no_narrow = std::getenv("HEDL_NO_NARROW") != nullptr;
+        const bool narrow = !ex && usw < 0 && packs == 1 && run <= 128 && !no_narrow;
         if (pair) {
             sc.h_stride = nh;                             // the two packs' heavy accumulators
             sc.t_stride = 2 * t_bytes / 16;               // one interleaved region of 64 B records
             sc.t_cap = 2 * t_bytes / 16;
+        } else if (narrow) {
+            sc.t_stride = t_bytes / 32;                   // 16 B records
+            sc.t_cap = t_bytes / 32;
         }
         if (ex) {
             sc.h_stride = nhx;
@@ -1179,7 +1213,7 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             k_slice_pack<<<dim3(cdiv(kb->W4, PK_WORDS), packs), 256, pk_smem, s>>>(kd, dd, run, sc.T, sc.t_stride,
                                                                                  ex ? dr.ex_umask : nullptr,
                                                                                  ex ? dr.ex_ubase : nullptr, d_ops,
-                                                                                 pair ? 4u : 2u);
+                                                                                 pair ? 4u : narrow ? 1u : 2u);
             count_launch();
             // rows read: one per materialised filler, the operand rows of a fused one
             double rows_read = run;
@@ -1199,8 +1233,8 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
                             kb->dirs[usw].UW4};
             if (rs.n_chunks) {
                 prof_begin(s, KC_SLICE_HEAVY);
-                if (cls == 0) k_slice_heavy<false, 1><<<dim3(rs.n_chunks, packs), 256, 0, s>>>(su, sc, dd, run);
-                else k_slice_heavy<true, 1><<<dim3(rs.n_chunks, packs), 256, 0, s>>>(su, sc, dd, run);
+                if (cls == 0) k_slice_heavy<false, 2><<<dim3(rs.n_chunks, packs), 256, 0, s>>>(su, sc, dd, run);
+                else k_slice_heavy<true, 2><<<dim3(rs.n_chunks, packs), 256, 0, s>>>(su, sc, dd, run);
                 count_launch();
                 prof_end(s, KC_SLICE_HEAVY, 36.0 * rs.E_heavy * packs, 32.0 * rs.E_heavy * packs);
             }
@@ -1218,15 +1252,19 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
         if (hd.n_chunks) {
             prof_begin(s, KC_SLICE_HEAVY);
             if (pair) {
-                if (cls == 0) k_slice_heavy<false, 2><<<dim3(hd.n_chunks, 1), 256, 0, s>>>(hd, sc, dd, run);
-                else k_slice_heavy<true, 2><<<dim3(hd.n_chunks, 1), 256, 0, s>>>(hd, sc, dd, run);
+                if (cls == 0) k_slice_heavy<false, 4><<<dim3(hd.n_chunks, 1), 256, 0, s>>>(hd, sc, dd, run);
+                else k_slice_heavy<true, 4><<<dim3(hd.n_chunks, 1), 256, 0, s>>>(hd, sc, dd, run);
+            } else if (narrow) {
+                if (cls == 0) k_slice_heavy<false, 1><<<dim3(hd.n_chunks, 1), 256, 0, s>>>(hd, sc, dd, run);
+                else k_slice_heavy<true, 1><<<dim3(hd.n_chunks, 1), 256, 0, s>>>(hd, sc, dd, run);
             } else {
-                if (cls == 0) k_slice_heavy<false, 1><<<dim3(hd.n_chunks, packs), 256, 0, s>>>(hd, sc, dd, run);
-                else k_slice_heavy<true, 1><<<dim3(hd.n_chunks, packs), 256, 0, s>>>(hd, sc, dd, run);
+                if (cls == 0) k_slice_heavy<false, 2><<<dim3(hd.n_chunks, packs), 256, 0, s>>>(hd, sc, dd, run);
+                else k_slice_heavy<true, 2><<<dim3(hd.n_chunks, packs), 256, 0, s>>>(hd, sc, dd, run);
             }
             count_launch();
             const double eh = ex ? (double)dr.E_ex_heavy : (double)dr.E_heavy;
-            prof_end(s, KC_SLICE_HEAVY, 4.0 * eh * (pair ? 1 : packs) + 32.0 * eh * packs, 32.0 * eh * packs);   // a pair: one CSR pass
+            const double hb = narrow ? 16.0 : 32.0;
+            prof_end(s, KC_SLICE_HEAVY, 4.0 * eh * (pair ? 1 : packs) + hb * eh * packs, hb * eh * packs);   // a pair: one CSR pass
         }
         if (ex) {
             prof_begin(s, KC_SLICE_EX);
@@ -1237,6 +1275,9 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             prof_end(s, KC_SLICE_EX, (8.0 * kb->M + 36.0 * dr.E_ex) * packs + 4.0 * kb->MW * run, 32.0 * dr.E_ex * packs);
         } else {
             prof_begin(s, KC_SLICE);
+            if (timing_enabled())
+                std::fprintf(stderr, "[hedl slice] full sweep: dir %u class %u nodes %u%s\n", dirid, cls, run,
+                             pair ? " (pair)" : narrow ? " (narrow)" : "");
 #ifdef HEDL_DEBUG_TILE
             // timing experiments only (tools/dbg_tile.sh): skips sweep phases, results are WRONG
             static const uint32_t dbg = getenv("HEDL_DBG_TILE") ? (uint32_t)atoi(getenv("HEDL_DBG_TILE")) : 0u;
@@ -1246,18 +1287,20 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
             // persistent grid: every resident CTA slot once (the tiles are taken dynamically);
             // occupancy per device (the carveout above is set per device)
             static std::once_flag occ_once[kMaxDevices];
-            static uint32_t occ[kMaxDevices][4];
+            static uint32_t occ[kMaxDevices][6];
             int cur = 0;
             cudaGetDevice(&cur);
             once_per_device(occ_once, [&] {
-                int b[4] = {0, 0, 0, 0};
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[0], k_slice_tile<false, 1>, 256, smem);
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[1], k_slice_tile<true, 1>, 256, smem);
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[2], k_slice_tile<false, 2>, 512, smem2);
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[3], k_slice_tile<true, 2>, 512, smem2);
-                for (int i = 0; i < 4; ++i) occ[(unsigned)cur % kMaxDevices][i] = (uint32_t)std::max(1, b[i]);
+                int b[6] = {0, 0, 0, 0, 0, 0};
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[0], k_slice_tile<false, 2>, 256, smem);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[1], k_slice_tile<true, 2>, 256, smem);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[2], k_slice_tile<false, 4>, 512, smem2);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[3], k_slice_tile<true, 4>, 512, smem2);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[4], k_slice_tile<false, 1>, 256, smem1);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[5], k_slice_tile<true, 1>, 256, smem1);
+                for (int i = 0; i < 6; ++i) occ[(unsigned)cur % kMaxDevices][i] = (uint32_t)std::max(1, b[i]);
             });
-            const uint32_t oi = (pair ? 2u : 0u) + (cls == 0 ? 0u : 1u);
+            const uint32_t oi = (pair ? 2u : narrow ? 4u : 0u) + (cls == 0 ? 0u : 1u);
             const uint32_t resident = occ[(unsigned)cur % kMaxDevices][oi] * std::max(1, kb->sm_count);
             uint32_t *sched = (uint32_t *)(base + need - 256);   // self-cleaning {next tile, CTAs done}
             const uint32_t grid = std::min(dr.n_tiles, resident);
@@ -1272,16 +1315,20 @@ hedl_status slice_run(const hedl_kb *kb, void **ws, size_t *ws_bytes, cudaStream
                 ut.ul[q] = kb->dirs[q].ulist;
             }
             if (pair) {
-                if (cls == 0) k_slice_tile<false, 2><<<grid, 512, smem2, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
-                else k_slice_tile<true, 2><<<grid, 512, smem2, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
+                if (cls == 0) k_slice_tile<false, 4><<<grid, 512, smem2, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
+                else k_slice_tile<true, 4><<<grid, 512, smem2, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
+            } else if (narrow) {
+                if (cls == 0) k_slice_tile<false, 1><<<grid, 256, smem1, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
+                else k_slice_tile<true, 1><<<grid, 256, smem1, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
             } else {
-                if (cls == 0) k_slice_tile<false, 1><<<grid, 256, smem, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
-                else k_slice_tile<true, 1><<<grid, 256, smem, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
+                if (cls == 0) k_slice_tile<false, 2><<<grid, 256, smem, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
+                else k_slice_tile<true, 2><<<grid, 256, smem, s>>>(kd, sd, sc, ut, dd, run, counts, sched, dbg);
             }
             count_launch();
             // minimal DRAM bytes of one lane-packed pass: CSR once + T once (32 B per individual)
             // + the output rows; the 32 B-per-edge T gathers are L2 traffic (DESIGN.md K-SLICE)
-            prof_end(s, KC_SLICE, csr + 32.0 * 32 * kb->W4 * packs + 4.0 * kb->W * run, 32.0 * (double)(dr.E - dr.E_heavy) * packs);
+            const double rb = narrow ? 16.0 : 32.0;       // T record bytes per pack
+            prof_end(s, KC_SLICE, csr + rb * 32 * kb->W4 * packs + 4.0 * kb->W * run, rb * (double)(dr.E - dr.E_heavy) * packs);
         }
         off += run;
     }
