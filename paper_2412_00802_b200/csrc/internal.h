@@ -35,7 +35,17 @@ struct NoInitAlloc : std::allocator<T> {
 constexpr uint32_t kLightDeg = 32;
 constexpr uint32_t kHeavyDeg = 512;
 constexpr uint32_t kMidDeg = 128;     // lane-packed sweep: medium rows up to this degree go 4 per warp
-constexpr uint32_t kHeavyChunk = 4096;
+#ifndef HEDL_HEAVY_CHUNK
+#define HEDL_HEAVY_CHUNK 4096
+#endif
+constexpr uint32_t kHeavyChunk = HEDL_HEAVY_CHUNK;
+// a direction's heavy-row chunk: half size when the full-size chunks would not give four
+// CTAs per SM (C4: 2.2M heavy edges per direction, 537 chunks of 4,096 on 148 SMs) --
+// measured: C4 heavy-row sweeps 1.50 -> 1.39 ms per step, C5 (enough chunks) unchanged
+inline uint32_t heavy_chunk(uint64_t heavy_edges, int sm_count) {
+    return heavy_edges >= (uint64_t)kHeavyChunk * 4u * (uint64_t)(sm_count > 0 ? sm_count : 148) ? kHeavyChunk
+                                                                                                  : kHeavyChunk / 2;
+}
 constexpr uint32_t kTopKMax = 4096;       // hedl_score_topk: k <= this
 constexpr uint32_t kMaxUDirs = 4;         // role directions whose U rows restrictions can emit / U sweeps
 

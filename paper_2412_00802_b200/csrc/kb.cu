@@ -332,6 +332,10 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
             if ((s = upload(kb, st, &dr.col, h.col.data(), h.col.size()))) return bail(s);
             std::vector<uint32_t> hx, hn;
             std::vector<uint4> chunks;
+            uint64_t eh = 0;                               // heavy edges: sizes the chunks
+            for (uint32_t x = 0; x < N; ++x)
+                if (h.row_ptr[x + 1] - h.row_ptr[x] > kHeavyDeg) eh += h.row_ptr[x + 1] - h.row_ptr[x];
+            const uint32_t hc = heavy_chunk(eh, kb->sm_count);
             for (uint32_t x = 0; x < N; ++x) {
                 const uint32_t a = h.row_ptr[x], b = h.row_ptr[x + 1], deg = b - a;
                 dr.max_deg = std::max(dr.max_deg, deg);
@@ -339,8 +343,8 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
                     const uint32_t hi = (uint32_t)hx.size();
                     hx.push_back(x);
                     uint32_t nc = 0;
-                    for (uint32_t e = a; e < b; e += kHeavyChunk, ++nc)
-                        chunks.push_back(make_uint4(hi, e, std::min(b, e + kHeavyChunk), 0));
+                    for (uint32_t e = a; e < b; e += hc, ++nc)
+                        chunks.push_back(make_uint4(hi, e, std::min(b, e + hc), 0));
                     hn.push_back(nc);
                     dr.E_heavy += deg;
                 }
@@ -488,6 +492,10 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
                 std::vector<uint4> ech;
                 std::vector<uint32_t> med, light;
                 auto degr = [&](uint32_t r) { return h.row_ptr[ex[r] + 1] - h.row_ptr[ex[r]]; };
+                uint64_t ehe = 0;
+                for (uint32_t r = 0; r < M; ++r)
+                    if (degr(r) > kHeavyDeg) ehe += degr(r);
+                const uint32_t ehc = heavy_chunk(ehe, kb->sm_count);
                 for (uint32_t b = 0; b < dr.n_ex_blocks; ++b) {
                     med.clear();
                     light.clear();
@@ -500,8 +508,8 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
                             ehr.push_back(r);
                             const uint32_t a = erp[r], e = erp[r + 1];     // in the example-row CSR
                             uint32_t nc = 0;
-                            for (uint32_t q = a; q < e; q += kHeavyChunk, ++nc)
-                                ech.push_back(make_uint4(hi, q, std::min(e, q + kHeavyChunk), 0));
+                            for (uint32_t q = a; q < e; q += ehc, ++nc)
+                                ech.push_back(make_uint4(hi, q, std::min(e, q + ehc), 0));
                             ehn.push_back(nc);
                             dr.E_ex_heavy += d;
                         } else {
@@ -544,6 +552,10 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
                 std::vector<uint4> tb(rs.n_blocks + 1), chs;
                 std::vector<uint32_t> ord, rhx, rhr, rhn, med, light;
                 auto deg = [&](uint32_t q) { return rp[q + 1] - rp[q]; };
+                uint64_t rhe = 0;
+                for (uint32_t q = 0; q < n; ++q)
+                    if (deg(q) > kHeavyDeg) rhe += deg(q);
+                const uint32_t rhc = heavy_chunk(rhe, kb->sm_count);
                 for (uint32_t b = 0; b < rs.n_blocks; ++b) {
                     med.clear();
                     light.clear();
@@ -555,8 +567,8 @@ extern "C" hedl_status hedl_kb_load(const hedl_kb_desc *desc, int device, void *
                             rhx.push_back(rows[q]);
                             rhr.push_back(q);
                             uint32_t nc = 0;
-                            for (uint32_t e = rp[q]; e < rp[q + 1]; e += kHeavyChunk, ++nc)
-                                chs.push_back(make_uint4(hi, e, std::min(rp[q + 1], e + kHeavyChunk), 0));
+                            for (uint32_t e = rp[q]; e < rp[q + 1]; e += rhc, ++nc)
+                                chs.push_back(make_uint4(hi, e, std::min(rp[q + 1], e + rhc), 0));
                             rhn.push_back(nc);
                             rs.E_heavy += dq;
                         } else {

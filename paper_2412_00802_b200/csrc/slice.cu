@@ -462,6 +462,10 @@ __global__ void __launch_bounds__(256, 4) k_slice_pack(KbDev kb, const RestrictD
 #pragma unroll
         for (int g = 0; g < LW; ++g) {
             if (rec == 1 && g >= 4) break;                 // a narrow pack: lanes 128.. are empty
+            if ((uint32_t)g * 32 >= count) {               // lanes without a node: zero words, no transposes
+                o[0][g] = o[1][g] = o[2][g] = o[3][g] = 0u;
+                continue;
+            }
             const uint4 v = *reinterpret_cast<const uint4 *>(sm + (g * 32 + lane) * PK_STRIDE + wq);
             o[0][g] = warp_transpose(v.x ^ cms[g], lane);
             o[1][g] = warp_transpose(v.y ^ cms[g], lane);
@@ -867,7 +871,8 @@ __global__ void __launch_bounds__(G == 4 ? 512 : 256, G == 4 ? 2 : 4) k_slice_ti
         const uint32_t g = G == 1 ? (wid & 3) : wid;
         const uint32_t wl0 = G == 1 ? (wid >> 2) * 16 : 0u, wl1 = G == 1 ? wl0 + 16 : 32u;
         uint32_t pw = 0, pbits = 0;                       // pending projected word of this lane's node
-        for (uint32_t wl = wl0; wl < ((dbg & 4) ? 0u : wl1); wl += 8) {
+        const bool col_live = g * 32 < count;             // warp-uniform: a column without nodes idles
+        for (uint32_t wl = wl0; col_live && wl < ((dbg & 4) ? 0u : wl1); wl += 8) {
             const uint32_t w = t * 32 + wl;
             if (w >= kb.W4) break;                         // W4 is a multiple of 8
             uint32_t o[8];
@@ -909,7 +914,7 @@ __global__ void __launch_bounds__(G == 4 ? 512 : 256, G == 4 ? 2 : 4) k_slice_ti
 #pragma unroll
         for (uint32_t dd = 0; dd < kMaxUDirs; ++dd) {
             if (!((s_udirs >> dd) & 1u)) continue;                        // block-uniform
-            if (G == 1 && wid >= 4) break;                                // a narrow pack: 4 columns
+            if ((G == 1 && wid >= 4) || !col_live) break;                 // a narrow pack: 4 columns
             const uint32_t bl = __ldg(ut.ub[dd] + t * 32);
             const uint32_t bh = t * 32 + 32 < kb.W4 ? __ldg(ut.ub[dd] + t * 32 + 32) : ut.nu[dd];
             if (bh <= bl) continue;
