@@ -871,8 +871,7 @@ __global__ void __launch_bounds__(G == 4 ? 512 : 256, G == 4 ? 2 : 4) k_slice_ti
         const uint32_t g = G == 1 ? (wid & 3) : wid;
         const uint32_t wl0 = G == 1 ? (wid >> 2) * 16 : 0u, wl1 = G == 1 ? wl0 + 16 : 32u;
         uint32_t pw = 0, pbits = 0;                       // pending projected word of this lane's node
-        const bool col_live = g * 32 < count;             // warp-uniform: a column without nodes idles
-        for (uint32_t wl = wl0; col_live && wl < ((dbg & 4) ? 0u : wl1); wl += 8) {
+        for (uint32_t wl = wl0; wl < ((dbg & 4) ? 0u : wl1); wl += 8) {
             const uint32_t w = t * 32 + wl;
             if (w >= kb.W4) break;                         // W4 is a multiple of 8
             uint32_t o[8];
@@ -914,7 +913,7 @@ __global__ void __launch_bounds__(G == 4 ? 512 : 256, G == 4 ? 2 : 4) k_slice_ti
 #pragma unroll
         for (uint32_t dd = 0; dd < kMaxUDirs; ++dd) {
             if (!((s_udirs >> dd) & 1u)) continue;                        // block-uniform
-            if ((G == 1 && wid >= 4) || !col_live) break;                 // a narrow pack: 4 columns
+            if (G == 1 && wid >= 4) break;                                // a narrow pack: 4 columns
             const uint32_t bl = __ldg(ut.ub[dd] + t * 32);
             const uint32_t bh = t * 32 + 32 < kb.W4 ? __ldg(ut.ub[dd] + t * 32 + 32) : ut.nu[dd];
             if (bh <= bl) continue;
