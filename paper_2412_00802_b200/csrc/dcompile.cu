@@ -64,7 +64,7 @@ struct DcCounters {
     unsigned long long n_ops;
     unsigned long long err;     // (node << 8) | code, minimum wins; ~0 = none
     uint32_t changed;
-    uint32_t pad;
+    uint32_t lvl_max;           // largest level assigned (levels only grow: the last pass's is exact)
 };
 
 struct DcKb {                    // what the device compiler needs of the KB
@@ -106,6 +106,7 @@ __global__ void k_dc_level(const hedl_node *__restrict__ nodes, uint32_t n, cons
                            uint64_t n_kids, uint32_t *lvl, uint8_t *bad, DcCounters *cnt) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     bool changed = false;
+    uint32_t lmax = 0;
     if (i < n) {
         const hedl_node nd = nodes[i];
         uint32_t L = 0;
@@ -124,8 +125,75 @@ __global__ void k_dc_level(const hedl_node *__restrict__ nodes, uint32_t n, cons
             lvl[i] = L;
             changed = true;
         }
+        lmax = max(lmax, L);
     }
     if (__any_sync(0xffffffffu, changed) && (threadIdx.x & 31) == 0) cnt->changed = 1;
+    lmax = __reduce_max_sync(0xffffffffu, lmax);
+    if ((threadIdx.x & 31) == 0 && lmax) atomicMax(&cnt->lvl_max, lmax);
+}
+
+// One pass instead of depth + 1 relaxation passes (each a launch and a host round trip): a
+// thread computes its node's level exactly by a bounded depth-first walk of its sub-DAG
+// (children have smaller indices; hypotheses are small trees).  A walk deeper than kDfsDepth
+// or longer than kDfsVisits leaves a lower bound and requests the relaxation passes, which
+// converge from there.
+constexpr int kDfsDepth = 12;
+constexpr uint32_t kDfsVisits = 96;
+__global__ void k_dc_level_dfs(const hedl_node *__restrict__ nodes, uint32_t n, const uint32_t *__restrict__ kids,
+                               uint64_t n_kids, uint32_t *lvl, uint8_t *bad, DcCounters *cnt) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    bool again = false;
+    uint32_t lmax = 0;
+    if (i < n) {
+        const hedl_node nd = nodes[i];
+        uint8_t b = 0;
+        if ((uint64_t)nd.child_begin + nd.child_count > n_kids) {
+            b = DE_CHILD_RANGE;
+        } else {
+            for (uint32_t k = 0; k < nd.child_count; ++k) {
+                const uint32_t c = kids[nd.child_begin + k];
+                if (c >= i) { b = c >= n ? DE_CHILD_RANGE : DE_CHILD_ORDER; break; }
+            }
+        }
+        uint32_t L = 0;
+        if (b) {
+            bad[i] = b;
+        } else if (nd.child_count) {
+            // frames: node, its child range, next child, best child level + 1 so far
+            uint32_t f_node[kDfsDepth], f_cb[kDfsDepth], f_cc[kDfsDepth], f_k[kDfsDepth], f_best[kDfsDepth];
+            int sp = 0;
+            uint32_t visits = 0;
+            f_node[0] = i; f_cb[0] = nd.child_begin; f_cc[0] = nd.child_count; f_k[0] = 0; f_best[0] = 0;
+            sp = 1;
+            while (sp > 0) {
+                const int t = sp - 1;
+                if (f_k[t] < f_cc[t]) {
+                    const uint32_t c = __ldg(kids + f_cb[t] + f_k[t]++);
+                    const hedl_node cn = nodes[c];
+                    const bool valid = c < f_node[t] && (uint64_t)cn.child_begin + cn.child_count <= n_kids;
+                    if (!valid || !cn.child_count) {          // a leaf (or an invalid child: its own
+                        f_best[t] = max(f_best[t], 1u);       // thread reports it)
+                    } else if (sp == kDfsDepth || ++visits > kDfsVisits) {
+                        again = true;                         // too deep / too shared: lower bound
+                        f_best[t] = max(f_best[t], 1u);
+                    } else {
+                        f_node[sp] = c; f_cb[sp] = cn.child_begin; f_cc[sp] = cn.child_count; f_k[sp] = 0; f_best[sp] = 0;
+                        ++sp;
+                    }
+                } else {
+                    const uint32_t lv = f_best[t];
+                    --sp;
+                    if (sp > 0) f_best[sp - 1] = max(f_best[sp - 1], lv + 1);
+                    else L = lv;
+                }
+            }
+        }
+        lvl[i] = L;
+        lmax = L;
+    }
+    if (__any_sync(0xffffffffu, again) && (threadIdx.x & 31) == 0) cnt->changed = 1;
+    lmax = __reduce_max_sync(0xffffffffu, lmax);
+    if ((threadIdx.x & 31) == 0 && lmax) atomicMax(&cnt->lvl_max, lmax);
 }
 
 // level histogram and scatter with block-level aggregation (few distinct levels: global
@@ -526,18 +594,19 @@ extern "C" hedl_status hedl_compile_device(const hedl_kb *kb, const hedl_node *n
         return fail(e.st, (code == DE_ROOT_RANGE ? "root " : "node ") + std::to_string(at) + ": " + e.msg);
     };
     hedl_status st;
-    // 1. levels by relaxation
-    uint32_t depth = 0;
-    for (;; ++depth) {
+    // 1. levels: one bounded depth-first pass; relaxation passes only if it ran out of budget
+    if (n) k_dc_level_dfs<<<nblk(n, 256), 256, 0, s>>>(nodes, n, child_idx, n_child_idx, lvl, bad, cnt);
+    count_launch();
+    if ((st = read_counters())) return st;
+    for (uint32_t depth = 0; hc->changed; ++depth) {
         if (depth > kDcMaxDepth) return fail(kDcErr[DE_DEPTH].st, kDcErr[DE_DEPTH].msg);
         HEDL_CUDA(kb, cudaMemsetAsync(&cnt->changed, 0, 4, s));
         if (n) k_dc_level<<<nblk(n, 256), 256, 0, s>>>(nodes, n, child_idx, n_child_idx, lvl, bad, cnt);
         count_launch();
         if ((st = read_counters())) return st;
-        if (!hc->changed) break;
     }
     timing_note("device compile: levels", now_ms() - t0);
-    const uint32_t L = depth + 1;     // levels 0 .. depth-1 occur (depth passes changed something)
+    const uint32_t L = hc->lvl_max + 1;   // levels 0 .. lvl_max occur
     // 2. level lists, reachability (top-down)
     HEDL_CUDA(kb, cudaMemsetAsync(hist, 0, (L + 1) * 4, s));
     if (n) k_dc_hist<<<std::min<uint32_t>(nblk(n, 1024), 1184), 1024, (L + 1) * 4, s>>>(lvl, n, hist, L + 1);

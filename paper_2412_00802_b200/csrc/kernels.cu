@@ -623,6 +623,96 @@ __global__ void __launch_bounds__(256) k_drange(KbDev kb, const uint32_t *__rest
     if (!UMAP && d.cover >= 0) block_cover(counts, d.cover, tp, fp);
 }
 
+// All range nodes of one data property in one pass (a launch group of k_drange nodes shares
+// row_ptr / val): blockIdx.y takes kDrMulti nodes, a lane reads its individual's values once
+// (up to kDrCache in registers; longer segments binary-search per node) and tests every node's
+// [lo, hi]; the node words come out of ballots, lane k keeping node k's word, so the stores,
+// projection scatters and coverage run one node per lane.  The values are read once per
+// kDrMulti nodes instead of once per node (C5: ~43 nodes per group over 1.5·10^7 values).
+constexpr uint32_t kDrMulti = 32, kDrCache = 4;
+template <bool UMAP>
+__global__ void __launch_bounds__(256) k_drange_multi(KbDev kb, const uint32_t *__restrict__ row_ptr,
+                                                      const float *__restrict__ val, const DrangeDesc *__restrict__ descs,
+                                                      uint32_t n_desc, hedl_counts *counts, const uint32_t *__restrict__ xmap) {
+    __shared__ float s_lo[kDrMulti], s_hi[kDrMulti];
+    __shared__ uint32_t s_tp[kDrMulti], s_fp[kDrMulti];
+    const uint32_t k0 = blockIdx.y * kDrMulti, nk = min(kDrMulti, n_desc - k0);
+    const uint32_t lane = threadIdx.x & 31;
+    if (threadIdx.x < kDrMulti) {
+        const bool v = threadIdx.x < nk;
+        s_lo[threadIdx.x] = v ? descs[k0 + threadIdx.x].lo : 1.0f;    // an empty range for
+        s_hi[threadIdx.x] = v ? descs[k0 + threadIdx.x].hi : 0.0f;    // the unused slots
+        s_tp[threadIdx.x] = s_fp[threadIdx.x] = 0;
+    }
+    __syncthreads();
+    DrangeDesc mine{};
+    const bool has = lane < nk;
+    if (has) mine = descs[k0 + lane];
+    uint32_t tp = 0, fp = 0;
+    const uint32_t w0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * kDrWords;
+    for (uint32_t u = 0; u < kDrWords; ++u) {
+        const uint32_t w = w0 + u;
+        if (w >= kb.W4) break;                                       // warp-uniform
+        const uint32_t pos = (w << 5) + lane;
+        uint32_t a = 0, b = 0;
+        if (w < kb.W && pos < kb.N) {
+            const uint32_t x = UMAP ? __ldg(xmap + pos) : pos;
+            a = __ldg(row_ptr + x);
+            b = __ldg(row_ptr + x + 1);
+        }
+        float v[kDrCache];
+#pragma unroll
+        for (uint32_t q = 0; q < kDrCache; ++q) v[q] = a + q < b ? __ldg(val + a + q) : __int_as_float(0x7fc00000);   // NaN: no match
+        const bool longseg = b - a > kDrCache;
+        uint32_t word_mine = 0;
+        for (uint32_t k = 0; k < nk; ++k) {
+            const float lo = s_lo[k], hi = s_hi[k];
+            bool hit = false;
+            if (!longseg) {
+#pragma unroll
+                for (uint32_t q = 0; q < kDrCache; ++q) hit |= v[q] >= lo && v[q] <= hi;
+            } else {                                                 // first value >= lo (sorted)
+                uint32_t l = a, h = b;
+                while (l < h) {
+                    const uint32_t m = (l + h) >> 1;
+                    if (__ldg(val + m) < lo) l = m + 1; else h = m;
+                }
+                hit = l < b && __ldg(val + l) <= hi;
+            }
+            const uint32_t word = __ballot_sync(FULL, hit);
+            if (lane == k) word_mine = word;
+        }
+        if (has) {
+            if (!UMAP && mine.proj && w < kb.W) proj_scatter(kb, mine.proj, w, word_mine);
+            if (mine.out) mine.out[w] = word_mine;
+            if (!UMAP && mine.cover >= 0 && w < kb.W) {
+                tp += __popc(word_mine & __ldg(kb.pos + w));
+                fp += __popc(word_mine & __ldg(kb.neg + w));
+            }
+        }
+    }
+    if (!UMAP && has && mine.cover >= 0 && (tp | fp)) {
+        atomicAdd(&s_tp[lane], tp);
+        atomicAdd(&s_fp[lane], fp);
+    }
+    __syncthreads();
+    if (!UMAP && threadIdx.x < nk) {
+        const int slot = descs[k0 + threadIdx.x].cover;
+        const uint32_t a = s_tp[threadIdx.x], b = s_fp[threadIdx.x];
+        if (slot >= 0) {
+            hedl_counts *c = counts + slot;
+            if (a) {
+                atomicAdd((unsigned long long *)&c->tp, (unsigned long long)a);
+                atomicAdd((unsigned long long *)&c->fn, (unsigned long long)(0ull - a));
+            }
+            if (b) {
+                atomicAdd((unsigned long long *)&c->fp, (unsigned long long)b);
+                atomicAdd((unsigned long long *)&c->tn, (unsigned long long)(0ull - b));
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------------------
 // String restrictions (Algs. 11-14).  Pull form: lane = subject x,
 // one warp per output word.  EQUAL compares interned ids (binary search of the
@@ -824,6 +914,19 @@ void launch_drange(cudaStream_t s, const KbDev &kb, const uint32_t *row_ptr, con
                    const uint32_t *xmap) {
     const uint32_t gx = cdiv(kb.W4, 8 * kDrWords);
     if (!gx) return;
+    static const bool no_multi = std::getenv("HEDL_NO_DRANGE_MULTI") != nullptr;
+    if (n_desc >= 2 && !no_multi) {                 // one pass over the values for every node
+        for (uint32_t off = 0; off < n_desc; off += 65535u * kDrMulti) {
+            const uint32_t nd = std::min<uint32_t>(n_desc - off, 65535u * kDrMulti);
+            prof_begin(s, KC_DRANGE);
+            if (xmap) k_drange_multi<true><<<dim3(gx, cdiv(nd, kDrMulti)), 256, 0, s>>>(kb, row_ptr, val, d_desc + off, nd, counts, xmap);
+            else k_drange_multi<false><<<dim3(gx, cdiv(nd, kDrMulti)), 256, 0, s>>>(kb, row_ptr, val, d_desc + off, nd, counts, nullptr);
+            count_launch();
+            // the segment arrays once per kDrMulti nodes (the per-node model's share) + the rows
+            prof_end(s, KC_DRANGE, alg_bytes / n_desc * cdiv(nd, kDrMulti) + 4.0 * kb.W * nd, nd);
+        }
+        return;
+    }
     for (uint32_t off = 0; off < n_desc; off += 65535) {
         const uint32_t nd = n_desc - off < 65535 ? n_desc - off : 65535;
         prof_begin(s, KC_DRANGE);

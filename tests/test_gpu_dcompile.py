@@ -123,3 +123,25 @@ def test_device_plan_subranges_and_fallback():
     bits, c = hedl.hedl_eval_batch(k, p2, 0, 3000, want_bits=True)
     torch.cuda.synchronize()
     assert np.array_equal(bits.cpu().numpy().view(np.uint32), ob) and np.array_equal(c, oc)
+
+
+def test_device_compile_deep_and_shared_dags():
+    """Levels on the device: one bounded depth-first pass (k_dc_level_dfs), falling back to
+    relaxation passes when a sub-DAG is deeper than the walk's stack (a 30-deep chain of
+    restrictions) or too shared for its visit budget (a ladder DAG whose paths double per
+    step, emitted with shared subtrees) -- both vs the oracle, next to plain trees."""
+    kb = abox.powerlaw_kb(3000, 8, 2, 5.0, 200, 0.5, 1.0, 0.05, seed=9)
+    A = lambda i: ("ATOM", i)
+    chain = A(0)
+    for d in range(30):
+        chain = ("EXISTS", d % 2, d % 3 == 0, chain) if d % 4 else ("AND", [chain, ("NOT", A(d % 8))])
+    def ladder(steps):
+        t = A(1)
+        for d in range(steps):
+            t = ("AND", [t, ("OR", [t, A((d + 2) % 8)])]) if d % 2 else ("OR", [t, ("EXISTS", 0, False, t)])
+        return t
+    for share, steps in ((False, 10), (True, 20)):       # unshared: 2^steps paths as a tree
+        lad = ladder(steps)
+        trees = [chain, lad, ("EXISTS", 1, True, lad), A(3), ("FORALL", 0, False, A(2))]
+        nodes, kids, roots = flatten(trees, share=share)
+        dev_parity(kb, nodes, kids, roots, tag=f"deep/shared DAGs share={share}")

@@ -157,3 +157,27 @@ def test_slice_degree_ladder_dense():
     # without EXACT lanes (packs of GE / LE only)
     trees2 = [t for t in trees if t[0] != "EXACT"]
     assert_parity(kb, trees2, eflags=FORCE, tag="degree ladder GE/LE only")
+
+
+@pytest.mark.parametrize("cls", ["or", "count"])
+def test_slice_pack_widths(cls):
+    """Full-pack sweep widths at their boundaries (DESIGN.md items 23, 23b): a group of k
+    restriction roots of one class, level and direction sweeps as a narrow pack (k <= 128,
+    one thread per row, 16 B T records), a single pack (129..256), a pack pair (257..512,
+    64 B records) or a pair plus a remainder; on a power-law KB with heavy rows (adaptive
+    heavy chunks), medium rows, SELL light slices and a ragged last tile."""
+    kb = abox.powerlaw_kb(50_000 + 77, 40, 2, 9.0, 3000, 0.5, 1.0, 0.02, seed=31)
+    C = kb["concept_bits"].shape[0]
+    A = lambda i: ("ATOM", i)
+    fillers = [("AND", [A(i), A(j)]) for i in range(C) for j in range(i + 1, C)]
+    fillers += [("OR", [A(i), ("NOT", A(j))]) for i in range(C) for j in range(C) if i != j]
+    for k in (1, 100, 128, 129, 256, 257, 300, 512, 513):
+        fs = fillers[:k]
+        if cls == "or":
+            trees = [("EXISTS", 0, False, f) if q % 2 == 0 else ("FORALL", 0, False, f) for q, f in enumerate(fs)]
+        else:
+            trees = [("MIN", 2 + q % 7, 0, False, f) if q % 2 == 0 else ("MAX", 1 + q % 5, 0, False, f)
+                     for q, f in enumerate(fs)]
+        assert_parity(kb, trees, eflags=FORCE, tag=f"pack width {cls} k={k}")
+        assert_parity(kb, [(t[0], *t[1:3], True, *t[4:]) if t[0] in ("MIN", "MAX") else (t[0], t[1], True, t[3])
+                           for t in trees], eflags=FORCE, tag=f"pack width {cls} k={k} inverse")
