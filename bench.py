@@ -673,12 +673,29 @@ def dry_run(args):
     return 0 if ok else 1
 
 
+def _gc_log():
+    """HEDL_BENCH_GCLOG=1: report Python garbage-collection pauses longer than 2 ms (stderr)."""
+    import gc
+    t0 = {}
+
+    def cb(phase, info):
+        if phase == "start":
+            t0["t"] = time.perf_counter()
+        elif "t" in t0:
+            dt = (time.perf_counter() - t0.pop("t")) * 1000.0
+            if dt > 2.0:
+                print(f"[bench gc] generation {info.get('generation')} pause {dt:.1f} ms", file=sys.stderr, flush=True)
+    gc.callbacks.append(cb)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
     if args.dry_run:
         return dry_run(args)
+    if os.environ.get("HEDL_BENCH_GCLOG"):
+        _gc_log()
     import torch
     import torch.distributed as dist
 
