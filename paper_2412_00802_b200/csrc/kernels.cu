@@ -283,7 +283,6 @@ __global__ void __launch_bounds__(256) k_restrict_tile(KbDev kb, DirDev dir, con
     }
     // light rows: SELL-16 slices
     const uint32_t sbeg = __ldg(dir.tile_slice + t), send = __ldg(dir.tile_slice + t + 1);
-#ifndef HEDL_RESTRICT_PAIR
     // a thread per row (as the narrow lane packs): the warp's halves take two slices, every
     // thread a row of each of two slice pairs, so four slices' dependent load chains (row
     // order, slice bounds, neighbour ids, probes) overlap per warp step; no pair reduction,
@@ -322,45 +321,6 @@ __global__ void __launch_bounds__(256) k_restrict_tile(KbDev kb, DirDev dir, con
             if (rv[h] && pred_eval(d.pred, min(c[h], sat), d.n))
                 atomicOr(&sbits[(x[h] - x0) >> 5], 1u << ((x[h] - x0) & 31));
     }
-#else
-    // (round-2 variant: a lane pair per row taking alternate neighbours, two slices per step)
-    for (uint32_t sl = sbeg + wid; sl < send; sl += 16) {
-        uint32_t x[2], w[2], c[2];
-        const uint32_t *cp[2];
-        bool rv[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const uint32_t s2 = sl + 8 * h;
-            const bool sv = s2 < send;
-            const uint32_t li = (s2 - sbeg) * 16 + (lane >> 1);
-            rv[h] = sv && li < ti.z;
-            x[h] = rv[h] ? __ldg(dir.order + ti.x + ti.y + li) : 0u;
-            cp[h] = sv ? dir.sell_col + __ldg(dir.sell_off + s2) + (lane >> 1) : nullptr;
-            w[h] = sv ? __ldg(dir.sell_w + s2) : 0u;
-            c[h] = 0;
-        }
-        const uint32_t wm = max(w[0], w[1]);
-        for (uint32_t k = lane & 1u; k < wm && (c[0] < sat || c[1] < sat); k += 8) {
-            uint32_t y[2][4];
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    y[h][u] = k + 2 * u < w[h] && c[h] < sat ? __ldg(cp[h] + (k + 2 * u) * 16) : 0xffffffffu;
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (y[h][u] != 0xffffffffu) c[h] += probe(d.child, y[h][u], d.cmask);
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const uint32_t cc = c[h] + __shfl_xor_sync(FULL, c[h], 1);
-            if (rv[h] && !(lane & 1u) && pred_eval(d.pred, min(cc, sat), d.n))
-                atomicOr(&sbits[(x[h] - x0) >> 5], 1u << ((x[h] - x0) & 31));
-        }
-    }
-#endif
     __syncthreads();
     if (wid == 0) {
         const uint32_t w = t * 32 + lane;
