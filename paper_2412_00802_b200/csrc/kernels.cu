@@ -840,7 +840,11 @@ void launch_bool(cudaStream_t s, const KbDev &kb, const BoolDesc *d_desc, uint32
                  const Operand *d_ops, hedl_counts *counts, double alg_bytes, uint64_t npos, uint64_t nneg,
                  bool full_rows) {
     const int kc = full_rows ? KC_BOOL : KC_BOOL_L2;
-    if (kb.W4 && (kb.W4 >> 2) <= kBoolWarpMaxN4 && n_desc >= 64) {
+    // a warp per node unless the launch has too few nodes to fill the SMs with warps while its
+    // rows are long (a few hundred U-space fillers of 5,000-word rows: one warp walking a row
+    // is a chain of ~20 dependent loads) -- then a CTA per row chunk (k_bool)
+    const bool few_long = n_desc < 148u * 8u && (kb.W4 >> 2) >= 256;
+    if (kb.W4 && (kb.W4 >> 2) <= kBoolWarpMaxN4 && n_desc >= 64 && !few_long) {
         const uint32_t g = std::min<uint32_t>(cdiv(n_desc, 8), 148u * 16u);
         prof_begin(s, kc);
         if (full_rows) k_bool_warp<true><<<g, 256, 0, s>>>(kb, d_desc, n_desc, d_ops, counts, npos, nneg);
