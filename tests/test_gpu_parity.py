@@ -312,3 +312,27 @@ def test_free_order_kb_before_program():
         _, c2 = hedl.hedl_eval_batch(k, prog, 3, 1)
         assert tuple(int(v) for v in c2[0]) == c
         prog.free()
+
+
+def test_drange_groups_long_segments():
+    """Range groups (several nodes on one data property in one launch: k_drange_multi) over
+    value segments of 0..12 values (the kernel caches four per individual and binary-searches
+    longer segments), NaN-free sorted per individual, with bounds at, between and outside the
+    values, empty and inverted ranges, +-inf; 1, 2, 31, 32, 33 and 70 nodes per group; full
+    rows (bits requested) and the example-projected counts path."""
+    rng = np.random.default_rng(77)
+    kb = abox.powerlaw_kb(9000 + 5, 6, 1, 4.0, 300, 0.0, 1.0, 0.05, seed=12)
+    N = kb["N"]
+    cnt = rng.integers(0, 13, size=N)
+    cnt[rng.random(N) < 0.3] = 0
+    subj = np.repeat(np.arange(N, dtype=np.uint32), cnt)
+    vals = np.round(rng.normal(0, 2, size=len(subj)), 1).astype(np.float32)
+    kb["data_off"] = np.array([0, len(subj)], np.uint64)
+    kb["data_subj"], kb["data_val"] = subj, vals
+    bounds = [-np.inf, -3.0, -1.0, -0.5, 0.0, 0.1, 0.5, 1.0, 2.5, 4.0, np.inf]
+    ranges = [(lo, hi) for lo in bounds for hi in bounds]          # incl. lo > hi (empty)
+    for k in (1, 2, 31, 32, 33, 70):
+        trees = [("DRANGE", 0, float(lo), float(hi)) for lo, hi in ranges[:k]]
+        trees += [("AND", [("ATOM", q % 6), ("DRANGE", 0, float(lo), float(hi))]) for q, (lo, hi) in enumerate(ranges[:k])]
+        trees += [("EXISTS", 0, q % 2 == 1, ("DRANGE", 0, float(lo), float(hi))) for q, (lo, hi) in enumerate(ranges[:k])]
+        assert_parity(kb, trees, tag=f"drange groups k={k}")
